@@ -1,0 +1,213 @@
+"""ctypes/numpy front end of the fp64 oracle ``libgio.so`` (TEST INFRASTRUCTURE).
+
+Every function takes fp32 parameters ``[N][8]`` = {mux, muy, l1, l2, l3,
+c'r, c'g, c'b} for ONE image and returns fp64 results.  Passages followed are
+cited in ``gio.cpp``.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "gio.cpp")
+_LIB = os.path.join(_HERE, "libgio.so")
+
+POS_LOGIT = 0
+POS_NORMALIZED = 1
+ALL_PAIRS, TILED, DENSE = 0, 1, 2
+
+
+def build(force: bool = False) -> str:
+    """Compile the oracle (plain g++, fp64, OpenMP, no FMA contraction)."""
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+        subprocess.check_call(["g++", "-O2", "-fopenmp", "-ffp-contract=off", "-fPIC",
+                               "-shared", "-std=c++17", _SRC, "-o", _LIB])
+    return _LIB
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        L = C.CDLL(build())
+        dp, fp, ip, up = (C.POINTER(C.c_double), C.POINTER(C.c_float),
+                          C.POINTER(C.c_int32), C.POINTER(C.c_uint32))
+        L.gio_eval_sigma.restype = C.c_double
+        L.gio_eval_sigma.argtypes = [dp, C.c_double, C.c_double]
+        L.gio_inverse2.argtypes = [dp, dp]
+        L.gio_chol_backward.argtypes = [dp, C.c_double, C.c_double, C.c_double, dp]
+        L.gio_project.argtypes = [fp, C.c_int, C.c_int, C.c_int, C.c_float, C.c_int, C.c_int,
+                                  dp, dp, dp, ip, ip, up]
+        L.gio_bin.restype = C.c_int64
+        L.gio_bin.argtypes = [fp, C.c_int, C.c_int, C.c_int, C.c_float, C.c_int, C.c_int, C.c_int,
+                              up, up, C.c_int64, up]
+        L.gio_render.argtypes = [fp, C.c_int, C.c_int, C.c_int, C.c_float, C.c_int, C.c_int,
+                                 C.c_int, dp]
+        L.gio_mse.restype = C.c_double
+        L.gio_mse.argtypes = [dp, fp, C.c_int, C.c_int, dp]
+        L.gio_backward.argtypes = [fp, C.c_int, C.c_int, C.c_int, C.c_float, C.c_int, C.c_int,
+                                   C.c_int, dp, dp]
+        L.gio_lr_at.restype = C.c_double
+        L.gio_lr_at.argtypes = [C.c_int, C.c_double, C.c_int]
+        L.gio_adam.argtypes = [fp, fp, fp, fp, C.c_int64, C.c_int, C.c_float, C.c_float,
+                               C.c_float, C.c_float, dp, dp, dp]
+        L.gio_half_to_double.restype = C.c_double
+        L.gio_half_to_double.argtypes = [C.c_uint32]
+        L.gio_vq_decode.restype = C.c_int
+        L.gio_vq_decode.argtypes = [C.POINTER(C.c_uint8), C.c_int64, C.c_int, C.c_int, C.c_int,
+                                    C.c_int, fp, fp, fp, fp]
+        L.gio_psnr.restype = C.c_double
+        L.gio_psnr.argtypes = [dp, fp, C.c_int64]
+        L.gio_num_threads.restype = C.c_int
+        L.gio_set_threads.argtypes = [C.c_int]
+        _lib = L
+    return _lib
+
+
+def _p(a, t):
+    return a.ctypes.data_as(C.POINTER(t))
+
+
+def _f32(a):
+    return np.ascontiguousarray(a, dtype=np.float32)
+
+
+def num_threads() -> int:
+    return lib().gio_num_threads()
+
+
+def set_threads(t: int) -> None:
+    lib().gio_set_threads(int(t))
+
+
+def eval_sigma(sinv, dx, dy) -> float:
+    s = np.ascontiguousarray(sinv, dtype=np.float64)
+    return lib().gio_eval_sigma(_p(s, C.c_double), float(dx), float(dy))
+
+
+def inverse2(S):
+    s = np.ascontiguousarray(S, dtype=np.float64)
+    out = np.zeros(3)
+    lib().gio_inverse2(_p(s, C.c_double), _p(out, C.c_double))
+    return out
+
+
+def chol_backward(G, l1e, l2, l3e):
+    g = np.ascontiguousarray(G, dtype=np.float64)
+    out = np.zeros(3)
+    lib().gio_chol_backward(_p(g, C.c_double), float(l1e), float(l2), float(l3e),
+                            _p(out, C.c_double))
+    return out
+
+
+def project(params, W, H, k=3.0, tile=16, pos_mode=POS_LOGIT):
+    """-> dict(mu[n,2], sigma[n,3], sinv[n,3], box[n,4], rect[n,4], touched[n])."""
+    p = _f32(params)
+    n = p.shape[0]
+    mu = np.zeros((n, 2)); sig = np.zeros((n, 3)); sinv = np.zeros((n, 3))
+    box = np.zeros((n, 4), np.int32); rect = np.zeros((n, 4), np.int32)
+    touched = np.zeros(n, np.uint32)
+    lib().gio_project(_p(p, C.c_float), n, int(W), int(H), float(k), int(tile), int(pos_mode),
+                      _p(mu, C.c_double), _p(sig, C.c_double), _p(sinv, C.c_double),
+                      _p(box, C.c_int32), _p(rect, C.c_int32), _p(touched, C.c_uint32))
+    return dict(mu=mu, sigma=sig, sinv=sinv, box=box, rect=rect, touched=touched)
+
+
+def n_tiles(W, H, tile=16) -> int:
+    return ((int(W) + tile - 1) // tile) * ((int(H) + tile - 1) // tile)
+
+
+def bin(params, W, H, k=3.0, tile=16, pos_mode=POS_LOGIT, method=1):
+    """-> (key_tile[K] u32, key_gid[K] u32, tile_range[T+1] u32)."""
+    p = _f32(params)
+    n = p.shape[0]
+    T = n_tiles(W, H, tile)
+    rng = np.zeros(T + 1, np.uint32)
+    L = lib()
+    K = L.gio_bin(_p(p, C.c_float), n, int(W), int(H), float(k), int(tile), int(pos_mode),
+                  int(method), None, None, 0, _p(rng, C.c_uint32))
+    kt = np.zeros(max(K, 1), np.uint32); kg = np.zeros(max(K, 1), np.uint32)
+    L.gio_bin(_p(p, C.c_float), n, int(W), int(H), float(k), int(tile), int(pos_mode),
+              int(method), _p(kt, C.c_uint32), _p(kg, C.c_uint32), K, _p(rng, C.c_uint32))
+    return kt[:K], kg[:K], rng
+
+
+def render(params, W, H, k=3.0, tile=16, pos_mode=POS_LOGIT, mode=ALL_PAIRS):
+    """Eq. 7 render -> fp64 planar [3][H][W]."""
+    p = _f32(params)
+    img = np.zeros((3, int(H), int(W)))
+    lib().gio_render(_p(p, C.c_float), p.shape[0], int(W), int(H), float(k), int(tile),
+                     int(pos_mode), int(mode), _p(img, C.c_double))
+    return img
+
+
+def mse(image, target):
+    """-> (loss, dL/dC) for the L2 loss of P:298 (mean over 3HW)."""
+    im = np.ascontiguousarray(image, dtype=np.float64)
+    t = _f32(target)
+    g = np.zeros_like(im)
+    H, W = im.shape[1], im.shape[2]
+    loss = lib().gio_mse(_p(im, C.c_double), _p(t, C.c_float), W, H, _p(g, C.c_double))
+    return loss, g
+
+
+def backward(params, dL_dC, W, H, k=3.0, tile=16, pos_mode=POS_LOGIT, mode=ALL_PAIRS):
+    """Appendix A backward -> fp64 grads [N][8] (mode ALL_PAIRS/TILED = boxed, DENSE)."""
+    p = _f32(params)
+    g = np.ascontiguousarray(dL_dC, dtype=np.float64)
+    out = np.zeros((p.shape[0], 8))
+    lib().gio_backward(_p(p, C.c_float), p.shape[0], int(W), int(H), float(k), int(tile),
+                       int(pos_mode), 2 if mode == DENSE else 0, _p(g, C.c_double),
+                       _p(out, C.c_double))
+    return out
+
+
+def loss_and_grads(params, target, k=3.0, tile=16, pos_mode=POS_LOGIT, mode=TILED):
+    t = _f32(target)
+    H, W = t.shape[1], t.shape[2]
+    img = render(params, W, H, k, tile, pos_mode, mode)
+    loss, g = mse(img, t)
+    return img, loss, backward(params, g, W, H, k, tile, pos_mode, mode)
+
+
+def lr_at(step, lr0=1e-3, half_every=20000) -> float:
+    return lib().gio_lr_at(int(step), float(lr0), int(half_every))
+
+
+def adam(p, g, m, v, step, lr, beta1=0.9, beta2=0.999, eps=1e-8):
+    """One fp64 Adam step from fp32 state -> (p, m, v) fp64."""
+    p, g, m, v = _f32(p), _f32(g), _f32(m), _f32(v)
+    po, mo, vo = np.zeros(p.shape), np.zeros(p.shape), np.zeros(p.shape)
+    lib().gio_adam(_p(p, C.c_float), _p(g, C.c_float), _p(m, C.c_float), _p(v, C.c_float),
+                   p.size, int(step), float(lr), float(beta1), float(beta2), float(eps),
+                   _p(po, C.c_double), _p(mo, C.c_double), _p(vo, C.c_double))
+    return po, mo, vo
+
+
+def half_to_double(bits: int) -> float:
+    return lib().gio_half_to_double(int(bits))
+
+
+def vq_decode(payload, n, gamma, beta, books, bits=6, stages=2, codebook=8):
+    """Attribute decode -> fp32 params [n][8] (positions normalised, pos_mode 1)."""
+    data = np.ascontiguousarray(payload, dtype=np.uint8)
+    g, b, cb = _f32(gamma), _f32(beta), _f32(books)
+    out = np.zeros((int(n), 8), np.float32)
+    rc = lib().gio_vq_decode(_p(data, C.c_uint8), data.size, int(n), int(bits), int(stages),
+                             int(codebook), _p(g, C.c_float), _p(b, C.c_float),
+                             _p(cb, C.c_float), _p(out, C.c_float))
+    if rc != 0:
+        raise ValueError("payload too short")
+    return out
+
+
+def psnr(x, y) -> float:
+    a = np.ascontiguousarray(x, dtype=np.float64)
+    b = _f32(y)
+    return lib().gio_psnr(_p(a, C.c_double), _p(b, C.c_float), a.size)
