@@ -1,0 +1,200 @@
+/* gi.h -- C ABI of libgi, the B200 (sm_100a) GaussianImage hot path.
+ *
+ * GaussianImage (arXiv 2403.08551) represents an image by N 2-D Gaussians of
+ * 8 parameters each (Sec. 3.2) and renders pixel i as the
+ * order-free accumulated sum  C_i = sum_n c'_n exp(-sigma_n)   (Eq. 7,
+ * PAPER.md:226-232), sigma_n = 1/2 d^T Sigma_n^-1 d (Eq. 5),
+ * Sigma = L L^T (Eq. 1).  Fitting minimises the L2 loss
+ * with the analytic gradients of Appendix A.
+ * Codec decode: fp16 positions, Eq. 8 dequantisation, Eq. 9 RVQ
+ * (PAPER.md:254-270).  Readings of silent/garbled passages (R1..R25) are in
+ * DESIGN.md; the numbers below refer to them.
+ *
+ * Conventions (all entry points):
+ *  - Every array argument is a caller-owned DEVICE pointer unless stated.
+ *    libgi never allocates on the hot path; workspaces are caller-provided and
+ *    sized by the *_workspace_bytes queries.
+ *  - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).
+ *    Every call is stream-ordered, never synchronises the host and is
+ *    CUDA-graph capturable.
+ *  - Layouts are fixed: parameters/gradients AoS [B][N][8] fp32 =
+ *    {mu_x, mu_y, l1, l2, l3, c'_r, c'_g, c'_b}, 16-byte aligned; images
+ *    planar fp32 [B][3][H][W], y down, pixel (x, y) has centre (x+1/2, y+1/2)
+ *    (R1, R2).  B = gi_frame.batch images of the same size and the same N
+ *    are processed per launch; tile and Gaussian ids are global:
+ *    tile = img*T + ty*ceil(W/16) + tx, gid = img*N + n.
+ *  - Errors: GI_EINVAL for bad host-visible arguments (nothing is launched);
+ *    GI_ECUDA for a launch failure (detail in gi_last_error(), thread-local);
+ *    device-side conditions (key-capacity overflow, non-finite parameters)
+ *    are written to device words the caller checks after a sync.
+ *  - No global mutable state: calls are re-entrant.
+ */
+#ifndef GI_H
+#define GI_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GI_ABI_VERSION 1
+
+typedef enum {
+    GI_OK = 0,
+    GI_EINVAL = 1,      /* bad argument (shape, alignment, size, NULL)        */
+    GI_ECUDA = 2,       /* CUDA launch / runtime error, see gi_last_error()   */
+    GI_ECAPACITY = 3,   /* more (tile, gaussian) keys than key_capacity       */
+    GI_EFORMAT = 4,     /* codec metadata inconsistent with the payload size  */
+    GI_ENONFINITE = 5   /* a parameter became NaN/Inf                         */
+} gi_status;
+
+/* One frame geometry shared by the B images of a launch. */
+typedef struct {
+    int32_t width, height;  /* pixels, 1..32767                                */
+    int32_t tile;           /* tile edge in pixels; must be 16 (R23)           */
+    int32_t batch;          /* images per launch B >= 1                        */
+    float k;                /* box half-extent in standard deviations (R6), >0 */
+} gi_frame;
+
+/* Position parameterisation of params[0:2]. */
+#define GI_POS_LOGIT 0u       /* raw logits, u = tanh(mu_raw) (App. C)  */
+#define GI_POS_NORMALIZED 1u  /* already u in [-1,1] (decode path, R19) */
+
+/* Size in bytes of one projected-Gaussian record (opaque, 16-B aligned). */
+#define GI_PROJ_BYTES 48
+
+const char* gi_status_string(gi_status s);
+const char* gi_last_error(void);
+int32_t gi_abi_version(void);
+
+/* T = ceil(W/16) * ceil(H/16) tiles per image. */
+int32_t gi_num_tiles(const gi_frame* f);
+size_t gi_proj_bytes(int32_t n, const gi_frame* f);   /* B * n * GI_PROJ_BYTES */
+
+/* --- a1. Projection ("formation"; Eq. 1; App. C) ---------------------
+ * For every Gaussian: u = tanh(mu_raw) (or u given), mu = (u + 1) * (W, H)/2
+ * in fp64, split into an integer pixel plus an fp32 fraction; effective
+ * L = [[l1 + 1/2, 0], [l2, l3 + 1/2]]; the conic of Sigma^-1 = L^-T L^-1; the
+ * integer pixel box of the k-sigma ellipse by the fp32 recipe of R7 (box
+ * empty and Gaussian culled iff l1+1/2 == 0 or l3+1/2 == 0, R8); its tile
+ * rectangle and tile count.
+ *   params         [B][n][8] fp32 in
+ *   proj           [B][n] records of GI_PROJ_BYTES out
+ *   tiles_touched  [B][n] u32 out: number of 16x16 tiles the box overlaps
+ * n may be 0. */
+gi_status gi_project(const float* params, int32_t n, const gi_frame* f, uint32_t flags,
+                     void* proj, uint32_t* tiles_touched, void* stream);
+
+/* --- a2. Tile binning, no depth key (north_star) --------------------
+ * Exclusive scan of tiles_touched -> gauss_offset; duplicate one key
+ * (tile, gid) per tile of each Gaussian's rectangle (row-major); stable LSD
+ * radix sort on the tile id ONLY (hand-written, CUB-free).  Emission is in
+ * ascending gid, so the result is the unique lexicographic (tile, gid) order
+ * (R9).  tile_range[t] = first key index with key_tile >= t (B*T + 1 entries).
+ *   gauss_offset  [B*n + 1] u32 out (gauss_offset[B*n] = K)
+ *   key_tile, key_gid  [key_capacity] u32 out (first K valid)
+ *   n_keys        [1] u32 device out: K, the TRUE key count.  If
+ *                 K > key_capacity the keys are truncated and the caller must
+ *                 retry with a larger capacity (gi_check reports GI_ECAPACITY).
+ *   ws            workspace of gi_bin_workspace_bytes() bytes (device). */
+size_t gi_bin_workspace_bytes(int32_t n, int64_t key_capacity, const gi_frame* f);
+gi_status gi_bin(const void* proj, const uint32_t* tiles_touched, int32_t n, const gi_frame* f,
+                 int64_t key_capacity, void* ws, size_t ws_bytes, uint32_t* gauss_offset,
+                 uint32_t* key_tile, uint32_t* key_gid, uint32_t* tile_range, uint32_t* n_keys,
+                 void* stream);
+
+/* --- a3. Forward accumulated summation (Eq. 7) -----------------------------
+ * C_k(x, y) = sum over keys of tile(x, y), ascending gid, of
+ *             [x0 <= x <= x1 and y0 <= y <= y1] c'_k exp(-sigma(x + 1/2, y + 1/2))
+ * Unclamped (R10).  image [B][3][H][W] fp32 out. */
+gi_status gi_render(const void* proj, const uint32_t* key_gid, const uint32_t* tile_range,
+                    int32_t n, const gi_frame* f, float* image, void* stream);
+
+/* --- a4. Loss + backward (Appendix A) ---------------------
+ * Upstream g = dL/dC: either given (dL_dimage != NULL), or the L2 loss
+ * L = mean over 3HW of (C - target)^2 with g = 2 (C - target) / (3HW), where
+ * C is recomputed in-kernel (fused forward; image_out may receive it).
+ * grads [B][n][8] fp32 OVERWRITTEN with dL/dparams (same layout as params;
+ * dl1 = 2 g1 l1 + 2 g2 l2, dl2 = 2 g2 l1 + 2 g3 l2 (R14 corrects P:627),
+ * dl3 = 2 g3 l3 in G = dL/dSigma; dmu_raw chained through tanh when flags ==
+ * GI_POS_LOGIT).  Deterministic: per-(tile, Gaussian) partial sums are
+ * written to the workspace and reduced per Gaussian in a fixed order.
+ *   loss       [B] fp32 out, or NULL (MSE mode only)
+ *   image_out  [B][3][H][W] fp32 out, or NULL (MSE mode only)
+ *   ws         gi_backward_workspace_bytes() bytes (device). */
+size_t gi_backward_workspace_bytes(int32_t n, int64_t key_capacity, const gi_frame* f);
+gi_status gi_render_backward(const float* params, const void* proj, const uint32_t* key_gid,
+                             const uint32_t* tile_range, const uint32_t* gauss_offset,
+                             int32_t n, const gi_frame* f, uint32_t flags,
+                             const float* dL_dimage, const float* target,
+                             int64_t key_capacity, void* ws, size_t ws_bytes,
+                             float* grads, float* loss, float* image_out, void* stream);
+
+/* --- a5. Adam (north_star; R16) ---------------------------------------------
+ * Elementwise over `count` fp32 scalars, step t >= 1 (1-based):
+ *   m = b1 m + (1-b1) g;  v = b2 v + (1-b2) g^2;
+ *   p -= lr * (m / (1 - b1^t)) / (sqrt(v / (1 - b2^t)) + eps)
+ * nonfinite_flag (device u32, may be NULL) gets bit 0 set if any updated p is
+ * NaN/Inf (GI_ENONFINITE via gi_check).  params/grads/m/v 16-B aligned. */
+gi_status gi_adam_step(float* params, const float* grads, float* m, float* v, int64_t count,
+                       int32_t step, float lr, float beta1, float beta2, float eps,
+                       uint32_t* nonfinite_flag, void* stream);
+
+/* lr_t = lr0 * 0.5^floor((t - 1) / half_every)  ("halved every 20000
+ * steps", R17).  Host helper. */
+double gi_lr_at(int32_t step, double lr0, int32_t half_every);
+
+/* --- fused fit iteration (graph-capturable) ---------------------------------
+ * One step of the fitting loop on B images: project -> bin -> fused
+ * forward/L2/backward -> Adam, with the 1-based step counter t kept on the
+ * device (*step_counter is incremented once per call, then used for the
+ * bias correction and lr_t = lr0 * 0.5^floor((t-1)/half_every)).  All buffers
+ * are the ones of the individual calls above; ws_* sizes as queried.
+ *   fit_ws  gi_fit_workspace_bytes() bytes: holds proj, tiles_touched,
+ *           gauss_offset, keys, ranges, n_keys and both stage workspaces. */
+size_t gi_fit_workspace_bytes(int32_t n, int64_t key_capacity, const gi_frame* f);
+gi_status gi_fit_step(float* params, float* grads, float* m, float* v, const float* target,
+                      int32_t n, const gi_frame* f, uint32_t flags, int64_t key_capacity,
+                      void* fit_ws, size_t ws_bytes, uint32_t* step_counter, float lr0,
+                      int32_t half_every, float beta1, float beta2, float eps, float* loss,
+                      uint32_t* status_flags, void* stream);
+/* Device status words inside fit_ws (for gi_check): */
+const uint32_t* gi_fit_n_keys(const void* fit_ws, int32_t n, int64_t key_capacity,
+                              const gi_frame* f);
+
+/* --- a6. Attribute decode (record layout SPEC.md:404) ------------
+ * payload: n records of R = 32 + 3*bits + stages*ceil(log2 codebook) bits,
+ * MSB-first, concatenated (device bytes, >= ceil(n*R/8)).  Per record:
+ *   u_x, u_y  = IEEE binary16 -> fp32 (exact)
+ *   l_i       = fmaf(code_i, gamma_i, beta_i)  (one fp32 rounding)    Eq. 8
+ *   c'        = C^1[i^1] + ... + C^M[i^M] (fp32, stage order)         Eq. 9
+ * params [n][8] fp32 out, positions normalised: project with
+ * GI_POS_NORMALIZED.  GI_EFORMAT if R > 64, bits > 16, codebook < 2 or
+ * stages > 8 or payload_bytes too small. */
+typedef struct {
+    int32_t n, bits, stages, codebook;
+    float gamma[3], beta[3];
+    const float* codebooks;   /* device [stages][codebook][3] fp32 */
+} gi_codec_meta;
+gi_status gi_vq_decode(const uint8_t* payload, size_t payload_bytes, const gi_codec_meta* meta,
+                       float* params, void* stream);
+
+/* --- harness helpers (not on the hot path) ---------------------------------
+ * PSNR of each image on [0,1]-clamped values, capped at 100 dB:
+ * psnr[B] fp32 out; ws of gi_psnr_workspace_bytes() bytes (device). */
+size_t gi_psnr_workspace_bytes(const gi_frame* f);
+gi_status gi_psnr(const float* image, const float* target, const gi_frame* f, float* psnr,
+                  void* ws, void* stream);
+
+/* Synchronise `stream` and translate the device status words:
+ * n_keys (device u32, may be NULL) > key_capacity -> GI_ECAPACITY;
+ * status_flags (device u32, may be NULL) bit 0 -> GI_ENONFINITE. */
+gi_status gi_check(const uint32_t* n_keys, int64_t key_capacity, const uint32_t* status_flags,
+                   void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GI_H */

@@ -1,0 +1,304 @@
+// C ABI of libgi (include/gi.h): argument validation, workspace carving and
+// dispatch to the sm_100a kernels.  Host-side only; no allocation, no sync
+// except in gi_check.
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+
+#include "gi_internal.cuh"
+
+namespace {
+
+thread_local char g_err[512] = "";
+
+gi_status cuda_status(cudaError_t e, const char* where) {
+    if (e == cudaSuccess) return GI_OK;
+    std::snprintf(g_err, sizeof(g_err), "%s: %s (%s)", where, cudaGetErrorName(e),
+                  cudaGetErrorString(e));
+    return GI_ECUDA;
+}
+
+gi_status invalid(const char* msg) {
+    std::snprintf(g_err, sizeof(g_err), "invalid argument: %s", msg);
+    return GI_EINVAL;
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+gi_status check_frame(const gi_frame* f) {
+    if (!f) return invalid("frame is NULL");
+    if (f->width < 1 || f->height < 1 || f->width > 32767 || f->height > 32767)
+        return invalid("width/height must be in [1, 32767]");
+    if (f->tile != gi::kTile) return invalid("tile must be 16");
+    if (f->batch < 1) return invalid("batch must be >= 1");
+    if (!(f->k > 0.0f) || !std::isfinite(f->k)) return invalid("k must be finite and > 0");
+    const int64_t tt = (int64_t)gi::tiles_x(f->width) * gi::tiles_y(f->height) * f->batch;
+    if (tt >= (1LL << 30)) return invalid("too many tiles");
+    return GI_OK;
+}
+
+gi_status check_n(int32_t n, const gi_frame* f) {
+    if (n < 0) return invalid("n must be >= 0");
+    if ((int64_t)n * f->batch >= (1LL << 30)) return invalid("batch * n too large");
+    return GI_OK;
+}
+
+cudaStream_t S(void* s) { return static_cast<cudaStream_t>(s); }
+
+struct FitWs {
+    gi::Proj* proj;
+    uint32_t* touched;
+    uint32_t* gauss_offset;
+    uint32_t* key_tile;
+    uint32_t* key_gid;
+    uint32_t* tile_range;
+    uint32_t* n_keys;
+    void* bin_ws;
+    void* bwd_ws;
+    size_t bytes;
+};
+
+FitWs carve_fit(void* base, int32_t n, int64_t cap, const gi_frame& f) {
+    using gi::align_up;
+    const size_t total = (size_t)n * f.batch;
+    const size_t T = (size_t)gi::tiles_x(f.width) * gi::tiles_y(f.height) * f.batch;
+    char* p = static_cast<char*>(base);
+    FitWs w;
+    size_t off = 0;
+    w.proj = reinterpret_cast<gi::Proj*>(p + off); off += align_up(sizeof(gi::Proj) * total);
+    w.touched = reinterpret_cast<uint32_t*>(p + off); off += align_up(4 * total);
+    w.gauss_offset = reinterpret_cast<uint32_t*>(p + off); off += align_up(4 * (total + 1));
+    w.key_tile = reinterpret_cast<uint32_t*>(p + off); off += align_up(4 * (size_t)cap);
+    w.key_gid = reinterpret_cast<uint32_t*>(p + off); off += align_up(4 * (size_t)cap);
+    w.tile_range = reinterpret_cast<uint32_t*>(p + off); off += align_up(4 * (T + 1));
+    w.n_keys = reinterpret_cast<uint32_t*>(p + off); off += align_up(4);
+    w.bin_ws = p + off; off += align_up(gi::bin_ws_bytes(n, cap, f));
+    w.bwd_ws = p + off; off += align_up(gi::backward_ws_bytes(n, cap, f));
+    w.bytes = off;
+    return w;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* gi_status_string(gi_status s) {
+    switch (s) {
+        case GI_OK: return "GI_OK";
+        case GI_EINVAL: return "GI_EINVAL";
+        case GI_ECUDA: return "GI_ECUDA";
+        case GI_ECAPACITY: return "GI_ECAPACITY";
+        case GI_EFORMAT: return "GI_EFORMAT";
+        case GI_ENONFINITE: return "GI_ENONFINITE";
+    }
+    return "GI_UNKNOWN";
+}
+
+const char* gi_last_error(void) { return g_err; }
+
+int32_t gi_abi_version(void) { return GI_ABI_VERSION; }
+
+int32_t gi_num_tiles(const gi_frame* f) {
+    if (check_frame(f) != GI_OK) return -1;
+    return gi::tiles_x(f->width) * gi::tiles_y(f->height);
+}
+
+size_t gi_proj_bytes(int32_t n, const gi_frame* f) {
+    if (check_frame(f) != GI_OK || n < 0) return 0;
+    return (size_t)n * f->batch * GI_PROJ_BYTES;
+}
+
+gi_status gi_project(const float* params, int32_t n, const gi_frame* f, uint32_t flags, void* proj,
+                     uint32_t* tiles_touched, void* stream) {
+    gi_status st;
+    if ((st = check_frame(f)) != GI_OK || (st = check_n(n, f)) != GI_OK) return st;
+    if (flags != GI_POS_LOGIT && flags != GI_POS_NORMALIZED) return invalid("flags");
+    if (n > 0 && (!params || !proj || !tiles_touched)) return invalid("NULL buffer");
+    if (!aligned16(params) || !aligned16(proj)) return invalid("params/proj must be 16-B aligned");
+    if (n == 0) return GI_OK;
+    return cuda_status(gi::launch_project(params, n, *f, flags, static_cast<gi::Proj*>(proj),
+                                          tiles_touched, nullptr, S(stream)),
+                       "gi_project");
+}
+
+size_t gi_bin_workspace_bytes(int32_t n, int64_t key_capacity, const gi_frame* f) {
+    if (check_frame(f) != GI_OK || n < 0 || key_capacity < 0) return 0;
+    return gi::bin_ws_bytes(n, key_capacity, *f);
+}
+
+gi_status gi_bin(const void* proj, const uint32_t* tiles_touched, int32_t n, const gi_frame* f,
+                 int64_t key_capacity, void* ws, size_t ws_bytes, uint32_t* gauss_offset,
+                 uint32_t* key_tile, uint32_t* key_gid, uint32_t* tile_range, uint32_t* n_keys,
+                 void* stream) {
+    gi_status st;
+    if ((st = check_frame(f)) != GI_OK || (st = check_n(n, f)) != GI_OK) return st;
+    if (key_capacity < 0 || key_capacity >= (1LL << 31)) return invalid("key_capacity");
+    if (ws_bytes < gi::bin_ws_bytes(n, key_capacity, *f)) return invalid("bin workspace too small");
+    if (!gauss_offset || !tile_range || !n_keys || (key_capacity > 0 && (!key_tile || !key_gid)) ||
+        (n > 0 && (!proj || !tiles_touched)) || !ws)
+        return invalid("NULL buffer");
+    return cuda_status(gi::launch_bin(static_cast<const gi::Proj*>(proj), tiles_touched, n, *f,
+                                      key_capacity, ws, gauss_offset, key_tile, key_gid,
+                                      tile_range, n_keys, S(stream)),
+                       "gi_bin");
+}
+
+gi_status gi_render(const void* proj, const uint32_t* key_gid, const uint32_t* tile_range,
+                    int32_t n, const gi_frame* f, float* image, void* stream) {
+    gi_status st;
+    if ((st = check_frame(f)) != GI_OK || (st = check_n(n, f)) != GI_OK) return st;
+    if (!tile_range || !image || (n > 0 && (!proj || !key_gid))) return invalid("NULL buffer");
+    return cuda_status(gi::launch_render(static_cast<const gi::Proj*>(proj), key_gid, tile_range, n,
+                                         *f, image, S(stream)),
+                       "gi_render");
+}
+
+size_t gi_backward_workspace_bytes(int32_t n, int64_t key_capacity, const gi_frame* f) {
+    if (check_frame(f) != GI_OK || n < 0 || key_capacity < 0) return 0;
+    return gi::backward_ws_bytes(n, key_capacity, *f);
+}
+
+gi_status gi_render_backward(const float* params, const void* proj, const uint32_t* key_gid,
+                             const uint32_t* tile_range, const uint32_t* gauss_offset, int32_t n,
+                             const gi_frame* f, uint32_t flags, const float* dL_dimage,
+                             const float* target, int64_t key_capacity, void* ws, size_t ws_bytes,
+                             float* grads, float* loss, float* image_out, void* stream) {
+    gi_status st;
+    if ((st = check_frame(f)) != GI_OK || (st = check_n(n, f)) != GI_OK) return st;
+    if (flags != GI_POS_LOGIT && flags != GI_POS_NORMALIZED) return invalid("flags");
+    if (key_capacity < 0 || key_capacity >= (1LL << 31)) return invalid("key_capacity");
+    if (ws_bytes < gi::backward_ws_bytes(n, key_capacity, *f)) return invalid("backward workspace too small");
+    if (!dL_dimage && !target) return invalid("need dL_dimage or target");
+    if (!tile_range || !gauss_offset || !ws || (n > 0 && (!params || !proj || !key_gid || !grads)))
+        return invalid("NULL buffer");
+    if (!aligned16(params) || !aligned16(grads) || !aligned16(ws)) return invalid("alignment");
+    return cuda_status(gi::launch_backward(params, static_cast<const gi::Proj*>(proj), key_gid,
+                                           tile_range, gauss_offset, n, *f, flags, dL_dimage,
+                                           target, key_capacity, ws, grads, loss, image_out,
+                                           S(stream)),
+                       "gi_render_backward");
+}
+
+gi_status gi_adam_step(float* params, const float* grads, float* m, float* v, int64_t count,
+                       int32_t step, float lr, float beta1, float beta2, float eps,
+                       uint32_t* nonfinite_flag, void* stream) {
+    if (count < 0) return invalid("count");
+    if (step < 1) return invalid("step is 1-based");
+    if (!(beta1 >= 0.f && beta1 < 1.f && beta2 >= 0.f && beta2 < 1.f)) return invalid("betas");
+    if (count > 0 && (!params || !grads || !m || !v)) return invalid("NULL buffer");
+    if (!aligned16(params) || !aligned16(grads) || !aligned16(m) || !aligned16(v))
+        return invalid("alignment");
+    if (count == 0) return GI_OK;
+    return cuda_status(gi::launch_adam(params, grads, m, v, count, step, nullptr, lr, 1, beta1,
+                                       beta2, eps, nonfinite_flag, S(stream)),
+                       "gi_adam_step");
+}
+
+double gi_lr_at(int32_t step, double lr0, int32_t half_every) {
+    if (step < 1 || half_every < 1) return 0.0;
+    return std::ldexp(lr0, -((step - 1) / half_every));
+}
+
+size_t gi_fit_workspace_bytes(int32_t n, int64_t key_capacity, const gi_frame* f) {
+    if (check_frame(f) != GI_OK || n < 0 || key_capacity < 0) return 0;
+    return carve_fit(nullptr, n, key_capacity, *f).bytes;
+}
+
+const uint32_t* gi_fit_n_keys(const void* fit_ws, int32_t n, int64_t key_capacity, const gi_frame* f) {
+    if (check_frame(f) != GI_OK || !fit_ws) return nullptr;
+    return carve_fit(const_cast<void*>(fit_ws), n, key_capacity, *f).n_keys;
+}
+
+gi_status gi_fit_step(float* params, float* grads, float* m, float* v, const float* target,
+                      int32_t n, const gi_frame* f, uint32_t flags, int64_t key_capacity,
+                      void* fit_ws, size_t ws_bytes, uint32_t* step_counter, float lr0,
+                      int32_t half_every, float beta1, float beta2, float eps, float* loss,
+                      uint32_t* status_flags, void* stream) {
+    gi_status st;
+    if ((st = check_frame(f)) != GI_OK || (st = check_n(n, f)) != GI_OK) return st;
+    if (flags != GI_POS_LOGIT && flags != GI_POS_NORMALIZED) return invalid("flags");
+    if (key_capacity < 0 || key_capacity >= (1LL << 31)) return invalid("key_capacity");
+    if (half_every < 1) return invalid("half_every");
+    if (!fit_ws || ws_bytes < carve_fit(nullptr, n, key_capacity, *f).bytes)
+        return invalid("fit workspace too small");
+    if (!step_counter || !target || (n > 0 && (!params || !grads || !m || !v)))
+        return invalid("NULL buffer");
+    if (!aligned16(params) || !aligned16(grads) || !aligned16(m) || !aligned16(v) || !aligned16(fit_ws))
+        return invalid("alignment");
+    FitWs w = carve_fit(fit_ws, n, key_capacity, *f);
+    cudaStream_t s = S(stream);
+    cudaError_t e;
+    if ((e = gi::launch_project(params, n, *f, flags, w.proj, w.touched, step_counter, s)) != cudaSuccess)
+        return cuda_status(e, "gi_fit_step/project");
+    if ((e = gi::launch_bin(w.proj, w.touched, n, *f, key_capacity, w.bin_ws, w.gauss_offset,
+                            w.key_tile, w.key_gid, w.tile_range, w.n_keys, s)) != cudaSuccess)
+        return cuda_status(e, "gi_fit_step/bin");
+    if ((e = gi::launch_backward(params, w.proj, w.key_gid, w.tile_range, w.gauss_offset, n, *f,
+                                 flags, nullptr, target, key_capacity, w.bwd_ws, grads, loss,
+                                 nullptr, s)) != cudaSuccess)
+        return cuda_status(e, "gi_fit_step/backward");
+    if (n > 0 &&
+        (e = gi::launch_adam(params, grads, m, v, (int64_t)n * 8 * f->batch, 0, step_counter, lr0,
+                             half_every, beta1, beta2, eps, status_flags, s)) != cudaSuccess)
+        return cuda_status(e, "gi_fit_step/adam");
+    return GI_OK;
+}
+
+gi_status gi_vq_decode(const uint8_t* payload, size_t payload_bytes, const gi_codec_meta* meta,
+                       float* params, void* stream) {
+    if (!meta) return invalid("meta is NULL");
+    if (meta->n < 0) return invalid("n");
+    if (meta->bits < 1 || meta->bits > 16 || meta->stages < 1 || meta->stages > 8 ||
+        meta->codebook < 2 || meta->codebook > 256) {
+        std::snprintf(g_err, sizeof(g_err), "codec metadata out of range");
+        return GI_EFORMAT;
+    }
+    int ib = 1;
+    while ((1 << ib) < meta->codebook) ++ib;
+    const int64_t rec = 32 + 3LL * meta->bits + (int64_t)meta->stages * ib;
+    if (rec > 64) {
+        std::snprintf(g_err, sizeof(g_err), "record wider than 64 bits");
+        return GI_EFORMAT;
+    }
+    if ((size_t)((rec * meta->n + 7) / 8) > payload_bytes) {
+        std::snprintf(g_err, sizeof(g_err), "payload shorter than n records");
+        return GI_EFORMAT;
+    }
+    if (meta->n > 0 && (!payload || !params || !meta->codebooks)) return invalid("NULL buffer");
+    if (!aligned16(params)) return invalid("alignment");
+    return cuda_status(gi::launch_vq_decode(payload, *meta, params, S(stream)), "gi_vq_decode");
+}
+
+gi_status gi_psnr(const float* image, const float* target, const gi_frame* f, float* psnr, void* ws,
+                  void* stream) {
+    gi_status st;
+    if ((st = check_frame(f)) != GI_OK) return st;
+    if (!image || !target || !psnr || !ws) return invalid("NULL buffer");
+    return cuda_status(gi::launch_psnr(image, target, *f, psnr, ws, S(stream)), "gi_psnr");
+}
+
+size_t gi_psnr_workspace_bytes(const gi_frame* f) {
+    if (check_frame(f) != GI_OK) return 0;
+    return (size_t)8 * 296 * f->batch;
+}
+
+gi_status gi_check(const uint32_t* n_keys, int64_t key_capacity, const uint32_t* status_flags,
+                   void* stream) {
+    cudaError_t e = cudaStreamSynchronize(S(stream));
+    if (e != cudaSuccess) return cuda_status(e, "gi_check/sync");
+    if (status_flags) {
+        uint32_t fl = 0;
+        if ((e = cudaMemcpy(&fl, status_flags, 4, cudaMemcpyDeviceToHost)) != cudaSuccess)
+            return cuda_status(e, "gi_check/flags");
+        if (fl & 1u) return GI_ENONFINITE;
+    }
+    if (n_keys) {
+        uint32_t k = 0;
+        if ((e = cudaMemcpy(&k, n_keys, 4, cudaMemcpyDeviceToHost)) != cudaSuccess)
+            return cuda_status(e, "gi_check/n_keys");
+        if ((int64_t)k > key_capacity) return GI_ECAPACITY;
+    }
+    return GI_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,96 @@
+// Internal definitions shared by the libgi CUDA sources (sm_100a only).
+// Nothing here is shared with the CPU oracle (oracle/).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/gi.h"
+
+#if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ != 1000)
+#error "libgi is written for sm_100a only"
+#endif
+
+namespace gi {
+
+constexpr int kTile = 16;            // tile edge (R23)
+constexpr int kTilePix = kTile * kTile;
+constexpr int kWarps = 8;            // 256-thread CTA per tile, one pixel per thread
+constexpr unsigned kFull = 0xffffffffu;
+
+// sqrt(1/2 * log2(e)): sigma * log2(e) = (a dx)^2 + (b dx + c dy)^2 with
+// (a, b, c) = kappa * (1/l1, -l2/(l1 l3), 1/l3)   [Sigma^-1 = L^-T L^-1]
+constexpr double kKappa = 0.84932180028801907;   // sqrt(0.5 / ln 2)
+constexpr double kLn2 = 0.69314718055994531;
+
+// Projected Gaussian record, GI_PROJ_BYTES = 48, three float4.
+//   q0 = {ix (int bits), iy (int bits), fx, fy}   centre = (ix + fx, iy + fy)
+//   q1 = {a, b, c, bx}     factored conic; bx = x0 | x1 << 16 (u16 each)
+//   q2 = {c'r, c'g, c'b, by}                    by = y0 | y1 << 16
+// An empty box has x0 > x1 (0xffff0001 style: x0 = 1, x1 = 0).
+struct __align__(16) Proj {
+    float4 q0, q1, q2;
+};
+static_assert(sizeof(Proj) == GI_PROJ_BYTES, "record size");
+
+constexpr uint32_t kEmptyBox = 1u;   // x0 = 1, x1 = 0
+
+__host__ __device__ inline int tiles_x(int W) { return (W + kTile - 1) / kTile; }
+__host__ __device__ inline int tiles_y(int H) { return (H + kTile - 1) / kTile; }
+
+__device__ __forceinline__ float ex2_approx(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
+__device__ __forceinline__ unsigned lanemask_lt() {
+    unsigned m;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+    return m;
+}
+
+// Generic device scan (u32, exclusive) over `count` elements, count either a
+// host constant or read from device memory.  Three launches, no inter-block
+// waiting.  ws needs scan_ws_words(max_count) u32.
+constexpr int kScanThreads = 256;
+constexpr int kScanItems = 8;
+constexpr int kScanTileElems = kScanThreads * kScanItems;   // 2048
+size_t scan_ws_words(int64_t max_count);
+// out may alias in.  count_dev: if non-null, count = *count_dev * count_mul
+// (clamped to max_count).  total_out (device, may be null) receives the sum.
+cudaError_t scan_exclusive(const uint32_t* in, uint32_t* out, int64_t max_count,
+                           const uint32_t* count_dev, uint32_t count_mul, uint32_t* ws,
+                           uint32_t* total_out, cudaStream_t s);
+// count = ceil(min(*count_dev, cap) / div) * mul, clamped to max_count.
+cudaError_t scan_exclusive_spec(const uint32_t* in, uint32_t* out, int64_t max_count,
+                                const uint32_t* count_dev, uint32_t div, uint32_t mul, int64_t cap,
+                                uint32_t* ws, uint32_t* total_out, cudaStream_t s);
+
+// Internal launchers (api.cu validates arguments).
+cudaError_t launch_project(const float* params, int n, const gi_frame& f, uint32_t flags,
+                           Proj* proj, uint32_t* tiles_touched, uint32_t* step_counter,
+                           cudaStream_t s);
+cudaError_t launch_bin(const Proj* proj, const uint32_t* tiles_touched, int n, const gi_frame& f,
+                       int64_t cap, void* ws, uint32_t* gauss_offset, uint32_t* key_tile,
+                       uint32_t* key_gid, uint32_t* tile_range, uint32_t* n_keys, cudaStream_t s);
+size_t bin_ws_bytes(int n, int64_t cap, const gi_frame& f);
+cudaError_t launch_render(const Proj* proj, const uint32_t* key_gid, const uint32_t* tile_range,
+                          int n, const gi_frame& f, float* image, cudaStream_t s);
+size_t backward_ws_bytes(int n, int64_t cap, const gi_frame& f);
+cudaError_t launch_backward(const float* params, const Proj* proj, const uint32_t* key_gid,
+                            const uint32_t* tile_range, const uint32_t* gauss_offset, int n,
+                            const gi_frame& f, uint32_t flags, const float* dL_dimage,
+                            const float* target, int64_t cap, void* ws, float* grads, float* loss,
+                            float* image_out, cudaStream_t s);
+cudaError_t launch_adam(float* params, const float* grads, float* m, float* v, int64_t count,
+                        int step, const uint32_t* step_dev, float lr, int half_every, float b1,
+                        float b2, float eps, uint32_t* flag, cudaStream_t s);
+cudaError_t launch_vq_decode(const uint8_t* payload, const gi_codec_meta& meta, float* params,
+                             cudaStream_t s);
+cudaError_t launch_psnr(const float* image, const float* target, const gi_frame& f, float* psnr,
+                        void* ws, cudaStream_t s);
+
+inline size_t align_up(size_t x, size_t a = 256) { return (x + a - 1) / a * a; }
+
+}  // namespace gi

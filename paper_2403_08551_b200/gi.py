@@ -1,0 +1,232 @@
+"""Thin Python binding of libgi (include/gi.h): same names, argument
+marshalling only.  Every step of the hot path runs in the CUDA kernels of
+``libgi.so``; there is no CPU fallback -- if the library or a CUDA device is
+missing, calls raise.
+
+Tensors are torch tensors on the CUDA device (torch is used for device memory
+and streams only).  ``stream=None`` means torch's current stream.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import torch
+
+from . import build as _build
+
+GI_OK, GI_EINVAL, GI_ECUDA, GI_ECAPACITY, GI_EFORMAT, GI_ENONFINITE = range(6)
+GI_POS_LOGIT = 0
+GI_POS_NORMALIZED = 1
+GI_PROJ_BYTES = 48
+TILE = 16
+
+_STATUS = {0: "GI_OK", 1: "GI_EINVAL", 2: "GI_ECUDA", 3: "GI_ECAPACITY", 4: "GI_EFORMAT",
+           5: "GI_ENONFINITE"}
+
+
+class GiError(RuntimeError):
+    def __init__(self, status: int, where: str, detail: str = ""):
+        self.status = status
+        super().__init__(f"{where}: {_STATUS.get(status, status)} {detail}".strip())
+
+
+class gi_frame(C.Structure):
+    _fields_ = [("width", C.c_int32), ("height", C.c_int32), ("tile", C.c_int32),
+                ("batch", C.c_int32), ("k", C.c_float)]
+
+
+class gi_codec_meta(C.Structure):
+    _fields_ = [("n", C.c_int32), ("bits", C.c_int32), ("stages", C.c_int32),
+                ("codebook", C.c_int32), ("gamma", C.c_float * 3), ("beta", C.c_float * 3),
+                ("codebooks", C.c_void_p)]
+
+
+def frame(width: int, height: int, batch: int = 1, k: float = 3.0, tile: int = TILE) -> gi_frame:
+    return gi_frame(int(width), int(height), int(tile), int(batch), float(k))
+
+
+# Every exported symbol of include/gi.h, with its ctypes signature.
+_vp, _sz, _i32, _i64, _u32, _f32, _f64 = (C.c_void_p, C.c_size_t, C.c_int32, C.c_int64,
+                                          C.c_uint32, C.c_float, C.c_double)
+_FP = C.POINTER(gi_frame)
+SIGNATURES = {
+    "gi_status_string": (C.c_char_p, [C.c_int]),
+    "gi_last_error": (C.c_char_p, []),
+    "gi_abi_version": (_i32, []),
+    "gi_num_tiles": (_i32, [_FP]),
+    "gi_proj_bytes": (_sz, [_i32, _FP]),
+    "gi_project": (C.c_int, [_vp, _i32, _FP, _u32, _vp, _vp, _vp]),
+    "gi_bin_workspace_bytes": (_sz, [_i32, _i64, _FP]),
+    "gi_bin": (C.c_int, [_vp, _vp, _i32, _FP, _i64, _vp, _sz, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "gi_render": (C.c_int, [_vp, _vp, _vp, _i32, _FP, _vp, _vp]),
+    "gi_backward_workspace_bytes": (_sz, [_i32, _i64, _FP]),
+    "gi_render_backward": (C.c_int, [_vp, _vp, _vp, _vp, _vp, _i32, _FP, _u32, _vp, _vp, _i64,
+                                     _vp, _sz, _vp, _vp, _vp, _vp]),
+    "gi_adam_step": (C.c_int, [_vp, _vp, _vp, _vp, _i64, _i32, _f32, _f32, _f32, _f32, _vp, _vp]),
+    "gi_lr_at": (_f64, [_i32, _f64, _i32]),
+    "gi_fit_workspace_bytes": (_sz, [_i32, _i64, _FP]),
+    "gi_fit_n_keys": (_vp, [_vp, _i32, _i64, _FP]),
+    "gi_fit_step": (C.c_int, [_vp, _vp, _vp, _vp, _vp, _i32, _FP, _u32, _i64, _vp, _sz, _vp,
+                              _f32, _i32, _f32, _f32, _f32, _vp, _vp, _vp]),
+    "gi_vq_decode": (C.c_int, [_vp, _sz, C.POINTER(gi_codec_meta), _vp, _vp]),
+    "gi_psnr_workspace_bytes": (_sz, [_FP]),
+    "gi_psnr": (C.c_int, [_vp, _vp, _FP, _vp, _vp, _vp]),
+    "gi_check": (C.c_int, [_vp, _i64, _vp, _vp]),
+}
+
+_lib = None
+
+
+def lib_path() -> str:
+    return _build.LIB
+
+
+def load(build_if_stale: bool = False):
+    """Load libgi.so (raises if it is missing; the product has no fallback)."""
+    global _lib
+    if _lib is None:
+        if build_if_stale:
+            _build.build()
+        if not os.path.exists(_build.LIB):
+            raise RuntimeError(f"libgi.so not built at {_build.LIB}: run __graft_entry__.build()")
+        L = C.CDLL(_build.LIB)
+        for name, (res, args) in SIGNATURES.items():
+            fn = getattr(L, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = L
+    return _lib
+
+
+def _ptr(t) -> int | None:
+    if t is None:
+        return None
+    if isinstance(t, int):
+        return t
+    if not t.is_cuda:
+        raise ValueError("libgi takes device tensors")
+    if not t.is_contiguous():
+        raise ValueError("tensor must be contiguous")
+    return t.data_ptr()
+
+
+def _stream(stream) -> int | None:
+    if stream is None:
+        return torch.cuda.current_stream().cuda_stream
+    if isinstance(stream, int):
+        return stream
+    return stream.cuda_stream
+
+
+def _ok(status: int, where: str):
+    if status != GI_OK:
+        detail = load().gi_last_error()
+        raise GiError(status, where, detail.decode() if detail else "")
+
+
+# ------------------------------------------------------------------ queries
+def gi_abi_version() -> int:
+    return load().gi_abi_version()
+
+
+def gi_num_tiles(f: gi_frame) -> int:
+    return load().gi_num_tiles(C.byref(f))
+
+
+def gi_proj_bytes(n: int, f: gi_frame) -> int:
+    return load().gi_proj_bytes(int(n), C.byref(f))
+
+
+def gi_bin_workspace_bytes(n: int, key_capacity: int, f: gi_frame) -> int:
+    return load().gi_bin_workspace_bytes(int(n), int(key_capacity), C.byref(f))
+
+
+def gi_backward_workspace_bytes(n: int, key_capacity: int, f: gi_frame) -> int:
+    return load().gi_backward_workspace_bytes(int(n), int(key_capacity), C.byref(f))
+
+
+def gi_fit_workspace_bytes(n: int, key_capacity: int, f: gi_frame) -> int:
+    return load().gi_fit_workspace_bytes(int(n), int(key_capacity), C.byref(f))
+
+
+def gi_psnr_workspace_bytes(f: gi_frame) -> int:
+    return load().gi_psnr_workspace_bytes(C.byref(f))
+
+
+def gi_lr_at(step: int, lr0: float = 1e-3, half_every: int = 20000) -> float:
+    return load().gi_lr_at(int(step), float(lr0), int(half_every))
+
+
+def gi_fit_n_keys(fit_ws, n: int, key_capacity: int, f: gi_frame) -> int:
+    return load().gi_fit_n_keys(_ptr(fit_ws), int(n), int(key_capacity), C.byref(f))
+
+
+# ------------------------------------------------------------- hot path
+def gi_project(params, n, f, flags, proj, tiles_touched, stream=None):
+    _ok(load().gi_project(_ptr(params), int(n), C.byref(f), int(flags), _ptr(proj),
+                          _ptr(tiles_touched), _stream(stream)), "gi_project")
+
+
+def gi_bin(proj, tiles_touched, n, f, key_capacity, ws, gauss_offset, key_tile, key_gid,
+           tile_range, n_keys, stream=None):
+    _ok(load().gi_bin(_ptr(proj), _ptr(tiles_touched), int(n), C.byref(f), int(key_capacity),
+                      _ptr(ws), ws.numel() * ws.element_size(), _ptr(gauss_offset),
+                      _ptr(key_tile), _ptr(key_gid), _ptr(tile_range), _ptr(n_keys),
+                      _stream(stream)), "gi_bin")
+
+
+def gi_render(proj, key_gid, tile_range, n, f, image, stream=None):
+    _ok(load().gi_render(_ptr(proj), _ptr(key_gid), _ptr(tile_range), int(n), C.byref(f),
+                         _ptr(image), _stream(stream)), "gi_render")
+
+
+def gi_render_backward(params, proj, key_gid, tile_range, gauss_offset, n, f, flags, dL_dimage,
+                       target, key_capacity, ws, grads, loss=None, image_out=None, stream=None):
+    _ok(load().gi_render_backward(_ptr(params), _ptr(proj), _ptr(key_gid), _ptr(tile_range),
+                                  _ptr(gauss_offset), int(n), C.byref(f), int(flags),
+                                  _ptr(dL_dimage), _ptr(target), int(key_capacity), _ptr(ws),
+                                  ws.numel() * ws.element_size(), _ptr(grads), _ptr(loss),
+                                  _ptr(image_out), _stream(stream)), "gi_render_backward")
+
+
+def gi_adam_step(params, grads, m, v, count, step, lr, beta1=0.9, beta2=0.999, eps=1e-8,
+                 nonfinite_flag=None, stream=None):
+    _ok(load().gi_adam_step(_ptr(params), _ptr(grads), _ptr(m), _ptr(v), int(count), int(step),
+                            float(lr), float(beta1), float(beta2), float(eps),
+                            _ptr(nonfinite_flag), _stream(stream)), "gi_adam_step")
+
+
+def gi_fit_step(params, grads, m, v, target, n, f, flags, key_capacity, fit_ws, step_counter,
+                lr0=1e-3, half_every=20000, beta1=0.9, beta2=0.999, eps=1e-8, loss=None,
+                status_flags=None, stream=None):
+    _ok(load().gi_fit_step(_ptr(params), _ptr(grads), _ptr(m), _ptr(v), _ptr(target), int(n),
+                           C.byref(f), int(flags), int(key_capacity), _ptr(fit_ws),
+                           fit_ws.numel() * fit_ws.element_size(), _ptr(step_counter),
+                           float(lr0), int(half_every), float(beta1), float(beta2), float(eps),
+                           _ptr(loss), _ptr(status_flags), _stream(stream)), "gi_fit_step")
+
+
+def gi_vq_decode(payload, meta: gi_codec_meta, params, stream=None):
+    _ok(load().gi_vq_decode(_ptr(payload), payload.numel(), C.byref(meta), _ptr(params),
+                            _stream(stream)), "gi_vq_decode")
+
+
+def gi_psnr(image, target, f, psnr, ws, stream=None):
+    _ok(load().gi_psnr(_ptr(image), _ptr(target), C.byref(f), _ptr(psnr), _ptr(ws),
+                       _stream(stream)), "gi_psnr")
+
+
+def gi_check(n_keys=None, key_capacity=0, status_flags=None, stream=None) -> int:
+    """Sync and translate device status words -> GI_OK / GI_ECAPACITY / GI_ENONFINITE."""
+    return load().gi_check(_ptr(n_keys), int(key_capacity), _ptr(status_flags), _stream(stream))
+
+
+def codec_meta(n, gamma, beta, codebooks, bits=6, stages=2, codebook=8) -> gi_codec_meta:
+    m = gi_codec_meta()
+    m.n, m.bits, m.stages, m.codebook = int(n), int(bits), int(stages), int(codebook)
+    for i in range(3):
+        m.gamma[i] = float(gamma[i])
+        m.beta[i] = float(beta[i])
+    m.codebooks = _ptr(codebooks)
+    return m

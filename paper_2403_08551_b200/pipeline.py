@@ -1,0 +1,158 @@
+"""Device-resident buffers around the libgi C ABI: allocation (torch, once),
+the render / fit-step sequences, and CUDA-graph capture of a fit step.
+
+No arithmetic of the method lives here -- every step is a libgi call.
+"""
+from __future__ import annotations
+
+import torch
+
+from . import gi
+
+
+def _u32(n: int, device) -> torch.Tensor:
+    # uint32 storage; torch.int32 has the same bits and full op support
+    return torch.zeros(max(int(n), 1), dtype=torch.int32, device=device)
+
+
+def _bytes(n: int, device) -> torch.Tensor:
+    # raw workspace of >= n bytes; torch allocations are >= 256-B aligned
+    return torch.zeros(max((int(n) + 15) // 16, 1) * 4, dtype=torch.float32, device=device)
+
+
+def default_capacity(n: int, batch: int) -> int:
+    """Generous key capacity: 16 tiles per Gaussian on average (the paper's
+    init touches ~1.8, a 3x-larger fitted cloud ~4.5), at least 64 Ki."""
+    return max(1 << 16, 16 * int(n) * int(batch))
+
+
+class Pipeline:
+    """All buffers of one (n, W, H, batch) problem on one device."""
+
+    def __init__(self, n: int, width: int, height: int, batch: int = 1, k: float = 3.0,
+                 key_capacity: int | None = None, device: str | torch.device = "cuda"):
+        gi.load()
+        self.device = torch.device(device)
+        self.n, self.W, self.H, self.B = int(n), int(width), int(height), int(batch)
+        self.f = gi.frame(width, height, batch, k)
+        self.T = gi.gi_num_tiles(self.f)
+        self.cap = int(key_capacity) if key_capacity else default_capacity(n, batch)
+        d = self.device
+        tot = self.n * self.B
+        self.proj = torch.zeros(max(tot, 1) * gi.GI_PROJ_BYTES // 4, dtype=torch.float32, device=d)
+        self.tiles_touched = _u32(tot, d)
+        self.gauss_offset = _u32(tot + 1, d)
+        self.key_tile = _u32(self.cap, d)
+        self.key_gid = _u32(self.cap, d)
+        self.tile_range = _u32(self.T * self.B + 1, d)
+        self.n_keys = _u32(1, d)
+        self.bin_ws = _bytes(gi.gi_bin_workspace_bytes(n, self.cap, self.f), d)
+        self.bwd_ws = _bytes(gi.gi_backward_workspace_bytes(n, self.cap, self.f), d)
+        self.psnr_ws = _bytes(gi.gi_psnr_workspace_bytes(self.f), d)
+        self.image = torch.zeros(self.B, 3, self.H, self.W, dtype=torch.float32, device=d)
+        self.grads = torch.zeros(self.B, max(self.n, 1), 8, dtype=torch.float32, device=d)
+        self.loss = torch.zeros(self.B, dtype=torch.float32, device=d)
+        self.psnr_out = torch.zeros(self.B, dtype=torch.float32, device=d)
+        self.flags_word = _u32(1, d)
+
+    # -- stages -----------------------------------------------------------
+    def project(self, params, flags=gi.GI_POS_LOGIT, stream=None):
+        gi.gi_project(params, self.n, self.f, flags, self.proj, self.tiles_touched, stream)
+
+    def bin(self, stream=None):
+        gi.gi_bin(self.proj, self.tiles_touched, self.n, self.f, self.cap, self.bin_ws,
+                  self.gauss_offset, self.key_tile, self.key_gid, self.tile_range, self.n_keys,
+                  stream)
+
+    def raster(self, stream=None):
+        gi.gi_render(self.proj, self.key_gid, self.tile_range, self.n, self.f, self.image, stream)
+
+    def render(self, params, flags=gi.GI_POS_LOGIT, stream=None) -> torch.Tensor:
+        """project -> bin -> render (Eq. 7); returns the [B][3][H][W] image buffer."""
+        self.project(params, flags, stream)
+        self.bin(stream)
+        self.raster(stream)
+        return self.image
+
+    def backward(self, params, target=None, dL_dimage=None, flags=gi.GI_POS_LOGIT,
+                 image_out=None, stream=None) -> torch.Tensor:
+        """Fused forward + L2 + backward on the current bins (after project/bin)."""
+        gi.gi_render_backward(params, self.proj, self.key_gid, self.tile_range, self.gauss_offset,
+                              self.n, self.f, flags, dL_dimage, target, self.cap, self.bwd_ws,
+                              self.grads, self.loss if dL_dimage is None else None, image_out,
+                              stream)
+        return self.grads
+
+    def psnr(self, image, target, stream=None) -> torch.Tensor:
+        gi.gi_psnr(image, target, self.f, self.psnr_out, self.psnr_ws, stream)
+        return self.psnr_out
+
+    def check(self, stream=None) -> int:
+        return gi.gi_check(self.n_keys, self.cap, self.flags_word, stream)
+
+    def keys(self) -> int:
+        return int(self.n_keys[0].item()) & 0xffffffff
+
+
+class Fitter:
+    """Adam fitting loop over B images with the device-resident fused step
+    (gi_fit_step), optionally replayed from a captured CUDA graph."""
+
+    def __init__(self, params: torch.Tensor, target: torch.Tensor, k: float = 3.0,
+                 key_capacity: int | None = None, lr0: float = 1e-3, half_every: int = 20000,
+                 beta1: float = 0.9, beta2: float = 0.999, eps: float = 1e-8,
+                 flags: int = gi.GI_POS_LOGIT):
+        gi.load()
+        assert params.dim() == 3 and params.shape[2] == 8, "params [B][N][8]"
+        B, n = params.shape[0], params.shape[1]
+        H, W = target.shape[-2], target.shape[-1]
+        self.device = params.device
+        self.params = params.contiguous()
+        self.target = target.contiguous()
+        self.n, self.B = n, B
+        self.f = gi.frame(W, H, B, k)
+        self.cap = int(key_capacity) if key_capacity else default_capacity(n, B)
+        self.fit_ws = _bytes(gi.gi_fit_workspace_bytes(n, self.cap, self.f), self.device)
+        self.grads = torch.zeros_like(self.params)
+        self.m = torch.zeros_like(self.params)
+        self.v = torch.zeros_like(self.params)
+        self.step_counter = _u32(1, self.device)
+        self.status = _u32(1, self.device)
+        self.loss = torch.zeros(B, dtype=torch.float32, device=self.device)
+        self.hyper = dict(lr0=lr0, half_every=half_every, beta1=beta1, beta2=beta2, eps=eps)
+        self.flags = flags
+        self.graph = None
+
+    def step(self, stream=None):
+        gi.gi_fit_step(self.params, self.grads, self.m, self.v, self.target, self.n, self.f,
+                       self.flags, self.cap, self.fit_ws, self.step_counter, loss=self.loss,
+                       status_flags=self.status, stream=stream, **self.hyper)
+
+    def capture(self, steps_per_graph: int = 1):
+        """Capture `steps_per_graph` fused steps into one CUDA graph."""
+        s = torch.cuda.Stream(device=self.device)
+        s.wait_stream(torch.cuda.current_stream(self.device))
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            for _ in range(steps_per_graph):
+                self.step()
+        torch.cuda.current_stream(self.device).wait_stream(s)
+        self.graph = g
+        self.steps_per_graph = steps_per_graph
+        return g
+
+    def replay(self):
+        self.graph.replay()
+
+    def n_keys(self) -> int:
+        ptr = gi.gi_fit_n_keys(self.fit_ws, self.n, self.cap, self.f)
+        base = self.fit_ws.data_ptr()
+        off = (ptr - base) // 4
+        return int(self.fit_ws.view(torch.int32)[off].item()) & 0xffffffff
+
+    def check(self) -> int:
+        ptr = gi.gi_fit_n_keys(self.fit_ws, self.n, self.cap, self.f)
+        return gi.gi_check(ptr, self.cap, self.status)
+
+    def steps_done(self) -> int:
+        return int(self.step_counter[0].item())

@@ -1,0 +1,312 @@
+"""CUDA path (through the C ABI) vs the fp64 oracle, element by element.
+
+Bars (north_star):
+  * keys, ranges, offsets, tile counts, boxes, decode: bit-exact
+  * pixels: max |gpu - oracle| <= 2e-5 on unclamped output
+  * gradients: ||g_gpu - g_ref|| / ||g_ref|| <= 1e-4 per group (mu, l, c')
+  * Adam: elementwise, tolerance derived from fp32 rounding of each term
+Configs: C1 64x64/256 (all-pairs oracle), ragged frames, C2 768x512/70k at the
+paper's init and at the 3x "fitted" proxy (tiled oracle, full frame), C3
+2040x1356/100k (full frame), batches of images per launch.
+"""
+import numpy as np
+import pytest
+import torch
+
+import synth
+
+pytestmark = pytest.mark.gpu
+
+DEV = "cuda:0"
+PIX_TOL = 2e-5
+GRAD_TOL = 1e-4
+GROUPS = {"mu": [0, 1], "l": [2, 3, 4], "c": [5, 6, 7]}
+
+CASES = {
+    "c1": (64, 64, 256, 0, False),
+    "ragged": (70, 45, 300, 1, False),
+    "tiny": (5, 3, 4, 2, False),
+    "c1_fitted": (64, 64, 256, 3, True),
+    "c2_init": (768, 512, 70000, 1, False),
+    "c2_fitted": (768, 512, 70000, 1, True),
+}
+
+
+def params_for(n, seed, fitted):
+    return synth.fitted_params(seed, n) if fitted else synth.init_params(seed, n)
+
+
+def to_dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).to(DEV)
+
+
+def u32(t):
+    return t.cpu().numpy().view(np.uint32)
+
+
+def run_gpu(gi, params_b, W, H, flags=0, target_b=None, dL=None):
+    from paper_2403_08551_b200.pipeline import Pipeline
+    B, n = params_b.shape[0], params_b.shape[1]
+    pipe = Pipeline(n, W, H, B, device=DEV)
+    p = to_dev(params_b)
+    pipe.render(p, flags)
+    img = pipe.image.clone()
+    out = dict(pipe=pipe, image=img.cpu().numpy())
+    if target_b is not None or dL is not None:
+        pipe.backward(p, target=None if target_b is None else to_dev(target_b),
+                      dL_dimage=None if dL is None else to_dev(dL), flags=flags)
+        out["grads"] = pipe.grads.cpu().numpy().astype(np.float64)
+        out["loss"] = pipe.loss.cpu().numpy().astype(np.float64)
+    torch.cuda.synchronize()
+    assert pipe.check() == gi.GI_OK
+    return out
+
+
+def group_err(g, ref):
+    errs = {}
+    for name, cols in GROUPS.items():
+        den = np.linalg.norm(ref[..., cols])
+        errs[name] = np.linalg.norm(g[..., cols] - ref[..., cols]) / max(den, 1e-300)
+    return errs
+
+
+@pytest.fixture(scope="module", params=list(CASES))
+def case(request, gio):
+    W, H, n, seed, fitted = CASES[request.param]
+    p = params_for(n, seed, fitted)
+    tgt = synth.image(seed, W, H)
+    mode = gio.ALL_PAIRS if W * H * n <= 64 * 64 * 300 else gio.TILED
+    ref_img, ref_loss, ref_g = gio.loss_and_grads(p, tgt, mode=mode)
+    return dict(name=request.param, W=W, H=H, n=n, p=p, tgt=tgt, ref_img=ref_img,
+                ref_loss=ref_loss, ref_g=ref_g)
+
+
+def test_project_and_bin_bitexact(gi, gio, case):
+    W, H, p = case["W"], case["H"], case["p"]
+    out = run_gpu(gi, p[None], W, H)
+    pipe = out["pipe"]
+    pr = gio.project(p, W, H)
+    touched = u32(pipe.tiles_touched)[: case["n"]]
+    assert np.array_equal(touched, pr["touched"])
+    rec = pipe.proj.view(-1, 12).cpu().numpy()
+    bx = rec[:, 7].view(np.uint32)
+    by = rec[:, 11].view(np.uint32)
+    valid = pr["touched"] > 0
+    box = np.stack([bx & 0xffff, bx >> 16, by & 0xffff, by >> 16], 1).astype(np.int32)
+    assert np.array_equal(box[valid], pr["box"][valid])
+    # split centre reproduces the fp64 centre to fp32 rounding of the fraction
+    ix = rec[:, 0].view(np.int32).astype(np.float64)
+    iy = rec[:, 1].view(np.int32).astype(np.float64)
+    assert np.abs(ix + rec[:, 2] - pr["mu"][:, 0]).max() < 1e-6
+    assert np.abs(iy + rec[:, 3] - pr["mu"][:, 1]).max() < 1e-6
+    kt, kg, rng = gio.bin(p, W, H)
+    K = len(kt)
+    assert pipe.keys() == K
+    assert np.array_equal(u32(pipe.key_tile)[:K], kt)
+    assert np.array_equal(u32(pipe.key_gid)[:K], kg)
+    assert np.array_equal(u32(pipe.tile_range)[: len(rng)], rng)
+    off = np.concatenate([[0], np.cumsum(pr["touched"].astype(np.int64))])
+    assert np.array_equal(u32(pipe.gauss_offset)[: case["n"] + 1], off.astype(np.uint32))
+
+
+def test_render_parity(gi, gio, case):
+    out = run_gpu(gi, case["p"][None], case["W"], case["H"])
+    err = np.abs(out["image"][0] - case["ref_img"]).max()
+    assert err <= PIX_TOL, err
+
+
+def test_loss_and_backward_parity(gi, gio, case):
+    out = run_gpu(gi, case["p"][None], case["W"], case["H"], target_b=case["tgt"][None])
+    errs = group_err(out["grads"][0], case["ref_g"])
+    assert max(errs.values()) <= GRAD_TOL, errs
+    assert abs(out["loss"][0] - case["ref_loss"]) <= 1e-5 * max(case["ref_loss"], 1e-3)
+
+
+def test_backward_explicit_upstream(gi, gio):
+    W, H, n = 70, 45, 300
+    p = synth.init_params(4, n)
+    rng = np.random.default_rng(4)
+    dL = rng.normal(size=(3, H, W)).astype(np.float32)
+    ref = gio.backward(p, dL.astype(np.float64), W, H)
+    out = run_gpu(gi, p[None], W, H, dL=dL[None])
+    errs = group_err(out["grads"][0], ref)
+    assert max(errs.values()) <= GRAD_TOL, errs
+
+
+def test_normalized_positions(gi, gio):
+    # decode path: params[0:2] already in (-1, 1) (GI_POS_NORMALIZED)
+    W, H, n = 96, 80, 400
+    p = synth.init_params(5, n)
+    p[:, :2] = np.tanh(p[:, :2].astype(np.float64)).astype(np.float32)
+    tgt = synth.image(5, W, H)
+    ref_img, ref_loss, ref_g = gio.loss_and_grads(p, tgt, pos_mode=gio.POS_NORMALIZED,
+                                                  mode=gio.ALL_PAIRS)
+    out = run_gpu(gi, p[None], W, H, flags=gi.GI_POS_NORMALIZED, target_b=tgt[None])
+    assert np.abs(out["image"][0] - ref_img).max() <= PIX_TOL
+    errs = group_err(out["grads"][0], ref_g)
+    assert max(errs.values()) <= GRAD_TOL, errs
+
+
+def test_batched_launch(gi, gio):
+    # B images per launch: tile ids img*T + t, gids img*N + n
+    W, H, n, B = 100, 60, 500, 3
+    pb = np.stack([synth.init_params(10 + b, n) for b in range(B)])
+    tb = np.stack([synth.image(10 + b, W, H) for b in range(B)])
+    out = run_gpu(gi, pb, W, H, target_b=tb)
+    pipe = out["pipe"]
+    T = gio.n_tiles(W, H)
+    kts, kgs = [], []
+    for b in range(B):
+        img, loss, g = gio.loss_and_grads(pb[b], tb[b], mode=gio.ALL_PAIRS)
+        assert np.abs(out["image"][b] - img).max() <= PIX_TOL
+        assert max(group_err(out["grads"][b], g).values()) <= GRAD_TOL
+        assert abs(out["loss"][b] - loss) <= 1e-5 * max(loss, 1e-3)
+        kt, kg, _ = gio.bin(pb[b], W, H)
+        kts.append(kt + b * T)
+        kgs.append(kg + b * n)
+    kt, kg = np.concatenate(kts), np.concatenate(kgs)
+    assert pipe.keys() == len(kt)
+    assert np.array_equal(u32(pipe.key_tile)[: len(kt)], kt)
+    assert np.array_equal(u32(pipe.key_gid)[: len(kg)], kg)
+
+
+def test_c3_render_sampled(gi, gio):
+    # C3 (DIV2K-shaped 2040x1356, 100k) full frame, in the bench launch shape
+    W, H, n = 2040, 1356, 100000
+    p = synth.init_params(2, n)
+    out = run_gpu(gi, p[None], W, H)
+    ref = gio.render(p, W, H, mode=gio.TILED)
+    assert np.abs(out["image"][0] - ref).max() <= PIX_TOL
+    kt, kg, rng = gio.bin(p, W, H)
+    assert out["pipe"].keys() == len(kt)
+    assert np.array_equal(u32(out["pipe"].key_gid)[: len(kg)], kg)
+
+
+def test_edge_cases(gi, gio):
+    from paper_2403_08551_b200.pipeline import Pipeline
+    # all Gaussians culled (l1 + 1/2 == 0): empty lists, zero image, zero grads
+    p = synth.init_params(6, 50)
+    p[:, 2] = -0.5
+    out = run_gpu(gi, p[None], 40, 30, target_b=synth.image(6, 40, 30)[None])
+    assert out["pipe"].keys() == 0
+    assert not out["image"].any() and not out["grads"].any()
+    # one huge Gaussian covering every tile of a ragged frame
+    p = np.array([[0.0, 0.0, 200.0, 5.0, 150.0, 0.5, -0.25, 1.0]], np.float32)
+    tgt = synth.image(7, 100, 37)
+    ref_img, _, ref_g = gio.loss_and_grads(p, tgt, mode=gio.ALL_PAIRS)
+    out = run_gpu(gi, p[None], 100, 37, target_b=tgt[None])
+    assert out["pipe"].keys() == gio.n_tiles(100, 37)
+    assert np.abs(out["image"][0] - ref_img).max() <= PIX_TOL
+    assert max(group_err(out["grads"][0], ref_g).values()) <= GRAD_TOL
+    # 1x1 frame
+    p = synth.init_params(8, 3)
+    ref = gio.render(p, 1, 1)
+    out = run_gpu(gi, p[None], 1, 1)
+    assert np.abs(out["image"][0] - ref).max() <= PIX_TOL
+    # n = 0
+    pipe = Pipeline(0, 32, 32, 1, device=DEV)
+    pipe.render(torch.zeros(1, 1, 8, device=DEV))
+    torch.cuda.synchronize()
+    assert pipe.keys() == 0 and not pipe.image.any()
+    # capacity overflow is reported, not a crash
+    p = synth.fitted_params(9, 2000)
+    pipe = Pipeline(2000, 128, 128, 1, key_capacity=64, device=DEV)
+    pipe.render(to_dev(p))
+    assert pipe.check() == gi.GI_ECAPACITY
+
+
+def test_adam_parity(gi, gio):
+    rng = np.random.default_rng(12)
+    n = 4096 + 3                               # float4 body + scalar tail
+    p = rng.normal(size=n).astype(np.float32)
+    g = (rng.normal(size=n) * 10.0 ** rng.uniform(-6, 1, size=n)).astype(np.float32)
+    m = (rng.normal(size=n) * 0.01).astype(np.float32)
+    v = (rng.uniform(0, 1, size=n) * 1e-3).astype(np.float32)
+    for step, lr in [(1, 1e-3), (7, 1e-3), (20001, 5e-4)]:
+        pt, gt, mt, vt = to_dev(p), to_dev(g), to_dev(m), to_dev(v)
+        flag = torch.zeros(1, dtype=torch.int32, device=DEV)
+        gi.gi_adam_step(pt, gt, mt, vt, n, step, lr, nonfinite_flag=flag)
+        po, mo, vo = gio.adam(p, g, m, v, step, lr)
+        b1, b2 = float(np.float32(0.9)), float(np.float32(0.999))
+        gd = g.astype(np.float64)
+        tol_m = 1e-6 * (np.abs(b1 * m) + np.abs((1 - b1) * gd)) + 1e-12
+        tol_v = 1e-6 * (np.abs(b2 * v) + np.abs((1 - b2) * gd * gd)) + 1e-12
+        upd = np.abs(po - p.astype(np.float64))
+        tol_p = 1e-6 * (np.abs(p) + upd) + 1e-12
+        assert np.all(np.abs(mt.cpu().numpy() - mo) <= tol_m)
+        assert np.all(np.abs(vt.cpu().numpy() - vo) <= tol_v)
+        assert np.all(np.abs(pt.cpu().numpy() - po) <= tol_p)
+        assert int(flag.item()) == 0
+    # non-finite detection
+    pt = to_dev(p); gt = to_dev(np.full(n, np.nan, np.float32))
+    flag = torch.zeros(1, dtype=torch.int32, device=DEV)
+    gi.gi_adam_step(pt, gt, to_dev(m), to_dev(v), n, 1, 1e-3, nonfinite_flag=flag)
+    assert gi.gi_check(None, 0, flag) == gi.GI_ENONFINITE
+
+
+@pytest.mark.parametrize("bits,n", [(6, 70000), (8, 1001), (6, 1)])
+def test_vq_decode_bitexact(gi, gio, bits, n):
+    data, gamma, beta, books = synth.payload(bits, n, bits=bits)
+    ref = gio.vq_decode(data, n, gamma, beta, books, bits=bits)
+    out = torch.zeros(n, 8, dtype=torch.float32, device=DEV)
+    bk = to_dev(books)
+    meta = gi.codec_meta(n, gamma, beta, bk, bits=bits)
+    gi.gi_vq_decode(to_dev(data), meta, out)
+    got = out.cpu().numpy()
+    assert np.array_equal(got.view(np.uint32), ref.view(np.uint32))
+
+
+def test_decode_then_render(gi, gio):
+    # C5 path: payload -> decode -> project(GI_POS_NORMALIZED) -> bin -> render
+    from paper_2403_08551_b200.pipeline import Pipeline
+    n, W, H = 4500, 768, 512
+    data, gamma, beta, books = synth.payload(3, n)
+    ref_p = gio.vq_decode(data, n, gamma, beta, books)
+    ref = gio.render(ref_p, W, H, pos_mode=gio.POS_NORMALIZED, mode=gio.TILED)
+    params = torch.zeros(1, n, 8, dtype=torch.float32, device=DEV)
+    gi.gi_vq_decode(to_dev(data), gi.codec_meta(n, gamma, beta, to_dev(books)), params)
+    pipe = Pipeline(n, W, H, 1, device=DEV)
+    img = pipe.render(params, gi.GI_POS_NORMALIZED)
+    assert np.abs(img[0].cpu().numpy() - ref).max() <= PIX_TOL
+
+
+def test_fit_step_matches_oracle(gi, gio):
+    # one fused device step (project, bin, fwd+L2+bwd, Adam) from a fresh state
+    from paper_2403_08551_b200.pipeline import Fitter
+    W, H, n = 64, 64, 256
+    p = synth.init_params(0, n)
+    tgt = synth.image(0, W, H)
+    fit = Fitter(to_dev(p)[None].contiguous(), to_dev(tgt)[None].contiguous())
+    fit.step()
+    torch.cuda.synchronize()
+    assert fit.check() == gi.GI_OK and fit.steps_done() == 1
+    img, loss, g = gio.loss_and_grads(p, tgt, mode=gio.ALL_PAIRS)
+    assert abs(float(fit.loss[0]) - loss) <= 1e-5 * loss
+    gg = fit.grads[0].cpu().numpy().astype(np.float64)
+    assert max(group_err(gg, g).values()) <= GRAD_TOL
+    # Adam step 1 from zero state, on the oracle's gradients: p - lr g/(|g|+eps);
+    # compare where the oracle gradient is well above the gradient error
+    z = np.zeros_like(p)
+    po, _, _ = gio.adam(p, g.astype(np.float32), z, z, 1, 1e-3)
+    got = fit.params[0].cpu().numpy().astype(np.float64)
+    big = np.abs(g) > 1e-3 * np.sqrt(np.mean(g ** 2, axis=0, keepdims=True))
+    assert big.mean() > 0.9
+    assert np.all(np.abs(got - po)[big] <= 1e-6 * np.abs(po)[big] + 1e-9)
+
+
+def test_fit_graph_loss_decreases(gi):
+    from paper_2403_08551_b200.pipeline import Fitter
+    W, H, n = 128, 96, 2000
+    p = synth.init_params(1, n)
+    tgt = synth.image(1, W, H)
+    fit = Fitter(to_dev(p)[None].contiguous(), to_dev(tgt)[None].contiguous())
+    fit.step()
+    torch.cuda.synchronize()
+    l0 = float(fit.loss[0])
+    fit.capture(10)
+    for _ in range(30):
+        fit.replay()
+    torch.cuda.synchronize()
+    assert fit.check() == gi.GI_OK
+    assert fit.steps_done() == 1 + 300        # capture records, it does not execute
+    assert float(fit.loss[0]) < 0.5 * l0
