@@ -1,0 +1,446 @@
+#!/usr/bin/env python
+"""GaussianImage hot-path benchmark on B200 (driver contract).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Workload (configs[1], "C2"): a Kodak-shaped 768x512 synthetic image fitted by
+70,000 Gaussians (560K parameters, Table 1) with Adam.  A STEP is one
+fit iteration of the whole hot path: project -> tile-bin (radix sort, no
+depth key) -> fused forward (Eq. 7) + L2 loss + Appendix-A backward ->
+per-Gaussian finalize -> Adam (paper schedule).  The JSON line's `value` is
+fit iterations/s over all ranks; `render_fps` (project + bin + render) and
+`decode_fps` (RVQ/fp16/b-bit decode + project + bin + render, configs[4] at
+70k records) are measured in the same run.  The L2 cache (126 MB) is flushed
+with a 256 MB write before every timed step (the C2 working set is ~60 MB).
+
+Multi-GPU (torchrun): each rank fits its own image (weak scaling, no
+collective on the data path); per-image PSNR is all-gathered over NCCL at
+the end; timings are the max over ranks.
+
+--impl reference: the fp64 CPU oracle (oracle/), unmodified, timed on the
+host cores for the same metric -- rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = ("render FPS + fit iters/s @768×512, 70k Gaussians; fraction of FP32/HBM "
+          "roofline")
+W_IMG, H_IMG, N_GAUSS = 768, 512, 70000
+PAPER_FIT_ITS = 50000 / 106.59        # Table 1a, V100, Adan: 469.1 it/s
+L2_FLUSH_BYTES = 256 << 20
+# algorithmic FP32 work per (pixel, Gaussian) pair in the box:
+#   forward  (Eq. 5 + 7, factored conic): 15 FLOP + 1 ex2
+#   backward (App. A, 5-moment form)   : 34 FLOP + 1 ex2
+FLOP_PER_PAIR_FUSED = 15 + 34
+FLOP_PER_PAIR_RENDER = 15
+FP32_LANES_PER_SM = 128
+N_SM = 148
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        return d, "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "sm_max_mhz": 1965.0}, "fallback"
+
+
+# ------------------------------------------------------------------ clocks
+class Clocks:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "50", "-i", str(self.index)],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        self.proc.terminate()
+        out, _ = self.proc.communicate(timeout=10)
+        sm, mx, reasons = [], [], set()
+        for line in out.strip().splitlines():
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for name, val in zip(self.NAMES, parts[2:6]):
+                if val.lower().startswith("active"):
+                    reasons.add(name)
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------- reference
+def run_reference(args):
+    """The oracle, as it stands, on the host cores: C2 fit iterations."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import synth
+    from oracle import gio
+    p = synth.init_params(1, N_GAUSS)
+    tgt = synth.image(1, W_IMG, H_IMG)
+    m = np.zeros_like(p)
+    v = np.zeros_like(p)
+
+    def it(step, p, m, v):
+        _, loss, g = gio.loss_and_grads(p, tgt, mode=gio.TILED)
+        po, mo, vo = gio.adam(p, g.astype(np.float32), m, v, step, gio.lr_at(step))
+        return po.astype(np.float32), mo.astype(np.float32), vo.astype(np.float32), loss
+
+    t0 = time.time()
+    p, m, v, _ = it(1, p, m, v)
+    est = time.time() - t0
+    budget = 150.0
+    warm = max(0, min(args.warmup, int(30.0 / max(est, 1e-3))))
+    steps = max(1, min(args.steps, int(budget / max(est, 1e-3))))
+    step = 2
+    for _ in range(warm):
+        p, m, v, _ = it(step, p, m, v)
+        step += 1
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        p, m, v, loss = it(step, p, m, v)
+        step += 1
+    dt = time.perf_counter() - t0
+    val = steps / dt
+    cores = gio.num_threads()
+    sample = (f"{steps} fp64 oracle fit iterations (tiled render + L2 + Appendix-A backward + "
+              f"Adam) of C2 768x512 / 70k Gaussians")
+    line = {"impl": "reference", "metric": METRIC, "value": val, "unit": "it/s",
+            "n_gpus": args.gpus, "steps": args.steps, "steps_timed": steps, "warmup": args.warmup,
+            "ms_per_step": 1000.0 * dt / steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": "C2: Kodak-shaped 768x512 synthetic image, 70k Gaussians, "
+                                   "Adam fit step", "oracle_threads": cores},
+            "cpu_baseline": {"value": val, "unit": "it/s", "cores": cores, "kind": "oracle",
+                             "sample": sample},
+            "e2e": {"value": val, "unit": "it/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0},
+            "gpu_launches": 0}
+    print(json.dumps(line), flush=True)
+
+
+def cpu_baseline(seconds: float):
+    import synth
+    from oracle import gio
+    p = synth.init_params(1, N_GAUSS)
+    tgt = synth.image(1, W_IMG, H_IMG)
+    m = np.zeros_like(p)
+    v = np.zeros_like(p)
+    n = 0
+    t0 = time.perf_counter()
+    while True:
+        _, loss, g = gio.loss_and_grads(p, tgt, mode=gio.TILED)
+        po, mo, vo = gio.adam(p, g.astype(np.float32), m, v, n + 1, gio.lr_at(n + 1))
+        p, m, v = po.astype(np.float32), mo.astype(np.float32), vo.astype(np.float32)
+        n += 1
+        if time.perf_counter() - t0 >= seconds:
+            break
+    dt = time.perf_counter() - t0
+    return {"value": n / dt, "unit": "it/s", "cores": gio.num_threads(), "kind": "oracle",
+            "sample": f"{n} fp64 oracle fit iterations of C2 (768x512, 70k Gaussians, tiled "
+                      f"render + L2 + backward + Adam) in {dt:.1f} s"}
+
+
+# ------------------------------------------------------------------- ours
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+    import torch
+    import torch.distributed as dist
+
+    import synth
+    from paper_2403_08551_b200 import gi
+    from paper_2403_08551_b200.pipeline import Fitter, Pipeline
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl")
+    dev = torch.device("cuda", local if world > 1 else 0)
+    torch.cuda.set_device(dev)
+    gi.load()
+    K, Wm = max(1, args.steps), max(3, args.warmup)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+
+    def max_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    seed = 1 + rank
+    p_host = synth.init_params(seed, N_GAUSS)
+    t_host = synth.image(seed, W_IMG, H_IMG)
+    params = torch.from_numpy(p_host).to(dev).view(1, N_GAUSS, 8).contiguous()
+    target = torch.from_numpy(t_host).to(dev).view(1, 3, H_IMG, W_IMG).contiguous()
+    flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    clocks = Clocks(local)
+
+    # ---------------- fit step (value) ----------------
+    fit = Fitter(params.clone(), target)
+    fit.step()
+    torch.cuda.synchronize(dev)
+    st = fit.check()
+    if st != gi.GI_OK:
+        raise RuntimeError(f"fit step status {st}")
+    stage_ev = [torch.cuda.Event(enable_timing=True, external=True) for _ in range(6)]
+    for e in stage_ev:
+        e.record(stream)
+    torch.cuda.synchronize(dev)
+    n0 = gi.gi_launch_count()
+    fit.capture(1, stage_events=stage_ev)
+    launches_per_step = gi.gi_launch_count() - n0
+    for _ in range(Wm):
+        fit.replay()
+    torch.cuda.synchronize(dev)
+    # pair count for the roofline at the state the timed steps start from
+    probe = Pipeline(N_GAUSS, W_IMG, H_IMG, 1, device=dev)
+    probe.project(fit.params)
+    rec = probe.proj.view(-1, 12).cpu().numpy()
+    bx, by = rec[:, 7].view(np.uint32), rec[:, 11].view(np.uint32)
+    wx = (bx >> 16).astype(np.int64) - (bx & 0xffff).astype(np.int64) + 1
+    wy = (by >> 16).astype(np.int64) - (by & 0xffff).astype(np.int64) + 1
+    touched = probe.tiles_touched.cpu().numpy() > 0
+    pairs = int(np.sum(np.where(touched, wx * wy, 0)))
+    keys = int(probe.tiles_touched.cpu().numpy().astype(np.int64).sum())
+    del probe
+
+    s_ev = [torch.cuda.Event(enable_timing=True) for _ in range(K)]
+    e_ev = [torch.cuda.Event(enable_timing=True) for _ in range(K)]
+    stage_ms = np.zeros(5)
+    barrier()
+    clocks.start()
+    for i in range(K):
+        flush.zero_()
+        s_ev[i].record(stream)
+        fit.replay()
+        e_ev[i].record(stream)
+        torch.cuda.synchronize(dev)
+        for j in range(5):
+            stage_ms[j] += stage_ev[j].elapsed_time(stage_ev[j + 1])
+    barrier()
+    fit_ms = sum(s_ev[i].elapsed_time(e_ev[i]) for i in range(K))
+    fit_ms_max = max_over_ranks(fit_ms)
+    fit_value = world * K / (fit_ms_max / 1000.0)
+    stage_ms /= K
+    st = fit.check()
+    if st != gi.GI_OK:
+        raise RuntimeError(f"fit status after timing {st}")
+
+    # ---------------- render FPS ----------------
+    pipe = Pipeline(N_GAUSS, W_IMG, H_IMG, 1, device=dev)
+    rparams = params.clone()
+    pipe.render(rparams)
+    torch.cuda.synchronize(dev)
+    rs = torch.cuda.Stream(device=dev)
+    rs.wait_stream(stream)
+    rg = torch.cuda.CUDAGraph()
+    r_ev = [torch.cuda.Event(enable_timing=True, external=True) for _ in range(2)]
+    for e in r_ev:
+        e.record(stream)
+    torch.cuda.synchronize(dev)
+    with torch.cuda.graph(rg, stream=rs):
+        pipe.project(rparams)
+        pipe.bin()
+        r_ev[0].record()
+        pipe.raster()
+        r_ev[1].record()
+    stream.wait_stream(rs)
+    for _ in range(Wm):
+        rg.replay()
+    barrier()
+    r_ms, r_kernel_ms = 0.0, 0.0
+    for i in range(K):
+        flush.zero_()
+        s_ev[i].record(stream)
+        rg.replay()
+        e_ev[i].record(stream)
+        torch.cuda.synchronize(dev)
+        r_kernel_ms += r_ev[0].elapsed_time(r_ev[1])
+    barrier()
+    r_ms = sum(s_ev[i].elapsed_time(e_ev[i]) for i in range(K))
+    render_fps = world * K / (max_over_ranks(r_ms) / 1000.0)
+    r_kernel_ms /= K
+    render_pairs = pairs_of(pipe, np)
+
+    # ---------------- decode FPS (configs[4]) ----------------
+    data, gamma, beta, books = synth.payload(seed, N_GAUSS)
+    d_payload = torch.from_numpy(data).to(dev)
+    d_books = torch.from_numpy(books).to(dev)
+    dparams = torch.zeros(1, N_GAUSS, 8, dtype=torch.float32, device=dev)
+    meta = gi.codec_meta(N_GAUSS, gamma, beta, d_books)
+    dpipe = Pipeline(N_GAUSS, W_IMG, H_IMG, 1, device=dev)
+    ds = torch.cuda.Stream(device=dev)
+    ds.wait_stream(stream)
+    dg = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(dg, stream=ds):
+        gi.gi_vq_decode(d_payload, meta, dparams)
+        dpipe.render(dparams, gi.GI_POS_NORMALIZED)
+    stream.wait_stream(ds)
+    for _ in range(Wm):
+        dg.replay()
+    barrier()
+    for i in range(K):
+        flush.zero_()
+        s_ev[i].record(stream)
+        dg.replay()
+        e_ev[i].record(stream)
+    barrier()
+    d_ms = sum(s_ev[i].elapsed_time(e_ev[i]) for i in range(K))
+    decode_fps = world * K / (max_over_ranks(d_ms) / 1000.0)
+
+    # ---------------- e2e through the public API, host buffers ----------------
+    pinned_t = torch.from_numpy(t_host).pin_memory()
+    pinned_loss = torch.zeros(1, dtype=torch.float32).pin_memory()
+    e2e_fit = Fitter(params.clone(), target.clone())
+    for _ in range(Wm):
+        e2e_fit.target.view(-1).copy_(pinned_t.view(-1), non_blocking=True)
+        e2e_fit.step()
+        pinned_loss.copy_(e2e_fit.loss, non_blocking=True)
+    barrier()
+    for i in range(K):
+        flush.zero_()
+        s_ev[i].record(stream)
+        e2e_fit.target.view(-1).copy_(pinned_t.view(-1), non_blocking=True)
+        e2e_fit.step()
+        pinned_loss.copy_(e2e_fit.loss, non_blocking=True)
+        e_ev[i].record(stream)
+    barrier()
+    clk = clocks.stop()
+    e2e_ms = sum(s_ev[i].elapsed_time(e_ev[i]) for i in range(K))
+    e2e_value = world * K / (max_over_ranks(e2e_ms) / 1000.0)
+
+    # ---------------- quality + the one collective (NCCL all-gather of PSNR) ----
+    img = pipe.render(fit.params)
+    psnr = pipe.psnr(img, target).clone()
+    if world > 1:
+        allp = [torch.zeros_like(psnr) for _ in range(world)]
+        dist.all_gather(allp, psnr)
+        psnrs = [float(x.item()) for x in allp]
+    else:
+        psnrs = [float(psnr.item())]
+
+    if rank == 0:
+        pk, pk_kind = peaks()
+        sm_mhz = float(pk.get("sm_max_mhz", 1965.0))
+        fp32_peak = 2 * FP32_LANES_PER_SM * N_SM * sm_mhz * 1e6 / 1e12     # TFLOP/s (FMA = 2)
+        kern_ms = stage_ms[2]
+        achieved = pairs * FLOP_PER_PAIR_FUSED / (kern_ms * 1e-3) / 1e12
+        traffic = None
+        prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+        if os.path.exists(prof):
+            try:
+                with open(prof) as f:
+                    traffic = json.load(f).get("backward_tile_kernel_dram_bytes")
+            except Exception:
+                traffic = None
+        ms_step = fit_ms_max / K
+        line = {
+            "metric": METRIC, "value": fit_value, "unit": "it/s", "n_gpus": world, "steps": K,
+            "warmup": Wm, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": fit_value / world / PAPER_FIT_ITS if world == 1 else None,
+            "dtype": "f32", "data": "synthetic",
+            "config": {"workload": "C2 (configs[1]): Kodak-shaped 768x512 synthetic image, 70k "
+                                   "Gaussians at the paper's init, one Adam fit step "
+                                   "(project+bin+fwd+L2+bwd+finalize+adam)",
+                       "images_per_gpu": 1, "l2": "flushed (256 MB write) before every timed step",
+                       "key_pairs_per_step": keys, "pixel_gaussian_pairs": pairs,
+                       "vs_baseline_ref": "paper fit 469.1 it/s (Table 1a P:331, V100, Adan, "
+                                          "real Kodak): context, other hardware"},
+            "render_fps": render_fps,
+            "decode_fps": decode_fps,
+            "stage_ms": {"project": stage_ms[0], "bin": stage_ms[1], "fused_fwd_bwd": stage_ms[2],
+                         "finalize_loss": stage_ms[3], "adam": stage_ms[4]},
+            "render_kernel_ms": r_kernel_ms,
+            "psnr_db_after_fit_steps": psnrs,
+            "roofline": {"kernel": "backward_tile_kernel (fused Eq.7 fwd + L2 + App.A bwd)",
+                         "bound": "alu", "achieved": achieved, "peak": fp32_peak,
+                         "unit": "TFLOP/s", "frac": achieved / fp32_peak, "traffic": traffic,
+                         "peak_kind": f"FP32 FMA pipe: 128 lanes x 2 FLOP x 148 SM x "
+                                      f"{sm_mhz:.0f} MHz ({pk_kind} sm_max_mhz)",
+                         "algorithmic": f"{FLOP_PER_PAIR_FUSED} FLOP per in-box pair x {pairs} "
+                                        f"pairs per launch",
+                         "render_kernel_frac": render_pairs * FLOP_PER_PAIR_RENDER
+                         / (r_kernel_ms * 1e-3) / 1e12 / fp32_peak},
+            "clocks": clk,
+            "e2e": {"value": e2e_value, "unit": "it/s",
+                    "h2d_bytes_per_step": int(t_host.nbytes), "d2h_bytes_per_step": 4,
+                    "path": "Fitter.step -> gi_fit_step (C ABI), per step H2D target from "
+                            "pinned host, D2H loss to pinned host, no graph"},
+            "gpu_launches": int(launches_per_step * K),
+            "gpu_launches_per_step": int(launches_per_step),
+        }
+        if world == 1 and not args.no_cpu_baseline:
+            line["cpu_baseline"] = cpu_baseline(args.cpu_seconds)
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def pairs_of(pipe, np_):
+    rec = pipe.proj.view(-1, 12).cpu().numpy()
+    bx, by = rec[:, 7].view(np_.uint32), rec[:, 11].view(np_.uint32)
+    wx = (bx >> 16).astype(np_.int64) - (bx & 0xffff).astype(np_.int64) + 1
+    wy = (by >> 16).astype(np_.int64) - (by & 0xffff).astype(np_.int64) + 1
+    touched = pipe.tiles_touched.cpu().numpy() > 0
+    return int(np_.sum(np_.where(touched, wx * wy, 0)))
+
+
+if __name__ == "__main__":
+    main()

@@ -148,18 +148,25 @@ double gi_lr_at(int32_t step, double lr0, int32_t half_every);
 
 /* --- fused fit iteration (graph-capturable) ---------------------------------
  * One step of the fitting loop on B images: project -> bin -> fused
- * forward/L2/backward -> Adam, with the 1-based step counter t kept on the
- * device (*step_counter is incremented once per call, then used for the
- * bias correction and lr_t = lr0 * 0.5^floor((t-1)/half_every)).  All buffers
- * are the ones of the individual calls above; ws_* sizes as queried.
- *   fit_ws  gi_fit_workspace_bytes() bytes: holds proj, tiles_touched,
- *           gauss_offset, keys, ranges, n_keys and both stage workspaces. */
+ * forward/L2/backward -> per-Gaussian finalize -> Adam, with the 1-based step
+ * counter t kept on the device (*step_counter is incremented once per call by
+ * the projection kernel, then used for the bias correction and
+ * lr_t = lr0 * 0.5^floor((t-1)/half_every)).
+ *   fit_ws        gi_fit_workspace_bytes() bytes: holds proj, tiles_touched,
+ *                 gauss_offset, keys, ranges, n_keys and both stage workspaces
+ *   loss          [B] fp32 out (L2 loss of the step's forward), may be NULL
+ *   status_flags  device u32, bit 0 set on a non-finite parameter, may be NULL
+ *   stage_events  NULL, or 6 cudaEvent_t (as void*) recorded (external) at
+ *                 the stage boundaries: [0] start, [1] after project,
+ *                 [2] after bin, [3] after the fused tile kernel,
+ *                 [4] after finalize + loss, [5] after Adam.  Lets a caller
+ *                 time each stage inside a captured CUDA graph. */
 size_t gi_fit_workspace_bytes(int32_t n, int64_t key_capacity, const gi_frame* f);
 gi_status gi_fit_step(float* params, float* grads, float* m, float* v, const float* target,
                       int32_t n, const gi_frame* f, uint32_t flags, int64_t key_capacity,
                       void* fit_ws, size_t ws_bytes, uint32_t* step_counter, float lr0,
                       int32_t half_every, float beta1, float beta2, float eps, float* loss,
-                      uint32_t* status_flags, void* stream);
+                      uint32_t* status_flags, void* const* stage_events, void* stream);
 /* Device status words inside fit_ws (for gi_check): */
 const uint32_t* gi_fit_n_keys(const void* fit_ws, int32_t n, int64_t key_capacity,
                               const gi_frame* f);
@@ -187,6 +194,10 @@ gi_status gi_vq_decode(const uint8_t* payload, size_t payload_bytes, const gi_co
 size_t gi_psnr_workspace_bytes(const gi_frame* f);
 gi_status gi_psnr(const float* image, const float* target, const gi_frame* f, float* psnr,
                   void* ws, void* stream);
+
+/* Number of kernels this thread has launched (or captured into a graph)
+ * through libgi since load.  Diagnostic; the bench reports it. */
+int64_t gi_launch_count(void);
 
 /* Synchronise `stream` and translate the device status words:
  * n_keys (device u32, may be NULL) > key_capacity -> GI_ECAPACITY;

@@ -83,12 +83,14 @@ cudaError_t launch_adam(float* params, const float* grads, float* m, float* v, i
             reinterpret_cast<float4*>(params), reinterpret_cast<const float4*>(grads),
             reinterpret_cast<float4*>(m), reinterpret_cast<float4*>(v), c4, step, step_dev, lr,
             half_every, b1, b2, eps, flag);
+        note_launches(1);
         cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) return e;
     }
     if (count % 4) {
         adam_tail_kernel<<<1, 32, 0, s>>>(params, grads, m, v, c4 * 4, count, step, step_dev, lr,
                                           half_every, b1, b2, eps, flag);
+        note_launches(1);
     }
     return cudaGetLastError();
 }

@@ -7,6 +7,14 @@
 
 #include "gi_internal.cuh"
 
+namespace gi {
+namespace {
+thread_local int64_t g_launches = 0;
+}
+void note_launches(int k) { g_launches += k; }
+int64_t g_launches_get() { return g_launches; }
+}  // namespace gi
+
 namespace {
 
 thread_local char g_err[512] = "";
@@ -209,16 +217,23 @@ const uint32_t* gi_fit_n_keys(const void* fit_ws, int32_t n, int64_t key_capacit
     return carve_fit(const_cast<void*>(fit_ws), n, key_capacity, *f).n_keys;
 }
 
+static cudaError_t record_stage(void* const* ev, int i, cudaStream_t s) {
+    if (ev == nullptr || ev[i] == nullptr) return cudaSuccess;
+    // external: becomes an event-record node when the stream is being captured
+    return cudaEventRecordWithFlags(static_cast<cudaEvent_t>(ev[i]), s, cudaEventRecordExternal);
+}
+
 gi_status gi_fit_step(float* params, float* grads, float* m, float* v, const float* target,
                       int32_t n, const gi_frame* f, uint32_t flags, int64_t key_capacity,
                       void* fit_ws, size_t ws_bytes, uint32_t* step_counter, float lr0,
                       int32_t half_every, float beta1, float beta2, float eps, float* loss,
-                      uint32_t* status_flags, void* stream) {
+                      uint32_t* status_flags, void* const* stage_events, void* stream) {
     gi_status st;
     if ((st = check_frame(f)) != GI_OK || (st = check_n(n, f)) != GI_OK) return st;
     if (flags != GI_POS_LOGIT && flags != GI_POS_NORMALIZED) return invalid("flags");
     if (key_capacity < 0 || key_capacity >= (1LL << 31)) return invalid("key_capacity");
     if (half_every < 1) return invalid("half_every");
+    if (!(beta1 >= 0.f && beta1 < 1.f && beta2 >= 0.f && beta2 < 1.f)) return invalid("betas");
     if (!fit_ws || ws_bytes < carve_fit(nullptr, n, key_capacity, *f).bytes)
         return invalid("fit workspace too small");
     if (!step_counter || !target || (n > 0 && (!params || !grads || !m || !v)))
@@ -228,21 +243,34 @@ gi_status gi_fit_step(float* params, float* grads, float* m, float* v, const flo
     FitWs w = carve_fit(fit_ws, n, key_capacity, *f);
     cudaStream_t s = S(stream);
     cudaError_t e;
-    if ((e = gi::launch_project(params, n, *f, flags, w.proj, w.touched, step_counter, s)) != cudaSuccess)
-        return cuda_status(e, "gi_fit_step/project");
-    if ((e = gi::launch_bin(w.proj, w.touched, n, *f, key_capacity, w.bin_ws, w.gauss_offset,
-                            w.key_tile, w.key_gid, w.tile_range, w.n_keys, s)) != cudaSuccess)
-        return cuda_status(e, "gi_fit_step/bin");
-    if ((e = gi::launch_backward(params, w.proj, w.key_gid, w.tile_range, w.gauss_offset, n, *f,
-                                 flags, nullptr, target, key_capacity, w.bwd_ws, grads, loss,
-                                 nullptr, s)) != cudaSuccess)
-        return cuda_status(e, "gi_fit_step/backward");
-    if (n > 0 &&
-        (e = gi::launch_adam(params, grads, m, v, (int64_t)n * 8 * f->batch, 0, step_counter, lr0,
-                             half_every, beta1, beta2, eps, status_flags, s)) != cudaSuccess)
-        return cuda_status(e, "gi_fit_step/adam");
+#define GI_TRY(expr, where) \
+    if ((e = (expr)) != cudaSuccess) return cuda_status(e, where)
+    GI_TRY(record_stage(stage_events, 0, s), "gi_fit_step/event");
+    GI_TRY(gi::launch_project(params, n, *f, flags, w.proj, w.touched, step_counter, s),
+           "gi_fit_step/project");
+    GI_TRY(record_stage(stage_events, 1, s), "gi_fit_step/event");
+    GI_TRY(gi::launch_bin(w.proj, w.touched, n, *f, key_capacity, w.bin_ws, w.gauss_offset,
+                          w.key_tile, w.key_gid, w.tile_range, w.n_keys, s),
+           "gi_fit_step/bin");
+    GI_TRY(record_stage(stage_events, 2, s), "gi_fit_step/event");
+    GI_TRY(gi::launch_backward_tiles(w.proj, w.key_gid, w.tile_range, w.gauss_offset, n, *f,
+                                     nullptr, target, key_capacity, w.bwd_ws, nullptr, s),
+           "gi_fit_step/backward");
+    GI_TRY(record_stage(stage_events, 3, s), "gi_fit_step/event");
+    GI_TRY(gi::launch_backward_finalize(params, w.gauss_offset, n, *f, flags, true, key_capacity,
+                                        w.bwd_ws, grads, loss, s),
+           "gi_fit_step/finalize");
+    GI_TRY(record_stage(stage_events, 4, s), "gi_fit_step/event");
+    if (n > 0)
+        GI_TRY(gi::launch_adam(params, grads, m, v, (int64_t)n * 8 * f->batch, 0, step_counter, lr0,
+                               half_every, beta1, beta2, eps, status_flags, s),
+               "gi_fit_step/adam");
+    GI_TRY(record_stage(stage_events, 5, s), "gi_fit_step/event");
+#undef GI_TRY
     return GI_OK;
 }
+
+int64_t gi_launch_count(void) { return gi::g_launches_get(); }
 
 gi_status gi_vq_decode(const uint8_t* payload, size_t payload_bytes, const gi_codec_meta* meta,
                        float* params, void* stream) {

@@ -279,11 +279,11 @@ BwdWs carve(void* base, int n, int64_t cap, const gi_frame& f) {
 
 size_t backward_ws_bytes(int n, int64_t cap, const gi_frame& f) { return carve(nullptr, n, cap, f).bytes; }
 
-cudaError_t launch_backward(const float* params, const Proj* proj, const uint32_t* key_gid,
-                            const uint32_t* tile_range, const uint32_t* gauss_offset, int n,
-                            const gi_frame& f, uint32_t flags, const float* dL_dimage,
-                            const float* target, int64_t cap, void* ws, float* grads, float* loss,
-                            float* image_out, cudaStream_t s) {
+cudaError_t launch_backward_tiles(const Proj* proj, const uint32_t* key_gid,
+                                  const uint32_t* tile_range, const uint32_t* gauss_offset, int n,
+                                  const gi_frame& f, const float* dL_dimage, const float* target,
+                                  int64_t cap, void* ws, float* image_out, cudaStream_t s) {
+    (void)n;
     BwdWs w = carve(ws, n, cap, f);
     const int TX = tiles_x(f.width), T = TX * tiles_y(f.height);
     const double count = 3.0 * (double)f.width * (double)f.height;
@@ -294,20 +294,43 @@ cudaError_t launch_backward(const float* params, const Proj* proj, const uint32_
                                               f.height, T, TX, dL_dimage, target, norm, cap,
                                               w.partial, mse ? w.sse : nullptr,
                                               mse ? image_out : nullptr);
-    cudaError_t e = cudaGetLastError();
-    if (e != cudaSuccess) return e;
+    note_launches(1);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_backward_finalize(const float* params, const uint32_t* gauss_offset, int n,
+                                     const gi_frame& f, uint32_t flags, bool mse, int64_t cap,
+                                     void* ws, float* grads, float* loss, cudaStream_t s) {
+    BwdWs w = carve(ws, n, cap, f);
+    const int T = tiles_x(f.width) * tiles_y(f.height);
+    const double count = 3.0 * (double)f.width * (double)f.height;
     const int total = n * f.batch;
+    cudaError_t e = cudaSuccess;
     if (total > 0) {
         finalize_kernel<<<(total + 255) / 256, 256, 0, s>>>(
             reinterpret_cast<const float4*>(params), gauss_offset, total, f.width, f.height, flags,
             cap, w.partial, reinterpret_cast<float4*>(grads));
+        note_launches(1);
         if ((e = cudaGetLastError()) != cudaSuccess) return e;
     }
     if (mse && loss != nullptr) {
         loss_kernel<<<f.batch, 256, 0, s>>>(w.sse, T, 1.0 / count, loss);
+        note_launches(1);
         e = cudaGetLastError();
     }
     return e;
+}
+
+cudaError_t launch_backward(const float* params, const Proj* proj, const uint32_t* key_gid,
+                            const uint32_t* tile_range, const uint32_t* gauss_offset, int n,
+                            const gi_frame& f, uint32_t flags, const float* dL_dimage,
+                            const float* target, int64_t cap, void* ws, float* grads, float* loss,
+                            float* image_out, cudaStream_t s) {
+    cudaError_t e = launch_backward_tiles(proj, key_gid, tile_range, gauss_offset, n, f, dL_dimage,
+                                          target, cap, ws, image_out, s);
+    if (e != cudaSuccess) return e;
+    return launch_backward_finalize(params, gauss_offset, n, f, flags, dL_dimage == nullptr, cap,
+                                    ws, grads, loss, s);
 }
 
 }  // namespace gi

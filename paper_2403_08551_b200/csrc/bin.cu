@@ -235,6 +235,7 @@ cudaError_t launch_bin(const Proj* proj, const uint32_t* tiles_touched, int n, c
         duplicate_kernel<<<(total + 255) / 256, 256, 0, s>>>(proj, tiles_touched, gauss_offset, total,
                                                              n, T, tiles_x(f.width), cap, bufk[cur],
                                                              bufv[cur]);
+        note_launches(1);
         if ((e = cudaGetLastError()) != cudaSuccess) return e;
     }
     const int64_t nc_max = max_chunks(cap);
@@ -244,6 +245,7 @@ cudaError_t launch_bin(const Proj* proj, const uint32_t* tiles_touched, int n, c
         if (nc_max > 0) {
             radix_hist_kernel<<<(unsigned)nc_max, kRadixThreads, 0, s>>>(bufk[cur], n_keys, cap, shift,
                                                                          bits, w.hist);
+            note_launches(1);
             if ((e = cudaGetLastError()) != cudaSuccess) return e;
         }
         e = scan_exclusive_spec(w.hist, w.hist, nc_max * (int64_t)(1 << bits), n_keys, kChunk,
@@ -252,6 +254,7 @@ cudaError_t launch_bin(const Proj* proj, const uint32_t* tiles_touched, int n, c
         if (nc_max > 0) {
             radix_scatter_kernel<<<(unsigned)nc_max, kRadixThreads, 0, s>>>(
                 bufk[cur], bufv[cur], bufk[cur ^ 1], bufv[cur ^ 1], n_keys, cap, shift, bits, w.hist);
+            note_launches(1);
             if ((e = cudaGetLastError()) != cudaSuccess) return e;
         }
         cur ^= 1;
@@ -259,6 +262,7 @@ cudaError_t launch_bin(const Proj* proj, const uint32_t* tiles_touched, int n, c
     // 3. ranges over the sorted keys
     ranges_kernel<<<(unsigned)((cap + 1 + 255) / 256), 256, 0, s>>>(key_tile, n_keys, cap, TT,
                                                                    tile_range);
+    note_launches(1);
     return cudaGetLastError();
 }
 

@@ -75,6 +75,7 @@ cudaError_t launch_vq_decode(const uint8_t* payload, const gi_codec_meta& meta, 
         payload, meta.n, meta.bits, meta.stages, meta.codebook, ib, rec, meta.gamma[0],
         meta.gamma[1], meta.gamma[2], meta.beta[0], meta.beta[1], meta.beta[2], meta.codebooks,
         reinterpret_cast<float4*>(params));
+    note_launches(1);
     return cudaGetLastError();
 }
 

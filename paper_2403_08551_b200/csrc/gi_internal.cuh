@@ -67,6 +67,11 @@ cudaError_t scan_exclusive_spec(const uint32_t* in, uint32_t* out, int64_t max_c
                                 const uint32_t* count_dev, uint32_t div, uint32_t mul, int64_t cap,
                                 uint32_t* ws, uint32_t* total_out, cudaStream_t s);
 
+// Per-thread count of kernels launched (or captured) through libgi; the
+// bench reports it as gpu_launches.  Diagnostic only, never read by kernels.
+void note_launches(int k);
+int64_t g_launches_get();
+
 // Internal launchers (api.cu validates arguments).
 cudaError_t launch_project(const float* params, int n, const gi_frame& f, uint32_t flags,
                            Proj* proj, uint32_t* tiles_touched, uint32_t* step_counter,
@@ -83,6 +88,13 @@ cudaError_t launch_backward(const float* params, const Proj* proj, const uint32_
                             const gi_frame& f, uint32_t flags, const float* dL_dimage,
                             const float* target, int64_t cap, void* ws, float* grads, float* loss,
                             float* image_out, cudaStream_t s);
+cudaError_t launch_backward_tiles(const Proj* proj, const uint32_t* key_gid,
+                                  const uint32_t* tile_range, const uint32_t* gauss_offset, int n,
+                                  const gi_frame& f, const float* dL_dimage, const float* target,
+                                  int64_t cap, void* ws, float* image_out, cudaStream_t s);
+cudaError_t launch_backward_finalize(const float* params, const uint32_t* gauss_offset, int n,
+                                     const gi_frame& f, uint32_t flags, bool mse, int64_t cap,
+                                     void* ws, float* grads, float* loss, cudaStream_t s);
 cudaError_t launch_adam(float* params, const float* grads, float* m, float* v, int64_t count,
                         int step, const uint32_t* step_dev, float lr, int half_every, float b1,
                         float b2, float eps, uint32_t* flag, cudaStream_t s);

@@ -98,6 +98,7 @@ cudaError_t launch_project(const float* params, int n, const gi_frame& f, uint32
     project_kernel<<<blocks > 0 ? blocks : 1, 256, 0, s>>>(
         reinterpret_cast<const float4*>(params), n, total, f.width, f.height, f.k, flags, proj,
         tiles_touched, step_counter);
+    note_launches(1);
     return cudaGetLastError();
 }
 

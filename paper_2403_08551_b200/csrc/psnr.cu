@@ -60,9 +60,11 @@ cudaError_t launch_psnr(const float* image, const float* target, const gi_frame&
     double* part = static_cast<double*>(ws);
     dim3 grid(kPsnrBlocks, f.batch);
     psnr_partial_kernel<<<grid, 256, 0, s>>>(image, target, count, part);
+    note_launches(1);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     psnr_final_kernel<<<f.batch, 256, 0, s>>>(part, kPsnrBlocks, count, psnr);
+    note_launches(1);
     return cudaGetLastError();
 }
 

@@ -60,6 +60,7 @@ cudaError_t launch_render(const Proj* proj, const uint32_t* key_gid, const uint3
     const int TX = tiles_x(f.width), T = TX * tiles_y(f.height);
     dim3 grid(T, f.batch);
     render_kernel<<<grid, 256, 0, s>>>(proj, key_gid, tile_range, f.width, f.height, T, TX, image);
+    note_launches(1);
     return cudaGetLastError();
 }
 

@@ -131,10 +131,13 @@ cudaError_t scan_exclusive_spec(const uint32_t* in, uint32_t* out, int64_t max_c
     const int64_t tiles = (max_count + kScanTileElems - 1) / kScanTileElems;
     if (tiles > 0) {
         scan_reduce_kernel<<<(unsigned)tiles, kScanThreads, 0, s>>>(in, cs, ws);
+        note_launches(1);
     }
     scan_top_kernel<<<1, 1024, 0, s>>>(ws, cs, total_out);
+    note_launches(1);
     if (tiles > 0) {
         scan_down_kernel<<<(unsigned)tiles, kScanThreads, 0, s>>>(in, out, cs, ws);
+        note_launches(1);
     }
     return cudaGetLastError();
 }

@@ -68,7 +68,8 @@ SIGNATURES = {
     "gi_fit_workspace_bytes": (_sz, [_i32, _i64, _FP]),
     "gi_fit_n_keys": (_vp, [_vp, _i32, _i64, _FP]),
     "gi_fit_step": (C.c_int, [_vp, _vp, _vp, _vp, _vp, _i32, _FP, _u32, _i64, _vp, _sz, _vp,
-                              _f32, _i32, _f32, _f32, _f32, _vp, _vp, _vp]),
+                              _f32, _i32, _f32, _f32, _f32, _vp, _vp, _vp, _vp]),
+    "gi_launch_count": (_i64, []),
     "gi_vq_decode": (C.c_int, [_vp, _sz, C.POINTER(gi_codec_meta), _vp, _vp]),
     "gi_psnr_workspace_bytes": (_sz, [_FP]),
     "gi_psnr": (C.c_int, [_vp, _vp, _FP, _vp, _vp, _vp]),
@@ -199,12 +200,22 @@ def gi_adam_step(params, grads, m, v, count, step, lr, beta1=0.9, beta2=0.999, e
 
 def gi_fit_step(params, grads, m, v, target, n, f, flags, key_capacity, fit_ws, step_counter,
                 lr0=1e-3, half_every=20000, beta1=0.9, beta2=0.999, eps=1e-8, loss=None,
-                status_flags=None, stream=None):
+                status_flags=None, stage_events=None, stream=None):
+    """stage_events: None or 6 recorded torch.cuda.Event(external=True) / raw handles."""
+    ev = None
+    if stage_events is not None:
+        handles = [e if isinstance(e, int) else e.cuda_event for e in stage_events]
+        assert len(handles) == 6 and all(handles), "6 initialised events"
+        ev = (C.c_void_p * 6)(*handles)
     _ok(load().gi_fit_step(_ptr(params), _ptr(grads), _ptr(m), _ptr(v), _ptr(target), int(n),
                            C.byref(f), int(flags), int(key_capacity), _ptr(fit_ws),
                            fit_ws.numel() * fit_ws.element_size(), _ptr(step_counter),
                            float(lr0), int(half_every), float(beta1), float(beta2), float(eps),
-                           _ptr(loss), _ptr(status_flags), _stream(stream)), "gi_fit_step")
+                           _ptr(loss), _ptr(status_flags), ev, _stream(stream)), "gi_fit_step")
+
+
+def gi_launch_count() -> int:
+    return load().gi_launch_count()
 
 
 def gi_vq_decode(payload, meta: gi_codec_meta, params, stream=None):

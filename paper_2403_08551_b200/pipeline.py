@@ -123,19 +123,21 @@ class Fitter:
         self.flags = flags
         self.graph = None
 
-    def step(self, stream=None):
+    def step(self, stream=None, stage_events=None):
         gi.gi_fit_step(self.params, self.grads, self.m, self.v, self.target, self.n, self.f,
                        self.flags, self.cap, self.fit_ws, self.step_counter, loss=self.loss,
-                       status_flags=self.status, stream=stream, **self.hyper)
+                       status_flags=self.status, stage_events=stage_events, stream=stream,
+                       **self.hyper)
 
-    def capture(self, steps_per_graph: int = 1):
-        """Capture `steps_per_graph` fused steps into one CUDA graph."""
+    def capture(self, steps_per_graph: int = 1, stage_events=None):
+        """Capture `steps_per_graph` fused steps into one CUDA graph (stage
+        events, if given, are recorded around the last captured step)."""
         s = torch.cuda.Stream(device=self.device)
         s.wait_stream(torch.cuda.current_stream(self.device))
         g = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g, stream=s):
-            for _ in range(steps_per_graph):
-                self.step()
+            for i in range(steps_per_graph):
+                self.step(stage_events=stage_events if i == steps_per_graph - 1 else None)
         torch.cuda.current_stream(self.device).wait_stream(s)
         self.graph = g
         self.steps_per_graph = steps_per_graph
