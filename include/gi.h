@@ -88,22 +88,23 @@ gi_status gi_project(const float* params, int32_t n, const gi_frame* f, uint32_t
                      void* proj, uint32_t* tiles_touched, void* stream);
 
 /* --- a2. Tile binning, no depth key (north_star) --------------------
- * Exclusive scan of tiles_touched -> gauss_offset; duplicate one key
- * (tile, gid) per tile of each Gaussian's rectangle (row-major); stable LSD
- * radix sort on the tile id ONLY (hand-written, CUB-free).  Emission is in
- * ascending gid, so the result is the unique lexicographic (tile, gid) order
- * (R9).  tile_range[t] = first key index with key_tile >= t (B*T + 1 entries).
- *   gauss_offset  [B*n + 1] u32 out (gauss_offset[B*n] = K)
+ * One key (tile, gid) per tile of each Gaussian's rectangle, grouped by tile
+ * id only (no depth key) and ascending gid inside a tile, i.e. the unique
+ * lexicographic (tile, gid) order (R9).  Done as one counting pass on the
+ * tile digit (per-tile counts -> scan -> slot scatter) followed by a per-tile
+ * sort on gid; hand-written, CUB-free.
  *   key_tile, key_gid  [key_capacity] u32 out (first K valid)
- *   n_keys        [1] u32 device out: K, the TRUE key count.  If
- *                 K > key_capacity the keys are truncated and the caller must
- *                 retry with a larger capacity (gi_check reports GI_ECAPACITY).
- *   ws            workspace of gi_bin_workspace_bytes() bytes (device). */
+ *   tile_range [B*T + 1] u32 out: tile_range[t] = first key index with
+ *              key_tile >= t (entries clamped to key_capacity)
+ *   n_keys     [1] u32 device out: K, the TRUE key count.  If
+ *              K > key_capacity the keys are truncated (consistently with
+ *              the clamped ranges) and the caller must retry with a larger
+ *              capacity (gi_check reports GI_ECAPACITY).
+ *   ws         workspace of gi_bin_workspace_bytes() bytes (device). */
 size_t gi_bin_workspace_bytes(int32_t n, int64_t key_capacity, const gi_frame* f);
 gi_status gi_bin(const void* proj, const uint32_t* tiles_touched, int32_t n, const gi_frame* f,
-                 int64_t key_capacity, void* ws, size_t ws_bytes, uint32_t* gauss_offset,
-                 uint32_t* key_tile, uint32_t* key_gid, uint32_t* tile_range, uint32_t* n_keys,
-                 void* stream);
+                 int64_t key_capacity, void* ws, size_t ws_bytes, uint32_t* key_tile,
+                 uint32_t* key_gid, uint32_t* tile_range, uint32_t* n_keys, void* stream);
 
 /* --- a3. Forward accumulated summation (Eq. 7) -----------------------------
  * C_k(x, y) = sum over keys of tile(x, y), ascending gid, of
@@ -120,14 +121,15 @@ gi_status gi_render(const void* proj, const uint32_t* key_gid, const uint32_t* t
  * dl1 = 2 g1 l1 + 2 g2 l2, dl2 = 2 g2 l1 + 2 g3 l2 (R14 corrects P:627),
  * dl3 = 2 g3 l3 in G = dL/dSigma; dmu_raw chained through tanh when flags ==
  * GI_POS_LOGIT).  Deterministic: per-(tile, Gaussian) partial sums are
- * written to the workspace and reduced per Gaussian in a fixed order.
+ * written to the workspace at the key's index and reduced per Gaussian in
+ * row-major tile order (no atomics).
  *   loss       [B] fp32 out, or NULL (MSE mode only)
  *   image_out  [B][3][H][W] fp32 out, or NULL (MSE mode only)
  *   ws         gi_backward_workspace_bytes() bytes (device). */
 size_t gi_backward_workspace_bytes(int32_t n, int64_t key_capacity, const gi_frame* f);
 gi_status gi_render_backward(const float* params, const void* proj, const uint32_t* key_gid,
-                             const uint32_t* tile_range, const uint32_t* gauss_offset,
-                             int32_t n, const gi_frame* f, uint32_t flags,
+                             const uint32_t* tile_range, int32_t n, const gi_frame* f,
+                             uint32_t flags,
                              const float* dL_dimage, const float* target,
                              int64_t key_capacity, void* ws, size_t ws_bytes,
                              float* grads, float* loss, float* image_out, void* stream);
@@ -147,19 +149,20 @@ gi_status gi_adam_step(float* params, const float* grads, float* m, float* v, in
 double gi_lr_at(int32_t step, double lr0, int32_t half_every);
 
 /* --- fused fit iteration (graph-capturable) ---------------------------------
- * One step of the fitting loop on B images: project -> bin -> fused
- * forward/L2/backward -> per-Gaussian finalize -> Adam, with the 1-based step
+ * One step of the fitting loop on B images: project (+ per-tile counts) ->
+ * bin -> fused forward/L2/backward -> per-Gaussian finalize fused with Adam
+ * (grads are still written out), with the 1-based step
  * counter t kept on the device (*step_counter is incremented once per call by
  * the projection kernel, then used for the bias correction and
  * lr_t = lr0 * 0.5^floor((t-1)/half_every)).
  *   fit_ws        gi_fit_workspace_bytes() bytes: holds proj, tiles_touched,
- *                 gauss_offset, keys, ranges, n_keys and both stage workspaces
+ *                 keys, ranges, n_keys and both stage workspaces
  *   loss          [B] fp32 out (L2 loss of the step's forward), may be NULL
  *   status_flags  device u32, bit 0 set on a non-finite parameter, may be NULL
  *   stage_events  NULL, or 6 cudaEvent_t (as void*) recorded (external) at
  *                 the stage boundaries: [0] start, [1] after project,
  *                 [2] after bin, [3] after the fused tile kernel,
- *                 [4] after finalize + loss, [5] after Adam.  Lets a caller
+ *                 [4] after finalize + Adam + loss, [5] end.  Lets a caller
  *                 time each stage inside a captured CUDA graph. */
 size_t gi_fit_workspace_bytes(int32_t n, int64_t key_capacity, const gi_frame* f);
 gi_status gi_fit_step(float* params, float* grads, float* m, float* v, const float* target,
@@ -167,6 +170,15 @@ gi_status gi_fit_step(float* params, float* grads, float* m, float* v, const flo
                       void* fit_ws, size_t ws_bytes, uint32_t* step_counter, float lr0,
                       int32_t half_every, float beta1, float beta2, float eps, float* loss,
                       uint32_t* status_flags, void* const* stage_events, void* stream);
+/* --- fused render of a frame (graph-capturable) ---------------------------
+ * project (+ per-tile counts) -> bin -> Eq. 7 render in one call; the per-tile
+ * gid ordering of binning happens inside the render kernel.  Same workspace
+ * layout and size as gi_fit_step (gi_fit_workspace_bytes); n_keys for
+ * gi_check via gi_fit_n_keys(frame_ws, ...).  image [B][3][H][W] out. */
+gi_status gi_render_frame(const float* params, int32_t n, const gi_frame* f, uint32_t flags,
+                          int64_t key_capacity, void* frame_ws, size_t ws_bytes, float* image,
+                          void* stream);
+
 /* Device status words inside fit_ws (for gi_check): */
 const uint32_t* gi_fit_n_keys(const void* fit_ws, int32_t n, int64_t key_capacity,
                               const gi_frame* f);

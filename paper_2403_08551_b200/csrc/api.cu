@@ -56,7 +56,6 @@ cudaStream_t S(void* s) { return static_cast<cudaStream_t>(s); }
 struct FitWs {
     gi::Proj* proj;
     uint32_t* touched;
-    uint32_t* gauss_offset;
     uint32_t* key_tile;
     uint32_t* key_gid;
     uint32_t* tile_range;
@@ -75,7 +74,6 @@ FitWs carve_fit(void* base, int32_t n, int64_t cap, const gi_frame& f) {
     size_t off = 0;
     w.proj = reinterpret_cast<gi::Proj*>(p + off); off += align_up(sizeof(gi::Proj) * total);
     w.touched = reinterpret_cast<uint32_t*>(p + off); off += align_up(4 * total);
-    w.gauss_offset = reinterpret_cast<uint32_t*>(p + off); off += align_up(4 * (total + 1));
     w.key_tile = reinterpret_cast<uint32_t*>(p + off); off += align_up(4 * (size_t)cap);
     w.key_gid = reinterpret_cast<uint32_t*>(p + off); off += align_up(4 * (size_t)cap);
     w.tile_range = reinterpret_cast<uint32_t*>(p + off); off += align_up(4 * (T + 1));
@@ -125,7 +123,7 @@ gi_status gi_project(const float* params, int32_t n, const gi_frame* f, uint32_t
     if (!aligned16(params) || !aligned16(proj)) return invalid("params/proj must be 16-B aligned");
     if (n == 0) return GI_OK;
     return cuda_status(gi::launch_project(params, n, *f, flags, static_cast<gi::Proj*>(proj),
-                                          tiles_touched, nullptr, S(stream)),
+                                          tiles_touched, gi::ProjectFuse{}, S(stream)),
                        "gi_project");
 }
 
@@ -135,19 +133,18 @@ size_t gi_bin_workspace_bytes(int32_t n, int64_t key_capacity, const gi_frame* f
 }
 
 gi_status gi_bin(const void* proj, const uint32_t* tiles_touched, int32_t n, const gi_frame* f,
-                 int64_t key_capacity, void* ws, size_t ws_bytes, uint32_t* gauss_offset,
-                 uint32_t* key_tile, uint32_t* key_gid, uint32_t* tile_range, uint32_t* n_keys,
-                 void* stream) {
+                 int64_t key_capacity, void* ws, size_t ws_bytes, uint32_t* key_tile,
+                 uint32_t* key_gid, uint32_t* tile_range, uint32_t* n_keys, void* stream) {
     gi_status st;
     if ((st = check_frame(f)) != GI_OK || (st = check_n(n, f)) != GI_OK) return st;
     if (key_capacity < 0 || key_capacity >= (1LL << 31)) return invalid("key_capacity");
     if (ws_bytes < gi::bin_ws_bytes(n, key_capacity, *f)) return invalid("bin workspace too small");
-    if (!gauss_offset || !tile_range || !n_keys || (key_capacity > 0 && (!key_tile || !key_gid)) ||
+    if (!tile_range || !n_keys || (key_capacity > 0 && (!key_tile || !key_gid)) ||
         (n > 0 && (!proj || !tiles_touched)) || !ws)
         return invalid("NULL buffer");
     return cuda_status(gi::launch_bin(static_cast<const gi::Proj*>(proj), tiles_touched, n, *f,
-                                      key_capacity, ws, gauss_offset, key_tile, key_gid,
-                                      tile_range, n_keys, S(stream)),
+                                      key_capacity, ws, key_tile, key_gid, tile_range, n_keys,
+                                      false, true, S(stream)),
                        "gi_bin");
 }
 
@@ -156,8 +153,10 @@ gi_status gi_render(const void* proj, const uint32_t* key_gid, const uint32_t* t
     gi_status st;
     if ((st = check_frame(f)) != GI_OK || (st = check_n(n, f)) != GI_OK) return st;
     if (!tile_range || !image || (n > 0 && (!proj || !key_gid))) return invalid("NULL buffer");
-    return cuda_status(gi::launch_render(static_cast<const gi::Proj*>(proj), key_gid, tile_range, n,
-                                         *f, image, S(stream)),
+    // gi_bin output is already in gid order: presorted, key_gid only read
+    return cuda_status(gi::launch_render(static_cast<const gi::Proj*>(proj),
+                                         const_cast<uint32_t*>(key_gid), tile_range, n, *f, true,
+                                         image, S(stream)),
                        "gi_render");
 }
 
@@ -167,23 +166,22 @@ size_t gi_backward_workspace_bytes(int32_t n, int64_t key_capacity, const gi_fra
 }
 
 gi_status gi_render_backward(const float* params, const void* proj, const uint32_t* key_gid,
-                             const uint32_t* tile_range, const uint32_t* gauss_offset, int32_t n,
-                             const gi_frame* f, uint32_t flags, const float* dL_dimage,
-                             const float* target, int64_t key_capacity, void* ws, size_t ws_bytes,
-                             float* grads, float* loss, float* image_out, void* stream) {
+                             const uint32_t* tile_range, int32_t n, const gi_frame* f,
+                             uint32_t flags, const float* dL_dimage, const float* target,
+                             int64_t key_capacity, void* ws, size_t ws_bytes, float* grads,
+                             float* loss, float* image_out, void* stream) {
     gi_status st;
     if ((st = check_frame(f)) != GI_OK || (st = check_n(n, f)) != GI_OK) return st;
     if (flags != GI_POS_LOGIT && flags != GI_POS_NORMALIZED) return invalid("flags");
     if (key_capacity < 0 || key_capacity >= (1LL << 31)) return invalid("key_capacity");
     if (ws_bytes < gi::backward_ws_bytes(n, key_capacity, *f)) return invalid("backward workspace too small");
     if (!dL_dimage && !target) return invalid("need dL_dimage or target");
-    if (!tile_range || !gauss_offset || !ws || (n > 0 && (!params || !proj || !key_gid || !grads)))
+    if (!tile_range || !ws || (n > 0 && (!params || !proj || !key_gid || !grads)))
         return invalid("NULL buffer");
     if (!aligned16(params) || !aligned16(grads) || !aligned16(ws)) return invalid("alignment");
     return cuda_status(gi::launch_backward(params, static_cast<const gi::Proj*>(proj), key_gid,
-                                           tile_range, gauss_offset, n, *f, flags, dL_dimage,
-                                           target, key_capacity, ws, grads, loss, image_out,
-                                           S(stream)),
+                                           tile_range, n, *f, flags, dL_dimage, target,
+                                           key_capacity, ws, grads, loss, image_out, S(stream)),
                        "gi_render_backward");
 }
 
@@ -246,31 +244,61 @@ gi_status gi_fit_step(float* params, float* grads, float* m, float* v, const flo
 #define GI_TRY(expr, where) \
     if ((e = (expr)) != cudaSuccess) return cuda_status(e, where)
     GI_TRY(record_stage(stage_events, 0, s), "gi_fit_step/event");
-    GI_TRY(gi::launch_project(params, n, *f, flags, w.proj, w.touched, step_counter, s),
-           "gi_fit_step/project");
+    GI_TRY(gi::bin_clear(w.bin_ws, n, key_capacity, *f, s), "gi_fit_step/clear");
+    gi::ProjectFuse pf{step_counter, gi::bin_tile_counts(w.bin_ws, n, key_capacity, *f),
+                       gi::bin_alloc_counter(w.bin_ws, n, key_capacity, *f),
+                       gi::backward_gauss_off(w.bwd_ws, n, key_capacity, *f)};
+    GI_TRY(gi::launch_project(params, n, *f, flags, w.proj, w.touched, pf, s), "gi_fit_step/project");
     GI_TRY(record_stage(stage_events, 1, s), "gi_fit_step/event");
-    GI_TRY(gi::launch_bin(w.proj, w.touched, n, *f, key_capacity, w.bin_ws, w.gauss_offset,
-                          w.key_tile, w.key_gid, w.tile_range, w.n_keys, s),
+    GI_TRY(gi::launch_bin(w.proj, w.touched, n, *f, key_capacity, w.bin_ws, w.key_tile, w.key_gid,
+                          w.tile_range, w.n_keys, true, false, s),
            "gi_fit_step/bin");
     GI_TRY(record_stage(stage_events, 2, s), "gi_fit_step/event");
-    GI_TRY(gi::launch_backward_tiles(w.proj, w.key_gid, w.tile_range, w.gauss_offset, n, *f,
-                                     nullptr, target, key_capacity, w.bwd_ws, nullptr, s),
+    GI_TRY(gi::launch_backward_tiles(w.proj, w.key_gid, w.tile_range, n, *f, false, nullptr, target,
+                                     key_capacity, w.bwd_ws, nullptr, s),
            "gi_fit_step/backward");
     GI_TRY(record_stage(stage_events, 3, s), "gi_fit_step/event");
-    GI_TRY(gi::launch_backward_finalize(params, w.gauss_offset, n, *f, flags, true, key_capacity,
-                                        w.bwd_ws, grads, loss, s),
-           "gi_fit_step/finalize");
+    gi::FusedAdam fa{params, m, v, step_counter, lr0, half_every, beta1, beta2, eps, status_flags};
+    GI_TRY(gi::launch_backward_finalize(params, w.proj, n, *f, flags, true, key_capacity, w.bwd_ws,
+                                        grads, loss, &fa, s),
+           "gi_fit_step/finalize+adam");
     GI_TRY(record_stage(stage_events, 4, s), "gi_fit_step/event");
-    if (n > 0)
-        GI_TRY(gi::launch_adam(params, grads, m, v, (int64_t)n * 8 * f->batch, 0, step_counter, lr0,
-                               half_every, beta1, beta2, eps, status_flags, s),
-               "gi_fit_step/adam");
     GI_TRY(record_stage(stage_events, 5, s), "gi_fit_step/event");
 #undef GI_TRY
     return GI_OK;
 }
 
 int64_t gi_launch_count(void) { return gi::g_launches_get(); }
+
+gi_status gi_render_frame(const float* params, int32_t n, const gi_frame* f, uint32_t flags,
+                          int64_t key_capacity, void* frame_ws, size_t ws_bytes, float* image,
+                          void* stream) {
+    gi_status st;
+    if ((st = check_frame(f)) != GI_OK || (st = check_n(n, f)) != GI_OK) return st;
+    if (flags != GI_POS_LOGIT && flags != GI_POS_NORMALIZED) return invalid("flags");
+    if (key_capacity < 0 || key_capacity >= (1LL << 31)) return invalid("key_capacity");
+    if (!frame_ws || ws_bytes < carve_fit(nullptr, n, key_capacity, *f).bytes)
+        return invalid("frame workspace too small");
+    if (!image || (n > 0 && !params)) return invalid("NULL buffer");
+    if (!aligned16(params) || !aligned16(frame_ws)) return invalid("alignment");
+    FitWs w = carve_fit(frame_ws, n, key_capacity, *f);
+    cudaStream_t s = S(stream);
+    cudaError_t e;
+#define GI_TRY(expr, where) \
+    if ((e = (expr)) != cudaSuccess) return cuda_status(e, where)
+    GI_TRY(gi::bin_clear(w.bin_ws, n, key_capacity, *f, s), "gi_render_frame/clear");
+    gi::ProjectFuse pf{nullptr, gi::bin_tile_counts(w.bin_ws, n, key_capacity, *f), nullptr,
+                       nullptr};
+    GI_TRY(gi::launch_project(params, n, *f, flags, w.proj, w.touched, pf, s),
+           "gi_render_frame/project");
+    GI_TRY(gi::launch_bin(w.proj, w.touched, n, *f, key_capacity, w.bin_ws, w.key_tile, w.key_gid,
+                          w.tile_range, w.n_keys, true, false, s),
+           "gi_render_frame/bin");
+    GI_TRY(gi::launch_render(w.proj, w.key_gid, w.tile_range, n, *f, false, image, s),
+           "gi_render_frame/render");
+#undef GI_TRY
+    return GI_OK;
+}
 
 gi_status gi_vq_decode(const uint8_t* payload, size_t payload_bytes, const gi_codec_meta* meta,
                        float* params, void* stream) {

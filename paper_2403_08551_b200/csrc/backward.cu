@@ -1,74 +1,62 @@
 // a4. L2 loss + analytic backward (Appendix A).
 //
-// Fused per-tile kernel: pass 1 recomputes C (Eq. 7) for the tile's pixels,
-// forms g = dL/dC = 2 (C - T) / (3HW) in registers and a per-tile partial of
-// the squared error; pass 2 walks the same key list and, for every pair
-// (n, pixel) with the pixel in n's box, accumulates
-//     dc'_n      += g w                                   (A.1)
-//     gamma       = dL/dsigma = -w <g, c'_n>              (A.1, R12)
-//     S_u += gamma u, S_v += gamma v, S_uu += gamma u^2, S_uv += gamma u v,
-//     S_vv += gamma v^2      with (u, v) = kappa L^-1 d,  sigma = (u^2+v^2)/(2 kappa^2)
-// i.e. the 5 moments from which dsigma/dmu (sign R13) and
-// dsigma/dSigma = -1/2 Sigma^-1 d d^T Sigma^-1 chained through
-// Sigma = L L^T (A.2, R14) follow in closed form per Gaussian.
-// The 8 values are reduced over the warp by a transpose-reduce (9 SHFL),
-// over the 8 warps of the tile in shared memory in a FIXED order, and
-// written once per (tile, Gaussian) to the key's pre-sort slot
-// gauss_offset[gid] + rank-of-tile-in-rect: no atomics, deterministic.
-// finalize_kernel then sums each Gaussian's contiguous slots in order and
-// applies the per-Gaussian chain rule (and tanh, App. C).
+// backward_tile_kernel -- one CTA per 16x16 tile:
+//   pass 1 (pixel-parallel, one pixel per thread, warp culling): recompute
+//          C (Eq. 7), g = dL/dC = 2 (C - T) / (3HW) (or a given dL/dC) and a
+//          per-tile partial of the squared error; g goes to shared memory.
+//   pass 2 (GAUSSIAN-parallel): each of the tile's Gaussians is owned by q
+//          consecutive lanes (q = 1..8, as many as the tile's 256 threads
+//          allow) that walk its box rows (row r -> lane r mod q) inside the
+//          tile and accumulate, per pair with w = exp(-sigma):
+//              dc'     += g w                               (A.1)
+//              gamma    = dL/dsigma = -w <g, c'>             (A.1, R12)
+//              S_u += gamma u, S_v += gamma v, S_uu += gamma u^2,
+//              S_uv += gamma u v, S_vv += gamma v^2
+//          with (u, v) = kappa L^-1 d, i.e. the 8 numbers from which
+//          dsigma/dmu (sign R13) and dsigma/dSigma chained
+//          through Sigma = L L^T (A.2, R14) follow in closed form.
+//          Every evaluated pair is an in-box pair (no warp-culling waste) and
+//          no per-pair warp reduction is needed; the q row-phases of one
+//          Gaussian are combined by a fixed xor tree, and the 8 sums are
+//          written once to the Gaussian's slot gauss_off[gid] + (rank of the
+//          tile in its rectangle) -- no atomics, deterministic.
+// finalize_kernel -- one thread per Gaussian: sums its contiguous slots in
+//   row-major tile order, applies the chain rule (and tanh, App. C) and
+//   optionally the Adam update (fused fit step).
 #include "raster_common.cuh"
 
 namespace gi {
 namespace {
 
-constexpr int kSub = 32;   // Gaussians per reduction sub-batch
-
 struct BwdShared {
     StagedRecords sr;
-    uint32_t slot[256];                 // pre-sort key slot of each staged record
-    float red[kWarps][kSub][8];         // per-warp reduced partials
+    WarpLists wl;
+    uint32_t sl[kSortMax];
+    float4 g[kTilePix];      // per-pixel upstream dL/dC (x, y, z), tile-local row-major
+    uint32_t slot[256];      // partial slot of each staged record
+    uint32_t scratch[kWarps];
     float sse[kWarps];
 };
 
-// Transpose-reduce 8 per-lane values over the warp: after it, lane l with
-// (l & 3) == 0 holds the warp sum of value index (l >> 2).
-__device__ __forceinline__ float warp_reduce8(float v0, float v1, float v2, float v3, float v4,
-                                              float v5, float v6, float v7, int lane) {
-    const bool h4 = lane & 16;
-    float k0 = h4 ? v4 : v0, k1 = h4 ? v5 : v1, k2 = h4 ? v6 : v2, k3 = h4 ? v7 : v3;
-    const float s0 = h4 ? v0 : v4, s1 = h4 ? v1 : v5, s2 = h4 ? v2 : v6, s3 = h4 ? v3 : v7;
-    k0 += __shfl_xor_sync(kFull, s0, 16);
-    k1 += __shfl_xor_sync(kFull, s1, 16);
-    k2 += __shfl_xor_sync(kFull, s2, 16);
-    k3 += __shfl_xor_sync(kFull, s3, 16);
-    const bool h3 = lane & 8;
-    float j0 = h3 ? k2 : k0, j1 = h3 ? k3 : k1;
-    const float t0 = h3 ? k0 : k2, t1 = h3 ? k1 : k3;
-    j0 += __shfl_xor_sync(kFull, t0, 8);
-    j1 += __shfl_xor_sync(kFull, t1, 8);
-    const bool h2 = lane & 4;
-    float i0 = h2 ? j1 : j0;
-    const float r0 = h2 ? j0 : j1;
-    i0 += __shfl_xor_sync(kFull, r0, 4);
-    i0 += __shfl_xor_sync(kFull, i0, 2);
-    i0 += __shfl_xor_sync(kFull, i0, 1);
-    return i0;
-}
-
 __global__ void __launch_bounds__(256) backward_tile_kernel(
-    const Proj* __restrict__ proj, const uint32_t* __restrict__ key_gid,
-    const uint32_t* __restrict__ tile_range, const uint32_t* __restrict__ gauss_offset, int W,
-    int H, int T, int TX, const float* __restrict__ dL_dimage, const float* __restrict__ target,
-    float norm, int64_t cap, float* __restrict__ partial, float* __restrict__ sse_part,
-    float* __restrict__ image_out) {
+    const Proj* __restrict__ proj, uint32_t* __restrict__ key_gid,
+    const uint32_t* __restrict__ tile_range, const uint32_t* __restrict__ gauss_off, int n,
+    int W, int H, int T, int TX, bool presorted, const float* __restrict__ dL_dimage,
+    const float* __restrict__ target, float norm, int64_t cap, float* __restrict__ partial,
+    float* __restrict__ sse_part, float* __restrict__ image_out) {
     __shared__ BwdShared sh;
     const TileCtx t = make_tile_ctx(W, H, TX);
     const uint32_t s = tile_range[t.img * T + t.tile];
     const uint32_t e = tile_range[t.img * T + t.tile + 1];
+    const uint32_t L = e - s;
     const size_t P = (size_t)W * H;
     const size_t pix = (size_t)t.img * 3 * P + (size_t)t.y * W + t.x;
-    bool staged_all = false;   // pass 1 left the whole list in shared memory
+    const int lpix = (t.y - t.ty * kTile) * kTile + (t.x - t.tx * kTile);
+    const int sorted = presorted ? -1
+                                 : sorted_segment(proj, key_gid, s, e, n, t.img, t.tx, t.ty, sh.sl,
+                                                  sh.scratch);
+    auto gid_at = [&](uint32_t i) -> uint32_t { return sorted >= 0 ? sh.sl[i] : key_gid[s + i]; };
+    bool staged_all = false;
 
     float g0 = 0.f, g1 = 0.f, g2 = 0.f;
     if (dL_dimage != nullptr) {
@@ -78,32 +66,17 @@ __global__ void __launch_bounds__(256) backward_tile_kernel(
             g2 = dL_dimage[pix + 2 * P];
         }
     } else {
-        // ---- pass 1: forward (Eq. 7) ----
+        // ---- pass 1: forward (Eq. 7), pixel-parallel ----
         float acc0 = 0.f, acc1 = 0.f, acc2 = 0.f;
-        for (uint32_t base = s; base < e; base += 256) {
-            const int cnt = (int)min(256u, e - base);
+        for (uint32_t base = 0; base < L; base += 256) {
+            const int cnt = (int)min(256u, L - base);
+            if (base > 0) __syncthreads();
+            if ((int)threadIdx.x < cnt) stage_gid(sh.sr, proj, gid_at(base + threadIdx.x), threadIdx.x, t);
             __syncthreads();
-            stage_record(sh.sr, proj, key_gid, base, cnt, t, nullptr);
-            __syncthreads();
-#pragma unroll 1
-            for (int q = 0; q < cnt; q += 32) {
-                const int jl = q + t.lane;
-                const bool ov = jl < cnt && warp_overlaps(sh.sr.c[jl], t);
-                unsigned m = __ballot_sync(kFull, ov);
-                while (m) {
-                    const int j = q + __ffs(m) - 1;
-                    m &= m - 1;
-                    const float4 A = sh.sr.a[j];
-                    const float4 B = sh.sr.b[j];
-                    const PairEval pe = eval_pair(A, B, t);
-                    const float w = pixel_in_box(sh.sr.c[j], t) ? pe.w : 0.f;
-                    acc0 = fmaf(B.y, w, acc0);
-                    acc1 = fmaf(B.z, w, acc1);
-                    acc2 = fmaf(B.w, w, acc2);
-                }
-            }
+            const int nl = build_warp_list(sh.sr, sh.wl, cnt, t);
+            forward_batch(sh.sr, sh.wl, nl, t, acc0, acc1, acc2);
         }
-        staged_all = (e - s) <= 256u;
+        staged_all = L <= 256u;
         float sq = 0.f;
         if (t.in_image) {
             const float r0 = acc0 - target[pix];
@@ -123,100 +96,160 @@ __global__ void __launch_bounds__(256) backward_tile_kernel(
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) sq += __shfl_xor_sync(kFull, sq, o);
             if (t.lane == 0) sh.sse[t.warp] = sq;
-            __syncthreads();
-            if (threadIdx.x == 0) {
-                float tot = 0.f;
-#pragma unroll
-                for (int w = 0; w < kWarps; ++w) tot += sh.sse[w];
-                sse_part[t.img * T + t.tile] = tot;
-            }
         }
     }
+    sh.g[lpix] = make_float4(g0, g1, g2, 0.f);
+    __syncthreads();
+    if (sse_part != nullptr && dL_dimage == nullptr && threadIdx.x == 0) {
+        float tot = 0.f;
+#pragma unroll
+        for (int w = 0; w < kWarps; ++w) tot += sh.sse[w];
+        sse_part[t.img * T + t.tile] = tot;
+    }
 
-    // ---- pass 2: gradients ----
-    for (uint32_t base = s; base < e; base += 256) {
-        const int cnt = (int)min(256u, e - base);
+    // ---- pass 2: gradients, Gaussian-parallel ----
+    const int tx0 = t.tx * kTile, ty0 = t.ty * kTile;
+    for (uint32_t base = 0; base < L; base += 256) {
+        const int cnt = (int)min(256u, L - base);
         __syncthreads();
-        {
-            const int j = threadIdx.x;
-            if (!staged_all) stage_record(sh.sr, proj, key_gid, base, cnt, t, nullptr);
-            if (j < cnt) {
-                // slot of key (tile, gid) in the pre-sort (gid-major, row-major
-                // rectangle) order; record j was staged by this same thread
-                const uint32_t gid = key_gid[base + j];
-                const int4 b = sh.sr.c[j];
-                const int tx0 = b.x / kTile, tx1 = (b.x + b.y) / kTile, ty0 = b.z / kTile;
-                sh.slot[j] = gauss_offset[gid] + (uint32_t)((t.ty - ty0) * (tx1 - tx0 + 1) + (t.tx - tx0));
-            }
+        if ((int)threadIdx.x < cnt) {
+            const uint32_t gid = gid_at(base + threadIdx.x);
+            if (!staged_all) stage_gid(sh.sr, proj, gid, threadIdx.x, t);
+            // slot: the Gaussian's contiguous partial range, tile rank in its
+            // rectangle (row-major) -- the same order finalize sums in
+            const int4 b = sh.sr.c[threadIdx.x];
+            const int rtx0 = b.x / kTile, rtx1 = (b.x + b.y) / kTile, rty0 = b.z / kTile;
+            sh.slot[threadIdx.x] =
+                gauss_off[gid] + (uint32_t)((t.ty - rty0) * (rtx1 - rtx0 + 1) + (t.tx - rtx0));
         }
         __syncthreads();
-        for (int q = 0; q < cnt; q += kSub) {
-            // zero this warp's reduction rows
-            {
-                float4* row = reinterpret_cast<float4*>(&sh.red[t.warp][t.lane][0]);
-                row[0] = make_float4(0.f, 0.f, 0.f, 0.f);
-                row[1] = make_float4(0.f, 0.f, 0.f, 0.f);
-            }
-            const int jl = q + t.lane;
-            const bool ov = jl < cnt && warp_overlaps(sh.sr.c[jl], t);
-            unsigned m = __ballot_sync(kFull, ov);
-            __syncwarp();
-            while (m) {
-                const int jj = __ffs(m) - 1;
-                m &= m - 1;
-                const int j = q + jj;
-                const float4 A = sh.sr.a[j];
-                const float4 B = sh.sr.b[j];
-                const PairEval pe = eval_pair(A, B, t);
-                const float w = pixel_in_box(sh.sr.c[j], t) ? pe.w : 0.f;
-                const float gw0 = g0 * w, gw1 = g1 * w, gw2 = g2 * w;
-                // gamma = dL/dsigma = -w <g, c'>
-                const float gam = -fmaf(B.y, gw0, fmaf(B.z, gw1, B.w * gw2));
-                const float gu = gam * pe.u, gv = gam * pe.v;
-                const float r = warp_reduce8(gw0, gw1, gw2, gu, gv, gu * pe.u, gu * pe.v,
-                                             gv * pe.v, t.lane);
-                if ((t.lane & 3) == 0) sh.red[t.warp][jj][t.lane >> 2] = r;
-            }
-            __syncthreads();
-            {
-                const int jj = threadIdx.x >> 3, c = threadIdx.x & 7;
-                if (q + jj < cnt) {
-                    float acc = 0.f;
-#pragma unroll
-                    for (int w = 0; w < kWarps; ++w) acc += sh.red[w][jj][c];
-                    const uint32_t slot = sh.slot[q + jj];
-                    if ((int64_t)slot < cap) partial[(size_t)slot * 8 + c] = acc;
+        // q lanes per Gaussian (power of two, <= 8, q * cnt <= 256)
+        int q = 1;
+        while (q < 8 && q * 2 * cnt <= 256) q <<= 1;
+        const int j = threadIdx.x / q;          // Gaussian of this lane
+        const int ph = threadIdx.x % q;         // row phase
+        float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f, a4 = 0.f, a5 = 0.f, a6 = 0.f, a7 = 0.f;
+        if (j < cnt) {
+            const float4 A = sh.sr.a[j];
+            const float4 B = sh.sr.b[j];
+            const int4 Cb = sh.sr.c[j];
+            const int lx0 = max(Cb.x - tx0, 0), lx1 = min(Cb.x + Cb.y - tx0, kTile - 1);
+            const int ly0 = max(Cb.z - ty0, 0), ly1 = min(Cb.z + Cb.w - ty0, kTile - 1);
+            const float dx0 = ((float)lx0 + 0.5f) - A.x;
+            for (int ly = ly0 + ph; ly <= ly1; ly += q) {
+                const float dy = ((float)ly + 0.5f) - A.y;
+                const float cdy = B.x * dy;
+                const float4* grow = &sh.g[ly * kTile];
+                float dx = dx0;
+                for (int lx = lx0; lx <= lx1; ++lx, dx += 1.0f) {
+                    const float u = A.z * dx;
+                    const float v = fmaf(A.w, dx, cdy);
+                    const float w = ex2_approx(fmaf(-u, u, -(v * v)));
+                    const float4 gp = grow[lx];
+                    const float gw0 = gp.x * w, gw1 = gp.y * w, gw2 = gp.z * w;
+                    const float sdot = fmaf(B.y, gw0, fmaf(B.z, gw1, B.w * gw2));   // -gamma
+                    const float gu = -sdot * u, gv = -sdot * v;
+                    a0 += gw0;
+                    a1 += gw1;
+                    a2 += gw2;
+                    a3 += gu;
+                    a4 += gv;
+                    a5 = fmaf(gu, u, a5);
+                    a6 = fmaf(gu, v, a6);
+                    a7 = fmaf(gv, v, a7);
                 }
             }
-            __syncthreads();
+        }
+        // combine the q row phases (fixed xor tree, deterministic)
+        for (int o = 1; o < q; o <<= 1) {
+            a0 += __shfl_xor_sync(kFull, a0, o);
+            a1 += __shfl_xor_sync(kFull, a1, o);
+            a2 += __shfl_xor_sync(kFull, a2, o);
+            a3 += __shfl_xor_sync(kFull, a3, o);
+            a4 += __shfl_xor_sync(kFull, a4, o);
+            a5 += __shfl_xor_sync(kFull, a5, o);
+            a6 += __shfl_xor_sync(kFull, a6, o);
+            a7 += __shfl_xor_sync(kFull, a7, o);
+        }
+        if (j < cnt && ph == 0) {
+            const uint32_t sl = sh.slot[j];
+            if ((int64_t)sl < cap) {
+                float4* dst = reinterpret_cast<float4*>(partial + (size_t)sl * 8);
+                dst[0] = make_float4(a0, a1, a2, a3);
+                dst[1] = make_float4(a4, a5, a6, a7);
+            }
         }
     }
 }
 
-// Per Gaussian: sum its tiles' partials in slot order, then the closed-form
-// chain rule.  With p = u / kappa, q = v / kappa (so sigma = (p^2 + q^2) / 2,
-// p = dx / l1, q = (dy - l2 p) / l3):
+__global__ void __launch_bounds__(256) alloc_kernel(const Proj* __restrict__ proj, int total,
+                                                    uint32_t* __restrict__ counter,
+                                                    uint32_t* __restrict__ gauss_off) {
+    const int g = blockIdx.x * blockDim.x + threadIdx.x;
+    uint32_t cnt = 0;
+    if (g < total) {
+        const Proj r = proj[g];
+        const uint32_t bx = __float_as_uint(r.q1.w), by = __float_as_uint(r.q2.w);
+        const int x0 = (int)(bx & 0xffffu), x1 = (int)(bx >> 16);
+        const int y0 = (int)(by & 0xffffu), y1 = (int)(by >> 16);
+        if (x0 <= x1 && y0 <= y1)
+            cnt = (uint32_t)((x1 / kTile - x0 / kTile + 1) * (y1 / kTile - y0 / kTile + 1));
+    }
+    const uint32_t off = warp_alloc(counter, cnt);
+    if (g < total) gauss_off[g] = off;
+}
+
+__device__ __forceinline__ float adam1(float p, float g, float& m, float& v, float b1, float b2,
+                                       float lr, float ibc1, float ibc2, float eps) {
+    m = fmaf(b1, m, (1.0f - b1) * g);
+    v = fmaf(b2, v, (1.0f - b2) * (g * g));
+    return p - lr * (m * ibc1) / (sqrtf(v * ibc2) + eps);
+}
+
+// Per Gaussian: sum its tiles' partials (row-major tile order), then the
+// closed-form chain rule.  With p = u / kappa, q = v / kappa (so
+// sigma = (p^2 + q^2) / 2, p = dx / l1, q = (dy - l2 p) / l3):
 //   dsigma/ddx = (p - q l2 / l3) / l1,  dsigma/ddy = q / l3,  d = pixel - mu
 //   dsigma/dl1 = -p dsigma/ddx, dsigma/dl2 = -p q / l3, dsigma/dl3 = -q^2 / l3
 // (equal to <dsigma/dSigma, dSigma/dl> of A.2 with the R14 correction).
-__global__ void __launch_bounds__(256) finalize_kernel(const float4* __restrict__ params,
-                                                       const uint32_t* __restrict__ gauss_offset,
-                                                       int total, int W, int H, uint32_t flags,
-                                                       int64_t cap, const float* __restrict__ partial,
-                                                       float4* __restrict__ grads) {
+__global__ void __launch_bounds__(256) finalize_kernel(
+    const float4* __restrict__ params, const Proj* __restrict__ proj,
+    const uint32_t* __restrict__ gauss_off, int total, int W, int H, uint32_t flags, int64_t cap,
+    const float* __restrict__ partial, float4* __restrict__ grads, FusedAdam adam) {
+    __shared__ float sconst[3];
+    if (adam.m != nullptr) {
+        if (threadIdx.x == 0) {
+            const int t = (int)*adam.step_dev;
+            sconst[0] = ldexpf(adam.lr0, -((t - 1) / adam.half_every));
+            sconst[1] = (float)(1.0 / (1.0 - pow((double)adam.b1, (double)t)));
+            sconst[2] = (float)(1.0 / (1.0 - pow((double)adam.b2, (double)t)));
+        }
+        __syncthreads();
+    }
     const int g = blockIdx.x * blockDim.x + threadIdx.x;
     if (g >= total) return;
-    const uint32_t o0 = gauss_offset[g], o1 = gauss_offset[g + 1];
-    float S[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-    for (uint32_t o = o0; o < o1 && (int64_t)o < cap; ++o) {
-        const float4 a = reinterpret_cast<const float4*>(partial)[2 * (size_t)o];
-        const float4 b = reinterpret_cast<const float4*>(partial)[2 * (size_t)o + 1];
-        S[0] += a.x; S[1] += a.y; S[2] += a.z; S[3] += a.w;
-        S[4] += b.x; S[5] += b.y; S[6] += b.z; S[7] += b.w;
-    }
     const float4 p0 = params[2 * (size_t)g], p1 = params[2 * (size_t)g + 1];
+    const Proj r = proj[g];
+    const uint32_t bx = __float_as_uint(r.q1.w), by = __float_as_uint(r.q2.w);
+    const int x0 = (int)(bx & 0xffffu), x1 = (int)(bx >> 16);
+    const int y0 = (int)(by & 0xffffu), y1 = (int)(by >> 16);
+    float S[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    bool any = false;
+    if (x0 <= x1 && y0 <= y1) {
+        const uint32_t cnt = (uint32_t)((x1 / kTile - x0 / kTile + 1) * (y1 / kTile - y0 / kTile + 1));
+        const uint32_t o0 = gauss_off[g];
+        const float4* pp = reinterpret_cast<const float4*>(partial);
+        for (uint32_t k = 0; k < cnt; ++k) {       // row-major tile order of the rectangle
+            if ((int64_t)(o0 + k) >= cap) break;
+            const float4 a = pp[2 * (size_t)(o0 + k)];
+            const float4 b = pp[2 * (size_t)(o0 + k) + 1];
+            S[0] += a.x; S[1] += a.y; S[2] += a.z; S[3] += a.w;
+            S[4] += b.x; S[5] += b.y; S[6] += b.z; S[7] += b.w;
+        }
+        any = true;
+    }
     float4 r0 = make_float4(0.f, 0.f, 0.f, 0.f), r1 = r0;
-    if (o1 > o0) {
+    if (any) {
         const double l1 = (double)p0.z + 0.5, l2 = (double)p0.w, l3 = (double)p1.x + 0.5;
         const double ik = 1.0 / kKappa, ik2 = ik * ik;
         const double Sp = S[3] * ik, Sq = S[4] * ik;
@@ -240,6 +273,28 @@ __global__ void __launch_bounds__(256) finalize_kernel(const float4* __restrict_
     }
     grads[2 * (size_t)g] = r0;
     grads[2 * (size_t)g + 1] = r1;
+    if (adam.m != nullptr) {
+        const float lr = sconst[0], ibc1 = sconst[1], ibc2 = sconst[2];
+        float4* mm = reinterpret_cast<float4*>(adam.m) + 2 * (size_t)g;
+        float4* vv = reinterpret_cast<float4*>(adam.v) + 2 * (size_t)g;
+        float4* pp = reinterpret_cast<float4*>(adam.params) + 2 * (size_t)g;
+        float4 m0 = mm[0], m1 = mm[1], v0 = vv[0], v1 = vv[1];
+        float4 q0, q1;
+        const float b1 = adam.b1, b2 = adam.b2, eps = adam.eps;
+        q0.x = adam1(p0.x, r0.x, m0.x, v0.x, b1, b2, lr, ibc1, ibc2, eps);
+        q0.y = adam1(p0.y, r0.y, m0.y, v0.y, b1, b2, lr, ibc1, ibc2, eps);
+        q0.z = adam1(p0.z, r0.z, m0.z, v0.z, b1, b2, lr, ibc1, ibc2, eps);
+        q0.w = adam1(p0.w, r0.w, m0.w, v0.w, b1, b2, lr, ibc1, ibc2, eps);
+        q1.x = adam1(p1.x, r1.x, m1.x, v1.x, b1, b2, lr, ibc1, ibc2, eps);
+        q1.y = adam1(p1.y, r1.y, m1.y, v1.y, b1, b2, lr, ibc1, ibc2, eps);
+        q1.z = adam1(p1.z, r1.z, m1.z, v1.z, b1, b2, lr, ibc1, ibc2, eps);
+        q1.w = adam1(p1.w, r1.w, m1.w, v1.w, b1, b2, lr, ibc1, ibc2, eps);
+        mm[0] = m0; mm[1] = m1; vv[0] = v0; vv[1] = v1;
+        pp[0] = q0; pp[1] = q1;
+        const bool bad = !(isfinite(q0.x) && isfinite(q0.y) && isfinite(q0.z) && isfinite(q0.w) &&
+                           isfinite(q1.x) && isfinite(q1.y) && isfinite(q1.z) && isfinite(q1.w));
+        if (bad && adam.flag != nullptr) atomicOr(adam.flag, 1u);
+    }
 }
 
 __global__ void __launch_bounds__(256) loss_kernel(const float* __restrict__ sse_part, int T,
@@ -259,17 +314,21 @@ __global__ void __launch_bounds__(256) loss_kernel(const float* __restrict__ sse
 
 struct BwdWs {
     float* partial;
+    uint32_t* gauss_off;
+    uint32_t* counter;
     float* sse;
     size_t bytes;
 };
 
 BwdWs carve(void* base, int n, int64_t cap, const gi_frame& f) {
-    (void)n;
     const int T = tiles_x(f.width) * tiles_y(f.height);
+    const size_t total = (size_t)n * f.batch;
     char* p = static_cast<char*>(base);
     BwdWs w;
     size_t off = 0;
     w.partial = reinterpret_cast<float*>(p + off); off += align_up(sizeof(float) * 8 * (size_t)cap);
+    w.gauss_off = reinterpret_cast<uint32_t*>(p + off); off += align_up(sizeof(uint32_t) * (total + 1));
+    w.counter = reinterpret_cast<uint32_t*>(p + off); off += align_up(sizeof(uint32_t));
     w.sse = reinterpret_cast<float*>(p + off); off += align_up(sizeof(float) * (size_t)T * f.batch);
     w.bytes = off;
     return w;
@@ -279,37 +338,57 @@ BwdWs carve(void* base, int n, int64_t cap, const gi_frame& f) {
 
 size_t backward_ws_bytes(int n, int64_t cap, const gi_frame& f) { return carve(nullptr, n, cap, f).bytes; }
 
-cudaError_t launch_backward_tiles(const Proj* proj, const uint32_t* key_gid,
-                                  const uint32_t* tile_range, const uint32_t* gauss_offset, int n,
-                                  const gi_frame& f, const float* dL_dimage, const float* target,
-                                  int64_t cap, void* ws, float* image_out, cudaStream_t s) {
-    (void)n;
+uint32_t* backward_alloc_counter(void* ws, int n, int64_t cap, const gi_frame& f) {
+    return carve(ws, n, cap, f).counter;
+}
+uint32_t* backward_gauss_off(void* ws, int n, int64_t cap, const gi_frame& f) {
+    return carve(ws, n, cap, f).gauss_off;
+}
+
+cudaError_t launch_backward_alloc(const Proj* proj, int n, const gi_frame& f, int64_t cap, void* ws,
+                                  cudaStream_t s) {
+    BwdWs w = carve(ws, n, cap, f);
+    const int total = n * f.batch;
+    cudaError_t e = cudaMemsetAsync(w.counter, 0, sizeof(uint32_t), s);
+    if (e != cudaSuccess || total == 0) return e;
+    alloc_kernel<<<(total + 255) / 256, 256, 0, s>>>(proj, total, w.counter, w.gauss_off);
+    note_launches(1);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_backward_tiles(const Proj* proj, uint32_t* key_gid, const uint32_t* tile_range,
+                                  int n, const gi_frame& f, bool presorted,
+                                  const float* dL_dimage, const float* target, int64_t cap,
+                                  void* ws, float* image_out, cudaStream_t s) {
     BwdWs w = carve(ws, n, cap, f);
     const int TX = tiles_x(f.width), T = TX * tiles_y(f.height);
     const double count = 3.0 * (double)f.width * (double)f.height;
     const float norm = (float)(2.0 / count);
     const bool mse = dL_dimage == nullptr;
     dim3 grid(T, f.batch);
-    backward_tile_kernel<<<grid, 256, 0, s>>>(proj, key_gid, tile_range, gauss_offset, f.width,
-                                              f.height, T, TX, dL_dimage, target, norm, cap,
-                                              w.partial, mse ? w.sse : nullptr,
+    backward_tile_kernel<<<grid, 256, 0, s>>>(proj, key_gid, tile_range, w.gauss_off, n, f.width,
+                                              f.height, T, TX, presorted, dL_dimage, target, norm,
+                                              cap, w.partial, mse ? w.sse : nullptr,
                                               mse ? image_out : nullptr);
     note_launches(1);
     return cudaGetLastError();
 }
 
-cudaError_t launch_backward_finalize(const float* params, const uint32_t* gauss_offset, int n,
+cudaError_t launch_backward_finalize(const float* params, const Proj* proj, int n,
                                      const gi_frame& f, uint32_t flags, bool mse, int64_t cap,
-                                     void* ws, float* grads, float* loss, cudaStream_t s) {
+                                     void* ws, float* grads, float* loss, const FusedAdam* adam,
+                                     cudaStream_t s) {
     BwdWs w = carve(ws, n, cap, f);
     const int T = tiles_x(f.width) * tiles_y(f.height);
     const double count = 3.0 * (double)f.width * (double)f.height;
     const int total = n * f.batch;
     cudaError_t e = cudaSuccess;
     if (total > 0) {
+        FusedAdam fa{};
+        if (adam) fa = *adam;
         finalize_kernel<<<(total + 255) / 256, 256, 0, s>>>(
-            reinterpret_cast<const float4*>(params), gauss_offset, total, f.width, f.height, flags,
-            cap, w.partial, reinterpret_cast<float4*>(grads));
+            reinterpret_cast<const float4*>(params), proj, w.gauss_off, total, f.width, f.height,
+            flags, cap, w.partial, reinterpret_cast<float4*>(grads), fa);
         note_launches(1);
         if ((e = cudaGetLastError()) != cudaSuccess) return e;
     }
@@ -322,15 +401,17 @@ cudaError_t launch_backward_finalize(const float* params, const uint32_t* gauss_
 }
 
 cudaError_t launch_backward(const float* params, const Proj* proj, const uint32_t* key_gid,
-                            const uint32_t* tile_range, const uint32_t* gauss_offset, int n,
-                            const gi_frame& f, uint32_t flags, const float* dL_dimage,
-                            const float* target, int64_t cap, void* ws, float* grads, float* loss,
-                            float* image_out, cudaStream_t s) {
-    cudaError_t e = launch_backward_tiles(proj, key_gid, tile_range, gauss_offset, n, f, dL_dimage,
-                                          target, cap, ws, image_out, s);
+                            const uint32_t* tile_range, int n, const gi_frame& f, uint32_t flags,
+                            const float* dL_dimage, const float* target, int64_t cap, void* ws,
+                            float* grads, float* loss, float* image_out, cudaStream_t s) {
+    cudaError_t e = launch_backward_alloc(proj, n, f, cap, ws, s);
     if (e != cudaSuccess) return e;
-    return launch_backward_finalize(params, gauss_offset, n, f, flags, dL_dimage == nullptr, cap,
-                                    ws, grads, loss, s);
+    // gi_bin output is already in gid order: no re-sort, key_gid not written
+    e = launch_backward_tiles(proj, const_cast<uint32_t*>(key_gid), tile_range, n, f, true,
+                              dL_dimage, target, cap, ws, image_out, s);
+    if (e != cudaSuccess) return e;
+    return launch_backward_finalize(params, proj, n, f, flags, dL_dimage == nullptr, cap, ws, grads,
+                                    loss, nullptr, s);
 }
 
 }  // namespace gi

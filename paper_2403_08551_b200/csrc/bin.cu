@@ -2,267 +2,323 @@
 // from rasterization"; north_star "duplicates (tile-id, gaussian-id) keys and
 // radix-sorts them, with no depth key").
 //
-//   1. gauss_offset = exclusive scan of tiles_touched            (scan.cu)
-//   2. duplicate: one (tile, gid) key per tile of each rectangle, row-major,
-//      written warp-cooperatively (one warp walks 32 Gaussians; the lanes of
-//      the warp write one Gaussian's keys in parallel -> coalesced, and one
-//      huge Gaussian does not serialise a single thread)
-//   3. stable LSD radix sort on the tile id only, ceil(log2(B*T)) bits in
-//      passes of <= 8 bits; each pass = block digit histogram -> exclusive
-//      scan of the digit-major [digit][chunk] table -> stable scatter, where
-//      the in-chunk rank comes from __match_any_sync per 32-key stripe and
-//      per-warp digit counters.  Hand-written, no CUB.
-//   4. tile_range[t] = first index with key_tile >= t.
-// Emission is in ascending gid, the sort is stable, so keys end in the unique
-// lexicographic (tile, gid) order (reading R9) and match the oracle bit-exact.
-#include "gi_internal.cuh"
+// The only order that matters is "grouped by tile" (R9); within a tile the
+// keys are kept in ascending gid so the output is the unique lexicographic
+// (tile, gid) order and the forward sum is deterministic.  On B200 the tile
+// count of one image (1536 at 768x512) is tiny next to the key count, so the
+// sort on the tile digit is done as ONE counting pass instead of LSD radix
+// passes over 8-bit digits:
+//
+//   1. count    per-tile key counts (one RED per (Gaussian, tile)) -- fused
+//               into the projection kernel on the fused paths
+//   2. scan     tile_range = exclusive scan of the counts (one CTA when the
+//               tile count is small; the 3-phase scan otherwise)
+//   3. scatter  each (Gaussian, tile) key claims a slot in its tile's
+//               segment with an atomic cursor: grouped by tile, gid order
+//               inside a segment arbitrary
+//   4. segsort  one CTA per tile restores ascending gid inside the segment:
+//               rank sort (<= 256 keys), shared-memory bitonic sort
+//               (<= 2048), or -- for a pathological segment -- a stable
+//               in-order scan of all Gaussians of the image (no sort needed).
+//               On the fused render / fit paths this step runs inside the
+//               consumer tile kernel instead (same device function).
+// Steps 1-3 are the counting (single-digit LSD radix) pass on the tile id;
+// step 4 is the secondary key.  Hand-written, CUB-free, no data-dependent
+// host sync: grids are sized by N, T or the key capacity.
+#include "raster_common.cuh"
 
 namespace gi {
 namespace {
 
-constexpr int kRadixThreads = 256;
-constexpr int kRadixWarps = kRadixThreads / 32;
-constexpr int kRadixStripes = 16;                                // stripes of 32 per warp
-constexpr int kChunk = kRadixThreads * kRadixStripes;            // 4096 keys per block
-constexpr int kWarpSpan = kChunk / kRadixWarps;                  // 512 keys per warp
+struct Rect {
+    int tx0, tx1, ty0, ty1;
+};
 
-__device__ __forceinline__ int64_t eff_keys(const uint32_t* n_keys, int64_t cap) {
-    int64_t k = (int64_t)*n_keys;
-    return k < cap ? k : cap;
+__device__ __forceinline__ Rect rect_of(const Proj& r) {
+    const uint32_t bx = __float_as_uint(r.q1.w), by = __float_as_uint(r.q2.w);
+    Rect q;
+    q.tx0 = (int)(bx & 0xffffu) / kTile;
+    q.tx1 = (int)(bx >> 16) / kTile;
+    q.ty0 = (int)(by & 0xffffu) / kTile;
+    q.ty1 = (int)(by >> 16) / kTile;
+    return q;
 }
 
-// ---------------------------------------------------------------- duplicate
-__global__ void __launch_bounds__(256) duplicate_kernel(const Proj* __restrict__ proj,
-                                                        const uint32_t* __restrict__ touched,
-                                                        const uint32_t* __restrict__ offset,
-                                                        int total, int n, int T, int TX,
-                                                        int64_t cap, uint32_t* __restrict__ key_tile,
-                                                        uint32_t* __restrict__ key_gid) {
-    const int lane = threadIdx.x & 31;
+// ------------------------------------------------------------------- count
+__global__ void __launch_bounds__(256) count_kernel(const Proj* __restrict__ proj,
+                                                    const uint32_t* __restrict__ touched, int total,
+                                                    int n, int T, int TX,
+                                                    uint32_t* __restrict__ tile_count) {
     const int g = blockIdx.x * blockDim.x + threadIdx.x;
-    uint32_t cnt = 0, off = 0, tx0 = 0, tw = 1, ty0 = 0, tbase = 0;
-    if (g < total) {
-        cnt = touched[g];
-        if (cnt) {
-            off = offset[g];
-            const float4 q1 = proj[g].q1;
-            const float4 q2 = proj[g].q2;
-            const uint32_t bx = __float_as_uint(q1.w), by = __float_as_uint(q2.w);
-            tx0 = (bx & 0xffffu) / kTile;
-            const uint32_t tx1 = (bx >> 16) / kTile;
-            ty0 = (by & 0xffffu) / kTile;
-            tw = tx1 - tx0 + 1;
-            tbase = (uint32_t)(g / n) * (uint32_t)T;
+    if (g >= total || touched[g] == 0) return;
+    const Rect q = rect_of(proj[g]);
+    const int base = (g / n) * T;
+    for (int ty = q.ty0; ty <= q.ty1; ++ty)
+        for (int tx = q.tx0; tx <= q.tx1; ++tx) atomicAdd(&tile_count[base + ty * TX + tx], 1u);
+}
+
+// -------------------------------------------------------------------- scan
+// One CTA: tile_range[0..TT] = exclusive scan of tile_count, n_keys = total.
+// Range entries are clamped to the key capacity so that consumers never read
+// past the key arrays when K > cap (n_keys still reports the true K).
+__global__ void __launch_bounds__(1024) tile_scan_kernel(const uint32_t* __restrict__ tile_count,
+                                                         int TT, int64_t cap,
+                                                         uint32_t* __restrict__ tile_range,
+                                                         uint32_t* __restrict__ n_keys) {
+    __shared__ uint32_t warp_tot[32];
+    __shared__ uint32_t carry_s;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int per = (TT + blockDim.x - 1) / blockDim.x;       // consecutive items per thread
+    const int i0 = threadIdx.x * per;
+    uint32_t s = 0;
+    for (int k = 0; k < per; ++k) {
+        const int i = i0 + k;
+        if (i < TT) s += tile_count[i];
+    }
+    uint32_t x = s;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(kFull, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) warp_tot[warp] = x;
+    __syncthreads();
+    if (warp == 0) {
+        const uint32_t w = lane < (int)(blockDim.x >> 5) ? warp_tot[lane] : 0u;
+        uint32_t wx = w;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(kFull, wx, o);
+            if (lane >= o) wx += y;
+        }
+        warp_tot[lane] = wx - w;
+        if (lane == 31) carry_s = wx;
+    }
+    __syncthreads();
+    uint32_t run = warp_tot[warp] + x - s;
+    for (int k = 0; k < per; ++k) {
+        const int i = i0 + k;
+        if (i < TT) {
+            tile_range[i] = (int64_t)run < cap ? run : (uint32_t)cap;
+            run += tile_count[i];
         }
     }
-    unsigned todo = __ballot_sync(kFull, cnt != 0);
-    while (todo) {
-        const int j = __ffs(todo) - 1;
-        todo &= todo - 1;
+    if (threadIdx.x == 0) {
+        tile_range[TT] = (int64_t)carry_s < cap ? carry_s : (uint32_t)cap;
+        *n_keys = carry_s;
+    }
+}
+
+__global__ void clamp_kernel(uint32_t* __restrict__ v, int64_t count, int64_t cap) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < count && (int64_t)v[i] > cap) v[i] = (uint32_t)cap;
+}
+
+// ----------------------------------------------------------------- scatter
+// Thread per Gaussian claims one slot per tile of its rectangle.  Gaussians
+// touching many tiles (> 16) are handed to the whole warp so that one large
+// splat does not serialise a thread.  With fuse_scan, every CTA first scans
+// the (small) per-tile count table itself into shared memory -- a redundant
+// 6 KB read per CTA instead of a separate launch -- and CTA 0 publishes
+// tile_range and n_keys.
+constexpr int kFusedScanMax = 4096;
+
+__global__ void __launch_bounds__(256) scatter_kernel(const Proj* __restrict__ proj,
+                                                      const uint32_t* __restrict__ touched,
+                                                      int total, int n, int T, int TX, int TT,
+                                                      int64_t cap, bool fuse_scan,
+                                                      const uint32_t* __restrict__ tile_count,
+                                                      uint32_t* __restrict__ tile_range,
+                                                      uint32_t* __restrict__ n_keys,
+                                                      uint32_t* __restrict__ fill,
+                                                      uint32_t* __restrict__ key_tile,
+                                                      uint32_t* __restrict__ key_gid) {
+    __shared__ uint32_t start_s[kFusedScanMax];
+    __shared__ uint32_t wtot[kWarps];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (fuse_scan) {
+        const int per = (TT + 255) / 256;                  // consecutive tiles per thread
+        const int i0 = threadIdx.x * per;
+        uint32_t sum = 0;
+        for (int k = 0; k < per; ++k)
+            if (i0 + k < TT) sum += tile_count[i0 + k];
+        uint32_t x = sum;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(kFull, x, o);
+            if (lane >= o) x += y;
+        }
+        if (lane == 31) wtot[warp] = x;
+        __syncthreads();
+        uint32_t before = 0, all = 0;
+#pragma unroll
+        for (int w = 0; w < kWarps; ++w) {
+            before += w < warp ? wtot[w] : 0u;
+            all += wtot[w];
+        }
+        uint32_t run = before + x - sum;
+        for (int k = 0; k < per; ++k) {
+            const int i = i0 + k;
+            if (i < TT) {
+                const uint32_t v = (int64_t)run < cap ? run : (uint32_t)cap;
+                start_s[i] = v;
+                if (blockIdx.x == 0) tile_range[i] = v;
+                run += tile_count[i];
+            }
+        }
+        if (blockIdx.x == 0 && threadIdx.x == 0) {
+            tile_range[TT] = (int64_t)all < cap ? all : (uint32_t)cap;
+            *n_keys = all;
+        }
+        __syncthreads();
+    }
+    const int g = blockIdx.x * blockDim.x + threadIdx.x;
+    uint32_t cnt = g < total ? touched[g] : 0u;
+    Rect q{0, -1, 0, -1};
+    int base = 0;
+    if (cnt) {
+        q = rect_of(proj[g]);
+        base = (g / n) * T;
+    }
+    if (cnt > 0 && cnt <= 16) {
+        for (int ty = q.ty0; ty <= q.ty1; ++ty)
+            for (int tx = q.tx0; tx <= q.tx1; ++tx) {
+                const int t = base + ty * TX + tx;
+                const uint32_t st = fuse_scan ? start_s[t] : tile_range[t];
+                const int64_t slot = (int64_t)st + atomicAdd(&fill[t], 1u);
+                if (slot < cap) {
+                    key_tile[slot] = (uint32_t)t;
+                    key_gid[slot] = (uint32_t)g;
+                }
+            }
+    }
+    unsigned big = __ballot_sync(kFull, cnt > 16);
+    while (big) {
+        const int j = __ffs(big) - 1;
+        big &= big - 1;
+        const int tx0 = __shfl_sync(kFull, q.tx0, j), tx1 = __shfl_sync(kFull, q.tx1, j);
+        const int ty0 = __shfl_sync(kFull, q.ty0, j);
         const uint32_t c = __shfl_sync(kFull, cnt, j);
-        const uint32_t o = __shfl_sync(kFull, off, j);
-        const uint32_t x0 = __shfl_sync(kFull, tx0, j);
-        const uint32_t w = __shfl_sync(kFull, tw, j);
-        const uint32_t y0 = __shfl_sync(kFull, ty0, j);
-        const uint32_t tb = __shfl_sync(kFull, tbase, j);
+        const int b = __shfl_sync(kFull, base, j);
+        const int w = tx1 - tx0 + 1;
         const uint32_t gid = (uint32_t)(g - lane + j);
         for (uint32_t i = lane; i < c; i += 32) {
-            const int64_t pos = (int64_t)o + i;
-            if (pos < cap) {
-                const uint32_t ty = y0 + i / w, tx = x0 + i % w;
-                key_tile[pos] = tb + ty * (uint32_t)TX + tx;
-                key_gid[pos] = gid;
+            const int t = b + (ty0 + (int)i / w) * TX + tx0 + (int)i % w;
+            const uint32_t st = fuse_scan ? start_s[t] : tile_range[t];
+            const int64_t slot = (int64_t)st + atomicAdd(&fill[t], 1u);
+            if (slot < cap) {
+                key_tile[slot] = (uint32_t)t;
+                key_gid[slot] = gid;
             }
         }
     }
 }
 
-// -------------------------------------------------------------- radix sort
-__global__ void __launch_bounds__(kRadixThreads) radix_hist_kernel(const uint32_t* __restrict__ keys,
-                                                                  const uint32_t* __restrict__ n_keys,
-                                                                  int64_t cap, int shift, int bits,
-                                                                  uint32_t* __restrict__ hist) {
-    __shared__ uint32_t cnt[256];
-    const int64_t K = eff_keys(n_keys, cap);
-    const int64_t nc = (K + kChunk - 1) / kChunk;
-    const int64_t b = blockIdx.x;
-    if (b >= nc) return;
-    const int R = 1 << bits;
-    const uint32_t mask = (uint32_t)R - 1u;
-    for (int i = threadIdx.x; i < R; i += blockDim.x) cnt[i] = 0;
-    __syncthreads();
-    const int64_t base = b * kChunk;
-    for (int i = threadIdx.x; i < kChunk; i += blockDim.x) {
-        const int64_t k = base + i;
-        if (k < K) atomicAdd(&cnt[(keys[k] >> shift) & mask], 1u);
-    }
-    __syncthreads();
-    for (int d = threadIdx.x; d < R; d += blockDim.x) hist[(int64_t)d * nc + b] = cnt[d];
-}
-
-__global__ void __launch_bounds__(kRadixThreads) radix_scatter_kernel(
-    const uint32_t* __restrict__ keys_in, const uint32_t* __restrict__ vals_in,
-    uint32_t* __restrict__ keys_out, uint32_t* __restrict__ vals_out,
-    const uint32_t* __restrict__ n_keys, int64_t cap, int shift, int bits,
-    const uint32_t* __restrict__ hist_scanned) {
-    __shared__ uint32_t whist[kRadixWarps][256];
-    const int64_t K = eff_keys(n_keys, cap);
-    const int64_t nc = (K + kChunk - 1) / kChunk;
-    const int64_t b = blockIdx.x;
-    if (b >= nc) return;
-    const int R = 1 << bits;
-    const uint32_t mask = (uint32_t)R - 1u;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    for (int i = threadIdx.x; i < kRadixWarps * 256; i += blockDim.x) (&whist[0][0])[i] = 0;
-    __syncthreads();
-
-    // Local stable ranks: warp w owns keys [base + w*512, +512) in 16 stripes.
-    const int64_t wbase = b * kChunk + (int64_t)warp * kWarpSpan;
-    uint32_t key[kRadixStripes], val[kRadixStripes], rank[kRadixStripes];
-    const unsigned lt = lanemask_lt();
-#pragma unroll
-    for (int s = 0; s < kRadixStripes; ++s) {
-        const int64_t k = wbase + s * 32 + lane;
-        const bool valid = k < K;
-        key[s] = valid ? keys_in[k] : 0u;
-        val[s] = valid ? vals_in[k] : 0u;
-        const unsigned act = __ballot_sync(kFull, valid);
-        rank[s] = 0;
-        if (valid) {
-            const uint32_t d = (key[s] >> shift) & mask;
-            const unsigned peers = __match_any_sync(act, d);
-            const uint32_t before = whist[warp][d];
-            rank[s] = before + __popc(peers & lt);
-            __syncwarp(act);
-            if ((peers & ~lt & ~(1u << lane)) == 0u)        // highest lane of the group
-                whist[warp][d] = before + __popc(peers);
-        }
-        __syncwarp();
-    }
-    __syncthreads();
-    // Cross-warp exclusive prefix per digit (warp order = key order).
-    for (int d = threadIdx.x; d < R; d += blockDim.x) {
-        uint32_t run = 0;
-#pragma unroll
-        for (int w = 0; w < kRadixWarps; ++w) {
-            const uint32_t c = whist[w][d];
-            whist[w][d] = run;
-            run += c;
-        }
-    }
-    __syncthreads();
-#pragma unroll
-    for (int s = 0; s < kRadixStripes; ++s) {
-        const int64_t k = wbase + s * 32 + lane;
-        if (k < K) {
-            const uint32_t d = (key[s] >> shift) & mask;
-            const uint32_t dst = hist_scanned[(int64_t)d * nc + b] + whist[warp][d] + rank[s];
-            keys_out[dst] = key[s];
-            vals_out[dst] = val[s];
-        }
-    }
-}
-
-// ------------------------------------------------------------------ ranges
-__global__ void __launch_bounds__(256) ranges_kernel(const uint32_t* __restrict__ key_tile,
-                                                     const uint32_t* __restrict__ n_keys,
-                                                     int64_t cap, uint32_t total_tiles,
-                                                     uint32_t* __restrict__ range) {
-    const int64_t K = eff_keys(n_keys, cap);
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i > K) return;
-    const int64_t prev = i > 0 ? (int64_t)key_tile[i - 1] : -1;
-    const int64_t cur = i < K ? (int64_t)key_tile[i] : (int64_t)total_tiles;
-    for (int64_t t = prev + 1; t <= cur; ++t) range[t] = (uint32_t)i;
+// ----------------------------------------------------------------- segsort
+// One CTA per tile: restore ascending gid inside the segment (see
+// sorted_segment in raster_common.cuh) and write it back.
+__global__ void __launch_bounds__(256) segsort_kernel(const Proj* __restrict__ proj, int n, int T,
+                                                      int TX, const uint32_t* __restrict__ tile_range,
+                                                      uint32_t* __restrict__ key_gid) {
+    __shared__ uint32_t sl[kSortMax];
+    __shared__ uint32_t scratch[kWarps];
+    const int t = blockIdx.x;
+    const uint32_t s0 = tile_range[t], s1 = tile_range[t + 1];
+    if (s1 - s0 <= 1) return;
+    const int img = t / T, tl = t % T;
+    const int cnt = sorted_segment(proj, key_gid, s0, s1, n, img, tl % TX, tl / TX, sl, scratch);
+    for (int i = threadIdx.x; i < cnt; i += blockDim.x) key_gid[s0 + i] = sl[i];
 }
 
 struct BinWs {
-    uint32_t* keys_a;
-    uint32_t* vals_a;
-    uint32_t* hist;
+    uint32_t* tile_count;
+    uint32_t* fill;
+    uint32_t* alloc_counter;
     uint32_t* scan_ws;
     size_t bytes;
 };
 
-int64_t max_chunks(int64_t cap) { return (cap + kChunk - 1) / kChunk; }
-
 BinWs carve(void* base, int n, int64_t cap, const gi_frame& f) {
-    const int64_t total = (int64_t)n * f.batch;
-    const int64_t hist_words = max_chunks(cap) * 256;
-    const int64_t scan_max = total + 1 > hist_words ? total + 1 : hist_words;
+    (void)n;
+    (void)cap;
+    const int64_t TT = (int64_t)tiles_x(f.width) * tiles_y(f.height) * f.batch;
     char* p = static_cast<char*>(base);
     BinWs w;
     size_t off = 0;
-    w.keys_a = reinterpret_cast<uint32_t*>(p + off); off += align_up(sizeof(uint32_t) * (size_t)cap);
-    w.vals_a = reinterpret_cast<uint32_t*>(p + off); off += align_up(sizeof(uint32_t) * (size_t)cap);
-    w.hist = reinterpret_cast<uint32_t*>(p + off); off += align_up(sizeof(uint32_t) * (size_t)hist_words);
-    w.scan_ws = reinterpret_cast<uint32_t*>(p + off); off += align_up(sizeof(uint32_t) * scan_ws_words(scan_max));
+    // tile_count, fill and alloc_counter are adjacent: one memset clears them
+    w.tile_count = reinterpret_cast<uint32_t*>(p + off); off += sizeof(uint32_t) * (size_t)TT;
+    w.fill = reinterpret_cast<uint32_t*>(p + off); off += sizeof(uint32_t) * (size_t)TT;
+    w.alloc_counter = reinterpret_cast<uint32_t*>(p + off); off += align_up(sizeof(uint32_t));
+    w.scan_ws = reinterpret_cast<uint32_t*>(p + off); off += align_up(sizeof(uint32_t) * scan_ws_words(TT + 1));
     w.bytes = off;
     return w;
 }
+
+constexpr int64_t kOneCtaScanMax = 1 << 16;
 
 }  // namespace
 
 size_t bin_ws_bytes(int n, int64_t cap, const gi_frame& f) { return carve(nullptr, n, cap, f).bytes; }
 
+uint32_t* bin_tile_counts(void* ws, int n, int64_t cap, const gi_frame& f) {
+    return carve(ws, n, cap, f).tile_count;
+}
+
+uint32_t* bin_alloc_counter(void* ws, int n, int64_t cap, const gi_frame& f) {
+    return carve(ws, n, cap, f).alloc_counter;
+}
+
+cudaError_t bin_clear(void* ws, int n, int64_t cap, const gi_frame& f, cudaStream_t s) {
+    BinWs w = carve(ws, n, cap, f);
+    const size_t TT = (size_t)tiles_x(f.width) * tiles_y(f.height) * f.batch;
+    return cudaMemsetAsync(w.tile_count, 0, sizeof(uint32_t) * (2 * TT + 1), s);
+}
+
 cudaError_t launch_bin(const Proj* proj, const uint32_t* tiles_touched, int n, const gi_frame& f,
-                       int64_t cap, void* ws, uint32_t* gauss_offset, uint32_t* key_tile,
-                       uint32_t* key_gid, uint32_t* tile_range, uint32_t* n_keys, cudaStream_t s) {
+                       int64_t cap, void* ws, uint32_t* key_tile, uint32_t* key_gid,
+                       uint32_t* tile_range, uint32_t* n_keys, bool counted, bool sort,
+                       cudaStream_t s) {
     BinWs w = carve(ws, n, cap, f);
     const int total = n * f.batch;
-    const int T = tiles_x(f.width) * tiles_y(f.height);
-    const uint32_t TT = (uint32_t)T * (uint32_t)f.batch;
+    const int TX = tiles_x(f.width);
+    const int T = TX * tiles_y(f.height);
+    const int TT = T * f.batch;
     cudaError_t e;
-
-    // 1. offsets (gauss_offset[total] = K, also copied to n_keys)
-    e = scan_exclusive(tiles_touched, gauss_offset, total, nullptr, 1, w.scan_ws, n_keys, s);
-    if (e != cudaSuccess) return e;
-    // gauss_offset[total] = K: scan of a zero-extended input is not available,
-    // so write it from n_keys
-    e = cudaMemcpyAsync(gauss_offset + total, n_keys, sizeof(uint32_t), cudaMemcpyDeviceToDevice, s);
-    if (e != cudaSuccess) return e;
-
-    // 2. radix plan: ceil(log2(TT)) key bits in passes of <= 8 bits
-    int key_bits = 0;
-    while ((1u << key_bits) < TT) ++key_bits;
-    const int passes = (key_bits + 7) / 8;
-    const int pass_bits = passes ? (key_bits + passes - 1) / passes : 0;
-    // ping-pong so that the last pass lands in the caller's output
-    uint32_t* bufk[2] = {w.keys_a, key_tile};
-    uint32_t* bufv[2] = {w.vals_a, key_gid};
-    int cur = (passes % 2 == 0) ? 1 : 0;       // emission buffer
+    if (!counted) {
+        if ((e = bin_clear(ws, n, cap, f, s)) != cudaSuccess) return e;
+        if (total > 0) {
+            count_kernel<<<(total + 255) / 256, 256, 0, s>>>(proj, tiles_touched, total, n, T, TX,
+                                                             w.tile_count);
+            note_launches(1);
+            if ((e = cudaGetLastError()) != cudaSuccess) return e;
+        }
+    }
+    const bool fuse = TT <= kFusedScanMax && total > 0;
+    if (!fuse) {
+        if (TT <= kOneCtaScanMax) {
+            tile_scan_kernel<<<1, 1024, 0, s>>>(w.tile_count, TT, cap, tile_range, n_keys);
+            note_launches(1);
+        } else {
+            e = scan_exclusive(w.tile_count, tile_range, TT, nullptr, 1, w.scan_ws, n_keys, s);
+            if (e != cudaSuccess) return e;
+            e = cudaMemcpyAsync(tile_range + TT, n_keys, sizeof(uint32_t), cudaMemcpyDeviceToDevice, s);
+            if (e != cudaSuccess) return e;
+            clamp_kernel<<<(TT + 1 + 255) / 256, 256, 0, s>>>(tile_range, TT + 1, cap);
+            note_launches(1);
+        }
+        if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    }
     if (total > 0) {
-        duplicate_kernel<<<(total + 255) / 256, 256, 0, s>>>(proj, tiles_touched, gauss_offset, total,
-                                                             n, T, tiles_x(f.width), cap, bufk[cur],
-                                                             bufv[cur]);
+        scatter_kernel<<<(total + 255) / 256, 256, 0, s>>>(proj, tiles_touched, total, n, T, TX, TT,
+                                                           cap, fuse, w.tile_count, tile_range,
+                                                           n_keys, w.fill, key_tile, key_gid);
         note_launches(1);
         if ((e = cudaGetLastError()) != cudaSuccess) return e;
     }
-    const int64_t nc_max = max_chunks(cap);
-    for (int p = 0; p < passes; ++p) {
-        const int shift = p * pass_bits;
-        const int bits = (key_bits - shift) < pass_bits ? (key_bits - shift) : pass_bits;
-        if (nc_max > 0) {
-            radix_hist_kernel<<<(unsigned)nc_max, kRadixThreads, 0, s>>>(bufk[cur], n_keys, cap, shift,
-                                                                         bits, w.hist);
-            note_launches(1);
-            if ((e = cudaGetLastError()) != cudaSuccess) return e;
-        }
-        e = scan_exclusive_spec(w.hist, w.hist, nc_max * (int64_t)(1 << bits), n_keys, kChunk,
-                                1u << bits, cap, w.scan_ws, nullptr, s);
-        if (e != cudaSuccess) return e;
-        if (nc_max > 0) {
-            radix_scatter_kernel<<<(unsigned)nc_max, kRadixThreads, 0, s>>>(
-                bufk[cur], bufv[cur], bufk[cur ^ 1], bufv[cur ^ 1], n_keys, cap, shift, bits, w.hist);
-            note_launches(1);
-            if ((e = cudaGetLastError()) != cudaSuccess) return e;
-        }
-        cur ^= 1;
+    if (sort) {
+        segsort_kernel<<<TT, 256, 0, s>>>(proj, n, T, TX, tile_range, key_gid);
+        note_launches(1);
     }
-    // 3. ranges over the sorted keys
-    ranges_kernel<<<(unsigned)((cap + 1 + 255) / 256), 256, 0, s>>>(key_tile, n_keys, cap, TT,
-                                                                   tile_range);
-    note_launches(1);
     return cudaGetLastError();
 }
 

@@ -50,6 +50,25 @@ __device__ __forceinline__ unsigned lanemask_lt() {
     return m;
 }
 
+// Contiguous partial slots per Gaussian: returns this lane's offset after a
+// warp-aggregated atomic bump of *counter by cnt (all 32 lanes must call).
+// The slot ORDER across Gaussians is arbitrary, but every value written to a
+// slot and the order finalize sums a Gaussian's slots in are fixed, so the
+// gradients are deterministic.
+__device__ __forceinline__ uint32_t warp_alloc(uint32_t* counter, uint32_t cnt) {
+    const int lane = threadIdx.x & 31;
+    uint32_t x = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(kFull, x, o);
+        if (lane >= o) x += y;
+    }
+    uint32_t base = 0;
+    if (lane == 31 && x > 0) base = atomicAdd(counter, x);
+    base = __shfl_sync(kFull, base, 31);
+    return base + x - cnt;
+}
+
 // Generic device scan (u32, exclusive) over `count` elements, count either a
 // host constant or read from device memory.  Three launches, no inter-block
 // waiting.  ws needs scan_ws_words(max_count) u32.
@@ -73,28 +92,59 @@ void note_launches(int k);
 int64_t g_launches_get();
 
 // Internal launchers (api.cu validates arguments).
+// Optional fused outputs (null to skip): tile_count accumulates the per-tile
+// key counts of binning step 1 (zeroed first, see bin_clear); alloc_counter +
+// gauss_off allocate each Gaussian's contiguous backward partial slots.
+struct ProjectFuse {
+    uint32_t* step_counter;
+    uint32_t* tile_count;
+    uint32_t* alloc_counter;
+    uint32_t* gauss_off;
+};
 cudaError_t launch_project(const float* params, int n, const gi_frame& f, uint32_t flags,
-                           Proj* proj, uint32_t* tiles_touched, uint32_t* step_counter,
+                           Proj* proj, uint32_t* tiles_touched, const ProjectFuse& fuse,
                            cudaStream_t s);
+// counted: the per-tile counts in ws were already accumulated (fused project).
+// sort: run the per-tile gid sort (gi_bin contract); the fused consumers sort
+// in shared memory instead.
 cudaError_t launch_bin(const Proj* proj, const uint32_t* tiles_touched, int n, const gi_frame& f,
-                       int64_t cap, void* ws, uint32_t* gauss_offset, uint32_t* key_tile,
-                       uint32_t* key_gid, uint32_t* tile_range, uint32_t* n_keys, cudaStream_t s);
+                       int64_t cap, void* ws, uint32_t* key_tile, uint32_t* key_gid,
+                       uint32_t* tile_range, uint32_t* n_keys, bool counted, bool sort,
+                       cudaStream_t s);
 size_t bin_ws_bytes(int n, int64_t cap, const gi_frame& f);
-cudaError_t launch_render(const Proj* proj, const uint32_t* key_gid, const uint32_t* tile_range,
-                          int n, const gi_frame& f, float* image, cudaStream_t s);
+uint32_t* bin_tile_counts(void* ws, int n, int64_t cap, const gi_frame& f);
+uint32_t* bin_alloc_counter(void* ws, int n, int64_t cap, const gi_frame& f);
+cudaError_t bin_clear(void* ws, int n, int64_t cap, const gi_frame& f, cudaStream_t s);
+cudaError_t launch_render(const Proj* proj, uint32_t* key_gid, const uint32_t* tile_range, int n,
+                          const gi_frame& f, bool presorted, float* image, cudaStream_t s);
 size_t backward_ws_bytes(int n, int64_t cap, const gi_frame& f);
 cudaError_t launch_backward(const float* params, const Proj* proj, const uint32_t* key_gid,
-                            const uint32_t* tile_range, const uint32_t* gauss_offset, int n,
-                            const gi_frame& f, uint32_t flags, const float* dL_dimage,
-                            const float* target, int64_t cap, void* ws, float* grads, float* loss,
-                            float* image_out, cudaStream_t s);
-cudaError_t launch_backward_tiles(const Proj* proj, const uint32_t* key_gid,
-                                  const uint32_t* tile_range, const uint32_t* gauss_offset, int n,
-                                  const gi_frame& f, const float* dL_dimage, const float* target,
-                                  int64_t cap, void* ws, float* image_out, cudaStream_t s);
-cudaError_t launch_backward_finalize(const float* params, const uint32_t* gauss_offset, int n,
+                            const uint32_t* tile_range, int n, const gi_frame& f, uint32_t flags,
+                            const float* dL_dimage, const float* target, int64_t cap, void* ws,
+                            float* grads, float* loss, float* image_out, cudaStream_t s);
+cudaError_t launch_backward_alloc(const Proj* proj, int n, const gi_frame& f, int64_t cap, void* ws,
+                                  cudaStream_t s);
+uint32_t* backward_gauss_off(void* ws, int n, int64_t cap, const gi_frame& f);
+cudaError_t launch_backward_tiles(const Proj* proj, uint32_t* key_gid, const uint32_t* tile_range,
+                                  int n, const gi_frame& f, bool presorted,
+                                  const float* dL_dimage, const float* target, int64_t cap,
+                                  void* ws, float* image_out, cudaStream_t s);
+// Per-Gaussian reduction of the per-key partials + chain rule -> grads.  If
+// adam_m is non-null the Adam update (device step counter) is fused in.
+struct FusedAdam {
+    float* params;
+    float* m;
+    float* v;
+    const uint32_t* step_dev;
+    float lr0;
+    int half_every;
+    float b1, b2, eps;
+    uint32_t* flag;
+};
+cudaError_t launch_backward_finalize(const float* params, const Proj* proj, int n,
                                      const gi_frame& f, uint32_t flags, bool mse, int64_t cap,
-                                     void* ws, float* grads, float* loss, cudaStream_t s);
+                                     void* ws, float* grads, float* loss, const FusedAdam* adam,
+                                     cudaStream_t s);
 cudaError_t launch_adam(float* params, const float* grads, float* m, float* v, int64_t count,
                         int step, const uint32_t* step_dev, float lr, int half_every, float b1,
                         float b2, float eps, uint32_t* flag, cudaStream_t s);

@@ -16,15 +16,10 @@
 namespace gi {
 namespace {
 
-__global__ void __launch_bounds__(256) project_kernel(const float4* __restrict__ params, int n,
-                                                      int total, int W, int H, float k,
-                                                      uint32_t flags, Proj* __restrict__ proj,
-                                                      uint32_t* __restrict__ tiles_touched,
-                                                      uint32_t* step_counter) {
-    const int g = blockIdx.x * blockDim.x + threadIdx.x;
-    if (step_counter != nullptr && g == 0) *step_counter += 1u;   // fused fit: t <- t + 1
-    if (g >= total) return;
-    (void)n;
+__device__ __forceinline__ uint32_t project_one(const float4* __restrict__ params, int g, int n,
+                                                int W, int H, float k, uint32_t flags,
+                                                Proj* __restrict__ proj,
+                                                uint32_t* __restrict__ tile_count) {
     const float4 p0 = params[2 * (size_t)g];       // mux, muy, l1, l2
     const float4 p1 = params[2 * (size_t)g + 1];   // l3, c'r, c'g, c'b
 
@@ -72,6 +67,12 @@ __global__ void __launch_bounds__(256) project_kernel(const float4* __restrict__
             bx = (uint32_t)x0 | ((uint32_t)x1 << 16);
             by = (uint32_t)y0 | ((uint32_t)y1 << 16);
             touched = (uint32_t)((x1 / kTile - x0 / kTile + 1) * (y1 / kTile - y0 / kTile + 1));
+            if (tile_count != nullptr) {   // fused first step of binning: per-tile key counts
+                const int TX = (W + kTile - 1) / kTile;
+                uint32_t* tc = tile_count + (size_t)(g / n) * (size_t)(TX * ((H + kTile - 1) / kTile));
+                for (int ty = y0 / kTile; ty <= y1 / kTile; ++ty)
+                    for (int tx = x0 / kTile; tx <= x1 / kTile; ++tx) atomicAdd(&tc[ty * TX + tx], 1u);
+            }
         }
     }
     // Sigma^-1 = L^-T L^-1 with L^-1 = [[1/l1, 0], [-l2/(l1 l3), 1/l3]], scaled by
@@ -84,20 +85,36 @@ __global__ void __launch_bounds__(256) project_kernel(const float4* __restrict__
     r.q1 = make_float4(ca, cb, cc, __uint_as_float(bx));
     r.q2 = make_float4(p1.y, p1.z, p1.w, __uint_as_float(by));
     proj[g] = r;
-    tiles_touched[g] = touched;
+    return touched;
+}
+
+__global__ void __launch_bounds__(256) project_kernel(const float4* __restrict__ params, int n,
+                                                      int total, int W, int H, float k,
+                                                      uint32_t flags, Proj* __restrict__ proj,
+                                                      uint32_t* __restrict__ tiles_touched,
+                                                      ProjectFuse fuse) {
+    const int g = blockIdx.x * blockDim.x + threadIdx.x;
+    if (fuse.step_counter != nullptr && g == 0) *fuse.step_counter += 1u;   // fused fit: t <- t + 1
+    uint32_t touched = 0;
+    if (g < total) touched = project_one(params, g, n, W, H, k, flags, proj, fuse.tile_count);
+    if (g < total) tiles_touched[g] = touched;
+    if (fuse.gauss_off != nullptr) {                    // all lanes: warp-aggregated
+        const uint32_t off = warp_alloc(fuse.alloc_counter, touched);
+        if (g < total) fuse.gauss_off[g] = off;
+    }
 }
 
 }  // namespace
 
 cudaError_t launch_project(const float* params, int n, const gi_frame& f, uint32_t flags,
-                           Proj* proj, uint32_t* tiles_touched, uint32_t* step_counter,
+                           Proj* proj, uint32_t* tiles_touched, const ProjectFuse& fuse,
                            cudaStream_t s) {
     const int total = n * f.batch;
     const int blocks = (total + 255) / 256;
-    if (blocks == 0 && step_counter == nullptr) return cudaSuccess;
+    if (blocks == 0 && fuse.step_counter == nullptr) return cudaSuccess;
     project_kernel<<<blocks > 0 ? blocks : 1, 256, 0, s>>>(
         reinterpret_cast<const float4*>(params), n, total, f.width, f.height, f.k, flags, proj,
-        tiles_touched, step_counter);
+        tiles_touched, fuse);
     note_launches(1);
     return cudaGetLastError();
 }

@@ -1,24 +1,31 @@
-// Tile rasteriser building blocks shared by the forward (render.cu) and the
-// fused forward + L2 + backward (backward.cu) kernels.
+// Tile rasteriser building blocks shared by the forward (render.cu), the
+// fused forward + L2 + backward (backward.cu) and the binning (bin.cu)
+// kernels.
 //
 // CTA = one 16x16 tile of one image, 256 threads, one pixel per thread.
 // Warp w covers an 8x4 pixel block (w & 1 -> x half, w >> 1 -> y quarter), so
-// a warp can skip a Gaussian whose box misses its block (warp culling): at
-// the paper's init scale this evaluates ~3x fewer pairs than whole-tile
+// a warp skips a Gaussian whose box misses its block (warp culling): at the
+// paper's init scale this evaluates ~3x fewer pairs than whole-tile
 // evaluation.
 //
-// Per batch of up to 256 keys of the tile, each thread stages one record in
-// shared memory, converted to TILE-LOCAL coordinates:
+// The tile's key segment is first brought into ascending-gid order in shared
+// memory (the scatter of binning leaves it unordered; see bin.cu), then, per
+// batch of up to 256 keys, each thread stages one record converted to
+// TILE-LOCAL coordinates:
 //   rA = {mx, my, a, b}   centre minus the tile origin, fp32 (ix - tx0 is an
 //                         exact small integer, + fx rounds once)
 //   rB = {c, c'r, c'g, c'b}
 //   rC = {x0, x1 - x0, y0, y1 - y0}   integer box, global pixels
-// so that a pair costs dx = (lx + 1/2) - mx (one FADD, no int->float
-// conversion) and an unsigned range test per axis.
+// Each warp then compacts the batch into its own candidate list: record
+// index + the 32-bit mask of its lanes whose pixel lies in the box, so the
+// inner loop needs no bit scanning and a one-instruction box test.
 #pragma once
 #include "gi_internal.cuh"
 
 namespace gi {
+
+constexpr int kSortMax = 2048;      // segments sorted in shared memory (8 KB)
+constexpr int kRankMax = 256;       // rank sort up to this size, bitonic above
 
 struct TileCtx {
     int img, tile, tx, ty;        // tile coordinates
@@ -55,34 +62,53 @@ struct StagedRecords {
     int4 c[256];
 };
 
-// Stage key j = threadIdx.x of [base, base + cnt) into shared memory.
-__device__ __forceinline__ void stage_record(StagedRecords& sr, const Proj* __restrict__ proj,
-                                             const uint32_t* __restrict__ key_gid, uint32_t base,
-                                             int cnt, const TileCtx& t, uint32_t* gid_out) {
-    const int j = threadIdx.x;
-    if (j < cnt) {
-        const uint32_t gid = key_gid[base + j];
-        const Proj r = proj[gid];
-        const int ix = __float_as_int(r.q0.x), iy = __float_as_int(r.q0.y);
-        const float mx = __fadd_rn((float)(ix - t.tx * kTile), r.q0.z);
-        const float my = __fadd_rn((float)(iy - t.ty * kTile), r.q0.w);
-        const uint32_t bx = __float_as_uint(r.q1.w), by = __float_as_uint(r.q2.w);
-        const int x0 = (int)(bx & 0xffffu), x1 = (int)(bx >> 16);
-        const int y0 = (int)(by & 0xffffu), y1 = (int)(by >> 16);
-        sr.a[j] = make_float4(mx, my, r.q1.x, r.q1.y);
-        sr.b[j] = make_float4(r.q1.z, r.q2.x, r.q2.y, r.q2.z);
-        sr.c[j] = make_int4(x0, x1 - x0, y0, y1 - y0);
-        if (gid_out) *gid_out = gid;
+// Per-warp compacted candidate list for one batch: (record index, lane mask).
+struct WarpLists {
+    uint2 ent[kWarps][256];
+    int cnt[kWarps];
+};
+
+// Stage record j = threadIdx.x (j < cnt) for gid into shared memory.
+__device__ __forceinline__ void stage_gid(StagedRecords& sr, const Proj* __restrict__ proj,
+                                          uint32_t gid, int j, const TileCtx& t) {
+    const Proj r = proj[gid];
+    const int ix = __float_as_int(r.q0.x), iy = __float_as_int(r.q0.y);
+    const float mx = __fadd_rn((float)(ix - t.tx * kTile), r.q0.z);
+    const float my = __fadd_rn((float)(iy - t.ty * kTile), r.q0.w);
+    const uint32_t bx = __float_as_uint(r.q1.w), by = __float_as_uint(r.q2.w);
+    const int x0 = (int)(bx & 0xffffu), x1 = (int)(bx >> 16);
+    const int y0 = (int)(by & 0xffffu), y1 = (int)(by >> 16);
+    sr.a[j] = make_float4(mx, my, r.q1.x, r.q1.y);
+    sr.b[j] = make_float4(r.q1.z, r.q2.x, r.q2.y, r.q2.z);
+    sr.c[j] = make_int4(x0, x1 - x0, y0, y1 - y0);
+}
+
+// Lanes of the 8x4 warp block (lane = ly * 8 + lx) inside box b.
+__device__ __forceinline__ uint32_t warp_box_mask(const int4 b, int wx0, int wy0) {
+    const int lo_x = max(b.x - wx0, 0), hi_x = min(b.x + b.y - wx0, 7);
+    const int lo_y = max(b.z - wy0, 0), hi_y = min(b.z + b.w - wy0, 3);
+    if (lo_x > hi_x || lo_y > hi_y) return 0u;
+    const uint32_t row = ((1u << (hi_x + 1)) - 1u) & ~((1u << lo_x) - 1u);
+    uint32_t m = 0u;
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+        if (r >= lo_y && r <= hi_y) m |= row << (8 * r);
+    return m;
+}
+
+// Build this warp's candidate list for a staged batch of cnt records.
+__device__ __forceinline__ int build_warp_list(const StagedRecords& sr, WarpLists& wl, int cnt,
+                                               const TileCtx& t) {
+    int n = 0;
+    for (int q = 0; q < cnt; q += 32) {
+        const int j = q + t.lane;
+        const uint32_t m = j < cnt ? warp_box_mask(sr.c[j], t.wx0, t.wy0) : 0u;
+        const unsigned hit = __ballot_sync(kFull, m != 0u);
+        if (m != 0u) wl.ent[t.warp][n + __popc(hit & lanemask_lt())] = make_uint2((uint32_t)j, m);
+        n += __popc(hit);
     }
-}
-
-// Does staged record j's box overlap this warp's 8x4 block?
-__device__ __forceinline__ bool warp_overlaps(const int4 b, const TileCtx& t) {
-    return (b.x <= t.wx0 + 7) && (b.x + b.y >= t.wx0) && (b.z <= t.wy0 + 3) && (b.z + b.w >= t.wy0);
-}
-
-__device__ __forceinline__ bool pixel_in_box(const int4 b, const TileCtx& t) {
-    return ((unsigned)(t.x - b.x) <= (unsigned)b.y) & ((unsigned)(t.y - b.z) <= (unsigned)b.w);
+    __syncwarp();
+    return n;
 }
 
 // exp(-sigma) for the staged record (factored conic, MUFU.EX2), and the
@@ -99,6 +125,106 @@ __device__ __forceinline__ PairEval eval_pair(const float4 A, const float4 B, co
     e.v = fmaf(A.w, dx, B.x * dy);
     e.w = ex2_approx(fmaf(-e.u, e.u, -(e.v * e.v)));
     return e;
+}
+
+// Accumulate Eq. 7 for this thread's pixel over the warp's candidate list
+// (ascending record index = ascending gid).
+__device__ __forceinline__ void forward_batch(const StagedRecords& sr, const WarpLists& wl, int n,
+                                              const TileCtx& t, float& acc0, float& acc1,
+                                              float& acc2) {
+    const uint2* ent = wl.ent[t.warp];
+#pragma unroll 2
+    for (int k = 0; k < n; ++k) {
+        const uint2 en = ent[k];
+        const float4 A = sr.a[en.x];
+        const float4 B = sr.b[en.x];
+        const PairEval pe = eval_pair(A, B, t);
+        const float w = (en.y >> t.lane) & 1u ? pe.w : 0.f;
+        acc0 = fmaf(B.y, w, acc0);
+        acc1 = fmaf(B.z, w, acc1);
+        acc2 = fmaf(B.w, w, acc2);
+    }
+}
+
+// ----------------------------------------------------- segment ordering
+// Bring the tile's key segment [s, e) into ascending gid order.  Returns the
+// segment length if it now sits sorted in `sl` (shared, kSortMax entries), or
+// -1 if it was longer than kSortMax and was rebuilt IN ORDER directly in the
+// global key_gid segment (stable scan of all Gaussians of the image).
+// Gids within a segment are distinct.  All threads of the CTA must call.
+__device__ __forceinline__ bool covers_tile(const Proj* __restrict__ proj, uint32_t g, int tx,
+                                            int ty) {
+    const uint32_t bx = __float_as_uint(proj[g].q1.w), by = __float_as_uint(proj[g].q2.w);
+    const int x0 = (int)(bx & 0xffffu), x1 = (int)(bx >> 16);
+    const int y0 = (int)(by & 0xffffu), y1 = (int)(by >> 16);
+    return x0 <= x1 && y0 <= y1 && x0 / kTile <= tx && x1 / kTile >= tx && y0 / kTile <= ty &&
+           y1 / kTile >= ty;
+}
+
+__device__ __forceinline__ int sorted_segment(const Proj* __restrict__ proj,
+                                              uint32_t* __restrict__ key_gid, uint32_t s,
+                                              uint32_t e, int n, int img, int tx, int ty,
+                                              uint32_t* sl, uint32_t* scratch8) {
+    const int cnt = (int)(e - s);
+    if (cnt <= kRankMax) {
+        uint32_t mine = 0xffffffffu;
+        if ((int)threadIdx.x < cnt) mine = key_gid[s + threadIdx.x];
+        sl[threadIdx.x] = mine;
+        __syncthreads();
+        int r = 0;
+        if ((int)threadIdx.x < cnt)
+            for (int k = 0; k < cnt; ++k) r += sl[k] < mine;
+        __syncthreads();
+        if ((int)threadIdx.x < cnt) sl[r] = mine;
+        __syncthreads();
+        return cnt;
+    }
+    if (cnt <= kSortMax) {
+        int P = 512;
+        while (P < cnt) P <<= 1;
+        for (int i = threadIdx.x; i < P; i += blockDim.x) sl[i] = i < cnt ? key_gid[s + i] : 0xffffffffu;
+        __syncthreads();
+        for (int k = 2; k <= P; k <<= 1) {
+            for (int j = k >> 1; j > 0; j >>= 1) {
+                for (int i = threadIdx.x; i < P; i += blockDim.x) {
+                    const int l = i ^ j;
+                    if (l > i) {
+                        const uint32_t a = sl[i], b = sl[l];
+                        if ((a > b) == ((i & k) == 0)) {
+                            sl[i] = b;
+                            sl[l] = a;
+                        }
+                    }
+                }
+                __syncthreads();
+            }
+        }
+        return cnt;
+    }
+    // pathological segment: stable in-order rebuild in global memory
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint32_t out = 0;
+    for (int base = 0; base < n; base += blockDim.x) {
+        const int g = base + threadIdx.x;
+        const bool hit = g < n && covers_tile(proj, (uint32_t)(img * n + g), tx, ty);
+        const unsigned m = __ballot_sync(kFull, hit);
+        if (lane == 0) scratch8[warp] = __popc(m);
+        __syncthreads();
+        uint32_t before = 0, tot = 0;
+        for (int w = 0; w < kWarps; ++w) {
+            before += w < warp ? scratch8[w] : 0u;
+            tot += scratch8[w];
+        }
+        if (hit) {
+            const uint32_t slot = s + out + before + __popc(m & lanemask_lt());
+            if (slot < e) key_gid[slot] = (uint32_t)(img * n + g);
+        }
+        out += tot;
+        __syncthreads();
+    }
+    __threadfence_block();
+    __syncthreads();
+    return -1;
 }
 
 }  // namespace gi

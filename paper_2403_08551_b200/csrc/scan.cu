@@ -1,5 +1,5 @@
-// Exclusive prefix sum over u32, used by binning (gauss_offset = scan of
-// tiles_touched) and by each radix pass (digit-major block histograms).
+// Exclusive prefix sum over u32, used by binning when the tile count is too
+// large for the one-CTA tile scan (batched launches).
 // Reduce-then-scan: per-tile reduction, one-block scan of tile sums,
 // per-tile downsweep.  No block ever waits on another (no look-back spin), so
 // nothing can deadlock; the element count may live on the device (it is the

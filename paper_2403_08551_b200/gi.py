@@ -58,10 +58,10 @@ SIGNATURES = {
     "gi_proj_bytes": (_sz, [_i32, _FP]),
     "gi_project": (C.c_int, [_vp, _i32, _FP, _u32, _vp, _vp, _vp]),
     "gi_bin_workspace_bytes": (_sz, [_i32, _i64, _FP]),
-    "gi_bin": (C.c_int, [_vp, _vp, _i32, _FP, _i64, _vp, _sz, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "gi_bin": (C.c_int, [_vp, _vp, _i32, _FP, _i64, _vp, _sz, _vp, _vp, _vp, _vp, _vp]),
     "gi_render": (C.c_int, [_vp, _vp, _vp, _i32, _FP, _vp, _vp]),
     "gi_backward_workspace_bytes": (_sz, [_i32, _i64, _FP]),
-    "gi_render_backward": (C.c_int, [_vp, _vp, _vp, _vp, _vp, _i32, _FP, _u32, _vp, _vp, _i64,
+    "gi_render_backward": (C.c_int, [_vp, _vp, _vp, _vp, _i32, _FP, _u32, _vp, _vp, _i64,
                                      _vp, _sz, _vp, _vp, _vp, _vp]),
     "gi_adam_step": (C.c_int, [_vp, _vp, _vp, _vp, _i64, _i32, _f32, _f32, _f32, _f32, _vp, _vp]),
     "gi_lr_at": (_f64, [_i32, _f64, _i32]),
@@ -70,6 +70,7 @@ SIGNATURES = {
     "gi_fit_step": (C.c_int, [_vp, _vp, _vp, _vp, _vp, _i32, _FP, _u32, _i64, _vp, _sz, _vp,
                               _f32, _i32, _f32, _f32, _f32, _vp, _vp, _vp, _vp]),
     "gi_launch_count": (_i64, []),
+    "gi_render_frame": (C.c_int, [_vp, _i32, _FP, _u32, _i64, _vp, _sz, _vp, _vp]),
     "gi_vq_decode": (C.c_int, [_vp, _sz, C.POINTER(gi_codec_meta), _vp, _vp]),
     "gi_psnr_workspace_bytes": (_sz, [_FP]),
     "gi_psnr": (C.c_int, [_vp, _vp, _FP, _vp, _vp, _vp]),
@@ -169,12 +170,11 @@ def gi_project(params, n, f, flags, proj, tiles_touched, stream=None):
                           _ptr(tiles_touched), _stream(stream)), "gi_project")
 
 
-def gi_bin(proj, tiles_touched, n, f, key_capacity, ws, gauss_offset, key_tile, key_gid,
-           tile_range, n_keys, stream=None):
+def gi_bin(proj, tiles_touched, n, f, key_capacity, ws, key_tile, key_gid, tile_range, n_keys,
+           stream=None):
     _ok(load().gi_bin(_ptr(proj), _ptr(tiles_touched), int(n), C.byref(f), int(key_capacity),
-                      _ptr(ws), ws.numel() * ws.element_size(), _ptr(gauss_offset),
-                      _ptr(key_tile), _ptr(key_gid), _ptr(tile_range), _ptr(n_keys),
-                      _stream(stream)), "gi_bin")
+                      _ptr(ws), ws.numel() * ws.element_size(), _ptr(key_tile), _ptr(key_gid),
+                      _ptr(tile_range), _ptr(n_keys), _stream(stream)), "gi_bin")
 
 
 def gi_render(proj, key_gid, tile_range, n, f, image, stream=None):
@@ -182,10 +182,10 @@ def gi_render(proj, key_gid, tile_range, n, f, image, stream=None):
                          _ptr(image), _stream(stream)), "gi_render")
 
 
-def gi_render_backward(params, proj, key_gid, tile_range, gauss_offset, n, f, flags, dL_dimage,
-                       target, key_capacity, ws, grads, loss=None, image_out=None, stream=None):
+def gi_render_backward(params, proj, key_gid, tile_range, n, f, flags, dL_dimage, target,
+                       key_capacity, ws, grads, loss=None, image_out=None, stream=None):
     _ok(load().gi_render_backward(_ptr(params), _ptr(proj), _ptr(key_gid), _ptr(tile_range),
-                                  _ptr(gauss_offset), int(n), C.byref(f), int(flags),
+                                  int(n), C.byref(f), int(flags),
                                   _ptr(dL_dimage), _ptr(target), int(key_capacity), _ptr(ws),
                                   ws.numel() * ws.element_size(), _ptr(grads), _ptr(loss),
                                   _ptr(image_out), _stream(stream)), "gi_render_backward")
@@ -212,6 +212,12 @@ def gi_fit_step(params, grads, m, v, target, n, f, flags, key_capacity, fit_ws, 
                            fit_ws.numel() * fit_ws.element_size(), _ptr(step_counter),
                            float(lr0), int(half_every), float(beta1), float(beta2), float(eps),
                            _ptr(loss), _ptr(status_flags), ev, _stream(stream)), "gi_fit_step")
+
+
+def gi_render_frame(params, n, f, flags, key_capacity, frame_ws, image, stream=None):
+    _ok(load().gi_render_frame(_ptr(params), int(n), C.byref(f), int(flags), int(key_capacity),
+                               _ptr(frame_ws), frame_ws.numel() * frame_ws.element_size(),
+                               _ptr(image), _stream(stream)), "gi_render_frame")
 
 
 def gi_launch_count() -> int:

@@ -41,7 +41,6 @@ class Pipeline:
         tot = self.n * self.B
         self.proj = torch.zeros(max(tot, 1) * gi.GI_PROJ_BYTES // 4, dtype=torch.float32, device=d)
         self.tiles_touched = _u32(tot, d)
-        self.gauss_offset = _u32(tot + 1, d)
         self.key_tile = _u32(self.cap, d)
         self.key_gid = _u32(self.cap, d)
         self.tile_range = _u32(self.T * self.B + 1, d)
@@ -61,8 +60,7 @@ class Pipeline:
 
     def bin(self, stream=None):
         gi.gi_bin(self.proj, self.tiles_touched, self.n, self.f, self.cap, self.bin_ws,
-                  self.gauss_offset, self.key_tile, self.key_gid, self.tile_range, self.n_keys,
-                  stream)
+                  self.key_tile, self.key_gid, self.tile_range, self.n_keys, stream)
 
     def raster(self, stream=None):
         gi.gi_render(self.proj, self.key_gid, self.tile_range, self.n, self.f, self.image, stream)
@@ -74,10 +72,23 @@ class Pipeline:
         self.raster(stream)
         return self.image
 
+    def render_frame(self, params, flags=gi.GI_POS_LOGIT, stream=None) -> torch.Tensor:
+        """Fused gi_render_frame (project + counts -> bin -> render with the
+        per-tile ordering inside the render kernel) into self.image."""
+        if not hasattr(self, "frame_ws"):
+            self.frame_ws = _bytes(gi.gi_fit_workspace_bytes(self.n, self.cap, self.f), self.device)
+        gi.gi_render_frame(params, self.n, self.f, flags, self.cap, self.frame_ws, self.image, stream)
+        return self.image
+
+    def frame_keys(self) -> int:
+        ptr = gi.gi_fit_n_keys(self.frame_ws, self.n, self.cap, self.f)
+        off = (ptr - self.frame_ws.data_ptr()) // 4
+        return int(self.frame_ws.view(torch.int32)[off].item()) & 0xffffffff
+
     def backward(self, params, target=None, dL_dimage=None, flags=gi.GI_POS_LOGIT,
                  image_out=None, stream=None) -> torch.Tensor:
         """Fused forward + L2 + backward on the current bins (after project/bin)."""
-        gi.gi_render_backward(params, self.proj, self.key_gid, self.tile_range, self.gauss_offset,
+        gi.gi_render_backward(params, self.proj, self.key_gid, self.tile_range,
                               self.n, self.f, flags, dL_dimage, target, self.cap, self.bwd_ws,
                               self.grads, self.loss if dL_dimage is None else None, image_out,
                               stream)

@@ -38,7 +38,7 @@ def test_host_queries_and_validation(lib):
     f = gi.frame(768, 512)
     assert gi.gi_num_tiles(f) == 48 * 32
     assert gi.gi_proj_bytes(70000, f) == 70000 * 48
-    assert gi.gi_bin_workspace_bytes(70000, 1 << 20, f) > 8 * (1 << 20)
+    assert gi.gi_bin_workspace_bytes(70000, 1 << 20, f) >= 2 * 4 * 1536   # counts + cursors
     assert gi.gi_backward_workspace_bytes(70000, 1 << 20, f) >= 32 * (1 << 20)
     assert gi.gi_lr_at(1) == 1e-3 and gi.gi_lr_at(20001) == 5e-4 and gi.gi_lr_at(40001) == 2.5e-4
     bad = gi.frame(768, 512, tile=8)

@@ -24,9 +24,10 @@ if [ $rc -eq 0 ] && [ "${SKIP_NCU:-0}" != "1" ]; then
   timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
       --log-file $OUT/${TAG}_launches.csv $PCMD > $OUT/${TAG}_ncu_list.log 2>&1
   echo "ncu list rc=$?"
-  timeout 900 ncu --set full --clock-control none --import-source on \
-      -k regex:${NCU_KERNEL:-backward_tile} -s ${NCU_SKIP:-3} -c ${NCU_COUNT:-1} \
-      -o $OUT/${TAG}_prof $PCMD > $OUT/${TAG}_ncu_full.log 2>&1
-  echo "ncu full rc=$?"
-  tail -3 $OUT/${TAG}_ncu_full.log
+  for K in ${NCU_KERNELS:-backward_tile render_kernel}; do
+    timeout 900 ncu --set full --clock-control none --import-source on \
+        -k regex:$K -s ${NCU_SKIP:-2} -c 1 \
+        -o $OUT/${TAG}_prof_$K $PCMD > $OUT/${TAG}_ncu_full_$K.log 2>&1
+    echo "ncu full $K rc=$?"
+  done
 fi
