@@ -197,6 +197,7 @@ def main():
 
     import synth
     from paper_2403_08551_b200 import gi
+    from paper_2403_08551_b200.dist import gather_psnr
     from paper_2403_08551_b200.pipeline import Fitter, Pipeline
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -373,12 +374,8 @@ def main():
     # ---------------- quality + the one collective (NCCL all-gather of PSNR) ----
     img = pipe.render_frame(fit.params)
     psnr = pipe.psnr(img, target).clone()
-    if world > 1:
-        allp = [torch.zeros_like(psnr) for _ in range(world)]
-        dist.all_gather(allp, psnr)
-        psnrs = [float(x.item()) for x in allp]
-    else:
-        psnrs = [float(psnr.item())]
+    # the one collective of the path: NCCL all-gather of per-image PSNR
+    psnrs = gather_psnr(psnr, world, world, rank).tolist()
 
     if rank == 0:
         pk, pk_kind = peaks()
