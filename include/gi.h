@@ -156,7 +156,9 @@ double gi_lr_at(int32_t step, double lr0, int32_t half_every);
  * the projection kernel, then used for the bias correction and
  * lr_t = lr0 * 0.5^floor((t-1)/half_every)).
  *   fit_ws        gi_fit_workspace_bytes() bytes: holds proj, tiles_touched,
- *                 keys, ranges, n_keys and both stage workspaces
+ *                 keys, ranges, n_keys and both stage workspaces.  MUST be
+ *                 zero-filled once before its first use (it carries per-tile
+ *                 counters that every fused call leaves zeroed for the next)
  *   loss          [B] fp32 out (L2 loss of the step's forward), may be NULL
  *   status_flags  device u32, bit 0 set on a non-finite parameter, may be NULL
  *   stage_events  NULL, or 6 cudaEvent_t (as void*) recorded (external) at
@@ -173,7 +175,8 @@ gi_status gi_fit_step(float* params, float* grads, float* m, float* v, const flo
 /* --- fused render of a frame (graph-capturable) ---------------------------
  * project (+ per-tile counts) -> bin -> Eq. 7 render in one call; the per-tile
  * gid ordering of binning happens inside the render kernel.  Same workspace
- * layout and size as gi_fit_step (gi_fit_workspace_bytes); n_keys for
+ * layout, size and zero-fill rule as gi_fit_step (gi_fit_workspace_bytes);
+ * consecutive kernels overlap via programmatic dependent launch; n_keys for
  * gi_check via gi_fit_n_keys(frame_ws, ...).  image [B][3][H][W] out. */
 gi_status gi_render_frame(const float* params, int32_t n, const gi_frame* f, uint32_t flags,
                           int64_t key_capacity, void* frame_ws, size_t ws_bytes, float* image,

@@ -3,6 +3,7 @@
 // except in gi_check.
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 
 #include "gi_internal.cuh"
@@ -12,6 +13,13 @@ namespace {
 thread_local int64_t g_launches = 0;
 }
 void note_launches(int k) { g_launches += k; }
+bool use_pdl() {
+    static const bool on = [] {
+        const char* e = std::getenv("GI_NO_PDL");
+        return !(e && e[0] == '1');
+    }();
+    return on;
+}
 int64_t g_launches_get() { return g_launches; }
 }  // namespace gi
 
@@ -144,7 +152,7 @@ gi_status gi_bin(const void* proj, const uint32_t* tiles_touched, int32_t n, con
         return invalid("NULL buffer");
     return cuda_status(gi::launch_bin(static_cast<const gi::Proj*>(proj), tiles_touched, n, *f,
                                       key_capacity, ws, key_tile, key_gid, tile_range, n_keys,
-                                      false, true, S(stream)),
+                                      false, true, nullptr, S(stream)),
                        "gi_bin");
 }
 
@@ -156,7 +164,7 @@ gi_status gi_render(const void* proj, const uint32_t* key_gid, const uint32_t* t
     // gi_bin output is already in gid order: presorted, key_gid only read
     return cuda_status(gi::launch_render(static_cast<const gi::Proj*>(proj),
                                          const_cast<uint32_t*>(key_gid), tile_range, n, *f, true,
-                                         image, S(stream)),
+                                         image, gi::ChainState{}, S(stream)),
                        "gi_render");
 }
 
@@ -243,19 +251,21 @@ gi_status gi_fit_step(float* params, float* grads, float* m, float* v, const flo
     cudaError_t e;
 #define GI_TRY(expr, where) \
     if ((e = (expr)) != cudaSuccess) return cuda_status(e, where)
+    // The per-tile counters in the workspace are zero on entry (zero-filled
+    // workspace, then left zeroed by the consumer tile kernel of each call).
+    uint32_t* gauss_off = gi::backward_gauss_off(w.bwd_ws, n, key_capacity, *f);
+    const gi::ChainState cs = gi::bin_chain_state(w.bin_ws, n, key_capacity, *f, gauss_off);
     GI_TRY(record_stage(stage_events, 0, s), "gi_fit_step/event");
-    GI_TRY(gi::bin_clear(w.bin_ws, n, key_capacity, *f, s), "gi_fit_step/clear");
-    gi::ProjectFuse pf{step_counter, gi::bin_tile_counts(w.bin_ws, n, key_capacity, *f),
-                       gi::bin_alloc_counter(w.bin_ws, n, key_capacity, *f),
-                       gi::backward_gauss_off(w.bwd_ws, n, key_capacity, *f)};
-    GI_TRY(gi::launch_project(params, n, *f, flags, w.proj, w.touched, pf, s), "gi_fit_step/project");
+    GI_TRY(gi::launch_project(params, n, *f, flags, w.proj, w.touched,
+                              gi::ProjectFuse{step_counter, cs.tile_count}, s),
+           "gi_fit_step/project");
     GI_TRY(record_stage(stage_events, 1, s), "gi_fit_step/event");
     GI_TRY(gi::launch_bin(w.proj, w.touched, n, *f, key_capacity, w.bin_ws, w.key_tile, w.key_gid,
-                          w.tile_range, w.n_keys, true, false, s),
+                          w.tile_range, w.n_keys, true, false, gauss_off, s),
            "gi_fit_step/bin");
     GI_TRY(record_stage(stage_events, 2, s), "gi_fit_step/event");
     GI_TRY(gi::launch_backward_tiles(w.proj, w.key_gid, w.tile_range, n, *f, false, nullptr, target,
-                                     key_capacity, w.bwd_ws, nullptr, s),
+                                     key_capacity, w.bwd_ws, nullptr, cs, s),
            "gi_fit_step/backward");
     GI_TRY(record_stage(stage_events, 3, s), "gi_fit_step/event");
     gi::FusedAdam fa{params, m, v, step_counter, lr0, half_every, beta1, beta2, eps, status_flags};
@@ -286,15 +296,14 @@ gi_status gi_render_frame(const float* params, int32_t n, const gi_frame* f, uin
     cudaError_t e;
 #define GI_TRY(expr, where) \
     if ((e = (expr)) != cudaSuccess) return cuda_status(e, where)
-    GI_TRY(gi::bin_clear(w.bin_ws, n, key_capacity, *f, s), "gi_render_frame/clear");
-    gi::ProjectFuse pf{nullptr, gi::bin_tile_counts(w.bin_ws, n, key_capacity, *f), nullptr,
-                       nullptr};
-    GI_TRY(gi::launch_project(params, n, *f, flags, w.proj, w.touched, pf, s),
+    const gi::ChainState cs = gi::bin_chain_state(w.bin_ws, n, key_capacity, *f, nullptr);
+    GI_TRY(gi::launch_project(params, n, *f, flags, w.proj, w.touched,
+                              gi::ProjectFuse{nullptr, cs.tile_count}, s),
            "gi_render_frame/project");
     GI_TRY(gi::launch_bin(w.proj, w.touched, n, *f, key_capacity, w.bin_ws, w.key_tile, w.key_gid,
-                          w.tile_range, w.n_keys, true, false, s),
+                          w.tile_range, w.n_keys, true, false, nullptr, s),
            "gi_render_frame/bin");
-    GI_TRY(gi::launch_render(w.proj, w.key_gid, w.tile_range, n, *f, false, image, s),
+    GI_TRY(gi::launch_render(w.proj, w.key_gid, w.tile_range, n, *f, false, image, cs, s),
            "gi_render_frame/render");
 #undef GI_TRY
     return GI_OK;

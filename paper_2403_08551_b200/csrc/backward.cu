@@ -36,6 +36,8 @@ struct BwdShared {
     uint32_t slot[256];      // partial slot of each staged record
     uint32_t scratch[kWarps];
     float sse[kWarps];
+    uint32_t hist[256];      // pass-2 work histogram (descending work order)
+    uint32_t perm[256];      // pass-2 lane group -> record
 };
 
 __global__ void __launch_bounds__(256) backward_tile_kernel(
@@ -43,9 +45,17 @@ __global__ void __launch_bounds__(256) backward_tile_kernel(
     const uint32_t* __restrict__ tile_range, const uint32_t* __restrict__ gauss_off, int n,
     int W, int H, int T, int TX, bool presorted, const float* __restrict__ dL_dimage,
     const float* __restrict__ target, float norm, int64_t cap, float* __restrict__ partial,
-    float* __restrict__ sse_part, float* __restrict__ image_out) {
+    float* __restrict__ sse_part, float* __restrict__ image_out, ChainState cs) {
     __shared__ BwdShared sh;
     const TileCtx t = make_tile_ctx(W, H, TX);
+    griddep_wait();
+    griddep_trigger();
+    if (threadIdx.x == 0 && cs.tile_count != nullptr) {   // leave the counters zero for the next call
+        const int tt = t.img * T + t.tile;
+        cs.tile_count[tt] = 0u;
+        cs.fill[tt] = 0u;
+        if (tt == 0 && cs.alloc_counter != nullptr) *cs.alloc_counter = 0u;
+    }
     const uint32_t s = tile_range[t.img * T + t.tile];
     const uint32_t e = tile_range[t.img * T + t.tile + 1];
     const uint32_t L = e - s;
@@ -126,7 +136,40 @@ __global__ void __launch_bounds__(256) backward_tile_kernel(
         // q lanes per Gaussian (power of two, <= 8, q * cnt <= 256)
         int q = 1;
         while (q < 8 && q * 2 * cnt <= 256) q <<= 1;
-        const int j = threadIdx.x / q;          // Gaussian of this lane
+        // Lane groups take the Gaussians in descending order of per-lane work
+        // (rows per lane x row width) so that the lanes of a warp finish
+        // together: counting sort on the work (256 bins, shared memory).
+        sh.hist[threadIdx.x] = 0u;
+        __syncthreads();
+        uint32_t bin = 0;
+        if ((int)threadIdx.x < cnt) {
+            const int4 b = sh.sr.c[threadIdx.x];
+            const int wdt = min(b.x + b.y - tx0, kTile - 1) - max(b.x - tx0, 0) + 1;
+            const int hgt = min(b.z + b.w - ty0, kTile - 1) - max(b.z - ty0, 0) + 1;
+            bin = 255u - (uint32_t)min(255, ((hgt + q - 1) / q) * wdt);
+            atomicAdd(&sh.hist[bin], 1u);
+        }
+        __syncthreads();
+        {
+            const uint32_t v = sh.hist[threadIdx.x];
+            uint32_t x = v;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(kFull, x, o);
+                if (t.lane >= o) x += y;
+            }
+            if (t.lane == 31) sh.scratch[t.warp] = x;
+            __syncthreads();
+            uint32_t before = 0;
+#pragma unroll
+            for (int w = 0; w < kWarps; ++w) before += w < t.warp ? sh.scratch[w] : 0u;
+            sh.hist[threadIdx.x] = before + x - v;            // exclusive start of the bin
+        }
+        __syncthreads();
+        if ((int)threadIdx.x < cnt) sh.perm[atomicAdd(&sh.hist[bin], 1u)] = threadIdx.x;
+        __syncthreads();
+        const int kk = threadIdx.x / q;         // lane group (work rank)
+        const int j = kk < cnt ? (int)sh.perm[kk] : cnt;   // Gaussian of this lane
         const int ph = threadIdx.x % q;         // row phase
         float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f, a4 = 0.f, a5 = 0.f, a6 = 0.f, a7 = 0.f;
         if (j < cnt) {
@@ -215,8 +258,25 @@ __device__ __forceinline__ float adam1(float p, float g, float& m, float& v, flo
 __global__ void __launch_bounds__(256) finalize_kernel(
     const float4* __restrict__ params, const Proj* __restrict__ proj,
     const uint32_t* __restrict__ gauss_off, int total, int W, int H, uint32_t flags, int64_t cap,
-    const float* __restrict__ partial, float4* __restrict__ grads, FusedAdam adam) {
+    const float* __restrict__ partial, float4* __restrict__ grads, FusedAdam adam,
+    const float* __restrict__ sse_part, int T, int batch, double inv_count,
+    float* __restrict__ loss) {
     __shared__ float sconst[3];
+    __shared__ double lsum[256];
+    griddep_wait();
+    griddep_trigger();
+    if (loss != nullptr && blockIdx.x < batch) {
+        // per-image L2 loss: fixed-order reduction of the per-tile partials
+        double acc = 0.0;
+        for (int i = threadIdx.x; i < T; i += blockDim.x) acc += (double)sse_part[blockIdx.x * T + i];
+        lsum[threadIdx.x] = acc;
+        __syncthreads();
+        for (int o = 128; o > 0; o >>= 1) {
+            if ((int)threadIdx.x < o) lsum[threadIdx.x] += lsum[threadIdx.x + o];
+            __syncthreads();
+        }
+        if (threadIdx.x == 0) loss[blockIdx.x] = (float)(lsum[0] * inv_count);
+    }
     if (adam.m != nullptr) {
         if (threadIdx.x == 0) {
             const int t = (int)*adam.step_dev;
@@ -359,19 +419,19 @@ cudaError_t launch_backward_alloc(const Proj* proj, int n, const gi_frame& f, in
 cudaError_t launch_backward_tiles(const Proj* proj, uint32_t* key_gid, const uint32_t* tile_range,
                                   int n, const gi_frame& f, bool presorted,
                                   const float* dL_dimage, const float* target, int64_t cap,
-                                  void* ws, float* image_out, cudaStream_t s) {
+                                  void* ws, float* image_out, const ChainState& cs,
+                                  cudaStream_t s) {
     BwdWs w = carve(ws, n, cap, f);
     const int TX = tiles_x(f.width), T = TX * tiles_y(f.height);
     const double count = 3.0 * (double)f.width * (double)f.height;
     const float norm = (float)(2.0 / count);
     const bool mse = dL_dimage == nullptr;
-    dim3 grid(T, f.batch);
-    backward_tile_kernel<<<grid, 256, 0, s>>>(proj, key_gid, tile_range, w.gauss_off, n, f.width,
-                                              f.height, T, TX, presorted, dL_dimage, target, norm,
-                                              cap, w.partial, mse ? w.sse : nullptr,
-                                              mse ? image_out : nullptr);
+    cudaError_t e = launch_pdl(backward_tile_kernel, dim3(T, f.batch), dim3(256), s, proj, key_gid,
+                               tile_range, (const uint32_t*)w.gauss_off, n, f.width, f.height, T,
+                               TX, presorted, dL_dimage, target, norm, cap, w.partial,
+                               mse ? w.sse : nullptr, mse ? image_out : nullptr, cs);
     note_launches(1);
-    return cudaGetLastError();
+    return e;
 }
 
 cudaError_t launch_backward_finalize(const float* params, const Proj* proj, int n,
@@ -383,16 +443,19 @@ cudaError_t launch_backward_finalize(const float* params, const Proj* proj, int 
     const double count = 3.0 * (double)f.width * (double)f.height;
     const int total = n * f.batch;
     cudaError_t e = cudaSuccess;
+    const bool fold = mse && loss != nullptr && total > 0 && (total + 255) / 256 >= f.batch;
     if (total > 0) {
         FusedAdam fa{};
         if (adam) fa = *adam;
-        finalize_kernel<<<(total + 255) / 256, 256, 0, s>>>(
-            reinterpret_cast<const float4*>(params), proj, w.gauss_off, total, f.width, f.height,
-            flags, cap, w.partial, reinterpret_cast<float4*>(grads), fa);
+        e = launch_pdl(finalize_kernel, dim3((total + 255) / 256), dim3(256), s,
+                       reinterpret_cast<const float4*>(params), proj, (const uint32_t*)w.gauss_off,
+                       total, f.width, f.height, flags, cap, (const float*)w.partial,
+                       reinterpret_cast<float4*>(grads), fa, (const float*)w.sse, T, f.batch,
+                       1.0 / count, fold ? loss : nullptr);
         note_launches(1);
         if ((e = cudaGetLastError()) != cudaSuccess) return e;
     }
-    if (mse && loss != nullptr) {
+    if (mse && loss != nullptr && !fold) {
         loss_kernel<<<f.batch, 256, 0, s>>>(w.sse, T, 1.0 / count, loss);
         note_launches(1);
         e = cudaGetLastError();
@@ -408,7 +471,7 @@ cudaError_t launch_backward(const float* params, const Proj* proj, const uint32_
     if (e != cudaSuccess) return e;
     // gi_bin output is already in gid order: no re-sort, key_gid not written
     e = launch_backward_tiles(proj, const_cast<uint32_t*>(key_gid), tile_range, n, f, true,
-                              dL_dimage, target, cap, ws, image_out, s);
+                              dL_dimage, target, cap, ws, image_out, ChainState{}, s);
     if (e != cudaSuccess) return e;
     return launch_backward_finalize(params, proj, n, f, flags, dL_dimage == nullptr, cap, ws, grads,
                                     loss, nullptr, s);

@@ -50,6 +50,8 @@ __global__ void __launch_bounds__(256) count_kernel(const Proj* __restrict__ pro
                                                     int n, int T, int TX,
                                                     uint32_t* __restrict__ tile_count) {
     const int g = blockIdx.x * blockDim.x + threadIdx.x;
+    griddep_wait();
+    griddep_trigger();
     if (g >= total || touched[g] == 0) return;
     const Rect q = rect_of(proj[g]);
     const int base = (g / n) * T;
@@ -68,6 +70,8 @@ __global__ void __launch_bounds__(1024) tile_scan_kernel(const uint32_t* __restr
     __shared__ uint32_t warp_tot[32];
     __shared__ uint32_t carry_s;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    griddep_wait();
+    griddep_trigger();
     const int per = (TT + blockDim.x - 1) / blockDim.x;       // consecutive items per thread
     const int i0 = threadIdx.x * per;
     uint32_t s = 0;
@@ -132,10 +136,14 @@ __global__ void __launch_bounds__(256) scatter_kernel(const Proj* __restrict__ p
                                                       uint32_t* __restrict__ n_keys,
                                                       uint32_t* __restrict__ fill,
                                                       uint32_t* __restrict__ key_tile,
-                                                      uint32_t* __restrict__ key_gid) {
+                                                      uint32_t* __restrict__ key_gid,
+                                                      uint32_t* __restrict__ alloc_counter,
+                                                      uint32_t* __restrict__ gauss_off) {
     __shared__ uint32_t start_s[kFusedScanMax];
     __shared__ uint32_t wtot[kWarps];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    griddep_wait();
+    griddep_trigger();
     if (fuse_scan) {
         const int per = (TT + 255) / 256;                  // consecutive tiles per thread
         const int i0 = threadIdx.x * per;
@@ -174,6 +182,12 @@ __global__ void __launch_bounds__(256) scatter_kernel(const Proj* __restrict__ p
     }
     const int g = blockIdx.x * blockDim.x + threadIdx.x;
     uint32_t cnt = g < total ? touched[g] : 0u;
+    if (gauss_off != nullptr) {
+        // contiguous backward partial slots per Gaussian (warp-aggregated
+        // atomic; its latency overlaps the slot claims below)
+        const uint32_t off = warp_alloc(alloc_counter, cnt);
+        if (g < total) gauss_off[g] = off;
+    }
     Rect q{0, -1, 0, -1};
     int base = 0;
     if (cnt) {
@@ -223,6 +237,8 @@ __global__ void __launch_bounds__(256) segsort_kernel(const Proj* __restrict__ p
     __shared__ uint32_t sl[kSortMax];
     __shared__ uint32_t scratch[kWarps];
     const int t = blockIdx.x;
+    griddep_wait();
+    griddep_trigger();
     const uint32_t s0 = tile_range[t], s1 = tile_range[t + 1];
     if (s1 - s0 <= 1) return;
     const int img = t / T, tl = t % T;
@@ -274,10 +290,15 @@ cudaError_t bin_clear(void* ws, int n, int64_t cap, const gi_frame& f, cudaStrea
     return cudaMemsetAsync(w.tile_count, 0, sizeof(uint32_t) * (2 * TT + 1), s);
 }
 
+ChainState bin_chain_state(void* bin_ws, int n, int64_t cap, const gi_frame& f, uint32_t* gauss_off) {
+    BinWs w = carve(bin_ws, n, cap, f);
+    return ChainState{w.tile_count, w.fill, w.alloc_counter, gauss_off};
+}
+
 cudaError_t launch_bin(const Proj* proj, const uint32_t* tiles_touched, int n, const gi_frame& f,
                        int64_t cap, void* ws, uint32_t* key_tile, uint32_t* key_gid,
                        uint32_t* tile_range, uint32_t* n_keys, bool counted, bool sort,
-                       cudaStream_t s) {
+                       uint32_t* gauss_off, cudaStream_t s) {
     BinWs w = carve(ws, n, cap, f);
     const int total = n * f.batch;
     const int TX = tiles_x(f.width);
@@ -287,8 +308,9 @@ cudaError_t launch_bin(const Proj* proj, const uint32_t* tiles_touched, int n, c
     if (!counted) {
         if ((e = bin_clear(ws, n, cap, f, s)) != cudaSuccess) return e;
         if (total > 0) {
-            count_kernel<<<(total + 255) / 256, 256, 0, s>>>(proj, tiles_touched, total, n, T, TX,
-                                                             w.tile_count);
+            e = launch_pdl(count_kernel, dim3((total + 255) / 256), dim3(256), s, proj, tiles_touched,
+                           total, n, T, TX, w.tile_count);
+            if (e != cudaSuccess) return e;
             note_launches(1);
             if ((e = cudaGetLastError()) != cudaSuccess) return e;
         }
@@ -296,7 +318,9 @@ cudaError_t launch_bin(const Proj* proj, const uint32_t* tiles_touched, int n, c
     const bool fuse = TT <= kFusedScanMax && total > 0;
     if (!fuse) {
         if (TT <= kOneCtaScanMax) {
-            tile_scan_kernel<<<1, 1024, 0, s>>>(w.tile_count, TT, cap, tile_range, n_keys);
+            e = launch_pdl(tile_scan_kernel, dim3(1), dim3(1024), s, (const uint32_t*)w.tile_count, TT,
+                           cap, tile_range, n_keys);
+            if (e != cudaSuccess) return e;
             note_launches(1);
         } else {
             e = scan_exclusive(w.tile_count, tile_range, TT, nullptr, 1, w.scan_ws, n_keys, s);
@@ -309,14 +333,18 @@ cudaError_t launch_bin(const Proj* proj, const uint32_t* tiles_touched, int n, c
         if ((e = cudaGetLastError()) != cudaSuccess) return e;
     }
     if (total > 0) {
-        scatter_kernel<<<(total + 255) / 256, 256, 0, s>>>(proj, tiles_touched, total, n, T, TX, TT,
-                                                           cap, fuse, w.tile_count, tile_range,
-                                                           n_keys, w.fill, key_tile, key_gid);
+        e = launch_pdl(scatter_kernel, dim3((total + 255) / 256), dim3(256), s, proj, tiles_touched,
+                       total, n, T, TX, TT, cap, fuse, (const uint32_t*)w.tile_count, tile_range,
+                       n_keys, w.fill, key_tile, key_gid, gauss_off ? w.alloc_counter : nullptr,
+                       gauss_off);
+        if (e != cudaSuccess) return e;
         note_launches(1);
         if ((e = cudaGetLastError()) != cudaSuccess) return e;
     }
     if (sort) {
-        segsort_kernel<<<TT, 256, 0, s>>>(proj, n, T, TX, tile_range, key_gid);
+        e = launch_pdl(segsort_kernel, dim3(TT), dim3(256), s, proj, n, T, TX,
+                       (const uint32_t*)tile_range, key_gid);
+        if (e != cudaSuccess) return e;
         note_launches(1);
     }
     return cudaGetLastError();

@@ -5,6 +5,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <utility>
+
 #include "../../include/gi.h"
 
 #if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ != 1000)
@@ -42,6 +44,33 @@ __device__ __forceinline__ float ex2_approx(float x) {
     float y;
     asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
     return y;
+}
+
+// Programmatic dependent launch (PDL): kernels of the fused chains are
+// launched with programmatic stream serialization so that a kernel's launch
+// and prologue overlap its predecessor's tail.  griddep_wait() must precede
+// any access to memory the predecessor reads or writes; griddep_trigger()
+// lets the successor be scheduled once every CTA of this grid has started.
+// Both are no-ops for a normal launch.
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void griddep_trigger() { asm volatile("griddepcontrol.launch_dependents;"); }
+
+bool use_pdl();   // default on; GI_NO_PDL=1 disables (A/B measurement)
+
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, cudaStream_t s,
+                       Args&&... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = use_pdl() ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
 }
 
 __device__ __forceinline__ unsigned lanemask_lt() {
@@ -92,12 +121,20 @@ void note_launches(int k);
 int64_t g_launches_get();
 
 // Internal launchers (api.cu validates arguments).
-// Optional fused outputs (null to skip): tile_count accumulates the per-tile
-// key counts of binning step 1 (zeroed first, see bin_clear); alloc_counter +
-// gauss_off allocate each Gaussian's contiguous backward partial slots.
+// Optional fused outputs (null to skip): step_counter is incremented once;
+// tile_count accumulates the per-tile key counts of binning step 1 (must be
+// zero on entry: bin_clear, or left zeroed by the previous fused call).
 struct ProjectFuse {
     uint32_t* step_counter;
     uint32_t* tile_count;
+};
+// Fused-chain bookkeeping passed to the bin scatter and the consumer tile
+// kernels (all may be null): alloc_counter + gauss_off allocate each
+// Gaussian's contiguous backward partial slots in the scatter; the consumer
+// re-zeroes tile_count / fill / alloc_counter for the next call.
+struct ChainState {
+    uint32_t* tile_count;
+    uint32_t* fill;
     uint32_t* alloc_counter;
     uint32_t* gauss_off;
 };
@@ -110,13 +147,15 @@ cudaError_t launch_project(const float* params, int n, const gi_frame& f, uint32
 cudaError_t launch_bin(const Proj* proj, const uint32_t* tiles_touched, int n, const gi_frame& f,
                        int64_t cap, void* ws, uint32_t* key_tile, uint32_t* key_gid,
                        uint32_t* tile_range, uint32_t* n_keys, bool counted, bool sort,
-                       cudaStream_t s);
+                       uint32_t* gauss_off, cudaStream_t s);
+ChainState bin_chain_state(void* bin_ws, int n, int64_t cap, const gi_frame& f, uint32_t* gauss_off);
 size_t bin_ws_bytes(int n, int64_t cap, const gi_frame& f);
 uint32_t* bin_tile_counts(void* ws, int n, int64_t cap, const gi_frame& f);
 uint32_t* bin_alloc_counter(void* ws, int n, int64_t cap, const gi_frame& f);
 cudaError_t bin_clear(void* ws, int n, int64_t cap, const gi_frame& f, cudaStream_t s);
 cudaError_t launch_render(const Proj* proj, uint32_t* key_gid, const uint32_t* tile_range, int n,
-                          const gi_frame& f, bool presorted, float* image, cudaStream_t s);
+                          const gi_frame& f, bool presorted, float* image, const ChainState& cs,
+                          cudaStream_t s);
 size_t backward_ws_bytes(int n, int64_t cap, const gi_frame& f);
 cudaError_t launch_backward(const float* params, const Proj* proj, const uint32_t* key_gid,
                             const uint32_t* tile_range, int n, const gi_frame& f, uint32_t flags,
@@ -128,7 +167,8 @@ uint32_t* backward_gauss_off(void* ws, int n, int64_t cap, const gi_frame& f);
 cudaError_t launch_backward_tiles(const Proj* proj, uint32_t* key_gid, const uint32_t* tile_range,
                                   int n, const gi_frame& f, bool presorted,
                                   const float* dL_dimage, const float* target, int64_t cap,
-                                  void* ws, float* image_out, cudaStream_t s);
+                                  void* ws, float* image_out, const ChainState& cs,
+                                  cudaStream_t s);
 // Per-Gaussian reduction of the per-key partials + chain rule -> grads.  If
 // adam_m is non-null the Adam update (device step counter) is fused in.
 struct FusedAdam {

@@ -94,14 +94,10 @@ __global__ void __launch_bounds__(256) project_kernel(const float4* __restrict__
                                                       uint32_t* __restrict__ tiles_touched,
                                                       ProjectFuse fuse) {
     const int g = blockIdx.x * blockDim.x + threadIdx.x;
+    griddep_wait();
+    griddep_trigger();
     if (fuse.step_counter != nullptr && g == 0) *fuse.step_counter += 1u;   // fused fit: t <- t + 1
-    uint32_t touched = 0;
-    if (g < total) touched = project_one(params, g, n, W, H, k, flags, proj, fuse.tile_count);
-    if (g < total) tiles_touched[g] = touched;
-    if (fuse.gauss_off != nullptr) {                    // all lanes: warp-aggregated
-        const uint32_t off = warp_alloc(fuse.alloc_counter, touched);
-        if (g < total) fuse.gauss_off[g] = off;
-    }
+    if (g < total) tiles_touched[g] = project_one(params, g, n, W, H, k, flags, proj, fuse.tile_count);
 }
 
 }  // namespace
@@ -112,9 +108,9 @@ cudaError_t launch_project(const float* params, int n, const gi_frame& f, uint32
     const int total = n * f.batch;
     const int blocks = (total + 255) / 256;
     if (blocks == 0 && fuse.step_counter == nullptr) return cudaSuccess;
-    project_kernel<<<blocks > 0 ? blocks : 1, 256, 0, s>>>(
-        reinterpret_cast<const float4*>(params), n, total, f.width, f.height, f.k, flags, proj,
-        tiles_touched, fuse);
+    launch_pdl(project_kernel, dim3(blocks > 0 ? blocks : 1), dim3(256), s,
+               reinterpret_cast<const float4*>(params), n, total, f.width, f.height, f.k, flags, proj,
+               tiles_touched, fuse);
     note_launches(1);
     return cudaGetLastError();
 }

@@ -21,9 +21,18 @@ __global__ void __launch_bounds__(256) render_kernel(const Proj* __restrict__ pr
                                                      uint32_t* __restrict__ key_gid,
                                                      const uint32_t* __restrict__ tile_range,
                                                      int n, int W, int H, int T, int TX,
-                                                     bool presorted, float* __restrict__ image) {
+                                                     bool presorted, float* __restrict__ image,
+                                                     ChainState cs) {
     __shared__ RenderShared sh;
     const TileCtx t = make_tile_ctx(W, H, TX);
+    griddep_wait();
+    griddep_trigger();
+    if (threadIdx.x == 0 && cs.tile_count != nullptr) {   // leave the counters zero for the next call
+        const int tt = t.img * T + t.tile;
+        cs.tile_count[tt] = 0u;
+        cs.fill[tt] = 0u;
+        if (tt == 0 && cs.alloc_counter != nullptr) *cs.alloc_counter = 0u;
+    }
     const uint32_t s = tile_range[t.img * T + t.tile];
     const uint32_t e = tile_range[t.img * T + t.tile + 1];
     // presorted: the segment comes from gi_bin (already in gid order); else it
@@ -55,13 +64,13 @@ __global__ void __launch_bounds__(256) render_kernel(const Proj* __restrict__ pr
 }  // namespace
 
 cudaError_t launch_render(const Proj* proj, uint32_t* key_gid, const uint32_t* tile_range, int n,
-                          const gi_frame& f, bool presorted, float* image, cudaStream_t s) {
+                          const gi_frame& f, bool presorted, float* image, const ChainState& cs,
+                          cudaStream_t s) {
     const int TX = tiles_x(f.width), T = TX * tiles_y(f.height);
-    dim3 grid(T, f.batch);
-    render_kernel<<<grid, 256, 0, s>>>(proj, key_gid, tile_range, n, f.width, f.height, T, TX,
-                                       presorted, image);
+    cudaError_t e = launch_pdl(render_kernel, dim3(T, f.batch), dim3(256), s, proj, key_gid,
+                               tile_range, n, f.width, f.height, T, TX, presorted, image, cs);
     note_launches(1);
-    return cudaGetLastError();
+    return e;
 }
 
 }  // namespace gi

@@ -152,6 +152,7 @@ class Fitter:
         torch.cuda.current_stream(self.device).wait_stream(s)
         self.graph = g
         self.steps_per_graph = steps_per_graph
+        self._graphs = getattr(self, "_graphs", []) + [g]   # keep every captured graph alive
         return g
 
     def replay(self):

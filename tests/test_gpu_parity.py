@@ -348,3 +348,28 @@ def test_fit_graph_loss_decreases(gi):
     assert fit.check() == gi.GI_OK
     assert fit.steps_done() == 1 + 300        # capture records, it does not execute
     assert float(fit.loss[0]) < 0.5 * l0
+
+
+def test_determinism_and_counter_reuse(gi):
+    # the fused paths leave their per-tile counters zeroed for the next call;
+    # repeated frames and two identical fits must agree bit for bit (no
+    # atomics on values, fixed reduction orders)
+    from paper_2403_08551_b200.pipeline import Fitter, Pipeline
+    W, H, n = 256, 192, 8000
+    p = synth.init_params(31, n)
+    tgt = synth.image(31, W, H)
+    pipe = Pipeline(n, W, H, 1, device=DEV)
+    a = pipe.render_frame(to_dev(p[None])).clone()
+    b = pipe.render_frame(to_dev(p[None])).clone()
+    assert torch.equal(a, b)
+    outs = []
+    for _ in range(2):
+        fit = Fitter(to_dev(p)[None].contiguous(), to_dev(tgt)[None].contiguous())
+        for _ in range(5):
+            fit.step()
+        torch.cuda.synchronize()
+        assert fit.check() == gi.GI_OK
+        outs.append((fit.params.clone(), fit.loss.clone(), fit.grads.clone()))
+    assert torch.equal(outs[0][0], outs[1][0])
+    assert torch.equal(outs[0][1], outs[1][1])
+    assert torch.equal(outs[0][2], outs[1][2])

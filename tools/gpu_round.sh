@@ -16,6 +16,11 @@ fi
 timeout 600 python bench.py > $OUT/${TAG}_bench.json 2> $OUT/${TAG}_bench.err
 echo "bench rc=$?"
 tail -c 3000 $OUT/${TAG}_bench.json
+if [ "${AB_PDL:-0}" = "1" ]; then
+  GI_NO_PDL=1 timeout 600 python bench.py --no-cpu-baseline > $OUT/${TAG}_bench_nopdl.json 2>&1
+  echo "bench (no PDL) rc=$?"
+  python -c "import json;d=json.load(open('$OUT/${TAG}_bench_nopdl.json'));print('NO-PDL fit',d['value'],'render',d['render_fps'],'decode',d['decode_fps'],d['stage_ms'])"
+fi
 PCMD="python bench.py --steps 5 --warmup 3 --no-cpu-baseline"
 timeout 300 $PCMD > $OUT/${TAG}_prof_plain.json 2> $OUT/${TAG}_prof_plain.err
 rc=$?
