@@ -172,6 +172,22 @@ gi_status gi_fit_step(float* params, float* grads, float* m, float* v, const flo
                       void* fit_ws, size_t ws_bytes, uint32_t* step_counter, float lr0,
                       int32_t half_every, float beta1, float beta2, float eps, float* loss,
                       uint32_t* status_flags, void* const* stage_events, void* stream);
+/* Chained fit steps: identical arithmetic to gi_fit_step, but the projection
+ * of step t+1 is fused into the finalize + Adam kernel of step t (the thread
+ * that updated a Gaussian projects it at once), so a step is 3 kernels.
+ * gi_fit_prime projects the current params into fit_ws; every
+ * gi_fit_step_chained call then REQUIRES that fit_ws holds the projection of
+ * the current params -- i.e. it follows gi_fit_prime or another chained call
+ * on the same params/fit_ws with no other writer of params in between -- and
+ * leaves it so for the next call.  Same arguments as gi_fit_step. */
+gi_status gi_fit_prime(const float* params, int32_t n, const gi_frame* f, uint32_t flags,
+                       int64_t key_capacity, void* fit_ws, size_t ws_bytes, void* stream);
+gi_status gi_fit_step_chained(float* params, float* grads, float* m, float* v, const float* target,
+                              int32_t n, const gi_frame* f, uint32_t flags, int64_t key_capacity,
+                              void* fit_ws, size_t ws_bytes, uint32_t* step_counter, float lr0,
+                              int32_t half_every, float beta1, float beta2, float eps, float* loss,
+                              uint32_t* status_flags, void* const* stage_events, void* stream);
+
 /* --- fused render of a frame (graph-capturable) ---------------------------
  * project (+ per-tile counts) -> bin -> Eq. 7 render in one call; the per-tile
  * gid ordering of binning happens inside the render kernel.  Same workspace

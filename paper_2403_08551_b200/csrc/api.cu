@@ -229,11 +229,12 @@ static cudaError_t record_stage(void* const* ev, int i, cudaStream_t s) {
     return cudaEventRecordWithFlags(static_cast<cudaEvent_t>(ev[i]), s, cudaEventRecordExternal);
 }
 
-gi_status gi_fit_step(float* params, float* grads, float* m, float* v, const float* target,
-                      int32_t n, const gi_frame* f, uint32_t flags, int64_t key_capacity,
-                      void* fit_ws, size_t ws_bytes, uint32_t* step_counter, float lr0,
-                      int32_t half_every, float beta1, float beta2, float eps, float* loss,
-                      uint32_t* status_flags, void* const* stage_events, void* stream) {
+static gi_status fit_step_impl(float* params, float* grads, float* m, float* v, const float* target,
+                               int32_t n, const gi_frame* f, uint32_t flags, int64_t key_capacity,
+                               void* fit_ws, size_t ws_bytes, uint32_t* step_counter, float lr0,
+                               int32_t half_every, float beta1, float beta2, float eps, float* loss,
+                               uint32_t* status_flags, void* const* stage_events, void* stream,
+                               bool chained) {
     gi_status st;
     if ((st = check_frame(f)) != GI_OK || (st = check_n(n, f)) != GI_OK) return st;
     if (flags != GI_POS_LOGIT && flags != GI_POS_NORMALIZED) return invalid("flags");
@@ -256,19 +257,22 @@ gi_status gi_fit_step(float* params, float* grads, float* m, float* v, const flo
     uint32_t* gauss_off = gi::backward_gauss_off(w.bwd_ws, n, key_capacity, *f);
     const gi::ChainState cs = gi::bin_chain_state(w.bin_ws, n, key_capacity, *f, gauss_off);
     GI_TRY(record_stage(stage_events, 0, s), "gi_fit_step/event");
-    GI_TRY(gi::launch_project(params, n, *f, flags, w.proj, w.touched,
-                              gi::ProjectFuse{step_counter, cs.tile_count}, s),
-           "gi_fit_step/project");
+    if (!chained)
+        GI_TRY(gi::launch_project(params, n, *f, flags, w.proj, w.touched,
+                                  gi::ProjectFuse{step_counter, cs.tile_count}, s),
+               "gi_fit_step/project");
     GI_TRY(record_stage(stage_events, 1, s), "gi_fit_step/event");
     GI_TRY(gi::launch_bin(w.proj, w.touched, n, *f, key_capacity, w.bin_ws, w.key_tile, w.key_gid,
-                          w.tile_range, w.n_keys, true, false, gauss_off, s),
+                          w.tile_range, w.n_keys, true, false, gauss_off, s,
+                          chained ? step_counter : nullptr),
            "gi_fit_step/bin");
     GI_TRY(record_stage(stage_events, 2, s), "gi_fit_step/event");
     GI_TRY(gi::launch_backward_tiles(w.proj, w.key_gid, w.tile_range, n, *f, false, nullptr, target,
                                      key_capacity, w.bwd_ws, nullptr, cs, s),
            "gi_fit_step/backward");
     GI_TRY(record_stage(stage_events, 3, s), "gi_fit_step/event");
-    gi::FusedAdam fa{params, m, v, step_counter, lr0, half_every, beta1, beta2, eps, status_flags};
+    gi::FusedAdam fa{params, m, v, step_counter, lr0, half_every, beta1, beta2, eps, status_flags,
+                     chained ? w.proj : nullptr, w.touched, cs.tile_count, f->k, flags};
     GI_TRY(gi::launch_backward_finalize(params, w.proj, n, *f, flags, true, key_capacity, w.bwd_ws,
                                         grads, loss, &fa, s),
            "gi_fit_step/finalize+adam");
@@ -276,6 +280,43 @@ gi_status gi_fit_step(float* params, float* grads, float* m, float* v, const flo
     GI_TRY(record_stage(stage_events, 5, s), "gi_fit_step/event");
 #undef GI_TRY
     return GI_OK;
+}
+
+gi_status gi_fit_step(float* params, float* grads, float* m, float* v, const float* target,
+                      int32_t n, const gi_frame* f, uint32_t flags, int64_t key_capacity,
+                      void* fit_ws, size_t ws_bytes, uint32_t* step_counter, float lr0,
+                      int32_t half_every, float beta1, float beta2, float eps, float* loss,
+                      uint32_t* status_flags, void* const* stage_events, void* stream) {
+    return fit_step_impl(params, grads, m, v, target, n, f, flags, key_capacity, fit_ws, ws_bytes,
+                         step_counter, lr0, half_every, beta1, beta2, eps, loss, status_flags,
+                         stage_events, stream, false);
+}
+
+gi_status gi_fit_prime(const float* params, int32_t n, const gi_frame* f, uint32_t flags,
+                       int64_t key_capacity, void* fit_ws, size_t ws_bytes, void* stream) {
+    gi_status st;
+    if ((st = check_frame(f)) != GI_OK || (st = check_n(n, f)) != GI_OK) return st;
+    if (flags != GI_POS_LOGIT && flags != GI_POS_NORMALIZED) return invalid("flags");
+    if (key_capacity < 0 || key_capacity >= (1LL << 31)) return invalid("key_capacity");
+    if (!fit_ws || ws_bytes < carve_fit(nullptr, n, key_capacity, *f).bytes)
+        return invalid("fit workspace too small");
+    if (n > 0 && !params) return invalid("NULL buffer");
+    if (!aligned16(params) || !aligned16(fit_ws)) return invalid("alignment");
+    FitWs w = carve_fit(fit_ws, n, key_capacity, *f);
+    const gi::ChainState cs = gi::bin_chain_state(w.bin_ws, n, key_capacity, *f, nullptr);
+    return cuda_status(gi::launch_project(params, n, *f, flags, w.proj, w.touched,
+                                          gi::ProjectFuse{nullptr, cs.tile_count}, S(stream)),
+                       "gi_fit_prime");
+}
+
+gi_status gi_fit_step_chained(float* params, float* grads, float* m, float* v, const float* target,
+                              int32_t n, const gi_frame* f, uint32_t flags, int64_t key_capacity,
+                              void* fit_ws, size_t ws_bytes, uint32_t* step_counter, float lr0,
+                              int32_t half_every, float beta1, float beta2, float eps, float* loss,
+                              uint32_t* status_flags, void* const* stage_events, void* stream) {
+    return fit_step_impl(params, grads, m, v, target, n, f, flags, key_capacity, fit_ws, ws_bytes,
+                         step_counter, lr0, half_every, beta1, beta2, eps, loss, status_flags,
+                         stage_events, stream, true);
 }
 
 int64_t gi_launch_count(void) { return gi::g_launches_get(); }

@@ -23,6 +23,7 @@
 // finalize_kernel -- one thread per Gaussian: sums its contiguous slots in
 //   row-major tile order, applies the chain rule (and tanh, App. C) and
 //   optionally the Adam update (fused fit step).
+#include "project_core.cuh"
 #include "raster_common.cuh"
 
 namespace gi {
@@ -256,8 +257,9 @@ __device__ __forceinline__ float adam1(float p, float g, float& m, float& v, flo
 //   dsigma/dl1 = -p dsigma/ddx, dsigma/dl2 = -p q / l3, dsigma/dl3 = -q^2 / l3
 // (equal to <dsigma/dSigma, dSigma/dl> of A.2 with the R14 correction).
 __global__ void __launch_bounds__(256) finalize_kernel(
-    const float4* __restrict__ params, const Proj* __restrict__ proj,
-    const uint32_t* __restrict__ gauss_off, int total, int W, int H, uint32_t flags, int64_t cap,
+    const float4* __restrict__ params, const Proj* proj /* may be rewritten (chained) */,
+    const uint32_t* __restrict__ gauss_off, int total, int n_per_image, int W, int H,
+    uint32_t flags, int64_t cap,
     const float* __restrict__ partial, float4* __restrict__ grads, FusedAdam adam,
     const float* __restrict__ sse_part, int T, int batch, double inv_count,
     float* __restrict__ loss) {
@@ -354,6 +356,9 @@ __global__ void __launch_bounds__(256) finalize_kernel(
         const bool bad = !(isfinite(q0.x) && isfinite(q0.y) && isfinite(q0.z) && isfinite(q0.w) &&
                            isfinite(q1.x) && isfinite(q1.y) && isfinite(q1.z) && isfinite(q1.w));
         if (bad && adam.flag != nullptr) atomicOr(adam.flag, 1u);
+        if (adam.proj_out != nullptr)    // chained: a1 of the next step on the updated Gaussian
+            adam.touched_out[g] = project_one(q0, q1, g, n_per_image, W, H, adam.k, adam.pos_flags,
+                                              adam.proj_out, adam.tile_count);
     }
 }
 
@@ -449,7 +454,7 @@ cudaError_t launch_backward_finalize(const float* params, const Proj* proj, int 
         if (adam) fa = *adam;
         e = launch_pdl(finalize_kernel, dim3((total + 255) / 256), dim3(256), s,
                        reinterpret_cast<const float4*>(params), proj, (const uint32_t*)w.gauss_off,
-                       total, f.width, f.height, flags, cap, (const float*)w.partial,
+                       total, n, f.width, f.height, flags, cap, (const float*)w.partial,
                        reinterpret_cast<float4*>(grads), fa, (const float*)w.sse, T, f.batch,
                        1.0 / count, fold ? loss : nullptr);
         note_launches(1);

@@ -138,12 +138,14 @@ __global__ void __launch_bounds__(256) scatter_kernel(const Proj* __restrict__ p
                                                       uint32_t* __restrict__ key_tile,
                                                       uint32_t* __restrict__ key_gid,
                                                       uint32_t* __restrict__ alloc_counter,
-                                                      uint32_t* __restrict__ gauss_off) {
+                                                      uint32_t* __restrict__ gauss_off,
+                                                      uint32_t* __restrict__ step_counter) {
     __shared__ uint32_t start_s[kFusedScanMax];
     __shared__ uint32_t wtot[kWarps];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     griddep_wait();
     griddep_trigger();
+    if (step_counter != nullptr && blockIdx.x == 0 && threadIdx.x == 0) *step_counter += 1u;
     if (fuse_scan) {
         const int per = (TT + 255) / 256;                  // consecutive tiles per thread
         const int i0 = threadIdx.x * per;
@@ -298,7 +300,7 @@ ChainState bin_chain_state(void* bin_ws, int n, int64_t cap, const gi_frame& f, 
 cudaError_t launch_bin(const Proj* proj, const uint32_t* tiles_touched, int n, const gi_frame& f,
                        int64_t cap, void* ws, uint32_t* key_tile, uint32_t* key_gid,
                        uint32_t* tile_range, uint32_t* n_keys, bool counted, bool sort,
-                       uint32_t* gauss_off, cudaStream_t s) {
+                       uint32_t* gauss_off, cudaStream_t s, uint32_t* step_counter) {
     BinWs w = carve(ws, n, cap, f);
     const int total = n * f.batch;
     const int TX = tiles_x(f.width);
@@ -336,7 +338,7 @@ cudaError_t launch_bin(const Proj* proj, const uint32_t* tiles_touched, int n, c
         e = launch_pdl(scatter_kernel, dim3((total + 255) / 256), dim3(256), s, proj, tiles_touched,
                        total, n, T, TX, TT, cap, fuse, (const uint32_t*)w.tile_count, tile_range,
                        n_keys, w.fill, key_tile, key_gid, gauss_off ? w.alloc_counter : nullptr,
-                       gauss_off);
+                       gauss_off, step_counter);
         if (e != cudaSuccess) return e;
         note_launches(1);
         if ((e = cudaGetLastError()) != cudaSuccess) return e;

@@ -147,7 +147,7 @@ cudaError_t launch_project(const float* params, int n, const gi_frame& f, uint32
 cudaError_t launch_bin(const Proj* proj, const uint32_t* tiles_touched, int n, const gi_frame& f,
                        int64_t cap, void* ws, uint32_t* key_tile, uint32_t* key_gid,
                        uint32_t* tile_range, uint32_t* n_keys, bool counted, bool sort,
-                       uint32_t* gauss_off, cudaStream_t s);
+                       uint32_t* gauss_off, cudaStream_t s, uint32_t* step_counter = nullptr);
 ChainState bin_chain_state(void* bin_ws, int n, int64_t cap, const gi_frame& f, uint32_t* gauss_off);
 size_t bin_ws_bytes(int n, int64_t cap, const gi_frame& f);
 uint32_t* bin_tile_counts(void* ws, int n, int64_t cap, const gi_frame& f);
@@ -180,6 +180,13 @@ struct FusedAdam {
     int half_every;
     float b1, b2, eps;
     uint32_t* flag;
+    // chained fit step: project the updated Gaussian for the NEXT step (record,
+    // tile count and per-tile key counts); null proj_out disables
+    Proj* proj_out;
+    uint32_t* touched_out;
+    uint32_t* tile_count;
+    float k;
+    uint32_t pos_flags;
 };
 cudaError_t launch_backward_finalize(const float* params, const Proj* proj, int n,
                                      const gi_frame& f, uint32_t flags, bool mse, int64_t cap,

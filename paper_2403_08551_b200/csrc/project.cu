@@ -11,82 +11,10 @@
 // explicitly rounded intrinsics (no FMA contraction), so that its
 // float -> int decisions are reproducible.  The conic is formed in fp64 and
 // rounded once.
-#include "gi_internal.cuh"
+#include "project_core.cuh"
 
 namespace gi {
 namespace {
-
-__device__ __forceinline__ uint32_t project_one(const float4* __restrict__ params, int g, int n,
-                                                int W, int H, float k, uint32_t flags,
-                                                Proj* __restrict__ proj,
-                                                uint32_t* __restrict__ tile_count) {
-    const float4 p0 = params[2 * (size_t)g];       // mux, muy, l1, l2
-    const float4 p1 = params[2 * (size_t)g + 1];   // l3, c'r, c'g, c'b
-
-    // App. C: u = tanh(mu_raw); R2: mu = (u + 1) * W / 2  (fp64, no contraction)
-    double ux = (double)p0.x, uy = (double)p0.y;
-    if (flags == GI_POS_LOGIT) {
-        ux = tanh(ux);
-        uy = tanh(uy);
-    }
-    const double mx = __dmul_rn(__dadd_rn(ux, 1.0), (double)W * 0.5);
-    const double my = __dmul_rn(__dadd_rn(uy, 1.0), (double)H * 0.5);
-
-    // Effective Cholesky factors (App. C "+0.5" on l1, l3), fp32 as stored.
-    const float l1e = __fadd_rn(p0.z, 0.5f);
-    const float l2 = p0.w;
-    const float l3e = __fadd_rn(p1.x, 0.5f);
-
-    Proj r;
-    uint32_t bx = kEmptyBox, by = kEmptyBox, touched = 0;
-    int ix = 0, iy = 0;
-    float fx = 0.f, fy = 0.f;
-    const bool centre_ok = (mx >= 0.0) && (mx <= (double)W) && (my >= 0.0) && (my <= (double)H);
-    if (centre_ok) {
-        const double fix = floor(mx), fiy = floor(my);
-        ix = (int)fix;
-        iy = (int)fiy;
-        fx = __double2float_rn(mx - fix);
-        fy = __double2float_rn(my - fiy);
-    }
-    if (centre_ok && l1e != 0.0f && l3e != 0.0f) {
-        // R6/R7: half extents k sqrt(Sxx) = k |l1e|, k sqrt(Syy) = k sqrt(l2^2 + l3e^2)
-        const float rx = __fmul_rn(k, fabsf(l1e));
-        const float ry = __fmul_rn(k, __fsqrt_rn(__fadd_rn(__fmul_rn(l2, l2), __fmul_rn(l3e, l3e))));
-        const float cx = __fsub_rn(fx, 0.5f), cy = __fsub_rn(fy, 0.5f);
-        const float bw = (float)(W + 1), bh = (float)(H + 1);
-        const float lox = fminf(fmaxf(__fsub_rn(cx, rx), -bw), bw);
-        const float hix = fminf(fmaxf(__fadd_rn(cx, rx), -bw), bw);
-        const float loy = fminf(fmaxf(__fsub_rn(cy, ry), -bh), bh);
-        const float hiy = fminf(fmaxf(__fadd_rn(cy, ry), -bh), bh);
-        const int x0 = max(0, ix + (int)ceilf(lox));
-        const int x1 = min(W - 1, ix + (int)floorf(hix));
-        const int y0 = max(0, iy + (int)ceilf(loy));
-        const int y1 = min(H - 1, iy + (int)floorf(hiy));
-        if (x0 <= x1 && y0 <= y1) {
-            bx = (uint32_t)x0 | ((uint32_t)x1 << 16);
-            by = (uint32_t)y0 | ((uint32_t)y1 << 16);
-            touched = (uint32_t)((x1 / kTile - x0 / kTile + 1) * (y1 / kTile - y0 / kTile + 1));
-            if (tile_count != nullptr) {   // fused first step of binning: per-tile key counts
-                const int TX = (W + kTile - 1) / kTile;
-                uint32_t* tc = tile_count + (size_t)(g / n) * (size_t)(TX * ((H + kTile - 1) / kTile));
-                for (int ty = y0 / kTile; ty <= y1 / kTile; ++ty)
-                    for (int tx = x0 / kTile; tx <= x1 / kTile; ++tx) atomicAdd(&tc[ty * TX + tx], 1u);
-            }
-        }
-    }
-    // Sigma^-1 = L^-T L^-1 with L^-1 = [[1/l1, 0], [-l2/(l1 l3), 1/l3]], scaled by
-    // kappa so that sigma * log2(e) = (a dx)^2 + (b dx + c dy)^2 (fp64, one rounding).
-    const double d1 = (double)l1e, d2 = (double)l2, d3 = (double)l3e;
-    const float ca = (float)(kKappa / d1);
-    const float cb = (float)(-kKappa * d2 / (d1 * d3));
-    const float cc = (float)(kKappa / d3);
-    r.q0 = make_float4(__int_as_float(ix), __int_as_float(iy), fx, fy);
-    r.q1 = make_float4(ca, cb, cc, __uint_as_float(bx));
-    r.q2 = make_float4(p1.y, p1.z, p1.w, __uint_as_float(by));
-    proj[g] = r;
-    return touched;
-}
 
 __global__ void __launch_bounds__(256) project_kernel(const float4* __restrict__ params, int n,
                                                       int total, int W, int H, float k,
@@ -97,7 +25,9 @@ __global__ void __launch_bounds__(256) project_kernel(const float4* __restrict__
     griddep_wait();
     griddep_trigger();
     if (fuse.step_counter != nullptr && g == 0) *fuse.step_counter += 1u;   // fused fit: t <- t + 1
-    if (g < total) tiles_touched[g] = project_one(params, g, n, W, H, k, flags, proj, fuse.tile_count);
+    if (g < total)
+        tiles_touched[g] = project_one(params[2 * (size_t)g], params[2 * (size_t)g + 1], g, n, W, H,
+                                       k, flags, proj, fuse.tile_count);
 }
 
 }  // namespace

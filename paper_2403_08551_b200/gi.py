@@ -70,6 +70,9 @@ SIGNATURES = {
     "gi_fit_step": (C.c_int, [_vp, _vp, _vp, _vp, _vp, _i32, _FP, _u32, _i64, _vp, _sz, _vp,
                               _f32, _i32, _f32, _f32, _f32, _vp, _vp, _vp, _vp]),
     "gi_launch_count": (_i64, []),
+    "gi_fit_prime": (C.c_int, [_vp, _i32, _FP, _u32, _i64, _vp, _sz, _vp]),
+    "gi_fit_step_chained": (C.c_int, [_vp, _vp, _vp, _vp, _vp, _i32, _FP, _u32, _i64, _vp, _sz, _vp,
+                                      _f32, _i32, _f32, _f32, _f32, _vp, _vp, _vp, _vp]),
     "gi_render_frame": (C.c_int, [_vp, _i32, _FP, _u32, _i64, _vp, _sz, _vp, _vp]),
     "gi_vq_decode": (C.c_int, [_vp, _sz, C.POINTER(gi_codec_meta), _vp, _vp]),
     "gi_psnr_workspace_bytes": (_sz, [_FP]),
@@ -198,20 +201,40 @@ def gi_adam_step(params, grads, m, v, count, step, lr, beta1=0.9, beta2=0.999, e
                             _ptr(nonfinite_flag), _stream(stream)), "gi_adam_step")
 
 
-def gi_fit_step(params, grads, m, v, target, n, f, flags, key_capacity, fit_ws, step_counter,
-                lr0=1e-3, half_every=20000, beta1=0.9, beta2=0.999, eps=1e-8, loss=None,
-                status_flags=None, stage_events=None, stream=None):
-    """stage_events: None or 6 recorded torch.cuda.Event(external=True) / raw handles."""
+def _fit_step(fn, params, grads, m, v, target, n, f, flags, key_capacity, fit_ws, step_counter,
+              lr0, half_every, beta1, beta2, eps, loss, status_flags, stage_events, stream, name):
     ev = None
     if stage_events is not None:
         handles = [e if isinstance(e, int) else e.cuda_event for e in stage_events]
         assert len(handles) == 6 and all(handles), "6 initialised events"
         ev = (C.c_void_p * 6)(*handles)
-    _ok(load().gi_fit_step(_ptr(params), _ptr(grads), _ptr(m), _ptr(v), _ptr(target), int(n),
-                           C.byref(f), int(flags), int(key_capacity), _ptr(fit_ws),
-                           fit_ws.numel() * fit_ws.element_size(), _ptr(step_counter),
-                           float(lr0), int(half_every), float(beta1), float(beta2), float(eps),
-                           _ptr(loss), _ptr(status_flags), ev, _stream(stream)), "gi_fit_step")
+    _ok(fn(_ptr(params), _ptr(grads), _ptr(m), _ptr(v), _ptr(target), int(n), C.byref(f),
+           int(flags), int(key_capacity), _ptr(fit_ws), fit_ws.numel() * fit_ws.element_size(),
+           _ptr(step_counter), float(lr0), int(half_every), float(beta1), float(beta2), float(eps),
+           _ptr(loss), _ptr(status_flags), ev, _stream(stream)), name)
+
+
+def gi_fit_step(params, grads, m, v, target, n, f, flags, key_capacity, fit_ws, step_counter,
+                lr0=1e-3, half_every=20000, beta1=0.9, beta2=0.999, eps=1e-8, loss=None,
+                status_flags=None, stage_events=None, stream=None):
+    """stage_events: None or 6 recorded torch.cuda.Event(external=True) / raw handles."""
+    _fit_step(load().gi_fit_step, params, grads, m, v, target, n, f, flags, key_capacity, fit_ws,
+              step_counter, lr0, half_every, beta1, beta2, eps, loss, status_flags, stage_events,
+              stream, "gi_fit_step")
+
+
+def gi_fit_step_chained(params, grads, m, v, target, n, f, flags, key_capacity, fit_ws,
+                        step_counter, lr0=1e-3, half_every=20000, beta1=0.9, beta2=0.999, eps=1e-8,
+                        loss=None, status_flags=None, stage_events=None, stream=None):
+    _fit_step(load().gi_fit_step_chained, params, grads, m, v, target, n, f, flags, key_capacity,
+              fit_ws, step_counter, lr0, half_every, beta1, beta2, eps, loss, status_flags,
+              stage_events, stream, "gi_fit_step_chained")
+
+
+def gi_fit_prime(params, n, f, flags, key_capacity, fit_ws, stream=None):
+    _ok(load().gi_fit_prime(_ptr(params), int(n), C.byref(f), int(flags), int(key_capacity),
+                            _ptr(fit_ws), fit_ws.numel() * fit_ws.element_size(), _stream(stream)),
+        "gi_fit_prime")
 
 
 def gi_render_frame(params, n, f, flags, key_capacity, frame_ws, image, stream=None):

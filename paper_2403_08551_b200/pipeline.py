@@ -112,8 +112,10 @@ class Fitter:
     def __init__(self, params: torch.Tensor, target: torch.Tensor, k: float = 3.0,
                  key_capacity: int | None = None, lr0: float = 1e-3, half_every: int = 20000,
                  beta1: float = 0.9, beta2: float = 0.999, eps: float = 1e-8,
-                 flags: int = gi.GI_POS_LOGIT):
+                 flags: int = gi.GI_POS_LOGIT, chained: bool = True):
         gi.load()
+        self.chained = bool(chained)
+        self.primed = False
         assert params.dim() == 3 and params.shape[2] == 8, "params [B][N][8]"
         B, n = params.shape[0], params.shape[1]
         H, W = target.shape[-2], target.shape[-1]
@@ -135,14 +137,36 @@ class Fitter:
         self.graph = None
 
     def step(self, stream=None, stage_events=None):
-        gi.gi_fit_step(self.params, self.grads, self.m, self.v, self.target, self.n, self.f,
-                       self.flags, self.cap, self.fit_ws, self.step_counter, loss=self.loss,
-                       status_flags=self.status, stage_events=stage_events, stream=stream,
-                       **self.hyper)
+        """One fused step.  In chained mode (default) the first call primes
+        the workspace and every step fuses the next step's projection into
+        its Adam kernel; the params must not be written by anyone else in
+        between (call unchain() after modifying them)."""
+        if self.chained:
+            if not self.primed:
+                gi.gi_fit_prime(self.params, self.n, self.f, self.flags, self.cap, self.fit_ws,
+                                stream)
+                self.primed = True
+            gi.gi_fit_step_chained(self.params, self.grads, self.m, self.v, self.target, self.n,
+                                   self.f, self.flags, self.cap, self.fit_ws, self.step_counter,
+                                   loss=self.loss, status_flags=self.status,
+                                   stage_events=stage_events, stream=stream, **self.hyper)
+        else:
+            gi.gi_fit_step(self.params, self.grads, self.m, self.v, self.target, self.n, self.f,
+                           self.flags, self.cap, self.fit_ws, self.step_counter, loss=self.loss,
+                           status_flags=self.status, stage_events=stage_events, stream=stream,
+                           **self.hyper)
+
+    def unchain(self):
+        """Params were modified externally: re-prime before the next chained step."""
+        self.primed = False
 
     def capture(self, steps_per_graph: int = 1, stage_events=None):
         """Capture `steps_per_graph` fused steps into one CUDA graph (stage
-        events, if given, are recorded around the last captured step)."""
+        events, if given, are recorded around the last captured step).  In
+        chained mode the workspace is primed (eagerly) first."""
+        if self.chained and not self.primed:
+            gi.gi_fit_prime(self.params, self.n, self.f, self.flags, self.cap, self.fit_ws)
+            self.primed = True
         s = torch.cuda.Stream(device=self.device)
         s.wait_stream(torch.cuda.current_stream(self.device))
         g = torch.cuda.CUDAGraph()

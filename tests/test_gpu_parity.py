@@ -363,8 +363,8 @@ def test_determinism_and_counter_reuse(gi):
     b = pipe.render_frame(to_dev(p[None])).clone()
     assert torch.equal(a, b)
     outs = []
-    for _ in range(2):
-        fit = Fitter(to_dev(p)[None].contiguous(), to_dev(tgt)[None].contiguous())
+    for chained in (True, False):     # the chained path must equal the plain one bitwise
+        fit = Fitter(to_dev(p)[None].contiguous(), to_dev(tgt)[None].contiguous(), chained=chained)
         for _ in range(5):
             fit.step()
         torch.cuda.synchronize()
