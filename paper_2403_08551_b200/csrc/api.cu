@@ -131,7 +131,8 @@ gi_status gi_project(const float* params, int32_t n, const gi_frame* f, uint32_t
     if (!aligned16(params) || !aligned16(proj)) return invalid("params/proj must be 16-B aligned");
     if (n == 0) return GI_OK;
     return cuda_status(gi::launch_project(params, n, *f, flags, static_cast<gi::Proj*>(proj),
-                                          tiles_touched, gi::ProjectFuse{}, S(stream)),
+                                          tiles_touched, gi::ProjectFuse{nullptr, gi::BinCounts{}},
+                                          S(stream)),
                        "gi_project");
 }
 
@@ -259,7 +260,9 @@ static gi_status fit_step_impl(float* params, float* grads, float* m, float* v, 
     GI_TRY(record_stage(stage_events, 0, s), "gi_fit_step/event");
     if (!chained)
         GI_TRY(gi::launch_project(params, n, *f, flags, w.proj, w.touched,
-                                  gi::ProjectFuse{step_counter, cs.tile_count}, s),
+                                  gi::ProjectFuse{step_counter,
+                                                  gi::bin_counts(w.bin_ws, n, key_capacity, *f)},
+                                  s),
                "gi_fit_step/project");
     GI_TRY(record_stage(stage_events, 1, s), "gi_fit_step/event");
     GI_TRY(gi::launch_bin(w.proj, w.touched, n, *f, key_capacity, w.bin_ws, w.key_tile, w.key_gid,
@@ -272,7 +275,8 @@ static gi_status fit_step_impl(float* params, float* grads, float* m, float* v, 
            "gi_fit_step/backward");
     GI_TRY(record_stage(stage_events, 3, s), "gi_fit_step/event");
     gi::FusedAdam fa{params, m, v, step_counter, lr0, half_every, beta1, beta2, eps, status_flags,
-                     chained ? w.proj : nullptr, w.touched, cs.tile_count, f->k, flags};
+                     chained ? w.proj : nullptr, w.touched,
+                     gi::bin_counts(w.bin_ws, n, key_capacity, *f), f->k, flags};
     GI_TRY(gi::launch_backward_finalize(params, w.proj, n, *f, flags, true, key_capacity, w.bwd_ws,
                                         grads, loss, &fa, s),
            "gi_fit_step/finalize+adam");
@@ -303,9 +307,10 @@ gi_status gi_fit_prime(const float* params, int32_t n, const gi_frame* f, uint32
     if (n > 0 && !params) return invalid("NULL buffer");
     if (!aligned16(params) || !aligned16(fit_ws)) return invalid("alignment");
     FitWs w = carve_fit(fit_ws, n, key_capacity, *f);
-    const gi::ChainState cs = gi::bin_chain_state(w.bin_ws, n, key_capacity, *f, nullptr);
     return cuda_status(gi::launch_project(params, n, *f, flags, w.proj, w.touched,
-                                          gi::ProjectFuse{nullptr, cs.tile_count}, S(stream)),
+                                          gi::ProjectFuse{nullptr,
+                                                          gi::bin_counts(w.bin_ws, n, key_capacity, *f)},
+                                          S(stream)),
                        "gi_fit_prime");
 }
 
@@ -339,7 +344,8 @@ gi_status gi_render_frame(const float* params, int32_t n, const gi_frame* f, uin
     if ((e = (expr)) != cudaSuccess) return cuda_status(e, where)
     const gi::ChainState cs = gi::bin_chain_state(w.bin_ws, n, key_capacity, *f, nullptr);
     GI_TRY(gi::launch_project(params, n, *f, flags, w.proj, w.touched,
-                              gi::ProjectFuse{nullptr, cs.tile_count}, s),
+                              gi::ProjectFuse{nullptr, gi::bin_counts(w.bin_ws, n, key_capacity, *f)},
+                              s),
            "gi_render_frame/project");
     GI_TRY(gi::launch_bin(w.proj, w.touched, n, *f, key_capacity, w.bin_ws, w.key_tile, w.key_gid,
                           w.tile_range, w.n_keys, true, false, nullptr, s),

@@ -54,6 +54,7 @@ __global__ void __launch_bounds__(256) backward_tile_kernel(
     if (threadIdx.x == 0 && cs.tile_count != nullptr) {   // leave the counters zero for the next call
         const int tt = t.img * T + t.tile;
         cs.tile_count[tt] = 0u;
+        cs.big_count[tt] = 0u;
         cs.fill[tt] = 0u;
         if (tt == 0 && cs.alloc_counter != nullptr) *cs.alloc_counter = 0u;
     }
@@ -264,20 +265,38 @@ __global__ void __launch_bounds__(256) finalize_kernel(
     const float* __restrict__ sse_part, int T, int batch, double inv_count,
     float* __restrict__ loss) {
     __shared__ float sconst[3];
-    __shared__ double lsum[256];
+    __shared__ double lsum[kWarps];
     griddep_wait();
     griddep_trigger();
+    const int g = blockIdx.x * blockDim.x + threadIdx.x;
+    // independent loads first (their latency overlaps the partial-sum chain)
+    float4 p0 = make_float4(0.f, 0.f, 0.f, 0.f), p1 = p0, m0 = p0, m1 = p0, v0 = p0, v1 = p0;
+    Proj r{};
+    uint32_t o0 = 0;
+    if (g < total) {
+        p0 = params[2 * (size_t)g];
+        p1 = params[2 * (size_t)g + 1];
+        r = proj[g];
+        o0 = gauss_off[g];
+        if (adam.m != nullptr) {
+            const float4* mm = reinterpret_cast<const float4*>(adam.m) + 2 * (size_t)g;
+            const float4* vv = reinterpret_cast<const float4*>(adam.v) + 2 * (size_t)g;
+            m0 = mm[0]; m1 = mm[1]; v0 = vv[0]; v1 = vv[1];
+        }
+    }
     if (loss != nullptr && blockIdx.x < batch) {
         // per-image L2 loss: fixed-order reduction of the per-tile partials
         double acc = 0.0;
         for (int i = threadIdx.x; i < T; i += blockDim.x) acc += (double)sse_part[blockIdx.x * T + i];
-        lsum[threadIdx.x] = acc;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(kFull, acc, o);
+        if ((threadIdx.x & 31) == 0) lsum[threadIdx.x >> 5] = acc;
         __syncthreads();
-        for (int o = 128; o > 0; o >>= 1) {
-            if ((int)threadIdx.x < o) lsum[threadIdx.x] += lsum[threadIdx.x + o];
-            __syncthreads();
+        if (threadIdx.x == 0) {
+            double tot = 0.0;
+            for (int w = 0; w < kWarps; ++w) tot += lsum[w];
+            loss[blockIdx.x] = (float)(tot * inv_count);
         }
-        if (threadIdx.x == 0) loss[blockIdx.x] = (float)(lsum[0] * inv_count);
     }
     if (adam.m != nullptr) {
         if (threadIdx.x == 0) {
@@ -288,10 +307,7 @@ __global__ void __launch_bounds__(256) finalize_kernel(
         }
         __syncthreads();
     }
-    const int g = blockIdx.x * blockDim.x + threadIdx.x;
     if (g >= total) return;
-    const float4 p0 = params[2 * (size_t)g], p1 = params[2 * (size_t)g + 1];
-    const Proj r = proj[g];
     const uint32_t bx = __float_as_uint(r.q1.w), by = __float_as_uint(r.q2.w);
     const int x0 = (int)(bx & 0xffffu), x1 = (int)(bx >> 16);
     const int y0 = (int)(by & 0xffffu), y1 = (int)(by >> 16);
@@ -299,7 +315,6 @@ __global__ void __launch_bounds__(256) finalize_kernel(
     bool any = false;
     if (x0 <= x1 && y0 <= y1) {
         const uint32_t cnt = (uint32_t)((x1 / kTile - x0 / kTile + 1) * (y1 / kTile - y0 / kTile + 1));
-        const uint32_t o0 = gauss_off[g];
         const float4* pp = reinterpret_cast<const float4*>(partial);
         for (uint32_t k = 0; k < cnt; ++k) {       // row-major tile order of the rectangle
             if ((int64_t)(o0 + k) >= cap) break;
@@ -312,23 +327,26 @@ __global__ void __launch_bounds__(256) finalize_kernel(
     }
     float4 r0 = make_float4(0.f, 0.f, 0.f, 0.f), r1 = r0;
     if (any) {
-        const double l1 = (double)p0.z + 0.5, l2 = (double)p0.w, l3 = (double)p1.x + 0.5;
-        const double ik = 1.0 / kKappa, ik2 = ik * ik;
-        const double Sp = S[3] * ik, Sq = S[4] * ik;
-        const double Spp = S[5] * ik2, Spq = S[6] * ik2, Sqq = S[7] * ik2;
-        const double Ax = (Sp - Sq * l2 / l3) / l1;   // sum gamma dsigma/ddx
-        const double Ay = Sq / l3;
-        double sx = (double)W * 0.5, sy = (double)H * 0.5;
+        // fp32 (the 1e-4 gradient bar leaves ample room); reciprocals once
+        const float l1 = p0.z + 0.5f, l2 = p0.w, l3 = p1.x + 0.5f;
+        const float il1 = 1.0f / l1, il3 = 1.0f / l3;
+        const float ik = (float)(1.0 / kKappa), ik2 = (float)(1.0 / (kKappa * kKappa));
+        const float Sp = S[3] * ik, Sq = S[4] * ik;
+        const float Spp = S[5] * ik2, Spq = S[6] * ik2, Sqq = S[7] * ik2;
+        const float l2l3 = l2 * il3;
+        const float Ax = (Sp - Sq * l2l3) * il1;         // sum gamma dsigma/ddx
+        const float Ay = Sq * il3;
+        float sx = (float)W * 0.5f, sy = (float)H * 0.5f;
         if (flags == GI_POS_LOGIT) {
-            const double chx = cosh((double)p0.x), chy = cosh((double)p0.y);
+            const float chx = coshf(p0.x), chy = coshf(p0.y);
             sx /= chx * chx;
             sy /= chy * chy;
         }
-        r0.x = (float)(-Ax * sx);                        // dmu = -dsigma/dd (R13)
-        r0.y = (float)(-Ay * sy);
-        r0.z = (float)(-(Spp - Spq * l2 / l3) / l1);     // dl1
-        r0.w = (float)(-Spq / l3);                       // dl2
-        r1.x = (float)(-Sqq / l3);                       // dl3
+        r0.x = -Ax * sx;                                  // dmu = -dsigma/dd (R13)
+        r0.y = -Ay * sy;
+        r0.z = -(Spp - Spq * l2l3) * il1;                 // dl1
+        r0.w = -Spq * il3;                                // dl2
+        r1.x = -Sqq * il3;                                // dl3
         r1.y = S[0];                                     // dc'
         r1.z = S[1];
         r1.w = S[2];
@@ -340,7 +358,6 @@ __global__ void __launch_bounds__(256) finalize_kernel(
         float4* mm = reinterpret_cast<float4*>(adam.m) + 2 * (size_t)g;
         float4* vv = reinterpret_cast<float4*>(adam.v) + 2 * (size_t)g;
         float4* pp = reinterpret_cast<float4*>(adam.params) + 2 * (size_t)g;
-        float4 m0 = mm[0], m1 = mm[1], v0 = vv[0], v1 = vv[1];
         float4 q0, q1;
         const float b1 = adam.b1, b2 = adam.b2, eps = adam.eps;
         q0.x = adam1(p0.x, r0.x, m0.x, v0.x, b1, b2, lr, ibc1, ibc2, eps);
@@ -358,7 +375,7 @@ __global__ void __launch_bounds__(256) finalize_kernel(
         if (bad && adam.flag != nullptr) atomicOr(adam.flag, 1u);
         if (adam.proj_out != nullptr)    // chained: a1 of the next step on the updated Gaussian
             adam.touched_out[g] = project_one(q0, q1, g, n_per_image, W, H, adam.k, adam.pos_flags,
-                                              adam.proj_out, adam.tile_count);
+                                              adam.proj_out, adam.counts);
     }
 }
 

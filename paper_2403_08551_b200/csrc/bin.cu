@@ -47,23 +47,24 @@ __device__ __forceinline__ Rect rect_of(const Proj& r) {
 // ------------------------------------------------------------------- count
 __global__ void __launch_bounds__(256) count_kernel(const Proj* __restrict__ proj,
                                                     const uint32_t* __restrict__ touched, int total,
-                                                    int n, int T, int TX,
-                                                    uint32_t* __restrict__ tile_count) {
+                                                    int n, int T, int TX, BinCounts bc) {
     const int g = blockIdx.x * blockDim.x + threadIdx.x;
     griddep_wait();
     griddep_trigger();
-    if (g >= total || touched[g] == 0) return;
+    if (g >= total) return;
+    const uint32_t cnt = touched[g];
+    if (cnt == 0) return;
     const Rect q = rect_of(proj[g]);
-    const int base = (g / n) * T;
-    for (int ty = q.ty0; ty <= q.ty1; ++ty)
-        for (int tx = q.tx0; tx <= q.tx1; ++tx) atomicAdd(&tile_count[base + ty * TX + tx], 1u);
+    count_keys(bc, g, q.tx0, q.tx1, q.ty0, q.ty1, cnt, (g / n) * T, TX);
 }
 
 // -------------------------------------------------------------------- scan
-// One CTA: tile_range[0..TT] = exclusive scan of tile_count, n_keys = total.
-// Range entries are clamped to the key capacity so that consumers never read
-// past the key arrays when K > cap (n_keys still reports the true K).
+// One CTA: tile_range[0..TT] = exclusive scan of (tile_count + big_count),
+// n_keys = total.  Range entries are clamped to the key capacity so that
+// consumers never read past the key arrays when K > cap (n_keys still
+// reports the true K).
 __global__ void __launch_bounds__(1024) tile_scan_kernel(const uint32_t* __restrict__ tile_count,
+                                                         const uint32_t* __restrict__ big_count,
                                                          int TT, int64_t cap,
                                                          uint32_t* __restrict__ tile_range,
                                                          uint32_t* __restrict__ n_keys) {
@@ -77,7 +78,7 @@ __global__ void __launch_bounds__(1024) tile_scan_kernel(const uint32_t* __restr
     uint32_t s = 0;
     for (int k = 0; k < per; ++k) {
         const int i = i0 + k;
-        if (i < TT) s += tile_count[i];
+        if (i < TT) s += tile_count[i] + big_count[i];
     }
     uint32_t x = s;
 #pragma unroll
@@ -104,7 +105,7 @@ __global__ void __launch_bounds__(1024) tile_scan_kernel(const uint32_t* __restr
         const int i = i0 + k;
         if (i < TT) {
             tile_range[i] = (int64_t)run < cap ? run : (uint32_t)cap;
-            run += tile_count[i];
+            run += tile_count[i] + big_count[i];
         }
     }
     if (threadIdx.x == 0) {
@@ -113,25 +114,32 @@ __global__ void __launch_bounds__(1024) tile_scan_kernel(const uint32_t* __restr
     }
 }
 
+__global__ void combine_kernel(const uint32_t* __restrict__ a, const uint32_t* __restrict__ b,
+                               uint32_t* __restrict__ out, int64_t count) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < count) out[i] = a[i] + b[i];
+}
+
 __global__ void clamp_kernel(uint32_t* __restrict__ v, int64_t count, int64_t cap) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i < count && (int64_t)v[i] > cap) v[i] = (uint32_t)cap;
 }
 
 // ----------------------------------------------------------------- scatter
-// Thread per Gaussian claims one slot per tile of its rectangle.  Gaussians
-// touching many tiles (> 16) are handed to the whole warp so that one large
-// splat does not serialise a thread.  With fuse_scan, every CTA first scans
-// the (small) per-tile count table itself into shared memory -- a redundant
-// 6 KB read per CTA instead of a separate launch -- and CTA 0 publishes
-// tile_range and n_keys.
-constexpr int kFusedScanMax = 4096;
+// Slot of key (t, g): tile_start[t] + rank, where the rank of a small
+// Gaussian's key was returned by its count atomic (key_rank), so the common
+// case needs no atomic here; keys of Gaussians touching > 4 tiles follow the
+// small ones (tile_start + tile_count) and claim a slot with an atomic on
+// fill (handed to the whole warp when > 16 tiles).  With fuse_scan, every CTA
+// first scans the (small) per-tile count tables itself into shared memory --
+// a redundant 12 KB read per CTA instead of a separate launch -- and CTA 0
+// publishes tile_range and n_keys.
+constexpr int kFusedScanMax = 2048;
 
 __global__ void __launch_bounds__(256) scatter_kernel(const Proj* __restrict__ proj,
                                                       const uint32_t* __restrict__ touched,
                                                       int total, int n, int T, int TX, int TT,
-                                                      int64_t cap, bool fuse_scan,
-                                                      const uint32_t* __restrict__ tile_count,
+                                                      int64_t cap, bool fuse_scan, BinCounts bc,
                                                       uint32_t* __restrict__ tile_range,
                                                       uint32_t* __restrict__ n_keys,
                                                       uint32_t* __restrict__ fill,
@@ -141,17 +149,31 @@ __global__ void __launch_bounds__(256) scatter_kernel(const Proj* __restrict__ p
                                                       uint32_t* __restrict__ gauss_off,
                                                       uint32_t* __restrict__ step_counter) {
     __shared__ uint32_t start_s[kFusedScanMax];
+    __shared__ uint32_t small_s[kFusedScanMax];
     __shared__ uint32_t wtot[kWarps];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     griddep_wait();
     griddep_trigger();
     if (step_counter != nullptr && blockIdx.x == 0 && threadIdx.x == 0) *step_counter += 1u;
+    // per-Gaussian inputs first: their latency overlaps the scan below
+    const int g = blockIdx.x * blockDim.x + threadIdx.x;
+    uint32_t cnt = g < total ? touched[g] : 0u;
+    Rect q{0, -1, 0, -1};
+    uint4 rk = make_uint4(0u, 0u, 0u, 0u);
+    if (cnt) {
+        q = rect_of(proj[g]);
+        if (cnt <= 4u) rk = bc.key_rank[g];
+    }
     if (fuse_scan) {
         const int per = (TT + 255) / 256;                  // consecutive tiles per thread
         const int i0 = threadIdx.x * per;
         uint32_t sum = 0;
         for (int k = 0; k < per; ++k)
-            if (i0 + k < TT) sum += tile_count[i0 + k];
+            if (i0 + k < TT) {
+                const uint32_t sm = bc.tile_count[i0 + k];
+                small_s[i0 + k] = sm;
+                sum += sm + bc.big_count[i0 + k];
+            }
         uint32_t x = sum;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -173,7 +195,7 @@ __global__ void __launch_bounds__(256) scatter_kernel(const Proj* __restrict__ p
                 const uint32_t v = (int64_t)run < cap ? run : (uint32_t)cap;
                 start_s[i] = v;
                 if (blockIdx.x == 0) tile_range[i] = v;
-                run += tile_count[i];
+                run += small_s[i] + bc.big_count[i];
             }
         }
         if (blockIdx.x == 0 && threadIdx.x == 0) {
@@ -182,26 +204,34 @@ __global__ void __launch_bounds__(256) scatter_kernel(const Proj* __restrict__ p
         }
         __syncthreads();
     }
-    const int g = blockIdx.x * blockDim.x + threadIdx.x;
-    uint32_t cnt = g < total ? touched[g] : 0u;
     if (gauss_off != nullptr) {
-        // contiguous backward partial slots per Gaussian (warp-aggregated
-        // atomic; its latency overlaps the slot claims below)
+        // contiguous backward partial slots per Gaussian (warp-aggregated atomic)
         const uint32_t off = warp_alloc(alloc_counter, cnt);
         if (g < total) gauss_off[g] = off;
     }
-    Rect q{0, -1, 0, -1};
-    int base = 0;
-    if (cnt) {
-        q = rect_of(proj[g]);
-        base = (g / n) * T;
-    }
-    if (cnt > 0 && cnt <= 16) {
+    const int base = cnt ? (g / n) * T : 0;
+    if (cnt > 0 && cnt <= 4) {
+        const int w = q.tx1 - q.tx0 + 1;
+        const uint32_t rks[4] = {rk.x, rk.y, rk.z, rk.w};
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            if (i < (int)cnt) {
+                const int t = base + (q.ty0 + i / w) * TX + q.tx0 + i % w;
+                const uint32_t st = fuse_scan ? start_s[t] : tile_range[t];
+                const int64_t slot = (int64_t)st + rks[i];
+                if (slot < cap) {
+                    key_tile[slot] = (uint32_t)t;
+                    key_gid[slot] = (uint32_t)g;
+                }
+            }
+        }
+    } else if (cnt > 4 && cnt <= 16) {
         for (int ty = q.ty0; ty <= q.ty1; ++ty)
             for (int tx = q.tx0; tx <= q.tx1; ++tx) {
                 const int t = base + ty * TX + tx;
                 const uint32_t st = fuse_scan ? start_s[t] : tile_range[t];
-                const int64_t slot = (int64_t)st + atomicAdd(&fill[t], 1u);
+                const uint32_t sm = fuse_scan ? small_s[t] : bc.tile_count[t];
+                const int64_t slot = (int64_t)st + sm + atomicAdd(&fill[t], 1u);
                 if (slot < cap) {
                     key_tile[slot] = (uint32_t)t;
                     key_gid[slot] = (uint32_t)g;
@@ -221,7 +251,8 @@ __global__ void __launch_bounds__(256) scatter_kernel(const Proj* __restrict__ p
         for (uint32_t i = lane; i < c; i += 32) {
             const int t = b + (ty0 + (int)i / w) * TX + tx0 + (int)i % w;
             const uint32_t st = fuse_scan ? start_s[t] : tile_range[t];
-            const int64_t slot = (int64_t)st + atomicAdd(&fill[t], 1u);
+            const uint32_t sm = fuse_scan ? small_s[t] : bc.tile_count[t];
+            const int64_t slot = (int64_t)st + sm + atomicAdd(&fill[t], 1u);
             if (slot < cap) {
                 key_tile[slot] = (uint32_t)t;
                 key_gid[slot] = gid;
@@ -250,23 +281,28 @@ __global__ void __launch_bounds__(256) segsort_kernel(const Proj* __restrict__ p
 
 struct BinWs {
     uint32_t* tile_count;
+    uint32_t* big_count;
     uint32_t* fill;
     uint32_t* alloc_counter;
+    uint4* key_rank;
     uint32_t* scan_ws;
     size_t bytes;
 };
 
 BinWs carve(void* base, int n, int64_t cap, const gi_frame& f) {
-    (void)n;
     (void)cap;
     const int64_t TT = (int64_t)tiles_x(f.width) * tiles_y(f.height) * f.batch;
+    const size_t total = (size_t)n * f.batch;
     char* p = static_cast<char*>(base);
     BinWs w;
     size_t off = 0;
-    // tile_count, fill and alloc_counter are adjacent: one memset clears them
+    // tile_count, big_count, fill and alloc_counter are adjacent: one memset
     w.tile_count = reinterpret_cast<uint32_t*>(p + off); off += sizeof(uint32_t) * (size_t)TT;
+    w.big_count = reinterpret_cast<uint32_t*>(p + off); off += sizeof(uint32_t) * (size_t)TT;
     w.fill = reinterpret_cast<uint32_t*>(p + off); off += sizeof(uint32_t) * (size_t)TT;
-    w.alloc_counter = reinterpret_cast<uint32_t*>(p + off); off += align_up(sizeof(uint32_t));
+    w.alloc_counter = reinterpret_cast<uint32_t*>(p + off); off += sizeof(uint32_t);
+    off = align_up(off);                                   // 256-B (uint4 key_rank)
+    w.key_rank = reinterpret_cast<uint4*>(p + off); off += align_up(sizeof(uint4) * (total + 1));
     w.scan_ws = reinterpret_cast<uint32_t*>(p + off); off += align_up(sizeof(uint32_t) * scan_ws_words(TT + 1));
     w.bytes = off;
     return w;
@@ -278,8 +314,9 @@ constexpr int64_t kOneCtaScanMax = 1 << 16;
 
 size_t bin_ws_bytes(int n, int64_t cap, const gi_frame& f) { return carve(nullptr, n, cap, f).bytes; }
 
-uint32_t* bin_tile_counts(void* ws, int n, int64_t cap, const gi_frame& f) {
-    return carve(ws, n, cap, f).tile_count;
+BinCounts bin_counts(void* ws, int n, int64_t cap, const gi_frame& f) {
+    BinWs w = carve(ws, n, cap, f);
+    return BinCounts{w.tile_count, w.big_count, w.key_rank};
 }
 
 uint32_t* bin_alloc_counter(void* ws, int n, int64_t cap, const gi_frame& f) {
@@ -289,12 +326,12 @@ uint32_t* bin_alloc_counter(void* ws, int n, int64_t cap, const gi_frame& f) {
 cudaError_t bin_clear(void* ws, int n, int64_t cap, const gi_frame& f, cudaStream_t s) {
     BinWs w = carve(ws, n, cap, f);
     const size_t TT = (size_t)tiles_x(f.width) * tiles_y(f.height) * f.batch;
-    return cudaMemsetAsync(w.tile_count, 0, sizeof(uint32_t) * (2 * TT + 1), s);
+    return cudaMemsetAsync(w.tile_count, 0, sizeof(uint32_t) * (3 * TT + 1), s);
 }
 
 ChainState bin_chain_state(void* bin_ws, int n, int64_t cap, const gi_frame& f, uint32_t* gauss_off) {
     BinWs w = carve(bin_ws, n, cap, f);
-    return ChainState{w.tile_count, w.fill, w.alloc_counter, gauss_off};
+    return ChainState{w.tile_count, w.big_count, w.fill, w.alloc_counter, gauss_off};
 }
 
 cudaError_t launch_bin(const Proj* proj, const uint32_t* tiles_touched, int n, const gi_frame& f,
@@ -311,7 +348,7 @@ cudaError_t launch_bin(const Proj* proj, const uint32_t* tiles_touched, int n, c
         if ((e = bin_clear(ws, n, cap, f, s)) != cudaSuccess) return e;
         if (total > 0) {
             e = launch_pdl(count_kernel, dim3((total + 255) / 256), dim3(256), s, proj, tiles_touched,
-                           total, n, T, TX, w.tile_count);
+                           total, n, T, TX, BinCounts{w.tile_count, w.big_count, w.key_rank});
             if (e != cudaSuccess) return e;
             note_launches(1);
             if ((e = cudaGetLastError()) != cudaSuccess) return e;
@@ -320,12 +357,14 @@ cudaError_t launch_bin(const Proj* proj, const uint32_t* tiles_touched, int n, c
     const bool fuse = TT <= kFusedScanMax && total > 0;
     if (!fuse) {
         if (TT <= kOneCtaScanMax) {
-            e = launch_pdl(tile_scan_kernel, dim3(1), dim3(1024), s, (const uint32_t*)w.tile_count, TT,
-                           cap, tile_range, n_keys);
+            e = launch_pdl(tile_scan_kernel, dim3(1), dim3(1024), s, (const uint32_t*)w.tile_count,
+                           (const uint32_t*)w.big_count, TT, cap, tile_range, n_keys);
             if (e != cudaSuccess) return e;
             note_launches(1);
         } else {
-            e = scan_exclusive(w.tile_count, tile_range, TT, nullptr, 1, w.scan_ws, n_keys, s);
+            combine_kernel<<<(TT + 255) / 256, 256, 0, s>>>(w.tile_count, w.big_count, tile_range, TT);
+            note_launches(1);
+            e = scan_exclusive(tile_range, tile_range, TT, nullptr, 1, w.scan_ws, n_keys, s);
             if (e != cudaSuccess) return e;
             e = cudaMemcpyAsync(tile_range + TT, n_keys, sizeof(uint32_t), cudaMemcpyDeviceToDevice, s);
             if (e != cudaSuccess) return e;
@@ -336,9 +375,9 @@ cudaError_t launch_bin(const Proj* proj, const uint32_t* tiles_touched, int n, c
     }
     if (total > 0) {
         e = launch_pdl(scatter_kernel, dim3((total + 255) / 256), dim3(256), s, proj, tiles_touched,
-                       total, n, T, TX, TT, cap, fuse, (const uint32_t*)w.tile_count, tile_range,
-                       n_keys, w.fill, key_tile, key_gid, gauss_off ? w.alloc_counter : nullptr,
-                       gauss_off, step_counter);
+                       total, n, T, TX, TT, cap, fuse, BinCounts{w.tile_count, w.big_count, w.key_rank},
+                       tile_range, n_keys, w.fill, key_tile, key_gid,
+                       gauss_off ? w.alloc_counter : nullptr, gauss_off, step_counter);
         if (e != cudaSuccess) return e;
         note_launches(1);
         if ((e = cudaGetLastError()) != cudaSuccess) return e;

@@ -121,12 +121,39 @@ void note_launches(int k);
 int64_t g_launches_get();
 
 // Internal launchers (api.cu validates arguments).
-// Optional fused outputs (null to skip): step_counter is incremented once;
-// tile_count accumulates the per-tile key counts of binning step 1 (must be
-// zero on entry: bin_clear, or left zeroed by the previous fused call).
+// Binning step 1 targets.  A Gaussian touching <= 4 tiles counts its keys on
+// tile_count with atomics that RETURN the key's rank within the tile, kept in
+// key_rank[g] (row-major rectangle order), so the scatter needs no atomics;
+// keys of larger Gaussians are counted on big_count and claim their slots
+// after the small ones.  All counters must be zero on entry (bin_clear, or
+// left zeroed by the consumer kernel of the previous fused call).
+struct BinCounts {
+    uint32_t* tile_count;   // [B*T] keys of small Gaussians (null: no counting)
+    uint32_t* big_count;    // [B*T] keys of Gaussians touching > 4 tiles
+    uint4* key_rank;        // [B*N] ranks of a small Gaussian's keys
+};
+
+// Count the keys of Gaussian g (rect in tiles, `touched` tiles) into bc.
+__device__ __forceinline__ void count_keys(const BinCounts& bc, int g, int tx0, int tx1, int ty0,
+                                           int ty1, uint32_t touched, int base, int TX) {
+    if (touched <= 4u) {
+        uint32_t r[4] = {0u, 0u, 0u, 0u};
+        int i = 0;
+        for (int ty = ty0; ty <= ty1; ++ty)
+            for (int tx = tx0; tx <= tx1; ++tx, ++i)
+                r[i & 3] = atomicAdd(&bc.tile_count[base + ty * TX + tx], 1u);
+        bc.key_rank[g] = make_uint4(r[0], r[1], r[2], r[3]);
+    } else {
+        for (int ty = ty0; ty <= ty1; ++ty)
+            for (int tx = tx0; tx <= tx1; ++tx) atomicAdd(&bc.big_count[base + ty * TX + tx], 1u);
+    }
+}
+
+// Optional fused outputs of the projection: step_counter is incremented once;
+// counts: binning step 1 (see BinCounts).
 struct ProjectFuse {
     uint32_t* step_counter;
-    uint32_t* tile_count;
+    BinCounts counts;
 };
 // Fused-chain bookkeeping passed to the bin scatter and the consumer tile
 // kernels (all may be null): alloc_counter + gauss_off allocate each
@@ -134,6 +161,7 @@ struct ProjectFuse {
 // re-zeroes tile_count / fill / alloc_counter for the next call.
 struct ChainState {
     uint32_t* tile_count;
+    uint32_t* big_count;
     uint32_t* fill;
     uint32_t* alloc_counter;
     uint32_t* gauss_off;
@@ -150,7 +178,7 @@ cudaError_t launch_bin(const Proj* proj, const uint32_t* tiles_touched, int n, c
                        uint32_t* gauss_off, cudaStream_t s, uint32_t* step_counter = nullptr);
 ChainState bin_chain_state(void* bin_ws, int n, int64_t cap, const gi_frame& f, uint32_t* gauss_off);
 size_t bin_ws_bytes(int n, int64_t cap, const gi_frame& f);
-uint32_t* bin_tile_counts(void* ws, int n, int64_t cap, const gi_frame& f);
+BinCounts bin_counts(void* ws, int n, int64_t cap, const gi_frame& f);
 uint32_t* bin_alloc_counter(void* ws, int n, int64_t cap, const gi_frame& f);
 cudaError_t bin_clear(void* ws, int n, int64_t cap, const gi_frame& f, cudaStream_t s);
 cudaError_t launch_render(const Proj* proj, uint32_t* key_gid, const uint32_t* tile_range, int n,
@@ -181,10 +209,10 @@ struct FusedAdam {
     float b1, b2, eps;
     uint32_t* flag;
     // chained fit step: project the updated Gaussian for the NEXT step (record,
-    // tile count and per-tile key counts); null proj_out disables
+    // tile count and binning step 1); null proj_out disables
     Proj* proj_out;
     uint32_t* touched_out;
-    uint32_t* tile_count;
+    BinCounts counts;
     float k;
     uint32_t pos_flags;
 };

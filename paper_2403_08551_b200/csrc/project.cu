@@ -27,7 +27,7 @@ __global__ void __launch_bounds__(256) project_kernel(const float4* __restrict__
     if (fuse.step_counter != nullptr && g == 0) *fuse.step_counter += 1u;   // fused fit: t <- t + 1
     if (g < total)
         tiles_touched[g] = project_one(params[2 * (size_t)g], params[2 * (size_t)g + 1], g, n, W, H,
-                                       k, flags, proj, fuse.tile_count);
+                                       k, flags, proj, fuse.counts);
 }
 
 }  // namespace

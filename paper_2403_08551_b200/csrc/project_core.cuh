@@ -10,8 +10,7 @@ namespace gi {
 __device__ __forceinline__ uint32_t project_one(const float4 p0 /* mux, muy, l1, l2 */,
                                                 const float4 p1 /* l3, c'r, c'g, c'b */, int g,
                                                 int n, int W, int H, float k, uint32_t flags,
-                                                Proj* __restrict__ proj,
-                                                uint32_t* __restrict__ tile_count) {
+                                                Proj* __restrict__ proj, const BinCounts& bc) {
     // App. C: u = tanh(mu_raw); R2: mu = (u + 1) * W / 2  (fp64, no contraction)
     double ux = (double)p0.x, uy = (double)p0.y;
     if (flags == GI_POS_LOGIT) {
@@ -56,20 +55,21 @@ __device__ __forceinline__ uint32_t project_one(const float4 p0 /* mux, muy, l1,
             bx = (uint32_t)x0 | ((uint32_t)x1 << 16);
             by = (uint32_t)y0 | ((uint32_t)y1 << 16);
             touched = (uint32_t)((x1 / kTile - x0 / kTile + 1) * (y1 / kTile - y0 / kTile + 1));
-            if (tile_count != nullptr) {   // fused first step of binning: per-tile key counts
+            if (bc.tile_count != nullptr) {   // fused binning step 1: counts and ranks
                 const int TX = (W + kTile - 1) / kTile;
-                uint32_t* tc = tile_count + (size_t)(g / n) * (size_t)(TX * ((H + kTile - 1) / kTile));
-                for (int ty = y0 / kTile; ty <= y1 / kTile; ++ty)
-                    for (int tx = x0 / kTile; tx <= x1 / kTile; ++tx) atomicAdd(&tc[ty * TX + tx], 1u);
+                const int T = TX * ((H + kTile - 1) / kTile);
+                count_keys(bc, g, x0 / kTile, x1 / kTile, y0 / kTile, y1 / kTile, touched,
+                           (g / n) * T, TX);
             }
         }
     }
     // Sigma^-1 = L^-T L^-1 with L^-1 = [[1/l1, 0], [-l2/(l1 l3), 1/l3]], scaled by
-    // kappa so that sigma * log2(e) = (a dx)^2 + (b dx + c dy)^2 (fp64, one rounding).
-    const double d1 = (double)l1e, d2 = (double)l2, d3 = (double)l3e;
-    const float ca = (float)(kKappa / d1);
-    const float cb = (float)(-kKappa * d2 / (d1 * d3));
-    const float cc = (float)(kKappa / d3);
+    // kappa so that sigma * log2(e) = (a dx)^2 + (b dx + c dy)^2.  IEEE fp32
+    // divisions (relative error <= 2 ulp -> < 1e-6 on sigma near the box edge).
+    const float kf = (float)kKappa;
+    const float ca = __fdiv_rn(kf, l1e);
+    const float cc = __fdiv_rn(kf, l3e);
+    const float cb = -__fdiv_rn(__fmul_rn(ca, l2), l3e);
     r.q0 = make_float4(__int_as_float(ix), __int_as_float(iy), fx, fy);
     r.q1 = make_float4(ca, cb, cc, __uint_as_float(bx));
     r.q2 = make_float4(p1.y, p1.z, p1.w, __uint_as_float(by));
