@@ -362,6 +362,26 @@ def main():
     d_ms = sum(s_ev[i].elapsed_time(e_ev[i]) for i in range(K))
     decode_fps = world * K / (max_over_ranks(d_ms) / 1000.0)
 
+    # ---------------- Adan fit step (the paper's optimiser, NEXT-1) ----------------
+    afit = Fitter(params.clone(), target, optimizer="adan")
+    afit.step()
+    torch.cuda.synchronize(dev)
+    ag = afit.capture(1)
+    for _ in range(Wm):
+        ag.replay()
+    barrier()
+    for i in range(K):
+        flush.zero_()
+        s_ev[i].record(stream)
+        ag.replay()
+        e_ev[i].record(stream)
+    barrier()
+    adan_value = world * K / (max_over_ranks(sum(s_ev[i].elapsed_time(e_ev[i]) for i in range(K)))
+                              / 1000.0)
+    if afit.check() != gi.GI_OK:
+        raise RuntimeError("adan fit status")
+    del afit, ag
+
     # ---------------- batched launch (configs[3] pattern): B images per launch ------------
     batched = None
     if args.batch_images > 1:
@@ -482,6 +502,7 @@ def main():
                        "vs_baseline_ref": "paper fit 469.1 it/s (Table 1a P:331, V100, Adan, "
                                           "real Kodak): context, other hardware"},
             "render_fps": render_fps,
+            "fit_its_adan": adan_value,
             "batched": batched,
             "decode_fps": decode_fps,
             "stage_ms": {"project_count": stage_ms[0], "bin": stage_ms[1],

@@ -144,6 +144,18 @@ gi_status gi_adam_step(float* params, const float* grads, float* m, float* v, in
                        int32_t step, float lr, float beta1, float beta2, float eps,
                        uint32_t* nonfinite_flag, void* stream);
 
+/* --- NEXT-1: Adan, the paper's optimiser (rule of the cited Adan
+ * reference, R28) -----------------------------------------------
+ *   d = g - g_prev (0 at t = 1); m = b1 m + (1-b1) g; v = b2 v + (1-b2) d;
+ *   n = b3 n + (1-b3) (g + b2 d)^2;
+ *   p = p (1 - lr wd) - lr (m/(1-b1^t) + b2 v/(1-b2^t)) / (sqrt(n/(1-b3^t)) + eps);
+ *   g_prev = g.   Defaults b = (0.98, 0.92, 0.99), eps = 1e-8, wd = 0.
+ * count multiple of 8, all buffers 16-B aligned. */
+gi_status gi_adan_step(float* params, const float* grads, float* m, float* v, float* n,
+                       float* grad_prev, int64_t count, int32_t step, float lr, float beta1,
+                       float beta2, float beta3, float eps, float weight_decay,
+                       uint32_t* nonfinite_flag, void* stream);
+
 /* lr_t = lr0 * 0.5^floor((t - 1) / half_every)  ("halved every 20000
  * steps", R17).  Host helper. */
 double gi_lr_at(int32_t step, double lr0, int32_t half_every);
@@ -172,6 +184,15 @@ gi_status gi_fit_step(float* params, float* grads, float* m, float* v, const flo
                       void* fit_ws, size_t ws_bytes, uint32_t* step_counter, float lr0,
                       int32_t half_every, float beta1, float beta2, float eps, float* loss,
                       uint32_t* status_flags, void* const* stage_events, void* stream);
+/* Fused fit step with Adan instead of Adam (same stages as gi_fit_step, the
+ * optimiser being a separate elementwise kernel; device step counter). */
+gi_status gi_fit_step_adan(float* params, float* grads, float* m, float* v, float* n,
+                           float* grad_prev, const float* target, int32_t n_gauss, const gi_frame* f,
+                           uint32_t flags, int64_t key_capacity, void* fit_ws, size_t ws_bytes,
+                           uint32_t* step_counter, float lr0, int32_t half_every, float beta1,
+                           float beta2, float beta3, float eps, float weight_decay, float* loss,
+                           uint32_t* status_flags, void* stream);
+
 /* Chained fit steps: identical arithmetic to gi_fit_step, but the projection
  * of step t+1 is fused into the finalize + Adam kernel of step t (the thread
  * that updated a Gaussian projects it at once), so a step is 3 kernels.

@@ -432,6 +432,37 @@ void gio_adam(const float* p_in, const float* g, const float* m_in, const float*
     }
 }
 
+// One Adan step ("optimized ... using the Adan optimizer"; the update
+// rule is the cited Adan reference's, reading R28), fp64 from fp32 state:
+//   d = g - g_prev (d = 0 at step 1: g_prev := g)
+//   m = b1 m + (1-b1) g
+//   v = b2 v + (1-b2) d
+//   n = b3 n + (1-b3) (g + b2 d)^2
+//   p = p (1 - lr wd) - lr (m/(1-b1^t) + b2 v/(1-b2^t)) / (sqrt(n/(1-b3^t)) + eps)
+// g_prev_out = g.
+void gio_adan(const float* p_in, const float* g, const float* m_in, const float* v_in,
+              const float* n_in, const float* gprev_in, int64_t count, int step, float lr,
+              float beta1, float beta2, float beta3, float eps, float wd, double* p_out,
+              double* m_out, double* v_out, double* n_out) {
+    const double b1 = beta1, b2 = beta2, b3 = beta3;
+    const double bc1 = 1.0 - std::pow(b1, (double)step);
+    const double bc2 = 1.0 - std::pow(b2, (double)step);
+    const double bc3 = 1.0 - std::pow(b3, (double)step);
+    for (int64_t i = 0; i < count; ++i) {
+        const double gi = g[i];
+        const double d = step == 1 ? 0.0 : gi - (double)gprev_in[i];
+        const double m = b1 * (double)m_in[i] + (1.0 - b1) * gi;
+        const double v = b2 * (double)v_in[i] + (1.0 - b2) * d;
+        const double u = gi + b2 * d;
+        const double nn = b3 * (double)n_in[i] + (1.0 - b3) * u * u;
+        const double upd = (m / bc1 + b2 * v / bc2) / (std::sqrt(nn / bc3) + (double)eps);
+        p_out[i] = (double)p_in[i] * (1.0 - (double)lr * (double)wd) - (double)lr * upd;
+        m_out[i] = m;
+        v_out[i] = v;
+        n_out[i] = nn;
+    }
+}
+
 // IEEE 754 binary16 -> double, written out from the format definition.
 double gio_half_to_double(uint32_t h) {
     int sign = (h >> 15) & 1;

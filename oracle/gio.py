@@ -57,6 +57,8 @@ def lib():
         L.gio_lr_at.argtypes = [C.c_int, C.c_double, C.c_int]
         L.gio_adam.argtypes = [fp, fp, fp, fp, C.c_int64, C.c_int, C.c_float, C.c_float,
                                C.c_float, C.c_float, dp, dp, dp]
+        L.gio_adan.argtypes = [fp, fp, fp, fp, fp, fp, C.c_int64, C.c_int, C.c_float, C.c_float,
+                               C.c_float, C.c_float, C.c_float, C.c_float, dp, dp, dp, dp]
         L.gio_half_to_double.restype = C.c_double
         L.gio_half_to_double.argtypes = [C.c_uint32]
         L.gio_vq_decode.restype = C.c_int
@@ -188,6 +190,17 @@ def adam(p, g, m, v, step, lr, beta1=0.9, beta2=0.999, eps=1e-8):
                    p.size, int(step), float(lr), float(beta1), float(beta2), float(eps),
                    _p(po, C.c_double), _p(mo, C.c_double), _p(vo, C.c_double))
     return po, mo, vo
+
+
+def adan(p, g, m, v, n, gprev, step, lr, beta1=0.98, beta2=0.92, beta3=0.99, eps=1e-8, wd=0.0):
+    """One fp64 Adan step from fp32 state -> (p, m, v, n) fp64 (g_prev' = g)."""
+    p, g, m, v, n, gp = (_f32(x) for x in (p, g, m, v, n, gprev))
+    outs = [np.zeros(p.shape) for _ in range(4)]
+    lib().gio_adan(_p(p, C.c_float), _p(g, C.c_float), _p(m, C.c_float), _p(v, C.c_float),
+                   _p(n, C.c_float), _p(gp, C.c_float), p.size, int(step), float(lr),
+                   float(beta1), float(beta2), float(beta3), float(eps), float(wd),
+                   *[_p(o, C.c_double) for o in outs])
+    return tuple(outs)
 
 
 def half_to_double(bits: int) -> float:

@@ -209,6 +209,24 @@ gi_status gi_adam_step(float* params, const float* grads, float* m, float* v, in
                        "gi_adam_step");
 }
 
+gi_status gi_adan_step(float* params, const float* grads, float* m, float* v, float* n,
+                       float* grad_prev, int64_t count, int32_t step, float lr, float beta1,
+                       float beta2, float beta3, float eps, float weight_decay,
+                       uint32_t* nonfinite_flag, void* stream) {
+    if (count < 0 || count % 8 != 0) return invalid("count must be a multiple of 8");
+    if (step < 1) return invalid("step is 1-based");
+    if (!(beta1 >= 0.f && beta1 < 1.f && beta2 >= 0.f && beta2 < 1.f && beta3 >= 0.f && beta3 < 1.f))
+        return invalid("betas");
+    if (count > 0 && (!params || !grads || !m || !v || !n || !grad_prev)) return invalid("NULL buffer");
+    if (!aligned16(params) || !aligned16(grads) || !aligned16(m) || !aligned16(v) || !aligned16(n) ||
+        !aligned16(grad_prev))
+        return invalid("alignment");
+    return cuda_status(gi::launch_adan(params, grads, m, v, n, grad_prev, count, step, nullptr, lr, 1,
+                                       beta1, beta2, beta3, eps, weight_decay, nonfinite_flag,
+                                       S(stream)),
+                       "gi_adan_step");
+}
+
 double gi_lr_at(int32_t step, double lr0, int32_t half_every) {
     if (step < 1 || half_every < 1) return 0.0;
     return std::ldexp(lr0, -((step - 1) / half_every));
@@ -294,6 +312,58 @@ gi_status gi_fit_step(float* params, float* grads, float* m, float* v, const flo
     return fit_step_impl(params, grads, m, v, target, n, f, flags, key_capacity, fit_ws, ws_bytes,
                          step_counter, lr0, half_every, beta1, beta2, eps, loss, status_flags,
                          stage_events, stream, false);
+}
+
+gi_status gi_fit_step_adan(float* params, float* grads, float* m, float* v, float* n,
+                           float* grad_prev, const float* target, int32_t n_gauss, const gi_frame* f,
+                           uint32_t flags, int64_t key_capacity, void* fit_ws, size_t ws_bytes,
+                           uint32_t* step_counter, float lr0, int32_t half_every, float beta1,
+                           float beta2, float beta3, float eps, float weight_decay, float* loss,
+                           uint32_t* status_flags, void* stream) {
+    gi_status st;
+    if ((st = check_frame(f)) != GI_OK || (st = check_n(n_gauss, f)) != GI_OK) return st;
+    if (flags != GI_POS_LOGIT && flags != GI_POS_NORMALIZED) return invalid("flags");
+    if (key_capacity < 0 || key_capacity >= (1LL << 31)) return invalid("key_capacity");
+    if (half_every < 1) return invalid("half_every");
+    if (!(beta1 >= 0.f && beta1 < 1.f && beta2 >= 0.f && beta2 < 1.f && beta3 >= 0.f && beta3 < 1.f))
+        return invalid("betas");
+    if (!fit_ws || ws_bytes < carve_fit(nullptr, n_gauss, key_capacity, *f).bytes)
+        return invalid("fit workspace too small");
+    if (!step_counter || !target ||
+        (n_gauss > 0 && (!params || !grads || !m || !v || !n || !grad_prev)))
+        return invalid("NULL buffer");
+    if (!aligned16(params) || !aligned16(grads) || !aligned16(m) || !aligned16(v) || !aligned16(n) ||
+        !aligned16(grad_prev) || !aligned16(fit_ws))
+        return invalid("alignment");
+    const int32_t nn = n_gauss;
+    FitWs w = carve_fit(fit_ws, nn, key_capacity, *f);
+    cudaStream_t s = S(stream);
+    cudaError_t e;
+#define GI_TRY(expr, where) \
+    if ((e = (expr)) != cudaSuccess) return cuda_status(e, where)
+    uint32_t* gauss_off = gi::backward_gauss_off(w.bwd_ws, nn, key_capacity, *f);
+    const gi::ChainState cs = gi::bin_chain_state(w.bin_ws, nn, key_capacity, *f, gauss_off);
+    GI_TRY(gi::launch_project(params, nn, *f, flags, w.proj, w.touched,
+                              gi::ProjectFuse{step_counter,
+                                              gi::bin_counts(w.bin_ws, nn, key_capacity, *f)},
+                              s),
+           "gi_fit_step_adan/project");
+    GI_TRY(gi::launch_bin(w.proj, w.touched, nn, *f, key_capacity, w.bin_ws, w.key_tile, w.key_gid,
+                          w.tile_range, w.n_keys, true, false, gauss_off, s),
+           "gi_fit_step_adan/bin");
+    GI_TRY(gi::launch_backward_tiles(w.proj, w.key_gid, w.tile_range, nn, *f, false, nullptr, target,
+                                     key_capacity, w.bwd_ws, nullptr, cs, s),
+           "gi_fit_step_adan/backward");
+    GI_TRY(gi::launch_backward_finalize(params, w.proj, nn, *f, flags, true, key_capacity, w.bwd_ws,
+                                        grads, loss, nullptr, s),
+           "gi_fit_step_adan/finalize");
+    if (nn > 0)
+        GI_TRY(gi::launch_adan(params, grads, m, v, n, grad_prev, (int64_t)nn * 8 * f->batch, 0,
+                               step_counter, lr0, half_every, beta1, beta2, beta3, eps,
+                               weight_decay, status_flags, s),
+               "gi_fit_step_adan/adan");
+#undef GI_TRY
+    return GI_OK;
 }
 
 gi_status gi_fit_prime(const float* params, int32_t n, const gi_frame* f, uint32_t flags,

@@ -112,9 +112,18 @@ class Fitter:
     def __init__(self, params: torch.Tensor, target: torch.Tensor, k: float = 3.0,
                  key_capacity: int | None = None, lr0: float = 1e-3, half_every: int = 20000,
                  beta1: float = 0.9, beta2: float = 0.999, eps: float = 1e-8,
-                 flags: int = gi.GI_POS_LOGIT, chained: bool = True):
+                 flags: int = gi.GI_POS_LOGIT, chained: bool = True, optimizer: str = "adam",
+                 beta3: float = 0.99, weight_decay: float = 0.0):
+        """optimizer: "adam" (north_star; fused into finalize) or "adan" (the
+        paper's; separate elementwise kernel, default betas
+        (0.98, 0.92, 0.99) when beta1/beta2 are left at Adam's defaults)."""
         gi.load()
-        self.chained = bool(chained)
+        if optimizer not in ("adam", "adan"):
+            raise ValueError("optimizer must be 'adam' or 'adan'")
+        self.optimizer = optimizer
+        if optimizer == "adan" and (beta1, beta2) == (0.9, 0.999):
+            beta1, beta2 = 0.98, 0.92
+        self.chained = bool(chained) and optimizer == "adam"
         self.primed = False
         assert params.dim() == 3 and params.shape[2] == 8, "params [B][N][8]"
         B, n = params.shape[0], params.shape[1]
@@ -133,6 +142,10 @@ class Fitter:
         self.status = _u32(1, self.device)
         self.loss = torch.zeros(B, dtype=torch.float32, device=self.device)
         self.hyper = dict(lr0=lr0, half_every=half_every, beta1=beta1, beta2=beta2, eps=eps)
+        if optimizer == "adan":
+            self.n_acc = torch.zeros_like(self.params)
+            self.grad_prev = torch.zeros_like(self.params)
+            self.adan_extra = dict(beta3=beta3, weight_decay=weight_decay)
         self.flags = flags
         self.graph = None
 
@@ -141,6 +154,12 @@ class Fitter:
         the workspace and every step fuses the next step's projection into
         its Adam kernel; the params must not be written by anyone else in
         between (call unchain() after modifying them)."""
+        if self.optimizer == "adan":
+            gi.gi_fit_step_adan(self.params, self.grads, self.m, self.v, self.n_acc, self.grad_prev,
+                                self.target, self.n, self.f, self.flags, self.cap, self.fit_ws,
+                                self.step_counter, loss=self.loss, status_flags=self.status,
+                                stream=stream, **self.hyper, **self.adan_extra)
+            return
         if self.chained:
             if not self.primed:
                 gi.gi_fit_prime(self.params, self.n, self.f, self.flags, self.cap, self.fit_ws,

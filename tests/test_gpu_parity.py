@@ -373,3 +373,48 @@ def test_determinism_and_counter_reuse(gi):
     assert torch.equal(outs[0][0], outs[1][0])
     assert torch.equal(outs[0][1], outs[1][1])
     assert torch.equal(outs[0][2], outs[1][2])
+
+
+def test_adan_parity(gi, gio):
+    # NEXT-1: elementwise Adan vs the fp64 oracle over three steps (the
+    # gradient-difference term is live from step 2)
+    rng = np.random.default_rng(13)
+    n = 8 * 1000
+    p = rng.normal(size=n).astype(np.float32)
+    st = {k: np.zeros(n, np.float32) for k in ("m", "v", "n", "gp")}
+    dev = {k: to_dev(v) for k, v in st.items()}
+    pt = to_dev(p)
+    for step in (1, 2, 3):
+        g = (rng.normal(size=n) * 10.0 ** rng.uniform(-4, 1, size=n)).astype(np.float32)
+        pref = pt.cpu().numpy()
+        ref = gio.adan(pref, g, dev["m"].cpu().numpy(), dev["v"].cpu().numpy(),
+                       dev["n"].cpu().numpy(), dev["gp"].cpu().numpy(), step, 1e-3)
+        gi.gi_adan_step(pt, to_dev(g), dev["m"], dev["v"], dev["n"], dev["gp"], n, step, 1e-3)
+        got = pt.cpu().numpy()
+        upd = np.abs(ref[0] - pref.astype(np.float64))
+        # fp32 rounding of p and of the update (a few ulp of each)
+        assert np.all(np.abs(got - ref[0]) <= 2e-6 * (np.abs(ref[0]) + upd) + 1e-12)
+        assert np.array_equal(dev["gp"].cpu().numpy(), g)
+
+
+def test_fit_step_adan(gi, gio):
+    # fused Adan fit step: gradients and the first update vs the oracle
+    from paper_2403_08551_b200.pipeline import Fitter
+    W, H, n = 64, 64, 256
+    p = synth.init_params(0, n)
+    tgt = synth.image(0, W, H)
+    fit = Fitter(to_dev(p)[None].contiguous(), to_dev(tgt)[None].contiguous(), optimizer="adan")
+    fit.step()
+    torch.cuda.synchronize()
+    assert fit.check() == gi.GI_OK and fit.steps_done() == 1
+    img, loss, g = gio.loss_and_grads(p, tgt, mode=gio.ALL_PAIRS)
+    assert max(group_err(fit.grads[0].cpu().numpy().astype(np.float64), g).values()) <= GRAD_TOL
+    z = np.zeros_like(p)
+    po, _, _, _ = gio.adan(p, g.astype(np.float32), z, z, z, z, 1, 1e-3)
+    got = fit.params[0].cpu().numpy().astype(np.float64)
+    big = np.abs(g) > 1e-3 * np.sqrt(np.mean(g ** 2, axis=0, keepdims=True))
+    assert np.all(np.abs(got - po)[big] <= 1e-6 * np.abs(po)[big] + 1e-9)
+    for _ in range(20):
+        fit.step()
+    torch.cuda.synchronize()
+    assert fit.check() == gi.GI_OK and float(fit.loss[0]) < loss

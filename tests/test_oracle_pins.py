@@ -440,3 +440,46 @@ def test_decode_rvq_exact_codeword_and_size(gio):
     assert np.array_equal(out[:, 2:5], codes.astype(np.float32))
     assert np.array_equal(out[:, 5:], books[0, idx[:, 0]] + books[1, idx[:, 1]])
     assert out[1, 1] == 65504.0 and out[0, 1] == 2.0 ** -24
+
+
+# ------------------------------------------------------------------- Adan
+def test_adan_closed_forms(gio):
+    # NEXT-1 (P:381 Adan; update rule of the cited Adan reference, R28)
+    rng = np.random.default_rng(9)
+    p = rng.normal(size=500).astype(np.float32)
+    g = rng.normal(size=500).astype(np.float32)
+    z = np.zeros(500, np.float32)
+    lr = 1e-3
+    b1, b2, b3 = (float(np.float32(x)) for x in (0.98, 0.92, 0.99))
+    gd = g.astype(np.float64)
+    # zero gradients from step 1 -> unchanged
+    po, mo, vo, no = gio.adan(p, z, z, z, z, z, 1, lr)
+    assert np.array_equal(po, p.astype(np.float64)) and not mo.any() and not no.any()
+    # constant gradient g from step 1: d = 0, m^ = g, n^ = g^2 -> p - lr g/(|g|+eps)
+    want = p.astype(np.float64) - float(np.float32(lr)) * gd / (np.abs(gd) + float(np.float32(1e-8)))
+    for t in (1, 2, 9):
+        m = ((1 - b1 ** (t - 1)) * gd).astype(np.float32)
+        n = ((1 - b3 ** (t - 1)) * gd ** 2).astype(np.float32)
+        po, mo, vo, no = gio.adan(p, g, m, z, n, g if t > 1 else z, t, lr)
+        assert np.allclose(po, want, rtol=1e-6, atol=1e-9)
+        assert not vo.any()
+    # the gradient-difference term: g1 = 0 then g2 = a gives, by hand,
+    # step = lr sign(a) [1/(1+b1) + b2/(1+b2)] (1+b3)^(1/2) / (1+b2)  (eps -> 0)
+    a = np.array([0.7, -2.0, 1e-3], np.float32)
+    z3 = np.zeros(3, np.float32)
+    p3 = np.zeros(3, np.float32)
+    _, m1, v1, n1 = gio.adan(p3, z3, z3, z3, z3, z3, 1, lr, eps=0.0)
+    po, _, _, _ = gio.adan(p3, a, m1.astype(np.float32), v1.astype(np.float32),
+                           n1.astype(np.float32), z3, 2, lr, eps=0.0)
+    k = (1 / (1 + b1) + b2 / (1 + b2)) * math.sqrt(1 + b3) / (1 + b2)
+    assert abs(k - 0.7231) < 1e-3
+    assert np.allclose(po, -float(np.float32(lr)) * np.sign(a) * k, rtol=1e-12)
+    # f(x) = x^2 from x0 = 1, lr = 1e-2, 500 steps -> |x| < 1e-2
+    x = np.ones(1, np.float32)
+    st = [np.zeros(1, np.float32) for _ in range(4)]      # m, v, n, g_prev
+    for t in range(1, 501):
+        gg = (2 * x).astype(np.float32)
+        xo, mo, vo, no = gio.adan(x, gg, st[0], st[1], st[2], st[3], t, 1e-2)
+        x = xo.astype(np.float32)
+        st = [mo.astype(np.float32), vo.astype(np.float32), no.astype(np.float32), gg]
+    assert abs(float(x[0])) < 1e-2
