@@ -139,33 +139,29 @@ __global__ void __launch_bounds__(256) backward_tile_kernel(
         int q = 1;
         while (q < 8 && q * 2 * cnt <= 256) q <<= 1;
         // Lane groups take the Gaussians in descending order of per-lane work
-        // (rows per lane x row width) so that the lanes of a warp finish
-        // together: counting sort on the work (256 bins, shared memory).
-        sh.hist[threadIdx.x] = 0u;
+        // (rows per lane x row width, in 32 bins of 8) so that the lanes of a
+        // warp finish together: counting sort in shared memory, bins scanned
+        // by warp 0.
+        if (threadIdx.x < 32) sh.hist[threadIdx.x] = 0u;
         __syncthreads();
         uint32_t bin = 0;
         if ((int)threadIdx.x < cnt) {
             const int4 b = sh.sr.c[threadIdx.x];
             const int wdt = min(b.x + b.y - tx0, kTile - 1) - max(b.x - tx0, 0) + 1;
             const int hgt = min(b.z + b.w - ty0, kTile - 1) - max(b.z - ty0, 0) + 1;
-            bin = 255u - (uint32_t)min(255, ((hgt + q - 1) / q) * wdt);
+            bin = 31u - (uint32_t)min(31, (((hgt + q - 1) / q) * wdt) >> 3);
             atomicAdd(&sh.hist[bin], 1u);
         }
         __syncthreads();
-        {
-            const uint32_t v = sh.hist[threadIdx.x];
+        if (t.warp == 0) {
+            const uint32_t v = sh.hist[t.lane];
             uint32_t x = v;
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
                 const uint32_t y = __shfl_up_sync(kFull, x, o);
                 if (t.lane >= o) x += y;
             }
-            if (t.lane == 31) sh.scratch[t.warp] = x;
-            __syncthreads();
-            uint32_t before = 0;
-#pragma unroll
-            for (int w = 0; w < kWarps; ++w) before += w < t.warp ? sh.scratch[w] : 0u;
-            sh.hist[threadIdx.x] = before + x - v;            // exclusive start of the bin
+            sh.hist[t.lane] = x - v;                          // exclusive start of the bin
         }
         __syncthreads();
         if ((int)threadIdx.x < cnt) sh.perm[atomicAdd(&sh.hist[bin], 1u)] = threadIdx.x;
@@ -448,7 +444,8 @@ cudaError_t launch_backward_tiles(const Proj* proj, uint32_t* key_gid, const uin
     const double count = 3.0 * (double)f.width * (double)f.height;
     const float norm = (float)(2.0 / count);
     const bool mse = dL_dimage == nullptr;
-    cudaError_t e = launch_pdl(backward_tile_kernel, dim3(T, f.batch), dim3(256), s, proj, key_gid,
+    cudaError_t e = launch_pdl(backward_tile_kernel, dim3(TX, T / TX, f.batch), dim3(256), s, proj,
+                               key_gid,
                                tile_range, (const uint32_t*)w.gauss_off, n, f.width, f.height, T,
                                TX, presorted, dL_dimage, target, norm, cap, w.partial,
                                mse ? w.sse : nullptr, mse ? image_out : nullptr, cs);

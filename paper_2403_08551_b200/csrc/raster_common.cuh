@@ -36,12 +36,13 @@ struct TileCtx {
     bool in_image;
 };
 
+// Grid: (tiles_x, tiles_y, images) -- no integer division per CTA.
 __device__ __forceinline__ TileCtx make_tile_ctx(int W, int H, int TX) {
     TileCtx c;
-    c.tile = blockIdx.x;
-    c.img = blockIdx.y;
-    c.tx = c.tile % TX;
-    c.ty = c.tile / TX;
+    c.tx = blockIdx.x;
+    c.ty = blockIdx.y;
+    c.img = blockIdx.z;
+    c.tile = c.ty * TX + c.tx;
     c.lane = threadIdx.x & 31;
     c.warp = threadIdx.x >> 5;
     const int lx = (c.warp & 1) * 8 + (c.lane & 7);

@@ -68,7 +68,7 @@ cudaError_t launch_render(const Proj* proj, uint32_t* key_gid, const uint32_t* t
                           const gi_frame& f, bool presorted, float* image, const ChainState& cs,
                           cudaStream_t s) {
     const int TX = tiles_x(f.width), T = TX * tiles_y(f.height);
-    cudaError_t e = launch_pdl(render_kernel, dim3(T, f.batch), dim3(256), s, proj, key_gid,
+    cudaError_t e = launch_pdl(render_kernel, dim3(TX, T / TX, f.batch), dim3(256), s, proj, key_gid,
                                tile_range, n, f.width, f.height, T, TX, presorted, image, cs);
     note_launches(1);
     return e;
