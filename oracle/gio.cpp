@@ -43,11 +43,19 @@ namespace {
 // ---------------------------------------------------------------- activation
 // App. C: "apply the tanh function to limit the range of position
 // parameters to (-1,1)"; reading R2: mu_pix = (u + 1) * W / 2, y-down.
-// pos_mode 1 (decode path, P:254 / R19): params already hold u in (-1, 1).
+// pos_mode bit 0 (decode path, P:254 / R19): params already hold u in (-1, 1).
+// pos_mode bit 1 (NEXT-3): params[2:5] = (theta, s1, s2) of the rotation-
+// scaling factorisation Sigma = (RS)(RS)^T (Eq. 2-3) instead of the
+// Cholesky vector (l1, l2, l3) (Eq. 1).
+constexpr int kPosNormalized = 1;
+constexpr int kCovRS = 2;
+
 struct Gauss {
     double u[2];      // normalised position in [-1, 1]
     double mu[2];     // pixel-space centre
-    double l1e, l2, l3e;   // effective Cholesky factors, App. C "+0.5"
+    double l1e, l2, l3e;   // effective Cholesky factors, App. C "+0.5" (Cholesky mode)
+    double th, s1e, s2e;   // rotation angle, effective scales (RS mode, App. C "+0.5")
+    int rs;
     double S[3];      // Sigma = [[S0, S1], [S1, S2]]
     double Si[3];     // Sigma^-1
     double c[3];      // weighted colour c'
@@ -58,21 +66,35 @@ struct Gauss {
 void activate(const float* p, int pos_mode, int W, int H, Gauss& g) {
     for (int a = 0; a < 2; ++a) {
         double r = (double)p[a];
-        g.u[a] = pos_mode == 0 ? std::tanh(r) : r;
+        g.u[a] = (pos_mode & kPosNormalized) ? r : std::tanh(r);
     }
     g.mu[0] = (g.u[0] + 1.0) * ((double)W * 0.5);
     g.mu[1] = (g.u[1] + 1.0) * ((double)H * 0.5);
+    g.rs = (pos_mode & kCovRS) != 0;
     g.l1e = (double)p[2] + 0.5;   // App. C "add 0.5 to the diagonal elements l1, l3"
     g.l2 = (double)p[3];
     g.l3e = (double)p[4] + 0.5;
+    g.th = (double)p[2];          // App. C "... or the scaling elements s1, s2"
+    g.s1e = (double)p[3] + 0.5;
+    g.s2e = (double)p[4] + 0.5;
     for (int k = 0; k < 3; ++k) g.c[k] = (double)p[5 + k];
 }
 
 // Eq. 1: Sigma = L L^T with L = [[l1, 0], [l2, l3]]
+// Eq. 2-3: Sigma = (R S)(R S)^T, R = [[cos, -sin], [sin, cos]], S = diag(s1, s2)
 void covariance(Gauss& g) {
-    g.S[0] = g.l1e * g.l1e;
-    g.S[1] = g.l1e * g.l2;
-    g.S[2] = g.l2 * g.l2 + g.l3e * g.l3e;
+    if (!g.rs) {
+        g.S[0] = g.l1e * g.l1e;
+        g.S[1] = g.l1e * g.l2;
+        g.S[2] = g.l2 * g.l2 + g.l3e * g.l3e;
+        return;
+    }
+    const double c = std::cos(g.th), s = std::sin(g.th);
+    const double R[2][2] = {{c, -s}, {s, c}};
+    const double M[2][2] = {{R[0][0] * g.s1e, R[0][1] * g.s2e}, {R[1][0] * g.s1e, R[1][1] * g.s2e}};
+    g.S[0] = M[0][0] * M[0][0] + M[0][1] * M[0][1];
+    g.S[1] = M[0][0] * M[1][0] + M[0][1] * M[1][1];
+    g.S[2] = M[1][0] * M[1][0] + M[1][1] * M[1][1];
 }
 
 // closed-form inverse of a symmetric 2x2 matrix (adjugate / determinant)
@@ -102,14 +124,23 @@ void box_fp32(Gauss& g, const float* p, float k, int W, int H) {
     int ix = (int)fix, iy = (int)fiy;
     float fx = (float)(mx - fix);
     float fy = (float)(my - fiy);
-    float l1e = p[2] + 0.5f;
-    float l2 = p[3];
-    float l3e = p[4] + 0.5f;
-    if (l1e == 0.0f || l3e == 0.0f) return;                       // R8 cull
-    float rx = k * std::fabs(l1e);                                // k sqrt(Sxx)
-    float l2sq = l2 * l2;
-    float l3sq = l3e * l3e;
-    float ry = k * std::sqrt(l2sq + l3sq);                        // k sqrt(Syy)
+    float rx, ry;
+    if (!g.rs) {
+        float l1e = p[2] + 0.5f;
+        float l2 = p[3];
+        float l3e = p[4] + 0.5f;
+        if (l1e == 0.0f || l3e == 0.0f) return;                   // R8 cull
+        rx = k * std::fabs(l1e);                                  // k sqrt(Sxx)
+        float l2sq = l2 * l2;
+        float l3sq = l3e * l3e;
+        ry = k * std::sqrt(l2sq + l3sq);                          // k sqrt(Syy)
+    } else {
+        // RS: Sxx, Syy from the fp64 covariance (Eq. 2-3), rounded once
+        float s1e = p[3] + 0.5f, s2e = p[4] + 0.5f;
+        if (s1e == 0.0f || s2e == 0.0f) return;                   // singular Sigma
+        rx = k * std::sqrt((float)g.S[0]);
+        ry = k * std::sqrt((float)g.S[2]);
+    }
     float cx = fx - 0.5f, cy = fy - 0.5f;
     float lox = cx - rx, hix = cx + rx;
     float loy = cy - ry, hiy = cy + ry;
@@ -208,6 +239,42 @@ void chol_backward(const double Gm[3], double l1, double l2, double l3, double d
     dl[2] = 2.0 * Gm[2] * l3;
 }
 
+// App. A.2 rotation-scaling: dL/dtheta = <G, dR/dtheta S S^T R^T +
+// R S S^T dR^T/dtheta>; dL/ds_i = <G, R diag(2 s_i e_i) R^T> (the elided inner
+// products of P:682-697 completed as in SPEC.md:188).
+void rs_backward(const double Gm[3], double th, double s1, double s2, double d[3]) {
+    const double c = std::cos(th), s = std::sin(th);
+    const double G[2][2] = {{Gm[0], Gm[1]}, {Gm[1], Gm[2]}};
+    const double R[2][2] = {{c, -s}, {s, c}};
+    const double Rt[2][2] = {{c, s}, {-s, c}};
+    const double dR[2][2] = {{-s, -c}, {c, -s}};
+    const double dRt[2][2] = {{-s, c}, {-c, -s}};
+    const double SS[2][2] = {{s1 * s1, 0.0}, {0.0, s2 * s2}};
+    auto mul = [](const double A[2][2], const double B[2][2], double C[2][2]) {
+        for (int i = 0; i < 2; ++i)
+            for (int j = 0; j < 2; ++j) C[i][j] = A[i][0] * B[0][j] + A[i][1] * B[1][j];
+    };
+    auto frob = [](const double A[2][2], const double B[2][2]) {
+        return A[0][0] * B[0][0] + A[0][1] * B[0][1] + A[1][0] * B[1][0] + A[1][1] * B[1][1];
+    };
+    double T1[2][2], T2[2][2], T3[2][2], T4[2][2], dS[2][2];
+    mul(dR, SS, T1); mul(T1, Rt, T2);               // dR S S^T R^T
+    mul(R, SS, T3);  mul(T3, dRt, T4);              // R S S^T dR^T
+    for (int i = 0; i < 2; ++i)
+        for (int j = 0; j < 2; ++j) dS[i][j] = T2[i][j] + T4[i][j];
+    d[0] = frob(G, dS);
+    const double D1[2][2] = {{2.0 * s1, 0.0}, {0.0, 0.0}};
+    const double D2[2][2] = {{0.0, 0.0}, {0.0, 2.0 * s2}};
+    mul(R, D1, T1); mul(T1, Rt, T2);
+    d[1] = frob(G, T2);
+    mul(R, D2, T1); mul(T1, Rt, T2);
+    d[2] = frob(G, T2);
+}
+
+bool singular(const Gauss& g) {
+    return g.rs ? (g.s1e == 0.0 || g.s2e == 0.0) : (g.l1e == 0.0 || g.l3e == 0.0);
+}
+
 }  // namespace
 
 extern "C" {
@@ -230,6 +297,11 @@ void gio_set_threads(int t) {
 
 // Eq. 5, exposed for pins.
 double gio_eval_sigma(const double* Si, double dx, double dy) { return eval_sigma(Si, dx, dy); }
+
+// A.2 rotation-scaling backward, exposed for pins.
+void gio_rs_backward(const double* G, double th, double s1e, double s2e, double* d) {
+    rs_backward(G, th, s1e, s2e, d);
+}
 
 // A.2 Cholesky backward, exposed for pins.
 void gio_chol_backward(const double* G, double l1e, double l2, double l3e, double* dl) {
@@ -314,7 +386,7 @@ void gio_render(const float* params, int n, int W, int H, float k, int ts, int p
             } else {
                 for (int i = 0; i < n; ++i) {
                     const Gauss& g = gs[i];
-                    if (g.l1e == 0.0 || g.l3e == 0.0) continue;
+                    if (singular(g)) continue;
                     add(g);
                 }
             }
@@ -354,7 +426,7 @@ void gio_backward(const float* params, int n, int W, int H, float k, int ts, int
         if (mode != 2) {
             if (!G.valid) continue;
             x0 = G.box[0]; x1 = G.box[1]; y0 = G.box[2]; y1 = G.box[3];
-        } else if (G.l1e == 0.0 || G.l3e == 0.0) {
+        } else if (singular(G)) {
             continue;
         }
         double dc[3] = {0, 0, 0};
@@ -385,11 +457,12 @@ void gio_backward(const float* params, int n, int W, int H, float k, int ts, int
             }
         }
         double dl[3];
-        chol_backward(Gm, G.l1e, G.l2, G.l3e, dl);
+        if (G.rs) rs_backward(Gm, G.th, G.s1e, G.s2e, dl);      // NEXT-3
+        else chol_backward(Gm, G.l1e, G.l2, G.l3e, dl);
         double dl1 = dl[0], dl2 = dl[1], dl3 = dl[2];
         // activation chain (App. C): mu = (tanh(r) + 1) W/2 => dmu/dr = W/2 sech^2 r
         double sx, sy;
-        if (pos_mode == 0) {
+        if ((pos_mode & kPosNormalized) == 0) {
             double chx = std::cosh((double)params[8 * (size_t)i]);
             double chy = std::cosh((double)params[8 * (size_t)i + 1]);
             sx = (double)W * 0.5 / (chx * chx);

@@ -18,6 +18,7 @@ _LIB = os.path.join(_HERE, "libgio.so")
 
 POS_LOGIT = 0
 POS_NORMALIZED = 1
+COV_RS = 2          # OR-ed into pos_mode: params[2:5] = (theta, s1, s2) (Eq. 2-3, NEXT-3)
 ALL_PAIRS, TILED, DENSE = 0, 1, 2
 
 
@@ -42,6 +43,7 @@ def lib():
         L.gio_eval_sigma.argtypes = [dp, C.c_double, C.c_double]
         L.gio_inverse2.argtypes = [dp, dp]
         L.gio_chol_backward.argtypes = [dp, C.c_double, C.c_double, C.c_double, dp]
+        L.gio_rs_backward.argtypes = [dp, C.c_double, C.c_double, C.c_double, dp]
         L.gio_project.argtypes = [fp, C.c_int, C.c_int, C.c_int, C.c_float, C.c_int, C.c_int,
                                   dp, dp, dp, ip, ip, up]
         L.gio_bin.restype = C.c_int64
@@ -105,6 +107,13 @@ def chol_backward(G, l1e, l2, l3e):
     out = np.zeros(3)
     lib().gio_chol_backward(_p(g, C.c_double), float(l1e), float(l2), float(l3e),
                             _p(out, C.c_double))
+    return out
+
+
+def rs_backward(G, th, s1e, s2e):
+    g = np.ascontiguousarray(G, dtype=np.float64)
+    out = np.zeros(3)
+    lib().gio_rs_backward(_p(g, C.c_double), float(th), float(s1e), float(s2e), _p(out, C.c_double))
     return out
 
 

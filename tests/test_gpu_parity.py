@@ -418,3 +418,39 @@ def test_fit_step_adan(gi, gio):
         fit.step()
     torch.cuda.synchronize()
     assert fit.check() == gi.GI_OK and float(fit.loss[0]) < loss
+
+
+def test_c3_backward_and_fit_step(gi, gio):
+    # configs[2] at full size: fused forward + L2 + backward and one fused fit
+    # step (the launch shape of a C3 fit) against the oracle, full gradient
+    from paper_2403_08551_b200.pipeline import Fitter
+    W, H, n = 2040, 1356, 100000
+    p = synth.init_params(2, n)
+    tgt = synth.image(2, W, H)
+    img, loss, g = gio.loss_and_grads(p, tgt, mode=gio.TILED)
+    out = run_gpu(gi, p[None], W, H, target_b=tgt[None])
+    assert np.abs(out["image"][0] - img).max() <= PIX_TOL
+    assert max(group_err(out["grads"][0], g).values()) <= GRAD_TOL
+    assert abs(out["loss"][0] - loss) <= 1e-5 * loss
+    fit = Fitter(to_dev(p)[None].contiguous(), to_dev(tgt)[None].contiguous())
+    fit.step()
+    torch.cuda.synchronize()
+    assert fit.check() == gi.GI_OK
+    assert abs(float(fit.loss[0]) - loss) <= 1e-5 * loss
+    assert max(group_err(fit.grads[0].cpu().numpy().astype(np.float64), g).values()) <= GRAD_TOL
+
+
+def test_batched_fit_step(gi, gio):
+    # configs[3] pattern: 4 images in one fused fit step, per-image parity
+    from paper_2403_08551_b200.pipeline import Fitter
+    W, H, n, B = 160, 96, 1500, 4
+    pb = np.stack([synth.init_params(40 + b, n) for b in range(B)])
+    tb = np.stack([synth.image(40 + b, W, H) for b in range(B)])
+    fit = Fitter(to_dev(pb).contiguous(), to_dev(tb).contiguous())
+    fit.step()
+    torch.cuda.synchronize()
+    assert fit.check() == gi.GI_OK
+    for b in range(B):
+        img, loss, g = gio.loss_and_grads(pb[b], tb[b], mode=gio.ALL_PAIRS)
+        assert abs(float(fit.loss[b]) - loss) <= 1e-5 * loss
+        assert max(group_err(fit.grads[b].cpu().numpy().astype(np.float64), g).values()) <= GRAD_TOL

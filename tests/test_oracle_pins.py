@@ -483,3 +483,80 @@ def test_adan_closed_forms(gio):
         x = xo.astype(np.float32)
         st = [mo.astype(np.float32), vo.astype(np.float32), no.astype(np.float32), gg]
     assert abs(float(x[0])) < 1e-2
+
+
+# ---------------------------------------------- NEXT-3: rotation-scaling (RS)
+RS = 2   # pos_mode bit: params[2:5] = (theta, s1, s2), Sigma = (RS)(RS)^T (Eq. 2-3)
+
+
+def test_rs_covariance_worked_examples(gio):
+    # RS raw (theta = 0, s1 = 0.5, s2 = 1.5) -> Sigma = [[1,0],[0,4]]
+    pr = gio.project(one((0, 0), (0.0, 0.5, 1.5), (1, 1, 1)), 64, 64, pos_mode=NORM | RS)
+    assert np.array_equal(pr["sigma"][0], [1.0, 0.0, 4.0])
+    # a quarter turn swaps the axes (Eq. 3 R(theta))
+    th = np.float32(np.pi / 2)
+    pr = gio.project(one((0, 0), (th, 0.5, 1.5), (1, 1, 1)), 64, 64, pos_mode=NORM | RS)
+    assert np.allclose(pr["sigma"][0], [4.0, 0.0, 1.0], atol=1e-6)
+    # eigen-structure: det = (s1 s2)^2, trace = s1^2 + s2^2 for any theta
+    rng = np.random.default_rng(4)
+    for _ in range(50):
+        t, a, b = rng.uniform(-4, 4), rng.uniform(0.1, 3), rng.uniform(0.1, 3)
+        p = one((0, 0), (t, a - 0.5, b - 0.5), (1, 1, 1))
+        S = gio.project(p, 64, 64, pos_mode=NORM | RS)["sigma"][0]
+        a32, b32 = float(np.float32(a - 0.5)) + 0.5, float(np.float32(b - 0.5)) + 0.5
+        assert abs(S[0] * S[2] - S[1] ** 2 - (a32 * b32) ** 2) < 1e-9 * (a32 * b32) ** 2
+        assert abs(S[0] + S[2] - a32 ** 2 - b32 ** 2) < 1e-12 * (a32 ** 2 + b32 ** 2)
+
+
+def test_rs_box_and_equivalence_with_cholesky(gio):
+    # theta = 0, s = (3.5, 0.5) -> Sigma = diag(16, 1): half extents (12, 3)
+    pr = gio.project(one((0, 0), (0.0, 3.5, 0.5), (1, 1, 1)), 101, 101, pos_mode=NORM | RS)
+    assert list(pr["box"][0]) == [38, 62, 47, 53]
+    # the same Sigma through the Cholesky parameterisation renders the same
+    # image (both factorisations express the same Sigma)
+    rng = np.random.default_rng(8)
+    for _ in range(20):
+        t, a, b = rng.uniform(-3, 3), rng.uniform(0.6, 2.5), rng.uniform(0.6, 2.5)
+        prs = one((0.05, -0.03), (t, a - 0.5, b - 0.5), (0.7, -0.2, 0.4))
+        S = gio.project(prs, 48, 40, pos_mode=NORM | RS)["sigma"][0]
+        l1 = np.sqrt(S[0]); l2 = S[1] / l1; l3 = np.sqrt(S[2] - l2 * l2)
+        pch = one((0.05, -0.03), (l1 - 0.5, l2, l3 - 0.5), (0.7, -0.2, 0.4))
+        a_img = gio.render(prs, 48, 40, pos_mode=NORM | RS, mode=gio.DENSE)
+        b_img = gio.render(pch, 48, 40, pos_mode=NORM, mode=gio.DENSE)
+        assert np.abs(a_img - b_img).max() < 2e-6
+
+
+def test_rs_backward_worked_examples(gio):
+    # theta = 0 and G diagonal -> dtheta = 0;
+    # G = [[1,0],[0,0]], theta = 0, s = (1,1) -> ds1 = 2, ds2 = 0
+    d = gio.rs_backward([0.7, 0.0, -1.3], 0.0, 1.2, 0.8)
+    assert abs(d[0]) < 1e-15
+    assert list(gio.rs_backward([1.0, 0.0, 0.0], 0.0, 1.0, 1.0)) == [0.0, 2.0, 0.0]
+    # FD of <G, Sigma(theta, s1, s2)> (Frobenius, symmetric G)
+    G = np.array([0.4, -0.9, 0.25]); x = np.array([0.7, 1.3, 0.6])
+
+    def f(t, a, b):
+        c, s = np.cos(t), np.sin(t)
+        R = np.array([[c, -s], [s, c]])
+        Sg = R @ np.diag([a * a, b * b]) @ R.T
+        return G[0] * Sg[0, 0] + 2 * G[1] * Sg[0, 1] + G[2] * Sg[1, 1]
+    h = 1e-6
+    fd = [(f(*(x + h * e)) - f(*(x - h * e))) / (2 * h) for e in np.eye(3)]
+    assert np.allclose(gio.rs_backward(G, *x), fd, rtol=1e-8)
+
+
+@pytest.mark.parametrize("seed", range(3))
+def test_rs_backward_matches_finite_differences(gio, seed):
+    rng = np.random.default_rng(300 + seed)
+    n, W, H = 3, 12, 10
+    p = synth.init_params(seed, n)
+    p[:, 2] = rng.uniform(-3, 3, size=n).astype(np.float32)          # theta
+    p[:, 3:5] = rng.uniform(0.3, 1.5, size=(n, 2)).astype(np.float32)  # s1, s2
+    p[:, 5:8] = rng.uniform(-1, 1, size=(n, 3)).astype(np.float32)
+    target = rng.uniform(0, 1, size=(3, H, W)).astype(np.float32)
+    img = gio.render(p, W, H, pos_mode=RS, mode=gio.DENSE)
+    _, g = gio.mse(img, target)
+    an = gio.backward(p, g, W, H, pos_mode=RS, mode=gio.DENSE)
+    fd = _fd_grads(gio, p, target, gio.DENSE, pos_mode=RS, h=1e-4)
+    err = np.abs(an - fd) / np.maximum(np.abs(fd), 1e-6)
+    assert err.max() < 1e-5, err.max()
