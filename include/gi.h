@@ -58,9 +58,14 @@ typedef struct {
     float k;                /* box half-extent in standard deviations (R6), >0 */
 } gi_frame;
 
-/* Position parameterisation of params[0:2]. */
+/* Parameterisation flags (bit field).  Position, params[0:2]: */
 #define GI_POS_LOGIT 0u       /* raw logits, u = tanh(mu_raw) (App. C)  */
 #define GI_POS_NORMALIZED 1u  /* already u in [-1,1] (decode path, R19) */
+/* Covariance, params[2:5]: Cholesky (l1, l2, l3), Sigma = L L^T (Eq. 1), the
+ * default; or, OR-ed in, the rotation-scaling factorisation (theta, s1, s2),
+ * Sigma = (R S)(R S)^T with S = diag(s1 + 1/2, s2 + 1/2) (Eq. 2-3, App. C;
+ * NEXT-3); its gradients follow App. A.2. */
+#define GI_COV_RS 2u
 
 /* Size in bytes of one projected-Gaussian record (opaque, 16-B aligned). */
 #define GI_PROJ_BYTES 48

@@ -126,7 +126,7 @@ gi_status gi_project(const float* params, int32_t n, const gi_frame* f, uint32_t
                      uint32_t* tiles_touched, void* stream) {
     gi_status st;
     if ((st = check_frame(f)) != GI_OK || (st = check_n(n, f)) != GI_OK) return st;
-    if (flags != GI_POS_LOGIT && flags != GI_POS_NORMALIZED) return invalid("flags");
+    if (!gi::flags_valid(flags)) return invalid("flags");
     if (n > 0 && (!params || !proj || !tiles_touched)) return invalid("NULL buffer");
     if (!aligned16(params) || !aligned16(proj)) return invalid("params/proj must be 16-B aligned");
     if (n == 0) return GI_OK;
@@ -181,7 +181,7 @@ gi_status gi_render_backward(const float* params, const void* proj, const uint32
                              float* loss, float* image_out, void* stream) {
     gi_status st;
     if ((st = check_frame(f)) != GI_OK || (st = check_n(n, f)) != GI_OK) return st;
-    if (flags != GI_POS_LOGIT && flags != GI_POS_NORMALIZED) return invalid("flags");
+    if (!gi::flags_valid(flags)) return invalid("flags");
     if (key_capacity < 0 || key_capacity >= (1LL << 31)) return invalid("key_capacity");
     if (ws_bytes < gi::backward_ws_bytes(n, key_capacity, *f)) return invalid("backward workspace too small");
     if (!dL_dimage && !target) return invalid("need dL_dimage or target");
@@ -256,7 +256,7 @@ static gi_status fit_step_impl(float* params, float* grads, float* m, float* v, 
                                bool chained) {
     gi_status st;
     if ((st = check_frame(f)) != GI_OK || (st = check_n(n, f)) != GI_OK) return st;
-    if (flags != GI_POS_LOGIT && flags != GI_POS_NORMALIZED) return invalid("flags");
+    if (!gi::flags_valid(flags)) return invalid("flags");
     if (key_capacity < 0 || key_capacity >= (1LL << 31)) return invalid("key_capacity");
     if (half_every < 1) return invalid("half_every");
     if (!(beta1 >= 0.f && beta1 < 1.f && beta2 >= 0.f && beta2 < 1.f)) return invalid("betas");
@@ -322,7 +322,7 @@ gi_status gi_fit_step_adan(float* params, float* grads, float* m, float* v, floa
                            uint32_t* status_flags, void* stream) {
     gi_status st;
     if ((st = check_frame(f)) != GI_OK || (st = check_n(n_gauss, f)) != GI_OK) return st;
-    if (flags != GI_POS_LOGIT && flags != GI_POS_NORMALIZED) return invalid("flags");
+    if (!gi::flags_valid(flags)) return invalid("flags");
     if (key_capacity < 0 || key_capacity >= (1LL << 31)) return invalid("key_capacity");
     if (half_every < 1) return invalid("half_every");
     if (!(beta1 >= 0.f && beta1 < 1.f && beta2 >= 0.f && beta2 < 1.f && beta3 >= 0.f && beta3 < 1.f))
@@ -370,7 +370,7 @@ gi_status gi_fit_prime(const float* params, int32_t n, const gi_frame* f, uint32
                        int64_t key_capacity, void* fit_ws, size_t ws_bytes, void* stream) {
     gi_status st;
     if ((st = check_frame(f)) != GI_OK || (st = check_n(n, f)) != GI_OK) return st;
-    if (flags != GI_POS_LOGIT && flags != GI_POS_NORMALIZED) return invalid("flags");
+    if (!gi::flags_valid(flags)) return invalid("flags");
     if (key_capacity < 0 || key_capacity >= (1LL << 31)) return invalid("key_capacity");
     if (!fit_ws || ws_bytes < carve_fit(nullptr, n, key_capacity, *f).bytes)
         return invalid("fit workspace too small");
@@ -401,7 +401,7 @@ gi_status gi_render_frame(const float* params, int32_t n, const gi_frame* f, uin
                           void* stream) {
     gi_status st;
     if ((st = check_frame(f)) != GI_OK || (st = check_n(n, f)) != GI_OK) return st;
-    if (flags != GI_POS_LOGIT && flags != GI_POS_NORMALIZED) return invalid("flags");
+    if (!gi::flags_valid(flags)) return invalid("flags");
     if (key_capacity < 0 || key_capacity >= (1LL << 31)) return invalid("key_capacity");
     if (!frame_ws || ws_bytes < carve_fit(nullptr, n, key_capacity, *f).bytes)
         return invalid("frame workspace too small");

@@ -322,8 +322,8 @@ __global__ void __launch_bounds__(256) finalize_kernel(
         any = true;
     }
     float4 r0 = make_float4(0.f, 0.f, 0.f, 0.f), r1 = r0;
-    if (any) {
-        // fp32 (the 1e-4 gradient bar leaves ample room); reciprocals once
+    if (any && !cov_rs(flags)) {
+        // Cholesky, fp32 (the 1e-4 gradient bar leaves ample room)
         const float l1 = p0.z + 0.5f, l2 = p0.w, l3 = p1.x + 0.5f;
         const float il1 = 1.0f / l1, il3 = 1.0f / l3;
         const float ik = (float)(1.0 / kKappa), ik2 = (float)(1.0 / (kKappa * kKappa));
@@ -332,18 +332,46 @@ __global__ void __launch_bounds__(256) finalize_kernel(
         const float l2l3 = l2 * il3;
         const float Ax = (Sp - Sq * l2l3) * il1;         // sum gamma dsigma/ddx
         const float Ay = Sq * il3;
+        r0.x = -Ax;                                       // dmu_pix = -dsigma/dd (R13)
+        r0.y = -Ay;
+        r0.z = -(Spp - Spq * l2l3) * il1;                 // dl1
+        r0.w = -Spq * il3;                                // dl2
+        r1.x = -Sqq * il3;                                // dl3
+    } else if (any) {
+        // NEXT-3 rotation-scaling: L = chol(Sigma) as in the projection, then
+        // G = dL/dSigma = -1/2 L^-T M L^-1 with M = sum gamma (p, q)(p, q)^T,
+        // chained through Sigma(theta, s1, s2) (App. A.2).
+        const double th = (double)p0.z;
+        const double s1 = (double)__fadd_rn(p0.w, 0.5f), s2 = (double)__fadd_rn(p1.x, 0.5f);
+        double Sg[3];
+        rs_sigma(th, s1, s2, Sg);
+        const double l1 = sqrt(Sg[0]), l2 = Sg[1] / l1, l3 = fabs(s1 * s2) / l1;
+        const double ik = 1.0 / kKappa, ik2 = ik * ik;
+        const double Sp = S[3] * ik, Sq = S[4] * ik;
+        const double Spp = S[5] * ik2, Spq = S[6] * ik2, Sqq = S[7] * ik2;
+        const double al = 1.0 / l1, be = -l2 / (l1 * l3), ga = 1.0 / l3;   // L^-1 = [[al,0],[be,ga]]
+        r0.x = (float)(-(al * Sp + be * Sq));             // dmu_pix = -L^-T (S_p, S_q)
+        r0.y = (float)(-(ga * Sq));
+        const double G11 = -0.5 * (al * al * Spp + 2.0 * al * be * Spq + be * be * Sqq);
+        const double G12 = -0.5 * (al * ga * Spq + be * ga * Sqq);
+        const double G22 = -0.5 * (ga * ga * Sqq);
+        const double c = cos(th), sn = sin(th);
+        const double s2t = 2.0 * sn * c, c2t = c * c - sn * sn;
+        r0.z = (float)((s1 * s1 - s2 * s2) * (-G11 * s2t + 2.0 * G12 * c2t + G22 * s2t));   // dtheta
+        r0.w = (float)(2.0 * s1 * (G11 * c * c + 2.0 * G12 * c * sn + G22 * sn * sn));     // ds1
+        r1.x = (float)(2.0 * s2 * (G11 * sn * sn - 2.0 * G12 * c * sn + G22 * c * c));     // ds2
+    }
+    if (any) {
+        // position activation chain (App. C): mu = (tanh(r) + 1) W/2
         float sx = (float)W * 0.5f, sy = (float)H * 0.5f;
-        if (flags == GI_POS_LOGIT) {
+        if (pos_logit(flags)) {
             const float chx = coshf(p0.x), chy = coshf(p0.y);
             sx /= chx * chx;
             sy /= chy * chy;
         }
-        r0.x = -Ax * sx;                                  // dmu = -dsigma/dd (R13)
-        r0.y = -Ay * sy;
-        r0.z = -(Spp - Spq * l2l3) * il1;                 // dl1
-        r0.w = -Spq * il3;                                // dl2
-        r1.x = -Sqq * il3;                                // dl3
-        r1.y = S[0];                                     // dc'
+        r0.x *= sx;
+        r0.y *= sy;
+        r1.y = S[0];                                      // dc'
         r1.z = S[1];
         r1.w = S[2];
     }

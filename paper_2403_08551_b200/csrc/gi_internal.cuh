@@ -234,4 +234,19 @@ cudaError_t launch_psnr(const float* image, const float* target, const gi_frame&
 
 inline size_t align_up(size_t x, size_t a = 256) { return (x + a - 1) / a * a; }
 
+__host__ __device__ inline bool pos_logit(uint32_t flags) { return (flags & GI_POS_NORMALIZED) == 0u; }
+__host__ __device__ inline bool cov_rs(uint32_t flags) { return (flags & GI_COV_RS) != 0u; }
+inline bool flags_valid(uint32_t flags) { return (flags & ~(GI_POS_NORMALIZED | GI_COV_RS)) == 0u; }
+
+// Rotation-scaling covariance (Eq. 2-3) in fp64 with a fixed operation order
+// (no contraction): Sigma = M M^T, M = R(theta) diag(s1e, s2e).
+__device__ __forceinline__ void rs_sigma(double th, double s1e, double s2e, double S[3]) {
+    const double c = cos(th), s = sin(th);
+    const double m00 = __dmul_rn(c, s1e), m01 = __dmul_rn(-s, s2e);
+    const double m10 = __dmul_rn(s, s1e), m11 = __dmul_rn(c, s2e);
+    S[0] = __dadd_rn(__dmul_rn(m00, m00), __dmul_rn(m01, m01));
+    S[1] = __dadd_rn(__dmul_rn(m00, m10), __dmul_rn(m01, m11));
+    S[2] = __dadd_rn(__dmul_rn(m10, m10), __dmul_rn(m11, m11));
+}
+
 }  // namespace gi

@@ -13,18 +13,21 @@ __device__ __forceinline__ uint32_t project_one(const float4 p0 /* mux, muy, l1,
                                                 Proj* __restrict__ proj, const BinCounts& bc) {
     // App. C: u = tanh(mu_raw); R2: mu = (u + 1) * W / 2  (fp64, no contraction)
     double ux = (double)p0.x, uy = (double)p0.y;
-    if (flags == GI_POS_LOGIT) {
+    if (pos_logit(flags)) {
         ux = tanh(ux);
         uy = tanh(uy);
     }
     const double mx = __dmul_rn(__dadd_rn(ux, 1.0), (double)W * 0.5);
     const double my = __dmul_rn(__dadd_rn(uy, 1.0), (double)H * 0.5);
 
-    // Effective Cholesky factors (App. C "+0.5" on l1, l3), fp32 as stored.
-    const float l1e = __fadd_rn(p0.z, 0.5f);
-    const float l2 = p0.w;
-    const float l3e = __fadd_rn(p1.x, 0.5f);
-
+    // Covariance factor: Cholesky (Eq. 1) or rotation-scaling (Eq. 2-3),
+    // App. C "+0.5" on l1, l3 resp. s1, s2 (fp32 as stored).
+    const bool rs = cov_rs(flags);
+    const float e1 = __fadd_rn(rs ? p0.w : p0.z, 0.5f);   // l1 + 1/2  |  s1 + 1/2
+    const float e2 = rs ? p0.z : p0.w;                    // l2        |  theta
+    const float e3 = __fadd_rn(p1.x, 0.5f);               // l3 + 1/2  |  s2 + 1/2
+    double Srs[3] = {0.0, 0.0, 0.0};
+    if (rs) rs_sigma((double)e2, (double)e1, (double)e3, Srs);
     Proj r;
     uint32_t bx = kEmptyBox, by = kEmptyBox, touched = 0;
     int ix = 0, iy = 0;
@@ -37,10 +40,14 @@ __device__ __forceinline__ uint32_t project_one(const float4 p0 /* mux, muy, l1,
         fx = __double2float_rn(mx - fix);
         fy = __double2float_rn(my - fiy);
     }
-    if (centre_ok && l1e != 0.0f && l3e != 0.0f) {
-        // R6/R7: half extents k sqrt(Sxx) = k |l1e|, k sqrt(Syy) = k sqrt(l2^2 + l3e^2)
-        const float rx = __fmul_rn(k, fabsf(l1e));
-        const float ry = __fmul_rn(k, __fsqrt_rn(__fadd_rn(__fmul_rn(l2, l2), __fmul_rn(l3e, l3e))));
+    if (centre_ok && e1 != 0.0f && e3 != 0.0f) {
+        // R6/R7: half extents k sqrt(Sxx), k sqrt(Syy): Cholesky k |l1e| and
+        // k sqrt(l2^2 + l3e^2) in fp32; RS from the fp64 Sigma rounded once
+        const float rx = rs ? __fmul_rn(k, __fsqrt_rn(__double2float_rn(Srs[0])))
+                            : __fmul_rn(k, fabsf(e1));
+        const float ry = rs ? __fmul_rn(k, __fsqrt_rn(__double2float_rn(Srs[2])))
+                            : __fmul_rn(k, __fsqrt_rn(__fadd_rn(__fmul_rn(e2, e2),
+                                                                __fmul_rn(e3, e3))));
         const float cx = __fsub_rn(fx, 0.5f), cy = __fsub_rn(fy, 0.5f);
         const float bw = (float)(W + 1), bh = (float)(H + 1);
         const float lox = fminf(fmaxf(__fsub_rn(cx, rx), -bw), bw);
@@ -64,12 +71,23 @@ __device__ __forceinline__ uint32_t project_one(const float4 p0 /* mux, muy, l1,
         }
     }
     // Sigma^-1 = L^-T L^-1 with L^-1 = [[1/l1, 0], [-l2/(l1 l3), 1/l3]], scaled by
-    // kappa so that sigma * log2(e) = (a dx)^2 + (b dx + c dy)^2.  IEEE fp32
-    // divisions (relative error <= 2 ulp -> < 1e-6 on sigma near the box edge).
-    const float kf = (float)kKappa;
-    const float ca = __fdiv_rn(kf, l1e);
-    const float cc = __fdiv_rn(kf, l3e);
-    const float cb = -__fdiv_rn(__fmul_rn(ca, l2), l3e);
+    // kappa so that sigma * log2(e) = (a dx)^2 + (b dx + c dy)^2.  Cholesky:
+    // IEEE fp32 divisions (< 1e-6 relative on sigma near the box edge).  RS:
+    // L = chol(Sigma) in fp64 (l3 = |s1 s2| / l1 since det Sigma = (s1 s2)^2).
+    float ca, cb, cc;
+    if (!rs) {
+        const float kf = (float)kKappa;
+        ca = __fdiv_rn(kf, e1);
+        cc = __fdiv_rn(kf, e3);
+        cb = -__fdiv_rn(__fmul_rn(ca, e2), e3);
+    } else {
+        const double l1 = sqrt(Srs[0]);
+        const double l2 = Srs[1] / l1;
+        const double l3 = fabs((double)e1 * (double)e3) / l1;
+        ca = (float)(kKappa / l1);
+        cb = (float)(-kKappa * l2 / (l1 * l3));
+        cc = (float)(kKappa / l3);
+    }
     r.q0 = make_float4(__int_as_float(ix), __int_as_float(iy), fx, fy);
     r.q1 = make_float4(ca, cb, cc, __uint_as_float(bx));
     r.q2 = make_float4(p1.y, p1.z, p1.w, __uint_as_float(by));

@@ -18,6 +18,7 @@ from . import build as _build
 GI_OK, GI_EINVAL, GI_ECUDA, GI_ECAPACITY, GI_EFORMAT, GI_ENONFINITE = range(6)
 GI_POS_LOGIT = 0
 GI_POS_NORMALIZED = 1
+GI_COV_RS = 2          # OR-ed flag: params[2:5] = (theta, s1, s2), Sigma = (RS)(RS)^T (NEXT-3)
 GI_PROJ_BYTES = 48
 TILE = 16
 

@@ -454,3 +454,57 @@ def test_batched_fit_step(gi, gio):
         img, loss, g = gio.loss_and_grads(pb[b], tb[b], mode=gio.ALL_PAIRS)
         assert abs(float(fit.loss[b]) - loss) <= 1e-5 * loss
         assert max(group_err(fit.grads[b].cpu().numpy().astype(np.float64), g).values()) <= GRAD_TOL
+
+
+def rs_params(seed, n, scale=1.0):
+    # NEXT-3: init-like rotation-scaling cloud (theta ~ U(-pi, pi), s ~ U[0,1) x scale)
+    p = synth.init_params(seed, n)
+    rng = np.random.default_rng(500 + seed)
+    p[:, 2] = rng.uniform(-np.pi, np.pi, size=n).astype(np.float32)
+    p[:, 3:5] = (rng.uniform(0.0, 1.0, size=(n, 2)) * scale).astype(np.float32)
+    return p
+
+
+@pytest.mark.parametrize("W,H,n,scale", [(64, 64, 256, 1.0), (70, 45, 300, 2.5), (768, 512, 70000, 1.0)])
+def test_rs_parity(gi, gio, W, H, n, scale):
+    RS = gi.GI_COV_RS
+    p = rs_params(n, n, scale)
+    tgt = synth.image(n % 7, W, H)
+    mode = gio.ALL_PAIRS if W * H * n <= 64 * 64 * 300 else gio.TILED
+    img, loss, g = gio.loss_and_grads(p, tgt, pos_mode=RS, mode=mode)
+    out = run_gpu(gi, p[None], W, H, flags=RS, target_b=tgt[None])
+    pr = gio.project(p, W, H, pos_mode=RS)
+    rec = out["pipe"].proj.view(-1, 12).cpu().numpy()
+    bx, by = rec[:, 7].view(np.uint32), rec[:, 11].view(np.uint32)
+    valid = pr["touched"] > 0
+    box = np.stack([bx & 0xffff, bx >> 16, by & 0xffff, by >> 16], 1).astype(np.int32)
+    assert np.array_equal(box[valid], pr["box"][valid])
+    kt, kg, _ = gio.bin(p, W, H, pos_mode=RS)
+    assert np.array_equal(u32(out["pipe"].key_gid)[: len(kg)], kg)
+    assert np.abs(out["image"][0] - img).max() <= PIX_TOL
+    assert max(group_err(out["grads"][0], g).values()) <= GRAD_TOL
+    assert abs(out["loss"][0] - loss) <= 1e-5 * max(loss, 1e-3)
+
+
+def test_rs_fit_steps(gi, gio):
+    # fused, chained and Adan fit steps in RS mode: gradients of step 1 vs the
+    # oracle; chained == plain bitwise over 4 steps
+    from paper_2403_08551_b200.pipeline import Fitter
+    RS = gi.GI_COV_RS
+    W, H, n = 96, 64, 600
+    p = rs_params(3, n)
+    tgt = synth.image(3, W, H)
+    _, loss, g = gio.loss_and_grads(p, tgt, pos_mode=RS, mode=gio.ALL_PAIRS)
+    res = []
+    for kw in (dict(chained=True), dict(chained=False), dict(optimizer="adan")):
+        fit = Fitter(to_dev(p)[None].contiguous(), to_dev(tgt)[None].contiguous(), flags=RS, **kw)
+        fit.step()
+        torch.cuda.synchronize()
+        assert fit.check() == gi.GI_OK
+        assert abs(float(fit.loss[0]) - loss) <= 1e-5 * loss
+        assert max(group_err(fit.grads[0].cpu().numpy().astype(np.float64), g).values()) <= GRAD_TOL
+        for _ in range(3):
+            fit.step()
+        torch.cuda.synchronize()
+        res.append(fit.params.clone())
+    assert torch.equal(res[0], res[1])
