@@ -31,17 +31,29 @@ namespace {
 
 struct BwdShared {
     StagedRecords sr;
-    WarpLists wl;
-    uint32_t sl[kSortMax];
+    union {
+        WarpLists wl;            // pass 1: per-warp candidate lists
+        float4 red[256][2];      // pass 2: the 8 sums of each chunk
+    } u;
+    alignas(16) uint32_t sl[kSortMax];
     float4 g[kTilePix];      // per-pixel upstream dL/dC (x, y, z), tile-local row-major
-    uint32_t slot[256];      // partial slot of each staged record
     uint32_t scratch[kWarps];
     float sse[kWarps];
-    uint32_t hist[256];      // pass-2 work histogram (descending work order)
-    uint32_t perm[256];      // pass-2 lane group -> record
+    uint32_t hist[64];       // pass-2 remainder-size histogram -> bin starts
+    uint32_t item[256];      // pass-2 chunk: record | k0 << 8 | k1 << 17
+    uint2 pa[kWarps], pb[kWarps];   // pass-2 per-warp partials
+    uint32_t pc[kWarps];
+    uint32_t n_items;
 };
 
-__global__ void __launch_bounds__(256) backward_tile_kernel(
+// floor(a / b) for 0 <= a < 2^16, 1 <= b < 2^16 given rb = 1/b (fp32): the
+// true quotient is at least 0.5/b away from an integer after the +0.5 shift,
+// far above the rounding error (< 2^-21 a / b).
+__device__ __forceinline__ uint32_t small_div(uint32_t a, float rb) {
+    return (uint32_t)(((float)a + 0.5f) * rb);
+}
+
+__global__ void __launch_bounds__(256, 5) backward_tile_kernel(
     const Proj* __restrict__ proj, uint32_t* __restrict__ key_gid,
     const uint32_t* __restrict__ tile_range, const uint32_t* __restrict__ gauss_off, int n,
     int W, int H, int T, int TX, bool presorted, const float* __restrict__ dL_dimage,
@@ -85,8 +97,8 @@ __global__ void __launch_bounds__(256) backward_tile_kernel(
             if (base > 0) __syncthreads();
             if ((int)threadIdx.x < cnt) stage_gid(sh.sr, proj, gid_at(base + threadIdx.x), threadIdx.x, t);
             __syncthreads();
-            const int nl = build_warp_list(sh.sr, sh.wl, cnt, t);
-            forward_batch(sh.sr, sh.wl, nl, t, acc0, acc1, acc2);
+            const int nl = build_warp_list(sh.sr, sh.u.wl, cnt, t);
+            forward_batch(sh.sr, sh.u.wl, nl, t, acc0, acc1, acc2);
         }
         staged_all = L <= 256u;
         float sq = 0.f;
@@ -119,106 +131,175 @@ __global__ void __launch_bounds__(256) backward_tile_kernel(
         sse_part[t.img * T + t.tile] = tot;
     }
 
-    // ---- pass 2: gradients, Gaussian-parallel ----
+    // ---- pass 2: gradients, Gaussian-parallel, work-balanced chunks ----
+    // Record j's in-tile box (w_j pixels, row-major) is cut into chunks of at
+    // most C pairs: floor(w_j / C) full chunks and one remainder.  C is the
+    // smallest of a few candidates >= ceil(sum w / 256) whose chunk count fits
+    // the 256 lanes (C = max w_j, one chunk per record, always fits).  Full
+    // chunks come first, remainders follow in descending size, so the lanes
+    // of a warp run nearly equal trip counts.  Each lane accumulates the 8
+    // sums of its chunk; thread j then adds its chunks in a fixed order.
     const int tx0 = t.tx * kTile, ty0 = t.ty * kTile;
+    const int j = threadIdx.x;
     for (uint32_t base = 0; base < L; base += 256) {
         const int cnt = (int)min(256u, L - base);
         __syncthreads();
-        if ((int)threadIdx.x < cnt) {
-            const uint32_t gid = gid_at(base + threadIdx.x);
-            if (!staged_all) stage_gid(sh.sr, proj, gid, threadIdx.x, t);
+        if (j < 64) sh.hist[j] = 0u;
+        uint32_t slot = 0, wj = 0;
+        if (j < cnt) {
+            const uint32_t gid = gid_at(base + j);
+            if (!staged_all) stage_gid(sh.sr, proj, gid, j, t);
             // slot: the Gaussian's contiguous partial range, tile rank in its
             // rectangle (row-major) -- the same order finalize sums in
-            const int4 b = sh.sr.c[threadIdx.x];
+            const int4 b = sh.sr.c[j];
             const int rtx0 = b.x / kTile, rtx1 = (b.x + b.y) / kTile, rty0 = b.z / kTile;
-            sh.slot[threadIdx.x] =
-                gauss_off[gid] + (uint32_t)((t.ty - rty0) * (rtx1 - rtx0 + 1) + (t.tx - rtx0));
-        }
-        __syncthreads();
-        // q lanes per Gaussian (power of two, <= 8, q * cnt <= 256)
-        int q = 1;
-        while (q < 8 && q * 2 * cnt <= 256) q <<= 1;
-        // Lane groups take the Gaussians in descending order of per-lane work
-        // (rows per lane x row width, in 32 bins of 8) so that the lanes of a
-        // warp finish together: counting sort in shared memory, bins scanned
-        // by warp 0.
-        if (threadIdx.x < 32) sh.hist[threadIdx.x] = 0u;
-        __syncthreads();
-        uint32_t bin = 0;
-        if ((int)threadIdx.x < cnt) {
-            const int4 b = sh.sr.c[threadIdx.x];
+            slot = gauss_off[gid] + (uint32_t)((t.ty - rty0) * (rtx1 - rtx0 + 1) + (t.tx - rtx0));
             const int wdt = min(b.x + b.y - tx0, kTile - 1) - max(b.x - tx0, 0) + 1;
             const int hgt = min(b.z + b.w - ty0, kTile - 1) - max(b.z - ty0, 0) + 1;
-            bin = 31u - (uint32_t)min(31, (((hgt + q - 1) / q) * wdt) >> 3);
-            atomicAdd(&sh.hist[bin], 1u);
+            wj = (uint32_t)(wdt * hgt);
+        }
+        // (1) sum and max of w over the batch
+        {
+            const uint32_t ws = __reduce_add_sync(kFull, wj), wm = __reduce_max_sync(kFull, wj);
+            if (t.lane == 0) sh.pa[t.warp] = make_uint2(ws, wm);
         }
         __syncthreads();
+        uint32_t tot = 0, mx = 0;
+#pragma unroll
+        for (int w = 0; w < kWarps; ++w) {
+            const uint2 x = sh.pa[w];
+            tot += x.x;
+            mx = max(mx, x.y);
+        }
+        // (2) chunk counts of the candidate chunk sizes
+        const uint32_t c0 = (tot + 255u) >> 8;
+        const uint32_t c1 = c0 + ((c0 + 3u) >> 2), c2 = c0 + ((c0 + 1u) >> 1);
+        {
+            uint32_t n01 = 0, n2 = 0;
+            if (j < cnt) {
+                n01 = small_div(wj + c0 - 1u, 1.0f / (float)c0) |
+                      small_div(wj + c1 - 1u, 1.0f / (float)c1) << 16;
+                n2 = small_div(wj + c2 - 1u, 1.0f / (float)c2);
+            }
+            n01 = __reduce_add_sync(kFull, n01);
+            n2 = __reduce_add_sync(kFull, n2);
+            if (t.lane == 0) sh.pb[t.warp] = make_uint2(n01, n2);
+        }
+        __syncthreads();
+        uint32_t C = mx;
+        {
+            uint32_t n01 = 0, n2 = 0;
+#pragma unroll
+            for (int w = 0; w < kWarps; ++w) {
+                const uint2 x = sh.pb[w];
+                n01 += x.x;
+                n2 += x.y;
+            }
+            if (n2 <= 256u) C = c2;
+            if ((n01 >> 16) <= 256u) C = c1;
+            if ((n01 & 0xffffu) <= 256u) C = c0;
+        }
+        // (3) full chunks: block scan of their counts; remainders: size bins
+        const uint32_t nf = small_div(wj, 1.0f / (float)C), rm = wj - nf * C;
+        uint32_t incl = nf;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(kFull, incl, o);
+            if (t.lane >= o) incl += y;
+        }
+        if (t.lane == 31) sh.pc[t.warp] = incl;
+        const uint32_t rbin = 64u - min(rm, 64u);        // larger remainder -> lower bin
+        uint32_t rrank = 0;
+        if (rm != 0u) rrank = atomicAdd(&sh.hist[rbin], 1u);
+        __syncthreads();
+        uint32_t F = 0, fstart = incl - nf;
+#pragma unroll
+        for (int w = 0; w < kWarps; ++w) {
+            const uint32_t x = sh.pc[w];
+            fstart += w < t.warp ? x : 0u;
+            F += x;
+        }
         if (t.warp == 0) {
-            const uint32_t v = sh.hist[t.lane];
+            const uint32_t h0 = sh.hist[2 * t.lane], h1 = sh.hist[2 * t.lane + 1];
+            const uint32_t v = h0 + h1;
             uint32_t x = v;
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
                 const uint32_t y = __shfl_up_sync(kFull, x, o);
                 if (t.lane >= o) x += y;
             }
-            sh.hist[t.lane] = x - v;                          // exclusive start of the bin
+            sh.hist[2 * t.lane] = F + x - v;
+            sh.hist[2 * t.lane + 1] = F + x - v + h0;
+            if (t.lane == 31) sh.n_items = F + x;
         }
         __syncthreads();
-        if ((int)threadIdx.x < cnt) sh.perm[atomicAdd(&sh.hist[bin], 1u)] = threadIdx.x;
-        __syncthreads();
-        const int kk = threadIdx.x / q;         // lane group (work rank)
-        const int j = kk < cnt ? (int)sh.perm[kk] : cnt;   // Gaussian of this lane
-        const int ph = threadIdx.x % q;         // row phase
-        float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f, a4 = 0.f, a5 = 0.f, a6 = 0.f, a7 = 0.f;
+        const uint32_t rpos = rm != 0u ? sh.hist[rbin] + rrank : 0u;
         if (j < cnt) {
-            const float4 A = sh.sr.a[j];
-            const float4 B = sh.sr.b[j];
-            const int4 Cb = sh.sr.c[j];
+            for (uint32_t i = 0; i < nf; ++i)
+                sh.item[fstart + i] = (uint32_t)j | (i * C) << 8 | ((i + 1u) * C) << 17;
+            if (rm != 0u) sh.item[rpos] = (uint32_t)j | (nf * C) << 8 | wj << 17;
+        }
+        __syncthreads();
+        if (j < (int)sh.n_items) {
+            const uint32_t it = sh.item[j];
+            const int r = (int)(it & 0xffu);
+            const int k0 = (int)((it >> 8) & 0x1ffu), k1 = (int)(it >> 17);
+            const float4 A = sh.sr.a[r];
+            const float4 B = sh.sr.b[r];
+            const int4 Cb = sh.sr.c[r];
             const int lx0 = max(Cb.x - tx0, 0), lx1 = min(Cb.x + Cb.y - tx0, kTile - 1);
-            const int ly0 = max(Cb.z - ty0, 0), ly1 = min(Cb.z + Cb.w - ty0, kTile - 1);
+            const int ly0 = max(Cb.z - ty0, 0);
+            const int wdt = lx1 - lx0 + 1;
+            const int row = (int)small_div((uint32_t)k0, 1.0f / (float)wdt), col = k0 - row * wdt;
             const float dx0 = ((float)lx0 + 0.5f) - A.x;
-            for (int ly = ly0 + ph; ly <= ly1; ly += q) {
-                const float dy = ((float)ly + 0.5f) - A.y;
-                const float cdy = B.x * dy;
-                const float4* grow = &sh.g[ly * kTile];
-                float dx = dx0;
-                for (int lx = lx0; lx <= lx1; ++lx, dx += 1.0f) {
-                    const float u = A.z * dx;
-                    const float v = fmaf(A.w, dx, cdy);
-                    const float w = ex2_approx(fmaf(-u, u, -(v * v)));
-                    const float4 gp = grow[lx];
-                    const float gw0 = gp.x * w, gw1 = gp.y * w, gw2 = gp.z * w;
-                    const float sdot = fmaf(B.y, gw0, fmaf(B.z, gw1, B.w * gw2));   // -gamma
-                    const float gu = -sdot * u, gv = -sdot * v;
-                    a0 += gw0;
-                    a1 += gw1;
-                    a2 += gw2;
-                    a3 += gu;
-                    a4 += gv;
-                    a5 = fmaf(gu, u, a5);
-                    a6 = fmaf(gu, v, a6);
-                    a7 = fmaf(gv, v, a7);
+            float dx = ((float)(lx0 + col) + 0.5f) - A.x;
+            float dy = ((float)(ly0 + row) + 0.5f) - A.y;
+            float cdy = B.x * dy;
+            const float4* gp_ptr = &sh.g[(ly0 + row) * kTile + lx0 + col];
+            int left = wdt - col;
+            float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f, a4 = 0.f, a5 = 0.f, a6 = 0.f, a7 = 0.f;
+            for (int k = k0; k < k1; ++k) {
+                const float u = A.z * dx;
+                const float v = fmaf(A.w, dx, cdy);
+                const float w = ex2_approx(fmaf(-u, u, -(v * v)));
+                const float4 gp = *gp_ptr;
+                const float gw0 = gp.x * w, gw1 = gp.y * w, gw2 = gp.z * w;
+                const float sdot = fmaf(B.y, gw0, fmaf(B.z, gw1, B.w * gw2));   // -gamma
+                const float gu = -sdot * u, gv = -sdot * v;
+                a0 += gw0;
+                a1 += gw1;
+                a2 += gw2;
+                a3 += gu;
+                a4 += gv;
+                a5 = fmaf(gu, u, a5);
+                a6 = fmaf(gu, v, a6);
+                a7 = fmaf(gv, v, a7);
+                ++gp_ptr;
+                dx += 1.0f;
+                if (--left == 0) {
+                    left = wdt;
+                    gp_ptr += kTile - wdt;
+                    dx = dx0;
+                    dy += 1.0f;
+                    cdy = B.x * dy;
                 }
             }
+            sh.u.red[j][0] = make_float4(a0, a1, a2, a3);
+            sh.u.red[j][1] = make_float4(a4, a5, a6, a7);
         }
-        // combine the q row phases (fixed xor tree, deterministic)
-        for (int o = 1; o < q; o <<= 1) {
-            a0 += __shfl_xor_sync(kFull, a0, o);
-            a1 += __shfl_xor_sync(kFull, a1, o);
-            a2 += __shfl_xor_sync(kFull, a2, o);
-            a3 += __shfl_xor_sync(kFull, a3, o);
-            a4 += __shfl_xor_sync(kFull, a4, o);
-            a5 += __shfl_xor_sync(kFull, a5, o);
-            a6 += __shfl_xor_sync(kFull, a6, o);
-            a7 += __shfl_xor_sync(kFull, a7, o);
-        }
-        if (j < cnt && ph == 0) {
-            const uint32_t sl = sh.slot[j];
-            if ((int64_t)sl < cap) {
-                float4* dst = reinterpret_cast<float4*>(partial + (size_t)sl * 8);
-                dst[0] = make_float4(a0, a1, a2, a3);
-                dst[1] = make_float4(a4, a5, a6, a7);
-            }
+        __syncthreads();
+        if (j < cnt && (int64_t)slot < cap) {
+            float4 s0 = make_float4(0.f, 0.f, 0.f, 0.f), s1 = s0;
+            auto add = [&](uint32_t i) {
+                const float4 x = sh.u.red[i][0], y = sh.u.red[i][1];
+                s0.x += x.x; s0.y += x.y; s0.z += x.z; s0.w += x.w;
+                s1.x += y.x; s1.y += y.y; s1.z += y.z; s1.w += y.w;
+            };
+            for (uint32_t i = 0; i < nf; ++i) add(fstart + i);
+            if (rm != 0u) add(rpos);
+            float4* dst = reinterpret_cast<float4*>(partial + (size_t)slot * 8);
+            dst[0] = s0;
+            dst[1] = s1;
         }
     }
 }

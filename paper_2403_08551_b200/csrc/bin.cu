@@ -267,7 +267,7 @@ __global__ void __launch_bounds__(256) scatter_kernel(const Proj* __restrict__ p
 __global__ void __launch_bounds__(256) segsort_kernel(const Proj* __restrict__ proj, int n, int T,
                                                       int TX, const uint32_t* __restrict__ tile_range,
                                                       uint32_t* __restrict__ key_gid) {
-    __shared__ uint32_t sl[kSortMax];
+    __shared__ alignas(16) uint32_t sl[kSortMax];
     __shared__ uint32_t scratch[kWarps];
     const int t = blockIdx.x;
     griddep_wait();

@@ -90,11 +90,8 @@ __device__ __forceinline__ uint32_t warp_box_mask(const int4 b, int wx0, int wy0
     const int lo_y = max(b.z - wy0, 0), hi_y = min(b.z + b.w - wy0, 3);
     if (lo_x > hi_x || lo_y > hi_y) return 0u;
     const uint32_t row = ((1u << (hi_x + 1)) - 1u) & ~((1u << lo_x) - 1u);
-    uint32_t m = 0u;
-#pragma unroll
-    for (int r = 0; r < 4; ++r)
-        if (r >= lo_y && r <= hi_y) m |= row << (8 * r);
-    return m;
+    const uint32_t rows = (0xffffffffu >> (8 * (3 - hi_y))) & (0xffffffffu << (8 * lo_y));
+    return (row * 0x01010101u) & rows;
 }
 
 // Build this warp's candidate list for a staged batch of cnt records.
@@ -172,9 +169,14 @@ __device__ __forceinline__ int sorted_segment(const Proj* __restrict__ proj,
         if ((int)threadIdx.x < cnt) mine = key_gid[s + threadIdx.x];
         sl[threadIdx.x] = mine;
         __syncthreads();
-        int r = 0;
-        if ((int)threadIdx.x < cnt)
-            for (int k = 0; k < cnt; ++k) r += sl[k] < mine;
+        int r = 0;   // entries >= cnt hold 0xffffffff and never count
+        if ((int)threadIdx.x < cnt) {
+            const uint4* s4 = reinterpret_cast<const uint4*>(sl);
+            for (int k = 0; k < (cnt + 3) >> 2; ++k) {
+                const uint4 v = s4[k];
+                r += (int)(v.x < mine) + (int)(v.y < mine) + (int)(v.z < mine) + (int)(v.w < mine);
+            }
+        }
         __syncthreads();
         if ((int)threadIdx.x < cnt) sl[r] = mine;
         __syncthreads();

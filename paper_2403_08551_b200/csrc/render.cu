@@ -13,7 +13,7 @@ namespace {
 struct RenderShared {
     StagedRecords sr;
     WarpLists wl;
-    uint32_t sl[kSortMax];
+    alignas(16) uint32_t sl[kSortMax];
     uint32_t scratch[kWarps];
 };
 
