@@ -95,7 +95,8 @@ __global__ void __launch_bounds__(256, 5) backward_tile_kernel(
         for (uint32_t base = 0; base < L; base += 256) {
             const int cnt = (int)min(256u, L - base);
             if (base > 0) __syncthreads();
-            if ((int)threadIdx.x < cnt) stage_gid(sh.sr, proj, gid_at(base + threadIdx.x), threadIdx.x, t);
+            if ((int)threadIdx.x < cnt)
+                stage_gid(sh.sr, proj, gid_at(base + threadIdx.x), threadIdx.x, t, gauss_off);
             __syncthreads();
             const int nl = build_warp_list(sh.sr, sh.u.wl, cnt, t);
             forward_batch(sh.sr, sh.u.wl, nl, t, acc0, acc1, acc2);
@@ -139,7 +140,6 @@ __global__ void __launch_bounds__(256, 5) backward_tile_kernel(
     // chunks come first, remainders follow in descending size, so the lanes
     // of a warp run nearly equal trip counts.  Each lane accumulates the 8
     // sums of its chunk; thread j then adds its chunks in a fixed order.
-    const int tx0 = t.tx * kTile, ty0 = t.ty * kTile;
     const int j = threadIdx.x;
     for (uint32_t base = 0; base < L; base += 256) {
         const int cnt = (int)min(256u, L - base);
@@ -147,16 +147,12 @@ __global__ void __launch_bounds__(256, 5) backward_tile_kernel(
         if (j < 64) sh.hist[j] = 0u;
         uint32_t slot = 0, wj = 0;
         if (j < cnt) {
-            const uint32_t gid = gid_at(base + j);
-            if (!staged_all) stage_gid(sh.sr, proj, gid, j, t);
-            // slot: the Gaussian's contiguous partial range, tile rank in its
-            // rectangle (row-major) -- the same order finalize sums in
-            const int4 b = sh.sr.c[j];
-            const int rtx0 = b.x / kTile, rtx1 = (b.x + b.y) / kTile, rty0 = b.z / kTile;
-            slot = gauss_off[gid] + (uint32_t)((t.ty - rty0) * (rtx1 - rtx0 + 1) + (t.tx - rtx0));
-            const int wdt = min(b.x + b.y - tx0, kTile - 1) - max(b.x - tx0, 0) + 1;
-            const int hgt = min(b.z + b.w - ty0, kTile - 1) - max(b.z - ty0, 0) + 1;
-            wj = (uint32_t)(wdt * hgt);
+            if (!staged_all) stage_gid(sh.sr, proj, gid_at(base + j), j, t, gauss_off);
+            const uint4 c = sh.sr.c[j];
+            slot = c.z;
+            const int lx0 = c.x & 0xff, lx1 = (c.x >> 8) & 0xff;
+            const int ly0 = (c.x >> 16) & 0xff, ly1 = c.x >> 24;
+            wj = (uint32_t)((lx1 - lx0 + 1) * (ly1 - ly0 + 1));
         }
         // (1) sum and max of w over the batch
         {
@@ -244,27 +240,26 @@ __global__ void __launch_bounds__(256, 5) backward_tile_kernel(
             const uint32_t it = sh.item[j];
             const int r = (int)(it & 0xffu);
             const int k0 = (int)((it >> 8) & 0x1ffu), k1 = (int)(it >> 17);
-            const float4 A = sh.sr.a[r];
-            const float4 B = sh.sr.b[r];
-            const int4 Cb = sh.sr.c[r];
-            const int lx0 = max(Cb.x - tx0, 0), lx1 = min(Cb.x + Cb.y - tx0, kTile - 1);
-            const int ly0 = max(Cb.z - ty0, 0);
+            const float4 A = sh.sr.a[r];          // {a, b, c, c'r}
+            const float4 B = sh.sr.b[r];          // {c'g, c'b, mx, my}
+            const uint32_t box = sh.sr.c[r].x;
+            const int lx0 = box & 0xff, lx1 = (box >> 8) & 0xff, ly0 = (box >> 16) & 0xff;
             const int wdt = lx1 - lx0 + 1;
             const int row = (int)small_div((uint32_t)k0, 1.0f / (float)wdt), col = k0 - row * wdt;
-            const float dx0 = ((float)lx0 + 0.5f) - A.x;
-            float dx = ((float)(lx0 + col) + 0.5f) - A.x;
-            float dy = ((float)(ly0 + row) + 0.5f) - A.y;
-            float cdy = B.x * dy;
+            const float dx0 = ((float)lx0 + 0.5f) - B.z;
+            float dx = ((float)(lx0 + col) + 0.5f) - B.z;
+            float dy = ((float)(ly0 + row) + 0.5f) - B.w;
+            float cdy = A.z * dy;
             const float4* gp_ptr = &sh.g[(ly0 + row) * kTile + lx0 + col];
             int left = wdt - col;
             float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f, a4 = 0.f, a5 = 0.f, a6 = 0.f, a7 = 0.f;
             for (int k = k0; k < k1; ++k) {
-                const float u = A.z * dx;
-                const float v = fmaf(A.w, dx, cdy);
+                const float u = A.x * dx;
+                const float v = fmaf(A.y, dx, cdy);
                 const float w = ex2_approx(fmaf(-u, u, -(v * v)));
                 const float4 gp = *gp_ptr;
                 const float gw0 = gp.x * w, gw1 = gp.y * w, gw2 = gp.z * w;
-                const float sdot = fmaf(B.y, gw0, fmaf(B.z, gw1, B.w * gw2));   // -gamma
+                const float sdot = fmaf(A.w, gw0, fmaf(B.x, gw1, B.y * gw2));   // -gamma
                 const float gu = -sdot * u, gv = -sdot * v;
                 a0 += gw0;
                 a1 += gw1;
@@ -281,7 +276,7 @@ __global__ void __launch_bounds__(256, 5) backward_tile_kernel(
                     gp_ptr += kTile - wdt;
                     dx = dx0;
                     dy += 1.0f;
-                    cdy = B.x * dy;
+                    cdy = A.z * dy;
                 }
             }
             sh.u.red[j][0] = make_float4(a0, a1, a2, a3);

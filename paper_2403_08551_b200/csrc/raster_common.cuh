@@ -18,7 +18,9 @@
 //   rC = {x0, x1 - x0, y0, y1 - y0}   integer box, global pixels
 // Each warp then compacts the batch into its own candidate list: record
 // index + the 32-bit mask of its lanes whose pixel lies in the box, so the
-// inner loop needs no bit scanning and a one-instruction box test.
+// inner loop needs no bit scanning and a one-instruction box test.  The box
+// is staged as 16-bit column / row masks of the tile, so a warp's 32-lane
+// mask is two bit-field extracts and two multiplies.
 #pragma once
 #include "gi_internal.cuh"
 
@@ -33,6 +35,7 @@ struct TileCtx {
     int x, y;                     // global pixel of this thread
     float cx, cy;                 // tile-local pixel centre (x + 1/2 - 16 tx)
     int wx0, wy0;                 // warp block origin (global pixels)
+    int csh, rsh;                 // warp block: column / row shift in the tile masks
     bool in_image;
 };
 
@@ -53,14 +56,22 @@ __device__ __forceinline__ TileCtx make_tile_ctx(int W, int H, int TX) {
     c.cy = (float)ly + 0.5f;
     c.wx0 = c.tx * kTile + (c.warp & 1) * 8;
     c.wy0 = c.ty * kTile + (c.warp >> 1) * 4;
+    c.csh = (c.warp & 1) * 8;
+    c.rsh = (c.warp >> 1) * 4;
     c.in_image = c.x < W && c.y < H;
     return c;
 }
 
+// Staged record j (tile-local):
+//   a = {a, b, c, c'r}          factored conic (sigma log2 e = (a dx)^2 + (b dx + c dy)^2)
+//   b = {c'g, c'b, mx, my}      centre minus the tile origin
+//   c = {lx0 | lx1 << 8 | ly0 << 16 | ly1 << 24   box clipped to the tile,
+//        column mask | row mask << 16,            the same as 16-bit masks,
+//        partial slot (backward only), 0}
 struct StagedRecords {
     float4 a[256];
     float4 b[256];
-    int4 c[256];
+    uint4 c[256];
 };
 
 // Per-warp compacted candidate list for one batch: (record index, lane mask).
@@ -69,29 +80,45 @@ struct WarpLists {
     int cnt[kWarps];
 };
 
-// Stage record j = threadIdx.x (j < cnt) for gid into shared memory.
+__device__ __forceinline__ uint32_t span_mask16(int lo, int hi) {
+    return ((2u << hi) - 1u) & ~((1u << lo) - 1u);
+}
+
+// Stage record j = threadIdx.x (j < cnt) for gid into shared memory.  With
+// gauss_off (backward), also the Gaussian's partial slot for this tile: its
+// contiguous range gauss_off[gid] + the rank of this tile in its tile
+// rectangle (row-major), the order finalize sums in.
 __device__ __forceinline__ void stage_gid(StagedRecords& sr, const Proj* __restrict__ proj,
-                                          uint32_t gid, int j, const TileCtx& t) {
+                                          uint32_t gid, int j, const TileCtx& t,
+                                          const uint32_t* __restrict__ gauss_off = nullptr) {
     const Proj r = proj[gid];
+    const int tx0 = t.tx * kTile, ty0 = t.ty * kTile;
     const int ix = __float_as_int(r.q0.x), iy = __float_as_int(r.q0.y);
-    const float mx = __fadd_rn((float)(ix - t.tx * kTile), r.q0.z);
-    const float my = __fadd_rn((float)(iy - t.ty * kTile), r.q0.w);
+    const float mx = __fadd_rn((float)(ix - tx0), r.q0.z);
+    const float my = __fadd_rn((float)(iy - ty0), r.q0.w);
     const uint32_t bx = __float_as_uint(r.q1.w), by = __float_as_uint(r.q2.w);
     const int x0 = (int)(bx & 0xffffu), x1 = (int)(bx >> 16);
     const int y0 = (int)(by & 0xffffu), y1 = (int)(by >> 16);
-    sr.a[j] = make_float4(mx, my, r.q1.x, r.q1.y);
-    sr.b[j] = make_float4(r.q1.z, r.q2.x, r.q2.y, r.q2.z);
-    sr.c[j] = make_int4(x0, x1 - x0, y0, y1 - y0);
+    const int lx0 = max(x0 - tx0, 0), lx1 = min(x1 - tx0, kTile - 1);
+    const int ly0 = max(y0 - ty0, 0), ly1 = min(y1 - ty0, kTile - 1);
+    uint32_t slot = 0;
+    if (gauss_off != nullptr) {
+        const int rtx0 = x0 / kTile, rtx1 = x1 / kTile, rty0 = y0 / kTile;
+        slot = gauss_off[gid] + (uint32_t)((t.ty - rty0) * (rtx1 - rtx0 + 1) + (t.tx - rtx0));
+    }
+    sr.a[j] = make_float4(r.q1.x, r.q1.y, r.q1.z, r.q2.x);
+    sr.b[j] = make_float4(r.q2.y, r.q2.z, mx, my);
+    sr.c[j] = make_uint4((uint32_t)(lx0 | lx1 << 8 | ly0 << 16 | ly1 << 24),
+                         span_mask16(lx0, lx1) | span_mask16(ly0, ly1) << 16, slot, 0u);
 }
 
-// Lanes of the 8x4 warp block (lane = ly * 8 + lx) inside box b.
-__device__ __forceinline__ uint32_t warp_box_mask(const int4 b, int wx0, int wy0) {
-    const int lo_x = max(b.x - wx0, 0), hi_x = min(b.x + b.y - wx0, 7);
-    const int lo_y = max(b.z - wy0, 0), hi_y = min(b.z + b.w - wy0, 3);
-    if (lo_x > hi_x || lo_y > hi_y) return 0u;
-    const uint32_t row = ((1u << (hi_x + 1)) - 1u) & ~((1u << lo_x) - 1u);
-    const uint32_t rows = (0xffffffffu >> (8 * (3 - hi_y))) & (0xffffffffu << (8 * lo_y));
-    return (row * 0x01010101u) & rows;
+// Lanes of the 8x4 warp block (lane = ly * 8 + lx) inside the box given by
+// its 16-bit tile column / row masks: the block's 8 columns replicated into
+// the bytes of its 4 set rows (bit i of the row nibble -> bit 8 i).
+__device__ __forceinline__ uint32_t warp_box_mask(uint32_t masks, const TileCtx& t) {
+    const uint32_t cols = (masks >> t.csh) & 0xffu;
+    const uint32_t rows = (masks >> (16 + t.rsh)) & 0xfu;
+    return ((rows * 0x00204081u) & 0x01010101u) * cols;
 }
 
 // Build this warp's candidate list for a staged batch of cnt records.
@@ -100,7 +127,7 @@ __device__ __forceinline__ int build_warp_list(const StagedRecords& sr, WarpList
     int n = 0;
     for (int q = 0; q < cnt; q += 32) {
         const int j = q + t.lane;
-        const uint32_t m = j < cnt ? warp_box_mask(sr.c[j], t.wx0, t.wy0) : 0u;
+        const uint32_t m = j < cnt ? warp_box_mask(sr.c[j].y, t) : 0u;
         const unsigned hit = __ballot_sync(kFull, m != 0u);
         if (m != 0u) wl.ent[t.warp][n + __popc(hit & lanemask_lt())] = make_uint2((uint32_t)j, m);
         n += __popc(hit);
@@ -117,10 +144,10 @@ struct PairEval {
 
 __device__ __forceinline__ PairEval eval_pair(const float4 A, const float4 B, const TileCtx& t) {
     PairEval e;
-    const float dx = t.cx - A.x;
-    const float dy = t.cy - A.y;
-    e.u = A.z * dx;
-    e.v = fmaf(A.w, dx, B.x * dy);
+    const float dx = t.cx - B.z;
+    const float dy = t.cy - B.w;
+    e.u = A.x * dx;
+    e.v = fmaf(A.y, dx, A.z * dy);
     e.w = ex2_approx(fmaf(-e.u, e.u, -(e.v * e.v)));
     return e;
 }
@@ -131,16 +158,17 @@ __device__ __forceinline__ void forward_batch(const StagedRecords& sr, const War
                                               const TileCtx& t, float& acc0, float& acc1,
                                               float& acc2) {
     const uint2* ent = wl.ent[t.warp];
+    const uint32_t bit = 1u << t.lane;
 #pragma unroll 2
     for (int k = 0; k < n; ++k) {
         const uint2 en = ent[k];
         const float4 A = sr.a[en.x];
         const float4 B = sr.b[en.x];
         const PairEval pe = eval_pair(A, B, t);
-        const float w = (en.y >> t.lane) & 1u ? pe.w : 0.f;
-        acc0 = fmaf(B.y, w, acc0);
-        acc1 = fmaf(B.z, w, acc1);
-        acc2 = fmaf(B.w, w, acc2);
+        const float w = (en.y & bit) ? pe.w : 0.f;
+        acc0 = fmaf(A.w, w, acc0);
+        acc1 = fmaf(B.x, w, acc1);
+        acc2 = fmaf(B.y, w, acc2);
     }
 }
 
