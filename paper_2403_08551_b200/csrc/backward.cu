@@ -57,7 +57,7 @@ __global__ void __launch_bounds__(256, 5) backward_tile_kernel(
     const Proj* __restrict__ proj, uint32_t* __restrict__ key_gid,
     const uint32_t* __restrict__ tile_range, const uint32_t* __restrict__ gauss_off, int n,
     int W, int H, int T, int TX, bool presorted, const float* __restrict__ dL_dimage,
-    const float* __restrict__ target, float norm, int64_t cap, float* __restrict__ partial,
+    const float* __restrict__ target, float norm, int64_t pcap, float* __restrict__ partial,
     float* __restrict__ sse_part, float* __restrict__ image_out, ChainState cs) {
     __shared__ BwdShared sh;
     const TileCtx t = make_tile_ctx(W, H, TX);
@@ -283,7 +283,7 @@ __global__ void __launch_bounds__(256, 5) backward_tile_kernel(
             sh.u.red[j][1] = make_float4(a4, a5, a6, a7);
         }
         __syncthreads();
-        if (j < cnt && (int64_t)slot < cap) {
+        if (j < cnt && (int64_t)slot < pcap) {
             float4 s0 = make_float4(0.f, 0.f, 0.f, 0.f), s1 = s0;
             auto add = [&](uint32_t i) {
                 const float4 x = sh.u.red[i][0], y = sh.u.red[i][1];
@@ -312,7 +312,13 @@ __global__ void __launch_bounds__(256) alloc_kernel(const Proj* __restrict__ pro
         if (x0 <= x1 && y0 <= y1)
             cnt = (uint32_t)((x1 / kTile - x0 / kTile + 1) * (y1 / kTile - y0 / kTile + 1));
     }
-    const uint32_t off = warp_alloc(counter, cnt);
+    // same layout as the fused scatter (bin.cu): 4 g for <= 4-tile Gaussians,
+    // 4 total + allocation for larger ones
+    uint32_t off = 4u * (uint32_t)g;
+    if (__any_sync(kFull, cnt > 4u)) {
+        const uint32_t big_off = warp_alloc(counter, cnt > 4u ? cnt : 0u);
+        if (cnt > 4u) off = 4u * (uint32_t)total + big_off;
+    }
     if (g < total) gauss_off[g] = off;
 }
 
@@ -332,7 +338,7 @@ __device__ __forceinline__ float adam1(float p, float g, float& m, float& v, flo
 __global__ void __launch_bounds__(256) finalize_kernel(
     const float4* __restrict__ params, const Proj* proj /* may be rewritten (chained) */,
     const uint32_t* __restrict__ gauss_off, int total, int n_per_image, int W, int H,
-    uint32_t flags, int64_t cap,
+    uint32_t flags, int64_t pcap,
     const float* __restrict__ partial, float4* __restrict__ grads, FusedAdam adam,
     const float* __restrict__ sse_part, int T, int batch, double inv_count,
     float* __restrict__ loss) {
@@ -344,12 +350,10 @@ __global__ void __launch_bounds__(256) finalize_kernel(
     // independent loads first (their latency overlaps the partial-sum chain)
     float4 p0 = make_float4(0.f, 0.f, 0.f, 0.f), p1 = p0, m0 = p0, m1 = p0, v0 = p0, v1 = p0;
     Proj r{};
-    uint32_t o0 = 0;
     if (g < total) {
         p0 = params[2 * (size_t)g];
         p1 = params[2 * (size_t)g + 1];
         r = proj[g];
-        o0 = gauss_off[g];
         if (adam.m != nullptr) {
             const float4* mm = reinterpret_cast<const float4*>(adam.m) + 2 * (size_t)g;
             const float4* vv = reinterpret_cast<const float4*>(adam.v) + 2 * (size_t)g;
@@ -388,12 +392,29 @@ __global__ void __launch_bounds__(256) finalize_kernel(
     if (x0 <= x1 && y0 <= y1) {
         const uint32_t cnt = (uint32_t)((x1 / kTile - x0 / kTile + 1) * (y1 / kTile - y0 / kTile + 1));
         const float4* pp = reinterpret_cast<const float4*>(partial);
-        for (uint32_t k = 0; k < cnt; ++k) {       // row-major tile order of the rectangle
-            if ((int64_t)(o0 + k) >= cap) break;
-            const float4 a = pp[2 * (size_t)(o0 + k)];
-            const float4 b = pp[2 * (size_t)(o0 + k) + 1];
+        auto add = [&](const float4 a, const float4 b) {
             S[0] += a.x; S[1] += a.y; S[2] += a.z; S[3] += a.w;
             S[4] += b.x; S[5] += b.y; S[6] += b.z; S[7] += b.w;
+        };
+        if (cnt <= 4u) {
+            // fixed slots 4 g .. 4 g + cnt - 1: all loads issued at once
+            float4 a[4], b[4];
+            const size_t o = 4 * (size_t)g;
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+                if ((uint32_t)k < cnt) {
+                    a[k] = pp[2 * (o + k)];
+                    b[k] = pp[2 * (o + k) + 1];
+                }
+#pragma unroll
+            for (int k = 0; k < 4; ++k)                // row-major tile order of the rectangle
+                if ((uint32_t)k < cnt) add(a[k], b[k]);
+        } else {
+            const uint32_t o0 = gauss_off[g];
+            for (uint32_t k = 0; k < cnt; ++k) {
+                if ((int64_t)(o0 + k) >= pcap) break;
+                add(pp[2 * (size_t)(o0 + k)], pp[2 * (size_t)(o0 + k) + 1]);
+            }
         }
         any = true;
     }
@@ -494,6 +515,10 @@ __global__ void __launch_bounds__(256) loss_kernel(const float* __restrict__ sse
     if (threadIdx.x == 0) loss[img] = (float)(sm[0] * inv_count);
 }
 
+// Partial slots: 4 per Gaussian (the <= 4-tile ones use 4 g .. 4 g + 3) plus
+// the key capacity for the Gaussians touching more tiles.
+int64_t partial_cap(int n, int64_t cap, const gi_frame& f) { return 4 * (int64_t)n * f.batch + cap; }
+
 struct BwdWs {
     float* partial;
     uint32_t* gauss_off;
@@ -508,7 +533,7 @@ BwdWs carve(void* base, int n, int64_t cap, const gi_frame& f) {
     char* p = static_cast<char*>(base);
     BwdWs w;
     size_t off = 0;
-    w.partial = reinterpret_cast<float*>(p + off); off += align_up(sizeof(float) * 8 * (size_t)cap);
+    w.partial = reinterpret_cast<float*>(p + off); off += align_up(sizeof(float) * 8 * (size_t)partial_cap(n, cap, f));
     w.gauss_off = reinterpret_cast<uint32_t*>(p + off); off += align_up(sizeof(uint32_t) * (total + 1));
     w.counter = reinterpret_cast<uint32_t*>(p + off); off += align_up(sizeof(uint32_t));
     w.sse = reinterpret_cast<float*>(p + off); off += align_up(sizeof(float) * (size_t)T * f.batch);
@@ -551,7 +576,7 @@ cudaError_t launch_backward_tiles(const Proj* proj, uint32_t* key_gid, const uin
     cudaError_t e = launch_pdl(backward_tile_kernel, dim3(TX, T / TX, f.batch), dim3(256), s, proj,
                                key_gid,
                                tile_range, (const uint32_t*)w.gauss_off, n, f.width, f.height, T,
-                               TX, presorted, dL_dimage, target, norm, cap, w.partial,
+                               TX, presorted, dL_dimage, target, norm, partial_cap(n, cap, f), w.partial,
                                mse ? w.sse : nullptr, mse ? image_out : nullptr, cs);
     note_launches(1);
     return e;
@@ -572,7 +597,7 @@ cudaError_t launch_backward_finalize(const float* params, const Proj* proj, int 
         if (adam) fa = *adam;
         e = launch_pdl(finalize_kernel, dim3((total + 255) / 256), dim3(256), s,
                        reinterpret_cast<const float4*>(params), proj, (const uint32_t*)w.gauss_off,
-                       total, n, f.width, f.height, flags, cap, (const float*)w.partial,
+                       total, n, f.width, f.height, flags, partial_cap(n, cap, f), (const float*)w.partial,
                        reinterpret_cast<float4*>(grads), fa, (const float*)w.sse, T, f.batch,
                        1.0 / count, fold ? loss : nullptr);
         note_launches(1);

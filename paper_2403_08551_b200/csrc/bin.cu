@@ -205,8 +205,14 @@ __global__ void __launch_bounds__(256) scatter_kernel(const Proj* __restrict__ p
         __syncthreads();
     }
     if (gauss_off != nullptr) {
-        // contiguous backward partial slots per Gaussian (warp-aggregated atomic)
-        const uint32_t off = warp_alloc(alloc_counter, cnt);
+        // contiguous backward partial slots per Gaussian: 4 g for the <= 4-tile
+        // Gaussians (fixed, no allocation), 4 total + a warp-aggregated
+        // allocation for the larger ones
+        uint32_t off = 4u * (uint32_t)g;
+        if (__any_sync(kFull, cnt > 4u)) {
+            const uint32_t big_off = warp_alloc(alloc_counter, cnt > 4u ? cnt : 0u);
+            if (cnt > 4u) off = 4u * (uint32_t)total + big_off;
+        }
         if (g < total) gauss_off[g] = off;
     }
     const int base = cnt ? (g / n) * T : 0;

@@ -137,11 +137,18 @@ struct BinCounts {
 __device__ __forceinline__ void count_keys(const BinCounts& bc, int g, int tx0, int tx1, int ty0,
                                            int ty1, uint32_t touched, int base, int TX) {
     if (touched <= 4u) {
+        // key i -> tile (tx0 + i mod w, ty0 + i / w); the (up to) 4 atomics are
+        // independent and issued back to back
+        const int w = tx1 - tx0 + 1;
         uint32_t r[4] = {0u, 0u, 0u, 0u};
-        int i = 0;
-        for (int ty = ty0; ty <= ty1; ++ty)
-            for (int tx = tx0; tx <= tx1; ++tx, ++i)
-                r[i & 3] = atomicAdd(&bc.tile_count[base + ty * TX + tx], 1u);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            if ((uint32_t)i < touched) {
+                const int dy = (i >= w) + (i >= 2 * w) + (i >= 3 * w);
+                const int dx = i - dy * w;
+                r[i] = atomicAdd(&bc.tile_count[base + (ty0 + dy) * TX + tx0 + dx], 1u);
+            }
+        }
         bc.key_rank[g] = make_uint4(r[0], r[1], r[2], r[3]);
     } else {
         for (int ty = ty0; ty <= ty1; ++ty)

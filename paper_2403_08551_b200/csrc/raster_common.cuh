@@ -86,7 +86,7 @@ __device__ __forceinline__ uint32_t span_mask16(int lo, int hi) {
 
 // Stage record j = threadIdx.x (j < cnt) for gid into shared memory.  With
 // gauss_off (backward), also the Gaussian's partial slot for this tile: its
-// contiguous range gauss_off[gid] + the rank of this tile in its tile
+// contiguous range (4 gid, or gauss_off[gid] above 4 tiles) + the rank of this tile in its tile
 // rectangle (row-major), the order finalize sums in.
 __device__ __forceinline__ void stage_gid(StagedRecords& sr, const Proj* __restrict__ proj,
                                           uint32_t gid, int j, const TileCtx& t,
@@ -103,8 +103,11 @@ __device__ __forceinline__ void stage_gid(StagedRecords& sr, const Proj* __restr
     const int ly0 = max(y0 - ty0, 0), ly1 = min(y1 - ty0, kTile - 1);
     uint32_t slot = 0;
     if (gauss_off != nullptr) {
-        const int rtx0 = x0 / kTile, rtx1 = x1 / kTile, rty0 = y0 / kTile;
-        slot = gauss_off[gid] + (uint32_t)((t.ty - rty0) * (rtx1 - rtx0 + 1) + (t.tx - rtx0));
+        // slots 4 gid.. for Gaussians touching <= 4 tiles (bin.cu scatter)
+        const int rtx0 = x0 / kTile, rtx1 = x1 / kTile, rty0 = y0 / kTile, rty1 = y1 / kTile;
+        const int rw = rtx1 - rtx0 + 1;
+        const uint32_t off = rw * (rty1 - rty0 + 1) <= 4 ? 4u * gid : gauss_off[gid];
+        slot = off + (uint32_t)((t.ty - rty0) * rw + (t.tx - rtx0));
     }
     sr.a[j] = make_float4(r.q1.x, r.q1.y, r.q1.z, r.q2.x);
     sr.b[j] = make_float4(r.q2.y, r.q2.z, mx, my);
