@@ -65,7 +65,7 @@ __global__ void __launch_bounds__(256, 5) backward_tile_kernel(
     griddep_trigger();
     if (threadIdx.x == 0 && cs.tile_count != nullptr) {   // leave the counters zero for the next call
         const int tt = t.img * T + t.tile;
-        cs.tile_count[tt] = 0u;
+        cs.tile_count[(size_t)tt * kCountStride] = 0u;
         cs.big_count[tt] = 0u;
         cs.fill[tt] = 0u;
         if (tt == 0 && cs.alloc_counter != nullptr) *cs.alloc_counter = 0u;
@@ -326,7 +326,9 @@ __device__ __forceinline__ float adam1(float p, float g, float& m, float& v, flo
                                        float lr, float ibc1, float ibc2, float eps) {
     m = fmaf(b1, m, (1.0f - b1) * g);
     v = fmaf(b2, v, (1.0f - b2) * (g * g));
-    return p - lr * (m * ibc1) / (sqrtf(v * ibc2) + eps);
+    float sq;
+    asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(sq) : "f"(v * ibc2));
+    return p - __fdividef(lr * (m * ibc1), sq + eps);
 }
 
 // Per Gaussian: sum its tiles' partials (row-major tile order), then the

@@ -78,7 +78,7 @@ __global__ void __launch_bounds__(1024) tile_scan_kernel(const uint32_t* __restr
     uint32_t s = 0;
     for (int k = 0; k < per; ++k) {
         const int i = i0 + k;
-        if (i < TT) s += tile_count[i] + big_count[i];
+        if (i < TT) s += tile_count[(size_t)i * kCountStride] + big_count[i];
     }
     uint32_t x = s;
 #pragma unroll
@@ -105,7 +105,7 @@ __global__ void __launch_bounds__(1024) tile_scan_kernel(const uint32_t* __restr
         const int i = i0 + k;
         if (i < TT) {
             tile_range[i] = (int64_t)run < cap ? run : (uint32_t)cap;
-            run += tile_count[i] + big_count[i];
+            run += tile_count[(size_t)i * kCountStride] + big_count[i];
         }
     }
     if (threadIdx.x == 0) {
@@ -117,7 +117,7 @@ __global__ void __launch_bounds__(1024) tile_scan_kernel(const uint32_t* __restr
 __global__ void combine_kernel(const uint32_t* __restrict__ a, const uint32_t* __restrict__ b,
                                uint32_t* __restrict__ out, int64_t count) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < count) out[i] = a[i] + b[i];
+    if (i < count) out[i] = a[i * kCountStride] + b[i];
 }
 
 __global__ void clamp_kernel(uint32_t* __restrict__ v, int64_t count, int64_t cap) {
@@ -170,7 +170,7 @@ __global__ void __launch_bounds__(256) scatter_kernel(const Proj* __restrict__ p
         uint32_t sum = 0;
         for (int k = 0; k < per; ++k)
             if (i0 + k < TT) {
-                const uint32_t sm = bc.tile_count[i0 + k];
+                const uint32_t sm = bc.tile_count[(size_t)(i0 + k) * kCountStride];
                 small_s[i0 + k] = sm;
                 sum += sm + bc.big_count[i0 + k];
             }
@@ -236,7 +236,7 @@ __global__ void __launch_bounds__(256) scatter_kernel(const Proj* __restrict__ p
             for (int tx = q.tx0; tx <= q.tx1; ++tx) {
                 const int t = base + ty * TX + tx;
                 const uint32_t st = fuse_scan ? start_s[t] : tile_range[t];
-                const uint32_t sm = fuse_scan ? small_s[t] : bc.tile_count[t];
+                const uint32_t sm = fuse_scan ? small_s[t] : bc.tile_count[(size_t)t * kCountStride];
                 const int64_t slot = (int64_t)st + sm + atomicAdd(&fill[t], 1u);
                 if (slot < cap) {
                     key_tile[slot] = (uint32_t)t;
@@ -257,7 +257,7 @@ __global__ void __launch_bounds__(256) scatter_kernel(const Proj* __restrict__ p
         for (uint32_t i = lane; i < c; i += 32) {
             const int t = b + (ty0 + (int)i / w) * TX + tx0 + (int)i % w;
             const uint32_t st = fuse_scan ? start_s[t] : tile_range[t];
-            const uint32_t sm = fuse_scan ? small_s[t] : bc.tile_count[t];
+            const uint32_t sm = fuse_scan ? small_s[t] : bc.tile_count[(size_t)t * kCountStride];
             const int64_t slot = (int64_t)st + sm + atomicAdd(&fill[t], 1u);
             if (slot < cap) {
                 key_tile[slot] = (uint32_t)t;
@@ -302,8 +302,8 @@ BinWs carve(void* base, int n, int64_t cap, const gi_frame& f) {
     char* p = static_cast<char*>(base);
     BinWs w;
     size_t off = 0;
-    // tile_count, big_count, fill and alloc_counter are adjacent: one memset
-    w.tile_count = reinterpret_cast<uint32_t*>(p + off); off += sizeof(uint32_t) * (size_t)TT;
+    // tile_count (strided), big_count, fill and alloc_counter are adjacent: one memset
+    w.tile_count = reinterpret_cast<uint32_t*>(p + off); off += sizeof(uint32_t) * (size_t)TT * kCountStride;
     w.big_count = reinterpret_cast<uint32_t*>(p + off); off += sizeof(uint32_t) * (size_t)TT;
     w.fill = reinterpret_cast<uint32_t*>(p + off); off += sizeof(uint32_t) * (size_t)TT;
     w.alloc_counter = reinterpret_cast<uint32_t*>(p + off); off += sizeof(uint32_t);
@@ -332,7 +332,7 @@ uint32_t* bin_alloc_counter(void* ws, int n, int64_t cap, const gi_frame& f) {
 cudaError_t bin_clear(void* ws, int n, int64_t cap, const gi_frame& f, cudaStream_t s) {
     BinWs w = carve(ws, n, cap, f);
     const size_t TT = (size_t)tiles_x(f.width) * tiles_y(f.height) * f.batch;
-    return cudaMemsetAsync(w.tile_count, 0, sizeof(uint32_t) * (3 * TT + 1), s);
+    return cudaMemsetAsync(w.tile_count, 0, sizeof(uint32_t) * ((kCountStride + 2) * TT + 1), s);
 }
 
 ChainState bin_chain_state(void* bin_ws, int n, int64_t cap, const gi_frame& f, uint32_t* gauss_off) {

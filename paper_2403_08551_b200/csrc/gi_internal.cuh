@@ -127,8 +127,16 @@ int64_t g_launches_get();
 // keys of larger Gaussians are counted on big_count and claim their slots
 // after the small ones.  All counters must be zero on entry (bin_clear, or
 // left zeroed by the consumer kernel of the previous fused call).
+// tile_count words are kCountStride u32 apart: the count atomics (one per
+// key, ~80 per tile, all issued within a few microseconds) then spread over
+// L2 slices instead of queueing on the few slices that hold a packed table.
+#ifndef GI_COUNT_STRIDE
+#define GI_COUNT_STRIDE 8
+#endif
+constexpr int kCountStride = GI_COUNT_STRIDE;
+
 struct BinCounts {
-    uint32_t* tile_count;   // [B*T] keys of small Gaussians (null: no counting)
+    uint32_t* tile_count;   // [B*T * kCountStride] keys of small Gaussians (null: no counting)
     uint32_t* big_count;    // [B*T] keys of Gaussians touching > 4 tiles
     uint4* key_rank;        // [B*N] ranks of a small Gaussian's keys
 };
@@ -146,7 +154,7 @@ __device__ __forceinline__ void count_keys(const BinCounts& bc, int g, int tx0, 
             if ((uint32_t)i < touched) {
                 const int dy = (i >= w) + (i >= 2 * w) + (i >= 3 * w);
                 const int dx = i - dy * w;
-                r[i] = atomicAdd(&bc.tile_count[base + (ty0 + dy) * TX + tx0 + dx], 1u);
+                r[i] = atomicAdd(&bc.tile_count[(size_t)(base + (ty0 + dy) * TX + tx0 + dx) * kCountStride], 1u);
             }
         }
         bc.key_rank[g] = make_uint4(r[0], r[1], r[2], r[3]);

@@ -29,7 +29,7 @@ __global__ void __launch_bounds__(256) render_kernel(const Proj* __restrict__ pr
     griddep_trigger();
     if (threadIdx.x == 0 && cs.tile_count != nullptr) {   // leave the counters zero for the next call
         const int tt = t.img * T + t.tile;
-        cs.tile_count[tt] = 0u;
+        cs.tile_count[(size_t)tt * kCountStride] = 0u;
         cs.big_count[tt] = 0u;
         cs.fill[tt] = 0u;
         if (tt == 0 && cs.alloc_counter != nullptr) *cs.alloc_counter = 0u;
