@@ -153,7 +153,7 @@ gi_status gi_bin(const void* proj, const uint32_t* tiles_touched, int32_t n, con
         return invalid("NULL buffer");
     return cuda_status(gi::launch_bin(static_cast<const gi::Proj*>(proj), tiles_touched, n, *f,
                                       key_capacity, ws, key_tile, key_gid, tile_range, n_keys,
-                                      false, true, nullptr, S(stream)),
+                                      S(stream)),
                        "gi_bin");
 }
 
@@ -271,30 +271,28 @@ static gi_status fit_step_impl(float* params, float* grads, float* m, float* v, 
     cudaError_t e;
 #define GI_TRY(expr, where) \
     if ((e = (expr)) != cudaSuccess) return cuda_status(e, where)
-    // The per-tile counters in the workspace are zero on entry (zero-filled
-    // workspace, then left zeroed by the consumer tile kernel of each call).
+    // Direct binning: the producer (project, or the previous step's finalize
+    // when chained) counts every key with a rank-returning atomic and writes it
+    // to its tile's slab of the key array; the per-tile counters are zero on
+    // entry (zero-filled workspace, then left zeroed by the consumer tile
+    // kernel of each call).
     uint32_t* gauss_off = gi::backward_gauss_off(w.bwd_ws, n, key_capacity, *f);
-    const gi::ChainState cs = gi::bin_chain_state(w.bin_ws, n, key_capacity, *f, gauss_off);
+    const gi::BinCounts bc = gi::bin_counts_direct(w.bin_ws, n, key_capacity, *f, w.key_gid, gauss_off);
+    const gi::ChainState cs = gi::bin_chain_direct(w.bin_ws, n, key_capacity, *f, w.key_gid, gauss_off,
+                                                   w.n_keys, chained ? step_counter : nullptr);
     GI_TRY(record_stage(stage_events, 0, s), "gi_fit_step/event");
     if (!chained)
         GI_TRY(gi::launch_project(params, n, *f, flags, w.proj, w.touched,
-                                  gi::ProjectFuse{step_counter,
-                                                  gi::bin_counts(w.bin_ws, n, key_capacity, *f)},
-                                  s),
+                                  gi::ProjectFuse{step_counter, bc}, s),
                "gi_fit_step/project");
     GI_TRY(record_stage(stage_events, 1, s), "gi_fit_step/event");
-    GI_TRY(gi::launch_bin(w.proj, w.touched, n, *f, key_capacity, w.bin_ws, w.key_tile, w.key_gid,
-                          w.tile_range, w.n_keys, true, false, gauss_off, s,
-                          chained ? step_counter : nullptr),
-           "gi_fit_step/bin");
     GI_TRY(record_stage(stage_events, 2, s), "gi_fit_step/event");
-    GI_TRY(gi::launch_backward_tiles(w.proj, w.key_gid, w.tile_range, n, *f, false, nullptr, target,
+    GI_TRY(gi::launch_backward_tiles(w.proj, w.key_gid, nullptr, n, *f, false, nullptr, target,
                                      key_capacity, w.bwd_ws, nullptr, cs, s),
            "gi_fit_step/backward");
     GI_TRY(record_stage(stage_events, 3, s), "gi_fit_step/event");
     gi::FusedAdam fa{params, m, v, step_counter, lr0, half_every, beta1, beta2, eps, status_flags,
-                     chained ? w.proj : nullptr, w.touched,
-                     gi::bin_counts(w.bin_ws, n, key_capacity, *f), f->k, flags};
+                     chained ? w.proj : nullptr, w.touched, bc, f->k, flags};
     GI_TRY(gi::launch_backward_finalize(params, w.proj, n, *f, flags, true, key_capacity, w.bwd_ws,
                                         grads, loss, &fa, s),
            "gi_fit_step/finalize+adam");
@@ -342,16 +340,13 @@ gi_status gi_fit_step_adan(float* params, float* grads, float* m, float* v, floa
 #define GI_TRY(expr, where) \
     if ((e = (expr)) != cudaSuccess) return cuda_status(e, where)
     uint32_t* gauss_off = gi::backward_gauss_off(w.bwd_ws, nn, key_capacity, *f);
-    const gi::ChainState cs = gi::bin_chain_state(w.bin_ws, nn, key_capacity, *f, gauss_off);
+    const gi::BinCounts bc = gi::bin_counts_direct(w.bin_ws, nn, key_capacity, *f, w.key_gid, gauss_off);
+    const gi::ChainState cs = gi::bin_chain_direct(w.bin_ws, nn, key_capacity, *f, w.key_gid,
+                                                   gauss_off, w.n_keys, nullptr);
     GI_TRY(gi::launch_project(params, nn, *f, flags, w.proj, w.touched,
-                              gi::ProjectFuse{step_counter,
-                                              gi::bin_counts(w.bin_ws, nn, key_capacity, *f)},
-                              s),
+                              gi::ProjectFuse{step_counter, bc}, s),
            "gi_fit_step_adan/project");
-    GI_TRY(gi::launch_bin(w.proj, w.touched, nn, *f, key_capacity, w.bin_ws, w.key_tile, w.key_gid,
-                          w.tile_range, w.n_keys, true, false, gauss_off, s),
-           "gi_fit_step_adan/bin");
-    GI_TRY(gi::launch_backward_tiles(w.proj, w.key_gid, w.tile_range, nn, *f, false, nullptr, target,
+    GI_TRY(gi::launch_backward_tiles(w.proj, w.key_gid, nullptr, nn, *f, false, nullptr, target,
                                      key_capacity, w.bwd_ws, nullptr, cs, s),
            "gi_fit_step_adan/backward");
     GI_TRY(gi::launch_backward_finalize(params, w.proj, nn, *f, flags, true, key_capacity, w.bwd_ws,
@@ -377,11 +372,13 @@ gi_status gi_fit_prime(const float* params, int32_t n, const gi_frame* f, uint32
     if (n > 0 && !params) return invalid("NULL buffer");
     if (!aligned16(params) || !aligned16(fit_ws)) return invalid("alignment");
     FitWs w = carve_fit(fit_ws, n, key_capacity, *f);
-    return cuda_status(gi::launch_project(params, n, *f, flags, w.proj, w.touched,
-                                          gi::ProjectFuse{nullptr,
-                                                          gi::bin_counts(w.bin_ws, n, key_capacity, *f)},
-                                          S(stream)),
-                       "gi_fit_prime");
+    uint32_t* gauss_off = gi::backward_gauss_off(w.bwd_ws, n, key_capacity, *f);
+    return cuda_status(
+        gi::launch_project(params, n, *f, flags, w.proj, w.touched,
+                           gi::ProjectFuse{nullptr, gi::bin_counts_direct(w.bin_ws, n, key_capacity,
+                                                                          *f, w.key_gid, gauss_off)},
+                           S(stream)),
+        "gi_fit_prime");
 }
 
 gi_status gi_fit_step_chained(float* params, float* grads, float* m, float* v, const float* target,
@@ -412,15 +409,14 @@ gi_status gi_render_frame(const float* params, int32_t n, const gi_frame* f, uin
     cudaError_t e;
 #define GI_TRY(expr, where) \
     if ((e = (expr)) != cudaSuccess) return cuda_status(e, where)
-    const gi::ChainState cs = gi::bin_chain_state(w.bin_ws, n, key_capacity, *f, nullptr);
+    const gi::ChainState cs = gi::bin_chain_direct(w.bin_ws, n, key_capacity, *f, w.key_gid, nullptr,
+                                                   w.n_keys, nullptr);
     GI_TRY(gi::launch_project(params, n, *f, flags, w.proj, w.touched,
-                              gi::ProjectFuse{nullptr, gi::bin_counts(w.bin_ws, n, key_capacity, *f)},
+                              gi::ProjectFuse{nullptr, gi::bin_counts_direct(w.bin_ws, n, key_capacity,
+                                                                             *f, w.key_gid, nullptr)},
                               s),
            "gi_render_frame/project");
-    GI_TRY(gi::launch_bin(w.proj, w.touched, n, *f, key_capacity, w.bin_ws, w.key_tile, w.key_gid,
-                          w.tile_range, w.n_keys, true, false, nullptr, s),
-           "gi_render_frame/bin");
-    GI_TRY(gi::launch_render(w.proj, w.key_gid, w.tile_range, n, *f, false, image, cs, s),
+    GI_TRY(gi::launch_render(w.proj, w.key_gid, nullptr, n, *f, false, image, cs, s),
            "gi_render_frame/render");
 #undef GI_TRY
     return GI_OK;

@@ -39,6 +39,7 @@ struct BwdShared {
     float4 g[kTilePix];      // per-pixel upstream dL/dC (x, y, z), tile-local row-major
     uint32_t scratch[kWarps];
     float sse[kWarps];
+    uint32_t cursor;   // segment count / stream cursor
     uint32_t hist[64];       // pass-2 remainder-size histogram -> bin starts
     uint32_t item[256];      // pass-2 chunk: record | k0 << 8 | k1 << 17
     uint2 pa[kWarps], pb[kWarps];   // pass-2 per-warp partials
@@ -58,28 +59,18 @@ __global__ void __launch_bounds__(256, 5) backward_tile_kernel(
     const uint32_t* __restrict__ tile_range, const uint32_t* __restrict__ gauss_off, int n,
     int W, int H, int T, int TX, bool presorted, const float* __restrict__ dL_dimage,
     const float* __restrict__ target, float norm, int64_t pcap, float* __restrict__ partial,
-    float* __restrict__ sse_part, float* __restrict__ image_out, ChainState cs) {
+    float* __restrict__ ovf, float* __restrict__ sse_part, float* __restrict__ image_out,
+    ChainState cs) {
     __shared__ BwdShared sh;
     const TileCtx t = make_tile_ctx(W, H, TX);
     griddep_wait();
     griddep_trigger();
-    if (threadIdx.x == 0 && cs.tile_count != nullptr) {   // leave the counters zero for the next call
-        const int tt = t.img * T + t.tile;
-        cs.tile_count[(size_t)tt * kCountStride] = 0u;
-        cs.big_count[tt] = 0u;
-        cs.fill[tt] = 0u;
-        if (tt == 0 && cs.alloc_counter != nullptr) *cs.alloc_counter = 0u;
-    }
-    const uint32_t s = tile_range[t.img * T + t.tile];
-    const uint32_t e = tile_range[t.img * T + t.tile + 1];
-    const uint32_t L = e - s;
+    const Seg sg = open_segment(proj, key_gid, tile_range, presorted, cs, n, T, t, sh.sl,
+                                sh.scratch, &sh.cursor);
+    const uint32_t L = sg.L;
     const size_t P = (size_t)W * H;
     const size_t pix = (size_t)t.img * 3 * P + (size_t)t.y * W + t.x;
     const int lpix = (t.y - t.ty * kTile) * kTile + (t.x - t.tx * kTile);
-    const int sorted = presorted ? -1
-                                 : sorted_segment(proj, key_gid, s, e, n, t.img, t.tx, t.ty, sh.sl,
-                                                  sh.scratch);
-    auto gid_at = [&](uint32_t i) -> uint32_t { return sorted >= 0 ? sh.sl[i] : key_gid[s + i]; };
     bool staged_all = false;
 
     float g0 = 0.f, g1 = 0.f, g2 = 0.f;
@@ -93,10 +84,11 @@ __global__ void __launch_bounds__(256, 5) backward_tile_kernel(
         // ---- pass 1: forward (Eq. 7), pixel-parallel ----
         float acc0 = 0.f, acc1 = 0.f, acc2 = 0.f;
         for (uint32_t base = 0; base < L; base += 256) {
-            const int cnt = (int)min(256u, L - base);
             if (base > 0) __syncthreads();
-            if ((int)threadIdx.x < cnt)
-                stage_gid(sh.sr, proj, gid_at(base + threadIdx.x), threadIdx.x, t, gauss_off);
+            uint32_t gid;
+            const int cnt =
+                batch_gid(sg, base, key_gid, sh.sl, proj, n, t, &sh.cursor, sh.scratch, gid);
+            if ((int)threadIdx.x < cnt) stage_gid(sh.sr, proj, gid, threadIdx.x, t, gauss_off);
             __syncthreads();
             const int nl = build_warp_list(sh.sr, sh.u.wl, cnt, t);
             forward_batch(sh.sr, sh.u.wl, nl, t, acc0, acc1, acc2);
@@ -141,15 +133,20 @@ __global__ void __launch_bounds__(256, 5) backward_tile_kernel(
     // of a warp run nearly equal trip counts.  Each lane accumulates the 8
     // sums of its chunk; thread j then adds its chunks in a fixed order.
     const int j = threadIdx.x;
+    if (threadIdx.x == 0) sh.cursor = 0u;        // kSegStream: pass 2 streams from the start
     for (uint32_t base = 0; base < L; base += 256) {
-        const int cnt = (int)min(256u, L - base);
         __syncthreads();
+        uint32_t gid = 0;
+        int cnt = (int)min(256u, L - base);
+        if (!staged_all)
+            cnt = batch_gid(sg, base, key_gid, sh.sl, proj, n, t, &sh.cursor, sh.scratch, gid);
         if (j < 64) sh.hist[j] = 0u;
-        uint32_t slot = 0, wj = 0;
+        uint32_t slot = 0, wj = 0, jgid = 0;
         if (j < cnt) {
-            if (!staged_all) stage_gid(sh.sr, proj, gid_at(base + j), j, t, gauss_off);
+            if (!staged_all) stage_gid(sh.sr, proj, gid, j, t, gauss_off);
             const uint4 c = sh.sr.c[j];
             slot = c.z;
+            jgid = c.w;
             const int lx0 = c.x & 0xff, lx1 = (c.x >> 8) & 0xff;
             const int ly0 = (c.x >> 16) & 0xff, ly1 = c.x >> 24;
             wj = (uint32_t)((lx1 - lx0 + 1) * (ly1 - ly0 + 1));
@@ -283,7 +280,7 @@ __global__ void __launch_bounds__(256, 5) backward_tile_kernel(
             sh.u.red[j][1] = make_float4(a4, a5, a6, a7);
         }
         __syncthreads();
-        if (j < cnt && (int64_t)slot < pcap) {
+        if (j < cnt && (slot == kOffOverflow || (int64_t)slot < pcap)) {
             float4 s0 = make_float4(0.f, 0.f, 0.f, 0.f), s1 = s0;
             auto add = [&](uint32_t i) {
                 const float4 x = sh.u.red[i][0], y = sh.u.red[i][1];
@@ -292,15 +289,23 @@ __global__ void __launch_bounds__(256, 5) backward_tile_kernel(
             };
             for (uint32_t i = 0; i < nf; ++i) add(fstart + i);
             if (rm != 0u) add(rpos);
-            float4* dst = reinterpret_cast<float4*>(partial + (size_t)slot * 8);
-            dst[0] = s0;
-            dst[1] = s1;
+            if (slot == kOffOverflow) {     // > 4-tile Gaussian without slots: accumulate
+                float* o = ovf + (size_t)jgid * 8;
+                atomicAdd(o + 0, s0.x); atomicAdd(o + 1, s0.y); atomicAdd(o + 2, s0.z);
+                atomicAdd(o + 3, s0.w); atomicAdd(o + 4, s1.x); atomicAdd(o + 5, s1.y);
+                atomicAdd(o + 6, s1.z); atomicAdd(o + 7, s1.w);
+            } else {
+                float4* dst = reinterpret_cast<float4*>(partial + (size_t)slot * 8);
+                dst[0] = s0;
+                dst[1] = s1;
+            }
         }
     }
+    close_segment(cs, t.img * T + t.tile);
 }
 
 __global__ void __launch_bounds__(256) alloc_kernel(const Proj* __restrict__ proj, int total,
-                                                    uint32_t* __restrict__ counter,
+                                                    int64_t pcap, uint32_t* __restrict__ counter,
                                                     uint32_t* __restrict__ gauss_off) {
     const int g = blockIdx.x * blockDim.x + threadIdx.x;
     uint32_t cnt = 0;
@@ -312,12 +317,13 @@ __global__ void __launch_bounds__(256) alloc_kernel(const Proj* __restrict__ pro
         if (x0 <= x1 && y0 <= y1)
             cnt = (uint32_t)((x1 / kTile - x0 / kTile + 1) * (y1 / kTile - y0 / kTile + 1));
     }
-    // same layout as the fused scatter (bin.cu): 4 g for <= 4-tile Gaussians,
-    // 4 total + allocation for larger ones
+    // same layout as direct binning (post_project_warp): 4 g for <= 4-tile
+    // Gaussians, 4 total + allocation for larger ones
     uint32_t off = 4u * (uint32_t)g;
     if (__any_sync(kFull, cnt > 4u)) {
         const uint32_t big_off = warp_alloc(counter, cnt > 4u ? cnt : 0u);
-        if (cnt > 4u) off = 4u * (uint32_t)total + big_off;
+        const int64_t first = 4ll * total + big_off;
+        if (cnt > 4u) off = first + cnt <= pcap ? (uint32_t)first : kOffOverflow;
     }
     if (g < total) gauss_off[g] = off;
 }
@@ -341,7 +347,8 @@ __global__ void __launch_bounds__(256) finalize_kernel(
     const float4* __restrict__ params, const Proj* proj /* may be rewritten (chained) */,
     const uint32_t* __restrict__ gauss_off, int total, int n_per_image, int W, int H,
     uint32_t flags, int64_t pcap,
-    const float* __restrict__ partial, float4* __restrict__ grads, FusedAdam adam,
+    const float* __restrict__ partial, float* __restrict__ ovf, float4* __restrict__ grads,
+    FusedAdam adam,
     const float* __restrict__ sse_part, int T, int batch, double inv_count,
     float* __restrict__ loss) {
     __shared__ float sconst[3];
@@ -385,120 +392,137 @@ __global__ void __launch_bounds__(256) finalize_kernel(
         }
         __syncthreads();
     }
-    if (g >= total) return;
-    const uint32_t bx = __float_as_uint(r.q1.w), by = __float_as_uint(r.q2.w);
-    const int x0 = (int)(bx & 0xffffu), x1 = (int)(bx >> 16);
-    const int y0 = (int)(by & 0xffffu), y1 = (int)(by >> 16);
-    float S[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-    bool any = false;
-    if (x0 <= x1 && y0 <= y1) {
-        const uint32_t cnt = (uint32_t)((x1 / kTile - x0 / kTile + 1) * (y1 / kTile - y0 / kTile + 1));
-        const float4* pp = reinterpret_cast<const float4*>(partial);
-        auto add = [&](const float4 a, const float4 b) {
-            S[0] += a.x; S[1] += a.y; S[2] += a.z; S[3] += a.w;
-            S[4] += b.x; S[5] += b.y; S[6] += b.z; S[7] += b.w;
-        };
-        if (cnt <= 4u) {
-            // fixed slots 4 g .. 4 g + cnt - 1: all loads issued at once
-            float4 a[4], b[4];
-            const size_t o = 4 * (size_t)g;
-#pragma unroll
-            for (int k = 0; k < 4; ++k)
-                if ((uint32_t)k < cnt) {
-                    a[k] = pp[2 * (o + k)];
-                    b[k] = pp[2 * (o + k) + 1];
+    uint32_t touched = 0;
+    int4 rect = make_int4(0, -1, 0, -1);
+    if (g < total) {
+        const uint32_t bx = __float_as_uint(r.q1.w), by = __float_as_uint(r.q2.w);
+        const int x0 = (int)(bx & 0xffffu), x1 = (int)(bx >> 16);
+        const int y0 = (int)(by & 0xffffu), y1 = (int)(by >> 16);
+        float S[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+        bool any = false;
+        if (x0 <= x1 && y0 <= y1) {
+            const uint32_t cnt = (uint32_t)((x1 / kTile - x0 / kTile + 1) * (y1 / kTile - y0 / kTile + 1));
+            const float4* pp = reinterpret_cast<const float4*>(partial);
+            auto add = [&](const float4 a, const float4 b) {
+                S[0] += a.x; S[1] += a.y; S[2] += a.z; S[3] += a.w;
+                S[4] += b.x; S[5] += b.y; S[6] += b.z; S[7] += b.w;
+            };
+            if (cnt <= 4u) {
+                // fixed slots 4 g .. 4 g + cnt - 1: all loads issued at once
+                float4 a[4], b[4];
+                const size_t o = 4 * (size_t)g;
+    #pragma unroll
+                for (int k = 0; k < 4; ++k)
+                    if ((uint32_t)k < cnt) {
+                        a[k] = pp[2 * (o + k)];
+                        b[k] = pp[2 * (o + k) + 1];
+                    }
+    #pragma unroll
+                for (int k = 0; k < 4; ++k)                // row-major tile order of the rectangle
+                    if ((uint32_t)k < cnt) add(a[k], b[k]);
+            } else {
+                const uint32_t o0 = gauss_off[g];
+                if (o0 == kOffOverflow) {          // summed atomically by the tiles; re-zero
+                    float4* o = reinterpret_cast<float4*>(ovf) + 2 * (size_t)g;
+                    add(o[0], o[1]);
+                    o[0] = make_float4(0.f, 0.f, 0.f, 0.f);
+                    o[1] = make_float4(0.f, 0.f, 0.f, 0.f);
+                } else {
+                    for (uint32_t k = 0; k < cnt; ++k) {
+                        if ((int64_t)(o0 + k) >= pcap) break;
+                        add(pp[2 * (size_t)(o0 + k)], pp[2 * (size_t)(o0 + k) + 1]);
+                    }
                 }
-#pragma unroll
-            for (int k = 0; k < 4; ++k)                // row-major tile order of the rectangle
-                if ((uint32_t)k < cnt) add(a[k], b[k]);
-        } else {
-            const uint32_t o0 = gauss_off[g];
-            for (uint32_t k = 0; k < cnt; ++k) {
-                if ((int64_t)(o0 + k) >= pcap) break;
-                add(pp[2 * (size_t)(o0 + k)], pp[2 * (size_t)(o0 + k) + 1]);
+            }
+            any = true;
+        }
+        float4 r0 = make_float4(0.f, 0.f, 0.f, 0.f), r1 = r0;
+        if (any && !cov_rs(flags)) {
+            // Cholesky, fp32 (the 1e-4 gradient bar leaves ample room)
+            const float l1 = p0.z + 0.5f, l2 = p0.w, l3 = p1.x + 0.5f;
+            const float il1 = 1.0f / l1, il3 = 1.0f / l3;
+            const float ik = (float)(1.0 / kKappa), ik2 = (float)(1.0 / (kKappa * kKappa));
+            const float Sp = S[3] * ik, Sq = S[4] * ik;
+            const float Spp = S[5] * ik2, Spq = S[6] * ik2, Sqq = S[7] * ik2;
+            const float l2l3 = l2 * il3;
+            const float Ax = (Sp - Sq * l2l3) * il1;         // sum gamma dsigma/ddx
+            const float Ay = Sq * il3;
+            r0.x = -Ax;                                       // dmu_pix = -dsigma/dd (R13)
+            r0.y = -Ay;
+            r0.z = -(Spp - Spq * l2l3) * il1;                 // dl1
+            r0.w = -Spq * il3;                                // dl2
+            r1.x = -Sqq * il3;                                // dl3
+        } else if (any) {
+            // NEXT-3 rotation-scaling: L = chol(Sigma) as in the projection, then
+            // G = dL/dSigma = -1/2 L^-T M L^-1 with M = sum gamma (p, q)(p, q)^T,
+            // chained through Sigma(theta, s1, s2) (App. A.2).
+            const double th = (double)p0.z;
+            const double s1 = (double)__fadd_rn(p0.w, 0.5f), s2 = (double)__fadd_rn(p1.x, 0.5f);
+            double Sg[3];
+            rs_sigma(th, s1, s2, Sg);
+            const double l1 = sqrt(Sg[0]), l2 = Sg[1] / l1, l3 = fabs(s1 * s2) / l1;
+            const double ik = 1.0 / kKappa, ik2 = ik * ik;
+            const double Sp = S[3] * ik, Sq = S[4] * ik;
+            const double Spp = S[5] * ik2, Spq = S[6] * ik2, Sqq = S[7] * ik2;
+            const double al = 1.0 / l1, be = -l2 / (l1 * l3), ga = 1.0 / l3;   // L^-1 = [[al,0],[be,ga]]
+            r0.x = (float)(-(al * Sp + be * Sq));             // dmu_pix = -L^-T (S_p, S_q)
+            r0.y = (float)(-(ga * Sq));
+            const double G11 = -0.5 * (al * al * Spp + 2.0 * al * be * Spq + be * be * Sqq);
+            const double G12 = -0.5 * (al * ga * Spq + be * ga * Sqq);
+            const double G22 = -0.5 * (ga * ga * Sqq);
+            const double c = cos(th), sn = sin(th);
+            const double s2t = 2.0 * sn * c, c2t = c * c - sn * sn;
+            r0.z = (float)((s1 * s1 - s2 * s2) * (-G11 * s2t + 2.0 * G12 * c2t + G22 * s2t));   // dtheta
+            r0.w = (float)(2.0 * s1 * (G11 * c * c + 2.0 * G12 * c * sn + G22 * sn * sn));     // ds1
+            r1.x = (float)(2.0 * s2 * (G11 * sn * sn - 2.0 * G12 * c * sn + G22 * c * c));     // ds2
+        }
+        if (any) {
+            // position activation chain (App. C): mu = (tanh(r) + 1) W/2
+            float sx = (float)W * 0.5f, sy = (float)H * 0.5f;
+            if (pos_logit(flags)) {
+                const float chx = coshf(p0.x), chy = coshf(p0.y);
+                sx /= chx * chx;
+                sy /= chy * chy;
+            }
+            r0.x *= sx;
+            r0.y *= sy;
+            r1.y = S[0];                                      // dc'
+            r1.z = S[1];
+            r1.w = S[2];
+        }
+        grads[2 * (size_t)g] = r0;
+        grads[2 * (size_t)g + 1] = r1;
+        if (adam.m != nullptr) {
+            const float lr = sconst[0], ibc1 = sconst[1], ibc2 = sconst[2];
+            float4* mm = reinterpret_cast<float4*>(adam.m) + 2 * (size_t)g;
+            float4* vv = reinterpret_cast<float4*>(adam.v) + 2 * (size_t)g;
+            float4* pp = reinterpret_cast<float4*>(adam.params) + 2 * (size_t)g;
+            float4 q0, q1;
+            const float b1 = adam.b1, b2 = adam.b2, eps = adam.eps;
+            q0.x = adam1(p0.x, r0.x, m0.x, v0.x, b1, b2, lr, ibc1, ibc2, eps);
+            q0.y = adam1(p0.y, r0.y, m0.y, v0.y, b1, b2, lr, ibc1, ibc2, eps);
+            q0.z = adam1(p0.z, r0.z, m0.z, v0.z, b1, b2, lr, ibc1, ibc2, eps);
+            q0.w = adam1(p0.w, r0.w, m0.w, v0.w, b1, b2, lr, ibc1, ibc2, eps);
+            q1.x = adam1(p1.x, r1.x, m1.x, v1.x, b1, b2, lr, ibc1, ibc2, eps);
+            q1.y = adam1(p1.y, r1.y, m1.y, v1.y, b1, b2, lr, ibc1, ibc2, eps);
+            q1.z = adam1(p1.z, r1.z, m1.z, v1.z, b1, b2, lr, ibc1, ibc2, eps);
+            q1.w = adam1(p1.w, r1.w, m1.w, v1.w, b1, b2, lr, ibc1, ibc2, eps);
+            mm[0] = m0; mm[1] = m1; vv[0] = v0; vv[1] = v1;
+            pp[0] = q0; pp[1] = q1;
+            const bool bad = !(isfinite(q0.x) && isfinite(q0.y) && isfinite(q0.z) && isfinite(q0.w) &&
+                               isfinite(q1.x) && isfinite(q1.y) && isfinite(q1.z) && isfinite(q1.w));
+            if (bad && adam.flag != nullptr) atomicOr(adam.flag, 1u);
+            if (adam.proj_out != nullptr) {  // chained: a1 of the next step on the updated Gaussian
+                touched = project_one(q0, q1, g, n_per_image, W, H, adam.k, adam.pos_flags,
+                                      adam.proj_out, adam.counts, rect);
+                adam.touched_out[g] = touched;
             }
         }
-        any = true;
     }
-    float4 r0 = make_float4(0.f, 0.f, 0.f, 0.f), r1 = r0;
-    if (any && !cov_rs(flags)) {
-        // Cholesky, fp32 (the 1e-4 gradient bar leaves ample room)
-        const float l1 = p0.z + 0.5f, l2 = p0.w, l3 = p1.x + 0.5f;
-        const float il1 = 1.0f / l1, il3 = 1.0f / l3;
-        const float ik = (float)(1.0 / kKappa), ik2 = (float)(1.0 / (kKappa * kKappa));
-        const float Sp = S[3] * ik, Sq = S[4] * ik;
-        const float Spp = S[5] * ik2, Spq = S[6] * ik2, Sqq = S[7] * ik2;
-        const float l2l3 = l2 * il3;
-        const float Ax = (Sp - Sq * l2l3) * il1;         // sum gamma dsigma/ddx
-        const float Ay = Sq * il3;
-        r0.x = -Ax;                                       // dmu_pix = -dsigma/dd (R13)
-        r0.y = -Ay;
-        r0.z = -(Spp - Spq * l2l3) * il1;                 // dl1
-        r0.w = -Spq * il3;                                // dl2
-        r1.x = -Sqq * il3;                                // dl3
-    } else if (any) {
-        // NEXT-3 rotation-scaling: L = chol(Sigma) as in the projection, then
-        // G = dL/dSigma = -1/2 L^-T M L^-1 with M = sum gamma (p, q)(p, q)^T,
-        // chained through Sigma(theta, s1, s2) (App. A.2).
-        const double th = (double)p0.z;
-        const double s1 = (double)__fadd_rn(p0.w, 0.5f), s2 = (double)__fadd_rn(p1.x, 0.5f);
-        double Sg[3];
-        rs_sigma(th, s1, s2, Sg);
-        const double l1 = sqrt(Sg[0]), l2 = Sg[1] / l1, l3 = fabs(s1 * s2) / l1;
-        const double ik = 1.0 / kKappa, ik2 = ik * ik;
-        const double Sp = S[3] * ik, Sq = S[4] * ik;
-        const double Spp = S[5] * ik2, Spq = S[6] * ik2, Sqq = S[7] * ik2;
-        const double al = 1.0 / l1, be = -l2 / (l1 * l3), ga = 1.0 / l3;   // L^-1 = [[al,0],[be,ga]]
-        r0.x = (float)(-(al * Sp + be * Sq));             // dmu_pix = -L^-T (S_p, S_q)
-        r0.y = (float)(-(ga * Sq));
-        const double G11 = -0.5 * (al * al * Spp + 2.0 * al * be * Spq + be * be * Sqq);
-        const double G12 = -0.5 * (al * ga * Spq + be * ga * Sqq);
-        const double G22 = -0.5 * (ga * ga * Sqq);
-        const double c = cos(th), sn = sin(th);
-        const double s2t = 2.0 * sn * c, c2t = c * c - sn * sn;
-        r0.z = (float)((s1 * s1 - s2 * s2) * (-G11 * s2t + 2.0 * G12 * c2t + G22 * s2t));   // dtheta
-        r0.w = (float)(2.0 * s1 * (G11 * c * c + 2.0 * G12 * c * sn + G22 * sn * sn));     // ds1
-        r1.x = (float)(2.0 * s2 * (G11 * sn * sn - 2.0 * G12 * c * sn + G22 * c * c));     // ds2
-    }
-    if (any) {
-        // position activation chain (App. C): mu = (tanh(r) + 1) W/2
-        float sx = (float)W * 0.5f, sy = (float)H * 0.5f;
-        if (pos_logit(flags)) {
-            const float chx = coshf(p0.x), chy = coshf(p0.y);
-            sx /= chx * chx;
-            sy /= chy * chy;
-        }
-        r0.x *= sx;
-        r0.y *= sy;
-        r1.y = S[0];                                      // dc'
-        r1.z = S[1];
-        r1.w = S[2];
-    }
-    grads[2 * (size_t)g] = r0;
-    grads[2 * (size_t)g + 1] = r1;
-    if (adam.m != nullptr) {
-        const float lr = sconst[0], ibc1 = sconst[1], ibc2 = sconst[2];
-        float4* mm = reinterpret_cast<float4*>(adam.m) + 2 * (size_t)g;
-        float4* vv = reinterpret_cast<float4*>(adam.v) + 2 * (size_t)g;
-        float4* pp = reinterpret_cast<float4*>(adam.params) + 2 * (size_t)g;
-        float4 q0, q1;
-        const float b1 = adam.b1, b2 = adam.b2, eps = adam.eps;
-        q0.x = adam1(p0.x, r0.x, m0.x, v0.x, b1, b2, lr, ibc1, ibc2, eps);
-        q0.y = adam1(p0.y, r0.y, m0.y, v0.y, b1, b2, lr, ibc1, ibc2, eps);
-        q0.z = adam1(p0.z, r0.z, m0.z, v0.z, b1, b2, lr, ibc1, ibc2, eps);
-        q0.w = adam1(p0.w, r0.w, m0.w, v0.w, b1, b2, lr, ibc1, ibc2, eps);
-        q1.x = adam1(p1.x, r1.x, m1.x, v1.x, b1, b2, lr, ibc1, ibc2, eps);
-        q1.y = adam1(p1.y, r1.y, m1.y, v1.y, b1, b2, lr, ibc1, ibc2, eps);
-        q1.z = adam1(p1.z, r1.z, m1.z, v1.z, b1, b2, lr, ibc1, ibc2, eps);
-        q1.w = adam1(p1.w, r1.w, m1.w, v1.w, b1, b2, lr, ibc1, ibc2, eps);
-        mm[0] = m0; mm[1] = m1; vv[0] = v0; vv[1] = v1;
-        pp[0] = q0; pp[1] = q1;
-        const bool bad = !(isfinite(q0.x) && isfinite(q0.y) && isfinite(q0.z) && isfinite(q0.w) &&
-                           isfinite(q1.x) && isfinite(q1.y) && isfinite(q1.z) && isfinite(q1.w));
-        if (bad && adam.flag != nullptr) atomicOr(adam.flag, 1u);
-        if (adam.proj_out != nullptr)    // chained: a1 of the next step on the updated Gaussian
-            adam.touched_out[g] = project_one(q0, q1, g, n_per_image, W, H, adam.k, adam.pos_flags,
-                                              adam.proj_out, adam.counts);
+    if (adam.m != nullptr && adam.proj_out != nullptr && adam.counts.tile_count != nullptr) {
+        const int TX = (W + kTile - 1) / kTile, T = TX * ((H + kTile - 1) / kTile);
+        post_project_warp(adam.counts, touched, rect, g, g < total ? (g / n_per_image) * T : 0, TX,
+                          total);
     }
 }
 
@@ -517,13 +541,10 @@ __global__ void __launch_bounds__(256) loss_kernel(const float* __restrict__ sse
     if (threadIdx.x == 0) loss[img] = (float)(sm[0] * inv_count);
 }
 
-// Partial slots: 4 per Gaussian (the <= 4-tile ones use 4 g .. 4 g + 3) plus
-// the key capacity for the Gaussians touching more tiles.
-int64_t partial_cap(int n, int64_t cap, const gi_frame& f) { return 4 * (int64_t)n * f.batch + cap; }
-
 struct BwdWs {
     float* partial;
     uint32_t* gauss_off;
+    float* ovf;
     uint32_t* counter;
     float* sse;
     size_t bytes;
@@ -537,6 +558,7 @@ BwdWs carve(void* base, int n, int64_t cap, const gi_frame& f) {
     size_t off = 0;
     w.partial = reinterpret_cast<float*>(p + off); off += align_up(sizeof(float) * 8 * (size_t)partial_cap(n, cap, f));
     w.gauss_off = reinterpret_cast<uint32_t*>(p + off); off += align_up(sizeof(uint32_t) * (total + 1));
+    w.ovf = reinterpret_cast<float*>(p + off); off += align_up(sizeof(float) * 8 * total);
     w.counter = reinterpret_cast<uint32_t*>(p + off); off += align_up(sizeof(uint32_t));
     w.sse = reinterpret_cast<float*>(p + off); off += align_up(sizeof(float) * (size_t)T * f.batch);
     w.bytes = off;
@@ -544,6 +566,13 @@ BwdWs carve(void* base, int n, int64_t cap, const gi_frame& f) {
 }
 
 }  // namespace
+
+// Partial slots: 4 per Gaussian (the <= 4-tile ones use 4 g .. 4 g + 3) plus
+// max(key capacity, 4 per Gaussian) for the Gaussians touching more tiles.
+int64_t partial_cap(int n, int64_t cap, const gi_frame& f) {
+    const int64_t fixed = 4 * (int64_t)n * f.batch;
+    return fixed + (cap > fixed ? cap : fixed);
+}
 
 size_t backward_ws_bytes(int n, int64_t cap, const gi_frame& f) { return carve(nullptr, n, cap, f).bytes; }
 
@@ -560,7 +589,8 @@ cudaError_t launch_backward_alloc(const Proj* proj, int n, const gi_frame& f, in
     const int total = n * f.batch;
     cudaError_t e = cudaMemsetAsync(w.counter, 0, sizeof(uint32_t), s);
     if (e != cudaSuccess || total == 0) return e;
-    alloc_kernel<<<(total + 255) / 256, 256, 0, s>>>(proj, total, w.counter, w.gauss_off);
+    alloc_kernel<<<(total + 255) / 256, 256, 0, s>>>(proj, total, partial_cap(n, cap, f), w.counter,
+                                                      w.gauss_off);
     note_launches(1);
     return cudaGetLastError();
 }
@@ -578,7 +608,7 @@ cudaError_t launch_backward_tiles(const Proj* proj, uint32_t* key_gid, const uin
     cudaError_t e = launch_pdl(backward_tile_kernel, dim3(TX, T / TX, f.batch), dim3(256), s, proj,
                                key_gid,
                                tile_range, (const uint32_t*)w.gauss_off, n, f.width, f.height, T,
-                               TX, presorted, dL_dimage, target, norm, partial_cap(n, cap, f), w.partial,
+                               TX, presorted, dL_dimage, target, norm, partial_cap(n, cap, f), w.partial, w.ovf,
                                mse ? w.sse : nullptr, mse ? image_out : nullptr, cs);
     note_launches(1);
     return e;
@@ -599,7 +629,7 @@ cudaError_t launch_backward_finalize(const float* params, const Proj* proj, int 
         if (adam) fa = *adam;
         e = launch_pdl(finalize_kernel, dim3((total + 255) / 256), dim3(256), s,
                        reinterpret_cast<const float4*>(params), proj, (const uint32_t*)w.gauss_off,
-                       total, n, f.width, f.height, flags, partial_cap(n, cap, f), (const float*)w.partial,
+                       total, n, f.width, f.height, flags, partial_cap(n, cap, f), (const float*)w.partial, w.ovf,
                        reinterpret_cast<float4*>(grads), fa, (const float*)w.sse, T, f.batch,
                        1.0 / count, fold ? loss : nullptr);
         note_launches(1);

@@ -144,17 +144,13 @@ __global__ void __launch_bounds__(256) scatter_kernel(const Proj* __restrict__ p
                                                       uint32_t* __restrict__ n_keys,
                                                       uint32_t* __restrict__ fill,
                                                       uint32_t* __restrict__ key_tile,
-                                                      uint32_t* __restrict__ key_gid,
-                                                      uint32_t* __restrict__ alloc_counter,
-                                                      uint32_t* __restrict__ gauss_off,
-                                                      uint32_t* __restrict__ step_counter) {
+                                                      uint32_t* __restrict__ key_gid) {
     __shared__ uint32_t start_s[kFusedScanMax];
     __shared__ uint32_t small_s[kFusedScanMax];
     __shared__ uint32_t wtot[kWarps];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     griddep_wait();
     griddep_trigger();
-    if (step_counter != nullptr && blockIdx.x == 0 && threadIdx.x == 0) *step_counter += 1u;
     // per-Gaussian inputs first: their latency overlaps the scan below
     const int g = blockIdx.x * blockDim.x + threadIdx.x;
     uint32_t cnt = g < total ? touched[g] : 0u;
@@ -203,17 +199,6 @@ __global__ void __launch_bounds__(256) scatter_kernel(const Proj* __restrict__ p
             *n_keys = all;
         }
         __syncthreads();
-    }
-    if (gauss_off != nullptr) {
-        // contiguous backward partial slots per Gaussian: 4 g for the <= 4-tile
-        // Gaussians (fixed, no allocation), 4 total + a warp-aggregated
-        // allocation for the larger ones
-        uint32_t off = 4u * (uint32_t)g;
-        if (__any_sync(kFull, cnt > 4u)) {
-            const uint32_t big_off = warp_alloc(alloc_counter, cnt > 4u ? cnt : 0u);
-            if (cnt > 4u) off = 4u * (uint32_t)total + big_off;
-        }
-        if (g < total) gauss_off[g] = off;
     }
     const int base = cnt ? (g / n) * T : 0;
     if (cnt > 0 && cnt <= 4) {
@@ -290,6 +275,7 @@ struct BinWs {
     uint32_t* big_count;
     uint32_t* fill;
     uint32_t* alloc_counter;
+    uint32_t* n_keys_acc;
     uint4* key_rank;
     uint32_t* scan_ws;
     size_t bytes;
@@ -307,6 +293,7 @@ BinWs carve(void* base, int n, int64_t cap, const gi_frame& f) {
     w.big_count = reinterpret_cast<uint32_t*>(p + off); off += sizeof(uint32_t) * (size_t)TT;
     w.fill = reinterpret_cast<uint32_t*>(p + off); off += sizeof(uint32_t) * (size_t)TT;
     w.alloc_counter = reinterpret_cast<uint32_t*>(p + off); off += sizeof(uint32_t);
+    w.n_keys_acc = reinterpret_cast<uint32_t*>(p + off); off += sizeof(uint32_t);
     off = align_up(off);                                   // 256-B (uint4 key_rank)
     w.key_rank = reinterpret_cast<uint4*>(p + off); off += align_up(sizeof(uint4) * (total + 1));
     w.scan_ws = reinterpret_cast<uint32_t*>(p + off); off += align_up(sizeof(uint32_t) * scan_ws_words(TT + 1));
@@ -322,7 +309,28 @@ size_t bin_ws_bytes(int n, int64_t cap, const gi_frame& f) { return carve(nullpt
 
 BinCounts bin_counts(void* ws, int n, int64_t cap, const gi_frame& f) {
     BinWs w = carve(ws, n, cap, f);
-    return BinCounts{w.tile_count, w.big_count, w.key_rank};
+    return BinCounts{w.tile_count, w.big_count, w.key_rank, nullptr, 0u, nullptr, nullptr, nullptr, 0u};
+}
+
+uint32_t slab_capacity(int64_t cap, const gi_frame& f) {
+    const int64_t TT = (int64_t)tiles_x(f.width) * tiles_y(f.height) * f.batch;
+    return TT > 0 ? (uint32_t)(cap / TT) : 0u;
+}
+
+BinCounts bin_counts_direct(void* ws, int n, int64_t cap, const gi_frame& f, uint32_t* slab,
+                            uint32_t* gauss_off) {
+    BinWs w = carve(ws, n, cap, f);
+    const int64_t pc = partial_cap(n, cap, f);
+    return BinCounts{w.tile_count, w.big_count, w.key_rank, slab, slab_capacity(cap, f),
+                     w.n_keys_acc, gauss_off, gauss_off ? w.alloc_counter : nullptr,
+                     (uint32_t)(pc < 0xffffffffll ? pc : 0xffffffffll)};
+}
+
+ChainState bin_chain_direct(void* ws, int n, int64_t cap, const gi_frame& f, uint32_t* slab,
+                            uint32_t* gauss_off, uint32_t* n_keys, uint32_t* step_counter) {
+    BinWs w = carve(ws, n, cap, f);
+    return ChainState{w.tile_count, w.big_count, w.fill, w.alloc_counter, gauss_off, slab,
+                      slab_capacity(cap, f), n_keys, w.n_keys_acc, step_counter};
 }
 
 uint32_t* bin_alloc_counter(void* ws, int n, int64_t cap, const gi_frame& f) {
@@ -332,33 +340,25 @@ uint32_t* bin_alloc_counter(void* ws, int n, int64_t cap, const gi_frame& f) {
 cudaError_t bin_clear(void* ws, int n, int64_t cap, const gi_frame& f, cudaStream_t s) {
     BinWs w = carve(ws, n, cap, f);
     const size_t TT = (size_t)tiles_x(f.width) * tiles_y(f.height) * f.batch;
-    return cudaMemsetAsync(w.tile_count, 0, sizeof(uint32_t) * ((kCountStride + 2) * TT + 1), s);
-}
-
-ChainState bin_chain_state(void* bin_ws, int n, int64_t cap, const gi_frame& f, uint32_t* gauss_off) {
-    BinWs w = carve(bin_ws, n, cap, f);
-    return ChainState{w.tile_count, w.big_count, w.fill, w.alloc_counter, gauss_off};
+    return cudaMemsetAsync(w.tile_count, 0, sizeof(uint32_t) * ((kCountStride + 2) * TT + 2), s);
 }
 
 cudaError_t launch_bin(const Proj* proj, const uint32_t* tiles_touched, int n, const gi_frame& f,
                        int64_t cap, void* ws, uint32_t* key_tile, uint32_t* key_gid,
-                       uint32_t* tile_range, uint32_t* n_keys, bool counted, bool sort,
-                       uint32_t* gauss_off, cudaStream_t s, uint32_t* step_counter) {
+                       uint32_t* tile_range, uint32_t* n_keys, cudaStream_t s) {
     BinWs w = carve(ws, n, cap, f);
     const int total = n * f.batch;
     const int TX = tiles_x(f.width);
     const int T = TX * tiles_y(f.height);
     const int TT = T * f.batch;
     cudaError_t e;
-    if (!counted) {
-        if ((e = bin_clear(ws, n, cap, f, s)) != cudaSuccess) return e;
-        if (total > 0) {
-            e = launch_pdl(count_kernel, dim3((total + 255) / 256), dim3(256), s, proj, tiles_touched,
-                           total, n, T, TX, BinCounts{w.tile_count, w.big_count, w.key_rank});
-            if (e != cudaSuccess) return e;
-            note_launches(1);
-            if ((e = cudaGetLastError()) != cudaSuccess) return e;
-        }
+    if ((e = bin_clear(ws, n, cap, f, s)) != cudaSuccess) return e;
+    if (total > 0) {
+        e = launch_pdl(count_kernel, dim3((total + 255) / 256), dim3(256), s, proj, tiles_touched,
+                       total, n, T, TX, BinCounts{w.tile_count, w.big_count, w.key_rank});
+        if (e != cudaSuccess) return e;
+        note_launches(1);
+        if ((e = cudaGetLastError()) != cudaSuccess) return e;
     }
     const bool fuse = TT <= kFusedScanMax && total > 0;
     if (!fuse) {
@@ -382,13 +382,12 @@ cudaError_t launch_bin(const Proj* proj, const uint32_t* tiles_touched, int n, c
     if (total > 0) {
         e = launch_pdl(scatter_kernel, dim3((total + 255) / 256), dim3(256), s, proj, tiles_touched,
                        total, n, T, TX, TT, cap, fuse, BinCounts{w.tile_count, w.big_count, w.key_rank},
-                       tile_range, n_keys, w.fill, key_tile, key_gid,
-                       gauss_off ? w.alloc_counter : nullptr, gauss_off, step_counter);
+                       tile_range, n_keys, w.fill, key_tile, key_gid);
         if (e != cudaSuccess) return e;
         note_launches(1);
         if ((e = cudaGetLastError()) != cudaSuccess) return e;
     }
-    if (sort) {
+    {   // per-tile gid order (the gi_bin contract)
         e = launch_pdl(segsort_kernel, dim3(TT), dim3(256), s, proj, n, T, TX,
                        (const uint32_t*)tile_range, key_gid);
         if (e != cudaSuccess) return e;

@@ -121,12 +121,20 @@ void note_launches(int k);
 int64_t g_launches_get();
 
 // Internal launchers (api.cu validates arguments).
-// Binning step 1 targets.  A Gaussian touching <= 4 tiles counts its keys on
-// tile_count with atomics that RETURN the key's rank within the tile, kept in
-// key_rank[g] (row-major rectangle order), so the scatter needs no atomics;
-// keys of larger Gaussians are counted on big_count and claim their slots
-// after the small ones.  All counters must be zero on entry (bin_clear, or
-// left zeroed by the consumer kernel of the previous fused call).
+//
+// Binning step 1 targets.  Every key (tile t, Gaussian g) is counted on
+// tile_count[t] with an atomic that RETURNS the key's rank within the tile.
+//  * direct binning (fused paths; slab != null): the key is written straight
+//    to slab[t * slab_cap + rank] -- no scan, no scatter pass.  A tile whose
+//    count exceeds slab_cap is served by its consumer from a stream of all
+//    Gaussians instead (raster_common.cuh), so the result never depends on
+//    the capacity.  Gaussians touching > 4 tiles are emitted warp-
+//    cooperatively (post_project_warp) and get backward partial slots
+//    allocated there.
+//  * gi_bin contract (slab == null): ranks of <= 4-tile Gaussians are kept
+//    in key_rank for the scatter; larger ones count on big_count.
+// All counters must be zero on entry (bin_clear, or left zeroed by the
+// consumer kernel of the previous fused call).
 // tile_count words are kCountStride u32 apart: the count atomics (one per
 // key, ~80 per tile, all issued within a few microseconds) then spread over
 // L2 slices instead of queueing on the few slices that hold a packed table.
@@ -136,12 +144,29 @@ int64_t g_launches_get();
 constexpr int kCountStride = GI_COUNT_STRIDE;
 
 struct BinCounts {
-    uint32_t* tile_count;   // [B*T * kCountStride] keys of small Gaussians (null: no counting)
-    uint32_t* big_count;    // [B*T] keys of Gaussians touching > 4 tiles
-    uint4* key_rank;        // [B*N] ranks of a small Gaussian's keys
+    uint32_t* tile_count;   // [B*T * kCountStride] key counts (null: no counting)
+    uint32_t* big_count;    // [B*T] gi_bin path: keys of Gaussians touching > 4 tiles
+    uint4* key_rank;        // [B*N] gi_bin path: ranks of a small Gaussian's keys
+    uint32_t* slab;         // direct binning: [B*T][slab_cap] key slots (null: gi_bin path)
+    uint32_t slab_cap;
+    uint32_t* n_keys_acc;   // direct binning: total keys accumulate here (may be null)
+    uint32_t* gauss_off;    // direct binning + backward: partial slots of > 4-tile Gaussians
+    uint32_t* alloc_counter;
+    uint32_t part_cap;      // partial slots in all (4 total fixed + the allocatable rest)
 };
 
+// gauss_off value of a > 4-tile Gaussian whose slots did not fit: its tiles
+// add their partial sums atomically into a per-Gaussian accumulator instead.
+constexpr uint32_t kOffOverflow = 0xffffffffu;
+// Backward partial slots: 4 per Gaussian + max(key capacity, 4 per Gaussian).
+int64_t partial_cap(int n, int64_t cap, const gi_frame& f);
+
+__device__ __forceinline__ uint32_t* count_word(const BinCounts& bc, int t) {
+    return &bc.tile_count[(size_t)t * kCountStride];
+}
+
 // Count the keys of Gaussian g (rect in tiles, `touched` tiles) into bc.
+// Direct binning handles <= 4 tiles here, larger ones in post_project_warp.
 __device__ __forceinline__ void count_keys(const BinCounts& bc, int g, int tx0, int tx1, int ty0,
                                            int ty1, uint32_t touched, int base, int TX) {
     if (touched <= 4u) {
@@ -149,18 +174,66 @@ __device__ __forceinline__ void count_keys(const BinCounts& bc, int g, int tx0, 
         // independent and issued back to back
         const int w = tx1 - tx0 + 1;
         uint32_t r[4] = {0u, 0u, 0u, 0u};
+        int t[4] = {0, 0, 0, 0};
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
             if ((uint32_t)i < touched) {
                 const int dy = (i >= w) + (i >= 2 * w) + (i >= 3 * w);
-                const int dx = i - dy * w;
-                r[i] = atomicAdd(&bc.tile_count[(size_t)(base + (ty0 + dy) * TX + tx0 + dx) * kCountStride], 1u);
+                t[i] = base + (ty0 + dy) * TX + tx0 + (i - dy * w);
+                r[i] = atomicAdd(count_word(bc, t[i]), 1u);
             }
         }
-        bc.key_rank[g] = make_uint4(r[0], r[1], r[2], r[3]);
-    } else {
+        if (bc.slab != nullptr) {
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+                if ((uint32_t)i < touched && r[i] < bc.slab_cap)
+                    bc.slab[(size_t)t[i] * bc.slab_cap + r[i]] = (uint32_t)g;
+        } else {
+            bc.key_rank[g] = make_uint4(r[0], r[1], r[2], r[3]);
+        }
+    } else if (bc.slab == nullptr) {
         for (int ty = ty0; ty <= ty1; ++ty)
             for (int tx = tx0; tx <= tx1; ++tx) atomicAdd(&bc.big_count[base + ty * TX + tx], 1u);
+    }
+}
+
+// Warp-uniform tail of a direct-binning producer (project_kernel, chained
+// finalize): accumulate the key total, allocate backward partial slots for
+// Gaussians touching > 4 tiles (4 total + offset; <= 4-tile Gaussians use
+// the fixed slots 4 g ..) and emit their keys with the lanes of the warp
+// striding over each one's tile rectangle.  touched = 0 for inactive lanes;
+// rect = (tx0, tx1, ty0, ty1); base = image * T.
+__device__ __forceinline__ void post_project_warp(const BinCounts& bc, uint32_t touched,
+                                                  int4 rect, int g, int base, int TX, int total) {
+    const int lane = threadIdx.x & 31;
+    if (bc.n_keys_acc != nullptr) {
+        const uint32_t sum = __reduce_add_sync(kFull, touched);
+        if (lane == 0 && sum != 0u) atomicAdd(bc.n_keys_acc, sum);
+    }
+    if (bc.slab == nullptr) return;
+    const bool big = touched > 4u;
+    unsigned m = __ballot_sync(kFull, big);
+    if (m == 0u) return;
+    if (bc.gauss_off != nullptr) {
+        const uint32_t off = warp_alloc(bc.alloc_counter, big ? touched : 0u);
+        const uint64_t first = 4ull * (uint32_t)total + off;
+        if (big) bc.gauss_off[g] = first + touched <= bc.part_cap ? (uint32_t)first : kOffOverflow;
+    }
+    while (m) {
+        const int j = __ffs(m) - 1;
+        m &= m - 1;
+        const int tx0 = __shfl_sync(kFull, rect.x, j), tx1 = __shfl_sync(kFull, rect.y, j);
+        const int ty0 = __shfl_sync(kFull, rect.z, j);
+        const uint32_t c = __shfl_sync(kFull, touched, j);
+        const int b = __shfl_sync(kFull, base, j);
+        const uint32_t gid = (uint32_t)__shfl_sync(kFull, g, j);
+        const int w = tx1 - tx0 + 1;
+        for (uint32_t i = lane; i < c; i += 32) {
+            const int dy = (int)i / w;
+            const int t = b + (ty0 + dy) * TX + tx0 + ((int)i - dy * w);
+            const uint32_t r = atomicAdd(count_word(bc, t), 1u);
+            if (r < bc.slab_cap) bc.slab[(size_t)t * bc.slab_cap + r] = gid;
+        }
     }
 }
 
@@ -180,20 +253,30 @@ struct ChainState {
     uint32_t* fill;
     uint32_t* alloc_counter;
     uint32_t* gauss_off;
+    // direct binning (fused paths): the consumer reads its keys from the slab,
+    // publishes *n_keys_acc to *n_keys and re-zeroes the accumulator
+    uint32_t* slab;
+    uint32_t slab_cap;
+    uint32_t* n_keys;
+    uint32_t* n_keys_acc;
+    uint32_t* step_counter;   // chained fit: incremented once by the consumer
 };
 cudaError_t launch_project(const float* params, int n, const gi_frame& f, uint32_t flags,
                            Proj* proj, uint32_t* tiles_touched, const ProjectFuse& fuse,
                            cudaStream_t s);
-// counted: the per-tile counts in ws were already accumulated (fused project).
-// sort: run the per-tile gid sort (gi_bin contract); the fused consumers sort
-// in shared memory instead.
+// gi_bin: count, scan, scatter and per-tile gid sort into contiguous arrays.
 cudaError_t launch_bin(const Proj* proj, const uint32_t* tiles_touched, int n, const gi_frame& f,
                        int64_t cap, void* ws, uint32_t* key_tile, uint32_t* key_gid,
-                       uint32_t* tile_range, uint32_t* n_keys, bool counted, bool sort,
-                       uint32_t* gauss_off, cudaStream_t s, uint32_t* step_counter = nullptr);
-ChainState bin_chain_state(void* bin_ws, int n, int64_t cap, const gi_frame& f, uint32_t* gauss_off);
+                       uint32_t* tile_range, uint32_t* n_keys, cudaStream_t s);
 size_t bin_ws_bytes(int n, int64_t cap, const gi_frame& f);
 BinCounts bin_counts(void* ws, int n, int64_t cap, const gi_frame& f);
+// Direct binning (fused paths): keys go to slab = a key_gid array of cap
+// entries, slab_cap = cap / (tiles x batch) per tile.
+uint32_t slab_capacity(int64_t cap, const gi_frame& f);
+BinCounts bin_counts_direct(void* ws, int n, int64_t cap, const gi_frame& f, uint32_t* slab,
+                            uint32_t* gauss_off);
+ChainState bin_chain_direct(void* ws, int n, int64_t cap, const gi_frame& f, uint32_t* slab,
+                            uint32_t* gauss_off, uint32_t* n_keys, uint32_t* step_counter);
 uint32_t* bin_alloc_counter(void* ws, int n, int64_t cap, const gi_frame& f);
 cudaError_t bin_clear(void* ws, int n, int64_t cap, const gi_frame& f, cudaStream_t s);
 cudaError_t launch_render(const Proj* proj, uint32_t* key_gid, const uint32_t* tile_range, int n,

@@ -25,9 +25,17 @@ __global__ void __launch_bounds__(256) project_kernel(const float4* __restrict__
     griddep_wait();
     griddep_trigger();
     if (fuse.step_counter != nullptr && g == 0) *fuse.step_counter += 1u;   // fused fit: t <- t + 1
-    if (g < total)
-        tiles_touched[g] = project_one(params[2 * (size_t)g], params[2 * (size_t)g + 1], g, n, W, H,
-                                       k, flags, proj, fuse.counts);
+    uint32_t touched = 0;
+    int4 rect = make_int4(0, -1, 0, -1);
+    if (g < total) {
+        touched = project_one(params[2 * (size_t)g], params[2 * (size_t)g + 1], g, n, W, H, k,
+                              flags, proj, fuse.counts, rect);
+        tiles_touched[g] = touched;
+    }
+    if (fuse.counts.tile_count != nullptr) {
+        const int TX = (W + kTile - 1) / kTile, T = TX * ((H + kTile - 1) / kTile);
+        post_project_warp(fuse.counts, touched, rect, g, g < total ? (g / n) * T : 0, TX, total);
+    }
 }
 
 }  // namespace

@@ -10,7 +10,8 @@ namespace gi {
 __device__ __forceinline__ uint32_t project_one(const float4 p0 /* mux, muy, l1, l2 */,
                                                 const float4 p1 /* l3, c'r, c'g, c'b */, int g,
                                                 int n, int W, int H, float k, uint32_t flags,
-                                                Proj* __restrict__ proj, const BinCounts& bc) {
+                                                Proj* __restrict__ proj, const BinCounts& bc,
+                                                int4& rect /* out: tile rect when touched > 0 */) {
     // App. C: u = tanh(mu_raw); R2: mu = (u + 1) * W / 2  (fp64, no contraction)
     double ux = (double)p0.x, uy = (double)p0.y;
     if (pos_logit(flags)) {
@@ -62,11 +63,11 @@ __device__ __forceinline__ uint32_t project_one(const float4 p0 /* mux, muy, l1,
             bx = (uint32_t)x0 | ((uint32_t)x1 << 16);
             by = (uint32_t)y0 | ((uint32_t)y1 << 16);
             touched = (uint32_t)((x1 / kTile - x0 / kTile + 1) * (y1 / kTile - y0 / kTile + 1));
+            rect = make_int4(x0 / kTile, x1 / kTile, y0 / kTile, y1 / kTile);
             if (bc.tile_count != nullptr) {   // fused binning step 1: counts and ranks
                 const int TX = (W + kTile - 1) / kTile;
                 const int T = TX * ((H + kTile - 1) / kTile);
-                count_keys(bc, g, x0 / kTile, x1 / kTile, y0 / kTile, y1 / kTile, touched,
-                           (g / n) * T, TX);
+                count_keys(bc, g, rect.x, rect.y, rect.z, rect.w, touched, (g / n) * T, TX);
             }
         }
     }

@@ -67,7 +67,7 @@ __device__ __forceinline__ TileCtx make_tile_ctx(int W, int H, int TX) {
 //   b = {c'g, c'b, mx, my}      centre minus the tile origin
 //   c = {lx0 | lx1 << 8 | ly0 << 16 | ly1 << 24   box clipped to the tile,
 //        column mask | row mask << 16,            the same as 16-bit masks,
-//        partial slot (backward only), 0}
+//        partial slot (backward only), gid}
 struct StagedRecords {
     float4 a[256];
     float4 b[256];
@@ -107,12 +107,13 @@ __device__ __forceinline__ void stage_gid(StagedRecords& sr, const Proj* __restr
         const int rtx0 = x0 / kTile, rtx1 = x1 / kTile, rty0 = y0 / kTile, rty1 = y1 / kTile;
         const int rw = rtx1 - rtx0 + 1;
         const uint32_t off = rw * (rty1 - rty0 + 1) <= 4 ? 4u * gid : gauss_off[gid];
-        slot = off + (uint32_t)((t.ty - rty0) * rw + (t.tx - rtx0));
+        slot = off == kOffOverflow ? kOffOverflow
+                                   : off + (uint32_t)((t.ty - rty0) * rw + (t.tx - rtx0));
     }
     sr.a[j] = make_float4(r.q1.x, r.q1.y, r.q1.z, r.q2.x);
     sr.b[j] = make_float4(r.q2.y, r.q2.z, mx, my);
     sr.c[j] = make_uint4((uint32_t)(lx0 | lx1 << 8 | ly0 << 16 | ly1 << 24),
-                         span_mask16(lx0, lx1) | span_mask16(ly0, ly1) << 16, slot, 0u);
+                         span_mask16(lx0, lx1) | span_mask16(ly0, ly1) << 16, slot, gid);
 }
 
 // Lanes of the 8x4 warp block (lane = ly * 8 + lx) inside the box given by
@@ -259,6 +260,128 @@ __device__ __forceinline__ int sorted_segment(const Proj* __restrict__ proj,
     __threadfence_block();
     __syncthreads();
     return -1;
+}
+
+
+// ----------------------------------------------------- segment sources
+// Where a consumer tile kernel takes its keys from.
+enum SegMode : int {
+    kSegSorted = 0,   // sorted into shared memory: sl[0 .. L)
+    kSegGlobal = 1,   // key_gid[s .. s + L), already in gid order
+    kSegStream = 2,   // overflowed slab: streamed in gid order from all Gaussians
+};
+struct Seg {
+    uint32_t s, L;
+    int mode;
+};
+
+// Open the tile's key segment; all threads must call.  Direct binning
+// (cs.slab): every thread reads the tile's count (one broadcast load, no
+// barrier on the critical path); close_segment re-zeroes it at the end of
+// the kernel.  *cursor is set to 0 for kSegStream.
+__device__ __forceinline__ Seg open_segment(const Proj* __restrict__ proj,
+                                            uint32_t* __restrict__ key_gid,
+                                            const uint32_t* __restrict__ tile_range,
+                                            bool presorted, const ChainState& cs, int n, int T,
+                                            const TileCtx& t, uint32_t* sl, uint32_t* scratch8,
+                                            uint32_t* cursor) {
+    const int tt = t.img * T + t.tile;
+    if (cs.slab != nullptr) {
+        const uint32_t count = *(volatile const uint32_t*)&cs.tile_count[(size_t)tt * kCountStride];
+        const uint32_t s = (uint32_t)tt * cs.slab_cap;
+        if (count > cs.slab_cap) {
+            if (threadIdx.x == 0) *cursor = 0u;
+            __syncthreads();
+            return Seg{s, count, kSegStream};
+        }
+        const int r = sorted_segment(proj, key_gid, s, s + count, n, t.img, t.tx, t.ty, sl, scratch8);
+        return Seg{s, count, r >= 0 ? kSegSorted : kSegGlobal};
+    }
+    if (threadIdx.x == 0 && cs.tile_count != nullptr) {   // leave the counters zero for the next call
+        cs.tile_count[(size_t)tt * kCountStride] = 0u;
+        cs.big_count[tt] = 0u;
+        cs.fill[tt] = 0u;
+        if (tt == 0 && cs.alloc_counter != nullptr) *cs.alloc_counter = 0u;
+    }
+    const uint32_t s = tile_range[tt], e = tile_range[tt + 1];
+    if (presorted) return Seg{s, e - s, kSegGlobal};
+    const int r = sorted_segment(proj, key_gid, s, e, n, t.img, t.tx, t.ty, sl, scratch8);
+    return Seg{s, e - s, r >= 0 ? kSegSorted : kSegGlobal};
+}
+
+// Direct binning, at the end of a consumer kernel (thread 0): leave the
+// tile's count zero for the next producer; CTA 0 publishes the producer's key
+// total, resets the partial-slot allocator and (chained fit) advances the
+// step counter.  The next kernel runs after this grid completes.
+__device__ __forceinline__ void close_segment(const ChainState& cs, int tt) {
+    if (threadIdx.x != 0 || cs.slab == nullptr) return;
+    cs.tile_count[(size_t)tt * kCountStride] = 0u;
+    if (tt == 0) {
+        if (cs.n_keys != nullptr) {
+            *cs.n_keys = *cs.n_keys_acc;
+            *cs.n_keys_acc = 0u;
+        }
+        if (cs.alloc_counter != nullptr) *cs.alloc_counter = 0u;
+        if (cs.step_counter != nullptr) *cs.step_counter += 1u;
+    }
+}
+
+// kSegStream: gather the next `want` (<= 256) Gaussians of image img whose
+// tile rectangle contains (tx, ty), in gid order, from *cursor on, into
+// out[0 ..).  Returns how many were found (want unless the image ran out).
+// All threads must call.
+__device__ __forceinline__ int stream_keys(const Proj* __restrict__ proj, int n, int img, int tx,
+                                           int ty, int want, uint32_t* cursor, uint32_t* out,
+                                           uint32_t* scratch8) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    int got = 0;
+    while (got < want) {
+        const uint32_t cur = *cursor;
+        if (cur >= (uint32_t)n) break;
+        const uint32_t gi = cur + threadIdx.x;
+        const bool hit = gi < (uint32_t)n && covers_tile(proj, (uint32_t)(img * n) + gi, tx, ty);
+        const unsigned m = __ballot_sync(kFull, hit);
+        if (lane == 0) scratch8[warp] = __popc(m);
+        __syncthreads();
+        int before = 0, tot = 0;
+#pragma unroll
+        for (int w = 0; w < kWarps; ++w) {
+            const int c = (int)scratch8[w];
+            before += w < warp ? c : 0;
+            tot += c;
+        }
+        const int take = min(tot, want - got);
+        const int rank = before + __popc(m & lanemask_lt());
+        if (hit && rank < take) out[got + rank] = (uint32_t)(img * n) + gi;
+        __syncthreads();
+        if (take == tot) {
+            if (threadIdx.x == 0) *cursor = cur + blockDim.x;
+        } else if (hit && rank == take - 1) {
+            *cursor = gi + 1u;
+        }
+        got += take;
+        __syncthreads();
+    }
+    return got;
+}
+
+// The gids of batch [base, base + 256) of the segment: thread i < returned
+// count gets key base + i.  All threads must call (kSegStream gathers the
+// batch block-wide into sl).
+__device__ __forceinline__ int batch_gid(const Seg& sg, uint32_t base, const uint32_t* key_gid,
+                                         uint32_t* sl, const Proj* __restrict__ proj, int n,
+                                         const TileCtx& t, uint32_t* cursor, uint32_t* scratch8,
+                                         uint32_t& gid) {
+    int cnt = (int)min(256u, sg.L - base);
+    if (sg.mode == kSegStream) {
+        cnt = stream_keys(proj, n, t.img, t.tx, t.ty, cnt, cursor, sl, scratch8);
+        gid = (int)threadIdx.x < cnt ? sl[threadIdx.x] : 0u;
+    } else if (sg.mode == kSegSorted) {
+        gid = (int)threadIdx.x < cnt ? sl[base + threadIdx.x] : 0u;
+    } else {
+        gid = (int)threadIdx.x < cnt ? key_gid[sg.s + base + threadIdx.x] : 0u;
+    }
+    return cnt;
 }
 
 }  // namespace gi

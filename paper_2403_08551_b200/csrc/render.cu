@@ -15,6 +15,7 @@ struct RenderShared {
     WarpLists wl;
     alignas(16) uint32_t sl[kSortMax];
     uint32_t scratch[kWarps];
+    uint32_t cursor;
 };
 
 __global__ void __launch_bounds__(256) render_kernel(const Proj* __restrict__ proj,
@@ -27,28 +28,16 @@ __global__ void __launch_bounds__(256) render_kernel(const Proj* __restrict__ pr
     const TileCtx t = make_tile_ctx(W, H, TX);
     griddep_wait();
     griddep_trigger();
-    if (threadIdx.x == 0 && cs.tile_count != nullptr) {   // leave the counters zero for the next call
-        const int tt = t.img * T + t.tile;
-        cs.tile_count[(size_t)tt * kCountStride] = 0u;
-        cs.big_count[tt] = 0u;
-        cs.fill[tt] = 0u;
-        if (tt == 0 && cs.alloc_counter != nullptr) *cs.alloc_counter = 0u;
-    }
-    const uint32_t s = tile_range[t.img * T + t.tile];
-    const uint32_t e = tile_range[t.img * T + t.tile + 1];
     // presorted: the segment comes from gi_bin (already in gid order); else it
-    // comes from the fused scatter and is ordered here
-    const int sorted = presorted ? -1
-                                 : sorted_segment(proj, key_gid, s, e, n, t.img, t.tx, t.ty, sh.sl,
-                                                  sh.scratch);
+    // comes from direct binning and is ordered here
+    const Seg sg = open_segment(proj, key_gid, tile_range, presorted, cs, n, T, t, sh.sl,
+                                sh.scratch, &sh.cursor);
     float acc0 = 0.f, acc1 = 0.f, acc2 = 0.f;
-    for (uint32_t base = 0; base < e - s; base += 256) {
-        const int cnt = (int)min(256u, e - s - base);
+    for (uint32_t base = 0; base < sg.L; base += 256) {
         if (base > 0) __syncthreads();
-        if ((int)threadIdx.x < cnt) {
-            const uint32_t gid = sorted >= 0 ? sh.sl[base + threadIdx.x] : key_gid[s + base + threadIdx.x];
-            stage_gid(sh.sr, proj, gid, threadIdx.x, t);
-        }
+        uint32_t gid;
+        const int cnt = batch_gid(sg, base, key_gid, sh.sl, proj, n, t, &sh.cursor, sh.scratch, gid);
+        if ((int)threadIdx.x < cnt) stage_gid(sh.sr, proj, gid, threadIdx.x, t);
         __syncthreads();
         const int nl = build_warp_list(sh.sr, sh.wl, cnt, t);
         forward_batch(sh.sr, sh.wl, nl, t, acc0, acc1, acc2);
@@ -60,6 +49,7 @@ __global__ void __launch_bounds__(256) render_kernel(const Proj* __restrict__ pr
         im[P] = acc1;
         im[2 * P] = acc2;
     }
+    close_segment(cs, t.img * T + t.tile);
 }
 
 }  // namespace

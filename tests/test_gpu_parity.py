@@ -508,3 +508,58 @@ def test_rs_fit_steps(gi, gio):
         torch.cuda.synchronize()
         res.append(fit.params.clone())
     assert torch.equal(res[0], res[1])
+
+
+@pytest.mark.parametrize("per_tile", [2, 40])
+def test_direct_binning_overflow(gi, gio, per_tile):
+    # slab capacity below the per-tile key count: overflowing tiles stream
+    # their keys in gid order from all Gaussians, so frames, gradients and
+    # updates are bitwise those of a roomy slab (and match the oracle)
+    from paper_2403_08551_b200.pipeline import Fitter, Pipeline
+    W, H, n = 96, 64, 600
+    p = params_for(n, 3, True)
+    tgt = synth.image(3, W, H)
+    TT = (W // 16) * (H // 16)
+    small = TT * per_tile
+    pd = to_dev(p)[None].contiguous()
+    a = Pipeline(n, W, H, 1, device=DEV).render_frame(pd).clone()
+    b = Pipeline(n, W, H, 1, key_capacity=small, device=DEV).render_frame(pd).clone()
+    torch.cuda.synchronize()
+    assert torch.equal(a, b)
+    ref_img, loss, g = gio.loss_and_grads(p, tgt, mode=gio.ALL_PAIRS)
+    assert np.abs(b[0].cpu().numpy() - ref_img).max() <= PIX_TOL
+    res = []
+    for cap in (None, small):
+        fit = Fitter(pd.clone(), to_dev(tgt)[None].contiguous(), key_capacity=cap)
+        fit.step()
+        torch.cuda.synchronize()
+        assert max(group_err(fit.grads[0].cpu().numpy().astype(np.float64), g).values()) <= GRAD_TOL
+        for _ in range(3):
+            fit.step()
+        torch.cuda.synchronize()
+        assert fit.check() == gi.GI_OK
+        res.append((fit.params.clone(), fit.loss.clone(), fit.n_keys()))
+    assert torch.equal(res[0][0], res[1][0]) and torch.equal(res[0][1], res[1][1])
+    assert res[0][2] == res[1][2]
+
+
+def test_partial_slot_overflow(gi, gio):
+    # Gaussians touching ~20 tiles with a tiny key capacity: their backward
+    # partial slots do not fit, so their tiles accumulate atomically; the
+    # gradients still match the oracle
+    from paper_2403_08551_b200.pipeline import Fitter
+    W, H, n = 96, 64, 300
+    p = synth.init_params(4, n)
+    rng = np.random.default_rng(44)
+    p[:, 2] = rng.uniform(6.0, 10.0, n).astype(np.float32)
+    p[:, 4] = rng.uniform(3.0, 6.0, n).astype(np.float32)
+    p[:, 5:8] *= np.float32(0.05)
+    tgt = synth.image(4, W, H)
+    _, loss, g = gio.loss_and_grads(p, tgt, mode=gio.ALL_PAIRS)
+    for cap in (None, 48):
+        fit = Fitter(to_dev(p)[None].contiguous(), to_dev(tgt)[None].contiguous(), key_capacity=cap)
+        fit.step()
+        torch.cuda.synchronize()
+        assert fit.check() == gi.GI_OK
+        assert abs(float(fit.loss[0]) - loss) <= 1e-5 * loss
+        assert max(group_err(fit.grads[0].cpu().numpy().astype(np.float64), g).values()) <= GRAD_TOL
