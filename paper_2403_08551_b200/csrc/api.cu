@@ -278,8 +278,15 @@ static gi_status fit_step_impl(float* params, float* grads, float* m, float* v, 
     // kernel of each call).
     uint32_t* gauss_off = gi::backward_gauss_off(w.bwd_ws, n, key_capacity, *f);
     const gi::BinCounts bc = gi::bin_counts_direct(w.bin_ws, n, key_capacity, *f, w.key_gid, gauss_off);
-    const gi::ChainState cs = gi::bin_chain_direct(w.bin_ws, n, key_capacity, *f, w.key_gid, gauss_off,
-                                                   w.n_keys, chained ? step_counter : nullptr);
+    gi::ChainState cs = gi::bin_chain_direct(w.bin_ws, n, key_capacity, *f, w.key_gid, gauss_off,
+                                             w.n_keys, chained ? step_counter : nullptr);
+    float* consts = gi::backward_adam_consts(w.bwd_ws, n, key_capacity, *f);
+    cs.adam_consts = consts;          // {lr_t, 1/(1 - b1^t), 1/(1 - b2^t)} from the tile kernel
+    cs.step_read = step_counter;
+    cs.lr0 = lr0;
+    cs.half_every = half_every;
+    cs.b1 = beta1;
+    cs.b2 = beta2;
     GI_TRY(record_stage(stage_events, 0, s), "gi_fit_step/event");
     if (!chained)
         GI_TRY(gi::launch_project(params, n, *f, flags, w.proj, w.touched,
@@ -291,7 +298,7 @@ static gi_status fit_step_impl(float* params, float* grads, float* m, float* v, 
                                      key_capacity, w.bwd_ws, nullptr, cs, s),
            "gi_fit_step/backward");
     GI_TRY(record_stage(stage_events, 3, s), "gi_fit_step/event");
-    gi::FusedAdam fa{params, m, v, step_counter, lr0, half_every, beta1, beta2, eps, status_flags,
+    gi::FusedAdam fa{params, m, v, consts, beta1, beta2, eps, status_flags,
                      chained ? w.proj : nullptr, w.touched, bc, f->k, flags};
     GI_TRY(gi::launch_backward_finalize(params, w.proj, n, *f, flags, true, key_capacity, w.bwd_ws,
                                         grads, loss, &fa, s),

@@ -29,6 +29,10 @@
 namespace gi {
 namespace {
 
+// Fixed-point scale of the per-tile squared-error sums (2^40: a tile's sum
+// is at most 768 on the [0, 1] scale, a batch image's at most ~1.2e18 / 2^40).
+constexpr double kSseScale = 1099511627776.0;
+
 struct BwdShared {
     StagedRecords sr;
     union {
@@ -59,7 +63,7 @@ __global__ void __launch_bounds__(256, 5) backward_tile_kernel(
     const uint32_t* __restrict__ tile_range, const uint32_t* __restrict__ gauss_off, int n,
     int W, int H, int T, int TX, bool presorted, const float* __restrict__ dL_dimage,
     const float* __restrict__ target, float norm, int64_t pcap, float* __restrict__ partial,
-    float* __restrict__ ovf, float* __restrict__ sse_part, float* __restrict__ image_out,
+    float* __restrict__ ovf, unsigned long long* __restrict__ sse_acc, float* __restrict__ image_out,
     ChainState cs) {
     __shared__ BwdShared sh;
     const TileCtx t = make_tile_ctx(W, H, TX);
@@ -109,7 +113,7 @@ __global__ void __launch_bounds__(256, 5) backward_tile_kernel(
                 image_out[pix + 2 * P] = acc2;
             }
         }
-        if (sse_part != nullptr) {
+        if (sse_acc != nullptr) {
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) sq += __shfl_xor_sync(kFull, sq, o);
             if (t.lane == 0) sh.sse[t.warp] = sq;
@@ -117,11 +121,13 @@ __global__ void __launch_bounds__(256, 5) backward_tile_kernel(
     }
     sh.g[lpix] = make_float4(g0, g1, g2, 0.f);
     __syncthreads();
-    if (sse_part != nullptr && dL_dimage == nullptr && threadIdx.x == 0) {
+    if (sse_acc != nullptr && dL_dimage == nullptr && threadIdx.x == 0) {
+        // per-image squared error in 2^-40 fixed point: integer addition is
+        // associative, so the loss is deterministic whatever the tile order
         float tot = 0.f;
 #pragma unroll
         for (int w = 0; w < kWarps; ++w) tot += sh.sse[w];
-        sse_part[t.img * T + t.tile] = tot;
+        atomicAdd(&sse_acc[t.img], (unsigned long long)__double2ll_rn((double)tot * kSseScale));
     }
 
     // ---- pass 2: gradients, Gaussian-parallel, work-balanced chunks ----
@@ -349,10 +355,8 @@ __global__ void __launch_bounds__(256) finalize_kernel(
     uint32_t flags, int64_t pcap,
     const float* __restrict__ partial, float* __restrict__ ovf, float4* __restrict__ grads,
     FusedAdam adam,
-    const float* __restrict__ sse_part, int T, int batch, double inv_count,
+    unsigned long long* __restrict__ sse_acc, int batch, double inv_count,
     float* __restrict__ loss) {
-    __shared__ float sconst[3];
-    __shared__ double lsum[kWarps];
     griddep_wait();
     griddep_trigger();
     const int g = blockIdx.x * blockDim.x + threadIdx.x;
@@ -369,28 +373,19 @@ __global__ void __launch_bounds__(256) finalize_kernel(
             m0 = mm[0]; m1 = mm[1]; v0 = vv[0]; v1 = vv[1];
         }
     }
-    if (loss != nullptr && blockIdx.x < batch) {
-        // per-image L2 loss: fixed-order reduction of the per-tile partials
-        double acc = 0.0;
-        for (int i = threadIdx.x; i < T; i += blockDim.x) acc += (double)sse_part[blockIdx.x * T + i];
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(kFull, acc, o);
-        if ((threadIdx.x & 31) == 0) lsum[threadIdx.x >> 5] = acc;
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            double tot = 0.0;
-            for (int w = 0; w < kWarps; ++w) tot += lsum[w];
-            loss[blockIdx.x] = (float)(tot * inv_count);
-        }
-    }
+    float lr = 0.f, ibc1 = 0.f, ibc2 = 0.f;
     if (adam.m != nullptr) {
-        if (threadIdx.x == 0) {
-            const int t = (int)*adam.step_dev;
-            sconst[0] = ldexpf(adam.lr0, -((t - 1) / adam.half_every));
-            sconst[1] = (float)(1.0 / (1.0 - pow((double)adam.b1, (double)t)));
-            sconst[2] = (float)(1.0 / (1.0 - pow((double)adam.b2, (double)t)));
+        lr = adam.consts[0];
+        ibc1 = adam.consts[1];
+        ibc2 = adam.consts[2];
+    }
+    if (sse_acc != nullptr && blockIdx.x == 0) {
+        // per-image L2 loss from the tiles' fixed-point sums; re-zero
+        for (int i = threadIdx.x; i < batch; i += blockDim.x) {
+            const unsigned long long a = sse_acc[i];
+            sse_acc[i] = 0ull;
+            if (loss != nullptr) loss[i] = (float)((double)a * (1.0 / kSseScale) * inv_count);
         }
-        __syncthreads();
     }
     uint32_t touched = 0;
     int4 rect = make_int4(0, -1, 0, -1);
@@ -493,8 +488,7 @@ __global__ void __launch_bounds__(256) finalize_kernel(
         grads[2 * (size_t)g] = r0;
         grads[2 * (size_t)g + 1] = r1;
         if (adam.m != nullptr) {
-            const float lr = sconst[0], ibc1 = sconst[1], ibc2 = sconst[2];
-            float4* mm = reinterpret_cast<float4*>(adam.m) + 2 * (size_t)g;
+                float4* mm = reinterpret_cast<float4*>(adam.m) + 2 * (size_t)g;
             float4* vv = reinterpret_cast<float4*>(adam.v) + 2 * (size_t)g;
             float4* pp = reinterpret_cast<float4*>(adam.params) + 2 * (size_t)g;
             float4 q0, q1;
@@ -526,19 +520,13 @@ __global__ void __launch_bounds__(256) finalize_kernel(
     }
 }
 
-__global__ void __launch_bounds__(256) loss_kernel(const float* __restrict__ sse_part, int T,
-                                                   double inv_count, float* __restrict__ loss) {
-    __shared__ double sm[256];
-    const int img = blockIdx.x;
-    double acc = 0.0;
-    for (int i = threadIdx.x; i < T; i += blockDim.x) acc += (double)sse_part[img * T + i];
-    sm[threadIdx.x] = acc;
-    __syncthreads();
-    for (int o = 128; o > 0; o >>= 1) {
-        if (threadIdx.x < o) sm[threadIdx.x] += sm[threadIdx.x + o];
-        __syncthreads();
+__global__ void loss_kernel(unsigned long long* __restrict__ sse_acc, int batch, double inv_count,
+                            float* __restrict__ loss) {
+    for (int i = threadIdx.x; i < batch; i += blockDim.x) {
+        const unsigned long long a = sse_acc[i];
+        sse_acc[i] = 0ull;
+        if (loss != nullptr) loss[i] = (float)((double)a * (1.0 / kSseScale) * inv_count);
     }
-    if (threadIdx.x == 0) loss[img] = (float)(sm[0] * inv_count);
 }
 
 struct BwdWs {
@@ -546,7 +534,8 @@ struct BwdWs {
     uint32_t* gauss_off;
     float* ovf;
     uint32_t* counter;
-    float* sse;
+    unsigned long long* sse_acc;
+    float* adam_consts;
     size_t bytes;
 };
 
@@ -560,7 +549,8 @@ BwdWs carve(void* base, int n, int64_t cap, const gi_frame& f) {
     w.gauss_off = reinterpret_cast<uint32_t*>(p + off); off += align_up(sizeof(uint32_t) * (total + 1));
     w.ovf = reinterpret_cast<float*>(p + off); off += align_up(sizeof(float) * 8 * total);
     w.counter = reinterpret_cast<uint32_t*>(p + off); off += align_up(sizeof(uint32_t));
-    w.sse = reinterpret_cast<float*>(p + off); off += align_up(sizeof(float) * (size_t)T * f.batch);
+    w.sse_acc = reinterpret_cast<unsigned long long*>(p + off); off += align_up(8 * (size_t)f.batch);
+    w.adam_consts = reinterpret_cast<float*>(p + off); off += align_up(4 * sizeof(float));
     w.bytes = off;
     return w;
 }
@@ -578,6 +568,9 @@ size_t backward_ws_bytes(int n, int64_t cap, const gi_frame& f) { return carve(n
 
 uint32_t* backward_alloc_counter(void* ws, int n, int64_t cap, const gi_frame& f) {
     return carve(ws, n, cap, f).counter;
+}
+float* backward_adam_consts(void* ws, int n, int64_t cap, const gi_frame& f) {
+    return carve(ws, n, cap, f).adam_consts;
 }
 uint32_t* backward_gauss_off(void* ws, int n, int64_t cap, const gi_frame& f) {
     return carve(ws, n, cap, f).gauss_off;
@@ -609,7 +602,7 @@ cudaError_t launch_backward_tiles(const Proj* proj, uint32_t* key_gid, const uin
                                key_gid,
                                tile_range, (const uint32_t*)w.gauss_off, n, f.width, f.height, T,
                                TX, presorted, dL_dimage, target, norm, partial_cap(n, cap, f), w.partial, w.ovf,
-                               mse ? w.sse : nullptr, mse ? image_out : nullptr, cs);
+                               mse ? w.sse_acc : nullptr, mse ? image_out : nullptr, cs);
     note_launches(1);
     return e;
 }
@@ -619,24 +612,21 @@ cudaError_t launch_backward_finalize(const float* params, const Proj* proj, int 
                                      void* ws, float* grads, float* loss, const FusedAdam* adam,
                                      cudaStream_t s) {
     BwdWs w = carve(ws, n, cap, f);
-    const int T = tiles_x(f.width) * tiles_y(f.height);
     const double count = 3.0 * (double)f.width * (double)f.height;
     const int total = n * f.batch;
     cudaError_t e = cudaSuccess;
-    const bool fold = mse && loss != nullptr && total > 0 && (total + 255) / 256 >= f.batch;
     if (total > 0) {
         FusedAdam fa{};
         if (adam) fa = *adam;
         e = launch_pdl(finalize_kernel, dim3((total + 255) / 256), dim3(256), s,
                        reinterpret_cast<const float4*>(params), proj, (const uint32_t*)w.gauss_off,
-                       total, n, f.width, f.height, flags, partial_cap(n, cap, f), (const float*)w.partial, w.ovf,
-                       reinterpret_cast<float4*>(grads), fa, (const float*)w.sse, T, f.batch,
-                       1.0 / count, fold ? loss : nullptr);
+                       total, n, f.width, f.height, flags, partial_cap(n, cap, f),
+                       (const float*)w.partial, w.ovf, reinterpret_cast<float4*>(grads), fa,
+                       mse ? w.sse_acc : nullptr, f.batch, 1.0 / count, mse ? loss : nullptr);
         note_launches(1);
         if ((e = cudaGetLastError()) != cudaSuccess) return e;
-    }
-    if (mse && loss != nullptr && !fold) {
-        loss_kernel<<<f.batch, 256, 0, s>>>(w.sse, T, 1.0 / count, loss);
+    } else if (mse) {
+        loss_kernel<<<1, 256, 0, s>>>(w.sse_acc, f.batch, 1.0 / count, loss);
         note_launches(1);
         e = cudaGetLastError();
     }

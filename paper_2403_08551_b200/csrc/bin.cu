@@ -329,8 +329,18 @@ BinCounts bin_counts_direct(void* ws, int n, int64_t cap, const gi_frame& f, uin
 ChainState bin_chain_direct(void* ws, int n, int64_t cap, const gi_frame& f, uint32_t* slab,
                             uint32_t* gauss_off, uint32_t* n_keys, uint32_t* step_counter) {
     BinWs w = carve(ws, n, cap, f);
-    return ChainState{w.tile_count, w.big_count, w.fill, w.alloc_counter, gauss_off, slab,
-                      slab_capacity(cap, f), n_keys, w.n_keys_acc, step_counter};
+    ChainState cs{};
+    cs.tile_count = w.tile_count;
+    cs.big_count = w.big_count;
+    cs.fill = w.fill;
+    cs.alloc_counter = w.alloc_counter;
+    cs.gauss_off = gauss_off;
+    cs.slab = slab;
+    cs.slab_cap = slab_capacity(cap, f);
+    cs.n_keys = n_keys;
+    cs.n_keys_acc = w.n_keys_acc;
+    cs.step_counter = step_counter;
+    return cs;
 }
 
 uint32_t* bin_alloc_counter(void* ws, int n, int64_t cap, const gi_frame& f) {

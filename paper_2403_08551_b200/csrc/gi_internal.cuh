@@ -260,6 +260,13 @@ struct ChainState {
     uint32_t* n_keys;
     uint32_t* n_keys_acc;
     uint32_t* step_counter;   // chained fit: incremented once by the consumer
+    // fused Adam: the consumer's CTA 0 turns the step t (after the increment)
+    // into {lr_t, 1 / (1 - b1^t), 1 / (1 - b2^t)} for the finalize kernel
+    float* adam_consts;
+    const uint32_t* step_read;
+    float lr0;
+    int half_every;
+    float b1, b2;
 };
 cudaError_t launch_project(const float* params, int n, const gi_frame& f, uint32_t flags,
                            Proj* proj, uint32_t* tiles_touched, const ProjectFuse& fuse,
@@ -289,6 +296,7 @@ cudaError_t launch_backward(const float* params, const Proj* proj, const uint32_
                             float* grads, float* loss, float* image_out, cudaStream_t s);
 cudaError_t launch_backward_alloc(const Proj* proj, int n, const gi_frame& f, int64_t cap, void* ws,
                                   cudaStream_t s);
+float* backward_adam_consts(void* ws, int n, int64_t cap, const gi_frame& f);
 uint32_t* backward_gauss_off(void* ws, int n, int64_t cap, const gi_frame& f);
 cudaError_t launch_backward_tiles(const Proj* proj, uint32_t* key_gid, const uint32_t* tile_range,
                                   int n, const gi_frame& f, bool presorted,
@@ -301,9 +309,7 @@ struct FusedAdam {
     float* params;
     float* m;
     float* v;
-    const uint32_t* step_dev;
-    float lr0;
-    int half_every;
+    const float* consts;      // {lr_t, 1 / (1 - b1^t), 1 / (1 - b2^t)} (ChainState.adam_consts)
     float b1, b2, eps;
     uint32_t* flag;
     // chained fit step: project the updated Gaussian for the NEXT step (record,

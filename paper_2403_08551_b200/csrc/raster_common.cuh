@@ -323,6 +323,12 @@ __device__ __forceinline__ void close_segment(const ChainState& cs, int tt) {
         }
         if (cs.alloc_counter != nullptr) *cs.alloc_counter = 0u;
         if (cs.step_counter != nullptr) *cs.step_counter += 1u;
+        if (cs.adam_consts != nullptr) {
+            const int st = (int)*cs.step_read;
+            cs.adam_consts[0] = ldexpf(cs.lr0, -((st - 1) / cs.half_every));
+            cs.adam_consts[1] = (float)(1.0 / (1.0 - pow((double)cs.b1, (double)st)));
+            cs.adam_consts[2] = (float)(1.0 / (1.0 - pow((double)cs.b2, (double)st)));
+        }
     }
 }
 
