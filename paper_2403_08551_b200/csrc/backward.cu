@@ -58,7 +58,10 @@ __device__ __forceinline__ uint32_t small_div(uint32_t a, float rb) {
     return (uint32_t)(((float)a + 0.5f) * rb);
 }
 
-__global__ void __launch_bounds__(256, 5) backward_tile_kernel(
+#ifndef GI_TILE_MINB
+#define GI_TILE_MINB 6
+#endif
+__global__ void __launch_bounds__(256, GI_TILE_MINB) backward_tile_kernel(
     const Proj* __restrict__ proj, uint32_t* __restrict__ key_gid,
     const uint32_t* __restrict__ tile_range, const uint32_t* __restrict__ gauss_off, int n,
     int W, int H, int T, int TX, bool presorted, const float* __restrict__ dL_dimage,
@@ -87,7 +90,7 @@ __global__ void __launch_bounds__(256, 5) backward_tile_kernel(
     } else {
         // ---- pass 1: forward (Eq. 7), pixel-parallel ----
         float acc0 = 0.f, acc1 = 0.f, acc2 = 0.f;
-        for (uint32_t base = 0; base < L; base += 256) {
+        for (uint32_t base = 0; base < L; base += kBatch) {
             if (base > 0) __syncthreads();
             uint32_t gid;
             const int cnt =
@@ -97,7 +100,7 @@ __global__ void __launch_bounds__(256, 5) backward_tile_kernel(
             const int nl = build_warp_list(sh.sr, sh.u.wl, cnt, t);
             forward_batch(sh.sr, sh.u.wl, nl, t, acc0, acc1, acc2);
         }
-        staged_all = L <= 256u;
+        staged_all = L <= (uint32_t)kBatch;
         float sq = 0.f;
         if (t.in_image) {
             const float r0 = acc0 - target[pix];
@@ -140,10 +143,10 @@ __global__ void __launch_bounds__(256, 5) backward_tile_kernel(
     // sums of its chunk; thread j then adds its chunks in a fixed order.
     const int j = threadIdx.x;
     if (threadIdx.x == 0) sh.cursor = 0u;        // kSegStream: pass 2 streams from the start
-    for (uint32_t base = 0; base < L; base += 256) {
+    for (uint32_t base = 0; base < L; base += kBatch) {
         __syncthreads();
         uint32_t gid = 0;
-        int cnt = (int)min(256u, L - base);
+        int cnt = (int)min((uint32_t)kBatch, L - base);
         if (!staged_all)
             cnt = batch_gid(sg, base, key_gid, sh.sl, proj, n, t, &sh.cursor, sh.scratch, gid);
         if (j < 64) sh.hist[j] = 0u;

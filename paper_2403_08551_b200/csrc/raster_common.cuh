@@ -28,6 +28,10 @@ namespace gi {
 
 constexpr int kSortMax = 2048;      // segments sorted in shared memory (8 KB)
 constexpr int kRankMax = 256;       // rank sort up to this size, bitonic above
+#ifndef GI_BATCH
+#define GI_BATCH 128
+#endif
+constexpr int kBatch = GI_BATCH;    // records staged per batch (<= 256)
 
 struct TileCtx {
     int img, tile, tx, ty;        // tile coordinates
@@ -69,14 +73,14 @@ __device__ __forceinline__ TileCtx make_tile_ctx(int W, int H, int TX) {
 //        column mask | row mask << 16,            the same as 16-bit masks,
 //        partial slot (backward only), gid}
 struct StagedRecords {
-    float4 a[256];
-    float4 b[256];
-    uint4 c[256];
+    float4 a[kBatch];
+    float4 b[kBatch];
+    uint4 c[kBatch];
 };
 
 // Per-warp compacted candidate list for one batch: (record index, lane mask).
 struct WarpLists {
-    uint2 ent[kWarps][256];
+    uint2 ent[kWarps][kBatch];
     int cnt[kWarps];
 };
 
@@ -378,7 +382,7 @@ __device__ __forceinline__ int batch_gid(const Seg& sg, uint32_t base, const uin
                                          uint32_t* sl, const Proj* __restrict__ proj, int n,
                                          const TileCtx& t, uint32_t* cursor, uint32_t* scratch8,
                                          uint32_t& gid) {
-    int cnt = (int)min(256u, sg.L - base);
+    int cnt = (int)min((uint32_t)kBatch, sg.L - base);
     if (sg.mode == kSegStream) {
         cnt = stream_keys(proj, n, t.img, t.tx, t.ty, cnt, cursor, sl, scratch8);
         gid = (int)threadIdx.x < cnt ? sl[threadIdx.x] : 0u;

@@ -18,7 +18,10 @@ struct RenderShared {
     uint32_t cursor;
 };
 
-__global__ void __launch_bounds__(256) render_kernel(const Proj* __restrict__ proj,
+#ifndef GI_RENDER_MINB
+#define GI_RENDER_MINB 8
+#endif
+__global__ void __launch_bounds__(256, GI_RENDER_MINB) render_kernel(const Proj* __restrict__ proj,
                                                      uint32_t* __restrict__ key_gid,
                                                      const uint32_t* __restrict__ tile_range,
                                                      int n, int W, int H, int T, int TX,
@@ -33,7 +36,7 @@ __global__ void __launch_bounds__(256) render_kernel(const Proj* __restrict__ pr
     const Seg sg = open_segment(proj, key_gid, tile_range, presorted, cs, n, T, t, sh.sl,
                                 sh.scratch, &sh.cursor);
     float acc0 = 0.f, acc1 = 0.f, acc2 = 0.f;
-    for (uint32_t base = 0; base < sg.L; base += 256) {
+    for (uint32_t base = 0; base < sg.L; base += kBatch) {
         if (base > 0) __syncthreads();
         uint32_t gid;
         const int cnt = batch_gid(sg, base, key_gid, sh.sl, proj, n, t, &sh.cursor, sh.scratch, gid);
