@@ -366,6 +366,7 @@ __global__ void __launch_bounds__(256) finalize_kernel(
     // independent loads first (their latency overlaps the partial-sum chain)
     float4 p0 = make_float4(0.f, 0.f, 0.f, 0.f), p1 = p0, m0 = p0, m1 = p0, v0 = p0, v1 = p0;
     Proj r{};
+    const float4* pp = reinterpret_cast<const float4*>(partial);
     if (g < total) {
         p0 = params[2 * (size_t)g];
         p1 = params[2 * (size_t)g + 1];
@@ -400,7 +401,6 @@ __global__ void __launch_bounds__(256) finalize_kernel(
         bool any = false;
         if (x0 <= x1 && y0 <= y1) {
             const uint32_t cnt = (uint32_t)((x1 / kTile - x0 / kTile + 1) * (y1 / kTile - y0 / kTile + 1));
-            const float4* pp = reinterpret_cast<const float4*>(partial);
             auto add = [&](const float4 a, const float4 b) {
                 S[0] += a.x; S[1] += a.y; S[2] += a.z; S[3] += a.w;
                 S[4] += b.x; S[5] += b.y; S[6] += b.z; S[7] += b.w;
