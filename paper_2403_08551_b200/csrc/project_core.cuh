@@ -7,17 +7,19 @@
 
 namespace gi {
 
-__device__ __forceinline__ uint32_t project_one(const float4 p0 /* mux, muy, l1, l2 */,
-                                                const float4 p1 /* l3, c'r, c'g, c'b */, int g,
-                                                int n, int W, int H, float k, uint32_t flags,
-                                                Proj* __restrict__ proj, const BinCounts& bc,
+// App. C: u = tanh(mu_raw) (fp64), or the stored u (normalised positions).
+__device__ __forceinline__ double activate_pos(float raw, uint32_t flags) {
+    return pos_logit(flags) ? tanh((double)raw) : (double)raw;
+}
+
+// The 48-byte record, pixel box and tile rectangle of one Gaussian from its
+// activated position (ux, uy) and parameters; returns the tiles touched.
+__device__ __forceinline__ uint32_t project_rec(double ux, double uy,
+                                                const float4 p0 /* mux, muy, l1, l2 */,
+                                                const float4 p1 /* l3, c'r, c'g, c'b */, int W,
+                                                int H, float k, uint32_t flags, Proj& r,
                                                 int4& rect /* out: tile rect when touched > 0 */) {
-    // App. C: u = tanh(mu_raw); R2: mu = (u + 1) * W / 2  (fp64, no contraction)
-    double ux = (double)p0.x, uy = (double)p0.y;
-    if (pos_logit(flags)) {
-        ux = tanh(ux);
-        uy = tanh(uy);
-    }
+    // R2: mu = (u + 1) * W / 2  (fp64, no contraction)
     const double mx = __dmul_rn(__dadd_rn(ux, 1.0), (double)W * 0.5);
     const double my = __dmul_rn(__dadd_rn(uy, 1.0), (double)H * 0.5);
 
@@ -29,7 +31,6 @@ __device__ __forceinline__ uint32_t project_one(const float4 p0 /* mux, muy, l1,
     const float e3 = __fadd_rn(p1.x, 0.5f);               // l3 + 1/2  |  s2 + 1/2
     double Srs[3] = {0.0, 0.0, 0.0};
     if (rs) rs_sigma((double)e2, (double)e1, (double)e3, Srs);
-    Proj r;
     uint32_t bx = kEmptyBox, by = kEmptyBox, touched = 0;
     int ix = 0, iy = 0;
     float fx = 0.f, fy = 0.f;
@@ -64,11 +65,6 @@ __device__ __forceinline__ uint32_t project_one(const float4 p0 /* mux, muy, l1,
             by = (uint32_t)y0 | ((uint32_t)y1 << 16);
             touched = (uint32_t)((x1 / kTile - x0 / kTile + 1) * (y1 / kTile - y0 / kTile + 1));
             rect = make_int4(x0 / kTile, x1 / kTile, y0 / kTile, y1 / kTile);
-            if (bc.tile_count != nullptr) {   // fused binning step 1: counts and ranks
-                const int TX = (W + kTile - 1) / kTile;
-                const int T = TX * ((H + kTile - 1) / kTile);
-                count_keys(bc, g, rect.x, rect.y, rect.z, rect.w, touched, (g / n) * T, TX);
-            }
         }
     }
     // Sigma^-1 = L^-T L^-1 with L^-1 = [[1/l1, 0], [-l2/(l1 l3), 1/l3]], scaled by
@@ -92,6 +88,22 @@ __device__ __forceinline__ uint32_t project_one(const float4 p0 /* mux, muy, l1,
     r.q0 = make_float4(__int_as_float(ix), __int_as_float(iy), fx, fy);
     r.q1 = make_float4(ca, cb, cc, __uint_as_float(bx));
     r.q2 = make_float4(p1.y, p1.z, p1.w, __uint_as_float(by));
+    return touched;
+}
+
+// a1 (+ binning step 1) of Gaussian g by one thread.
+__device__ __forceinline__ uint32_t project_one(const float4 p0, const float4 p1, int g, int n, int W,
+                                                int H, float k, uint32_t flags,
+                                                Proj* __restrict__ proj, const BinCounts& bc,
+                                                int4& rect) {
+    Proj r;
+    const uint32_t touched = project_rec(activate_pos(p0.x, flags), activate_pos(p0.y, flags), p0,
+                                         p1, W, H, k, flags, r, rect);
+    if (touched > 0u && bc.tile_count != nullptr) {   // fused binning step 1: counts and ranks
+        const int TX = (W + kTile - 1) / kTile;
+        const int T = TX * ((H + kTile - 1) / kTile);
+        count_keys(bc, g, rect.x, rect.y, rect.z, rect.w, touched, (g / n) * T, TX);
+    }
     proj[g] = r;
     return touched;
 }
