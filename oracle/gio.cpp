@@ -18,6 +18,8 @@
 //                    "1e-3, halved every 20000 steps"
 //   * decode      -- fp16 positions, Eq. 8 dequant, Eq. 9
 //                    RVQ sum, record layout SPEC.md:404
+//   * encode      -- (NEXT-2) the quantisers those invert: fp16 rounding of
+//                    the post-tanh position, Eq. 8 codes, Eq. 9 greedy RVQ
 //   * binning     -- (tile, gaussian) pairs grouped by tile, no depth key
 //                    (north_star), by two independent methods
 // Floating point is fp64 except the box recipe (reading R7), which is stated
@@ -607,6 +609,92 @@ double gio_psnr(const double* x, const float* y, int64_t count) {
     double mse = s / (double)count;
     if (mse <= 1e-10) return 100.0;
     return std::min(100.0, 10.0 * std::log10(1.0 / mse));
+}
+
+
+// ------------------------------------------------------------ encoder (NEXT-2)
+// IEEE 754 binary16 from binary32, round to nearest, ties to even (SPEC
+// "fp16 = IEEE 754 binary16, round-to-nearest-even from float32"), written
+// from the format definition: 1 sign, 5 exponent (bias 15), 10 fraction bits.
+uint32_t gio_float_to_half(float x) {
+    uint32_t b;
+    std::memcpy(&b, &x, 4);
+    const uint32_t sign = (b >> 16) & 0x8000u;
+    const uint32_t e = (b >> 23) & 0xffu, m = b & 0x7fffffu;
+    if (e == 0xffu) return sign | 0x7c00u | (m ? 0x200u : 0u);         // inf, nan
+    const int E = (int)e - 127;
+    if (E > 15) return sign | 0x7c00u;                                  // overflow
+    if (E >= -14) {                                                     // normal half
+        uint32_t h = ((uint32_t)(E + 15) << 10) | (m >> 13);
+        const uint32_t rest = m & 0x1fffu;
+        if (rest > 0x1000u || (rest == 0x1000u && (h & 1u))) h += 1u;   // may carry to inf
+        return sign | h;
+    }
+    if (E < -25 || e == 0u) return sign;                                // below 2^-25: zero
+    // subnormal half: value / 2^-24 = (m | 2^23) * 2^(E + 1)
+    const uint32_t mf = m | 0x800000u;
+    const int sh = -(E + 1);                                            // 14 .. 24
+    uint32_t q = mf >> sh;
+    const uint32_t rem = mf & ((1u << sh) - 1u), half = 1u << (sh - 1);
+    if (rem > half || (rem == half && (q & 1u))) q += 1u;
+    return sign | q;
+}
+
+// Attribute quantisation of one cloud (SPEC quant module):
+//   position: u = tanh(mu_raw) (fp64, App. C) rounded to fp32 then to fp16
+//             ("16-bit float precision for position parameters")
+//   l_i:      code = round_half_even(clamp((l_i - beta_i) / gamma_i, 0,
+//             2^b - 1)) in fp32 (Eq. 8; the paper fixes no precision, so the
+//             decision is taken in the kernel's, reading R30)
+//   c':       greedy RVQ (Eq. 9): i^m = argmin_k ||C^m[k] - (c' - c^^{m-1})||^2
+//             with c^^{m-1} = sum_{k<m} C^k[i^k] in fp32 stage order and the
+//             distance in fp32 ((d0^2 + d1^2) + d2^2); ties -> lowest index
+// Outputs the codes and the dequantised ("effective") parameters exactly as
+// gio_vq_decode produces them from the packed record.
+void gio_vq_encode(const float* params, int n, int pos_mode, const float* gamma,
+                   const float* beta, const float* books, int bits, int stages, int codebook,
+                   uint32_t* pos16, uint32_t* codes, uint32_t* idx, float* eff) {
+    const float qmax = (float)((1u << bits) - 1u);
+    for (int i = 0; i < n; ++i) {
+        const float* p = params + 8 * (size_t)i;
+        float* out = eff + 8 * (size_t)i;
+        for (int a = 0; a < 2; ++a) {
+            double u = (pos_mode & kPosNormalized) ? (double)p[a] : std::tanh((double)p[a]);
+            uint32_t h = gio_float_to_half((float)u);
+            pos16[2 * (size_t)i + a] = h;
+            out[a] = (float)gio_half_to_double(h);
+        }
+        for (int j = 0; j < 3; ++j) {
+            float d = p[2 + j] - beta[j];
+            float x = d / gamma[j];
+            x = std::fmin(std::fmax(x, 0.0f), qmax);
+            uint32_t code = (uint32_t)std::nearbyint(x);
+            codes[3 * (size_t)i + j] = code;
+            out[2 + j] = std::fmaf((float)code, gamma[j], beta[j]);
+        }
+        float chat[3] = {0.0f, 0.0f, 0.0f};
+        for (int m = 0; m < stages; ++m) {
+            float r[3];
+            for (int j = 0; j < 3; ++j) r[j] = p[5 + j] - chat[j];
+            int best = 0;
+            float bestd = INFINITY;
+            for (int k = 0; k < codebook; ++k) {
+                const float* cw = books + ((size_t)m * codebook + k) * 3;
+                float d0 = cw[0] - r[0], d1 = cw[1] - r[1], d2 = cw[2] - r[2];
+                float dd = d0 * d0;
+                dd = dd + d1 * d1;
+                dd = dd + d2 * d2;
+                if (dd < bestd) {
+                    bestd = dd;
+                    best = k;
+                }
+            }
+            idx[(size_t)i * stages + m] = (uint32_t)best;
+            const float* cw = books + ((size_t)m * codebook + best) * 3;
+            for (int j = 0; j < 3; ++j) chat[j] = (m == 0) ? cw[j] : chat[j] + cw[j];
+        }
+        out[5] = chat[0]; out[6] = chat[1]; out[7] = chat[2];
+    }
 }
 
 }  // extern "C"

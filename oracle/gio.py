@@ -39,6 +39,10 @@ def lib():
         L = C.CDLL(build())
         dp, fp, ip, up = (C.POINTER(C.c_double), C.POINTER(C.c_float),
                           C.POINTER(C.c_int32), C.POINTER(C.c_uint32))
+        L.gio_float_to_half.restype = C.c_uint32
+        L.gio_float_to_half.argtypes = [C.c_float]
+        L.gio_vq_encode.argtypes = [fp, C.c_int, C.c_int, fp, fp, fp, C.c_int, C.c_int, C.c_int,
+                                    up, up, up, fp]
         L.gio_eval_sigma.restype = C.c_double
         L.gio_eval_sigma.argtypes = [dp, C.c_double, C.c_double]
         L.gio_inverse2.argtypes = [dp, dp]
@@ -233,3 +237,25 @@ def psnr(x, y) -> float:
     a = np.ascontiguousarray(x, dtype=np.float64)
     b = _f32(y)
     return lib().gio_psnr(_p(a, C.c_double), _p(b, C.c_float), a.size)
+
+
+def float_to_half(x) -> int:
+    return int(lib().gio_float_to_half(float(np.float32(x))))
+
+
+def vq_encode(params, gamma, beta, books, bits=6, stages=2, codebook=8, pos_mode=POS_LOGIT):
+    """Attribute quantisation (NEXT-2): -> dict(pos16 [n][2], codes [n][3],
+    idx [n][M] (uint32), eff [n][8] fp32 = what vq_decode returns)."""
+    p = _f32(params).reshape(-1, 8)
+    n = p.shape[0]
+    g, b, cb = _f32(gamma), _f32(beta), _f32(books)
+    pos16 = np.zeros((n, 2), np.uint32)
+    codes = np.zeros((n, 3), np.uint32)
+    idx = np.zeros((n, int(stages)), np.uint32)
+    eff = np.zeros((n, 8), np.float32)
+    up = C.POINTER(C.c_uint32)
+    lib().gio_vq_encode(_p(p, C.c_float), n, int(pos_mode), _p(g, C.c_float), _p(b, C.c_float),
+                        _p(cb, C.c_float), int(bits), int(stages), int(codebook), _p(pos16, C.c_uint32),
+                        _p(codes, C.c_uint32), _p(idx, C.c_uint32), _p(eff, C.c_float))
+    return dict(pos16=pos16, codes=codes, idx=idx, eff=eff)
+
