@@ -245,6 +245,22 @@ typedef struct {
 gi_status gi_vq_decode(const uint8_t* payload, size_t payload_bytes, const gi_codec_meta* meta,
                        float* params, void* stream);
 
+/* --- NEXT-2 encoder: attribute quantisation (SPEC quant/codec) ---
+ * The inverse of gi_vq_decode: per Gaussian of params [n][8] fp32 (raw
+ * positions through tanh unless flags & GI_POS_NORMALIZED; Cholesky l as
+ * stored; colours c'):
+ *   u     = binary16(round_fp32(tanh(mu_raw))), round to nearest even
+ *   code  = rint(clamp((l_i - beta_i) / gamma_i, 0, 2^bits - 1)) in fp32 Eq. 8
+ *   i^m   = argmin_k ||C^m[k] - (c' - c^^{m-1})||^2, fp32, ties -> lowest
+ *           index, c^^{m-1} = C^1[i^1] + ... in stage order              Eq. 9
+ * (reading R30: the paper fixes no precision or tie rule).  Outputs (either
+ * may be NULL): payload -- the records packed exactly as gi_vq_decode reads
+ * them (the call zero-fills the first ceil(n*R/8) bytes; payload_bytes must
+ * cover them); eff [n][8] fp32 -- the dequantised parameters, bit-identical
+ * to gi_vq_decode(payload).  Same GI_EFORMAT rules as gi_vq_decode. */
+gi_status gi_vq_encode(const float* params, uint32_t flags, const gi_codec_meta* meta,
+                       uint8_t* payload, size_t payload_bytes, float* eff, void* stream);
+
 /* --- harness helpers (not on the hot path) ---------------------------------
  * PSNR of each image on [0,1]-clamped values, capped at 100 dB:
  * psnr[B] fp32 out; ws of gi_psnr_workspace_bytes() bytes (device). */

@@ -454,6 +454,36 @@ gi_status gi_vq_decode(const uint8_t* payload, size_t payload_bytes, const gi_co
     return cuda_status(gi::launch_vq_decode(payload, *meta, params, S(stream)), "gi_vq_decode");
 }
 
+gi_status gi_vq_encode(const float* params, uint32_t flags, const gi_codec_meta* meta,
+                       uint8_t* payload, size_t payload_bytes, float* eff, void* stream) {
+    if (!meta) return invalid("meta is NULL");
+    if (meta->n < 0) return invalid("n");
+    if (!gi::flags_valid(flags) || (flags & GI_COV_RS)) return invalid("flags");
+    if (meta->bits < 1 || meta->bits > 16 || meta->stages < 1 || meta->stages > 8 ||
+        meta->codebook < 2 || meta->codebook > 256) {
+        std::snprintf(g_err, sizeof(g_err), "codec metadata out of range");
+        return GI_EFORMAT;
+    }
+    int ib = 1;
+    while ((1 << ib) < meta->codebook) ++ib;
+    const int64_t rec = 32 + 3LL * meta->bits + (int64_t)meta->stages * ib;
+    if (rec > 64) {
+        std::snprintf(g_err, sizeof(g_err), "record wider than 64 bits");
+        return GI_EFORMAT;
+    }
+    size_t need = (size_t)((rec * meta->n + 7) / 8);
+    if (rec % 8 != 0) need = (need + 3) & ~(size_t)3;   // whole words (see launch_vq_encode)
+    if (payload && need > payload_bytes) {
+        std::snprintf(g_err, sizeof(g_err), "payload buffer shorter than the packed records");
+        return GI_EFORMAT;
+    }
+    if (meta->n > 0 && (!params || !meta->codebooks)) return invalid("NULL buffer");
+    if (!aligned16(params) || !aligned16(eff)) return invalid("alignment");
+    return cuda_status(gi::launch_vq_encode(params, !(flags & GI_POS_NORMALIZED), *meta, payload,
+                                            eff, S(stream)),
+                       "gi_vq_encode");
+}
+
 gi_status gi_psnr(const float* image, const float* target, const gi_frame* f, float* psnr, void* ws,
                   void* stream) {
     gi_status st;

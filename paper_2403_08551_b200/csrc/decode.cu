@@ -63,6 +63,98 @@ __global__ void __launch_bounds__(256) vq_decode_kernel(const uint8_t* __restric
     params[2 * (size_t)r + 1] = make_float4(l3, c0, c1, c2);
 }
 
+// NEXT-2 encoder (the inverse of vq_decode_kernel; see gi.h): one thread per
+// Gaussian.  Every arithmetic step that decides a code is an explicitly
+// rounded fp32 intrinsic (no FMA contraction), so the codes are the same
+// function of the inputs as the oracle's.  Records are written MSB-first:
+// with whole-byte records (the paper's 56-bit default) by plain byte stores,
+// otherwise by atomicOr into the 32-bit words they straddle (the payload is
+// zero-filled first; OR is order-independent, so the result is
+// deterministic).
+__global__ void __launch_bounds__(256) vq_encode_kernel(
+    const float4* __restrict__ params, int n, bool logit, int bits, int stages, int codebook, int ib,
+    int rec_bits, float g0, float g1, float g2, float b0, float b1, float b2,
+    const float* __restrict__ books, uint8_t* __restrict__ payload, float4* __restrict__ eff) {
+    __shared__ float sb[kMaxBook];
+    const int nb = stages * codebook * 3;
+    for (int i = threadIdx.x; i < nb; i += blockDim.x) sb[i] = books[i];
+    __syncthreads();
+    const int r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= n) return;
+    const float4 p0 = params[2 * (size_t)r], p1 = params[2 * (size_t)r + 1];
+    const double ux = logit ? tanh((double)p0.x) : (double)p0.x;
+    const double uy = logit ? tanh((double)p0.y) : (double)p0.y;
+    const __half hx = __float2half_rn(__double2float_rn(ux));
+    const __half hy = __float2half_rn(__double2float_rn(uy));
+    const float qmax = (float)((1u << bits) - 1u);
+    const float g[3] = {g0, g1, g2}, be[3] = {b0, b1, b2}, l[3] = {p0.z, p0.w, p1.x};
+    uint32_t code[3];
+    float lq[3];
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+        float x = __fdiv_rn(__fsub_rn(l[j], be[j]), g[j]);
+        x = fminf(fmaxf(x, 0.0f), qmax);
+        code[j] = __float2uint_rn(x);
+        lq[j] = __fmaf_rn((float)code[j], g[j], be[j]);
+    }
+    uint64_t v = ((uint64_t)__half_as_ushort(hx) << 16) | (uint64_t)__half_as_ushort(hy);
+#pragma unroll
+    for (int j = 0; j < 3; ++j) v = (v << bits) | code[j];
+    const float c[3] = {p1.y, p1.z, p1.w};
+    float ch0 = 0.f, ch1 = 0.f, ch2 = 0.f;
+    for (int m = 0; m < stages; ++m) {
+        const float r0 = __fsub_rn(c[0], ch0), r1 = __fsub_rn(c[1], ch1), r2 = __fsub_rn(c[2], ch2);
+        int best = 0;
+        float bestd = __int_as_float(0x7f800000);
+        for (int k = 0; k < codebook; ++k) {
+            const float* cw = sb + (m * codebook + k) * 3;
+            const float d0 = __fsub_rn(cw[0], r0), d1 = __fsub_rn(cw[1], r1), d2 = __fsub_rn(cw[2], r2);
+            float dd = __fmul_rn(d0, d0);
+            dd = __fadd_rn(dd, __fmul_rn(d1, d1));
+            dd = __fadd_rn(dd, __fmul_rn(d2, d2));
+            if (dd < bestd) {
+                bestd = dd;
+                best = k;
+            }
+        }
+        const float* cw = sb + (m * codebook + best) * 3;
+        if (m == 0) {
+            ch0 = cw[0]; ch1 = cw[1]; ch2 = cw[2];
+        } else {
+            ch0 = __fadd_rn(ch0, cw[0]); ch1 = __fadd_rn(ch1, cw[1]); ch2 = __fadd_rn(ch2, cw[2]);
+        }
+        v = (v << ib) | (uint64_t)best;
+    }
+    if (eff != nullptr) {
+        eff[2 * (size_t)r] = make_float4(__half2float(hx), __half2float(hy), lq[0], lq[1]);
+        eff[2 * (size_t)r + 1] = make_float4(lq[2], ch0, ch1, ch2);
+    }
+    if (payload == nullptr) return;
+    const int64_t bit0 = (int64_t)r * rec_bits;
+    if ((rec_bits & 7) == 0) {                     // whole bytes: plain stores
+        uint8_t* dst = payload + (bit0 >> 3);
+        for (int i = 0; i < rec_bits / 8; ++i) dst[i] = (uint8_t)(v >> (rec_bits - 8 * (i + 1)));
+        return;
+    }
+    // straddling records: the record's bits, MSB-first from bit0, OR-ed into
+    // the little-endian 32-bit words that hold those bytes
+    const int sh = (int)(bit0 & 7);
+    const int nbytes = (sh + rec_bits + 7) >> 3;   // <= 9
+    const uint64_t top = v << (64 - rec_bits);     // record at the MSB of a 64-bit window
+    uint32_t* words = reinterpret_cast<uint32_t*>(payload);
+    for (int i = 0; i < nbytes; ++i) {
+        // bits [8 i - sh, 8 i - sh + 8) of the record go to byte byte0 + i
+        const int lo = 8 * i - sh;
+        uint32_t byte;
+        if (lo < 0) byte = (uint32_t)(top >> (64 - 8 + sh)) & (0xffu >> sh);
+        else if (lo < 64) byte = (uint32_t)((top << lo) >> 56);
+        else byte = 0u;
+        if (byte == 0u) continue;
+        const int64_t j = (bit0 >> 3) + i;
+        atomicOr(&words[j >> 2], byte << (8 * (j & 3)));
+    }
+}
+
 }  // namespace
 
 cudaError_t launch_vq_decode(const uint8_t* payload, const gi_codec_meta& meta, float* params,
@@ -75,6 +167,27 @@ cudaError_t launch_vq_decode(const uint8_t* payload, const gi_codec_meta& meta, 
         payload, meta.n, meta.bits, meta.stages, meta.codebook, ib, rec, meta.gamma[0],
         meta.gamma[1], meta.gamma[2], meta.beta[0], meta.beta[1], meta.beta[2], meta.codebooks,
         reinterpret_cast<float4*>(params));
+    note_launches(1);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_vq_encode(const float* params, bool logit, const gi_codec_meta& meta,
+                             uint8_t* payload, float* eff, cudaStream_t s) {
+    if (meta.n == 0) return cudaSuccess;
+    int ib = 1;
+    while ((1 << ib) < meta.codebook) ++ib;
+    const int rec = 32 + 3 * meta.bits + meta.stages * ib;
+    if (payload != nullptr && (rec & 7) != 0) {
+        const size_t bytes = ((size_t)rec * meta.n + 7) / 8;
+        // whole 32-bit words (the atomics OR into words); the caller's buffer
+        // is rounded the same way by gi_vq_encode's size check
+        cudaError_t e = cudaMemsetAsync(payload, 0, (bytes + 3) & ~(size_t)3, s);
+        if (e != cudaSuccess) return e;
+    }
+    vq_encode_kernel<<<(meta.n + 255) / 256, 256, 0, s>>>(
+        reinterpret_cast<const float4*>(params), meta.n, logit, meta.bits, meta.stages,
+        meta.codebook, ib, rec, meta.gamma[0], meta.gamma[1], meta.gamma[2], meta.beta[0],
+        meta.beta[1], meta.beta[2], meta.codebooks, payload, reinterpret_cast<float4*>(eff));
     note_launches(1);
     return cudaGetLastError();
 }

@@ -81,6 +81,7 @@ SIGNATURES = {
                                       _f32, _i32, _f32, _f32, _f32, _vp, _vp, _vp, _vp]),
     "gi_render_frame": (C.c_int, [_vp, _i32, _FP, _u32, _i64, _vp, _sz, _vp, _vp]),
     "gi_vq_decode": (C.c_int, [_vp, _sz, C.POINTER(gi_codec_meta), _vp, _vp]),
+    "gi_vq_encode": (C.c_int, [_vp, C.c_uint32, C.POINTER(gi_codec_meta), _vp, _sz, _vp, _vp]),
     "gi_psnr_workspace_bytes": (_sz, [_FP]),
     "gi_psnr": (C.c_int, [_vp, _vp, _FP, _vp, _vp, _vp]),
     "gi_check": (C.c_int, [_vp, _i64, _vp, _vp]),
@@ -272,6 +273,14 @@ def gi_render_frame(params, n, f, flags, key_capacity, frame_ws, image, stream=N
 
 def gi_launch_count() -> int:
     return load().gi_launch_count()
+
+
+def gi_vq_encode(params, meta: gi_codec_meta, payload=None, eff=None, flags=0, stream=None):
+    """NEXT-2 encoder: quantise params [n][8] into packed records (payload,
+    uint8 device tensor) and/or the dequantised parameters eff [n][8]."""
+    _ok(load().gi_vq_encode(_ptr(params), int(flags), C.byref(meta), _ptr(payload),
+                            0 if payload is None else payload.numel(), _ptr(eff), _stream(stream)),
+        "gi_vq_encode")
 
 
 def gi_vq_decode(payload, meta: gi_codec_meta, params, stream=None):

@@ -302,7 +302,8 @@ def test_decode_then_render(gi, gio):
     ref_p = gio.vq_decode(data, n, gamma, beta, books)
     ref = gio.render(ref_p, W, H, pos_mode=gio.POS_NORMALIZED, mode=gio.TILED)
     params = torch.zeros(1, n, 8, dtype=torch.float32, device=DEV)
-    gi.gi_vq_decode(to_dev(data), gi.codec_meta(n, gamma, beta, to_dev(books)), params)
+    bk = to_dev(books)                      # keep alive: the meta holds the raw pointer
+    gi.gi_vq_decode(to_dev(data), gi.codec_meta(n, gamma, beta, bk), params)
     pipe = Pipeline(n, W, H, 1, device=DEV)
     img = pipe.render(params, gi.GI_POS_NORMALIZED)
     assert np.abs(img[0].cpu().numpy() - ref).max() <= PIX_TOL
@@ -563,3 +564,32 @@ def test_partial_slot_overflow(gi, gio):
         assert fit.check() == gi.GI_OK
         assert abs(float(fit.loss[0]) - loss) <= 1e-5 * loss
         assert max(group_err(fit.grads[0].cpu().numpy().astype(np.float64), g).values()) <= GRAD_TOL
+
+
+@pytest.mark.parametrize("bits,stages,codebook,pos_mode", [(6, 2, 8, 0), (5, 3, 16, 0),
+                                                           (8, 2, 8, 1), (4, 1, 256, 0)])
+def test_vq_encode_bitexact(gi, gio, bits, stages, codebook, pos_mode):
+    # NEXT-2 encoder: codes, packed bytes and dequantised parameters equal the
+    # oracle's bit for bit; GPU decode of the GPU payload returns them too
+    n = 5003
+    rng = np.random.default_rng(bits * 100 + stages)
+    p = synth.fitted_params(bits, n)
+    if pos_mode:
+        p[:, :2] = rng.uniform(-1, 1, (n, 2)).astype(np.float32)
+    gamma = np.float32([0.06, 0.05, 0.06]) * np.float32(64.0 / (1 << bits))
+    beta = np.float32([-1.5, -1.6, -1.5])
+    books = rng.normal(0, 0.3, (stages, codebook, 3)).astype(np.float32)
+    ref = gio.vq_encode(p, gamma, beta, books, bits, stages, codebook, pos_mode)
+    data = synth.pack_records(ref["pos16"].astype(np.uint16), ref["codes"], ref["idx"], bits,
+                              codebook)
+    bk = to_dev(books)                      # keep alive: meta holds the raw pointer
+    meta = gi.codec_meta(n, gamma, beta, bk, bits=bits, stages=stages, codebook=codebook)
+    payload = torch.full((data.size + 8,), 0xAB, dtype=torch.uint8, device=DEV)
+    eff = torch.zeros(n, 8, dtype=torch.float32, device=DEV)
+    gi.gi_vq_encode(to_dev(p), meta, payload, eff, flags=gi.GI_POS_NORMALIZED if pos_mode else 0)
+    torch.cuda.synchronize()
+    assert np.array_equal(eff.cpu().numpy().view(np.uint32), ref["eff"].view(np.uint32))
+    assert np.array_equal(payload[: data.size].cpu().numpy(), data)
+    dec = torch.zeros(n, 8, dtype=torch.float32, device=DEV)
+    gi.gi_vq_decode(payload, meta, dec)
+    assert torch.equal(dec, eff)
