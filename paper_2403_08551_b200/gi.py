@@ -305,4 +305,5 @@ def codec_meta(n, gamma, beta, codebooks, bits=6, stages=2, codebook=8) -> gi_co
         m.gamma[i] = float(gamma[i])
         m.beta[i] = float(beta[i])
     m.codebooks = _ptr(codebooks)
+    m._keep = codebooks        # the struct holds a raw pointer: keep the tensor alive
     return m
