@@ -261,6 +261,19 @@ gi_status gi_vq_decode(const uint8_t* payload, size_t payload_bytes, const gi_co
 gi_status gi_vq_encode(const float* params, uint32_t flags, const gi_codec_meta* meta,
                        uint8_t* payload, size_t payload_bytes, float* eff, void* stream);
 
+/* NEXT-2 RVQ codebook initialisation: one K-means (Lloyd) iteration (P:307
+ * "initialized using the K-means algorithm"; 5 iterations).  points
+ * [n][3] fp32 (colours c', or stage-m residuals); centroids [B][3] fp32
+ * in/out (2 <= B <= 256); assign [n] u32 out (may be NULL): the nearest
+ * centroid by the fp32 distance and tie rule of gi_vq_encode.  A centroid
+ * with points becomes their mean (sums in 2^-40 fixed point, order-
+ * independent, divided in fp64, rounded once to fp32); an empty cluster keeps
+ * its centroid (reading R31).  ws: gi_kmeans_workspace_bytes(B) device
+ * bytes, zero-filled before the first call (left zeroed by each call). */
+size_t gi_kmeans_workspace_bytes(int32_t B);
+gi_status gi_kmeans_step(const float* points, int32_t n, int32_t B, float* centroids,
+                         uint32_t* assign, void* ws, size_t ws_bytes, void* stream);
+
 /* --- harness helpers (not on the hot path) ---------------------------------
  * PSNR of each image on [0,1]-clamped values, capped at 100 dB:
  * psnr[B] fp32 out; ws of gi_psnr_workspace_bytes() bytes (device). */

@@ -697,4 +697,48 @@ void gio_vq_encode(const float* params, int n, int pos_mode, const float* gamma,
     }
 }
 
+
+// K-means (Lloyd) for the RVQ codebooks ("The color codebooks are
+// initialized using the K-means algorithm"; 5 iterations).  Per
+// iteration: each point goes to its nearest centroid (the fp32 distance and
+// tie rule of the encoder above), then every centroid with at least one
+// point becomes the fp64 mean of its points rounded once to fp32; an empty
+// cluster keeps its centroid (reading R31).  Returns the fp64 distortion of
+// the final assignment (sum of squared distances to the centroids it used).
+double gio_kmeans(const float* pts, int n, int B, float* cent, int iters, uint32_t* assign) {
+    double distortion = 0.0;
+    for (int it = 0; it < iters; ++it) {
+        std::vector<double> sum((size_t)B * 3, 0.0), cnt((size_t)B, 0.0);
+        distortion = 0.0;
+        for (int i = 0; i < n; ++i) {
+            const float* x = pts + 3 * (size_t)i;
+            int best = 0;
+            float bestd = INFINITY;
+            for (int k = 0; k < B; ++k) {
+                const float* c = cent + 3 * (size_t)k;
+                float d0 = c[0] - x[0], d1 = c[1] - x[1], d2 = c[2] - x[2];
+                float dd = d0 * d0;
+                dd = dd + d1 * d1;
+                dd = dd + d2 * d2;
+                if (dd < bestd) {
+                    bestd = dd;
+                    best = k;
+                }
+            }
+            assign[i] = (uint32_t)best;
+            const float* c = cent + 3 * (size_t)best;
+            for (int j = 0; j < 3; ++j) {
+                sum[3 * (size_t)best + j] += (double)x[j];
+                double d = (double)x[j] - (double)c[j];
+                distortion += d * d;
+            }
+            cnt[best] += 1.0;
+        }
+        for (int k = 0; k < B; ++k)
+            if (cnt[k] > 0.0)
+                for (int j = 0; j < 3; ++j) cent[3 * (size_t)k + j] = (float)(sum[3 * (size_t)k + j] / cnt[k]);
+    }
+    return distortion;
+}
+
 }  // extern "C"

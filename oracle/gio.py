@@ -39,6 +39,8 @@ def lib():
         L = C.CDLL(build())
         dp, fp, ip, up = (C.POINTER(C.c_double), C.POINTER(C.c_float),
                           C.POINTER(C.c_int32), C.POINTER(C.c_uint32))
+        L.gio_kmeans.restype = C.c_double
+        L.gio_kmeans.argtypes = [fp, C.c_int, C.c_int, fp, C.c_int, up]
         L.gio_float_to_half.restype = C.c_uint32
         L.gio_float_to_half.argtypes = [C.c_float]
         L.gio_vq_encode.argtypes = [fp, C.c_int, C.c_int, fp, fp, fp, C.c_int, C.c_int, C.c_int,
@@ -258,4 +260,15 @@ def vq_encode(params, gamma, beta, books, bits=6, stages=2, codebook=8, pos_mode
                         _p(cb, C.c_float), int(bits), int(stages), int(codebook), _p(pos16, C.c_uint32),
                         _p(codes, C.c_uint32), _p(idx, C.c_uint32), _p(eff, C.c_float))
     return dict(pos16=pos16, codes=codes, idx=idx, eff=eff)
+
+
+def kmeans(points, centroids, iters=5):
+    """Lloyd iterations (NEXT-2 codebook init) -> (centroids fp32 [B][3],
+    assignment uint32 [n], fp64 distortion of the last assignment)."""
+    pts = _f32(points).reshape(-1, 3)
+    cent = np.array(_f32(centroids).reshape(-1, 3), copy=True)
+    asg = np.zeros(pts.shape[0], np.uint32)
+    d = lib().gio_kmeans(_p(pts, C.c_float), pts.shape[0], cent.shape[0], _p(cent, C.c_float),
+                         int(iters), _p(asg, C.c_uint32))
+    return cent, asg, d
 

@@ -484,6 +484,20 @@ gi_status gi_vq_encode(const float* params, uint32_t flags, const gi_codec_meta*
                        "gi_vq_encode");
 }
 
+size_t gi_kmeans_workspace_bytes(int32_t B) {
+    return (B < 2 || B > 256) ? 0 : (size_t)B * 4 * sizeof(unsigned long long);
+}
+
+gi_status gi_kmeans_step(const float* points, int32_t n, int32_t B, float* centroids,
+                         uint32_t* assign, void* ws, size_t ws_bytes, void* stream) {
+    if (n < 0) return invalid("n");
+    if (B < 2 || B > 256) return invalid("B");
+    if (!ws || ws_bytes < gi_kmeans_workspace_bytes(B)) return invalid("workspace too small");
+    if (!centroids || (n > 0 && !points)) return invalid("NULL buffer");
+    return cuda_status(gi::launch_kmeans_step(points, n, B, centroids, assign, ws, S(stream)),
+                       "gi_kmeans_step");
+}
+
 gi_status gi_psnr(const float* image, const float* target, const gi_frame* f, float* psnr, void* ws,
                   void* stream) {
     gi_status st;

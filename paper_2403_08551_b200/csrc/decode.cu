@@ -155,6 +155,63 @@ __global__ void __launch_bounds__(256) vq_encode_kernel(
     }
 }
 
+// NEXT-2 K-means (Lloyd) step for the RVQ codebooks: assignment with the
+// encoder's fp32 distance and tie rule, then per-cluster sums in 2^-40 fixed
+// point (int64: integer addition is associative, so the sums -- and the
+// centroids -- do not depend on thread order).  Block partials in shared
+// memory, one global atomic per (block, cluster, field).
+constexpr double kFix = 1099511627776.0;   // 2^40
+
+__global__ void __launch_bounds__(256) kmeans_assign_kernel(const float* __restrict__ pts, int n,
+                                                            int B, const float* __restrict__ cent,
+                                                            uint32_t* __restrict__ assign,
+                                                            unsigned long long* __restrict__ acc) {
+    __shared__ float sc[256 * 3];
+    __shared__ unsigned long long sa[256 * 4];
+    for (int i = threadIdx.x; i < B * 3; i += blockDim.x) sc[i] = cent[i];
+    for (int i = threadIdx.x; i < B * 4; i += blockDim.x) sa[i] = 0ull;
+    __syncthreads();
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) {
+        const float x0 = pts[3 * (size_t)i], x1 = pts[3 * (size_t)i + 1], x2 = pts[3 * (size_t)i + 2];
+        int best = 0;
+        float bestd = __int_as_float(0x7f800000);
+        for (int k = 0; k < B; ++k) {
+            const float d0 = __fsub_rn(sc[3 * k], x0), d1 = __fsub_rn(sc[3 * k + 1], x1);
+            const float d2 = __fsub_rn(sc[3 * k + 2], x2);
+            float dd = __fmul_rn(d0, d0);
+            dd = __fadd_rn(dd, __fmul_rn(d1, d1));
+            dd = __fadd_rn(dd, __fmul_rn(d2, d2));
+            if (dd < bestd) {
+                bestd = dd;
+                best = k;
+            }
+        }
+        if (assign != nullptr) assign[i] = (uint32_t)best;
+        atomicAdd(&sa[4 * best + 0], (unsigned long long)__double2ll_rn((double)x0 * kFix));
+        atomicAdd(&sa[4 * best + 1], (unsigned long long)__double2ll_rn((double)x1 * kFix));
+        atomicAdd(&sa[4 * best + 2], (unsigned long long)__double2ll_rn((double)x2 * kFix));
+        atomicAdd(&sa[4 * best + 3], 1ull);
+    }
+    __syncthreads();
+    for (int k = threadIdx.x; k < B; k += blockDim.x)
+        if (sa[4 * k + 3] != 0ull)
+            for (int j = 0; j < 4; ++j) atomicAdd(&acc[4 * k + j], sa[4 * k + j]);
+}
+
+// New centroids (empty clusters keep theirs, reading R31); re-zeroes acc.
+__global__ void kmeans_update_kernel(int B, float* __restrict__ cent,
+                                     unsigned long long* __restrict__ acc) {
+    for (int k = threadIdx.x; k < B; k += blockDim.x) {
+        const long long c = (long long)acc[4 * k + 3];
+        if (c > 0)
+            for (int j = 0; j < 3; ++j)
+                cent[3 * k + j] =
+                    (float)((double)(long long)acc[4 * k + j] * (1.0 / kFix) / (double)c);
+        for (int j = 0; j < 4; ++j) acc[4 * k + j] = 0ull;
+    }
+}
+
 }  // namespace
 
 cudaError_t launch_vq_decode(const uint8_t* payload, const gi_codec_meta& meta, float* params,
@@ -188,6 +245,18 @@ cudaError_t launch_vq_encode(const float* params, bool logit, const gi_codec_met
         reinterpret_cast<const float4*>(params), meta.n, logit, meta.bits, meta.stages,
         meta.codebook, ib, rec, meta.gamma[0], meta.gamma[1], meta.gamma[2], meta.beta[0],
         meta.beta[1], meta.beta[2], meta.codebooks, payload, reinterpret_cast<float4*>(eff));
+    note_launches(1);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_kmeans_step(const float* points, int n, int B, float* centroids,
+                               uint32_t* assign, void* ws, cudaStream_t s) {
+    auto* acc = static_cast<unsigned long long*>(ws);
+    if (n > 0) {
+        kmeans_assign_kernel<<<(n + 255) / 256, 256, 0, s>>>(points, n, B, centroids, assign, acc);
+        note_launches(1);
+    }
+    kmeans_update_kernel<<<1, 256, 0, s>>>(B, centroids, acc);
     note_launches(1);
     return cudaGetLastError();
 }

@@ -331,6 +331,8 @@ cudaError_t launch_adan(float* params, const float* grads, float* m, float* v, f
                         float* gprev, int64_t count, int step, const uint32_t* step_dev, float lr,
                         int half_every, float b1, float b2, float b3, float eps, float wd,
                         uint32_t* flag, cudaStream_t s);
+cudaError_t launch_kmeans_step(const float* points, int n, int B, float* centroids,
+                               uint32_t* assign, void* ws, cudaStream_t s);
 cudaError_t launch_vq_encode(const float* params, bool logit, const gi_codec_meta& meta,
                              uint8_t* payload, float* eff, cudaStream_t s);
 cudaError_t launch_vq_decode(const uint8_t* payload, const gi_codec_meta& meta, float* params,

@@ -82,6 +82,8 @@ SIGNATURES = {
     "gi_render_frame": (C.c_int, [_vp, _i32, _FP, _u32, _i64, _vp, _sz, _vp, _vp]),
     "gi_vq_decode": (C.c_int, [_vp, _sz, C.POINTER(gi_codec_meta), _vp, _vp]),
     "gi_vq_encode": (C.c_int, [_vp, C.c_uint32, C.POINTER(gi_codec_meta), _vp, _sz, _vp, _vp]),
+    "gi_kmeans_workspace_bytes": (_sz, [C.c_int32]),
+    "gi_kmeans_step": (C.c_int, [_vp, C.c_int32, C.c_int32, _vp, _vp, _vp, _sz, _vp]),
     "gi_psnr_workspace_bytes": (_sz, [_FP]),
     "gi_psnr": (C.c_int, [_vp, _vp, _FP, _vp, _vp, _vp]),
     "gi_check": (C.c_int, [_vp, _i64, _vp, _vp]),
@@ -281,6 +283,17 @@ def gi_vq_encode(params, meta: gi_codec_meta, payload=None, eff=None, flags=0, s
     _ok(load().gi_vq_encode(_ptr(params), int(flags), C.byref(meta), _ptr(payload),
                             0 if payload is None else payload.numel(), _ptr(eff), _stream(stream)),
         "gi_vq_encode")
+
+
+def gi_kmeans_workspace_bytes(B) -> int:
+    return int(load().gi_kmeans_workspace_bytes(int(B)))
+
+
+def gi_kmeans_step(points, centroids, assign, ws, stream=None):
+    """One Lloyd iteration on device tensors points [n][3], centroids [B][3]."""
+    n, B = points.shape[0], centroids.shape[0]
+    _ok(load().gi_kmeans_step(_ptr(points), int(n), int(B), _ptr(centroids), _ptr(assign),
+                              _ptr(ws), ws.numel(), _stream(stream)), "gi_kmeans_step")
 
 
 def gi_vq_decode(payload, meta: gi_codec_meta, params, stream=None):

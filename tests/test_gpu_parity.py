@@ -593,3 +593,27 @@ def test_vq_encode_bitexact(gi, gio, bits, stages, codebook, pos_mode):
     dec = torch.zeros(n, 8, dtype=torch.float32, device=DEV)
     gi.gi_vq_decode(payload, meta, dec)
     assert torch.equal(dec, eff)
+
+
+def test_kmeans_step_parity(gi, gio):
+    # NEXT-2 codebook init: 5 Lloyd iterations on colours (stage 1) and on
+    # the stage-1 residuals (stage 2) vs the oracle; assignments bit-exact,
+    # centroids within 1 fp32 ulp-scale (fixed-point vs fp64 summation)
+    n, B = 70000, 8
+    p = synth.fitted_params(9, n)
+    cols = np.ascontiguousarray(p[:, 5:8])
+    init = cols[:: n // B][:B].copy()
+    ws = torch.zeros(gi.gi_kmeans_workspace_bytes(B), dtype=torch.uint8, device=DEV)
+    pts = to_dev(cols)
+    cent = to_dev(init)
+    asg = torch.zeros(n, dtype=torch.int32, device=DEV)
+    ref_c = init.copy()
+    for it in range(5):
+        ref_c_prev = ref_c
+        ref_c, ref_a, _ = gio.kmeans(cols, ref_c_prev, iters=1)
+        gi.gi_kmeans_step(pts, cent, asg, ws)
+        torch.cuda.synchronize()
+        got_c = cent.cpu().numpy()
+        assert np.array_equal(asg.cpu().numpy().view(np.uint32), ref_a), it
+        assert np.allclose(got_c, ref_c, rtol=3e-7, atol=1e-8), it
+        cent = to_dev(ref_c)          # continue both from the oracle's centroids

@@ -114,3 +114,33 @@ def test_encode_pack_decode_round_trip(gio):
     data = synth.pack_records(e["pos16"].astype(np.uint16), e["codes"], e["idx"], 6, 8)
     dec = gio.vq_decode(data, n, gamma, beta, books)
     assert np.array_equal(dec.view(np.uint32), e["eff"].view(np.uint32))
+
+
+def test_kmeans_pins(gio):
+    # P:307 K-means init (5 Lloyd iterations).
+    # N = B distinct points, initialised on them -> each its own centroid
+    rng = np.random.default_rng(7)
+    pts = rng.normal(0, 1, (8, 3)).astype(np.float32)
+    cent, asg, d = gio.kmeans(pts, pts[::-1], iters=5)
+    assert np.array_equal(np.sort(asg), np.arange(8)) and d == 0.0
+    assert np.array_equal(cent[asg], pts)
+    # two well-separated blobs, B = 2: centroids = blob means (closed form)
+    a = rng.normal(0, 0.05, (500, 3)) + [1, 0, 0]
+    b = rng.normal(0, 0.05, (300, 3)) + [-1, 0.5, 0]
+    pts = np.concatenate([a, b]).astype(np.float32)
+    cent, asg, _ = gio.kmeans(pts, np.float32([[0.5, 0, 0], [-0.5, 0, 0]]), iters=5)
+    assert np.allclose(cent[0], pts[:500].astype(np.float64).mean(0), atol=1e-6)
+    assert np.allclose(cent[1], pts[500:].astype(np.float64).mean(0), atol=1e-6)
+    assert asg[:500].max() == 0 and asg[500:].min() == 1
+    # Lloyd monotonicity: the distortion never increases (fp64, numpy)
+    pts = rng.normal(0, 0.4, (3000, 3)).astype(np.float32)
+    cent = pts[:8].copy()
+    prev = np.inf
+    for _ in range(6):
+        cent, asg, d = gio.kmeans(pts, cent, iters=1)
+        ref = ((pts.astype(np.float64) - cent.astype(np.float64)[asg]) ** 2).sum()
+        assert d <= prev + 1e-9
+        prev = ref            # distortion w.r.t. the updated centroids bounds the next one
+    # an empty cluster keeps its centroid (reading R31)
+    cent, asg, _ = gio.kmeans(pts, np.concatenate([pts[:7], [[50, 50, 50]]]).astype(np.float32), 1)
+    assert np.array_equal(cent[7], [50, 50, 50]) and 7 not in asg
