@@ -272,3 +272,86 @@ def kmeans(points, centroids, iters=5):
                          int(iters), _p(asg, C.c_uint32))
     return cent, asg, d
 
+
+
+def qat_step(params, target, state, step, lr, lam=1.0, decay=0.99, bits=6, stages=2, codebook=8,
+             mode=TILED, k=3.0, beta1=0.9, beta2=0.999, eps=1e-8):
+    """One attribute quantisation-aware fine-tuning step (NEXT-2; P:249-276,
+    P:301-307; SPEC quant module), composed from the oracle's pinned parts:
+
+      1. forward on the quantised cloud p^ = Q(p)  (vq_encode: fp16 position,
+         Eq. 8 codes, Eq. 9 greedy RVQ), L_rec = L2 of its render
+      2. straight-through gradients (reading R32): position d/draw = d/du *
+         (1 - tanh^2 raw); l: d/dl = d/dl^ inside the clamp range, 0 outside;
+         gamma_i += d/dl^ * (code - x) inside, * code outside (LSQ+ without
+         gradient scaling); beta_i += d/dl^ outside the range only; c' gets
+         d/dc^ (Eq. 10's stop-gradient leaves the commitment term to the
+         codebooks)
+      3. Adam (R16 constants, constant lr) on p and on (gamma, beta)
+      4. EMA codebooks (SPEC ema_update, reading R33): per stage m and
+         codeword k with n_k assigned residuals r = c' - c^^{m-1} summing to
+         s_k: N_k <- d N_k + (1 - d) n_k, S_k <- d S_k + (1 - d) s_k, and
+         C^m[k] <- S_k / N_k when n_k > 0 (unchanged otherwise)
+      5. L_c (Eq. 10) = 1/(N B) sum_m sum_n ||r_n^{m-1} - C^m[i_n^m]||^2 with
+         the pre-update codebooks; L = L_rec + lam L_c
+
+    state: dict(m, v [N][8]; gamma, beta [3]; qm, qv [6] (Adam state of
+    gamma|beta); books [M][B][3]; ema_n [M][B]; ema_s [M][B][3]) -- fp32
+    arrays, returned updated (fp32) with grads / eff / losses.
+    """
+    p = _f32(params).reshape(-1, 8)
+    n = p.shape[0]
+    gamma, beta = _f32(state["gamma"]), _f32(state["beta"])
+    books = _f32(state["books"]).reshape(stages, codebook, 3)
+    enc = vq_encode(p, gamma, beta, books, bits, stages, codebook, POS_LOGIT)
+    eff = enc["eff"]
+    t = _f32(target)
+    H, W = t.shape[1], t.shape[2]
+    img = render(eff, W, H, k, 16, POS_NORMALIZED, mode)
+    l_rec, dimg = mse(img, t)
+    ge = backward(eff, dimg, W, H, k, 16, POS_NORMALIZED, mode)          # d/dp^ (fp64)
+    # 2. straight-through map
+    g = np.array(ge, copy=True)
+    th = np.tanh(p[:, :2].astype(np.float64))
+    g[:, :2] = ge[:, :2] * (1.0 - th * th)
+    qmax = float((1 << bits) - 1)
+    x = ((p[:, 2:5] - beta[None, :]) / gamma[None, :]).astype(np.float32)   # fp32 as the encoder
+    inside = (x >= 0) & (x <= qmax)
+    code = enc["codes"].astype(np.float64)
+    g[:, 2:5] = np.where(inside, ge[:, 2:5], 0.0)
+    dgamma = (ge[:, 2:5] * np.where(inside, code - x.astype(np.float64), code)).sum(0)
+    dbeta = (ge[:, 2:5] * np.where(inside, 0.0, 1.0)).sum(0)
+    # 3. Adam
+    po, mo, vo = adam(p, g.astype(np.float32), state["m"], state["v"], step, lr, beta1, beta2, eps)
+    qg = np.concatenate([dgamma, dbeta]).astype(np.float32)
+    qp = np.concatenate([gamma, beta])
+    qpo, qmo, qvo = adam(qp, qg, state["qm"], state["qv"], step, lr, beta1, beta2, eps)
+    # 4./5. residuals per stage with the pre-update books, EMA, commitment
+    c = p[:, 5:8]
+    chat = np.zeros((n, 3), np.float32)
+    ema_n = np.array(_f32(state["ema_n"]).reshape(stages, codebook), np.float64)
+    ema_s = np.array(_f32(state["ema_s"]).reshape(stages, codebook, 3), np.float64)
+    new_books = np.array(books, copy=True)
+    l_c = 0.0
+    for m in range(stages):
+        r = (c - chat).astype(np.float32)                                 # fp32 as the encoder
+        ii = enc["idx"][:, m].astype(np.int64)
+        cw = books[m][ii]
+        l_c += ((r.astype(np.float64) - cw.astype(np.float64)) ** 2).sum()
+        cnt = np.bincount(ii, minlength=codebook).astype(np.float64)
+        sums = np.zeros((codebook, 3))
+        np.add.at(sums, ii, r.astype(np.float64))
+        ema_n[m] = decay * ema_n[m] + (1.0 - decay) * cnt
+        ema_s[m] = decay * ema_s[m] + (1.0 - decay) * sums
+        upd = cnt > 0
+        new_books[m][upd] = (ema_s[m][upd] / ema_n[m][upd][:, None]).astype(np.float32)
+        chat = (cw if m == 0 else (chat + cw)).astype(np.float32)
+    l_c /= float(n * codebook)
+    out = dict(state)
+    out.update(m=mo.astype(np.float32), v=vo.astype(np.float32), gamma=qpo[:3].astype(np.float32),
+               beta=qpo[3:].astype(np.float32), qm=qmo.astype(np.float32),
+               qv=qvo.astype(np.float32), books=new_books, ema_n=ema_n.astype(np.float32),
+               ema_s=ema_s.astype(np.float32))
+    return dict(params=po.astype(np.float32), state=out, grads=g, grads_eff=ge, eff=eff,
+                dgamma=dgamma, dbeta=dbeta, l_rec=l_rec, l_c=l_c, loss=l_rec + lam * l_c,
+                enc=enc)

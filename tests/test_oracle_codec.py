@@ -144,3 +144,106 @@ def test_kmeans_pins(gio):
     # an empty cluster keeps its centroid (reading R31)
     cent, asg, _ = gio.kmeans(pts, np.concatenate([pts[:7], [[50, 50, 50]]]).astype(np.float32), 1)
     assert np.array_equal(cent[7], [50, 50, 50]) and 7 not in asg
+
+
+def _qat_state(n, rng, stages=2, codebook=8):
+    books = rng.normal(0, 0.3, (stages, codebook, 3)).astype(np.float32)
+    return dict(m=np.zeros((n, 8), np.float32), v=np.zeros((n, 8), np.float32),
+                gamma=np.float32([0.05, 0.04, 0.05]), beta=np.float32([-1.0, -1.2, -1.0]),
+                qm=np.zeros(6, np.float32), qv=np.zeros(6, np.float32), books=books,
+                ema_n=np.ones((stages, codebook), np.float32), ema_s=books.copy())
+
+
+def test_qat_straight_through_gradients_fd(gio):
+    # Reading R32 (LSQ+ straight-through estimator): the oracle's gradients
+    # w.r.t. raw positions, l, gamma and beta equal central finite
+    # differences of L_rec through the quantiser with its rounding offsets
+    # frozen at the base point (dense render: no box discontinuities)
+    rng = np.random.default_rng(11)
+    W = H = 24
+    n = 40
+    p = synth.fitted_params(11, n)
+    p[:, 2:5] = rng.uniform(-1.2, 2.0, (n, 3)).astype(np.float32)   # some clamp on both sides
+    t = synth.image(11, W, H)
+    st = _qat_state(n, rng)
+    out = gio.qat_step(p, t, st, 1, 1e-4, mode=gio.DENSE)
+    enc = out["enc"]
+    gamma, beta = st["gamma"].astype(np.float64), st["beta"].astype(np.float64)
+    qmax = 63.0
+    x0 = ((p[:, 2:5] - st["beta"]) / st["gamma"]).astype(np.float32).astype(np.float64)
+    inside = (x0 >= 0) & (x0 <= qmax)
+    delta = enc["codes"] - x0                         # frozen rounding offsets
+    u0 = np.tanh(p[:, :2].astype(np.float64))
+    du = enc["eff"][:, :2] - u0                        # frozen fp16 offsets
+
+    def loss(raw_xy, l, g, b):
+        e = np.array(enc["eff"], np.float64)
+        e[:, :2] = np.tanh(raw_xy) + du
+        x = (l - b) / g
+        e[:, 2:5] = np.where(inside, g * (x + delta) + b, g * enc["codes"] + b)
+        img = gio.render(e.astype(np.float64).astype(np.float32), W, H, pos_mode=gio.POS_NORMALIZED,
+                         mode=gio.DENSE)
+        return float(((img - t) ** 2).mean())
+
+    raw = p[:, :2].astype(np.float64)
+    l = p[:, 2:5].astype(np.float64)
+    # Richardson-extrapolated central differences (params reach the render in
+    # fp32, which bounds how small h can be); 1e-2 still separates every
+    # plausible slip (sign, code vs code - x, inside/outside swapped: O(1))
+    def rich(f, h):
+        d1 = (f(h) - f(-h)) / (2 * h)
+        d2 = (f(h / 2) - f(-h / 2)) / h
+        return (4 * d2 - d1) / 3
+
+    for j in range(3):
+        e = np.zeros(3); e[j] = 1.0
+        fd_g = rich(lambda s: loss(raw, l, gamma + s * e, beta), 4e-4)
+        fd_b = rich(lambda s: loss(raw, l, gamma, beta + s * e), 4e-4)
+        assert abs(fd_g - out["dgamma"][j]) <= 1e-2 * abs(fd_g) + 1e-7, (j, fd_g, out["dgamma"][j])
+        assert abs(fd_b - out["dbeta"][j]) <= 1e-2 * abs(fd_b) + 1e-7, (j, fd_b, out["dbeta"][j])
+    h = 1e-4
+    for (i, j) in [(0, 0), (3, 1), (7, 2), (11, 0)]:
+        d = np.zeros_like(l); d[i, j] = h
+        fd = (loss(raw, l + d, gamma, beta) - loss(raw, l - d, gamma, beta)) / (2 * h)
+        assert abs(fd - out["grads"][i, 2 + j]) <= 2e-3 * abs(fd) + 1e-7
+        d = np.zeros_like(raw); d[i, j % 2] = h
+        fd = (loss(raw + d, l, gamma, beta) - loss(raw - d, l, gamma, beta)) / (2 * h)
+        assert abs(fd - out["grads"][i, j % 2]) <= 2e-3 * abs(fd) + 1e-7
+
+
+def test_qat_ema_and_commitment_pins(gio):
+    # SPEC ema_update and Eq. 10 commitment loss
+    rng = np.random.default_rng(12)
+    W = H = 16
+    n = 64
+    p = synth.init_params(12, n)
+    t = synth.image(12, W, H)
+    st = _qat_state(n, rng)
+    # exact codewords (stage-2 codeword 0 = 0): L_c = 0 and the books only
+    # move by the EMA of themselves
+    st["books"][1, 0] = 0.0
+    st["ema_s"] = st["books"].copy()
+    pick = rng.integers(0, 8, n)
+    p[:, 5:8] = st["books"][0][pick]
+    out = gio.qat_step(p, t, st, 1, 1e-4, mode=gio.DENSE)
+    assert out["l_c"] == 0.0
+    assert np.array_equal(out["enc"]["idx"][:, 0], pick)
+    # decay 0: each used codeword becomes the mean of its residuals, unused
+    # codewords are unchanged (stationary in one step)
+    p2 = synth.init_params(13, n)
+    out = gio.qat_step(p2, t, st, 1, 1e-4, decay=0.0, mode=gio.DENSE)
+    idx = out["enc"]["idx"][:, 0]
+    for kk in range(8):
+        sel = idx == kk
+        if sel.any():
+            assert np.allclose(out["state"]["books"][0, kk], p2[sel, 5:8].astype(np.float64).mean(0),
+                               atol=1e-6)
+        else:
+            assert np.array_equal(out["state"]["books"][0, kk], st["books"][0, kk])
+    # N = 1, B = 1, M = 1: c' = (1, 0, 0), C = 0 -> L_c = 1
+    one = np.zeros((1, 8), np.float32); one[0, 5] = 1.0
+    s1 = _qat_state(1, rng, stages=1, codebook=1)
+    s1["books"][:] = 0.0
+    s1["ema_s"] = s1["books"].copy()
+    out = gio.qat_step(one, t, s1, 1, 1e-4, stages=1, codebook=1, mode=gio.DENSE)
+    assert out["l_c"] == 1.0
