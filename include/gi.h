@@ -274,6 +274,34 @@ size_t gi_kmeans_workspace_bytes(int32_t B);
 gi_status gi_kmeans_step(const float* points, int32_t n, int32_t B, float* centroids,
                          uint32_t* assign, void* ws, size_t ws_bytes, void* stream);
 
+/* NEXT-2 attribute quantisation-aware fine-tuning step (QAT; Fig. 3, P:249-
+ * 276), one image (f->batch == 1), graph-capturable:
+ *   p^ = Q(p) (gi_vq_encode's quantisers, gamma|beta = qparams[0..5] and
+ *   books read on the device) -> project + direct binning -> fused Eq. 7 +
+ *   L2 + App. A backward on p^ (positions normalised) -> straight-through
+ *   gradients (reading R32: d/draw_mu = d/du / cosh^2, l passes inside the
+ *   clamp range, LSQ+ gamma/beta gradients without scaling, c' gets d/dc^)
+ *   -> Adam (constant cfg->lr, bias-corrected by the device step counter) on
+ *   params and on qparams -> EMA codebooks (reading R33: N <- d N + (1-d) n,
+ *   S <- d S + (1-d) sum r, C <- S / N where n > 0).
+ * params, m, v [n][8] in/out; eff [n][8] out (p^); grads [n][8] out
+ * (d/draw); qparams, qm, qv [6] in/out; books [M][B][3], ema_n [M][B],
+ * ema_s [M][B][3] in/out; losses [9] out = {L_rec + lambda L_c, L_rec, L_c
+ * (Eq. 10 with the pre-update books), d/dgamma_0..2, d/dbeta_0..2}.  All sums across Gaussians are
+ * fixed-point integer sums: deterministic.  ws: gi_qat_workspace_bytes()
+ * device bytes, zero-filled once. */
+typedef struct {
+    int32_t bits, stages, codebook;
+    float lr, lambda, decay, beta1, beta2, eps;
+} gi_qat_config;
+size_t gi_qat_workspace_bytes(int32_t n, int64_t key_capacity, const gi_frame* f,
+                              const gi_qat_config* cfg);
+gi_status gi_qat_step(float* params, float* m, float* v, float* eff, float* grads, float* qparams,
+                      float* qm, float* qv, float* books, float* ema_n, float* ema_s,
+                      const float* target, int32_t n, const gi_frame* f, const gi_qat_config* cfg,
+                      int64_t key_capacity, void* ws, size_t ws_bytes, uint32_t* step_counter,
+                      float* losses, uint32_t* status_flags, void* stream);
+
 /* --- harness helpers (not on the hot path) ---------------------------------
  * PSNR of each image on [0,1]-clamped values, capped at 100 dB:
  * psnr[B] fp32 out; ws of gi_psnr_workspace_bytes() bytes (device). */

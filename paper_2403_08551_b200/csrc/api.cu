@@ -6,6 +6,7 @@
 #include <cstdlib>
 #include <cstring>
 
+#include "codec_core.cuh"
 #include "gi_internal.cuh"
 
 namespace gi {
@@ -496,6 +497,92 @@ gi_status gi_kmeans_step(const float* points, int32_t n, int32_t B, float* centr
     if (!centroids || (n > 0 && !points)) return invalid("NULL buffer");
     return cuda_status(gi::launch_kmeans_step(points, n, B, centroids, assign, ws, S(stream)),
                        "gi_kmeans_step");
+}
+
+static gi_status check_qat_cfg(const gi_qat_config* cfg) {
+    if (!cfg) return invalid("cfg is NULL");
+    if (cfg->bits < 1 || cfg->bits > 16 || cfg->stages < 1 || cfg->stages > 8 ||
+        cfg->codebook < 2 || cfg->codebook > 256) {
+        std::snprintf(g_err, sizeof(g_err), "codec metadata out of range");
+        return GI_EFORMAT;
+    }
+    int ib = 1;
+    while ((1 << ib) < cfg->codebook) ++ib;
+    if (32 + 3 * cfg->bits + cfg->stages * ib > 64) {
+        std::snprintf(g_err, sizeof(g_err), "record wider than 64 bits");
+        return GI_EFORMAT;
+    }
+    if (!(cfg->decay >= 0.f && cfg->decay < 1.f) || !(cfg->beta1 >= 0.f && cfg->beta1 < 1.f) ||
+        !(cfg->beta2 >= 0.f && cfg->beta2 < 1.f) || !(cfg->lr >= 0.f))
+        return invalid("qat config");
+    return GI_OK;
+}
+
+size_t gi_qat_workspace_bytes(int32_t n, int64_t key_capacity, const gi_frame* f,
+                              const gi_qat_config* cfg) {
+    if (check_frame(f) != GI_OK || n < 0 || key_capacity < 0 || check_qat_cfg(cfg) != GI_OK)
+        return 0;
+    return carve_fit(nullptr, n, key_capacity, *f).bytes +
+           gi::align_up(8 * gi::qat_acc_words(cfg->stages, cfg->codebook)) + gi::align_up(16);
+}
+
+gi_status gi_qat_step(float* params, float* m, float* v, float* eff, float* grads, float* qparams,
+                      float* qm, float* qv, float* books, float* ema_n, float* ema_s,
+                      const float* target, int32_t n, const gi_frame* f, const gi_qat_config* cfg,
+                      int64_t key_capacity, void* ws, size_t ws_bytes, uint32_t* step_counter,
+                      float* losses, uint32_t* status_flags, void* stream) {
+    gi_status st;
+    if ((st = check_frame(f)) != GI_OK || (st = check_n(n, f)) != GI_OK) return st;
+    if (f->batch != 1) return invalid("gi_qat_step takes one image (batch 1)");
+    if ((st = check_qat_cfg(cfg)) != GI_OK) return st;
+    if (key_capacity < 0 || key_capacity >= (1LL << 31)) return invalid("key_capacity");
+    if (!ws || ws_bytes < gi_qat_workspace_bytes(n, key_capacity, f, cfg))
+        return invalid("qat workspace too small");
+    if (!step_counter || !target || !losses || !qparams || !qm || !qv || !books || !ema_n ||
+        !ema_s || (n > 0 && (!params || !m || !v || !eff || !grads)))
+        return invalid("NULL buffer");
+    if (!aligned16(params) || !aligned16(m) || !aligned16(v) || !aligned16(eff) ||
+        !aligned16(grads) || !aligned16(ws))
+        return invalid("alignment");
+    FitWs w = carve_fit(ws, n, key_capacity, *f);
+    char* extra = static_cast<char*>(ws) + w.bytes;
+    void* acc = extra;
+    float* consts = reinterpret_cast<float*>(extra + gi::align_up(8 * gi::qat_acc_words(cfg->stages,
+                                                                                        cfg->codebook)));
+    cudaStream_t s = S(stream);
+    cudaError_t e;
+#define GI_TRY(expr, where) \
+    if ((e = (expr)) != cudaSuccess) return cuda_status(e, where)
+    int ib = 1;
+    while ((1 << ib) < cfg->codebook) ++ib;
+    const gi::QuantParams qp{cfg->bits, cfg->stages, cfg->codebook, ib, {1.f, 1.f, 1.f},
+                             {0.f, 0.f, 0.f}};
+    GI_TRY(gi::launch_qat_quantize(params, n, qp, qparams, books, eff, acc, step_counter, consts,
+                                   cfg->lr, cfg->beta1, cfg->beta2, s),
+           "gi_qat_step/quantize");
+    uint32_t* gauss_off = gi::backward_gauss_off(w.bwd_ws, n, key_capacity, *f);
+    const gi::BinCounts bc = gi::bin_counts_direct(w.bin_ws, n, key_capacity, *f, w.key_gid, gauss_off);
+    const gi::ChainState cs = gi::bin_chain_direct(w.bin_ws, n, key_capacity, *f, w.key_gid,
+                                                   gauss_off, w.n_keys, nullptr);
+    GI_TRY(gi::launch_project(eff, n, *f, GI_POS_NORMALIZED, w.proj, w.touched,
+                              gi::ProjectFuse{nullptr, bc}, s),
+           "gi_qat_step/project");
+    GI_TRY(gi::launch_backward_tiles(w.proj, w.key_gid, nullptr, n, *f, false, nullptr, target,
+                                     key_capacity, w.bwd_ws, nullptr, cs, s),
+           "gi_qat_step/backward");
+    GI_TRY(gi::launch_backward_finalize(eff, w.proj, n, *f, GI_POS_NORMALIZED, true, key_capacity,
+                                        w.bwd_ws, grads, losses + 1, nullptr, s),
+           "gi_qat_step/finalize");
+    GI_TRY(gi::launch_qat_update(params, m, v, grads, n, cfg->bits, qparams, consts, cfg->beta1,
+                                 cfg->beta2, cfg->eps, acc, cfg->stages, cfg->codebook,
+                                 status_flags, s),
+           "gi_qat_step/update");
+    GI_TRY(gi::launch_qat_finish(qparams, qm, qv, books, ema_n, ema_s, acc, cfg->stages,
+                                 cfg->codebook, n, consts, cfg->beta1, cfg->beta2, cfg->eps,
+                                 cfg->decay, cfg->lambda, losses, s),
+           "gi_qat_step/finish");
+#undef GI_TRY
+    return GI_OK;
 }
 
 gi_status gi_psnr(const float* image, const float* target, const gi_frame* f, float* psnr, void* ws,

@@ -6,14 +6,10 @@
 // One thread per record; R <= 64-bit records are read through a 72-bit
 // big-endian window; codebooks (M*B*3 floats) are staged in shared memory.
 // Output feeds gi_project(GI_POS_NORMALIZED).
-#include <cuda_fp16.h>
-
-#include "gi_internal.cuh"
+#include "codec_core.cuh"
 
 namespace gi {
 namespace {
-
-constexpr int kMaxBook = 8 * 256 * 3;   // stages <= 8, codebook <= 256
 
 __global__ void __launch_bounds__(256) vq_decode_kernel(const uint8_t* __restrict__ payload,
                                                         int n, int bits, int stages, int codebook,
@@ -81,53 +77,13 @@ __global__ void __launch_bounds__(256) vq_encode_kernel(
     __syncthreads();
     const int r = blockIdx.x * blockDim.x + threadIdx.x;
     if (r >= n) return;
-    const float4 p0 = params[2 * (size_t)r], p1 = params[2 * (size_t)r + 1];
-    const double ux = logit ? tanh((double)p0.x) : (double)p0.x;
-    const double uy = logit ? tanh((double)p0.y) : (double)p0.y;
-    const __half hx = __float2half_rn(__double2float_rn(ux));
-    const __half hy = __float2half_rn(__double2float_rn(uy));
-    const float qmax = (float)((1u << bits) - 1u);
-    const float g[3] = {g0, g1, g2}, be[3] = {b0, b1, b2}, l[3] = {p0.z, p0.w, p1.x};
-    uint32_t code[3];
-    float lq[3];
-#pragma unroll
-    for (int j = 0; j < 3; ++j) {
-        float x = __fdiv_rn(__fsub_rn(l[j], be[j]), g[j]);
-        x = fminf(fmaxf(x, 0.0f), qmax);
-        code[j] = __float2uint_rn(x);
-        lq[j] = __fmaf_rn((float)code[j], g[j], be[j]);
-    }
-    uint64_t v = ((uint64_t)__half_as_ushort(hx) << 16) | (uint64_t)__half_as_ushort(hy);
-#pragma unroll
-    for (int j = 0; j < 3; ++j) v = (v << bits) | code[j];
-    const float c[3] = {p1.y, p1.z, p1.w};
-    float ch0 = 0.f, ch1 = 0.f, ch2 = 0.f;
-    for (int m = 0; m < stages; ++m) {
-        const float r0 = __fsub_rn(c[0], ch0), r1 = __fsub_rn(c[1], ch1), r2 = __fsub_rn(c[2], ch2);
-        int best = 0;
-        float bestd = __int_as_float(0x7f800000);
-        for (int k = 0; k < codebook; ++k) {
-            const float* cw = sb + (m * codebook + k) * 3;
-            const float d0 = __fsub_rn(cw[0], r0), d1 = __fsub_rn(cw[1], r1), d2 = __fsub_rn(cw[2], r2);
-            float dd = __fmul_rn(d0, d0);
-            dd = __fadd_rn(dd, __fmul_rn(d1, d1));
-            dd = __fadd_rn(dd, __fmul_rn(d2, d2));
-            if (dd < bestd) {
-                bestd = dd;
-                best = k;
-            }
-        }
-        const float* cw = sb + (m * codebook + best) * 3;
-        if (m == 0) {
-            ch0 = cw[0]; ch1 = cw[1]; ch2 = cw[2];
-        } else {
-            ch0 = __fadd_rn(ch0, cw[0]); ch1 = __fadd_rn(ch1, cw[1]); ch2 = __fadd_rn(ch2, cw[2]);
-        }
-        v = (v << ib) | (uint64_t)best;
-    }
+    const QuantParams qp{bits, stages, codebook, ib, {g0, g1, g2}, {b0, b1, b2}};
+    float4 e0, e1;
+    const uint64_t v = encode_one(params[2 * (size_t)r], params[2 * (size_t)r + 1], logit, qp, sb,
+                                  e0, e1, [](int, int, float, float, float, const float*) {});
     if (eff != nullptr) {
-        eff[2 * (size_t)r] = make_float4(__half2float(hx), __half2float(hy), lq[0], lq[1]);
-        eff[2 * (size_t)r + 1] = make_float4(lq[2], ch0, ch1, ch2);
+        eff[2 * (size_t)r] = e0;
+        eff[2 * (size_t)r + 1] = e1;
     }
     if (payload == nullptr) return;
     const int64_t bit0 = (int64_t)r * rec_bits;

@@ -331,6 +331,20 @@ cudaError_t launch_adan(float* params, const float* grads, float* m, float* v, f
                         float* gprev, int64_t count, int step, const uint32_t* step_dev, float lr,
                         int half_every, float b1, float b2, float b3, float eps, float wd,
                         uint32_t* flag, cudaStream_t s);
+struct QuantParams;
+size_t qat_acc_words(int stages, int codebook);
+cudaError_t launch_qat_quantize(const float* params, int n, const QuantParams& qp,
+                                const float* qparams, const float* books, float* eff, void* acc,
+                                uint32_t* step, float* consts, float lr, float b1, float b2,
+                                cudaStream_t s);
+cudaError_t launch_qat_update(float* params, float* m, float* v, float* grads, int n, int bits,
+                              const float* qparams, const float* consts, float b1, float b2,
+                              float eps, void* acc, int stages, int codebook, uint32_t* flag,
+                              cudaStream_t s);
+cudaError_t launch_qat_finish(float* qparams, float* qm, float* qv, float* books, float* ema_n,
+                              float* ema_s, void* acc, int stages, int codebook, int n,
+                              const float* consts, float b1, float b2, float eps, float decay,
+                              float lambda, float* losses, cudaStream_t s);
 cudaError_t launch_kmeans_step(const float* points, int n, int B, float* centroids,
                                uint32_t* assign, void* ws, cudaStream_t s);
 cudaError_t launch_vq_encode(const float* params, bool logit, const gi_codec_meta& meta,

@@ -43,6 +43,12 @@ class gi_codec_meta(C.Structure):
                 ("codebooks", C.c_void_p)]
 
 
+class gi_qat_config(C.Structure):
+    _fields_ = [("bits", C.c_int32), ("stages", C.c_int32), ("codebook", C.c_int32),
+                ("lr", C.c_float), ("lam", C.c_float), ("decay", C.c_float), ("beta1", C.c_float),
+                ("beta2", C.c_float), ("eps", C.c_float)]
+
+
 def frame(width: int, height: int, batch: int = 1, k: float = 3.0, tile: int = TILE) -> gi_frame:
     return gi_frame(int(width), int(height), int(tile), int(batch), float(k))
 
@@ -83,6 +89,11 @@ SIGNATURES = {
     "gi_vq_decode": (C.c_int, [_vp, _sz, C.POINTER(gi_codec_meta), _vp, _vp]),
     "gi_vq_encode": (C.c_int, [_vp, C.c_uint32, C.POINTER(gi_codec_meta), _vp, _sz, _vp, _vp]),
     "gi_kmeans_workspace_bytes": (_sz, [C.c_int32]),
+    "gi_qat_workspace_bytes": (_sz, [C.c_int32, C.c_int64, C.POINTER(gi_frame),
+                                     C.POINTER(gi_qat_config)]),
+    "gi_qat_step": (C.c_int, [_vp] * 11 + [_vp, C.c_int32, C.POINTER(gi_frame),
+                                           C.POINTER(gi_qat_config), C.c_int64, _vp, _sz, _vp, _vp,
+                                           _vp, _vp]),
     "gi_kmeans_step": (C.c_int, [_vp, C.c_int32, C.c_int32, _vp, _vp, _vp, _sz, _vp]),
     "gi_psnr_workspace_bytes": (_sz, [_FP]),
     "gi_psnr": (C.c_int, [_vp, _vp, _FP, _vp, _vp, _vp]),
@@ -281,7 +292,7 @@ def gi_vq_encode(params, meta: gi_codec_meta, payload=None, eff=None, flags=0, s
     """NEXT-2 encoder: quantise params [n][8] into packed records (payload,
     uint8 device tensor) and/or the dequantised parameters eff [n][8]."""
     _ok(load().gi_vq_encode(_ptr(params), int(flags), C.byref(meta), _ptr(payload),
-                            0 if payload is None else payload.numel(), _ptr(eff), _stream(stream)),
+                            0 if payload is None else payload.numel() * payload.element_size(), _ptr(eff), _stream(stream)),
         "gi_vq_encode")
 
 
@@ -293,11 +304,31 @@ def gi_kmeans_step(points, centroids, assign, ws, stream=None):
     """One Lloyd iteration on device tensors points [n][3], centroids [B][3]."""
     n, B = points.shape[0], centroids.shape[0]
     _ok(load().gi_kmeans_step(_ptr(points), int(n), int(B), _ptr(centroids), _ptr(assign),
-                              _ptr(ws), ws.numel(), _stream(stream)), "gi_kmeans_step")
+                              _ptr(ws), ws.numel() * ws.element_size(), _stream(stream)), "gi_kmeans_step")
+
+
+def qat_config(bits=6, stages=2, codebook=8, lr=1e-4, lam=1.0, decay=0.99, beta1=0.9,
+               beta2=0.999, eps=1e-8) -> gi_qat_config:
+    return gi_qat_config(int(bits), int(stages), int(codebook), float(lr), float(lam),
+                         float(decay), float(beta1), float(beta2), float(eps))
+
+
+def gi_qat_workspace_bytes(n, key_capacity, f: gi_frame, cfg: gi_qat_config) -> int:
+    return int(load().gi_qat_workspace_bytes(int(n), int(key_capacity), C.byref(f), C.byref(cfg)))
+
+
+def gi_qat_step(params, m, v, eff, grads, qparams, qm, qv, books, ema_n, ema_s, target, n,
+                f: gi_frame, cfg: gi_qat_config, key_capacity, ws, step_counter, losses,
+                status_flags=None, stream=None):
+    _ok(load().gi_qat_step(*(_ptr(t) for t in (params, m, v, eff, grads, qparams, qm, qv, books,
+                                                ema_n, ema_s, target)), int(n), C.byref(f),
+                           C.byref(cfg), int(key_capacity), _ptr(ws), ws.numel() * ws.element_size(),
+                           _ptr(step_counter), _ptr(losses), _ptr(status_flags), _stream(stream)),
+        "gi_qat_step")
 
 
 def gi_vq_decode(payload, meta: gi_codec_meta, params, stream=None):
-    _ok(load().gi_vq_decode(_ptr(payload), payload.numel(), C.byref(meta), _ptr(params),
+    _ok(load().gi_vq_decode(_ptr(payload), payload.numel() * payload.element_size(), C.byref(meta), _ptr(params),
                             _stream(stream)), "gi_vq_decode")
 
 

@@ -214,3 +214,65 @@ class Fitter:
 
     def steps_done(self) -> int:
         return int(self.step_counter[0].item())
+
+
+class QatFitter:
+    """NEXT-2 attribute quantisation-aware fine-tuning (gi_qat_step) of one
+    image's fitted cloud: fp16 positions, b-bit Cholesky codes with learned
+    gamma/beta, M-stage RVQ colours with EMA codebooks."""
+
+    def __init__(self, params: torch.Tensor, target: torch.Tensor, gamma, beta,
+                 books: torch.Tensor, k: float = 3.0, key_capacity: int | None = None,
+                 **cfg):
+        gi.load()
+        assert params.dim() == 2 and params.shape[1] == 8, "params [N][8] (one image)"
+        self.device = params.device
+        n = params.shape[0]
+        H, W = target.shape[-2], target.shape[-1]
+        self.n = n
+        self.f = gi.frame(W, H, 1, k)
+        self.cfg = gi.qat_config(**cfg)
+        self.cap = int(key_capacity) if key_capacity else default_capacity(n, 1)
+        self.ws = _bytes(gi.gi_qat_workspace_bytes(n, self.cap, self.f, self.cfg), self.device)
+        self.params = params.contiguous()
+        self.target = target.contiguous()
+        self.m = torch.zeros_like(self.params)
+        self.v = torch.zeros_like(self.params)
+        self.eff = torch.zeros_like(self.params)
+        self.grads = torch.zeros_like(self.params)
+        self.qparams = torch.tensor(list(gamma) + list(beta), dtype=torch.float32,
+                                    device=self.device)
+        self.qm = torch.zeros(6, dtype=torch.float32, device=self.device)
+        self.qv = torch.zeros(6, dtype=torch.float32, device=self.device)
+        self.books = books.contiguous().clone()
+        M, Bk = self.books.shape[0], self.books.shape[1]
+        self.ema_n = torch.ones(M, Bk, dtype=torch.float32, device=self.device)
+        self.ema_s = self.books.clone()
+        self.step_counter = _u32(1, self.device)
+        self.status = _u32(1, self.device)
+        self.losses = torch.zeros(9, dtype=torch.float32, device=self.device)
+        self.graph = None
+
+    def step(self, stream=None):
+        gi.gi_qat_step(self.params, self.m, self.v, self.eff, self.grads, self.qparams, self.qm,
+                       self.qv, self.books, self.ema_n, self.ema_s, self.target, self.n, self.f,
+                       self.cfg, self.cap, self.ws, self.step_counter, self.losses, self.status,
+                       stream)
+
+    def capture(self, steps_per_graph: int = 1):
+        s = torch.cuda.Stream(self.device)
+        s.wait_stream(torch.cuda.current_stream(self.device))
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            for _ in range(steps_per_graph):
+                self.step(s)
+        torch.cuda.current_stream(self.device).wait_stream(s)
+        self.graph = g
+        return g
+
+    def replay(self):
+        self.graph.replay()
+
+    def check(self) -> int:
+        return gi.gi_check(None, self.cap, self.status)
+

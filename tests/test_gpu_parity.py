@@ -617,3 +617,48 @@ def test_kmeans_step_parity(gi, gio):
         assert np.array_equal(asg.cpu().numpy().view(np.uint32), ref_a), it
         assert np.allclose(got_c, ref_c, rtol=3e-7, atol=1e-8), it
         cent = to_dev(ref_c)          # continue both from the oracle's centroids
+
+
+def test_qat_step_parity(gi, gio):
+    # NEXT-2 QAT step vs the oracle's composition (straight-through LSQ+
+    # gradients, Adam, EMA codebooks, Eq. 10): quantised cloud bit-exact,
+    # gradients per group <= 1e-4, losses, gamma/beta gradients, the updated
+    # parameters and codebooks
+    from paper_2403_08551_b200.pipeline import QatFitter
+    W, H, n = 96, 64, 600
+    rng = np.random.default_rng(21)
+    p = synth.fitted_params(21, n)
+    tgt = synth.image(21, W, H)
+    gamma = np.float32([0.05, 0.04, 0.05])
+    beta = np.float32([-1.0, -1.2, -1.0])
+    books = rng.normal(0, 0.3, (2, 8, 3)).astype(np.float32)
+    st = dict(m=np.zeros((n, 8), np.float32), v=np.zeros((n, 8), np.float32), gamma=gamma,
+              beta=beta, qm=np.zeros(6, np.float32), qv=np.zeros(6, np.float32), books=books,
+              ema_n=np.ones((2, 8), np.float32), ema_s=books.copy())
+    ref = gio.qat_step(p, tgt, st, 1, 1e-4, lam=1.0, decay=0.99, mode=gio.ALL_PAIRS)
+    q = QatFitter(to_dev(p), to_dev(tgt)[None].contiguous(), gamma, beta, to_dev(books), lr=1e-4)
+    q.step()
+    torch.cuda.synchronize()
+    assert q.check() == gi.GI_OK
+    assert np.array_equal(q.eff.cpu().numpy().view(np.uint32), ref["eff"].view(np.uint32))
+    errs = group_err(q.grads.cpu().numpy().astype(np.float64), ref["grads"])
+    assert max(errs.values()) <= GRAD_TOL, errs
+    L = q.losses.cpu().numpy().astype(np.float64)
+    assert abs(L[1] - ref["l_rec"]) <= 1e-5 * ref["l_rec"]
+    assert abs(L[2] - ref["l_c"]) <= 1e-6 * ref["l_c"]
+    assert abs(L[0] - ref["loss"]) <= 1e-5 * ref["loss"]
+    dq = np.concatenate([ref["dgamma"], ref["dbeta"]])
+    assert np.allclose(L[3:], dq, rtol=1e-4, atol=1e-9 * np.abs(dq).max())
+    got = q.params.cpu().numpy().astype(np.float64)
+    g = ref["grads"]
+    big = np.abs(g) > 1e-3 * np.sqrt(np.mean(g ** 2, axis=0, keepdims=True))
+    assert np.all(np.abs(got - ref["params"])[big] <= 1e-6 * np.abs(ref["params"])[big] + 1e-9)
+    assert np.allclose(q.books.cpu().numpy(), ref["state"]["books"], atol=1e-6)
+    assert np.allclose(q.ema_n.cpu().numpy(), ref["state"]["ema_n"], rtol=1e-6)
+    assert np.allclose(q.ema_s.cpu().numpy(), ref["state"]["ema_s"], atol=1e-6)
+    # a captured graph of QAT steps keeps running and the loss falls
+    q.capture(10)
+    for _ in range(5):
+        q.replay()
+    torch.cuda.synchronize()
+    assert q.check() == gi.GI_OK and float(q.losses[0]) < ref["loss"]
