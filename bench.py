@@ -382,6 +382,52 @@ def main():
         raise RuntimeError("adan fit status")
     del afit, ag
 
+    # ---------------- NEXT-2: encoder (gi_vq_encode) and QAT step (gi_qat_step) ------------
+    from paper_2403_08551_b200.pipeline import QatFitter
+    fp = torch.from_numpy(synth.fitted_params(seed, N_GAUSS)).to(dev).contiguous()
+    qgamma, qbeta = [0.05, 0.04, 0.05], [-1.0, -1.2, -1.0]
+    qbooks = torch.from_numpy(np.random.default_rng(seed).normal(0, 0.3, (2, 8, 3))
+                              .astype(np.float32)).to(dev)
+    emeta = gi.codec_meta(N_GAUSS, qgamma, qbeta, qbooks)
+    epay = torch.zeros((N_GAUSS * 56 + 7) // 8 + 16, dtype=torch.uint8, device=dev)
+    eeff = torch.zeros(N_GAUSS, 8, dtype=torch.float32, device=dev)
+    gi.gi_vq_encode(fp, emeta, epay, eeff)
+    es = torch.cuda.Stream(device=dev)
+    es.wait_stream(stream)
+    eg = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(eg, stream=es):
+        gi.gi_vq_encode(fp, emeta, epay, eeff, stream=es)
+    stream.wait_stream(es)
+    for _ in range(Wm):
+        eg.replay()
+    barrier()
+    for i in range(K):
+        flush.zero_()
+        s_ev[i].record(stream)
+        eg.replay()
+        e_ev[i].record(stream)
+    barrier()
+    enc_ms = max_over_ranks(sum(s_ev[i].elapsed_time(e_ev[i]) for i in range(K)))
+    encode_fps = world * K / (enc_ms / 1000.0)
+    qfit = QatFitter(fp.clone(), target, qgamma, qbeta, qbooks)
+    qfit.step()
+    torch.cuda.synchronize(dev)
+    qg = qfit.capture(1)
+    for _ in range(Wm):
+        qg.replay()
+    barrier()
+    for i in range(K):
+        flush.zero_()
+        s_ev[i].record(stream)
+        qg.replay()
+        e_ev[i].record(stream)
+    barrier()
+    qat_ms = max_over_ranks(sum(s_ev[i].elapsed_time(e_ev[i]) for i in range(K)))
+    qat_its = world * K / (qat_ms / 1000.0)
+    if qfit.check() != gi.GI_OK:
+        raise RuntimeError("qat status")
+    del qfit, qg, eg
+
     # ---------------- batched launch (configs[3] pattern): B images per launch ------------
     batched = None
     if args.batch_images > 1:
@@ -505,6 +551,12 @@ def main():
             "fit_its_adan": adan_value,
             "batched": batched,
             "decode_fps": decode_fps,
+            "encode_fps": encode_fps,
+            "qat_its": qat_its,
+            "next2_note": "encode_fps: gi_vq_encode of 70k fitted records (fp16 positions, "
+                          "6-bit codes, 2x8 RVQ, packed 56-bit records + dequantised params); "
+                          "qat_its: gi_qat_step on the C2 fitted proxy (quantise, fused fit "
+                          "core, straight-through Adam, EMA codebooks)",
             "stage_ms": {"project_count": stage_ms[0], "bin": stage_ms[1],
                          "fused_fwd_bwd": stage_ms[2], "finalize_adam_loss": stage_ms[3]},
             "render_kernel_ms": r_kernel_ms,
