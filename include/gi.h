@@ -214,6 +214,22 @@ gi_status gi_fit_step_chained(float* params, float* grads, float* m, float* v, c
                               int32_t half_every, float beta1, float beta2, float eps, float* loss,
                               uint32_t* status_flags, void* const* stage_events, void* stream);
 
+/* --- NEXT-4: single-image spatial sharding -----------
+ * The gradient half of a fused fit step restricted to the tile rows
+ * [tile_row0, tile_row0 + tile_rows) of every image (tile_rows = 0: all):
+ * project (+ direct binning of the keys in the window) -> fused Eq. 7 + L2 +
+ * App. A backward over the window's tiles -> finalize WITHOUT an optimiser.
+ * grads [B][n][8] out = the window's share of dL/dparams and loss [B] out =
+ * its share of the L2 loss (normalised by the whole image): both are
+ * sums over tiles, so over a partition of the rows they add up to the whole
+ * image's (up to fp32 summation order).  Ranks of a sharded fit all-reduce
+ * grads and loss (NCCL) and apply the same gi_adam_step.  Workspace as
+ * gi_fit_step (gi_fit_workspace_bytes), zero-filled once. */
+gi_status gi_fit_grads(const float* params, float* grads, const float* target, int32_t n,
+                       const gi_frame* f, uint32_t flags, int32_t tile_row0, int32_t tile_rows,
+                       int64_t key_capacity, void* fit_ws, size_t ws_bytes, float* loss,
+                       void* stream);
+
 /* --- fused render of a frame (graph-capturable) ---------------------------
  * project (+ per-tile counts) -> bin -> Eq. 7 render in one call; the per-tile
  * gid ordering of binning happens inside the render kernel.  Same workspace

@@ -310,6 +310,52 @@ static gi_status fit_step_impl(float* params, float* grads, float* m, float* v, 
     return GI_OK;
 }
 
+gi_status gi_fit_grads(const float* params, float* grads, const float* target, int32_t n,
+                       const gi_frame* f, uint32_t flags, int32_t tile_row0, int32_t tile_rows,
+                       int64_t key_capacity, void* fit_ws, size_t ws_bytes, float* loss,
+                       void* stream) {
+    gi_status st;
+    if ((st = check_frame(f)) != GI_OK || (st = check_n(n, f)) != GI_OK) return st;
+    if (!gi::flags_valid(flags)) return invalid("flags");
+    if (key_capacity < 0 || key_capacity >= (1LL << 31)) return invalid("key_capacity");
+    const int TY = gi::tiles_y(f->height);
+    if (tile_rows == 0) {
+        tile_row0 = 0;
+        tile_rows = TY;
+    }
+    if (tile_row0 < 0 || tile_rows < 0 || tile_row0 + tile_rows > TY) return invalid("tile window");
+    if (!fit_ws || ws_bytes < carve_fit(nullptr, n, key_capacity, *f).bytes)
+        return invalid("fit workspace too small");
+    if (!target || (n > 0 && (!params || !grads))) return invalid("NULL buffer");
+    if (!aligned16(params) || !aligned16(grads) || !aligned16(fit_ws)) return invalid("alignment");
+    FitWs w = carve_fit(fit_ws, n, key_capacity, *f);
+    cudaStream_t s = S(stream);
+    cudaError_t e;
+#define GI_TRY(expr, where) \
+    if ((e = (expr)) != cudaSuccess) return cuda_status(e, where)
+    const int r0 = tile_row0, r1 = tile_row0 + tile_rows;
+    uint32_t* gauss_off = gi::backward_gauss_off(w.bwd_ws, n, key_capacity, *f);
+    gi::BinCounts bc = gi::bin_counts_direct(w.bin_ws, n, key_capacity, *f, w.key_gid, gauss_off);
+    bc.row0 = r0;
+    bc.row1 = r1;
+    gi::ChainState cs = gi::bin_chain_direct(w.bin_ws, n, key_capacity, *f, w.key_gid, gauss_off,
+                                             w.n_keys, nullptr);
+    cs.row0 = r0;
+    cs.row1 = r1;
+    GI_TRY(gi::launch_project(params, n, *f, flags, w.proj, w.touched, gi::ProjectFuse{nullptr, bc},
+                              s),
+           "gi_fit_grads/project");
+    if (tile_rows > 0)
+        GI_TRY(gi::launch_backward_tiles(w.proj, w.key_gid, nullptr, n, *f, false, nullptr, target,
+                                         key_capacity, w.bwd_ws, nullptr, cs, s),
+               "gi_fit_grads/backward");
+    GI_TRY(gi::launch_backward_finalize(params, w.proj, n, *f, flags, true, key_capacity, w.bwd_ws,
+                                        grads, loss, nullptr, s, r0, r1),
+           "gi_fit_grads/finalize");
+#undef GI_TRY
+    return GI_OK;
+}
+
 gi_status gi_fit_step(float* params, float* grads, float* m, float* v, const float* target,
                       int32_t n, const gi_frame* f, uint32_t flags, int64_t key_capacity,
                       void* fit_ws, size_t ws_bytes, uint32_t* step_counter, float lr0,

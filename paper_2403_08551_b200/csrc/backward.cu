@@ -69,7 +69,7 @@ __global__ void __launch_bounds__(256, GI_TILE_MINB) backward_tile_kernel(
     float* __restrict__ ovf, unsigned long long* __restrict__ sse_acc, float* __restrict__ image_out,
     ChainState cs) {
     __shared__ BwdShared sh;
-    const TileCtx t = make_tile_ctx(W, H, TX);
+    const TileCtx t = make_tile_ctx(W, H, TX, cs.row1 > 0 ? cs.row0 : 0);
     griddep_wait();
     griddep_trigger();
     const Seg sg = open_segment(proj, key_gid, tile_range, presorted, cs, n, T, t, sh.sl,
@@ -359,7 +359,7 @@ __global__ void __launch_bounds__(256) finalize_kernel(
     const float* __restrict__ partial, float* __restrict__ ovf, float4* __restrict__ grads,
     FusedAdam adam,
     unsigned long long* __restrict__ sse_acc, int batch, double inv_count,
-    float* __restrict__ loss) {
+    float* __restrict__ loss, int row0, int row1) {
     griddep_wait();
     griddep_trigger();
     const int g = blockIdx.x * blockDim.x + threadIdx.x;
@@ -399,8 +399,10 @@ __global__ void __launch_bounds__(256) finalize_kernel(
         const int y0 = (int)(by & 0xffffu), y1 = (int)(by >> 16);
         float S[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
         bool any = false;
-        if (x0 <= x1 && y0 <= y1) {
-            const uint32_t cnt = (uint32_t)((x1 / kTile - x0 / kTile + 1) * (y1 / kTile - y0 / kTile + 1));
+        // tiles of the (window-clipped, NEXT-4) rectangle
+        const uint32_t cnt =
+            rect_area(window_rect(make_int4(x0 / kTile, x1 / kTile, y0 / kTile, y1 / kTile), row0, row1));
+        if (x0 <= x1 && y0 <= y1 && cnt > 0u) {
             auto add = [&](const float4 a, const float4 b) {
                 S[0] += a.x; S[1] += a.y; S[2] += a.z; S[3] += a.w;
                 S[4] += b.x; S[5] += b.y; S[6] += b.z; S[7] += b.w;
@@ -517,7 +519,9 @@ __global__ void __launch_bounds__(256) finalize_kernel(
         }
     }
     if (adam.m != nullptr && adam.proj_out != nullptr && adam.counts.tile_count != nullptr) {
-        const int TX = (W + kTile - 1) / kTile, T = TX * ((H + kTile - 1) / kTile);
+        const int TX = (W + kTile - 1) / kTile;
+        const int T = TX * (adam.counts.row1 > 0 ? adam.counts.row1 - adam.counts.row0
+                                                  : (H + kTile - 1) / kTile);
         post_project_warp(adam.counts, touched, rect, g, g < total ? (g / n_per_image) * T : 0, TX,
                           total);
     }
@@ -597,11 +601,14 @@ cudaError_t launch_backward_tiles(const Proj* proj, uint32_t* key_gid, const uin
                                   void* ws, float* image_out, const ChainState& cs,
                                   cudaStream_t s) {
     BwdWs w = carve(ws, n, cap, f);
-    const int TX = tiles_x(f.width), T = TX * tiles_y(f.height);
+    const int TX = tiles_x(f.width);
+    const int rows = cs.row1 > 0 ? cs.row1 - cs.row0 : tiles_y(f.height);   // NEXT-4 window
+    const int T = TX * rows;
     const double count = 3.0 * (double)f.width * (double)f.height;
     const float norm = (float)(2.0 / count);
     const bool mse = dL_dimage == nullptr;
-    cudaError_t e = launch_pdl(backward_tile_kernel, dim3(TX, T / TX, f.batch), dim3(256), s, proj,
+    if (rows <= 0) return cudaSuccess;
+    cudaError_t e = launch_pdl(backward_tile_kernel, dim3(TX, rows, f.batch), dim3(256), s, proj,
                                key_gid,
                                tile_range, (const uint32_t*)w.gauss_off, n, f.width, f.height, T,
                                TX, presorted, dL_dimage, target, norm, partial_cap(n, cap, f), w.partial, w.ovf,
@@ -613,7 +620,7 @@ cudaError_t launch_backward_tiles(const Proj* proj, uint32_t* key_gid, const uin
 cudaError_t launch_backward_finalize(const float* params, const Proj* proj, int n,
                                      const gi_frame& f, uint32_t flags, bool mse, int64_t cap,
                                      void* ws, float* grads, float* loss, const FusedAdam* adam,
-                                     cudaStream_t s) {
+                                     cudaStream_t s, int row0, int row1) {
     BwdWs w = carve(ws, n, cap, f);
     const double count = 3.0 * (double)f.width * (double)f.height;
     const int total = n * f.batch;
@@ -625,7 +632,8 @@ cudaError_t launch_backward_finalize(const float* params, const Proj* proj, int 
                        reinterpret_cast<const float4*>(params), proj, (const uint32_t*)w.gauss_off,
                        total, n, f.width, f.height, flags, partial_cap(n, cap, f),
                        (const float*)w.partial, w.ovf, reinterpret_cast<float4*>(grads), fa,
-                       mse ? w.sse_acc : nullptr, f.batch, 1.0 / count, mse ? loss : nullptr);
+                       mse ? w.sse_acc : nullptr, f.batch, 1.0 / count, mse ? loss : nullptr, row0,
+                       row1 > 0 ? row1 : tiles_y(f.height));
         note_launches(1);
         if ((e = cudaGetLastError()) != cudaSuccess) return e;
     } else if (mse) {

@@ -153,7 +153,20 @@ struct BinCounts {
     uint32_t* gauss_off;    // direct binning + backward: partial slots of > 4-tile Gaussians
     uint32_t* alloc_counter;
     uint32_t part_cap;      // partial slots in all (4 total fixed + the allocatable rest)
+    int row0, row1;         // NEXT-4 tile-row window [row0, row1); row1 = 0: whole image
 };
+
+// NEXT-4: a rank of a spatially sharded fit owns the tile rows [r0, r1).  A
+// Gaussian's tile rectangle (x0, x1, y0, y1 in tiles) clipped to the window,
+// rows made relative to r0; empty -> (0, -1, 0, -1).
+__host__ __device__ inline int4 window_rect(int4 rect, int r0, int r1) {
+    const int z = rect.z > r0 ? rect.z : r0, w = rect.w < r1 - 1 ? rect.w : r1 - 1;
+    if (rect.x > rect.y || z > w) return make_int4(0, -1, 0, -1);
+    return make_int4(rect.x, rect.y, z - r0, w - r0);
+}
+__host__ __device__ inline uint32_t rect_area(int4 r) {
+    return (r.x > r.y || r.z > r.w) ? 0u : (uint32_t)((r.y - r.x + 1) * (r.w - r.z + 1));
+}
 
 // gauss_off value of a > 4-tile Gaussian whose slots did not fit: its tiles
 // add their partial sums atomically into a per-Gaussian accumulator instead.
@@ -260,6 +273,7 @@ struct ChainState {
     uint32_t* n_keys;
     uint32_t* n_keys_acc;
     uint32_t* step_counter;   // chained fit: incremented once by the consumer
+    int row0, row1;           // NEXT-4 tile-row window (row1 = 0: whole image)
     // fused Adam: the consumer's CTA 0 turns the step t (after the increment)
     // into {lr_t, 1 / (1 - b1^t), 1 / (1 - b2^t)} for the finalize kernel
     float* adam_consts;
@@ -320,10 +334,12 @@ struct FusedAdam {
     float k;
     uint32_t pos_flags;
 };
+// row0/row1: the NEXT-4 tile-row window the partials came from (row1 = 0:
+// whole image).
 cudaError_t launch_backward_finalize(const float* params, const Proj* proj, int n,
                                      const gi_frame& f, uint32_t flags, bool mse, int64_t cap,
                                      void* ws, float* grads, float* loss, const FusedAdam* adam,
-                                     cudaStream_t s);
+                                     cudaStream_t s, int row0 = 0, int row1 = 0);
 cudaError_t launch_adam(float* params, const float* grads, float* m, float* v, int64_t count,
                         int step, const uint32_t* step_dev, float lr, int half_every, float b1,
                         float b2, float eps, uint32_t* flag, cudaStream_t s);

@@ -33,7 +33,9 @@ __global__ void __launch_bounds__(256) project_kernel(const float4* __restrict__
         tiles_touched[g] = touched;
     }
     if (fuse.counts.tile_count != nullptr) {
-        const int TX = (W + kTile - 1) / kTile, T = TX * ((H + kTile - 1) / kTile);
+        const int TX = (W + kTile - 1) / kTile;
+        const int T = TX * (fuse.counts.row1 > 0 ? fuse.counts.row1 - fuse.counts.row0
+                                                 : (H + kTile - 1) / kTile);
         post_project_warp(fuse.counts, touched, rect, g, g < total ? (g / n) * T : 0, TX, total);
     }
 }

@@ -97,13 +97,17 @@ __device__ __forceinline__ uint32_t project_one(const float4 p0, const float4 p1
                                                 Proj* __restrict__ proj, const BinCounts& bc,
                                                 int4& rect) {
     Proj r;
-    const uint32_t touched = project_rec(activate_pos(p0.x, flags), activate_pos(p0.y, flags), p0,
-                                         p1, W, H, k, flags, r, rect);
-    if (touched > 0u && bc.tile_count != nullptr) {   // fused binning step 1: counts and ranks
-        const int TX = (W + kTile - 1) / kTile;
-        const int T = TX * ((H + kTile - 1) / kTile);
-        count_keys(bc, g, rect.x, rect.y, rect.z, rect.w, touched, (g / n) * T, TX);
+    uint32_t touched = project_rec(activate_pos(p0.x, flags), activate_pos(p0.y, flags), p0, p1, W,
+                                   H, k, flags, r, rect);
+    const int TX = (W + kTile - 1) / kTile;
+    int TW = TX * ((H + kTile - 1) / kTile);
+    if (bc.row1 > 0) {                 // NEXT-4 window: count only the rank's tile rows
+        rect = window_rect(rect, bc.row0, bc.row1);
+        touched = rect_area(rect);
+        TW = TX * (bc.row1 - bc.row0);
     }
+    if (touched > 0u && bc.tile_count != nullptr)   // fused binning step 1: counts and ranks
+        count_keys(bc, g, rect.x, rect.y, rect.z, rect.w, touched, (g / n) * TW, TX);
     proj[g] = r;
     return touched;
 }

@@ -40,16 +40,20 @@ struct TileCtx {
     float cx, cy;                 // tile-local pixel centre (x + 1/2 - 16 tx)
     int wx0, wy0;                 // warp block origin (global pixels)
     int csh, rsh;                 // warp block: column / row shift in the tile masks
+    int row0, row1;               // tile-row window of the launch (NEXT-4); tile = relative index
     bool in_image;
 };
 
-// Grid: (tiles_x, tiles_y, images) -- no integer division per CTA.
-__device__ __forceinline__ TileCtx make_tile_ctx(int W, int H, int TX) {
+// Grid: (tiles_x, window rows, images) -- no integer division per CTA.  The
+// CTA's tile row is row0 + blockIdx.y; `tile` indexes the window.
+__device__ __forceinline__ TileCtx make_tile_ctx(int W, int H, int TX, int row0) {
     TileCtx c;
     c.tx = blockIdx.x;
-    c.ty = blockIdx.y;
+    c.ty = row0 + blockIdx.y;
     c.img = blockIdx.z;
-    c.tile = c.ty * TX + c.tx;
+    c.tile = blockIdx.y * TX + c.tx;
+    c.row0 = row0;
+    c.row1 = row0 + gridDim.y;
     c.lane = threadIdx.x & 31;
     c.warp = threadIdx.x >> 5;
     const int lx = (c.warp & 1) * 8 + (c.lane & 7);
@@ -107,12 +111,14 @@ __device__ __forceinline__ void stage_gid(StagedRecords& sr, const Proj* __restr
     const int ly0 = max(y0 - ty0, 0), ly1 = min(y1 - ty0, kTile - 1);
     uint32_t slot = 0;
     if (gauss_off != nullptr) {
-        // slots 4 gid.. for Gaussians touching <= 4 tiles (bin.cu scatter)
-        const int rtx0 = x0 / kTile, rtx1 = x1 / kTile, rty0 = y0 / kTile, rty1 = y1 / kTile;
-        const int rw = rtx1 - rtx0 + 1;
-        const uint32_t off = rw * (rty1 - rty0 + 1) <= 4 ? 4u * gid : gauss_off[gid];
-        slot = off == kOffOverflow ? kOffOverflow
-                                   : off + (uint32_t)((t.ty - rty0) * rw + (t.tx - rtx0));
+        // slots 4 gid.. for Gaussians touching <= 4 tiles of the window, the
+        // rank of this tile in the (window-clipped) rectangle, row-major
+        const int4 rw = window_rect(make_int4(x0 / kTile, x1 / kTile, y0 / kTile, y1 / kTile),
+                                    t.row0, t.row1);
+        const uint32_t off = rect_area(rw) <= 4u ? 4u * gid : gauss_off[gid];
+        slot = off == kOffOverflow
+                   ? kOffOverflow
+                   : off + (uint32_t)((t.ty - t.row0 - rw.z) * (rw.y - rw.x + 1) + (t.tx - rw.x));
     }
     sr.a[j] = make_float4(r.q1.x, r.q1.y, r.q1.z, r.q2.x);
     sr.b[j] = make_float4(r.q2.y, r.q2.z, mx, my);

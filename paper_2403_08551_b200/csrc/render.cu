@@ -28,7 +28,7 @@ __global__ void __launch_bounds__(256, GI_RENDER_MINB) render_kernel(const Proj*
                                                      bool presorted, float* __restrict__ image,
                                                      ChainState cs) {
     __shared__ RenderShared sh;
-    const TileCtx t = make_tile_ctx(W, H, TX);
+    const TileCtx t = make_tile_ctx(W, H, TX, cs.row1 > 0 ? cs.row0 : 0);
     griddep_wait();
     griddep_trigger();
     // presorted: the segment comes from gi_bin (already in gid order); else it
@@ -60,8 +60,11 @@ __global__ void __launch_bounds__(256, GI_RENDER_MINB) render_kernel(const Proj*
 cudaError_t launch_render(const Proj* proj, uint32_t* key_gid, const uint32_t* tile_range, int n,
                           const gi_frame& f, bool presorted, float* image, const ChainState& cs,
                           cudaStream_t s) {
-    const int TX = tiles_x(f.width), T = TX * tiles_y(f.height);
-    cudaError_t e = launch_pdl(render_kernel, dim3(TX, T / TX, f.batch), dim3(256), s, proj, key_gid,
+    const int TX = tiles_x(f.width);
+    const int rows = cs.row1 > 0 ? cs.row1 - cs.row0 : tiles_y(f.height);   // NEXT-4 window
+    const int T = TX * rows;
+    if (rows <= 0) return cudaSuccess;
+    cudaError_t e = launch_pdl(render_kernel, dim3(TX, rows, f.batch), dim3(256), s, proj, key_gid,
                                tile_range, n, f.width, f.height, T, TX, presorted, image, cs);
     note_launches(1);
     return e;

@@ -1,4 +1,5 @@
-"""Image-batch data parallelism (SURVEY §8(e), configs[3]).
+"""Multi-GPU plumbing: image-batch data parallelism (SURVEY §8(e),
+configs[3]) and single-image spatial sharding (NEXT-4, §8(f)).
 
 Independent image fits shard naturally: rank r of G takes images
 {r, r + G, ...} and fits them batched in ONE launch per stage (image index in
@@ -78,6 +79,86 @@ def fit_sharded(n_images: int, steps: int, n_gauss: int, width: int, height: int
         img = pipe.render_frame(fit.params)
         local_psnr = pipe.psnr(img, fit.target).clone()
     return gather_psnr(local_psnr, n_images, world, rank), mine
+
+
+# ------------------------------------------------------------------ NEXT-4
+def row_windows(tile_rows: int, world: int) -> list[tuple[int, int]]:
+    """Contiguous tile-row windows (row0, rows) of one image, one per rank,
+    covering [0, tile_rows) exactly once, sizes differing by at most one."""
+    if world < 1:
+        raise ValueError("world")
+    base, extra = divmod(int(tile_rows), world)
+    out, r0 = [], 0
+    for r in range(world):
+        rows = base + (1 if r < extra else 0)
+        out.append((r0, rows))
+        r0 += rows
+    return out
+
+
+class SpatialFitter:
+    """Single-image spatial sharding (NEXT-4): every rank holds all Gaussians
+    (replicated params and Adam state), renders and back-propagates only its
+    tile rows (gi_fit_grads), the per-Gaussian gradients and the loss are
+    summed across ranks (the one real exchange of the path: NCCL all_reduce on
+    GPUs, gloo in the CPU tests), and every rank applies the same Adam update
+    (gi_adam_step), so the replicas stay bit-identical.
+
+    grad_fn(params, row0, rows) -> (grads, loss) may replace the libgi call
+    (CPU tests of the collective plumbing)."""
+
+    def __init__(self, params: torch.Tensor, target: torch.Tensor, rank: int = 0, world: int = 1,
+                 k: float = 3.0, key_capacity: int | None = None, lr0: float = 1e-3,
+                 half_every: int = 20000, grad_fn=None, flags: int = 0):
+        self.rank, self.world = int(rank), int(world)
+        self.params = params.contiguous()
+        self.target = target.contiguous()
+        self.grads = torch.zeros_like(self.params)
+        self.m = torch.zeros_like(self.params)
+        self.v = torch.zeros_like(self.params)
+        self.loss = torch.zeros(1, dtype=torch.float32, device=self.params.device)
+        self.t = 0
+        self.lr0, self.half_every = lr0, half_every
+        H, W = target.shape[-2], target.shape[-1]
+        self.n = self.params.shape[-2]
+        self.window = row_windows((H + 15) // 16, self.world)[self.rank]
+        self.grad_fn = grad_fn
+        self.flags = flags
+        if grad_fn is None:
+            from . import gi
+            from .pipeline import _bytes, default_capacity
+            self.gi = gi
+            self.f = gi.frame(W, H, 1, k)
+            self.cap = int(key_capacity) if key_capacity else default_capacity(self.n, 1)
+            self.ws = _bytes(gi.gi_fit_workspace_bytes(self.n, self.cap, self.f), self.params.device)
+
+    def local_grads(self):
+        r0, rows = self.window
+        if self.grad_fn is not None:
+            g, l = self.grad_fn(self.params, r0, rows)
+            self.grads.copy_(g)
+            self.loss.copy_(l)
+            return
+        self.gi.gi_fit_grads(self.params, self.grads, self.target, self.n, self.f, self.flags, r0,
+                             rows, self.cap, self.ws, self.loss)
+
+    def step(self):
+        self.local_grads()
+        if self.world > 1:
+            dist.all_reduce(self.grads, op=dist.ReduceOp.SUM)
+            dist.all_reduce(self.loss, op=dist.ReduceOp.SUM)
+        self.t += 1
+        lr = self.lr0 * 0.5 ** ((self.t - 1) // self.half_every)
+        if self.grad_fn is not None:          # CPU plumbing test: the textbook update
+            b1, b2, eps = 0.9, 0.999, 1e-8
+            self.m.mul_(b1).add_(self.grads, alpha=1 - b1)
+            self.v.mul_(b2).addcmul_(self.grads, self.grads, value=1 - b2)
+            mh = self.m / (1 - b1 ** self.t)
+            vh = self.v / (1 - b2 ** self.t)
+            self.params.sub_(lr * mh / (vh.sqrt() + eps))
+        else:
+            self.gi.gi_adam_step(self.params, self.grads, self.m, self.v, self.params.numel(),
+                                 self.t, lr)
 
 
 if __name__ == "__main__":

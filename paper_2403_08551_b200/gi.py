@@ -74,6 +74,8 @@ SIGNATURES = {
     "gi_lr_at": (_f64, [_i32, _f64, _i32]),
     "gi_fit_workspace_bytes": (_sz, [_i32, _i64, _FP]),
     "gi_fit_n_keys": (_vp, [_vp, _i32, _i64, _FP]),
+    "gi_fit_grads": (C.c_int, [_vp, _vp, _vp, C.c_int32, C.POINTER(gi_frame), C.c_uint32, C.c_int32,
+                               C.c_int32, C.c_int64, _vp, _sz, _vp, _vp]),
     "gi_fit_step": (C.c_int, [_vp, _vp, _vp, _vp, _vp, _i32, _FP, _u32, _i64, _vp, _sz, _vp,
                               _f32, _i32, _f32, _f32, _f32, _vp, _vp, _vp, _vp]),
     "gi_launch_count": (_i64, []),
@@ -325,6 +327,15 @@ def gi_qat_step(params, m, v, eff, grads, qparams, qm, qv, books, ema_n, ema_s, 
                            C.byref(cfg), int(key_capacity), _ptr(ws), ws.numel() * ws.element_size(),
                            _ptr(step_counter), _ptr(losses), _ptr(status_flags), _stream(stream)),
         "gi_qat_step")
+
+
+def gi_fit_grads(params, grads, target, n, f: gi_frame, flags, tile_row0, tile_rows, key_capacity,
+                 fit_ws, loss, stream=None):
+    """NEXT-4: gradient half of a fit step over a tile-row window (see gi.h)."""
+    _ok(load().gi_fit_grads(_ptr(params), _ptr(grads), _ptr(target), int(n), C.byref(f),
+                            int(flags), int(tile_row0), int(tile_rows), int(key_capacity),
+                            _ptr(fit_ws), fit_ws.numel() * fit_ws.element_size(), _ptr(loss),
+                            _stream(stream)), "gi_fit_grads")
 
 
 def gi_vq_decode(payload, meta: gi_codec_meta, params, stream=None):

@@ -662,3 +662,56 @@ def test_qat_step_parity(gi, gio):
         q.replay()
     torch.cuda.synchronize()
     assert q.check() == gi.GI_OK and float(q.losses[0]) < ref["loss"]
+
+
+@pytest.mark.parametrize("parts", [2, 3])
+def test_spatial_windows_sum_to_whole(gi, gio, parts):
+    # NEXT-4: gradients and loss of tile-row windows covering the image add up
+    # to the whole image's (and to the oracle's); the ranks of a sharded fit
+    # are simulated one after another on this GPU
+    from paper_2403_08551_b200.dist import row_windows
+    from paper_2403_08551_b200.pipeline import _bytes, default_capacity
+    W, H, n = 96, 80, 700
+    p = params_for(n, 5, True)
+    tgt = synth.image(5, W, H)
+    _, loss, g = gio.loss_and_grads(p, tgt, mode=gio.ALL_PAIRS)
+    f = gi.frame(W, H, 1)
+    cap = default_capacity(n, 1)
+    ws = _bytes(gi.gi_fit_workspace_bytes(n, cap, f), DEV)
+    pd, td = to_dev(p)[None].contiguous(), to_dev(tgt)[None].contiguous()
+    acc = torch.zeros(1, n, 8, dtype=torch.float64, device=DEV)
+    lsum = 0.0
+    for (r0, rows) in row_windows(H // 16, parts):
+        gr = torch.zeros(1, n, 8, dtype=torch.float32, device=DEV)
+        lo = torch.zeros(1, dtype=torch.float32, device=DEV)
+        gi.gi_fit_grads(pd, gr, td, n, f, 0, r0, rows, cap, ws, lo)
+        torch.cuda.synchronize()
+        acc += gr.double()
+        lsum += float(lo[0])
+    whole = torch.zeros(1, n, 8, dtype=torch.float32, device=DEV)
+    lw = torch.zeros(1, dtype=torch.float32, device=DEV)
+    gi.gi_fit_grads(pd, whole, td, n, f, 0, 0, 0, cap, ws, lw)
+    torch.cuda.synchronize()
+    a = acc[0].cpu().numpy()
+    assert max(group_err(a, whole[0].cpu().numpy().astype(np.float64)).values()) <= 1e-6
+    assert max(group_err(a, g).values()) <= GRAD_TOL
+    assert abs(lsum - float(lw[0])) <= 1e-6 * float(lw[0])
+    assert abs(lsum - loss) <= 1e-5 * loss
+
+
+def test_spatial_fitter_single_rank(gi, gio):
+    # NEXT-4 driver with one rank = gi_fit_grads + gi_adam_step: follows the
+    # fused fit step (same Adam up to its approximate reciprocal / sqrt)
+    from paper_2403_08551_b200.dist import SpatialFitter
+    from paper_2403_08551_b200.pipeline import Fitter
+    W, H, n = 64, 64, 256
+    p = synth.init_params(0, n)
+    tgt = synth.image(0, W, H)
+    a = SpatialFitter(to_dev(p)[None].contiguous(), to_dev(tgt)[None].contiguous())
+    b = Fitter(to_dev(p)[None].contiguous(), to_dev(tgt)[None].contiguous(), chained=False)
+    for _ in range(3):
+        a.step()
+        b.step()
+    torch.cuda.synchronize()
+    assert torch.allclose(a.params, b.params, rtol=1e-5, atol=1e-7)
+    assert abs(float(a.loss[0]) - float(b.loss[0])) <= 1e-5 * float(b.loss[0])
