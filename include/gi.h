@@ -216,7 +216,9 @@ gi_status gi_fit_step_chained(float* params, float* grads, float* m, float* v, c
 
 /* --- NEXT-4: single-image spatial sharding -----------
  * The gradient half of a fused fit step restricted to the tile rows
- * [tile_row0, tile_row0 + tile_rows) of every image (tile_rows = 0: all):
+ * [tile_row0, tile_row0 + tile_rows) of every image (tile_rows < 0: all;
+ * tile_rows = 0: an empty window -- zero grads and loss, as for a rank that
+ * owns no rows):
  * project (+ direct binning of the keys in the window) -> fused Eq. 7 + L2 +
  * App. A backward over the window's tiles -> finalize WITHOUT an optimiser.
  * grads [B][n][8] out = the window's share of dL/dparams and loss [B] out =

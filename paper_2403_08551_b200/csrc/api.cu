@@ -319,11 +319,11 @@ gi_status gi_fit_grads(const float* params, float* grads, const float* target, i
     if (!gi::flags_valid(flags)) return invalid("flags");
     if (key_capacity < 0 || key_capacity >= (1LL << 31)) return invalid("key_capacity");
     const int TY = gi::tiles_y(f->height);
-    if (tile_rows == 0) {
+    if (tile_rows < 0) {
         tile_row0 = 0;
         tile_rows = TY;
     }
-    if (tile_row0 < 0 || tile_rows < 0 || tile_row0 + tile_rows > TY) return invalid("tile window");
+    if (tile_row0 < 0 || tile_row0 + tile_rows > TY) return invalid("tile window");
     if (!fit_ws || ws_bytes < carve_fit(nullptr, n, key_capacity, *f).bytes)
         return invalid("fit workspace too small");
     if (!target || (n > 0 && (!params || !grads))) return invalid("NULL buffer");
@@ -333,6 +333,13 @@ gi_status gi_fit_grads(const float* params, float* grads, const float* target, i
     cudaError_t e;
 #define GI_TRY(expr, where) \
     if ((e = (expr)) != cudaSuccess) return cuda_status(e, where)
+    if (tile_rows == 0) {             // empty window: this rank contributes nothing
+        if (n > 0)
+            GI_TRY(cudaMemsetAsync(grads, 0, sizeof(float) * 8 * (size_t)n * f->batch, s),
+                   "gi_fit_grads/zero");
+        if (loss) GI_TRY(cudaMemsetAsync(loss, 0, sizeof(float) * f->batch, s), "gi_fit_grads/zero");
+        return GI_OK;
+    }
     const int r0 = tile_row0, r1 = tile_row0 + tile_rows;
     uint32_t* gauss_off = gi::backward_gauss_off(w.bwd_ws, n, key_capacity, *f);
     gi::BinCounts bc = gi::bin_counts_direct(w.bin_ws, n, key_capacity, *f, w.key_gid, gauss_off);

@@ -57,6 +57,27 @@ def test_host_queries_and_validation(lib):
     meta.bits = 6
     assert lib.gi_vq_decode(None, 69, C.byref(meta), None, None) == gi.GI_EFORMAT  # needs 70 B
     assert lib.gi_status_string(3) == b"GI_ECAPACITY"
+    # NEXT-2 / NEXT-4 entry points validate before any launch
+    meta.bits = 20
+    assert lib.gi_vq_encode(None, 0, C.byref(meta), None, 0, None, None) == gi.GI_EFORMAT
+    meta.bits = 6
+    fake = C.c_void_p(256)                  # never dereferenced: validation comes first
+    assert lib.gi_vq_encode(fake, 0, C.byref(meta), fake, 69, None, None) == gi.GI_EFORMAT
+    assert lib.gi_vq_encode(None, 2, C.byref(meta), None, 0, None, None) == gi.GI_EINVAL  # RS flag
+    assert gi.gi_kmeans_workspace_bytes(1) == 0 and gi.gi_kmeans_workspace_bytes(8) == 8 * 32
+    assert lib.gi_kmeans_step(None, 10, 1, None, None, None, 0, None) == gi.GI_EINVAL
+    cfg = gi.qat_config(bits=20)
+    assert gi.gi_qat_workspace_bytes(100, 1 << 16, f, cfg) == 0
+    cfg = gi.qat_config()
+    assert gi.gi_qat_workspace_bytes(100, 1 << 16, f, cfg) > gi.gi_fit_workspace_bytes(100, 1 << 16, f)
+    f2 = gi.frame(768, 512, batch=2)
+    rc = lib.gi_qat_step(*([None] * 12), 10, C.byref(f2), C.byref(cfg), 1 << 16, None, 0, None,
+                         None, None, None)
+    assert rc == gi.GI_EINVAL and b"batch 1" in lib.gi_last_error()
+    rc = lib.gi_fit_grads(None, None, None, 10, C.byref(f), 0, 30, 5, 1 << 16, None, 0, None, None)
+    assert rc == gi.GI_EINVAL and b"tile window" in lib.gi_last_error()
+    rc = lib.gi_fit_grads(None, None, None, 10, C.byref(f), 0, -1, 0, 1 << 16, None, 0, None, None)
+    assert rc == gi.GI_EINVAL and b"tile window" in lib.gi_last_error()
 
 
 def test_product_package_does_not_import_oracle():

@@ -690,7 +690,7 @@ def test_spatial_windows_sum_to_whole(gi, gio, parts):
         lsum += float(lo[0])
     whole = torch.zeros(1, n, 8, dtype=torch.float32, device=DEV)
     lw = torch.zeros(1, dtype=torch.float32, device=DEV)
-    gi.gi_fit_grads(pd, whole, td, n, f, 0, 0, 0, cap, ws, lw)
+    gi.gi_fit_grads(pd, whole, td, n, f, 0, 0, -1, cap, ws, lw)
     torch.cuda.synchronize()
     a = acc[0].cpu().numpy()
     assert max(group_err(a, whole[0].cpu().numpy().astype(np.float64)).values()) <= 1e-6
@@ -715,3 +715,42 @@ def test_spatial_fitter_single_rank(gi, gio):
     torch.cuda.synchronize()
     assert torch.allclose(a.params, b.params, rtol=1e-5, atol=1e-7)
     assert abs(float(a.loss[0]) - float(b.loss[0])) <= 1e-5 * float(b.loss[0])
+
+
+def test_next_edge_cases(gi, gio):
+    # NEXT-2/4 entry points on empty and tiny inputs
+    from paper_2403_08551_b200.pipeline import QatFitter, _bytes, default_capacity
+    books = to_dev(np.zeros((2, 8, 3), np.float32))
+    meta = gi.codec_meta(0, [0.1] * 3, [0.0] * 3, books)
+    gi.gi_vq_encode(torch.zeros(1, 8, device=DEV), meta,
+                    torch.zeros(8, dtype=torch.uint8, device=DEV), torch.zeros(1, 8, device=DEV))
+    ws = torch.zeros(gi.gi_kmeans_workspace_bytes(8), dtype=torch.uint8, device=DEV)
+    cent = to_dev(np.arange(24, dtype=np.float32).reshape(8, 3))
+    gi.gi_kmeans_step(torch.zeros(0, 3, device=DEV), cent, None, ws)
+    torch.cuda.synchronize()
+    assert torch.equal(cent.cpu(), torch.arange(24, dtype=torch.float32).view(8, 3))
+    # one Gaussian: QAT step against the oracle
+    p = synth.fitted_params(2, 1)
+    tgt = synth.image(2, 20, 12)
+    st = dict(m=np.zeros((1, 8), np.float32), v=np.zeros((1, 8), np.float32),
+              gamma=np.float32([0.05] * 3), beta=np.float32([-1.0] * 3),
+              qm=np.zeros(6, np.float32), qv=np.zeros(6, np.float32),
+              books=np.zeros((2, 8, 3), np.float32), ema_n=np.ones((2, 8), np.float32),
+              ema_s=np.zeros((2, 8, 3), np.float32))
+    ref = gio.qat_step(p, tgt, st, 1, 1e-4, mode=gio.ALL_PAIRS)
+    q = QatFitter(to_dev(p), to_dev(tgt)[None].contiguous(), [0.05] * 3, [-1.0] * 3, books)
+    q.step()
+    torch.cuda.synchronize()
+    assert np.array_equal(q.eff.cpu().numpy().view(np.uint32), ref["eff"].view(np.uint32))
+    assert abs(float(q.losses[1]) - ref["l_rec"]) <= 1e-5 * ref["l_rec"]
+    # a zero-row window contributes nothing
+    f = gi.frame(64, 48, 1)
+    pp = to_dev(synth.init_params(3, 100))[None].contiguous()
+    cap = default_capacity(100, 1)
+    fws = _bytes(gi.gi_fit_workspace_bytes(100, cap, f), DEV)
+    gr = torch.ones(1, 100, 8, device=DEV)
+    lo = torch.ones(1, device=DEV)
+    gi.gi_fit_grads(pp, gr, to_dev(synth.image(3, 64, 48))[None].contiguous(), 100, f, 0, 1, 0,
+                    cap, fws, lo)
+    torch.cuda.synchronize()
+    assert not gr.any() and float(lo[0]) == 0.0
