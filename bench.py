@@ -283,7 +283,7 @@ def main():
     fit_ms_max = max_over_ranks(fit_ms)
     fit_value = world * K / (fit_ms_max / 1000.0)
     # stage split (instrumented graph, same flush protocol)
-    stage_ms = np.zeros(5)   # project(+count), bin, fused tile kernel, finalize+adam+loss, tail
+    stage_ms = np.zeros(5)   # [empty], [empty], tile kernel, finalize+Adam+next projection, tail
     KS = min(K, 100)
     for i in range(KS):
         flush.zero_()
@@ -583,8 +583,12 @@ def main():
                           "6-bit codes, 2x8 RVQ, packed 56-bit records + dequantised params); "
                           "qat_its: gi_qat_step on the C2 fitted proxy (quantise, fused fit "
                           "core, straight-through Adam, EMA codebooks)",
-            "stage_ms": {"project_count": stage_ms[0], "bin": stage_ms[1],
-                         "fused_fwd_bwd": stage_ms[2], "finalize_adam_loss": stage_ms[3]},
+            "stage_ms": {"tile_kernel_fwd_l2_bwd": stage_ms[2],
+                         "finalize_adam_next_projection_binning": stage_ms[3],
+                         "event_overhead_empty_stages": stage_ms[0] + stage_ms[1],
+                         "note": "chained step = 2 kernels; staged graph with event nodes "
+                                 "(each costs a few us), so the stages add up to more than "
+                                 "ms_per_step"},
             "render_kernel_ms": r_kernel_ms,
             "psnr_db_after_fit_steps": psnrs,
             "roofline": {"kernel": "backward_tile_kernel (fused Eq.7 fwd + L2 + App.A bwd)",
