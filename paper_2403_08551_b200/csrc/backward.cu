@@ -352,48 +352,49 @@ __device__ __forceinline__ float adam1(float p, float g, float& m, float& v, flo
 //   dsigma/ddx = (p - q l2 / l3) / l1,  dsigma/ddy = q / l3,  d = pixel - mu
 //   dsigma/dl1 = -p dsigma/ddx, dsigma/dl2 = -p q / l3, dsigma/dl3 = -q^2 / l3
 // (equal to <dsigma/dSigma, dSigma/dl> of A.2 with the R14 correction).
-__global__ void __launch_bounds__(256) finalize_kernel(
-    const float4* __restrict__ params, const Proj* proj /* may be rewritten (chained) */,
-    const uint32_t* __restrict__ gauss_off, int total, int n_per_image, int W, int H,
-    uint32_t flags, int64_t pcap,
-    const float* __restrict__ partial, float* __restrict__ ovf, float4* __restrict__ grads,
-    FusedAdam adam,
-    unsigned long long* __restrict__ sse_acc, int batch, double inv_count,
-    float* __restrict__ loss, int row0, int row1) {
-    griddep_wait();
-    griddep_trigger();
-    const int g = blockIdx.x * blockDim.x + threadIdx.x;
+// Everything the per-Gaussian finalize needs (the finalize kernel's
+// arguments minus the loss).
+struct FinArgs {
+    const float4* params;
+    const Proj* proj;          // this step's records (the chained step rewrites proj[g] in place)
+    const uint32_t* gauss_off;
+    int total, n_per_image, W, H;
+    uint32_t flags;
+    int64_t pcap;
+    const float* partial;
+    float* ovf;
+    float4* grads;
+    FusedAdam adam;
+    int row0, row1;
+    uint32_t* done;            // fused step: re-zero the Gaussian's tile-completion counter
+};
+
+// Finalize Gaussian g (live = g is a real Gaussian for this thread).  All
+// lanes of the warp must call (the direct-binning tail is warp-cooperative).
+// lr, ibc1, ibc2: the Adam step constants.
+__device__ __forceinline__ void finalize_one(int g, bool live, const FinArgs& a, float lr,
+                                             float ibc1, float ibc2) {
+    const FusedAdam& adam = a.adam;
+    const int W = a.W, H = a.H, n_per_image = a.n_per_image, total = a.total;
+    const uint32_t flags = a.flags;
     // independent loads first (their latency overlaps the partial-sum chain)
     float4 p0 = make_float4(0.f, 0.f, 0.f, 0.f), p1 = p0, m0 = p0, m1 = p0, v0 = p0, v1 = p0;
     Proj r{};
-    const float4* pp = reinterpret_cast<const float4*>(partial);
-    if (g < total) {
-        p0 = params[2 * (size_t)g];
-        p1 = params[2 * (size_t)g + 1];
-        r = proj[g];
+    const float4* pp = reinterpret_cast<const float4*>(a.partial);
+    if (live) {
+        p0 = a.params[2 * (size_t)g];
+        p1 = a.params[2 * (size_t)g + 1];
+        r = a.proj[g];
         if (adam.m != nullptr) {
             const float4* mm = reinterpret_cast<const float4*>(adam.m) + 2 * (size_t)g;
             const float4* vv = reinterpret_cast<const float4*>(adam.v) + 2 * (size_t)g;
             m0 = mm[0]; m1 = mm[1]; v0 = vv[0]; v1 = vv[1];
         }
-    }
-    float lr = 0.f, ibc1 = 0.f, ibc2 = 0.f;
-    if (adam.m != nullptr) {
-        lr = adam.consts[0];
-        ibc1 = adam.consts[1];
-        ibc2 = adam.consts[2];
-    }
-    if (sse_acc != nullptr && blockIdx.x == 0) {
-        // per-image L2 loss (P:298) from the tiles' fixed-point sums; re-zero
-        for (int i = threadIdx.x; i < batch; i += blockDim.x) {
-            const unsigned long long a = sse_acc[i];
-            sse_acc[i] = 0ull;
-            if (loss != nullptr) loss[i] = (float)((double)a * (1.0 / kSseScale) * inv_count);
-        }
+        if (a.done != nullptr) a.done[g] = 0u;
     }
     uint32_t touched = 0;
     int4 rect = make_int4(0, -1, 0, -1);
-    if (g < total) {
+    if (live) {
         const uint32_t bx = __float_as_uint(r.q1.w), by = __float_as_uint(r.q2.w);
         const int x0 = (int)(bx & 0xffffu), x1 = (int)(bx >> 16);
         const int y0 = (int)(by & 0xffffu), y1 = (int)(by >> 16);
@@ -401,36 +402,37 @@ __global__ void __launch_bounds__(256) finalize_kernel(
         bool any = false;
         // tiles of the (window-clipped, NEXT-4) rectangle
         const uint32_t cnt =
-            rect_area(window_rect(make_int4(x0 / kTile, x1 / kTile, y0 / kTile, y1 / kTile), row0, row1));
+            rect_area(window_rect(make_int4(x0 / kTile, x1 / kTile, y0 / kTile, y1 / kTile), a.row0,
+                                  a.row1));
         if (x0 <= x1 && y0 <= y1 && cnt > 0u) {
-            auto add = [&](const float4 a, const float4 b) {
-                S[0] += a.x; S[1] += a.y; S[2] += a.z; S[3] += a.w;
-                S[4] += b.x; S[5] += b.y; S[6] += b.z; S[7] += b.w;
+            auto add = [&](const float4 u, const float4 w) {
+                S[0] += u.x; S[1] += u.y; S[2] += u.z; S[3] += u.w;
+                S[4] += w.x; S[5] += w.y; S[6] += w.z; S[7] += w.w;
             };
             if (cnt <= 4u) {
                 // fixed slots 4 g .. 4 g + cnt - 1: all loads issued at once
-                float4 a[4], b[4];
+                float4 a4[4], b4[4];
                 const size_t o = 4 * (size_t)g;
     #pragma unroll
                 for (int k = 0; k < 4; ++k)
                     if ((uint32_t)k < cnt) {
-                        a[k] = pp[2 * (o + k)];
-                        b[k] = pp[2 * (o + k) + 1];
+                        a4[k] = pp[2 * (o + k)];
+                        b4[k] = pp[2 * (o + k) + 1];
                     }
     #pragma unroll
                 for (int k = 0; k < 4; ++k)                // row-major tile order of the rectangle
-                    if ((uint32_t)k < cnt) add(a[k], b[k]);
+                    if ((uint32_t)k < cnt) add(a4[k], b4[k]);
             } else {
-                const uint32_t o0 = gauss_off[g];
+                const uint32_t o0 = a.gauss_off[g];
                 if (o0 == kOffOverflow) {          // summed atomically by the tiles; re-zero
-                    float4* o = reinterpret_cast<float4*>(ovf) + 2 * (size_t)g;
-                    add(o[0], o[1]);
+                    float4* o = reinterpret_cast<float4*>(a.ovf) + 2 * (size_t)g;
+                    add(__ldcg(o), __ldcg(o + 1));
                     o[0] = make_float4(0.f, 0.f, 0.f, 0.f);
                     o[1] = make_float4(0.f, 0.f, 0.f, 0.f);
                 } else {
                     for (uint32_t k = 0; k < cnt; ++k) {
-                        if ((int64_t)(o0 + k) >= pcap) break;
-                        add(pp[2 * (size_t)(o0 + k)], pp[2 * (size_t)(o0 + k) + 1]);
+                        if ((int64_t)(o0 + k) >= a.pcap) break;
+                        add(__ldcg(pp + 2 * (size_t)(o0 + k)), __ldcg(pp + 2 * (size_t)(o0 + k) + 1));
                     }
                 }
             }
@@ -490,12 +492,12 @@ __global__ void __launch_bounds__(256) finalize_kernel(
             r1.z = S[1];
             r1.w = S[2];
         }
-        grads[2 * (size_t)g] = r0;
-        grads[2 * (size_t)g + 1] = r1;
+        a.grads[2 * (size_t)g] = r0;
+        a.grads[2 * (size_t)g + 1] = r1;
         if (adam.m != nullptr) {
                 float4* mm = reinterpret_cast<float4*>(adam.m) + 2 * (size_t)g;
             float4* vv = reinterpret_cast<float4*>(adam.v) + 2 * (size_t)g;
-            float4* pp = reinterpret_cast<float4*>(adam.params) + 2 * (size_t)g;
+            float4* pw = reinterpret_cast<float4*>(adam.params) + 2 * (size_t)g;
             float4 q0, q1;
             const float b1 = adam.b1, b2 = adam.b2, eps = adam.eps;
             q0.x = adam1(p0.x, r0.x, m0.x, v0.x, b1, b2, lr, ibc1, ibc2, eps);
@@ -507,7 +509,7 @@ __global__ void __launch_bounds__(256) finalize_kernel(
             q1.z = adam1(p1.z, r1.z, m1.z, v1.z, b1, b2, lr, ibc1, ibc2, eps);
             q1.w = adam1(p1.w, r1.w, m1.w, v1.w, b1, b2, lr, ibc1, ibc2, eps);
             mm[0] = m0; mm[1] = m1; vv[0] = v0; vv[1] = v1;
-            pp[0] = q0; pp[1] = q1;
+            pw[0] = q0; pw[1] = q1;
             const bool bad = !(isfinite(q0.x) && isfinite(q0.y) && isfinite(q0.z) && isfinite(q0.w) &&
                                isfinite(q1.x) && isfinite(q1.y) && isfinite(q1.z) && isfinite(q1.w));
             if (bad && adam.flag != nullptr) atomicOr(adam.flag, 1u);
@@ -522,9 +524,33 @@ __global__ void __launch_bounds__(256) finalize_kernel(
         const int TX = (W + kTile - 1) / kTile;
         const int T = TX * (adam.counts.row1 > 0 ? adam.counts.row1 - adam.counts.row0
                                                   : (H + kTile - 1) / kTile);
-        post_project_warp(adam.counts, touched, rect, g, g < total ? (g / n_per_image) * T : 0, TX,
+        post_project_warp(adam.counts, touched, rect, g, live ? (g / n_per_image) * T : 0, TX,
                           total);
     }
+}
+
+__global__ void __launch_bounds__(256) finalize_kernel(FinArgs a,
+                                                       unsigned long long* __restrict__ sse_acc,
+                                                       int batch, double inv_count,
+                                                       float* __restrict__ loss) {
+    griddep_wait();
+    griddep_trigger();
+    const int g = blockIdx.x * blockDim.x + threadIdx.x;
+    float lr = 0.f, ibc1 = 0.f, ibc2 = 0.f;
+    if (a.adam.m != nullptr) {
+        lr = a.adam.consts[0];
+        ibc1 = a.adam.consts[1];
+        ibc2 = a.adam.consts[2];
+    }
+    if (sse_acc != nullptr && blockIdx.x == 0) {
+        // per-image L2 loss (P:298) from the tiles' fixed-point sums; re-zero
+        for (int i = threadIdx.x; i < batch; i += blockDim.x) {
+            const unsigned long long v = sse_acc[i];
+            sse_acc[i] = 0ull;
+            if (loss != nullptr) loss[i] = (float)((double)v * (1.0 / kSseScale) * inv_count);
+        }
+    }
+    finalize_one(g, g < a.total, a, lr, ibc1, ibc2);
 }
 
 __global__ void loss_kernel(unsigned long long* __restrict__ sse_acc, int batch, double inv_count,
@@ -628,12 +654,12 @@ cudaError_t launch_backward_finalize(const float* params, const Proj* proj, int 
     if (total > 0) {
         FusedAdam fa{};
         if (adam) fa = *adam;
-        e = launch_pdl(finalize_kernel, dim3((total + 255) / 256), dim3(256), s,
-                       reinterpret_cast<const float4*>(params), proj, (const uint32_t*)w.gauss_off,
-                       total, n, f.width, f.height, flags, partial_cap(n, cap, f),
-                       (const float*)w.partial, w.ovf, reinterpret_cast<float4*>(grads), fa,
-                       mse ? w.sse_acc : nullptr, f.batch, 1.0 / count, mse ? loss : nullptr, row0,
-                       row1 > 0 ? row1 : tiles_y(f.height));
+        FinArgs fa_args{reinterpret_cast<const float4*>(params), proj, (const uint32_t*)w.gauss_off,
+                        total, n, f.width, f.height, flags, partial_cap(n, cap, f),
+                        (const float*)w.partial, w.ovf, reinterpret_cast<float4*>(grads), fa, row0,
+                        row1 > 0 ? row1 : tiles_y(f.height), nullptr};
+        e = launch_pdl(finalize_kernel, dim3((total + 255) / 256), dim3(256), s, fa_args,
+                       mse ? w.sse_acc : nullptr, f.batch, 1.0 / count, mse ? loss : nullptr);
         note_launches(1);
         if ((e = cudaGetLastError()) != cudaSuccess) return e;
     } else if (mse) {
