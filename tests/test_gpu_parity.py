@@ -664,6 +664,33 @@ def test_qat_step_parity(gi, gio):
     assert q.check() == gi.GI_OK and float(q.losses[0]) < ref["loss"]
 
 
+def test_spatial_windows_batch2(gi, gio):
+    # NEXT-4 windows on a 2-image launch: per image, the windows add up to
+    # the whole image
+    from paper_2403_08551_b200.dist import row_windows
+    from paper_2403_08551_b200.pipeline import _bytes, default_capacity
+    W, H, n, B = 80, 64, 400, 2
+    p = np.stack([params_for(n, 11 + b, True) for b in range(B)])
+    tgt = np.stack([synth.image(11 + b, W, H) for b in range(B)])
+    f = gi.frame(W, H, B)
+    cap = default_capacity(n, B)
+    ws = _bytes(gi.gi_fit_workspace_bytes(n, cap, f), DEV)
+    pd, td = to_dev(p).contiguous(), to_dev(tgt).contiguous()
+    acc = torch.zeros(B, n, 8, dtype=torch.float64, device=DEV)
+    lsum = torch.zeros(B, dtype=torch.float64, device=DEV)
+    for (r0, rows) in row_windows(H // 16, 3):
+        gr = torch.zeros(B, n, 8, dtype=torch.float32, device=DEV)
+        lo = torch.zeros(B, dtype=torch.float32, device=DEV)
+        gi.gi_fit_grads(pd, gr, td, n, f, 0, r0, rows, cap, ws, lo)
+        torch.cuda.synchronize()
+        acc += gr.double()
+        lsum += lo.double()
+    for b in range(B):
+        _, loss, g = gio.loss_and_grads(p[b], tgt[b], mode=gio.TILED)
+        assert max(group_err(acc[b].cpu().numpy(), g).values()) <= GRAD_TOL
+        assert abs(float(lsum[b]) - loss) <= 1e-5 * loss
+
+
 @pytest.mark.parametrize("parts", [2, 3])
 def test_spatial_windows_sum_to_whole(gi, gio, parts):
     # NEXT-4: gradients and loss of tile-row windows covering the image add up
