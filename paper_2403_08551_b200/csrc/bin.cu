@@ -331,8 +331,6 @@ ChainState bin_chain_direct(void* ws, int n, int64_t cap, const gi_frame& f, uin
     BinWs w = carve(ws, n, cap, f);
     ChainState cs{};
     cs.tile_count = w.tile_count;
-    cs.big_count = w.big_count;
-    cs.fill = w.fill;
     cs.alloc_counter = w.alloc_counter;
     cs.gauss_off = gauss_off;
     cs.slab = slab;

@@ -256,14 +256,12 @@ struct ProjectFuse {
     uint32_t* step_counter;
     BinCounts counts;
 };
-// Fused-chain bookkeeping passed to the bin scatter and the consumer tile
-// kernels (all may be null): alloc_counter + gauss_off allocate each
-// Gaussian's contiguous backward partial slots in the scatter; the consumer
-// re-zeroes tile_count / fill / alloc_counter for the next call.
+// Direct-binning bookkeeping passed to the consumer tile kernels (all null on
+// the gi_bin / tile_range paths): the consumer reads its count and slab,
+// re-zeroes the count for the next call, and its CTA 0 resets the partial-
+// slot allocator (close_segment).
 struct ChainState {
     uint32_t* tile_count;
-    uint32_t* big_count;
-    uint32_t* fill;
     uint32_t* alloc_counter;
     uint32_t* gauss_off;
     // direct binning (fused paths): the consumer reads its keys from the slab,

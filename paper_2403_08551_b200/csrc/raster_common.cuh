@@ -307,12 +307,6 @@ __device__ __forceinline__ Seg open_segment(const Proj* __restrict__ proj,
         const int r = sorted_segment(proj, key_gid, s, s + count, n, t.img, t.tx, t.ty, sl, scratch8);
         return Seg{s, count, r >= 0 ? kSegSorted : kSegGlobal};
     }
-    if (threadIdx.x == 0 && cs.tile_count != nullptr) {   // leave the counters zero for the next call
-        cs.tile_count[(size_t)tt * kCountStride] = 0u;
-        cs.big_count[tt] = 0u;
-        cs.fill[tt] = 0u;
-        if (tt == 0 && cs.alloc_counter != nullptr) *cs.alloc_counter = 0u;
-    }
     const uint32_t s = tile_range[tt], e = tile_range[tt + 1];
     if (presorted) return Seg{s, e - s, kSegGlobal};
     const int r = sorted_segment(proj, key_gid, s, e, n, t.img, t.tx, t.ty, sl, scratch8);
