@@ -4,10 +4,10 @@
 //   pass 1 (pixel-parallel, one pixel per thread, warp culling): recompute
 //          C (Eq. 7), g = dL/dC = 2 (C - T) / (3HW) (or a given dL/dC) and a
 //          per-tile partial of the squared error; g goes to shared memory.
-//   pass 2 (GAUSSIAN-parallel): each of the tile's Gaussians is owned by q
-//          consecutive lanes (q = 1..8, as many as the tile's 256 threads
-//          allow) that walk its box rows (row r -> lane r mod q) inside the
-//          tile and accumulate, per pair with w = exp(-sigma):
+//   pass 2 (GAUSSIAN-parallel): each staged record's in-tile box (row-major
+//          pixels) is cut into work-balanced chunks, one per lane (see the
+//          planner below); a lane walks its chunk and accumulates, per pair
+//          with w = exp(-sigma):
 //              dc'     += g w                               (A.1)
 //              gamma    = dL/dsigma = -w <g, c'>             (A.1, R12)
 //              S_u += gamma u, S_v += gamma v, S_uu += gamma u^2,
@@ -16,9 +16,9 @@
 //          dsigma/dmu (sign R13) and dsigma/dSigma chained
 //          through Sigma = L L^T (A.2, R14) follow in closed form.
 //          Every evaluated pair is an in-box pair (no warp-culling waste) and
-//          no per-pair warp reduction is needed; the q row-phases of one
-//          Gaussian are combined by a fixed xor tree, and the 8 sums are
-//          written once to the Gaussian's slot gauss_off[gid] + (rank of the
+//          no per-pair warp reduction is needed; a record's chunk sums are
+//          added in a fixed order and written once to the Gaussian's partial
+//          slot (4 gid, or gauss_off[gid] above 4 tiles, + the rank of the
 //          tile in its rectangle) -- no atomics, deterministic.
 // finalize_kernel -- one thread per Gaussian: sums its contiguous slots in
 //   row-major tile order, applies the chain rule (and tanh, App. C) and
@@ -252,24 +252,26 @@ __global__ void __launch_bounds__(256, GI_TILE_MINB) backward_tile_kernel(
             const int lx0 = box & 0xff, lx1 = (box >> 8) & 0xff, ly0 = (box >> 16) & 0xff;
             const int wdt = lx1 - lx0 + 1;
             const int row = (int)small_div((uint32_t)k0, 1.0f / (float)wdt), col = k0 - row * wdt;
+            // row-major walk: dx steps by 1 and wraps half a pixel past the
+            // box's last column (far above the stepping's rounding), c dy
+            // advances by c per row
             const float dx0 = ((float)lx0 + 0.5f) - B.z;
+            const float dx1 = ((float)lx1 + 1.0f) - B.z;
             float dx = ((float)(lx0 + col) + 0.5f) - B.z;
-            float dy = ((float)(ly0 + row) + 0.5f) - B.w;
-            float cdy = A.z * dy;
+            float cdy = A.z * (((float)(ly0 + row) + 0.5f) - B.w);
             const float4* gp_ptr = &sh.g[(ly0 + row) * kTile + lx0 + col];
-            int left = wdt - col;
+            const int wrap = kTile - wdt;
             float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f, a4 = 0.f, a5 = 0.f, a6 = 0.f, a7 = 0.f;
             for (int k = k0; k < k1; ++k) {
                 const float u = A.x * dx;
                 const float v = fmaf(A.y, dx, cdy);
                 const float w = ex2_approx(fmaf(-u, u, -(v * v)));
                 const float4 gp = *gp_ptr;
-                const float gw0 = gp.x * w, gw1 = gp.y * w, gw2 = gp.z * w;
-                const float sdot = fmaf(A.w, gw0, fmaf(B.x, gw1, B.y * gw2));   // -gamma
+                a0 = fmaf(gp.x, w, a0);
+                a1 = fmaf(gp.y, w, a1);
+                a2 = fmaf(gp.z, w, a2);
+                const float sdot = w * fmaf(A.w, gp.x, fmaf(B.x, gp.y, B.y * gp.z));   // -gamma
                 const float gu = -sdot * u, gv = -sdot * v;
-                a0 += gw0;
-                a1 += gw1;
-                a2 += gw2;
                 a3 += gu;
                 a4 += gv;
                 a5 = fmaf(gu, u, a5);
@@ -277,12 +279,10 @@ __global__ void __launch_bounds__(256, GI_TILE_MINB) backward_tile_kernel(
                 a7 = fmaf(gv, v, a7);
                 ++gp_ptr;
                 dx += 1.0f;
-                if (--left == 0) {
-                    left = wdt;
-                    gp_ptr += kTile - wdt;
+                if (dx > dx1) {
+                    gp_ptr += wrap;
                     dx = dx0;
-                    dy += 1.0f;
-                    cdy = A.z * dy;
+                    cdy += A.z;
                 }
             }
             sh.u.red[j][0] = make_float4(a0, a1, a2, a3);

@@ -9,16 +9,14 @@
 // evaluation.
 //
 // The tile's key segment is first brought into ascending-gid order in shared
-// memory (the scatter of binning leaves it unordered; see bin.cu), then, per
-// batch of up to 256 keys, each thread stages one record converted to
-// TILE-LOCAL coordinates:
-//   rA = {mx, my, a, b}   centre minus the tile origin, fp32 (ix - tx0 is an
-//                         exact small integer, + fx rounds once)
-//   rB = {c, c'r, c'g, c'b}
-//   rC = {x0, x1 - x0, y0, y1 - y0}   integer box, global pixels
-// Each warp then compacts the batch into its own candidate list: record
-// index + the 32-bit mask of its lanes whose pixel lies in the box, so the
-// inner loop needs no bit scanning and a one-instruction box test.  The box
+// memory (direct binning leaves it in atomic order), then, per batch of up to
+// kBatch keys, each thread stages one record converted to TILE-LOCAL
+// coordinates (StagedRecords below: conic + colour, centre minus the tile
+// origin -- ix - tx0 is an exact small integer, + fx rounds once -- and the
+// box clipped to the tile).  Each warp then compacts the batch into its own
+// candidate list: the record index + the 32-bit mask of its lanes
+// whose pixel lies in the box, so the inner loop needs no bit scanning and a
+// one-instruction box test.  The box
 // is staged as 16-bit column / row masks of the tile, so a warp's 32-lane
 // mask is two bit-field extracts and two multiplies.
 #pragma once
@@ -201,6 +199,19 @@ __device__ __forceinline__ bool covers_tile(const Proj* __restrict__ proj, uint3
            y1 / kTile >= ty;
 }
 
+// r - #{v.x, v.y, v.z, v.w < mine}: the borrow of v - mine is the compare,
+// subtracted straight from r (2 instructions per compare instead of 3).
+__device__ __forceinline__ uint32_t count_below4(const uint4 v, uint32_t mine, uint32_t r) {
+    asm("{\n\t.reg .u32 t;\n\t"
+        "sub.cc.u32 t, %1, %5;\n\tsubc.u32 %0, %0, 0;\n\t"
+        "sub.cc.u32 t, %2, %5;\n\tsubc.u32 %0, %0, 0;\n\t"
+        "sub.cc.u32 t, %3, %5;\n\tsubc.u32 %0, %0, 0;\n\t"
+        "sub.cc.u32 t, %4, %5;\n\tsubc.u32 %0, %0, 0;\n\t}"
+        : "+r"(r)
+        : "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w), "r"(mine));
+    return r;
+}
+
 __device__ __forceinline__ int sorted_segment(const Proj* __restrict__ proj,
                                               uint32_t* __restrict__ key_gid, uint32_t s,
                                               uint32_t e, int n, int img, int tx, int ty,
@@ -211,16 +222,13 @@ __device__ __forceinline__ int sorted_segment(const Proj* __restrict__ proj,
         if ((int)threadIdx.x < cnt) mine = key_gid[s + threadIdx.x];
         sl[threadIdx.x] = mine;
         __syncthreads();
-        int r = 0;   // entries >= cnt hold 0xffffffff and never count
+        uint32_t r = 0;   // entries >= cnt hold 0xffffffff and never count
         if ((int)threadIdx.x < cnt) {
             const uint4* s4 = reinterpret_cast<const uint4*>(sl);
-            for (int k = 0; k < (cnt + 3) >> 2; ++k) {
-                const uint4 v = s4[k];
-                r += (int)(v.x < mine) + (int)(v.y < mine) + (int)(v.z < mine) + (int)(v.w < mine);
-            }
+            for (int k = 0; k < (cnt + 3) >> 2; ++k) r = count_below4(s4[k], mine, r);
         }
         __syncthreads();
-        if ((int)threadIdx.x < cnt) sl[r] = mine;
+        if ((int)threadIdx.x < cnt) sl[0u - r] = mine;
         __syncthreads();
         return cnt;
     }
