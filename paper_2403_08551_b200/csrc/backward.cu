@@ -70,13 +70,13 @@ __global__ void __launch_bounds__(256, GI_TILE_MINB) backward_tile_kernel(
     ChainState cs) {
     __shared__ BwdShared sh;
     const TileCtx t = make_tile_ctx(W, H, TX, cs.row1 > 0 ? cs.row0 : 0);
+    const size_t P = (size_t)W * H;
+    const size_t pix = (size_t)t.img * 3 * P + (size_t)t.y * W + t.x;
     griddep_wait();
     griddep_trigger();
     const Seg sg = open_segment(proj, key_gid, tile_range, presorted, cs, n, T, t, sh.sl,
                                 sh.scratch, &sh.cursor);
     const uint32_t L = sg.L;
-    const size_t P = (size_t)W * H;
-    const size_t pix = (size_t)t.img * 3 * P + (size_t)t.y * W + t.x;
     const int lpix = (t.y - t.ty * kTile) * kTile + (t.x - t.tx * kTile);
     bool staged_all = false;
 
@@ -366,7 +366,6 @@ struct FinArgs {
     float4* grads;
     FusedAdam adam;
     int row0, row1;
-    uint32_t* done;            // fused step: re-zero the Gaussian's tile-completion counter
 };
 
 // Finalize Gaussian g (live = g is a real Gaussian for this thread).  All
@@ -390,7 +389,6 @@ __device__ __forceinline__ void finalize_one(int g, bool live, const FinArgs& a,
             const float4* vv = reinterpret_cast<const float4*>(adam.v) + 2 * (size_t)g;
             m0 = mm[0]; m1 = mm[1]; v0 = vv[0]; v1 = vv[1];
         }
-        if (a.done != nullptr) a.done[g] = 0u;
     }
     uint32_t touched = 0;
     int4 rect = make_int4(0, -1, 0, -1);
@@ -533,9 +531,14 @@ __global__ void __launch_bounds__(256) finalize_kernel(FinArgs a,
                                                        unsigned long long* __restrict__ sse_acc,
                                                        int batch, double inv_count,
                                                        float* __restrict__ loss) {
+    const int g = blockIdx.x * blockDim.x + threadIdx.x;
+    if (a.adam.m != nullptr && g < a.total) {   // CTAs resident in the tile kernel's tail warm L2
+        prefetch_l2(a.params + 2 * (size_t)g);
+        prefetch_l2(a.adam.m + 8 * (size_t)g);
+        prefetch_l2(a.adam.v + 8 * (size_t)g);
+    }
     griddep_wait();
     griddep_trigger();
-    const int g = blockIdx.x * blockDim.x + threadIdx.x;
     float lr = 0.f, ibc1 = 0.f, ibc2 = 0.f;
     if (a.adam.m != nullptr) {
         lr = a.adam.consts[0];
@@ -657,7 +660,7 @@ cudaError_t launch_backward_finalize(const float* params, const Proj* proj, int 
         FinArgs fa_args{reinterpret_cast<const float4*>(params), proj, (const uint32_t*)w.gauss_off,
                         total, n, f.width, f.height, flags, partial_cap(n, cap, f),
                         (const float*)w.partial, w.ovf, reinterpret_cast<float4*>(grads), fa, row0,
-                        row1 > 0 ? row1 : tiles_y(f.height), nullptr};
+                        row1 > 0 ? row1 : tiles_y(f.height)};
         e = launch_pdl(finalize_kernel, dim3((total + 255) / 256), dim3(256), s, fa_args,
                        mse ? w.sse_acc : nullptr, f.batch, 1.0 / count, mse ? loss : nullptr);
         note_launches(1);

@@ -54,6 +54,11 @@ __device__ __forceinline__ float ex2_approx(float x) {
 // Both are no-ops for a normal launch.
 __device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void griddep_trigger() { asm volatile("griddepcontrol.launch_dependents;"); }
+// L2 prefetch: no data reaches the thread, so it is safe before
+// griddep_wait() (L2 is the coherence point; a later load sees any write).
+__device__ __forceinline__ void prefetch_l2(const void* p) {
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+}
 
 bool use_pdl();   // default on; GI_NO_PDL=1 disables (A/B measurement)
 
