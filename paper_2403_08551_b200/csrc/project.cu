@@ -22,6 +22,7 @@ __global__ void __launch_bounds__(256) project_kernel(const float4* __restrict__
                                                       uint32_t* __restrict__ tiles_touched,
                                                       ProjectFuse fuse) {
     const int g = blockIdx.x * blockDim.x + threadIdx.x;
+    if (g < total) prefetch_l2(params + 2 * (size_t)g);   // 32 B record; safe before the wait
     griddep_wait();
     griddep_trigger();
     if (fuse.step_counter != nullptr && g == 0) *fuse.step_counter += 1u;   // fused fit: t <- t + 1
