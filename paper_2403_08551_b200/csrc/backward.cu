@@ -166,12 +166,12 @@ __global__ void __launch_bounds__(256, GI_TILE_MINB) backward_tile_kernel(
             if (t.lane == 0) sh.pa[t.warp] = make_uint2(ws, wm);
         }
         __syncthreads();
-        uint32_t tot = 0, mx = 0;
-#pragma unroll
-        for (int w = 0; w < kWarps; ++w) {
-            const uint2 x = sh.pa[w];
-            tot += x.x;
-            mx = max(mx, x.y);
+        // 8-way combines of per-warp partials: lane w < 8 loads warp w's, one redux
+        uint32_t tot, mx;
+        {
+            const uint2 x = t.lane < kWarps ? sh.pa[t.lane] : make_uint2(0u, 0u);
+            tot = __reduce_add_sync(kFull, x.x);
+            mx = __reduce_max_sync(kFull, x.y);
         }
         // (2) chunk counts of the candidate chunk sizes
         const uint32_t c0 = (tot + 255u) >> 8;
@@ -190,13 +190,8 @@ __global__ void __launch_bounds__(256, GI_TILE_MINB) backward_tile_kernel(
         __syncthreads();
         uint32_t C = mx;
         {
-            uint32_t n01 = 0, n2 = 0;
-#pragma unroll
-            for (int w = 0; w < kWarps; ++w) {
-                const uint2 x = sh.pb[w];
-                n01 += x.x;
-                n2 += x.y;
-            }
+            const uint2 x = t.lane < kWarps ? sh.pb[t.lane] : make_uint2(0u, 0u);
+            const uint32_t n01 = __reduce_add_sync(kFull, x.x), n2 = __reduce_add_sync(kFull, x.y);
             if (n2 <= 256u) C = c2;
             if ((n01 >> 16) <= 256u) C = c1;
             if ((n01 & 0xffffu) <= 256u) C = c0;
@@ -214,12 +209,11 @@ __global__ void __launch_bounds__(256, GI_TILE_MINB) backward_tile_kernel(
         uint32_t rrank = 0;
         if (rm != 0u) rrank = atomicAdd(&sh.hist[rbin], 1u);
         __syncthreads();
-        uint32_t F = 0, fstart = incl - nf;
-#pragma unroll
-        for (int w = 0; w < kWarps; ++w) {
-            const uint32_t x = sh.pc[w];
-            fstart += w < t.warp ? x : 0u;
-            F += x;
+        uint32_t F, fstart;
+        {
+            const uint32_t x = t.lane < kWarps ? sh.pc[t.lane] : 0u;
+            F = __reduce_add_sync(kFull, x);
+            fstart = incl - nf + __reduce_add_sync(kFull, t.lane < t.warp ? x : 0u);
         }
         if (t.warp == 0) {
             const uint32_t h0 = sh.hist[2 * t.lane], h1 = sh.hist[2 * t.lane + 1];

@@ -54,8 +54,9 @@ __device__ __forceinline__ TileCtx make_tile_ctx(int W, int H, int TX, int row0)
     c.row1 = row0 + gridDim.y;
     c.lane = threadIdx.x & 31;
     c.warp = threadIdx.x >> 5;
-    const int lx = (c.warp & 1) * 8 + (c.lane & 7);
-    const int ly = (c.warp >> 1) * 4 + (c.lane >> 3);
+    // thread bits: [0,3) column in the block, [3,5) row, [5] x half, [6,8) y quarter
+    const int lx = (int)((threadIdx.x & 7u) | ((threadIdx.x >> 2) & 8u));
+    const int ly = (int)(((threadIdx.x >> 3) & 3u) | ((threadIdx.x >> 4) & 12u));
     c.x = c.tx * kTile + lx;
     c.y = c.ty * kTile + ly;
     c.cx = (float)lx + 0.5f;
