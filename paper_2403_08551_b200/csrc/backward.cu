@@ -51,11 +51,19 @@ struct BwdShared {
     uint32_t n_items;
 };
 
-// floor(a / b) for 0 <= a < 2^16, 1 <= b < 2^16 given rb = 1/b (fp32): the
-// true quotient is at least 0.5/b away from an integer after the +0.5 shift,
-// far above the rounding error (< 2^-21 a / b).
+// floor(a / b) for 0 <= a < 2^16, 1 <= b < 2^16 given rb ~ 1/b (fp32 within
+// 1 ulp, e.g. rcp.approx): (a + 1/2) / b is at least 0.5/b away from an
+// integer, and the product's relative error (< 1.5 2^-23) moves it by less
+// than (a + 1/2) 2^-22.4 / b < 0.5 / b since a < 2^16.
 __device__ __forceinline__ uint32_t small_div(uint32_t a, float rb) {
     return (uint32_t)(((float)a + 0.5f) * rb);
+}
+
+// 1/x by MUFU.RCP (rcp.approx: at most 1 ulp), for small_div.
+__device__ __forceinline__ float rcp_approx(float x) {
+    float r;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
 }
 
 #ifndef GI_TILE_MINB
@@ -179,9 +187,9 @@ __global__ void __launch_bounds__(256, GI_TILE_MINB) backward_tile_kernel(
         {
             uint32_t n01 = 0, n2 = 0;
             if (j < cnt) {
-                n01 = small_div(wj + c0 - 1u, 1.0f / (float)c0) |
-                      small_div(wj + c1 - 1u, 1.0f / (float)c1) << 16;
-                n2 = small_div(wj + c2 - 1u, 1.0f / (float)c2);
+                n01 = small_div(wj + c0 - 1u, rcp_approx((float)c0)) |
+                      small_div(wj + c1 - 1u, rcp_approx((float)c1)) << 16;
+                n2 = small_div(wj + c2 - 1u, rcp_approx((float)c2));
             }
             n01 = __reduce_add_sync(kFull, n01);
             n2 = __reduce_add_sync(kFull, n2);
@@ -197,7 +205,7 @@ __global__ void __launch_bounds__(256, GI_TILE_MINB) backward_tile_kernel(
             if ((n01 & 0xffffu) <= 256u) C = c0;
         }
         // (3) full chunks: block scan of their counts; remainders: size bins
-        const uint32_t nf = small_div(wj, 1.0f / (float)C), rm = wj - nf * C;
+        const uint32_t nf = small_div(wj, rcp_approx((float)C)), rm = wj - nf * C;
         uint32_t incl = nf;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -245,7 +253,7 @@ __global__ void __launch_bounds__(256, GI_TILE_MINB) backward_tile_kernel(
             const uint32_t box = sh.sr.c[r].x;
             const int lx0 = box & 0xff, lx1 = (box >> 8) & 0xff, ly0 = (box >> 16) & 0xff;
             const int wdt = lx1 - lx0 + 1;
-            const int row = (int)small_div((uint32_t)k0, 1.0f / (float)wdt), col = k0 - row * wdt;
+            const int row = (int)small_div((uint32_t)k0, rcp_approx((float)wdt)), col = k0 - row * wdt;
             // row-major walk: dx steps by 1 and wraps half a pixel past the
             // box's last column (far above the stepping's rounding), c dy
             // advances by c per row
