@@ -189,8 +189,10 @@ gi_status gi_fit_step(float* params, float* grads, float* m, float* v, const flo
                       void* fit_ws, size_t ws_bytes, uint32_t* step_counter, float lr0,
                       int32_t half_every, float beta1, float beta2, float eps, float* loss,
                       uint32_t* status_flags, void* const* stage_events, void* stream);
-/* Fused fit step with Adan instead of Adam (same stages as gi_fit_step, the
- * optimiser being a separate elementwise kernel; device step counter). */
+/* Fused fit step with Adan (NEXT-1, the paper's optimiser; update rule
+ * of gi_adan_step) instead of Adam: the same stages as gi_fit_step, the Adan
+ * update fused into the finalize kernel (3 kernels); device step counter.
+ * n, grad_prev: [B][N][8] fp32 Adan state (zero before step 1), 16-B aligned. */
 gi_status gi_fit_step_adan(float* params, float* grads, float* m, float* v, float* n,
                            float* grad_prev, const float* target, int32_t n_gauss, const gi_frame* f,
                            uint32_t flags, int64_t key_capacity, void* fit_ws, size_t ws_bytes,
@@ -200,7 +202,7 @@ gi_status gi_fit_step_adan(float* params, float* grads, float* m, float* v, floa
 
 /* Chained fit steps: identical arithmetic to gi_fit_step, but the projection
  * of step t+1 is fused into the finalize + Adam kernel of step t (the thread
- * that updated a Gaussian projects it at once), so a step is 3 kernels.
+ * that updated a Gaussian projects it at once), so a step is 2 kernels.
  * gi_fit_prime projects the current params into fit_ws; every
  * gi_fit_step_chained call then REQUIRES that fit_ws holds the projection of
  * the current params -- i.e. it follows gi_fit_prime or another chained call
@@ -213,6 +215,15 @@ gi_status gi_fit_step_chained(float* params, float* grads, float* m, float* v, c
                               void* fit_ws, size_t ws_bytes, uint32_t* step_counter, float lr0,
                               int32_t half_every, float beta1, float beta2, float eps, float* loss,
                               uint32_t* status_flags, void* const* stage_events, void* stream);
+/* Chained Adan fit step: gi_fit_step_adan's arithmetic with gi_fit_step_chained's
+ * structure (2 kernels; requires gi_fit_prime as gi_fit_step_chained does). */
+gi_status gi_fit_step_adan_chained(float* params, float* grads, float* m, float* v, float* n,
+                                   float* grad_prev, const float* target, int32_t n_gauss,
+                                   const gi_frame* f, uint32_t flags, int64_t key_capacity,
+                                   void* fit_ws, size_t ws_bytes, uint32_t* step_counter, float lr0,
+                                   int32_t half_every, float beta1, float beta2, float beta3,
+                                   float eps, float weight_decay, float* loss,
+                                   uint32_t* status_flags, void* stream);
 
 /* --- NEXT-4: single-image spatial sharding -----------
  * The gradient half of a fused fit step restricted to the tile rows

@@ -13,23 +13,6 @@
 namespace gi {
 namespace {
 
-struct AdanConsts {
-    float lr, ibc1, ibc2, isbc3, b1, b2, b3, eps, decay;
-    int first;
-};
-
-__device__ __forceinline__ float adan1(float p, float g, float& m, float& v, float& n, float& gp,
-                                       const AdanConsts& c) {
-    const float d = c.first ? 0.0f : g - gp;
-    m = fmaf(c.b1, m, (1.0f - c.b1) * g);
-    v = fmaf(c.b2, v, (1.0f - c.b2) * d);
-    const float u = fmaf(c.b2, d, g);
-    n = fmaf(c.b3, n, (1.0f - c.b3) * (u * u));
-    gp = g;
-    const float upd = fmaf(c.b2 * c.ibc2, v, m * c.ibc1) / fmaf(sqrtf(n), c.isbc3, c.eps);
-    return fmaf(-c.lr, upd, p * c.decay);
-}
-
 __global__ void __launch_bounds__(256) adan_kernel(float4* __restrict__ p, const float4* __restrict__ g,
                                                    float4* __restrict__ m, float4* __restrict__ v,
                                                    float4* __restrict__ n, float4* __restrict__ gp,

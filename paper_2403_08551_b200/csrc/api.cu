@@ -249,12 +249,19 @@ static cudaError_t record_stage(void* const* ev, int i, cudaStream_t s) {
     return cudaEventRecordWithFlags(static_cast<cudaEvent_t>(ev[i]), s, cudaEventRecordExternal);
 }
 
+// Adan state of a fused Adan fit step (NEXT-1); null for Adam.
+struct AdanOpt {
+    float* n;
+    float* grad_prev;
+    float beta3, weight_decay;
+};
+
 static gi_status fit_step_impl(float* params, float* grads, float* m, float* v, const float* target,
                                int32_t n, const gi_frame* f, uint32_t flags, int64_t key_capacity,
                                void* fit_ws, size_t ws_bytes, uint32_t* step_counter, float lr0,
                                int32_t half_every, float beta1, float beta2, float eps, float* loss,
                                uint32_t* status_flags, void* const* stage_events, void* stream,
-                               bool chained) {
+                               bool chained, const AdanOpt* adan = nullptr) {
     gi_status st;
     if ((st = check_frame(f)) != GI_OK || (st = check_n(n, f)) != GI_OK) return st;
     if (!gi::flags_valid(flags)) return invalid("flags");
@@ -267,6 +274,11 @@ static gi_status fit_step_impl(float* params, float* grads, float* m, float* v, 
         return invalid("NULL buffer");
     if (!aligned16(params) || !aligned16(grads) || !aligned16(m) || !aligned16(v) || !aligned16(fit_ws))
         return invalid("alignment");
+    if (adan != nullptr) {
+        if (!(adan->beta3 >= 0.f && adan->beta3 < 1.f)) return invalid("betas");
+        if (n > 0 && (!adan->n || !adan->grad_prev)) return invalid("NULL buffer");
+        if (!aligned16(adan->n) || !aligned16(adan->grad_prev)) return invalid("alignment");
+    }
     FitWs w = carve_fit(fit_ws, n, key_capacity, *f);
     cudaStream_t s = S(stream);
     cudaError_t e;
@@ -288,6 +300,11 @@ static gi_status fit_step_impl(float* params, float* grads, float* m, float* v, 
     cs.half_every = half_every;
     cs.b1 = beta1;
     cs.b2 = beta2;
+    if (adan != nullptr) {
+        cs.adan = 1;
+        cs.b3 = adan->beta3;
+        cs.wd = adan->weight_decay;
+    }
     GI_TRY(record_stage(stage_events, 0, s), "gi_fit_step/event");
     if (!chained)
         GI_TRY(gi::launch_project(params, n, *f, flags, w.proj, w.touched,
@@ -299,8 +316,25 @@ static gi_status fit_step_impl(float* params, float* grads, float* m, float* v, 
                                      key_capacity, w.bwd_ws, nullptr, cs, s),
            "gi_fit_step/backward");
     GI_TRY(record_stage(stage_events, 3, s), "gi_fit_step/event");
-    gi::FusedAdam fa{params, m, v, consts, beta1, beta2, eps, status_flags,
-                     chained ? w.proj : nullptr, w.touched, bc, f->k, flags};
+    gi::FusedAdam fa{};
+    fa.params = params;
+    fa.m = m;
+    fa.v = v;
+    fa.consts = consts;
+    fa.b1 = beta1;
+    fa.b2 = beta2;
+    fa.eps = eps;
+    fa.flag = status_flags;
+    if (adan != nullptr) {
+        fa.n = adan->n;
+        fa.gprev = adan->grad_prev;
+        fa.b3 = adan->beta3;
+    }
+    fa.proj_out = chained ? w.proj : nullptr;
+    fa.touched_out = w.touched;
+    fa.counts = bc;
+    fa.k = f->k;
+    fa.pos_flags = flags;
     GI_TRY(gi::launch_backward_finalize(params, w.proj, n, *f, flags, true, key_capacity, w.bwd_ws,
                                         grads, loss, &fa, s),
            "gi_fit_step/finalize+adam");
@@ -379,47 +413,23 @@ gi_status gi_fit_step_adan(float* params, float* grads, float* m, float* v, floa
                            uint32_t* step_counter, float lr0, int32_t half_every, float beta1,
                            float beta2, float beta3, float eps, float weight_decay, float* loss,
                            uint32_t* status_flags, void* stream) {
-    gi_status st;
-    if ((st = check_frame(f)) != GI_OK || (st = check_n(n_gauss, f)) != GI_OK) return st;
-    if (!gi::flags_valid(flags)) return invalid("flags");
-    if (key_capacity < 0 || key_capacity >= (1LL << 31)) return invalid("key_capacity");
-    if (half_every < 1) return invalid("half_every");
-    if (!(beta1 >= 0.f && beta1 < 1.f && beta2 >= 0.f && beta2 < 1.f && beta3 >= 0.f && beta3 < 1.f))
-        return invalid("betas");
-    if (!fit_ws || ws_bytes < carve_fit(nullptr, n_gauss, key_capacity, *f).bytes)
-        return invalid("fit workspace too small");
-    if (!step_counter || !target ||
-        (n_gauss > 0 && (!params || !grads || !m || !v || !n || !grad_prev)))
-        return invalid("NULL buffer");
-    if (!aligned16(params) || !aligned16(grads) || !aligned16(m) || !aligned16(v) || !aligned16(n) ||
-        !aligned16(grad_prev) || !aligned16(fit_ws))
-        return invalid("alignment");
-    const int32_t nn = n_gauss;
-    FitWs w = carve_fit(fit_ws, nn, key_capacity, *f);
-    cudaStream_t s = S(stream);
-    cudaError_t e;
-#define GI_TRY(expr, where) \
-    if ((e = (expr)) != cudaSuccess) return cuda_status(e, where)
-    uint32_t* gauss_off = gi::backward_gauss_off(w.bwd_ws, nn, key_capacity, *f);
-    const gi::BinCounts bc = gi::bin_counts_direct(w.bin_ws, nn, key_capacity, *f, w.key_gid, gauss_off);
-    const gi::ChainState cs = gi::bin_chain_direct(w.bin_ws, nn, key_capacity, *f, w.key_gid,
-                                                   gauss_off, w.n_keys, nullptr);
-    GI_TRY(gi::launch_project(params, nn, *f, flags, w.proj, w.touched,
-                              gi::ProjectFuse{step_counter, bc}, s),
-           "gi_fit_step_adan/project");
-    GI_TRY(gi::launch_backward_tiles(w.proj, w.key_gid, nullptr, nn, *f, false, nullptr, target,
-                                     key_capacity, w.bwd_ws, nullptr, cs, s),
-           "gi_fit_step_adan/backward");
-    GI_TRY(gi::launch_backward_finalize(params, w.proj, nn, *f, flags, true, key_capacity, w.bwd_ws,
-                                        grads, loss, nullptr, s),
-           "gi_fit_step_adan/finalize");
-    if (nn > 0)
-        GI_TRY(gi::launch_adan(params, grads, m, v, n, grad_prev, (int64_t)nn * 8 * f->batch, 0,
-                               step_counter, lr0, half_every, beta1, beta2, beta3, eps,
-                               weight_decay, status_flags, s),
-               "gi_fit_step_adan/adan");
-#undef GI_TRY
-    return GI_OK;
+    const AdanOpt opt{n, grad_prev, beta3, weight_decay};
+    return fit_step_impl(params, grads, m, v, target, n_gauss, f, flags, key_capacity, fit_ws,
+                         ws_bytes, step_counter, lr0, half_every, beta1, beta2, eps, loss,
+                         status_flags, nullptr, stream, false, &opt);
+}
+
+gi_status gi_fit_step_adan_chained(float* params, float* grads, float* m, float* v, float* n,
+                                   float* grad_prev, const float* target, int32_t n_gauss,
+                                   const gi_frame* f, uint32_t flags, int64_t key_capacity,
+                                   void* fit_ws, size_t ws_bytes, uint32_t* step_counter, float lr0,
+                                   int32_t half_every, float beta1, float beta2, float beta3,
+                                   float eps, float weight_decay, float* loss,
+                                   uint32_t* status_flags, void* stream) {
+    const AdanOpt opt{n, grad_prev, beta3, weight_decay};
+    return fit_step_impl(params, grads, m, v, target, n_gauss, f, flags, key_capacity, fit_ws,
+                         ws_bytes, step_counter, lr0, half_every, beta1, beta2, eps, loss,
+                         status_flags, nullptr, stream, true, &opt);
 }
 
 gi_status gi_fit_prime(const float* params, int32_t n, const gi_frame* f, uint32_t flags,

@@ -373,6 +373,7 @@ struct FinArgs {
 // Finalize Gaussian g (live = g is a real Gaussian for this thread).  All
 // lanes of the warp must call (the direct-binning tail is warp-cooperative).
 // lr, ibc1, ibc2: the Adam step constants.
+template <bool kAdan>
 __device__ __forceinline__ void finalize_one(int g, bool live, const FinArgs& a, float lr,
                                              float ibc1, float ibc2) {
     const FusedAdam& adam = a.adam;
@@ -390,6 +391,14 @@ __device__ __forceinline__ void finalize_one(int g, bool live, const FinArgs& a,
             const float4* mm = reinterpret_cast<const float4*>(adam.m) + 2 * (size_t)g;
             const float4* vv = reinterpret_cast<const float4*>(adam.v) + 2 * (size_t)g;
             m0 = mm[0]; m1 = mm[1]; v0 = vv[0]; v1 = vv[1];
+        }
+    }
+    float4 n0{}, n1{}, gp0{}, gp1{};      // Adan: third moment, previous gradient
+    if constexpr (kAdan) {
+        if (live) {
+            const float4* nn = reinterpret_cast<const float4*>(adam.n) + 2 * (size_t)g;
+            const float4* gg = reinterpret_cast<const float4*>(adam.gprev) + 2 * (size_t)g;
+            n0 = nn[0]; n1 = nn[1]; gp0 = gg[0]; gp1 = gg[1];
         }
     }
     uint32_t touched = 0;
@@ -500,14 +509,36 @@ __device__ __forceinline__ void finalize_one(int g, bool live, const FinArgs& a,
             float4* pw = reinterpret_cast<float4*>(adam.params) + 2 * (size_t)g;
             float4 q0, q1;
             const float b1 = adam.b1, b2 = adam.b2, eps = adam.eps;
-            q0.x = adam1(p0.x, r0.x, m0.x, v0.x, b1, b2, lr, ibc1, ibc2, eps);
-            q0.y = adam1(p0.y, r0.y, m0.y, v0.y, b1, b2, lr, ibc1, ibc2, eps);
-            q0.z = adam1(p0.z, r0.z, m0.z, v0.z, b1, b2, lr, ibc1, ibc2, eps);
-            q0.w = adam1(p0.w, r0.w, m0.w, v0.w, b1, b2, lr, ibc1, ibc2, eps);
-            q1.x = adam1(p1.x, r1.x, m1.x, v1.x, b1, b2, lr, ibc1, ibc2, eps);
-            q1.y = adam1(p1.y, r1.y, m1.y, v1.y, b1, b2, lr, ibc1, ibc2, eps);
-            q1.z = adam1(p1.z, r1.z, m1.z, v1.z, b1, b2, lr, ibc1, ibc2, eps);
-            q1.w = adam1(p1.w, r1.w, m1.w, v1.w, b1, b2, lr, ibc1, ibc2, eps);
+            if constexpr (kAdan) {          // NEXT-1: the paper's optimiser, fused
+                AdanConsts c;
+                c.lr = lr;
+                c.ibc1 = ibc1;
+                c.ibc2 = ibc2;
+                c.isbc3 = adam.consts[3];
+                c.decay = adam.consts[4];
+                c.first = adam.consts[5] != 0.0f;
+                c.b1 = b1; c.b2 = b2; c.b3 = adam.b3; c.eps = eps;
+                q0.x = adan1(p0.x, r0.x, m0.x, v0.x, n0.x, gp0.x, c);
+                q0.y = adan1(p0.y, r0.y, m0.y, v0.y, n0.y, gp0.y, c);
+                q0.z = adan1(p0.z, r0.z, m0.z, v0.z, n0.z, gp0.z, c);
+                q0.w = adan1(p0.w, r0.w, m0.w, v0.w, n0.w, gp0.w, c);
+                q1.x = adan1(p1.x, r1.x, m1.x, v1.x, n1.x, gp1.x, c);
+                q1.y = adan1(p1.y, r1.y, m1.y, v1.y, n1.y, gp1.y, c);
+                q1.z = adan1(p1.z, r1.z, m1.z, v1.z, n1.z, gp1.z, c);
+                q1.w = adan1(p1.w, r1.w, m1.w, v1.w, n1.w, gp1.w, c);
+                float4* nn = reinterpret_cast<float4*>(adam.n) + 2 * (size_t)g;
+                float4* gg = reinterpret_cast<float4*>(adam.gprev) + 2 * (size_t)g;
+                nn[0] = n0; nn[1] = n1; gg[0] = gp0; gg[1] = gp1;
+            } else {
+                q0.x = adam1(p0.x, r0.x, m0.x, v0.x, b1, b2, lr, ibc1, ibc2, eps);
+                q0.y = adam1(p0.y, r0.y, m0.y, v0.y, b1, b2, lr, ibc1, ibc2, eps);
+                q0.z = adam1(p0.z, r0.z, m0.z, v0.z, b1, b2, lr, ibc1, ibc2, eps);
+                q0.w = adam1(p0.w, r0.w, m0.w, v0.w, b1, b2, lr, ibc1, ibc2, eps);
+                q1.x = adam1(p1.x, r1.x, m1.x, v1.x, b1, b2, lr, ibc1, ibc2, eps);
+                q1.y = adam1(p1.y, r1.y, m1.y, v1.y, b1, b2, lr, ibc1, ibc2, eps);
+                q1.z = adam1(p1.z, r1.z, m1.z, v1.z, b1, b2, lr, ibc1, ibc2, eps);
+                q1.w = adam1(p1.w, r1.w, m1.w, v1.w, b1, b2, lr, ibc1, ibc2, eps);
+            }
             mm[0] = m0; mm[1] = m1; vv[0] = v0; vv[1] = v1;
             pw[0] = q0; pw[1] = q1;
             const bool bad = !(isfinite(q0.x) && isfinite(q0.y) && isfinite(q0.z) && isfinite(q0.w) &&
@@ -529,6 +560,7 @@ __device__ __forceinline__ void finalize_one(int g, bool live, const FinArgs& a,
     }
 }
 
+template <bool kAdan>
 __global__ void __launch_bounds__(256) finalize_kernel(FinArgs a,
                                                        unsigned long long* __restrict__ sse_acc,
                                                        int batch, double inv_count,
@@ -538,6 +570,10 @@ __global__ void __launch_bounds__(256) finalize_kernel(FinArgs a,
         prefetch_l2(a.params + 2 * (size_t)g);
         prefetch_l2(a.adam.m + 8 * (size_t)g);
         prefetch_l2(a.adam.v + 8 * (size_t)g);
+        if constexpr (kAdan) {
+            prefetch_l2(a.adam.n + 8 * (size_t)g);
+            prefetch_l2(a.adam.gprev + 8 * (size_t)g);
+        }
     }
     griddep_wait();
     griddep_trigger();
@@ -555,7 +591,7 @@ __global__ void __launch_bounds__(256) finalize_kernel(FinArgs a,
             if (loss != nullptr) loss[i] = (float)((double)v * (1.0 / kSseScale) * inv_count);
         }
     }
-    finalize_one(g, g < a.total, a, lr, ibc1, ibc2);
+    finalize_one<kAdan>(g, g < a.total, a, lr, ibc1, ibc2);
 }
 
 __global__ void loss_kernel(unsigned long long* __restrict__ sse_acc, int batch, double inv_count,
@@ -588,7 +624,7 @@ BwdWs carve(void* base, int n, int64_t cap, const gi_frame& f) {
     w.ovf = reinterpret_cast<float*>(p + off); off += align_up(sizeof(float) * 8 * total);
     w.counter = reinterpret_cast<uint32_t*>(p + off); off += align_up(sizeof(uint32_t));
     w.sse_acc = reinterpret_cast<unsigned long long*>(p + off); off += align_up(8 * (size_t)f.batch);
-    w.adam_consts = reinterpret_cast<float*>(p + off); off += align_up(4 * sizeof(float));
+    w.adam_consts = reinterpret_cast<float*>(p + off); off += align_up(8 * sizeof(float));
     w.bytes = off;
     return w;
 }
@@ -663,8 +699,12 @@ cudaError_t launch_backward_finalize(const float* params, const Proj* proj, int 
                         total, n, f.width, f.height, flags, partial_cap(n, cap, f),
                         (const float*)w.partial, w.ovf, reinterpret_cast<float4*>(grads), fa, row0,
                         row1 > 0 ? row1 : tiles_y(f.height)};
-        e = launch_pdl(finalize_kernel, dim3((total + 255) / 256), dim3(256), s, fa_args,
-                       mse ? w.sse_acc : nullptr, f.batch, 1.0 / count, mse ? loss : nullptr);
+        if (adam != nullptr && adam->n != nullptr)
+            e = launch_pdl(finalize_kernel<true>, dim3((total + 255) / 256), dim3(256), s, fa_args,
+                           mse ? w.sse_acc : nullptr, f.batch, 1.0 / count, mse ? loss : nullptr);
+        else
+            e = launch_pdl(finalize_kernel<false>, dim3((total + 255) / 256), dim3(256), s, fa_args,
+                           mse ? w.sse_acc : nullptr, f.batch, 1.0 / count, mse ? loss : nullptr);
         note_launches(1);
         if ((e = cudaGetLastError()) != cudaSuccess) return e;
     } else if (mse) {

@@ -284,7 +284,34 @@ struct ChainState {
     float lr0;
     int half_every;
     float b1, b2;
+    // fused Adan (NEXT-1): adan != 0 -> consts = {lr_t, 1/(1-b1^t), 1/(1-b2^t),
+    // 1/sqrt(1-b3^t), 1 - lr_t wd, t == 1}
+    int adan;
+    float b3, wd;
 };
+
+// Adan step constants for step t (1-based), as the standalone adan_kernel and
+// the fused finalize use them.
+struct AdanConsts {
+    float lr, ibc1, ibc2, isbc3, b1, b2, b3, eps, decay;
+    int first;
+};
+
+// One Adan update of a scalar (NEXT-1, reading R28; see adan.cu):
+//   d = g - g_prev (0 at t = 1); m = b1 m + (1-b1) g; v = b2 v + (1-b2) d;
+//   n = b3 n + (1-b3) (g + b2 d)^2; g_prev = g;
+//   p = p (1 - lr wd) - lr (m/(1-b1^t) + b2 v/(1-b2^t)) / (sqrt(n/(1-b3^t)) + eps)
+__device__ __forceinline__ float adan1(float p, float g, float& m, float& v, float& n, float& gp,
+                                       const AdanConsts& c) {
+    const float d = c.first ? 0.0f : g - gp;
+    m = fmaf(c.b1, m, (1.0f - c.b1) * g);
+    v = fmaf(c.b2, v, (1.0f - c.b2) * d);
+    const float u = fmaf(c.b2, d, g);
+    n = fmaf(c.b3, n, (1.0f - c.b3) * (u * u));
+    gp = g;
+    const float upd = fmaf(c.b2 * c.ibc2, v, m * c.ibc1) / fmaf(sqrtf(n), c.isbc3, c.eps);
+    return fmaf(-c.lr, upd, p * c.decay);
+}
 cudaError_t launch_project(const float* params, int n, const gi_frame& f, uint32_t flags,
                            Proj* proj, uint32_t* tiles_touched, const ProjectFuse& fuse,
                            cudaStream_t s);
@@ -329,6 +356,11 @@ struct FusedAdam {
     const float* consts;      // {lr_t, 1 / (1 - b1^t), 1 / (1 - b2^t)} (ChainState.adam_consts)
     float b1, b2, eps;
     uint32_t* flag;
+    // Adan instead of Adam (n != null): the third moment and the previous
+    // gradient; consts as ChainState's Adan layout
+    float* n;
+    float* gprev;
+    float b3;
     // chained fit step: project the updated Gaussian for the NEXT step (record,
     // tile count and binning step 1); null proj_out disables
     Proj* proj_out;

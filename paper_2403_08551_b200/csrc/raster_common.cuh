@@ -338,9 +338,15 @@ __device__ __forceinline__ void close_segment(const ChainState& cs, int tt) {
         if (cs.step_counter != nullptr) *cs.step_counter += 1u;
         if (cs.adam_consts != nullptr) {
             const int st = (int)*cs.step_read;
-            cs.adam_consts[0] = ldexpf(cs.lr0, -((st - 1) / cs.half_every));
+            const float lr_t = ldexpf(cs.lr0, -((st - 1) / cs.half_every));
+            cs.adam_consts[0] = lr_t;
             cs.adam_consts[1] = (float)(1.0 / (1.0 - pow((double)cs.b1, (double)st)));
             cs.adam_consts[2] = (float)(1.0 / (1.0 - pow((double)cs.b2, (double)st)));
+            if (cs.adan) {      // the same expressions as adan_kernel's
+                cs.adam_consts[3] = (float)(1.0 / sqrt(1.0 - pow((double)cs.b3, (double)st)));
+                cs.adam_consts[4] = 1.0f - lr_t * cs.wd;
+                cs.adam_consts[5] = st == 1 ? 1.0f : 0.0f;
+            }
         }
     }
 }

@@ -84,6 +84,9 @@ SIGNATURES = {
     "gi_fit_step_adan": (C.c_int, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _i32, _FP, _u32, _i64, _vp,
                                    _sz, _vp, _f32, _i32, _f32, _f32, _f32, _f32, _f32, _vp, _vp,
                                    _vp]),
+    "gi_fit_step_adan_chained": (C.c_int, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _i32, _FP, _u32, _i64, _vp,
+                                   _sz, _vp, _f32, _i32, _f32, _f32, _f32, _f32, _f32, _vp, _vp,
+                                   _vp]),
     "gi_fit_prime": (C.c_int, [_vp, _i32, _FP, _u32, _i64, _vp, _sz, _vp]),
     "gi_fit_step_chained": (C.c_int, [_vp, _vp, _vp, _vp, _vp, _i32, _FP, _u32, _i64, _vp, _sz, _vp,
                                       _f32, _i32, _f32, _f32, _f32, _vp, _vp, _vp, _vp]),
@@ -272,6 +275,20 @@ def gi_fit_step_adan(params, grads, m, v, n, grad_prev, target, n_gauss, f, flag
                                 float(lr0), int(half_every), float(beta1), float(beta2),
                                 float(beta3), float(eps), float(weight_decay), _ptr(loss),
                                 _ptr(status_flags), _stream(stream)), "gi_fit_step_adan")
+
+
+def gi_fit_step_adan_chained(params, grads, m, v, n, grad_prev, target, n_gauss, f, flags,
+                             key_capacity, fit_ws, step_counter, lr0=1e-3, half_every=20000,
+                             beta1=0.98, beta2=0.92, beta3=0.99, eps=1e-8, weight_decay=0.0,
+                             loss=None, status_flags=None, stream=None):
+    _ok(load().gi_fit_step_adan_chained(_ptr(params), _ptr(grads), _ptr(m), _ptr(v), _ptr(n),
+                                        _ptr(grad_prev), _ptr(target), int(n_gauss), C.byref(f),
+                                        int(flags), int(key_capacity), _ptr(fit_ws),
+                                        fit_ws.numel() * fit_ws.element_size(), _ptr(step_counter),
+                                        float(lr0), int(half_every), float(beta1), float(beta2),
+                                        float(beta3), float(eps), float(weight_decay), _ptr(loss),
+                                        _ptr(status_flags), _stream(stream)),
+        "gi_fit_step_adan_chained")
 
 
 def gi_fit_prime(params, n, f, flags, key_capacity, fit_ws, stream=None):

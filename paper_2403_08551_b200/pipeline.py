@@ -114,16 +114,16 @@ class Fitter:
                  beta1: float = 0.9, beta2: float = 0.999, eps: float = 1e-8,
                  flags: int = gi.GI_POS_LOGIT, chained: bool = True, optimizer: str = "adam",
                  beta3: float = 0.99, weight_decay: float = 0.0):
-        """optimizer: "adam" (north_star; fused into finalize) or "adan" (the
-        paper's; separate elementwise kernel, default betas
-        (0.98, 0.92, 0.99) when beta1/beta2 are left at Adam's defaults)."""
+        """optimizer: "adam" (north_star) or "adan" (the paper's, P:381;
+        default betas (0.98, 0.92, 0.99) when beta1/beta2 are left at Adam's
+        defaults); either is fused into the finalize kernel, chained or not."""
         gi.load()
         if optimizer not in ("adam", "adan"):
             raise ValueError("optimizer must be 'adam' or 'adan'")
         self.optimizer = optimizer
         if optimizer == "adan" and (beta1, beta2) == (0.9, 0.999):
             beta1, beta2 = 0.98, 0.92
-        self.chained = bool(chained) and optimizer == "adam"
+        self.chained = bool(chained)
         self.primed = False
         assert params.dim() == 3 and params.shape[2] == 8, "params [B][N][8]"
         B, n = params.shape[0], params.shape[1]
@@ -154,17 +154,16 @@ class Fitter:
         the workspace and every step fuses the next step's projection into
         its Adam kernel; the params must not be written by anyone else in
         between (call unchain() after modifying them)."""
+        if self.chained and not self.primed:
+            gi.gi_fit_prime(self.params, self.n, self.f, self.flags, self.cap, self.fit_ws, stream)
+            self.primed = True
         if self.optimizer == "adan":
-            gi.gi_fit_step_adan(self.params, self.grads, self.m, self.v, self.n_acc, self.grad_prev,
-                                self.target, self.n, self.f, self.flags, self.cap, self.fit_ws,
-                                self.step_counter, loss=self.loss, status_flags=self.status,
-                                stream=stream, **self.hyper, **self.adan_extra)
+            fn = gi.gi_fit_step_adan_chained if self.chained else gi.gi_fit_step_adan
+            fn(self.params, self.grads, self.m, self.v, self.n_acc, self.grad_prev, self.target,
+               self.n, self.f, self.flags, self.cap, self.fit_ws, self.step_counter, loss=self.loss,
+               status_flags=self.status, stream=stream, **self.hyper, **self.adan_extra)
             return
         if self.chained:
-            if not self.primed:
-                gi.gi_fit_prime(self.params, self.n, self.f, self.flags, self.cap, self.fit_ws,
-                                stream)
-                self.primed = True
             gi.gi_fit_step_chained(self.params, self.grads, self.m, self.v, self.target, self.n,
                                    self.f, self.flags, self.cap, self.fit_ws, self.step_counter,
                                    loss=self.loss, status_flags=self.status,

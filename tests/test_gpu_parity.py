@@ -421,6 +421,36 @@ def test_fit_step_adan(gi, gio):
     assert fit.check() == gi.GI_OK and float(fit.loss[0]) < loss
 
 
+def test_adan_fused_matches_kernel_sequence(gi, gio):
+    # NEXT-1: the Adan update fused into finalize -- plain (3 kernels) and
+    # chained (2 kernels) -- is bitwise the standalone sequence
+    # gi_render_backward -> gi_adan_step over 4 steps
+    from paper_2403_08551_b200.pipeline import Fitter, Pipeline
+    W, H, n = 96, 64, 600
+    p = synth.init_params(5, n)
+    tgt = synth.image(5, W, H)
+    res = []
+    for chained in (True, False):
+        fit = Fitter(to_dev(p)[None].contiguous(), to_dev(tgt)[None].contiguous(),
+                     optimizer="adan", chained=chained)
+        for _ in range(4):
+            fit.step()
+        torch.cuda.synchronize()
+        assert fit.check() == gi.GI_OK and fit.steps_done() == 4
+        res.append(fit.params.clone())
+    assert torch.equal(res[0], res[1])
+    pipe = Pipeline(n, W, H, 1, device=DEV)
+    pt = to_dev(p)[None].contiguous()
+    st = {k: torch.zeros_like(pt) for k in ("m", "v", "n", "gp")}
+    t_dev = to_dev(tgt)[None].contiguous()
+    for step in range(1, 5):
+        pipe.render(pt)
+        pipe.backward(pt, target=t_dev)
+        gi.gi_adan_step(pt, pipe.grads, st["m"], st["v"], st["n"], st["gp"], n * 8, step, 1e-3)
+    torch.cuda.synchronize()
+    assert torch.equal(pt, res[1])
+
+
 def test_c3_backward_and_fit_step(gi, gio):
     # configs[2] at full size: fused forward + L2 + backward and one fused fit
     # step (the launch shape of a C3 fit) against the oracle, full gradient
