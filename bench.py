@@ -334,7 +334,7 @@ def main():
     r_kernel_ms /= K
     render_pairs = pairs_of(pipe, np)
 
-    # ---------------- decode FPS (configs[4]): decode -> gi_render_frame ----------------
+    # ---------------- decode FPS (configs[4]): gi_decode_render_frame (decode fused into project) ----
     data, gamma, beta, books = synth.payload(seed, N_GAUSS)
     d_payload = torch.from_numpy(data).to(dev)
     d_books = torch.from_numpy(books).to(dev)
@@ -348,8 +348,7 @@ def main():
     ds.wait_stream(stream)
     dg = torch.cuda.CUDAGraph()
     with torch.cuda.graph(dg, stream=ds):
-        gi.gi_vq_decode(d_payload, meta, dparams)
-        dpipe.render_frame(dparams, gi.GI_POS_NORMALIZED)
+        dpipe.decode_render_frame(d_payload, meta, dparams)
     stream.wait_stream(ds)
     for _ in range(Wm):
         dg.replay()

@@ -274,6 +274,20 @@ typedef struct {
 gi_status gi_vq_decode(const uint8_t* payload, size_t payload_bytes, const gi_codec_meta* meta,
                        float* params, void* stream);
 
+/* Decode + render of one codec frame (configs[4]) in two kernels: the decode
+ * of record g (exactly gi_vq_decode's) is fused into the projection of
+ * Gaussian g (GI_POS_NORMALIZED; a6 + a1 in one pass, no parameter round
+ * trip), then the Eq. 7 render as in gi_render_frame.  f->batch must be 1 and
+ * n = meta->n.  frame_ws: as gi_render_frame (gi_fit_workspace_bytes(n, ...),
+ * zero-filled once).  params [n][8] out (may be NULL): the decoded records,
+ * bit-identical to gi_vq_decode.  image [1][3][H][W] out: bit-identical to
+ * gi_vq_decode followed by gi_render_frame(GI_POS_NORMALIZED).  Errors as
+ * gi_vq_decode and gi_render_frame. */
+gi_status gi_decode_render_frame(const uint8_t* payload, size_t payload_bytes,
+                                 const gi_codec_meta* meta, const gi_frame* f,
+                                 int64_t key_capacity, void* frame_ws, size_t ws_bytes,
+                                 float* params, float* image, void* stream);
+
 /* --- NEXT-2 encoder: attribute quantisation (SPEC quant/codec) ---
  * The inverse of gi_vq_decode: per Gaussian of params [n][8] fp32 (raw
  * positions through tanh unless flags & GI_POS_NORMALIZED; Cholesky l as

@@ -518,6 +518,65 @@ gi_status gi_vq_decode(const uint8_t* payload, size_t payload_bytes, const gi_co
     return cuda_status(gi::launch_vq_decode(payload, *meta, params, S(stream)), "gi_vq_decode");
 }
 
+// Shared gi_codec_meta checks of the decode entry points; rec_out = bits per record.
+static gi_status check_codec(const gi_codec_meta* meta, size_t payload_bytes, int64_t* rec_out) {
+    if (!meta) return invalid("meta is NULL");
+    if (meta->n < 0) return invalid("n");
+    if (meta->bits < 1 || meta->bits > 16 || meta->stages < 1 || meta->stages > 8 ||
+        meta->codebook < 2 || meta->codebook > 256) {
+        std::snprintf(g_err, sizeof(g_err), "codec metadata out of range");
+        return GI_EFORMAT;
+    }
+    int ib = 1;
+    while ((1 << ib) < meta->codebook) ++ib;
+    const int64_t rec = 32 + 3LL * meta->bits + (int64_t)meta->stages * ib;
+    if (rec > 64) {
+        std::snprintf(g_err, sizeof(g_err), "record wider than 64 bits");
+        return GI_EFORMAT;
+    }
+    if ((size_t)((rec * meta->n + 7) / 8) > payload_bytes) {
+        std::snprintf(g_err, sizeof(g_err), "payload shorter than n records");
+        return GI_EFORMAT;
+    }
+    *rec_out = rec;
+    return GI_OK;
+}
+
+gi_status gi_decode_render_frame(const uint8_t* payload, size_t payload_bytes,
+                                 const gi_codec_meta* meta, const gi_frame* f,
+                                 int64_t key_capacity, void* frame_ws, size_t ws_bytes,
+                                 float* params, float* image, void* stream) {
+    gi_status st;
+    int64_t rec = 0;
+    if ((st = check_codec(meta, payload_bytes, &rec)) != GI_OK) return st;
+    if ((st = check_frame(f)) != GI_OK) return st;
+    if (f->batch != 1) return invalid("batch (one image per payload)");
+    const int32_t n = meta->n;
+    if ((st = check_n(n, f)) != GI_OK) return st;
+    if (key_capacity < 0 || key_capacity >= (1LL << 31)) return invalid("key_capacity");
+    if (!frame_ws || ws_bytes < carve_fit(nullptr, n, key_capacity, *f).bytes)
+        return invalid("frame workspace too small");
+    if (!image || (n > 0 && (!payload || !meta->codebooks))) return invalid("NULL buffer");
+    if (!aligned16(params) || !aligned16(frame_ws)) return invalid("alignment");
+    FitWs w = carve_fit(frame_ws, n, key_capacity, *f);
+    cudaStream_t s = S(stream);
+    cudaError_t e;
+#define GI_TRY(expr, where) \
+    if ((e = (expr)) != cudaSuccess) return cuda_status(e, where)
+    const gi::ChainState cs = gi::bin_chain_direct(w.bin_ws, n, key_capacity, *f, w.key_gid, nullptr,
+                                                   w.n_keys, nullptr);
+    GI_TRY(gi::launch_decode_project(payload, *meta, params, *f, w.proj, w.touched,
+                                     gi::ProjectFuse{nullptr, gi::bin_counts_direct(
+                                                                  w.bin_ws, n, key_capacity, *f,
+                                                                  w.key_gid, nullptr)},
+                                     s),
+           "gi_decode_render_frame/decode+project");
+    GI_TRY(gi::launch_render(w.proj, w.key_gid, nullptr, n, *f, false, image, cs, s),
+           "gi_decode_render_frame/render");
+#undef GI_TRY
+    return GI_OK;
+}
+
 gi_status gi_vq_encode(const float* params, uint32_t flags, const gi_codec_meta* meta,
                        uint8_t* payload, size_t payload_bytes, float* eff, void* stream) {
     if (!meta) return invalid("meta is NULL");

@@ -16,6 +16,60 @@ struct QuantParams {
     float gamma[3], beta[3];
 };
 
+// a6. Decode record r of the payload (record layout
+// SPEC.md:404, reading R21) into the parameter records p0 = {u_x, u_y, l1, l2},
+// p1 = {l3, c'}: binary16 positions (exact in fp32), l_i = code_i gamma_i +
+// beta_i (Eq. 8, one fp32 rounding), c' = C^1[i^1] + ... (Eq. 9, fp32, stage
+// order).  R <= 64-bit records are read through a 72-bit big-endian window;
+// sb = the codebooks (stages x codebook x 3 floats), staged in shared memory.
+__device__ __forceinline__ void decode_one(const uint8_t* __restrict__ payload, int r, int rec_bits,
+                                           const QuantParams& qp, const float* sb, float4& p0,
+                                           float4& p1) {
+    const int64_t bit0 = (int64_t)r * rec_bits;
+    const int64_t byte0 = bit0 >> 3;
+    const int sh = (int)(bit0 & 7);
+    const int nbytes = (sh + rec_bits + 7) >> 3;      // bytes the record touches (<= 9)
+    uint64_t hi = 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) hi = (hi << 8) | (i < nbytes ? (uint64_t)payload[byte0 + i] : 0ull);
+    const uint64_t extra = nbytes > 8 ? (uint64_t)payload[byte0 + 8] : 0ull;
+    // window: the record's bits start at the MSB
+    const uint64_t win = sh ? ((hi << sh) | (extra >> (8 - sh))) : hi;
+    int pos = 0;
+    auto take = [&](int width) -> uint32_t {
+        const uint32_t v = (uint32_t)((win << pos) >> (64 - width));
+        pos += width;
+        return v;
+    };
+    const uint32_t hx = take(16), hy = take(16);
+    const float ux = __half2float(__ushort_as_half((unsigned short)hx));
+    const float uy = __half2float(__ushort_as_half((unsigned short)hy));
+    const float l1 = __fmaf_rn((float)take(qp.bits), qp.gamma[0], qp.beta[0]);
+    const float l2 = __fmaf_rn((float)take(qp.bits), qp.gamma[1], qp.beta[1]);
+    const float l3 = __fmaf_rn((float)take(qp.bits), qp.gamma[2], qp.beta[2]);
+    float c0 = 0.f, c1 = 0.f, c2 = 0.f;
+    for (int m = 0; m < qp.stages; ++m) {
+        const uint32_t idx = take(qp.ib);
+        const float* cw = sb + (m * qp.codebook + (int)idx) * 3;
+        if (m == 0) {
+            c0 = cw[0]; c1 = cw[1]; c2 = cw[2];
+        } else {
+            c0 = __fadd_rn(c0, cw[0]); c1 = __fadd_rn(c1, cw[1]); c2 = __fadd_rn(c2, cw[2]);
+        }
+    }
+    p0 = make_float4(ux, uy, l1, l2);
+    p1 = make_float4(l3, c0, c1, c2);
+}
+
+// Codec source of the fused decode + projection (gi_decode_render_frame).
+struct DecodeSrc {
+    const uint8_t* payload;
+    const float* books;       // device [stages][codebook][3]
+    int rec_bits;
+    QuantParams qp;
+    float4* params_out;       // decoded records [n][8], or null
+};
+
 // Returns the record (MSB-first, 32 + 3 bits + stages ib bits) and the
 // dequantised parameters e0, e1 (= what vq_decode returns); on_stage(m, i^m,
 // residual r = c' - c^^{m-1}, C^m[i^m]) is called per RVQ stage.

@@ -78,6 +78,23 @@ cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, cudaStre
     return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
 }
 
+// launch_pdl with dynamic shared memory.
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl_smem(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                            cudaStream_t s, Args&&... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = use_pdl() ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
+
 __device__ __forceinline__ unsigned lanemask_lt() {
     unsigned m;
     asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
@@ -402,6 +419,11 @@ cudaError_t launch_vq_encode(const float* params, bool logit, const gi_codec_met
                              uint8_t* payload, float* eff, cudaStream_t s);
 cudaError_t launch_vq_decode(const uint8_t* payload, const gi_codec_meta& meta, float* params,
                              cudaStream_t s);
+// a6 + a1 fused (gi_decode_render_frame): decode record g and project it in
+// one thread, direct binning as in launch_project; params_out may be null.
+cudaError_t launch_decode_project(const uint8_t* payload, const gi_codec_meta& meta,
+                                  float* params_out, const gi_frame& f, Proj* proj,
+                                  uint32_t* tiles_touched, const ProjectFuse& fuse, cudaStream_t s);
 cudaError_t launch_psnr(const float* image, const float* target, const gi_frame& f, float* psnr,
                         void* ws, cudaStream_t s);
 

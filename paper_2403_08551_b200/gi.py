@@ -92,6 +92,8 @@ SIGNATURES = {
                                       _f32, _i32, _f32, _f32, _f32, _vp, _vp, _vp, _vp]),
     "gi_render_frame": (C.c_int, [_vp, _i32, _FP, _u32, _i64, _vp, _sz, _vp, _vp]),
     "gi_vq_decode": (C.c_int, [_vp, _sz, C.POINTER(gi_codec_meta), _vp, _vp]),
+    "gi_decode_render_frame": (C.c_int, [_vp, _sz, C.POINTER(gi_codec_meta), _FP, _i64, _vp, _sz,
+                                         _vp, _vp, _vp]),
     "gi_vq_encode": (C.c_int, [_vp, C.c_uint32, C.POINTER(gi_codec_meta), _vp, _sz, _vp, _vp]),
     "gi_kmeans_workspace_bytes": (_sz, [C.c_int32]),
     "gi_qat_workspace_bytes": (_sz, [C.c_int32, C.c_int64, C.POINTER(gi_frame),
@@ -358,6 +360,15 @@ def gi_fit_grads(params, grads, target, n, f: gi_frame, flags, tile_row0, tile_r
 def gi_vq_decode(payload, meta: gi_codec_meta, params, stream=None):
     _ok(load().gi_vq_decode(_ptr(payload), payload.numel() * payload.element_size(), C.byref(meta), _ptr(params),
                             _stream(stream)), "gi_vq_decode")
+
+
+def gi_decode_render_frame(payload, meta: gi_codec_meta, f: gi_frame, key_capacity, frame_ws,
+                           image, params=None, stream=None):
+    """configs[4] in two kernels: decode fused into the projection, then render."""
+    _ok(load().gi_decode_render_frame(_ptr(payload), payload.numel() * payload.element_size(),
+                                      C.byref(meta), C.byref(f), int(key_capacity), _ptr(frame_ws),
+                                      frame_ws.numel() * frame_ws.element_size(), _ptr(params),
+                                      _ptr(image), _stream(stream)), "gi_decode_render_frame")
 
 
 def gi_psnr(image, target, f, psnr, ws, stream=None):

@@ -80,6 +80,15 @@ class Pipeline:
         gi.gi_render_frame(params, self.n, self.f, flags, self.cap, self.frame_ws, self.image, stream)
         return self.image
 
+    def decode_render_frame(self, payload, meta, params_out=None, stream=None) -> torch.Tensor:
+        """configs[4]: gi_decode_render_frame (decode fused into the
+        projection, then render) into self.image; params_out optional."""
+        if not hasattr(self, "frame_ws"):
+            self.frame_ws = _bytes(gi.gi_fit_workspace_bytes(self.n, self.cap, self.f), self.device)
+        gi.gi_decode_render_frame(payload, meta, self.f, self.cap, self.frame_ws, self.image,
+                                  params_out, stream)
+        return self.image
+
     def frame_keys(self) -> int:
         ptr = gi.gi_fit_n_keys(self.frame_ws, self.n, self.cap, self.f)
         off = (ptr - self.frame_ws.data_ptr()) // 4

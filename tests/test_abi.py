@@ -56,6 +56,18 @@ def test_host_queries_and_validation(lib):
     assert lib.gi_vq_decode(None, 0, C.byref(meta), None, None) == gi.GI_EFORMAT
     meta.bits = 6
     assert lib.gi_vq_decode(None, 69, C.byref(meta), None, None) == gi.GI_EFORMAT  # needs 70 B
+    # fused decode + render: codec checks, one image per payload, buffers
+    f1, f2b = gi.frame(768, 512), gi.frame(768, 512, batch=2)
+    meta.bits = 20
+    assert lib.gi_decode_render_frame(None, 0, C.byref(meta), C.byref(f1), 1 << 16, None, 0, None,
+                                      None, None) == gi.GI_EFORMAT
+    meta.bits = 6
+    assert lib.gi_decode_render_frame(None, 69, C.byref(meta), C.byref(f1), 1 << 16, None, 0, None,
+                                      None, None) == gi.GI_EFORMAT
+    assert lib.gi_decode_render_frame(None, 70, C.byref(meta), C.byref(f2b), 1 << 16, None, 0, None,
+                                      None, None) == gi.GI_EINVAL
+    assert lib.gi_decode_render_frame(None, 70, C.byref(meta), C.byref(f1), 1 << 16, None, 0, None,
+                                      None, None) == gi.GI_EINVAL        # no workspace
     assert lib.gi_status_string(3) == b"GI_ECAPACITY"
     # NEXT-2 / NEXT-4 entry points validate before any launch
     meta.bits = 20

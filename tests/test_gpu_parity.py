@@ -309,6 +309,41 @@ def test_decode_then_render(gi, gio):
     assert np.abs(img[0].cpu().numpy() - ref).max() <= PIX_TOL
 
 
+@pytest.mark.parametrize("n", [4500, 70000])
+def test_decode_render_frame_fused(gi, gio, n):
+    # configs[4] in two kernels (decode fused into the projection): image and
+    # decoded params bitwise those of gi_vq_decode -> gi_render_frame, and the
+    # image within the pixel bar of the oracle's decode -> render
+    from paper_2403_08551_b200.pipeline import Pipeline
+    W, H = 768, 512
+    data, gamma, beta, books = synth.payload(4, n)
+    bk = to_dev(books)
+    meta = gi.codec_meta(n, gamma, beta, bk)
+    pay = to_dev(data)
+    p_ref = torch.zeros(1, n, 8, dtype=torch.float32, device=DEV)
+    gi.gi_vq_decode(pay, meta, p_ref)
+    a = Pipeline(n, W, H, 1, device=DEV)
+    img_ref = a.render_frame(p_ref, gi.GI_POS_NORMALIZED).clone()
+    b = Pipeline(n, W, H, 1, device=DEV)
+    p_out = torch.full((1, n, 8), float("nan"), dtype=torch.float32, device=DEV)
+    for _ in range(2):                      # counters left zeroed for the next frame
+        img = b.decode_render_frame(pay, meta, p_out).clone()
+        torch.cuda.synchronize()
+        assert torch.equal(img, img_ref)
+        assert torch.equal(p_out, p_ref)
+    b.decode_render_frame(pay, meta)        # params output is optional
+    torch.cuda.synchronize()
+    assert torch.equal(b.image, img_ref)
+    assert b.frame_keys() == a.frame_keys()
+    if n <= 4500:
+        ref_p = gio.vq_decode(data, n, gamma, beta, books)
+        ref = gio.render(ref_p, W, H, pos_mode=gio.POS_NORMALIZED, mode=gio.TILED)
+        assert np.abs(img[0].cpu().numpy() - ref).max() <= PIX_TOL
+    with pytest.raises(RuntimeError):       # one image per payload
+        bad = Pipeline(n, W, H, 2, device=DEV)
+        bad.decode_render_frame(pay, meta)
+
+
 def test_fit_step_matches_oracle(gi, gio):
     # one fused device step (project, bin, fwd+L2+bwd, Adam) from a fresh state
     from paper_2403_08551_b200.pipeline import Fitter
