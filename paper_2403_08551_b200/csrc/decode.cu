@@ -112,15 +112,17 @@ __global__ void __launch_bounds__(256) kmeans_assign_kernel(const float* __restr
             }
         }
         if (assign != nullptr) assign[i] = (uint32_t)best;
-        atomicAdd(&sa[4 * best + 0], (unsigned long long)__double2ll_rn((double)x0 * kFix));
-        atomicAdd(&sa[4 * best + 1], (unsigned long long)__double2ll_rn((double)x1 * kFix));
-        atomicAdd(&sa[4 * best + 2], (unsigned long long)__double2ll_rn((double)x2 * kFix));
-        atomicAdd(&sa[4 * best + 3], 1ull);
+        uint32_t* a = reinterpret_cast<uint32_t*>(sa) + 8 * best;   // (lo, hi) pairs
+        shared_add_u64(a + 0, (unsigned long long)__double2ll_rn((double)x0 * kFix));
+        shared_add_u64(a + 2, (unsigned long long)__double2ll_rn((double)x1 * kFix));
+        shared_add_u64(a + 4, (unsigned long long)__double2ll_rn((double)x2 * kFix));
+        atomicAdd(a + 6, 1u);
     }
     __syncthreads();
+    const uint32_t* sp = reinterpret_cast<const uint32_t*>(sa);
     for (int k = threadIdx.x; k < B; k += blockDim.x)
-        if (sa[4 * k + 3] != 0ull)
-            for (int j = 0; j < 4; ++j) atomicAdd(&acc[4 * k + j], sa[4 * k + j]);
+        if (shared_read_u64(sp + 8 * k + 6) != 0ull)
+            for (int j = 0; j < 4; ++j) atomicAdd(&acc[4 * k + j], shared_read_u64(sp + 8 * k + 2 * j));
 }
 
 // New centroids (empty clusters keep theirs, reading R31); re-zeroes acc.

@@ -95,6 +95,24 @@ cudaError_t launch_pdl_smem(void (*kernel)(KArgs...), dim3 grid, dim3 block, siz
     return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
 }
 
+// 64-bit integer add into a shared-memory (lo, hi) word pair by two native
+// 32-bit atomics: exact mod 2^64 and order-independent like a 64-bit atomic
+// add, without the compare-and-swap loop the compiler emits for 64-bit shared
+// atomics (each wrap of the low word is seen as the carry of exactly one add).
+__device__ __forceinline__ void shared_add_u64(uint32_t* pair, unsigned long long v) {
+    const uint32_t lo = (uint32_t)v;
+    uint32_t hi = (uint32_t)(v >> 32);
+    if (lo != 0u) {
+        const uint32_t old = atomicAdd(&pair[0], lo);
+        hi += (uint32_t)(old + lo < old);
+    }
+    if (hi != 0u) atomicAdd(&pair[1], hi);
+}
+
+__device__ __forceinline__ unsigned long long shared_read_u64(const uint32_t* pair) {
+    return (unsigned long long)pair[1] << 32 | pair[0];
+}
+
 __device__ __forceinline__ unsigned lanemask_lt() {
     unsigned m;
     asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));

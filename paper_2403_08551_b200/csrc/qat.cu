@@ -32,7 +32,7 @@ __global__ void __launch_bounds__(256) qat_quantize_kernel(
     float* __restrict__ consts, float lr, float b1, float b2) {
     extern __shared__ unsigned long long dyn[];     // [nb][5] accumulators, then [nb][3] books
     const int nb = qp.stages * qp.codebook;
-    unsigned long long* sa = dyn;
+    uint32_t* sa = reinterpret_cast<uint32_t*>(dyn);   // (lo, hi) pairs
     float* sb = reinterpret_cast<float*>(dyn + (size_t)nb * 5);
 #pragma unroll
     for (int j = 0; j < 3; ++j) {          // gamma / beta live on the device (updated each step)
@@ -40,7 +40,7 @@ __global__ void __launch_bounds__(256) qat_quantize_kernel(
         qp.beta[j] = qparams[3 + j];
     }
     for (int i = threadIdx.x; i < nb * 3; i += blockDim.x) sb[i] = books[i];
-    for (int i = threadIdx.x; i < nb * 5; i += blockDim.x) sa[i] = 0ull;
+    for (int i = threadIdx.x; i < nb * 5 * 2; i += blockDim.x) sa[i] = 0u;
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         const uint32_t t = *step + 1u;
         *step = t;
@@ -54,22 +54,22 @@ __global__ void __launch_bounds__(256) qat_quantize_kernel(
         float4 e0, e1;
         encode_one(params[2 * (size_t)i], params[2 * (size_t)i + 1], true, qp, sb, e0, e1,
                    [&](int m, int k, float r0, float r1, float r2, const float* cw) {
-                       unsigned long long* a = sa + (m * qp.codebook + k) * 5;
-                       atomicAdd(a + 0, fix(r0, kFixR));
-                       atomicAdd(a + 1, fix(r1, kFixR));
-                       atomicAdd(a + 2, fix(r2, kFixR));
-                       atomicAdd(a + 3, 1ull);
+                       uint32_t* a = sa + (m * qp.codebook + k) * 10;
+                       shared_add_u64(a + 0, fix(r0, kFixR));
+                       shared_add_u64(a + 2, fix(r1, kFixR));
+                       shared_add_u64(a + 4, fix(r2, kFixR));
+                       atomicAdd(a + 6, 1u);      // counts stay far below 2^32
                        const double d0 = (double)r0 - cw[0], d1 = (double)r1 - cw[1],
                                     d2 = (double)r2 - cw[2];
-                       atomicAdd(a + 4, fix(d0 * d0 + d1 * d1 + d2 * d2, kFixC));
+                       shared_add_u64(a + 8, fix(d0 * d0 + d1 * d1 + d2 * d2, kFixC));
                    });
         eff[2 * (size_t)i] = e0;
         eff[2 * (size_t)i + 1] = e1;
     }
     __syncthreads();
     for (int k = threadIdx.x; k < nb; k += blockDim.x)
-        if (sa[5 * k + 3] != 0ull)
-            for (int j = 0; j < 5; ++j) atomicAdd(&acc[5 * k + j], sa[5 * k + j]);
+        if (shared_read_u64(sa + 10 * k + 6) != 0ull)
+            for (int j = 0; j < 5; ++j) atomicAdd(&acc[5 * k + j], shared_read_u64(sa + 10 * k + 2 * j));
 }
 
 __device__ __forceinline__ float adam_step(float p, float g, float& m, float& v, float b1, float b2,
