@@ -14,11 +14,11 @@
 // coordinates (StagedRecords below: conic + colour, centre minus the tile
 // origin -- ix - tx0 is an exact small integer, + fx rounds once -- and the
 // box clipped to the tile).  Each warp then compacts the batch into its own
-// candidate list: the record index + the 32-bit mask of its lanes
-// whose pixel lies in the box, so the inner loop needs no bit scanning and a
-// one-instruction box test.  The box
-// is staged as 16-bit column / row masks of the tile, so a warp's 32-lane
-// mask is two bit-field extracts and two multiplies.
+// candidate list: the record index + the 32-bit mask of its lanes whose pixel
+// lies in the box, so the inner loop needs no bit scanning and a
+// one-instruction box test.  The box is staged as 16-bit column / row masks of
+// the tile, so a warp's 32-lane mask is two bit-field extracts and two
+// multiplies.
 #pragma once
 #include "gi_internal.cuh"
 
