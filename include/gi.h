@@ -243,6 +243,34 @@ gi_status gi_fit_grads(const float* params, float* grads, const float* target, i
                        int64_t key_capacity, void* fit_ws, size_t ws_bytes, float* loss,
                        void* stream);
 
+/* --- NEXT-4 gradient exchange over peer memory -----------------------------
+ * The exchange of spatial sharding fused with the optimiser: each of G ranks
+ * (one process per GPU of a node, NVLink/NVSwitch peers) writes its window's
+ * gradients ([B][n][8] fp32, `count` floats) followed by its n_loss loss
+ * floats into an exchange buffer from gi_peer_alloc; the ranks swap the
+ * 64-byte IPC handles (any host channel, e.g. torch.distributed) and map each
+ * other's buffers with gi_peer_open.  gi_peer_adam_step then reads the G
+ * buffers (grads[r], rank order r = 0 .. G-1, the same array on every rank),
+ * sums them elementwise in that order -- so every rank computes identical
+ * sums and the replicas stay bit-identical -- and applies Adam with
+ * gi_adam_step's arithmetic (bit-identical to gi_adam_step on the summed
+ * gradient); loss_out[j] = sum_r grads[r][count + j].  The caller orders the
+ * ranks around the step (every rank's gradients complete before any rank
+ * reads them; every read complete before the next step overwrites them):
+ * a barrier of its host channel after a stream sync, on both sides.
+ * G <= 8, n_loss <= 32; buffers 16-B aligned (gi_peer_alloc's are).
+ * gi_peer_alloc: cudaMalloc of `bytes` (zero-filled) + its IPC handle
+ * (handle: 64 bytes out); gi_peer_open: map a peer's handle (not one of this
+ * process's own allocations); gi_peer_close / gi_peer_free undo them. */
+gi_status gi_peer_alloc(size_t bytes, void** ptr, void* handle);
+gi_status gi_peer_free(void* ptr);
+gi_status gi_peer_open(const void* handle, void** ptr);
+gi_status gi_peer_close(void* ptr);
+gi_status gi_peer_adam_step(float* params, float* m, float* v, const float* const* grads,
+                            int32_t G, int64_t count, int32_t step, float lr, float beta1,
+                            float beta2, float eps, int32_t n_loss, float* loss_out,
+                            uint32_t* nonfinite_flag, void* stream);
+
 /* --- fused render of a frame (graph-capturable) ---------------------------
  * project (+ per-tile counts) -> bin -> Eq. 7 render in one call; the per-tile
  * gid ordering of binning happens inside the render kernel.  Same workspace

@@ -11,12 +11,7 @@ namespace {
 __device__ __forceinline__ float adam1(float& p, float g, float& m, float& v, float b1, float b2,
                                        float omb1, float omb2, float lr, float ibc1, float ibc2,
                                        float eps) {
-    m = fmaf(b1, m, omb1 * g);
-    v = fmaf(b2, v, omb2 * (g * g));
-    const float mhat = m * ibc1;
-    const float vhat = v * ibc2;
-    p = p - lr * mhat / (sqrtf(vhat) + eps);
-    return p;
+    return adam_update(p, g, m, v, b1, b2, omb1, omb2, lr, ibc1, ibc2, eps);
 }
 
 __global__ void __launch_bounds__(256) adam_kernel(float4* __restrict__ p, const float4* __restrict__ g,

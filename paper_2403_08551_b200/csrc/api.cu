@@ -210,6 +210,49 @@ gi_status gi_adam_step(float* params, const float* grads, float* m, float* v, in
                        "gi_adam_step");
 }
 
+// --- NEXT-4 peer exchange ------------------------------------------------
+gi_status gi_peer_alloc(size_t bytes, void** ptr, void* handle) {
+    if (!ptr || !handle || bytes == 0) return invalid("NULL argument or zero size");
+    *ptr = nullptr;
+    cudaError_t e = cudaMalloc(ptr, bytes);
+    if (e != cudaSuccess) return cuda_status(e, "gi_peer_alloc");
+    if ((e = cudaMemset(*ptr, 0, bytes)) != cudaSuccess) return cuda_status(e, "gi_peer_alloc");
+    cudaIpcMemHandle_t h;
+    if ((e = cudaIpcGetMemHandle(&h, *ptr)) != cudaSuccess) return cuda_status(e, "gi_peer_alloc");
+    std::memcpy(handle, &h, sizeof(h));
+    return GI_OK;
+}
+
+gi_status gi_peer_free(void* ptr) { return cuda_status(cudaFree(ptr), "gi_peer_free"); }
+
+gi_status gi_peer_open(const void* handle, void** ptr) {
+    if (!ptr || !handle) return invalid("NULL argument");
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handle, sizeof(h));
+    return cuda_status(cudaIpcOpenMemHandle(ptr, h, cudaIpcMemLazyEnablePeerAccess), "gi_peer_open");
+}
+
+gi_status gi_peer_close(void* ptr) { return cuda_status(cudaIpcCloseMemHandle(ptr), "gi_peer_close"); }
+
+gi_status gi_peer_adam_step(float* params, float* m, float* v, const float* const* grads,
+                            int32_t G, int64_t count, int32_t step, float lr, float beta1,
+                            float beta2, float eps, int32_t n_loss, float* loss_out,
+                            uint32_t* nonfinite_flag, void* stream) {
+    if (count < 0) return invalid("count");
+    if (G < 1 || G > gi::kMaxPeers) return invalid("G must be 1..8");
+    if (n_loss < 0 || n_loss > 32) return invalid("n_loss must be 0..32");
+    if (step < 1) return invalid("step is 1-based");
+    if (!(beta1 >= 0.f && beta1 < 1.f && beta2 >= 0.f && beta2 < 1.f)) return invalid("betas");
+    if (!grads) return invalid("NULL buffer");
+    for (int r = 0; r < G; ++r)
+        if (!grads[r] || !aligned16(grads[r])) return invalid("grads[r] NULL or unaligned");
+    if (count > 0 && (!params || !m || !v)) return invalid("NULL buffer");
+    if (!aligned16(params) || !aligned16(m) || !aligned16(v)) return invalid("alignment");
+    return cuda_status(gi::launch_peer_adam(params, m, v, grads, G, count, step, lr, beta1, beta2,
+                                            eps, n_loss, loss_out, nonfinite_flag, S(stream)),
+                       "gi_peer_adam_step");
+}
+
 gi_status gi_adan_step(float* params, const float* grads, float* m, float* v, float* n,
                        float* grad_prev, int64_t count, int32_t step, float lr, float beta1,
                        float beta2, float beta3, float eps, float weight_decay,

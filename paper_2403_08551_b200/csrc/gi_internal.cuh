@@ -325,6 +325,20 @@ struct ChainState {
     float b3, wd;
 };
 
+// One Adam update of a scalar (a5, reading R16): the arithmetic of
+// gi_adam_step, shared with the peer-exchange step (NEXT-4) so the two agree
+// bit for bit.
+__device__ __forceinline__ float adam_update(float& p, float g, float& m, float& v, float b1,
+                                             float b2, float omb1, float omb2, float lr, float ibc1,
+                                             float ibc2, float eps) {
+    m = fmaf(b1, m, omb1 * g);
+    v = fmaf(b2, v, omb2 * (g * g));
+    const float mhat = m * ibc1;
+    const float vhat = v * ibc2;
+    p = p - lr * mhat / (sqrtf(vhat) + eps);
+    return p;
+}
+
 // Adan step constants for step t (1-based), as the standalone adan_kernel and
 // the fused finalize use them.
 struct AdanConsts {
@@ -435,6 +449,12 @@ cudaError_t launch_kmeans_step(const float* points, int n, int B, float* centroi
                                uint32_t* assign, void* ws, cudaStream_t s);
 cudaError_t launch_vq_encode(const float* params, bool logit, const gi_codec_meta& meta,
                              uint8_t* payload, float* eff, cudaStream_t s);
+// NEXT-4 peer exchange: g = sum over r of grads[r] (rank order) then Adam;
+// the n_loss floats after each rank's count gradients are summed into loss_out.
+constexpr int kMaxPeers = 8;
+cudaError_t launch_peer_adam(float* params, float* m, float* v, const float* const* grads, int G,
+                             int64_t count, int step, float lr, float b1, float b2, float eps,
+                             int n_loss, float* loss_out, uint32_t* flag, cudaStream_t s);
 cudaError_t launch_vq_decode(const uint8_t* payload, const gi_codec_meta& meta, float* params,
                              cudaStream_t s);
 // a6 + a1 fused (gi_decode_render_frame): decode record g and project it in

@@ -105,11 +105,18 @@ class SpatialFitter:
     (gi_adam_step), so the replicas stay bit-identical.
 
     grad_fn(params, row0, rows) -> (grads, loss) may replace the libgi call
-    (CPU tests of the collective plumbing)."""
+    (CPU tests of the collective plumbing).
+
+    exchange="peer" (GPU ranks of one node): instead of all_reduce + Adam,
+    every rank writes its window's gradients and loss into an IPC-mapped
+    exchange buffer (gi_peer_alloc / gi_peer_open, handles swapped over the
+    process group) and gi_peer_adam_step sums the G buffers in rank order and
+    applies Adam in one kernel, reading the peers' gradients over NVLink.  The
+    process group only carries the handles and the two barriers per step."""
 
     def __init__(self, params: torch.Tensor, target: torch.Tensor, rank: int = 0, world: int = 1,
                  k: float = 3.0, key_capacity: int | None = None, lr0: float = 1e-3,
-                 half_every: int = 20000, grad_fn=None, flags: int = 0):
+                 half_every: int = 20000, grad_fn=None, flags: int = 0, exchange: str = "nccl"):
         self.rank, self.world = int(rank), int(world)
         self.params = params.contiguous()
         self.target = target.contiguous()
@@ -131,6 +138,32 @@ class SpatialFitter:
             self.f = gi.frame(W, H, 1, k)
             self.cap = int(key_capacity) if key_capacity else default_capacity(self.n, 1)
             self.ws = _bytes(gi.gi_fit_workspace_bytes(self.n, self.cap, self.f), self.params.device)
+        if exchange not in ("nccl", "peer"):
+            raise ValueError("exchange must be 'nccl' or 'peer'")
+        self.exchange = exchange
+        if exchange == "peer":
+            if grad_fn is not None:
+                raise ValueError("the peer exchange runs on libgi device buffers")
+            self.count = self.params.numel()
+            self.buf, handle = self.gi.gi_peer_alloc(4 * (self.count + 1))
+            handles = [handle]
+            if self.world > 1:
+                handles = [None] * self.world
+                dist.all_gather_object(handles, handle)
+            self.peers = [self.buf if r == self.rank else self.gi.gi_peer_open(handles[r])
+                          for r in range(self.world)]
+
+    def close(self):
+        """Unmap the peers' exchange buffers and free this rank's (peer mode)."""
+        if getattr(self, "exchange", "nccl") == "peer" and self.buf:
+            if self.world > 1:
+                torch.cuda.synchronize()
+                dist.barrier()
+            for r, ptr in enumerate(self.peers):
+                if r != self.rank:
+                    self.gi.gi_peer_close(ptr)
+            self.gi.gi_peer_free(self.buf)
+            self.buf = 0
 
     def local_grads(self):
         r0, rows = self.window
@@ -142,7 +175,26 @@ class SpatialFitter:
         self.gi.gi_fit_grads(self.params, self.grads, self.target, self.n, self.f, self.flags, r0,
                              rows, self.cap, self.ws, self.loss)
 
+    def _peer_step(self):
+        r0, rows = self.window
+        # this rank's window gradients + loss into its exchange buffer
+        self.gi.gi_fit_grads(self.params, self.buf, self.target, self.n, self.f, self.flags, r0,
+                             rows, self.cap, self.ws, self.buf + 4 * self.count)
+        if self.world > 1:                 # every rank's buffer complete
+            torch.cuda.synchronize()
+            dist.barrier()
+        self.t += 1
+        lr = self.lr0 * 0.5 ** ((self.t - 1) // self.half_every)
+        self.gi.gi_peer_adam_step(self.params, self.m, self.v, self.peers, self.count, self.t, lr,
+                                  n_loss=1, loss_out=self.loss)
+        if self.world > 1:                 # every peer read done before the next overwrite
+            torch.cuda.synchronize()
+            dist.barrier()
+
     def step(self):
+        if self.exchange == "peer":
+            self._peer_step()
+            return
         self.local_grads()
         if self.world > 1:
             dist.all_reduce(self.grads, op=dist.ReduceOp.SUM)

@@ -76,6 +76,12 @@ SIGNATURES = {
     "gi_fit_n_keys": (_vp, [_vp, _i32, _i64, _FP]),
     "gi_fit_grads": (C.c_int, [_vp, _vp, _vp, C.c_int32, C.POINTER(gi_frame), C.c_uint32, C.c_int32,
                                C.c_int32, C.c_int64, _vp, _sz, _vp, _vp]),
+    "gi_peer_alloc": (C.c_int, [_sz, C.POINTER(_vp), _vp]),
+    "gi_peer_free": (C.c_int, [_vp]),
+    "gi_peer_open": (C.c_int, [_vp, C.POINTER(_vp)]),
+    "gi_peer_close": (C.c_int, [_vp]),
+    "gi_peer_adam_step": (C.c_int, [_vp, _vp, _vp, C.POINTER(_vp), C.c_int32, _i64, C.c_int32,
+                                    _f32, _f32, _f32, _f32, C.c_int32, _vp, _vp, _vp]),
     "gi_fit_step": (C.c_int, [_vp, _vp, _vp, _vp, _vp, _i32, _FP, _u32, _i64, _vp, _sz, _vp,
                               _f32, _i32, _f32, _f32, _f32, _vp, _vp, _vp, _vp]),
     "gi_launch_count": (_i64, []),
@@ -355,6 +361,40 @@ def gi_fit_grads(params, grads, target, n, f: gi_frame, flags, tile_row0, tile_r
                             int(flags), int(tile_row0), int(tile_rows), int(key_capacity),
                             _ptr(fit_ws), fit_ws.numel() * fit_ws.element_size(), _ptr(loss),
                             _stream(stream)), "gi_fit_grads")
+
+
+# --- NEXT-4 peer exchange (see gi.h) ---------------------------------------
+def gi_peer_alloc(nbytes: int):
+    """cudaMalloc'd, zero-filled exchange buffer: (device pointer, 64-byte IPC handle)."""
+    ptr = C.c_void_p()
+    h = C.create_string_buffer(64)
+    _ok(load().gi_peer_alloc(int(nbytes), C.byref(ptr), h), "gi_peer_alloc")
+    return int(ptr.value), bytes(h.raw)
+
+
+def gi_peer_free(ptr: int):
+    _ok(load().gi_peer_free(ptr), "gi_peer_free")
+
+
+def gi_peer_open(handle: bytes) -> int:
+    ptr = C.c_void_p()
+    _ok(load().gi_peer_open(C.create_string_buffer(bytes(handle), 64), C.byref(ptr)),
+        "gi_peer_open")
+    return int(ptr.value)
+
+
+def gi_peer_close(ptr: int):
+    _ok(load().gi_peer_close(ptr), "gi_peer_close")
+
+
+def gi_peer_adam_step(params, m, v, grad_ptrs, count, step, lr, beta1=0.9, beta2=0.999, eps=1e-8,
+                      n_loss=0, loss_out=None, nonfinite_flag=None, stream=None):
+    """Sum the G exchange buffers (rank order) and apply Adam (NEXT-4)."""
+    arr = (_vp * len(grad_ptrs))(*[_ptr(g) for g in grad_ptrs])
+    _ok(load().gi_peer_adam_step(_ptr(params), _ptr(m), _ptr(v), arr, len(grad_ptrs), int(count),
+                                 int(step), float(lr), float(beta1), float(beta2), float(eps),
+                                 int(n_loss), _ptr(loss_out), _ptr(nonfinite_flag),
+                                 _stream(stream)), "gi_peer_adam_step")
 
 
 def gi_vq_decode(payload, meta: gi_codec_meta, params, stream=None):

@@ -919,6 +919,104 @@ def test_spatial_fitter_single_rank(gi, gio):
     assert abs(float(a.loss[0]) - float(b.loss[0])) <= 1e-5 * float(b.loss[0])
 
 
+def test_peer_adam_step_local(gi):
+    # NEXT-4 exchange kernel with G local buffers: the rank-order sum followed
+    # by Adam is bitwise gi_adam_step on that sum; the loss tail is summed
+    rng = np.random.default_rng(41)
+    count = 8 * 1001
+    p0 = to_dev(rng.normal(size=count).astype(np.float32))
+    bufs = [to_dev(rng.normal(size=count + 2).astype(np.float32)) for _ in range(3)]
+    for G in (1, 3):
+        p, m, v = p0.clone(), torch.zeros_like(p0), torch.zeros_like(p0)
+        q, mq, vq = p0.clone(), torch.zeros_like(p0), torch.zeros_like(p0)
+        loss = torch.zeros(2, device=DEV)
+        for step in (1, 2):
+            gi.gi_peer_adam_step(p, m, v, [b.data_ptr() for b in bufs[:G]], count, step, 1e-3,
+                                 n_loss=2, loss_out=loss)
+            gsum = bufs[0][:count].clone()
+            for b in bufs[1:G]:
+                gsum += b[:count]
+            gi.gi_adam_step(q, gsum, mq, vq, count, step, 1e-3)
+        torch.cuda.synchronize()
+        assert torch.equal(p, q) and torch.equal(m, mq) and torch.equal(v, vq)
+        lsum = bufs[0][count:].clone()
+        for b in bufs[1:G]:
+            lsum += b[count:]
+        assert torch.equal(loss, lsum)
+    ptr, handle = gi.gi_peer_alloc(4096)
+    assert len(handle) == 64
+    gi.gi_peer_free(ptr)
+
+
+def _peer_worker(rank, world, port, p, tgt, steps, q):
+    import os
+    import torch.distributed as dist
+    from paper_2403_08551_b200.dist import SpatialFitter
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    torch.cuda.set_device(0)                   # both ranks on the one GPU: the IPC plumbing
+    f = SpatialFitter(torch.from_numpy(p).cuda()[None].contiguous(),
+                      torch.from_numpy(tgt).cuda()[None].contiguous(), rank=rank, world=world,
+                      exchange="peer")
+    for _ in range(steps):
+        f.step()
+    torch.cuda.synchronize()
+    q.put((rank, f.params.cpu().numpy(), float(f.loss[0])))
+    f.close()
+    dist.destroy_process_group()
+
+
+def test_spatial_peer_exchange_two_processes(gi, gio):
+    # NEXT-4 over peer memory end to end: two processes (gloo for the handle
+    # exchange and the barriers; both on this GPU -- no kernel waits on the
+    # other process) run 3 peer-exchange steps; both replicas equal, bitwise,
+    # the same 3 steps computed in one process (window gradients of both row
+    # windows -> gi_peer_adam_step over the two buffers)
+    import socket
+    import torch.multiprocessing as mp
+    from paper_2403_08551_b200.dist import row_windows
+    from paper_2403_08551_b200.pipeline import _bytes, default_capacity
+    W, H, n, steps = 96, 64, 600, 3
+    p = synth.init_params(12, n)
+    tgt = synth.image(12, W, H)
+    sock = socket.socket()
+    sock.bind(("127.0.0.1", 0))
+    port = sock.getsockname()[1]
+    sock.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_peer_worker, args=(r, 2, port, p, tgt, steps, q)) for r in range(2)]
+    for pr in procs:
+        pr.start()
+    res = dict((r, (pp, ll)) for r, pp, ll in (q.get(timeout=300) for _ in range(2)))
+    for pr in procs:
+        pr.join(timeout=120)
+        assert pr.exitcode == 0
+    assert np.array_equal(res[0][0], res[1][0]) and res[0][1] == res[1][1]
+    # single-process reference
+    f = gi.frame(W, H, 1)
+    cap = default_capacity(n, 1)
+    ws = _bytes(gi.gi_fit_workspace_bytes(n, cap, f), DEV)
+    prm = to_dev(p)[None].contiguous()
+    m, v = torch.zeros_like(prm), torch.zeros_like(prm)
+    t_dev = to_dev(tgt)[None].contiguous()
+    bufs = [torch.zeros(n * 8 + 1, device=DEV) for _ in range(2)]
+    loss = torch.zeros(1, device=DEV)
+    wins = row_windows((H + 15) // 16, 2)
+    for step in range(1, steps + 1):
+        for b, (r0, rows) in zip(bufs, wins):
+            gi.gi_fit_grads(prm, b, t_dev, n, f, 0, r0, rows, cap, ws, b[n * 8:])
+        gi.gi_peer_adam_step(prm, m, v, [b.data_ptr() for b in bufs], n * 8, step, 1e-3,
+                             n_loss=1, loss_out=loss)
+    torch.cuda.synchronize()
+    assert np.array_equal(prm[0].cpu().numpy(), res[0][0][0])
+    assert float(loss[0]) == res[0][1]
+    # and it fits: the loss after 3 steps is the whole image's (up to fp32 order)
+    _, ref_loss, _ = gio.loss_and_grads(p, tgt, mode=gio.ALL_PAIRS)
+    assert res[0][1] < 1.01 * ref_loss
+
+
 def test_next_edge_cases(gi, gio):
     # NEXT-2/4 entry points on empty and tiny inputs
     from paper_2403_08551_b200.pipeline import QatFitter, _bytes, default_capacity
