@@ -236,7 +236,8 @@ gi_status gi_fit_step_adan_chained(float* params, float* grads, float* m, float*
  * its share of the L2 loss (normalised by the whole image): both are
  * sums over tiles, so over a partition of the rows they add up to the whole
  * image's (up to fp32 summation order).  Ranks of a sharded fit all-reduce
- * grads and loss (NCCL) and apply the same gi_adam_step.  Workspace as
+ * grads and loss (NCCL) and apply the same gi_adam_step, or exchange them
+ * over peer memory with gi_peer_adam_step (below).  Workspace as
  * gi_fit_step (gi_fit_workspace_bytes), zero-filled once. */
 gi_status gi_fit_grads(const float* params, float* grads, const float* target, int32_t n,
                        const gi_frame* f, uint32_t flags, int32_t tile_row0, int32_t tile_rows,
