@@ -561,7 +561,10 @@ __device__ __forceinline__ void finalize_one(int g, bool live, const FinArgs& a,
 }
 
 template <bool kAdan>
-__global__ void __launch_bounds__(256) finalize_kernel(FinArgs a,
+#ifndef GI_FIN_THREADS
+#define GI_FIN_THREADS 128
+#endif
+__global__ void __launch_bounds__(GI_FIN_THREADS) finalize_kernel(FinArgs a,
                                                        unsigned long long* __restrict__ sse_acc,
                                                        int batch, double inv_count,
                                                        float* __restrict__ loss) {
@@ -700,10 +703,12 @@ cudaError_t launch_backward_finalize(const float* params, const Proj* proj, int 
                         (const float*)w.partial, w.ovf, reinterpret_cast<float4*>(grads), fa, row0,
                         row1 > 0 ? row1 : tiles_y(f.height)};
         if (adam != nullptr && adam->n != nullptr)
-            e = launch_pdl(finalize_kernel<true>, dim3((total + 255) / 256), dim3(256), s, fa_args,
+            e = launch_pdl(finalize_kernel<true>, dim3((total + GI_FIN_THREADS - 1) / GI_FIN_THREADS),
+                           dim3(GI_FIN_THREADS), s, fa_args,
                            mse ? w.sse_acc : nullptr, f.batch, 1.0 / count, mse ? loss : nullptr);
         else
-            e = launch_pdl(finalize_kernel<false>, dim3((total + 255) / 256), dim3(256), s, fa_args,
+            e = launch_pdl(finalize_kernel<false>, dim3((total + GI_FIN_THREADS - 1) / GI_FIN_THREADS),
+                           dim3(GI_FIN_THREADS), s, fa_args,
                            mse ? w.sse_acc : nullptr, f.batch, 1.0 / count, mse ? loss : nullptr);
         note_launches(1);
         if ((e = cudaGetLastError()) != cudaSuccess) return e;
