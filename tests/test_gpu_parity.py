@@ -1017,6 +1017,32 @@ def test_spatial_peer_exchange_two_processes(gi, gio):
     assert res[0][1] < 1.01 * ref_loss
 
 
+def test_new_entry_edge_cases(gi, gio):
+    # gi_decode_render_frame with no records: a zero frame; chained Adan on a
+    # 2-image launch equals the plain fused Adan step bitwise over 3 steps
+    from paper_2403_08551_b200.pipeline import Fitter, Pipeline
+    books = to_dev(np.zeros((2, 8, 3), np.float32))
+    meta = gi.codec_meta(0, [0.1] * 3, [0.0] * 3, books)
+    pipe = Pipeline(0, 40, 24, 1, device=DEV)
+    pipe.image.fill_(1.0)
+    pipe.decode_render_frame(torch.zeros(8, dtype=torch.uint8, device=DEV), meta)
+    torch.cuda.synchronize()
+    assert not pipe.image.any()
+    W, H, n = 80, 48, 300
+    ps = np.stack([synth.init_params(20 + b, n) for b in range(2)])
+    ts = np.stack([synth.image(20 + b, W, H) for b in range(2)])
+    res = []
+    for chained in (True, False):
+        fit = Fitter(to_dev(ps).contiguous(), to_dev(ts).contiguous(), optimizer="adan",
+                     chained=chained)
+        for _ in range(3):
+            fit.step()
+        torch.cuda.synchronize()
+        assert fit.check() == gi.GI_OK
+        res.append(fit.params.clone())
+    assert torch.equal(res[0], res[1])
+
+
 def test_next_edge_cases(gi, gio):
     # NEXT-2/4 entry points on empty and tiny inputs
     from paper_2403_08551_b200.pipeline import QatFitter, _bytes, default_capacity
