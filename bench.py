@@ -404,8 +404,78 @@ def main():
                          "psnr_db": float(psnr_pipe.psnr(img, target)[0])}
         if ffit.check() != gi.GI_OK:
             raise RuntimeError("50k fit status")
+        if opt == "adam":
+            fitted = ffit.params.clone()
         del ffit, fg
-    del psnr_pipe
+
+    # ---------------- the fitted state (SURVEY d.1): render FPS of the cloud the
+    # 50k-step fit produced, and configs[4] from it -- C5 payload built as the
+    # survey's recipe: fp16 positions, l codes with gamma = (max - min)/63,
+    # beta = min, colours by 5 K-means iterations per RVQ stage (gi_kmeans_step,
+    # B = 8, M = 2), packed by gi_vq_encode; then decode + render timed
+    def timed_fps(fn):
+        gs = torch.cuda.Stream(device=dev)
+        gs.wait_stream(stream)
+        gg = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(gg, stream=gs):
+            fn()
+        stream.wait_stream(gs)
+        for _ in range(Wm):
+            gg.replay()
+        barrier()
+        for i in range(K):
+            flush.zero_()
+            s_ev[i].record(stream)
+            gg.replay()
+            e_ev[i].record(stream)
+        barrier()
+        return world * K / (max_over_ranks(sum(s_ev[i].elapsed_time(e_ev[i]) for i in range(K)))
+                            / 1000.0)
+
+    fpipe = Pipeline(N_GAUSS, W_IMG, H_IMG, 1, device=dev)
+    fitted_state = {"render_fps": timed_fps(lambda: fpipe.render_frame(fitted))}
+    fpipe.render_frame(fitted)
+    torch.cuda.synchronize(dev)
+    fitted_state["keys"] = fpipe.frame_keys()
+    fp_host = fitted[0].cpu().numpy()
+    lmin, lmax = fp_host[:, 2:5].min(axis=0), fp_host[:, 2:5].max(axis=0)
+    c_gamma = [float(x) for x in np.maximum((lmax - lmin) / 63.0, 1e-6)]
+    c_beta = [float(x) for x in lmin]
+    cols = torch.from_numpy(np.ascontiguousarray(fp_host[:, 5:8])).to(dev)
+    kws = torch.zeros(gi.gi_kmeans_workspace_bytes(8), dtype=torch.uint8, device=dev)
+    asg = torch.zeros(N_GAUSS, dtype=torch.int32, device=dev)
+    books = torch.zeros(2, 8, 3, dtype=torch.float32, device=dev)
+    pts = cols
+    for st in range(2):
+        cent = pts[:: N_GAUSS // 8][:8].clone()
+        for _ in range(5):
+            gi.gi_kmeans_step(pts, cent, asg, kws)
+        gi.gi_kmeans_step(pts, cent, asg, kws)        # final assignment for the residuals
+        books[st] = cent
+        pts = (pts - cent[asg.long()]).contiguous()   # stage-2 input: residuals
+    cmeta = gi.codec_meta(N_GAUSS, c_gamma, c_beta, books)
+    cpay = torch.zeros((N_GAUSS * 56 + 7) // 8 + 16, dtype=torch.uint8, device=dev)
+    gi.gi_vq_encode(fitted[0].contiguous(), cmeta, cpay)
+    cparams = torch.zeros(1, N_GAUSS, 8, dtype=torch.float32, device=dev)
+    cpipe = Pipeline(N_GAUSS, W_IMG, H_IMG, 1, device=dev)
+    fitted_state["decode_fps"] = timed_fps(lambda: cpipe.decode_render_frame(cpay, cmeta, cparams))
+    dimg = cpipe.decode_render_frame(cpay, cmeta, cparams)
+    fitted_state["psnr_db_fitted"] = float(fpipe.psnr(fpipe.render_frame(fitted), target)[0])
+    fitted_state["psnr_db_decoded"] = float(cpipe.psnr(dimg, target)[0])
+    fitted_state["bpp"] = 56.0 * N_GAUSS / (W_IMG * H_IMG)
+    # the paper's remedy (Fig. 3): quantisation-aware fine-tuning,
+    # then re-encode with the learned gamma / beta and EMA codebooks
+    from paper_2403_08551_b200.pipeline import QatFitter
+    qf = QatFitter(fitted[0].clone(), target, c_gamma, c_beta, books)
+    for _ in range(2000):
+        qf.step()
+    torch.cuda.synchronize(dev)
+    qp = qf.qparams.cpu().numpy()
+    qmeta = gi.codec_meta(N_GAUSS, qp[:3], qp[3:], qf.books)
+    gi.gi_vq_encode(qf.params, qmeta, cpay)
+    dimg = cpipe.decode_render_frame(cpay, qmeta, cparams)
+    fitted_state["psnr_db_decoded_after_qat2000"] = float(cpipe.psnr(dimg, target)[0])
+    del psnr_pipe, fpipe, cpipe, qf
 
     # ---------------- fitting as a user runs it: 100 chained steps per graph, warm L2 ----
     # (context only: `value` above is the cold-L2 single-step number)
@@ -623,6 +693,11 @@ def main():
             "fit_its_adan": adan_value,
             "fit_its_warm_graph100": warm_its,
             "fit_50k_steps": full_fit,
+            "fitted_state": fitted_state,
+            "fitted_note": "context: the cloud the 50k-step Adam fit produced -- render FPS, and "
+                           "configs[4] decode + render of its C5 payload (fp16 positions, 6-bit "
+                           "l codes, 2x8 RVQ colours by K-means, 56-bit records); PSNR before "
+                           "and after the codec, without and with 2000 QAT steps (gi_qat_step)",
             "fit_50k_note": "the paper's training length (50k steps, P:381) on the C2 synthetic "
                             "image from the init cloud: device seconds per rank (max), PSNR of "
                             "the result; paper: 106.59 s on a V100 (Table 1a, P:331), context",
