@@ -213,23 +213,37 @@ __device__ __forceinline__ uint32_t count_below4(const uint4 v, uint32_t mine, u
     return r;
 }
 
+// NT = threads per CTA (256, or 128 for the two-pixel render kernel): each
+// thread ranks kRankMax / NT of the keys.
+template <int NT = 256>
 __device__ __forceinline__ int sorted_segment(const Proj* __restrict__ proj,
                                               uint32_t* __restrict__ key_gid, uint32_t s,
                                               uint32_t e, int n, int img, int tx, int ty,
                                               uint32_t* sl, uint32_t* scratch8) {
+    constexpr int E = kRankMax / NT;
     const int cnt = (int)(e - s);
     if (cnt <= kRankMax) {
-        uint32_t mine = 0xffffffffu;
-        if ((int)threadIdx.x < cnt) mine = key_gid[s + threadIdx.x];
-        sl[threadIdx.x] = mine;
-        __syncthreads();
-        uint32_t r = 0;   // entries >= cnt hold 0xffffffff and never count
-        if ((int)threadIdx.x < cnt) {
-            const uint4* s4 = reinterpret_cast<const uint4*>(sl);
-            for (int k = 0; k < (cnt + 3) >> 2; ++k) r = count_below4(s4[k], mine, r);
+        uint32_t mine[E];
+#pragma unroll
+        for (int q = 0; q < E; ++q) {
+            const int i = (int)threadIdx.x + q * NT;
+            mine[q] = i < cnt ? key_gid[s + i] : 0xffffffffu;
+            sl[i] = mine[q];
         }
         __syncthreads();
-        if ((int)threadIdx.x < cnt) sl[0u - r] = mine;
+        uint32_t r[E];   // entries >= cnt hold 0xffffffff and never count
+#pragma unroll
+        for (int q = 0; q < E; ++q) {
+            r[q] = 0u;
+            if ((int)threadIdx.x + q * NT < cnt) {
+                const uint4* s4 = reinterpret_cast<const uint4*>(sl);
+                for (int k = 0; k < (cnt + 3) >> 2; ++k) r[q] = count_below4(s4[k], mine[q], r[q]);
+            }
+        }
+        __syncthreads();
+#pragma unroll
+        for (int q = 0; q < E; ++q)
+            if ((int)threadIdx.x + q * NT < cnt) sl[0u - r[q]] = mine[q];
         __syncthreads();
         return cnt;
     }
@@ -265,7 +279,7 @@ __device__ __forceinline__ int sorted_segment(const Proj* __restrict__ proj,
         if (lane == 0) scratch8[warp] = __popc(m);
         __syncthreads();
         uint32_t before = 0, tot = 0;
-        for (int w = 0; w < kWarps; ++w) {
+        for (int w = 0; w < NT / 32; ++w) {
             before += w < warp ? scratch8[w] : 0u;
             tot += scratch8[w];
         }
@@ -298,6 +312,7 @@ struct Seg {
 // (cs.slab): every thread reads the tile's count (one broadcast load, no
 // barrier on the critical path); close_segment re-zeroes it at the end of
 // the kernel.  *cursor is set to 0 for kSegStream.
+template <int NT = 256>
 __device__ __forceinline__ Seg open_segment(const Proj* __restrict__ proj,
                                             uint32_t* __restrict__ key_gid,
                                             const uint32_t* __restrict__ tile_range,
@@ -313,12 +328,13 @@ __device__ __forceinline__ Seg open_segment(const Proj* __restrict__ proj,
             __syncthreads();
             return Seg{s, count, kSegStream};
         }
-        const int r = sorted_segment(proj, key_gid, s, s + count, n, t.img, t.tx, t.ty, sl, scratch8);
+        const int r = sorted_segment<NT>(proj, key_gid, s, s + count, n, t.img, t.tx, t.ty, sl,
+                                         scratch8);
         return Seg{s, count, r >= 0 ? kSegSorted : kSegGlobal};
     }
     const uint32_t s = tile_range[tt], e = tile_range[tt + 1];
     if (presorted) return Seg{s, e - s, kSegGlobal};
-    const int r = sorted_segment(proj, key_gid, s, e, n, t.img, t.tx, t.ty, sl, scratch8);
+    const int r = sorted_segment<NT>(proj, key_gid, s, e, n, t.img, t.tx, t.ty, sl, scratch8);
     return Seg{s, e - s, r >= 0 ? kSegSorted : kSegGlobal};
 }
 
@@ -355,6 +371,7 @@ __device__ __forceinline__ void close_segment(const ChainState& cs, int tt) {
 // tile rectangle contains (tx, ty), in gid order, from *cursor on, into
 // out[0 ..).  Returns how many were found (want unless the image ran out).
 // All threads must call.
+template <int NT = 256>
 __device__ __forceinline__ int stream_keys(const Proj* __restrict__ proj, int n, int img, int tx,
                                            int ty, int want, uint32_t* cursor, uint32_t* out,
                                            uint32_t* scratch8) {
@@ -370,7 +387,7 @@ __device__ __forceinline__ int stream_keys(const Proj* __restrict__ proj, int n,
         __syncthreads();
         int before = 0, tot = 0;
 #pragma unroll
-        for (int w = 0; w < kWarps; ++w) {
+        for (int w = 0; w < NT / 32; ++w) {
             const int c = (int)scratch8[w];
             before += w < warp ? c : 0;
             tot += c;
@@ -393,13 +410,14 @@ __device__ __forceinline__ int stream_keys(const Proj* __restrict__ proj, int n,
 // The gids of batch [base, base + 256) of the segment: thread i < returned
 // count gets key base + i.  All threads must call (kSegStream gathers the
 // batch block-wide into sl).
+template <int NT = 256>
 __device__ __forceinline__ int batch_gid(const Seg& sg, uint32_t base, const uint32_t* key_gid,
                                          uint32_t* sl, const Proj* __restrict__ proj, int n,
                                          const TileCtx& t, uint32_t* cursor, uint32_t* scratch8,
                                          uint32_t& gid) {
     int cnt = (int)min((uint32_t)kBatch, sg.L - base);
     if (sg.mode == kSegStream) {
-        cnt = stream_keys(proj, n, t.img, t.tx, t.ty, cnt, cursor, sl, scratch8);
+        cnt = stream_keys<NT>(proj, n, t.img, t.tx, t.ty, cnt, cursor, sl, scratch8);
         gid = (int)threadIdx.x < cnt ? sl[threadIdx.x] : 0u;
     } else if (sg.mode == kSegSorted) {
         gid = (int)threadIdx.x < cnt ? sl[base + threadIdx.x] : 0u;

@@ -1043,6 +1043,32 @@ def test_new_entry_edge_cases(gi, gio):
     assert torch.equal(res[0], res[1])
 
 
+def test_render_one_pixel_variant():
+    # the one-pixel-per-thread render kernel (GI_RENDER2=0, the A/B baseline
+    # of the default two-pixel kernel) stays within the pixel bar: C2 init and
+    # a ragged frame, fused frame vs the oracle, in a fresh process
+    import os
+    import subprocess
+    import sys
+    code = """
+import numpy as np, torch, synth
+from oracle import gio
+from paper_2403_08551_b200.pipeline import Pipeline
+for W, H, n, seed in ((768, 512, 70000, 1), (70, 45, 300, 1)):
+    p = synth.init_params(seed, n)
+    ref = gio.render(p, W, H, mode=gio.TILED)
+    img = Pipeline(n, W, H, 1).render_frame(torch.from_numpy(p).cuda()[None].contiguous())
+    err = float(np.abs(img[0].cpu().numpy() - ref).max())
+    assert err <= 2e-5, err
+print("ok")
+"""
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, GI_RENDER2="0", PYTHONPATH=root)
+    out = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True,
+                         text=True, timeout=600)
+    assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-2000:]
+
+
 def test_next_edge_cases(gi, gio):
     # NEXT-2/4 entry points on empty and tiny inputs
     from paper_2403_08551_b200.pipeline import QatFitter, _bytes, default_capacity
