@@ -23,6 +23,8 @@
 // finalize_kernel -- one thread per Gaussian: sums its contiguous slots in
 //   row-major tile order, applies the chain rule (and tanh, App. C) and
 //   optionally the Adam update (fused fit step).
+#include <cstdlib>
+
 #include "project_core.cuh"
 #include "raster_common.cuh"
 
@@ -313,6 +315,361 @@ __global__ void __launch_bounds__(256, GI_TILE_MINB) backward_tile_kernel(
         }
     }
     close_segment(cs, t.img * T + t.tile);
+}
+
+// ---- two pixels per thread: the render2_kernel layout (128 threads, 8x8
+// warp blocks, pixels (x, y) and (x, y + 4) per lane) for pass 1; pass 2
+// plans its chunks over 128 lanes.  Chosen for launches with many tiles
+// (use_tile2 below).
+struct Bwd2Shared {
+    StagedRecords sr;
+    union {
+        uint4 ent[4][kBatch];    // pass 1: (record, pixel-0 mask, pixel-1 mask)
+        float4 red[128][2];      // pass 2: the 8 sums of each chunk
+    } u;
+    alignas(16) uint32_t sl[kSortMax];
+    float4 g[kTilePix];
+    uint32_t scratch[kWarps];
+    float sse[4];
+    uint32_t cursor;
+    uint32_t hist[64];
+    uint32_t item[128];
+    uint2 pa[4], pb[4];
+    uint32_t pc[4];
+    uint32_t n_items;
+};
+
+__global__ void __launch_bounds__(128) backward_tile2_kernel(
+    const Proj* __restrict__ proj, uint32_t* __restrict__ key_gid,
+    const uint32_t* __restrict__ tile_range, const uint32_t* __restrict__ gauss_off, int n,
+    int W, int H, int T, int TX, bool presorted, const float* __restrict__ dL_dimage,
+    const float* __restrict__ target, float norm, int64_t pcap, float* __restrict__ partial,
+    float* __restrict__ ovf, unsigned long long* __restrict__ sse_acc, float* __restrict__ image_out,
+    ChainState cs) {
+    __shared__ Bwd2Shared sh;
+    TileCtx t;
+    t.tx = blockIdx.x;
+    t.row0 = cs.row1 > 0 ? cs.row0 : 0;
+    t.ty = t.row0 + blockIdx.y;
+    t.img = blockIdx.z;
+    t.tile = blockIdx.y * TX + t.tx;
+    t.row1 = t.row0 + gridDim.y;
+    t.lane = threadIdx.x & 31;
+    t.warp = threadIdx.x >> 5;
+    // two pixels per thread: (lx, ly) and (lx, ly + 4) of the warp's 8x8 block
+    const int lx = (t.warp & 1) * 8 + (t.lane & 7), ly = (t.warp >> 1) * 8 + (t.lane >> 3);
+    const float cx = (float)lx + 0.5f, cy0 = (float)ly + 0.5f;
+    const int csh = (t.warp & 1) * 8, rsh = (t.warp >> 1) * 8;
+    const int x = t.tx * kTile + lx, y = t.ty * kTile + ly;
+    const bool in0 = x < W && y < H, in1 = x < W && y + 4 < H;
+    const size_t P = (size_t)W * H;
+    const size_t pix = (size_t)t.img * 3 * P + (size_t)y * W + x;
+    const size_t pix1 = pix + 4 * (size_t)W;
+    griddep_wait();
+    griddep_trigger();
+    const Seg sg = open_segment<128>(proj, key_gid, tile_range, presorted, cs, n, T, t, sh.sl,
+                                     sh.scratch, &sh.cursor);
+    const uint32_t L = sg.L;
+    const int lpix = ly * kTile + lx;
+    bool staged_all = false;
+
+    float g0 = 0.f, g1 = 0.f, g2 = 0.f, h0 = 0.f, h1 = 0.f, h2 = 0.f;   // pixel 0, pixel 1
+    if (dL_dimage != nullptr) {
+        if (in0) {
+            g0 = dL_dimage[pix];
+            g1 = dL_dimage[pix + P];
+            g2 = dL_dimage[pix + 2 * P];
+        }
+        if (in1) {
+            h0 = dL_dimage[pix1];
+            h1 = dL_dimage[pix1 + P];
+            h2 = dL_dimage[pix1 + 2 * P];
+        }
+    } else {
+        // ---- pass 1: forward (Eq. 7), pixel-parallel, two pixels per lane ----
+        float a0 = 0.f, a1 = 0.f, a2 = 0.f, b0 = 0.f, b1 = 0.f, b2 = 0.f;
+        const uint32_t bit = 1u << t.lane;
+        for (uint32_t base = 0; base < L; base += kBatch) {
+            if (base > 0) __syncthreads();
+            uint32_t gid;
+            const int cnt =
+                batch_gid<128>(sg, base, key_gid, sh.sl, proj, n, t, &sh.cursor, sh.scratch, gid);
+            if ((int)threadIdx.x < cnt) stage_gid(sh.sr, proj, gid, threadIdx.x, t, gauss_off);
+            __syncthreads();
+            int nl = 0;
+            for (int q = 0; q < cnt; q += 32) {
+                const int jj = q + t.lane;
+                uint32_t m0 = 0u, m1 = 0u;
+                if (jj < cnt) {
+                    const uint32_t masks = sh.sr.c[jj].y;
+                    const uint32_t cols = (masks >> csh) & 0xffu;
+                    const uint32_t rows = (masks >> (16 + rsh)) & 0xffu;
+                    m0 = (((rows & 0xfu) * 0x00204081u) & 0x01010101u) * cols;
+                    m1 = (((rows >> 4) * 0x00204081u) & 0x01010101u) * cols;
+                }
+                const unsigned hit = __ballot_sync(kFull, (m0 | m1) != 0u);
+                if ((m0 | m1) != 0u)
+                    sh.u.ent[t.warp][nl + __popc(hit & lanemask_lt())] = make_uint4((uint32_t)jj, m0, m1, 0u);
+                nl += __popc(hit);
+            }
+            __syncwarp();
+            const uint4* ent = sh.u.ent[t.warp];
+#pragma unroll 2
+            for (int k = 0; k < nl; ++k) {
+                const uint4 en = ent[k];
+                const float4 A = sh.sr.a[en.x];      // {a, b, c, c'r}
+                const float4 B = sh.sr.b[en.x];      // {c'g, c'b, mx, my}
+                const float dx = cx - B.z;
+                const float dy = cy0 - B.w;
+                const float u = A.x * dx;
+                const float v0 = fmaf(A.y, dx, A.z * dy);
+                const float v1 = fmaf(A.z, 4.0f, v0);
+                const float uu = u * u;
+                float w0 = ex2_approx(fmaf(-v0, v0, -uu));
+                float w1 = ex2_approx(fmaf(-v1, v1, -uu));
+                w0 = (en.y & bit) ? w0 : 0.f;
+                w1 = (en.z & bit) ? w1 : 0.f;
+                a0 = fmaf(A.w, w0, a0);
+                a1 = fmaf(B.x, w0, a1);
+                a2 = fmaf(B.y, w0, a2);
+                b0 = fmaf(A.w, w1, b0);
+                b1 = fmaf(B.x, w1, b1);
+                b2 = fmaf(B.y, w1, b2);
+            }
+        }
+        staged_all = L <= (uint32_t)kBatch;
+        float sq = 0.f;
+        if (in0) {
+            const float r0 = a0 - target[pix];
+            const float r1 = a1 - target[pix + P];
+            const float r2 = a2 - target[pix + 2 * P];
+            g0 = norm * r0;
+            g1 = norm * r1;
+            g2 = norm * r2;
+            sq = fmaf(r0, r0, fmaf(r1, r1, r2 * r2));
+            if (image_out != nullptr) {
+                image_out[pix] = a0;
+                image_out[pix + P] = a1;
+                image_out[pix + 2 * P] = a2;
+            }
+        }
+        if (in1) {
+            const float r0 = b0 - target[pix1];
+            const float r1 = b1 - target[pix1 + P];
+            const float r2 = b2 - target[pix1 + 2 * P];
+            h0 = norm * r0;
+            h1 = norm * r1;
+            h2 = norm * r2;
+            sq += fmaf(r0, r0, fmaf(r1, r1, r2 * r2));
+            if (image_out != nullptr) {
+                image_out[pix1] = b0;
+                image_out[pix1 + P] = b1;
+                image_out[pix1 + 2 * P] = b2;
+            }
+        }
+        if (sse_acc != nullptr) {
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) sq += __shfl_xor_sync(kFull, sq, o);
+            if (t.lane == 0) sh.sse[t.warp] = sq;
+        }
+    }
+    sh.g[lpix] = make_float4(g0, g1, g2, 0.f);
+    sh.g[lpix + 4 * kTile] = make_float4(h0, h1, h2, 0.f);
+    __syncthreads();
+    if (sse_acc != nullptr && dL_dimage == nullptr && threadIdx.x == 0) {
+        // per-image squared error in 2^-40 fixed point (see backward_tile_kernel)
+        float tot = 0.f;
+#pragma unroll
+        for (int w = 0; w < 4; ++w) tot += sh.sse[w];
+        atomicAdd(&sse_acc[t.img], (unsigned long long)__double2ll_rn((double)tot * kSseScale));
+    }
+
+    // ---- pass 2: gradients, Gaussian-parallel, work-balanced chunks ----
+    // Record j's in-tile box (w_j pixels, row-major) is cut into chunks of at
+    // most C pairs: floor(w_j / C) full chunks and one remainder.  C is the
+    // smallest of a few candidates >= ceil(sum w / 256) whose chunk count fits
+    // the 256 lanes (C = max w_j, one chunk per record, always fits).  Full
+    // chunks come first, remainders follow in descending size, so the lanes
+    // of a warp run nearly equal trip counts.  Each lane accumulates the 8
+    // sums of its chunk; thread j then adds its chunks in a fixed order.
+    const int j = threadIdx.x;
+    if (threadIdx.x == 0) sh.cursor = 0u;        // kSegStream: pass 2 streams from the start
+    for (uint32_t base = 0; base < L; base += kBatch) {
+        __syncthreads();
+        uint32_t gid = 0;
+        int cnt = (int)min((uint32_t)kBatch, L - base);
+        if (!staged_all)
+            cnt = batch_gid<128>(sg, base, key_gid, sh.sl, proj, n, t, &sh.cursor, sh.scratch, gid);
+        if (j < 64) sh.hist[j] = 0u;
+        uint32_t slot = 0, wj = 0, jgid = 0;
+        if (j < cnt) {
+            if (!staged_all) stage_gid(sh.sr, proj, gid, j, t, gauss_off);
+            const uint4 c = sh.sr.c[j];
+            slot = c.z;
+            jgid = c.w;
+            const int lx0 = c.x & 0xff, lx1 = (c.x >> 8) & 0xff;
+            const int ly0 = (c.x >> 16) & 0xff, ly1 = c.x >> 24;
+            wj = (uint32_t)((lx1 - lx0 + 1) * (ly1 - ly0 + 1));
+        }
+        // (1) sum and max of w over the batch
+        {
+            const uint32_t ws = __reduce_add_sync(kFull, wj), wm = __reduce_max_sync(kFull, wj);
+            if (t.lane == 0) sh.pa[t.warp] = make_uint2(ws, wm);
+        }
+        __syncthreads();
+        // 8-way combines of per-warp partials: lane w < 8 loads warp w's, one redux
+        uint32_t tot, mx;
+        {
+            const uint2 x = t.lane < 4 ? sh.pa[t.lane] : make_uint2(0u, 0u);
+            tot = __reduce_add_sync(kFull, x.x);
+            mx = __reduce_max_sync(kFull, x.y);
+        }
+        // (2) chunk counts of the candidate chunk sizes
+        const uint32_t c0 = (tot + 127u) >> 7;
+        const uint32_t c1 = c0 + ((c0 + 3u) >> 2), c2 = c0 + ((c0 + 1u) >> 1);
+        {
+            uint32_t n01 = 0, n2 = 0;
+            if (j < cnt) {
+                n01 = small_div(wj + c0 - 1u, rcp_approx((float)c0)) |
+                      small_div(wj + c1 - 1u, rcp_approx((float)c1)) << 16;
+                n2 = small_div(wj + c2 - 1u, rcp_approx((float)c2));
+            }
+            n01 = __reduce_add_sync(kFull, n01);
+            n2 = __reduce_add_sync(kFull, n2);
+            if (t.lane == 0) sh.pb[t.warp] = make_uint2(n01, n2);
+        }
+        __syncthreads();
+        uint32_t C = mx;
+        {
+            const uint2 x = t.lane < 4 ? sh.pb[t.lane] : make_uint2(0u, 0u);
+            const uint32_t n01 = __reduce_add_sync(kFull, x.x), n2 = __reduce_add_sync(kFull, x.y);
+            if (n2 <= 128u) C = c2;
+            if ((n01 >> 16) <= 128u) C = c1;
+            if ((n01 & 0xffffu) <= 128u) C = c0;
+        }
+        // (3) full chunks: block scan of their counts; remainders: size bins
+        const uint32_t nf = small_div(wj, rcp_approx((float)C)), rm = wj - nf * C;
+        uint32_t incl = nf;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(kFull, incl, o);
+            if (t.lane >= o) incl += y;
+        }
+        if (t.lane == 31) sh.pc[t.warp] = incl;
+        const uint32_t rbin = 64u - min(rm, 64u);        // larger remainder -> lower bin
+        uint32_t rrank = 0;
+        if (rm != 0u) rrank = atomicAdd(&sh.hist[rbin], 1u);
+        __syncthreads();
+        uint32_t F, fstart;
+        {
+            const uint32_t x = t.lane < 4 ? sh.pc[t.lane] : 0u;
+            F = __reduce_add_sync(kFull, x);
+            fstart = incl - nf + __reduce_add_sync(kFull, t.lane < t.warp ? x : 0u);
+        }
+        if (t.warp == 0) {
+            const uint32_t h0 = sh.hist[2 * t.lane], h1 = sh.hist[2 * t.lane + 1];
+            const uint32_t v = h0 + h1;
+            uint32_t x = v;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(kFull, x, o);
+                if (t.lane >= o) x += y;
+            }
+            sh.hist[2 * t.lane] = F + x - v;
+            sh.hist[2 * t.lane + 1] = F + x - v + h0;
+            if (t.lane == 31) sh.n_items = F + x;
+        }
+        __syncthreads();
+        const uint32_t rpos = rm != 0u ? sh.hist[rbin] + rrank : 0u;
+        if (j < cnt) {
+            for (uint32_t i = 0; i < nf; ++i)
+                sh.item[fstart + i] = (uint32_t)j | (i * C) << 8 | ((i + 1u) * C) << 17;
+            if (rm != 0u) sh.item[rpos] = (uint32_t)j | (nf * C) << 8 | wj << 17;
+        }
+        __syncthreads();
+        if (j < (int)sh.n_items) {
+            const uint32_t it = sh.item[j];
+            const int r = (int)(it & 0xffu);
+            const int k0 = (int)((it >> 8) & 0x1ffu), k1 = (int)(it >> 17);
+            const float4 A = sh.sr.a[r];          // {a, b, c, c'r}
+            const float4 B = sh.sr.b[r];          // {c'g, c'b, mx, my}
+            const uint32_t box = sh.sr.c[r].x;
+            const int lx0 = box & 0xff, lx1 = (box >> 8) & 0xff, ly0 = (box >> 16) & 0xff;
+            const int wdt = lx1 - lx0 + 1;
+            const int row = (int)small_div((uint32_t)k0, rcp_approx((float)wdt)), col = k0 - row * wdt;
+            // row-major walk: dx steps by 1 and wraps half a pixel past the
+            // box's last column (far above the stepping's rounding), c dy
+            // advances by c per row
+            const float dx0 = ((float)lx0 + 0.5f) - B.z;
+            const float dx1 = ((float)lx1 + 1.0f) - B.z;
+            float dx = ((float)(lx0 + col) + 0.5f) - B.z;
+            float cdy = A.z * (((float)(ly0 + row) + 0.5f) - B.w);
+            const float4* gp_ptr = &sh.g[(ly0 + row) * kTile + lx0 + col];
+            const int wrap = kTile - wdt;
+            float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f, a4 = 0.f, a5 = 0.f, a6 = 0.f, a7 = 0.f;
+            for (int k = k0; k < k1; ++k) {
+                const float u = A.x * dx;
+                const float v = fmaf(A.y, dx, cdy);
+                const float w = ex2_approx(fmaf(-u, u, -(v * v)));
+                const float4 gp = *gp_ptr;
+                a0 = fmaf(gp.x, w, a0);
+                a1 = fmaf(gp.y, w, a1);
+                a2 = fmaf(gp.z, w, a2);
+                const float sdot = w * fmaf(A.w, gp.x, fmaf(B.x, gp.y, B.y * gp.z));   // -gamma
+                const float gu = -sdot * u, gv = -sdot * v;
+                a3 += gu;
+                a4 += gv;
+                a5 = fmaf(gu, u, a5);
+                a6 = fmaf(gu, v, a6);
+                a7 = fmaf(gv, v, a7);
+                ++gp_ptr;
+                dx += 1.0f;
+                if (dx > dx1) {
+                    gp_ptr += wrap;
+                    dx = dx0;
+                    cdy += A.z;
+                }
+            }
+            sh.u.red[j][0] = make_float4(a0, a1, a2, a3);
+            sh.u.red[j][1] = make_float4(a4, a5, a6, a7);
+        }
+        __syncthreads();
+        if (j < cnt && (slot == kOffOverflow || (int64_t)slot < pcap)) {
+            float4 s0 = make_float4(0.f, 0.f, 0.f, 0.f), s1 = s0;
+            auto add = [&](uint32_t i) {
+                const float4 x = sh.u.red[i][0], y = sh.u.red[i][1];
+                s0.x += x.x; s0.y += x.y; s0.z += x.z; s0.w += x.w;
+                s1.x += y.x; s1.y += y.y; s1.z += y.z; s1.w += y.w;
+            };
+            for (uint32_t i = 0; i < nf; ++i) add(fstart + i);
+            if (rm != 0u) add(rpos);
+            if (slot == kOffOverflow) {     // > 4-tile Gaussian without slots: accumulate
+                float* o = ovf + (size_t)jgid * 8;
+                atomicAdd(o + 0, s0.x); atomicAdd(o + 1, s0.y); atomicAdd(o + 2, s0.z);
+                atomicAdd(o + 3, s0.w); atomicAdd(o + 4, s1.x); atomicAdd(o + 5, s1.y);
+                atomicAdd(o + 6, s1.z); atomicAdd(o + 7, s1.w);
+            } else {
+                float4* dst = reinterpret_cast<float4*>(partial + (size_t)slot * 8);
+                dst[0] = s0;
+                dst[1] = s1;
+            }
+        }
+    }
+    close_segment(cs, t.img * T + t.tile);
+}
+
+
+// Kernel choice: the two-pixel kernel wins when a launch has many tiles
+// (C3: 10,880 tiles, fit 8.9k -> 10.6k it/s; 64 C2 images: 36.9k -> 39.4k
+// image-it/s) and loses on one C2 image (1,536 tiles: 24.4k -> 23.4k), where
+// its 28 warps/SM hide less latency.  GI_TILE2=0/1 forces either (A/B).
+constexpr int kTile2MinTiles = 4096;
+bool use_tile2(int tiles) {
+    static const int force = [] {
+        const char* e = std::getenv("GI_TILE2");
+        return e == nullptr ? -1 : (e[0] == '1' ? 1 : 0);
+    }();
+    return force >= 0 ? force == 1 : tiles >= kTile2MinTiles;
 }
 
 __global__ void __launch_bounds__(256) alloc_kernel(const Proj* __restrict__ proj, int total,
@@ -678,11 +1035,15 @@ cudaError_t launch_backward_tiles(const Proj* proj, uint32_t* key_gid, const uin
     const float norm = (float)(2.0 / count);
     const bool mse = dL_dimage == nullptr;
     if (rows <= 0) return cudaSuccess;
-    cudaError_t e = launch_pdl(backward_tile_kernel, dim3(TX, rows, f.batch), dim3(256), s, proj,
-                               key_gid,
-                               tile_range, (const uint32_t*)w.gauss_off, n, f.width, f.height, T,
-                               TX, presorted, dL_dimage, target, norm, partial_cap(n, cap, f), w.partial, w.ovf,
-                               mse ? w.sse_acc : nullptr, mse ? image_out : nullptr, cs);
+    cudaError_t e = use_tile2(T * f.batch)
+        ? launch_pdl(backward_tile2_kernel, dim3(TX, rows, f.batch), dim3(128), s, proj, key_gid,
+                     tile_range, (const uint32_t*)w.gauss_off, n, f.width, f.height, T, TX,
+                     presorted, dL_dimage, target, norm, partial_cap(n, cap, f), w.partial, w.ovf,
+                     mse ? w.sse_acc : nullptr, mse ? image_out : nullptr, cs)
+        : launch_pdl(backward_tile_kernel, dim3(TX, rows, f.batch), dim3(256), s, proj, key_gid,
+                     tile_range, (const uint32_t*)w.gauss_off, n, f.width, f.height, T, TX,
+                     presorted, dL_dimage, target, norm, partial_cap(n, cap, f), w.partial, w.ovf,
+                     mse ? w.sse_acc : nullptr, mse ? image_out : nullptr, cs);
     note_launches(1);
     return e;
 }

@@ -1069,6 +1069,42 @@ print("ok")
     assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-2000:]
 
 
+@pytest.mark.parametrize("force", ["0", "1"])
+def test_tile_kernel_variants(force):
+    # both fused tile kernels (one pixel per thread, two per thread) in a
+    # fresh process with the choice forced: C2 init frame + fused fit-step
+    # gradients and a 3-image launch vs the oracle
+    import os
+    import subprocess
+    import sys
+    code = """
+import numpy as np, torch, synth
+from oracle import gio
+from paper_2403_08551_b200.pipeline import Fitter
+cases = [(768, 512, [synth.init_params(1, 70000)], [synth.image(1, 768, 512)]),
+         (96, 70, [synth.fitted_params(s, 900) for s in (3, 4, 5)],
+          [synth.image(s, 96, 70) for s in (3, 4, 5)])]
+for W, H, ps, ts in cases:
+    fit = Fitter(torch.from_numpy(np.stack(ps)).cuda().contiguous(),
+                 torch.from_numpy(np.stack(ts)).cuda().contiguous())
+    fit.step()
+    g = fit.grads.cpu().numpy().astype(np.float64)
+    for b in range(len(ps)):
+        mode = gio.TILED if W * H > 10000 else gio.ALL_PAIRS
+        _, loss, rg = gio.loss_and_grads(ps[b], ts[b], mode=mode)
+        assert abs(float(fit.loss[b]) - loss) <= 1e-5 * loss
+        for cols in ([0, 1], [2, 3, 4], [5, 6, 7]):
+            e = np.linalg.norm(g[b][:, cols] - rg[:, cols]) / np.linalg.norm(rg[:, cols])
+            assert e <= 1e-4, (b, cols, e)
+print("ok")
+"""
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, GI_TILE2=force, PYTHONPATH=root)
+    out = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True,
+                         text=True, timeout=900)
+    assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-2000:]
+
+
 def test_next_edge_cases(gi, gio):
     # NEXT-2/4 entry points on empty and tiny inputs
     from paper_2403_08551_b200.pipeline import QatFitter, _bytes, default_capacity
