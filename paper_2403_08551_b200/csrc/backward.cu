@@ -321,13 +321,17 @@ __global__ void __launch_bounds__(256, GI_TILE_MINB) backward_tile_kernel(
 // warp blocks, pixels (x, y) and (x, y + 4) per lane) for pass 1; pass 2
 // plans its chunks over 128 lanes.  Chosen for launches with many tiles
 // (use_tile2 below).
+#ifndef GI_TILE2_MINB
+#define GI_TILE2_MINB 8
+#endif
+constexpr int kSortMax2 = 1024;   // 4 KB sort buffer: one more CTA per SM
 struct Bwd2Shared {
     StagedRecords sr;
     union {
         uint4 ent[4][kBatch];    // pass 1: (record, pixel-0 mask, pixel-1 mask)
         float4 red[128][2];      // pass 2: the 8 sums of each chunk
     } u;
-    alignas(16) uint32_t sl[kSortMax];
+    alignas(16) uint32_t sl[kSortMax2];   // segments beyond are rebuilt in order (rare)
     float4 g[kTilePix];
     uint32_t scratch[kWarps];
     float sse[4];
@@ -339,7 +343,7 @@ struct Bwd2Shared {
     uint32_t n_items;
 };
 
-__global__ void __launch_bounds__(128) backward_tile2_kernel(
+__global__ void __launch_bounds__(128, GI_TILE2_MINB) backward_tile2_kernel(
     const Proj* __restrict__ proj, uint32_t* __restrict__ key_gid,
     const uint32_t* __restrict__ tile_range, const uint32_t* __restrict__ gauss_off, int n,
     int W, int H, int T, int TX, bool presorted, const float* __restrict__ dL_dimage,
@@ -367,8 +371,8 @@ __global__ void __launch_bounds__(128) backward_tile2_kernel(
     const size_t pix1 = pix + 4 * (size_t)W;
     griddep_wait();
     griddep_trigger();
-    const Seg sg = open_segment<128>(proj, key_gid, tile_range, presorted, cs, n, T, t, sh.sl,
-                                     sh.scratch, &sh.cursor);
+    const Seg sg = open_segment<128, kSortMax2>(proj, key_gid, tile_range, presorted, cs, n, T, t,
+                                                sh.sl, sh.scratch, &sh.cursor);
     const uint32_t L = sg.L;
     const int lpix = ly * kTile + lx;
     bool staged_all = false;

@@ -215,7 +215,7 @@ __device__ __forceinline__ uint32_t count_below4(const uint4 v, uint32_t mine, u
 
 // NT = threads per CTA (256, or 128 for the two-pixel render kernel): each
 // thread ranks kRankMax / NT of the keys.
-template <int NT = 256>
+template <int NT = 256, int SMAX = kSortMax>
 __device__ __forceinline__ int sorted_segment(const Proj* __restrict__ proj,
                                               uint32_t* __restrict__ key_gid, uint32_t s,
                                               uint32_t e, int n, int img, int tx, int ty,
@@ -247,7 +247,7 @@ __device__ __forceinline__ int sorted_segment(const Proj* __restrict__ proj,
         __syncthreads();
         return cnt;
     }
-    if (cnt <= kSortMax) {
+    if (cnt <= SMAX) {
         int P = 512;
         while (P < cnt) P <<= 1;
         for (int i = threadIdx.x; i < P; i += blockDim.x) sl[i] = i < cnt ? key_gid[s + i] : 0xffffffffu;
@@ -312,7 +312,7 @@ struct Seg {
 // (cs.slab): every thread reads the tile's count (one broadcast load, no
 // barrier on the critical path); close_segment re-zeroes it at the end of
 // the kernel.  *cursor is set to 0 for kSegStream.
-template <int NT = 256>
+template <int NT = 256, int SMAX = kSortMax>
 __device__ __forceinline__ Seg open_segment(const Proj* __restrict__ proj,
                                             uint32_t* __restrict__ key_gid,
                                             const uint32_t* __restrict__ tile_range,
@@ -328,13 +328,13 @@ __device__ __forceinline__ Seg open_segment(const Proj* __restrict__ proj,
             __syncthreads();
             return Seg{s, count, kSegStream};
         }
-        const int r = sorted_segment<NT>(proj, key_gid, s, s + count, n, t.img, t.tx, t.ty, sl,
-                                         scratch8);
+        const int r = sorted_segment<NT, SMAX>(proj, key_gid, s, s + count, n, t.img, t.tx,
+                                               t.ty, sl, scratch8);
         return Seg{s, count, r >= 0 ? kSegSorted : kSegGlobal};
     }
     const uint32_t s = tile_range[tt], e = tile_range[tt + 1];
     if (presorted) return Seg{s, e - s, kSegGlobal};
-    const int r = sorted_segment<NT>(proj, key_gid, s, e, n, t.img, t.tx, t.ty, sl, scratch8);
+    const int r = sorted_segment<NT, SMAX>(proj, key_gid, s, e, n, t.img, t.tx, t.ty, sl, scratch8);
     return Seg{s, e - s, r >= 0 ? kSegSorted : kSegGlobal};
 }
 

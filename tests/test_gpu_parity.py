@@ -1081,9 +1081,14 @@ def test_tile_kernel_variants(force):
 import numpy as np, torch, synth
 from oracle import gio
 from paper_2403_08551_b200.pipeline import Fitter
+big = synth.init_params(6, 1500)
+big[:, 2] += 3.0                    # boxes ~ 20 px: ~1,500 keys per tile, past the
+big[:, 4] += 3.0                    # two-pixel kernel's 1,024-key sort buffer
+big[:, 5:8] *= 0.002
 cases = [(768, 512, [synth.init_params(1, 70000)], [synth.image(1, 768, 512)]),
          (96, 70, [synth.fitted_params(s, 900) for s in (3, 4, 5)],
-          [synth.image(s, 96, 70) for s in (3, 4, 5)])]
+          [synth.image(s, 96, 70) for s in (3, 4, 5)]),
+         (32, 32, [big], [synth.image(6, 32, 32)])]
 for W, H, ps, ts in cases:
     fit = Fitter(torch.from_numpy(np.stack(ps)).cuda().contiguous(),
                  torch.from_numpy(np.stack(ts)).cuda().contiguous())
