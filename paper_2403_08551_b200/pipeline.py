@@ -158,28 +158,32 @@ class Fitter:
         self.flags = flags
         self.graph = None
 
-    def step(self, stream=None, stage_events=None):
+    def step(self, stream=None, stage_events=None, loss_out=None):
         """One fused step.  In chained mode (default) the first call primes
         the workspace and every step fuses the next step's projection into
         its Adam kernel; the params must not be written by anyone else in
-        between (call unchain() after modifying them)."""
+        between (call unchain() after modifying them).  loss_out: where the
+        per-image losses go instead of self.loss -- e.g. the address of
+        pinned host memory, which the finalize kernel then writes directly
+        (mapped, no copy-engine transfer)."""
+        loss = self.loss if loss_out is None else loss_out
         if self.chained and not self.primed:
             gi.gi_fit_prime(self.params, self.n, self.f, self.flags, self.cap, self.fit_ws, stream)
             self.primed = True
         if self.optimizer == "adan":
             fn = gi.gi_fit_step_adan_chained if self.chained else gi.gi_fit_step_adan
             fn(self.params, self.grads, self.m, self.v, self.n_acc, self.grad_prev, self.target,
-               self.n, self.f, self.flags, self.cap, self.fit_ws, self.step_counter, loss=self.loss,
+               self.n, self.f, self.flags, self.cap, self.fit_ws, self.step_counter, loss=loss,
                status_flags=self.status, stream=stream, **self.hyper, **self.adan_extra)
             return
         if self.chained:
             gi.gi_fit_step_chained(self.params, self.grads, self.m, self.v, self.target, self.n,
                                    self.f, self.flags, self.cap, self.fit_ws, self.step_counter,
-                                   loss=self.loss, status_flags=self.status,
+                                   loss=loss, status_flags=self.status,
                                    stage_events=stage_events, stream=stream, **self.hyper)
         else:
             gi.gi_fit_step(self.params, self.grads, self.m, self.v, self.target, self.n, self.f,
-                           self.flags, self.cap, self.fit_ws, self.step_counter, loss=self.loss,
+                           self.flags, self.cap, self.fit_ws, self.step_counter, loss=loss,
                            status_flags=self.status, stage_events=stage_events, stream=stream,
                            **self.hyper)
 
