@@ -653,8 +653,9 @@ def main():
     clk = clocks.stop()
     e2e_ms = s_ev[0].elapsed_time(e_ev[0])
     e2e_value = world * K / (max_over_ranks(e2e_ms) / 1000.0)
-    if not np.all(np.isfinite(pinned_loss.numpy())):
-        raise RuntimeError("e2e loss not finite")
+    e2e_losses = pinned_loss.numpy()[: K + Wm]
+    if not (np.all(np.isfinite(e2e_losses)) and np.all(e2e_losses > 0)):
+        raise RuntimeError("e2e losses missing or not finite")
 
     # ---------------- quality + the one collective (NCCL all-gather of PSNR) ----
     img = pipe.render_frame(fit.params)

@@ -53,9 +53,12 @@ def run(K, h2d=True, fl=True, d2h=True):
         if h2d:
             stream.wait_event(copied[b])
         fit.target = tbuf[b]
-        fit.step()
+        if d2h == "mapped":
+            fit.step(loss_out=ploss[i % 1000].data_ptr())
+        else:
+            fit.step()
         consumed[b].record(stream)
-        if d2h:
+        if d2h is True:
             ds.wait_event(consumed[b])
             with torch.cuda.stream(ds):
                 ploss[i % 1000].copy_(fit.loss[0], non_blocking=True)
@@ -69,7 +72,8 @@ def run(K, h2d=True, fl=True, d2h=True):
 
 
 fit.step()
-for args in (dict(), dict(fl=False), dict(d2h=False), dict(h2d=False), dict(h2d=False, fl=False, d2h=False)):
+for args in (dict(), dict(d2h="mapped"), dict(fl=False), dict(d2h=False), dict(h2d=False),
+             dict(h2d=False, fl=False, d2h=False)):
     run(20, **args)
     dev_its, host_enq, host_tot = run(200, **args)
     print(args, "device it/s", round(dev_its), "host enqueue it/s", round(host_enq), "wall it/s", round(host_tot))
