@@ -322,7 +322,7 @@ __global__ void __launch_bounds__(256, GI_TILE_MINB) backward_tile_kernel(
 // plans its chunks over 128 lanes.  Chosen for launches with many tiles
 // (use_tile2 below).
 #ifndef GI_TILE2_MINB
-#define GI_TILE2_MINB 8
+#define GI_TILE2_MINB 9
 #endif
 constexpr int kSortMax2 = 1024;   // 4 KB sort buffer: one more CTA per SM
 struct Bwd2Shared {
