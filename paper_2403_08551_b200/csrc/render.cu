@@ -66,15 +66,19 @@ __global__ void __launch_bounds__(256, GI_RENDER_MINB) render_kernel(const Proj*
 // 21.2k -> 24.4k FPS) and on long segments (fitted proxy, decoded clouds);
 // 8x8 culling evaluates more lane-pairs than 8x4, which evens it out at the
 // C2 init scale.
+#ifndef GI_RENDER2_MINB
+#define GI_RENDER2_MINB 9
+#endif
+constexpr int kSortMaxR2 = 1024;     // 4 KB sort buffer; longer segments are rebuilt in order
 struct Render2Shared {
     StagedRecords sr;
     uint4 ent[4][kBatch];            // (record, pixel-0 lane mask, pixel-1 lane mask)
-    alignas(16) uint32_t sl[kSortMax];
+    alignas(16) uint32_t sl[kSortMaxR2];
     uint32_t scratch[kWarps];
     uint32_t cursor;
 };
 
-__global__ void __launch_bounds__(128) render2_kernel(const Proj* __restrict__ proj,
+__global__ void __launch_bounds__(128, GI_RENDER2_MINB) render2_kernel(const Proj* __restrict__ proj,
                                                       uint32_t* __restrict__ key_gid,
                                                       const uint32_t* __restrict__ tile_range,
                                                       int n, int W, int H, int T, int TX,
@@ -94,8 +98,8 @@ __global__ void __launch_bounds__(128) render2_kernel(const Proj* __restrict__ p
     const int csh = (warp & 1) * 8, rsh = (warp >> 1) * 8;
     griddep_wait();
     griddep_trigger();
-    const Seg sg = open_segment<128>(proj, key_gid, tile_range, presorted, cs, n, T, t, sh.sl,
-                                     sh.scratch, &sh.cursor);
+    const Seg sg = open_segment<128, kSortMaxR2>(proj, key_gid, tile_range, presorted, cs, n, T,
+                                                 t, sh.sl, sh.scratch, &sh.cursor);
     float a0 = 0.f, a1 = 0.f, a2 = 0.f, b0 = 0.f, b1 = 0.f, b2 = 0.f;
     const uint32_t bit = 1u << lane;
     for (uint32_t base = 0; base < sg.L; base += kBatch) {
