@@ -663,11 +663,13 @@ __global__ void __launch_bounds__(128, GI_TILE2_MINB) backward_tile2_kernel(
 }
 
 
-// Kernel choice: the two-pixel kernel wins when a launch has many tiles
-// (C3: 10,880 tiles, fit 8.9k -> 10.6k it/s; 64 C2 images: 36.9k -> 39.4k
-// image-it/s) and loses on one C2 image (1,536 tiles: 24.4k -> 23.4k), where
-// its 28 warps/SM hide less latency.  GI_TILE2=0/1 forces either (A/B).
-constexpr int kTile2MinTiles = 4096;
+// Kernel choice: the two-pixel kernel wins when a launch has more tiles than
+// one C2 image (C3: 10,880 tiles, fit 8.9k -> 11.4k it/s; C2 x 2 images:
+// 28.6k -> 29.1k image-it/s, x 8: 34.7k -> 37.3k, x 64: 36.9k -> 40.5k) and
+// loses on one C2 image (1,536 tiles: 24.4k -> 23.2k: its CTAs live twice as
+// long, so the last of ~1.2 waves leaves SMs idle).  GI_TILE2=0/1 forces
+// either (A/B).
+constexpr int kTile2MinTiles = 3072;
 bool use_tile2(int tiles) {
     static const int force = [] {
         const char* e = std::getenv("GI_TILE2");
