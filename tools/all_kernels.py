@@ -1,6 +1,6 @@
 #!/usr/bin/env python
 """Diagnostic (for `ncu --set full -k regex:gi::`): every libgi kernel once on
-C2-sized inputs -- the gi_bin path (count, scan, scatter, segsort), render,
+C2-sized inputs (a 3-image launch for the two-pixel tile kernel) -- the gi_bin path (count, scan, scatter, segsort), render,
 the unfused backward (alloc, tile, finalize, loss), Adam, Adan, decode,
 encode, K-means, PSNR, the fused frame and fit steps."""
 import os
@@ -44,5 +44,10 @@ gi.gi_kmeans_step(pts, cent, assign, _bytes(gi.gi_kmeans_workspace_bytes(8), dev
 fit = Fitter(p.clone(), t)
 for _ in range(3):
     fit.step()                      # chained: tile kernel + finalize (+ next projection)
+pb = p.repeat(3, 1, 1).contiguous()     # 3 images per launch: the two-pixel tile kernel
+fb = Fitter(pb, t.repeat(3, 1, 1, 1).contiguous())
+fb.step()
+fa = Fitter(p.clone(), t, optimizer="adan")
+fa.step()                           # finalize_kernel<true> (fused Adan)
 torch.cuda.synchronize()
 print("ok", pipe.keys(), fit.n_keys())
