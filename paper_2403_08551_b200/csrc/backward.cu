@@ -321,14 +321,28 @@ __global__ void __launch_bounds__(256, GI_TILE_MINB) backward_tile_kernel(
 // warp blocks, pixels (x, y) and (x, y + 4) per lane) for pass 1; pass 2
 // plans its chunks over 128 lanes.  Chosen for launches with many tiles
 // (use_tile2 below).
+// 48 registers, 18.8 KB of shared memory: 10 CTAs (40 warps) per SM
 #ifndef GI_TILE2_MINB
-#define GI_TILE2_MINB 9
+#define GI_TILE2_MINB 10
 #endif
-constexpr int kSortMax2 = 1024;   // 4 KB sort buffer: one more CTA per SM
+#ifndef GI_TILE2_SORT
+#define GI_TILE2_SORT 512
+#endif
+#ifndef GI_TILE2_UNPACKED
+#define GI_TILE2_PACKED     // candidate entries as (mask pair, byte index): 9 B instead of 16
+#endif
+constexpr int kSortMax2 = GI_TILE2_SORT;   // sort buffer; longer segments are rebuilt in order
 struct Bwd2Shared {
     StagedRecords sr;
     union {
+#ifdef GI_TILE2_PACKED
+        struct {
+            uint2 m[4][kBatch];      // pass 1: (pixel-0 mask, pixel-1 mask)
+            uint8_t j[4][kBatch];    //         record index
+        } ent;
+#else
         uint4 ent[4][kBatch];    // pass 1: (record, pixel-0 mask, pixel-1 mask)
+#endif
         float4 red[128][2];      // pass 2: the 8 sums of each chunk
     } u;
     alignas(16) uint32_t sl[kSortMax2];   // segments beyond are rebuilt in order (rare)
@@ -412,15 +426,32 @@ __global__ void __launch_bounds__(128, GI_TILE2_MINB) backward_tile2_kernel(
                     m1 = (((rows >> 4) * 0x00204081u) & 0x01010101u) * cols;
                 }
                 const unsigned hit = __ballot_sync(kFull, (m0 | m1) != 0u);
-                if ((m0 | m1) != 0u)
-                    sh.u.ent[t.warp][nl + __popc(hit & lanemask_lt())] = make_uint4((uint32_t)jj, m0, m1, 0u);
+                if ((m0 | m1) != 0u) {
+                    const int at = nl + __popc(hit & lanemask_lt());
+#ifdef GI_TILE2_PACKED
+                    sh.u.ent.m[t.warp][at] = make_uint2(m0, m1);
+                    sh.u.ent.j[t.warp][at] = (uint8_t)jj;
+#else
+                    sh.u.ent[t.warp][at] = make_uint4((uint32_t)jj, m0, m1, 0u);
+#endif
+                }
                 nl += __popc(hit);
             }
             __syncwarp();
+#ifdef GI_TILE2_PACKED
+            const uint2* entm = sh.u.ent.m[t.warp];
+            const uint8_t* entj = sh.u.ent.j[t.warp];
+#else
             const uint4* ent = sh.u.ent[t.warp];
+#endif
 #pragma unroll 2
             for (int k = 0; k < nl; ++k) {
+#ifdef GI_TILE2_PACKED
+                const uint2 mm = entm[k];
+                const uint4 en = make_uint4((uint32_t)entj[k], mm.x, mm.y, 0u);
+#else
                 const uint4 en = ent[k];
+#endif
                 const float4 A = sh.sr.a[en.x];      // {a, b, c, c'r}
                 const float4 B = sh.sr.b[en.x];      // {c'g, c'b, mx, my}
                 const float dx = cx - B.z;
