@@ -13,10 +13,12 @@
  * Conventions (all entry points):
  *  - Every array argument is a caller-owned DEVICE pointer unless stated.
  *    libgi never allocates on the hot path; workspaces are caller-provided and
- *    sized by the *_workspace_bytes queries.
+ *    sized by the *_workspace_bytes queries (the one exception is the setup
+ *    call gi_peer_alloc, which creates an IPC-shareable exchange buffer).
  *  - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).
- *    Every call is stream-ordered, never synchronises the host and is
- *    CUDA-graph capturable.
+ *    Every call taking a stream is stream-ordered, never synchronises the host
+ *    and is CUDA-graph capturable (gi_check, which syncs, and the gi_peer_*
+ *    setup calls are the exceptions).
  *  - Layouts are fixed: parameters/gradients AoS [B][N][8] fp32 =
  *    {mu_x, mu_y, l1, l2, l3, c'_r, c'_g, c'_b}, 16-byte aligned; images
  *    planar fp32 [B][3][H][W], y down, pixel (x, y) has centre (x+1/2, y+1/2)
