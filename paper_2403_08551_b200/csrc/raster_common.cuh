@@ -6,7 +6,10 @@
 // Warp w covers an 8x4 pixel block (w & 1 -> x half, w >> 1 -> y quarter), so
 // a warp skips a Gaussian whose box misses its block (warp culling): at the
 // paper's init scale this evaluates ~3x fewer pairs than whole-tile
-// evaluation.
+// evaluation.  The two-pixel kernels (render2_kernel,
+// backward_tile2_kernel) use 128 threads and 8x8 warp blocks instead; the
+// segment helpers below take the CTA size (NT) and sort-buffer size (SMAX)
+// as template parameters.
 //
 // The tile's key segment is first brought into ascending-gid order in shared
 // memory (direct binning leaves it in atomic order), then, per batch of up to
