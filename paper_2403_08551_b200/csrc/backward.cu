@@ -715,8 +715,8 @@ __global__ void __launch_bounds__(256) alloc_kernel(const Proj* __restrict__ pro
     const int g = blockIdx.x * blockDim.x + threadIdx.x;
     uint32_t cnt = 0;
     if (g < total) {
-        const Proj r = proj[g];
-        const uint32_t bx = __float_as_uint(r.q1.w), by = __float_as_uint(r.q2.w);
+        const uint32_t* rw = reinterpret_cast<const uint32_t*>(proj + g);   // box words only
+        const uint32_t bx = rw[7], by = rw[11];
         const int x0 = (int)(bx & 0xffffu), x1 = (int)(bx >> 16);
         const int y0 = (int)(by & 0xffffu), y1 = (int)(by >> 16);
         if (x0 <= x1 && y0 <= y1)
@@ -775,12 +775,14 @@ __device__ __forceinline__ void finalize_one(int g, bool live, const FinArgs& a,
     const uint32_t flags = a.flags;
     // independent loads first (their latency overlaps the partial-sum chain)
     float4 p0 = make_float4(0.f, 0.f, 0.f, 0.f), p1 = p0, m0 = p0, m1 = p0, v0 = p0, v1 = p0;
-    Proj r{};
+    uint32_t bx = 0u, by = 0u;     // the record's box words: all finalize needs of it
     const float4* pp = reinterpret_cast<const float4*>(a.partial);
     if (live) {
         p0 = a.params[2 * (size_t)g];
         p1 = a.params[2 * (size_t)g + 1];
-        r = a.proj[g];
+        const uint32_t* rw = reinterpret_cast<const uint32_t*>(a.proj + g);
+        bx = rw[7];                 // q1.w: x0 | x1 << 16
+        by = rw[11];                // q2.w: y0 | y1 << 16
         if (adam.m != nullptr) {
             const float4* mm = reinterpret_cast<const float4*>(adam.m) + 2 * (size_t)g;
             const float4* vv = reinterpret_cast<const float4*>(adam.v) + 2 * (size_t)g;
@@ -798,7 +800,6 @@ __device__ __forceinline__ void finalize_one(int g, bool live, const FinArgs& a,
     uint32_t touched = 0;
     int4 rect = make_int4(0, -1, 0, -1);
     if (live) {
-        const uint32_t bx = __float_as_uint(r.q1.w), by = __float_as_uint(r.q2.w);
         const int x0 = (int)(bx & 0xffffu), x1 = (int)(bx >> 16);
         const int y0 = (int)(by & 0xffffu), y1 = (int)(by >> 16);
         float S[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};

@@ -3,6 +3,7 @@
 #pragma once
 
 #include <cuda_runtime.h>
+#include <stddef.h>
 #include <stdint.h>
 
 #include <utility>
@@ -34,6 +35,8 @@ struct __align__(16) Proj {
     float4 q0, q1, q2;
 };
 static_assert(sizeof(Proj) == GI_PROJ_BYTES, "record size");
+// finalize / alloc read only the box words: q1.w (word 7) and q2.w (word 11)
+static_assert(offsetof(Proj, q1) == 16 && offsetof(Proj, q2) == 32, "record layout");
 
 constexpr uint32_t kEmptyBox = 1u;   // x0 = 1, x1 = 0
 
