@@ -361,6 +361,35 @@ def main():
     barrier()
     d_ms = sum(s_ev[i].elapsed_time(e_ev[i]) for i in range(K))
     decode_fps = world * K / (max_over_ranks(d_ms) / 1000.0)
+    # codec-realistic record counts (~0.3 / 0.6 bpp at 56-bit records)
+    decode_small = {}
+    for n_small in (2200, 4500):
+        sdata, sg, sb, sbooks = synth.payload(seed, n_small)
+        s_pay = torch.from_numpy(sdata).to(dev)
+        s_books = torch.from_numpy(sbooks).to(dev)
+        s_meta = gi.codec_meta(n_small, sg, sb, s_books)
+        s_params = torch.zeros(1, n_small, 8, dtype=torch.float32, device=dev)
+        s_pipe = Pipeline(n_small, W_IMG, H_IMG, 1, device=dev)
+        s_pipe.decode_render_frame(s_pay, s_meta, s_params)
+        torch.cuda.synchronize(dev)
+        sgs = torch.cuda.Stream(device=dev)
+        sgs.wait_stream(stream)
+        sgr = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(sgr, stream=sgs):
+            s_pipe.decode_render_frame(s_pay, s_meta, s_params)
+        stream.wait_stream(sgs)
+        for _ in range(Wm):
+            sgr.replay()
+        barrier()
+        for i in range(K):
+            flush.zero_()
+            s_ev[i].record(stream)
+            sgr.replay()
+            e_ev[i].record(stream)
+        barrier()
+        sms = sum(s_ev[i].elapsed_time(e_ev[i]) for i in range(K))
+        decode_small[str(n_small)] = world * K / (max_over_ranks(sms) / 1000.0)
+        del sgr, s_pipe
 
     # ---------------- Adan fit step (the paper's optimiser, NEXT-1) ----------------
     afit = Fitter(params.clone(), target, optimizer="adan")
@@ -708,6 +737,7 @@ def main():
                              "replay, no L2 flush between steps (a long fit as a user runs it)",
             "batched": batched,
             "decode_fps": decode_fps,
+            "decode_fps_codec_sizes": decode_small,
             "encode_fps": encode_fps,
             "qat_its": qat_its,
             "next2_note": "encode_fps: gi_vq_encode of 70k fitted records (fp16 positions, "
