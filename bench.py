@@ -38,14 +38,20 @@ sys.path.insert(0, ROOT)
 METRIC = ("render FPS + fit iters/s @768×512, 70k Gaussians; fraction of FP32/HBM "
           "roofline")
 W_IMG, H_IMG, N_GAUSS = 768, 512, 70000
+W_C3, H_C3, N_C3 = 2040, 1356, 100000          # configs[2], DIV2K-shaped (R24)
 PAPER_FIT_ITS = 50000 / 106.59        # Table 1a, V100, Adan: 469.1 it/s
 L2_FLUSH_BYTES = 256 << 20
-# algorithmic FP32 work per (pixel, Gaussian) pair in the box:
-#   forward  (Eq. 5 + 7, factored conic): 15 FLOP + 1 ex2
-#   backward (App. A, 5-moment form)   : 34 FLOP + 1 ex2
+# Algorithmic work per (pixel, Gaussian) pair in the box, SURVEY.md §8(d.3):
+#   render (Eq. 5 + 7): 10 FP32 lane-ops + 1 MUFU.EX2
+#   backward (App. A):  26 FP32 lane-ops + 1 MUFU.EX2
+# The fused tile kernel does both per pair: 36 lane-ops + 2 ex2.  The FP32
+# pipe retires 128 lane-ops per SM per clock (FMA or FADD alike) and the MUFU
+# 16 ex2.  The FLOP view (FMA = 2) of our own kernels is kept
+# beside it: 15 + 34 = 49 FLOP per pair.
+LANE_OPS_FUSED, LANE_OPS_RENDER = 36, 10
+MUFU_FUSED, MUFU_RENDER = 2, 1
 FLOP_PER_PAIR_FUSED = 15 + 34
-FLOP_PER_PAIR_RENDER = 15
-FP32_LANES_PER_SM = 128
+FP32_LANES_PER_SM, MUFU_PER_SM = 128, 16
 N_SM = 148
 
 
@@ -60,6 +66,9 @@ def parse():
     ap.add_argument("--batch-images", type=int, default=-1,
                     help="images per launch for the extra batched measurement (0 = skip; "
                          "default: configs[3], 64 images sharded over the ranks)")
+    ap.add_argument("--quick", action="store_true",
+                    help="value, render, decode, batched and e2e only (skips C3, the 50k-step "
+                         "fits, the fitted state, the encoder and QAT): the multi-rank tests")
     return ap.parse_args()
 
 
@@ -206,25 +215,34 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    if world > 1:
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl")
-    dev = torch.device("cuda", local if world > 1 else 0)
+    # one process per GPU over NCCL; GI_DIST_BACKEND=gloo lets the multi-rank
+    # tests run several ranks on one GPU (host-staged collectives, no kernel
+    # of one rank waits on another's)
+    backend = os.environ.get("GI_DIST_BACKEND", "nccl")
+    dev = torch.device("cuda", local % max(1, torch.cuda.device_count()))
     torch.cuda.set_device(dev)
+    if world > 1:
+        dist.init_process_group(backend)
+    coll_dev = dev if backend == "nccl" else torch.device("cpu")
     gi.load()
     K, Wm = max(1, args.steps), max(3, args.warmup)
+    quick = args.quick
 
     def barrier():
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize(dev)
 
-    def max_over_ranks(x: float) -> float:
+    def all_ranks(x: float) -> list:
         if world == 1:
-            return x
-        t = torch.tensor([x], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return float(t.item())
+            return [x]
+        t = torch.tensor([x], dtype=torch.float64, device=coll_dev)
+        parts = [torch.empty_like(t) for _ in range(world)]
+        dist.all_gather(parts, t)
+        return [float(p.item()) for p in parts]
+
+    def max_over_ranks(x: float) -> float:
+        return max(all_ranks(x))
 
     seed = 1 + rank
     p_host = synth.init_params(seed, N_GAUSS)
@@ -233,137 +251,145 @@ def main():
     target = torch.from_numpy(t_host).to(dev).view(1, 3, H_IMG, W_IMG).contiguous()
     flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
     stream = torch.cuda.current_stream(dev)
+    s_ev = [torch.cuda.Event(enable_timing=True) for _ in range(max(K, 100))]
+    e_ev = [torch.cuda.Event(enable_timing=True) for _ in range(max(K, 100))]
 
-    clocks = Clocks(local)
+    def capture(fn):
+        gs = torch.cuda.Stream(device=dev)
+        gs.wait_stream(stream)
+        gg = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(gg, stream=gs):
+            fn()
+        stream.wait_stream(gs)
+        return gg
 
-    # ---------------- fit step (value) ----------------
-    # Two graphs of one fused step: `plain` (what `value` times) and `staged`
-    # (external event nodes at the stage boundaries, for the stage split and
-    # the roofline kernel time).  Event nodes cost several us each inside a
-    # graph, so they are kept out of the timed value.
+    def timed_ms(g, steps, flush_l2=True):
+        """Device ms of `steps` replays (events around each, L2 flushed before
+        each), this rank; barriers on both sides."""
+        for _ in range(Wm):
+            g.replay()
+        barrier()
+        for i in range(steps):
+            if flush_l2:
+                flush.zero_()
+            s_ev[i].record(stream)
+            g.replay()
+            e_ev[i].record(stream)
+        barrier()
+        return sum(s_ev[i].elapsed_time(e_ev[i]) for i in range(steps))
+
+    def rate(g, steps, units_per_replay=1):
+        """Whole-job units/s: all ranks' units / the max-over-ranks time."""
+        return world * steps * units_per_replay / (max_over_ranks(timed_ms(g, steps)) / 1000.0)
+
+    def pairs_keys(pipe):
+        rec = pipe.proj.view(-1, 12).cpu().numpy()
+        bx, by = rec[:, 7].view(np.uint32), rec[:, 11].view(np.uint32)
+        wx = (bx >> 16).astype(np.int64) - (bx & 0xffff).astype(np.int64) + 1
+        wy = (by >> 16).astype(np.int64) - (by & 0xffff).astype(np.int64) + 1
+        tt = pipe.tiles_touched.cpu().numpy().astype(np.int64)
+        return int(np.sum(np.where(tt > 0, wx * wy, 0))), int(tt.sum())
+
+    def tile_counts(p, W, H):
+        """Per-tile key counts of params p (gi_fit_prime into a fresh workspace)."""
+        f = Fitter(p.clone(), torch.zeros(p.shape[0], 3, H, W, device=dev))
+        gi.gi_fit_prime(f.params, f.n, f.f, f.flags, f.cap, f.fit_ws)
+        torch.cuda.synchronize(dev)
+        tc, stride, _, scap = gi.gi_fit_bin_view(f.fit_ws, f.n, f.cap, f.f)
+        off = (tc - f.fit_ws.data_ptr()) // 4
+        T = gi.gi_num_tiles(f.f) * p.shape[0]
+        c = f.fit_ws.view(torch.int32)[off:off + T * stride:stride].cpu().numpy().view(np.uint32)
+        return {"keys": int(c.sum()), "tiles": int(T), "max_per_tile": int(c.max()),
+                "p99_per_tile": float(np.percentile(c, 99)), "slab": int(scap),
+                "tiles_past_slab": int((c > scap).sum()), "tiles_past_512": int((c > 512).sum())}
+
+    def fit_graphs(fit):
+        """(plain graph, staged graph + its 6 stage events) of one fused step;
+        fit.first_seg = the segment statistics of its first step."""
+        fit.step()
+        torch.cuda.synchronize(dev)
+        if fit.check() != gi.GI_OK:
+            raise RuntimeError("fit status")
+        fit.first_seg = fit.seg_stats()
+        plain = fit.capture(1)
+        ev = [torch.cuda.Event(enable_timing=True, external=True) for _ in range(6)]
+        for e in ev:
+            e.record(stream)
+        torch.cuda.synchronize(dev)
+        staged = fit.capture(1, stage_events=ev)
+        return plain, staged, ev
+
+    def stage_split(staged, ev, reps):
+        out = np.zeros(5)
+        for _ in range(reps):
+            flush.zero_()
+            staged.replay()
+            torch.cuda.synchronize(dev)
+            for j in range(5):
+                out[j] += ev[j].elapsed_time(ev[j + 1])
+        return out / reps
+
+    clocks = Clocks(dev.index)
+    pk, pk_kind = peaks()
+    sm_mhz = float(pk.get("sm_max_mhz", 1965.0))
+    lane_peak = FP32_LANES_PER_SM * N_SM * sm_mhz * 1e6          # lane-op/s
+    mufu_peak = MUFU_PER_SM * N_SM * sm_mhz * 1e6                # ex2/s
+    flop_peak = 2 * lane_peak                                    # FLOP/s (FMA = 2)
+
+    # ---------------- fit step (value): C2, one chained Adam step per replay ----------------
     fit = Fitter(params.clone(), target)
-    fit.step()
-    torch.cuda.synchronize(dev)
-    st = fit.check()
-    if st != gi.GI_OK:
-        raise RuntimeError(f"fit status {st}")
-    n0 = gi.gi_launch_count()
-    plain_g = fit.capture(1)
-    launches_per_step = gi.gi_launch_count() - n0
-    stage_ev = [torch.cuda.Event(enable_timing=True, external=True) for _ in range(6)]
-    for e in stage_ev:
-        e.record(stream)
-    torch.cuda.synchronize(dev)
-    staged_g = fit.capture(1, stage_events=stage_ev)
-    for _ in range(Wm):
-        plain_g.replay()
-    torch.cuda.synchronize(dev)
-    # pair count for the roofline at the state the timed steps start from
+    plain_g, staged_g, stage_ev = fit_graphs(fit)
+    # kernels one captured step launches (the capture records the graph's launches)
+    n1 = gi.gi_launch_count()
+    probe_g = fit.capture(1)
+    launches_per_step = gi.gi_launch_count() - n1
+    del probe_g
     probe = Pipeline(N_GAUSS, W_IMG, H_IMG, 1, device=dev)
     probe.project(fit.params)
-    rec = probe.proj.view(-1, 12).cpu().numpy()
-    bx, by = rec[:, 7].view(np.uint32), rec[:, 11].view(np.uint32)
-    wx = (bx >> 16).astype(np.int64) - (bx & 0xffff).astype(np.int64) + 1
-    wy = (by >> 16).astype(np.int64) - (by & 0xffff).astype(np.int64) + 1
-    touched = probe.tiles_touched.cpu().numpy() > 0
-    pairs = int(np.sum(np.where(touched, wx * wy, 0)))
-    keys = int(probe.tiles_touched.cpu().numpy().astype(np.int64).sum())
+    pairs, keys = pairs_keys(probe)
     del probe
-
-    s_ev = [torch.cuda.Event(enable_timing=True) for _ in range(max(K, 10))]
-    e_ev = [torch.cuda.Event(enable_timing=True) for _ in range(max(K, 10))]
-    barrier()
     clocks.start()
-    for i in range(K):
-        flush.zero_()
-        s_ev[i].record(stream)
-        plain_g.replay()
-        e_ev[i].record(stream)
-    barrier()
-    fit_ms = sum(s_ev[i].elapsed_time(e_ev[i]) for i in range(K))
-    fit_ms_max = max_over_ranks(fit_ms)
+    fit_ms = timed_ms(plain_g, K)
+    rank_ms = all_ranks(fit_ms)
+    fit_ms_max = max(rank_ms)
     fit_value = world * K / (fit_ms_max / 1000.0)
-    # stage split (instrumented graph, same flush protocol)
-    stage_ms = np.zeros(5)   # [empty], [empty], tile kernel, finalize+Adam+next projection, tail
-    KS = min(K, 100)
-    for i in range(KS):
-        flush.zero_()
-        staged_g.replay()
-        torch.cuda.synchronize(dev)
-        for j in range(5):
-            stage_ms[j] += stage_ev[j].elapsed_time(stage_ev[j + 1])
-    stage_ms /= KS
-    st = fit.check()
-    if st != gi.GI_OK:
-        raise RuntimeError(f"fit status after timing {st}")
+    stage_ms = stage_split(staged_g, stage_ev, min(K, 100))
+    if fit.check() != gi.GI_OK:
+        raise RuntimeError("fit status after timing")
+    fit_seg = fit.first_seg
 
-    # ---------------- render FPS (gi_render_frame: project+count -> bin -> render) --------
+    # ---------------- render FPS (gi_render_frame: project+count -> render) --------
     pipe = Pipeline(N_GAUSS, W_IMG, H_IMG, 1, device=dev)
     rparams = params.clone()
     pipe.render_frame(rparams)
     torch.cuda.synchronize(dev)
-    rs = torch.cuda.Stream(device=dev)
-    rs.wait_stream(stream)
-    rg = torch.cuda.CUDAGraph()
-    with torch.cuda.graph(rg, stream=rs):
-        pipe.render_frame(rparams)
-    stream.wait_stream(rs)
-    for _ in range(Wm):
-        rg.replay()
-    barrier()
-    for i in range(K):
-        flush.zero_()
-        s_ev[i].record(stream)
-        rg.replay()
-        e_ev[i].record(stream)
-    barrier()
-    r_ms = sum(s_ev[i].elapsed_time(e_ev[i]) for i in range(K))
-    render_fps = world * K / (max_over_ranks(r_ms) / 1000.0)
+    render_fps = rate(capture(lambda: pipe.render_frame(rparams)), K)
     # render-kernel-only time (ABI gi_render on gi_bin output, events around it)
     pipe.project(rparams)
     pipe.bin()
-    r_ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
     r_kernel_ms = 0.0
     for i in range(K):
         flush.zero_()
-        r_ev[0].record(stream)
+        s_ev[0].record(stream)
         pipe.raster()
-        r_ev[1].record(stream)
+        e_ev[0].record(stream)
         torch.cuda.synchronize(dev)
-        r_kernel_ms += r_ev[0].elapsed_time(r_ev[1])
+        r_kernel_ms += s_ev[0].elapsed_time(e_ev[0])
     r_kernel_ms /= K
-    render_pairs = pairs_of(pipe, np)
+    render_pairs, _ = pairs_keys(pipe)
 
-    # ---------------- decode FPS (configs[4]): gi_decode_render_frame (decode fused into project) ----
+    # ---------------- decode FPS (configs[4]): gi_decode_render_frame ----
     data, gamma, beta, books = synth.payload(seed, N_GAUSS)
     d_payload = torch.from_numpy(data).to(dev)
     d_books = torch.from_numpy(books).to(dev)
     dparams = torch.zeros(1, N_GAUSS, 8, dtype=torch.float32, device=dev)
     meta = gi.codec_meta(N_GAUSS, gamma, beta, d_books)
     dpipe = Pipeline(N_GAUSS, W_IMG, H_IMG, 1, device=dev)
-    gi.gi_vq_decode(d_payload, meta, dparams)
-    dpipe.render_frame(dparams, gi.GI_POS_NORMALIZED)
+    dpipe.decode_render_frame(d_payload, meta, dparams)
     torch.cuda.synchronize(dev)
-    ds = torch.cuda.Stream(device=dev)
-    ds.wait_stream(stream)
-    dg = torch.cuda.CUDAGraph()
-    with torch.cuda.graph(dg, stream=ds):
-        dpipe.decode_render_frame(d_payload, meta, dparams)
-    stream.wait_stream(ds)
-    for _ in range(Wm):
-        dg.replay()
-    barrier()
-    for i in range(K):
-        flush.zero_()
-        s_ev[i].record(stream)
-        dg.replay()
-        e_ev[i].record(stream)
-    barrier()
-    d_ms = sum(s_ev[i].elapsed_time(e_ev[i]) for i in range(K))
-    decode_fps = world * K / (max_over_ranks(d_ms) / 1000.0)
-    # codec-realistic record counts (~0.3 / 0.6 bpp at 56-bit records)
+    decode_fps = rate(capture(lambda: dpipe.decode_render_frame(d_payload, meta, dparams)), K)
     decode_small = {}
-    for n_small in (2200, 4500):
+    for n_small in (() if quick else (2200, 4500)):   # SURVEY C5: ~0.3 / 0.6 bpp at 56 bits
         sdata, sg, sb, sbooks = synth.payload(seed, n_small)
         s_pay = torch.from_numpy(sdata).to(dev)
         s_books = torch.from_numpy(sbooks).to(dev)
@@ -372,276 +398,220 @@ def main():
         s_pipe = Pipeline(n_small, W_IMG, H_IMG, 1, device=dev)
         s_pipe.decode_render_frame(s_pay, s_meta, s_params)
         torch.cuda.synchronize(dev)
-        sgs = torch.cuda.Stream(device=dev)
-        sgs.wait_stream(stream)
-        sgr = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(sgr, stream=sgs):
-            s_pipe.decode_render_frame(s_pay, s_meta, s_params)
-        stream.wait_stream(sgs)
-        for _ in range(Wm):
-            sgr.replay()
-        barrier()
-        for i in range(K):
-            flush.zero_()
-            s_ev[i].record(stream)
-            sgr.replay()
-            e_ev[i].record(stream)
-        barrier()
-        sms = sum(s_ev[i].elapsed_time(e_ev[i]) for i in range(K))
-        decode_small[str(n_small)] = world * K / (max_over_ranks(sms) / 1000.0)
-        del sgr, s_pipe
+        decode_small[str(n_small)] = rate(
+            capture(lambda: s_pipe.decode_render_frame(s_pay, s_meta, s_params)), K)
+        del s_pipe
 
     # ---------------- Adan fit step (the paper's optimiser, NEXT-1) ----------------
     afit = Fitter(params.clone(), target, optimizer="adan")
     afit.step()
     torch.cuda.synchronize(dev)
-    ag = afit.capture(1)
-    for _ in range(Wm):
-        ag.replay()
-    barrier()
-    for i in range(K):
-        flush.zero_()
-        s_ev[i].record(stream)
-        ag.replay()
-        e_ev[i].record(stream)
-    barrier()
-    adan_value = world * K / (max_over_ranks(sum(s_ev[i].elapsed_time(e_ev[i]) for i in range(K)))
-                              / 1000.0)
+    adan_value = rate(afit.capture(1), K)
     if afit.check() != gi.GI_OK:
         raise RuntimeError("adan fit status")
-    del afit, ag
+    del afit
+
+    # ---------------- configs[2]: C3, DIV2K-shaped 2040x1356, 100k Gaussians ----------------
+    c3 = None
+    if not quick:
+        c3p = torch.from_numpy(synth.init_params(2 + rank, N_C3)).to(dev)[None].contiguous()
+        c3t = torch.from_numpy(synth.image(2 + rank, W_C3, H_C3)).to(dev)[None].contiguous()
+        c3fit = Fitter(c3p.clone(), c3t)
+        c3plain, c3staged, c3ev = fit_graphs(c3fit)
+        c3_fit = rate(c3plain, K)
+        c3_stage = stage_split(c3staged, c3ev, min(K, 50))
+        c3_seg = c3fit.first_seg
+        c3pipe = Pipeline(N_C3, W_C3, H_C3, 1, device=dev)
+        c3pipe.render_frame(c3p)
+        torch.cuda.synchronize(dev)
+        c3_render = rate(capture(lambda: c3pipe.render_frame(c3p)), K)
+        c3pipe.project(c3p)
+        c3_pairs, c3_keys = pairs_keys(c3pipe)
+        c3_lane = c3_pairs * LANE_OPS_FUSED / (c3_stage[2] * 1e-3)
+        # the fitted proxy (Gaussians ~3x larger, SURVEY "x3")
+        c3f = torch.from_numpy(synth.fitted_params(2 + rank, N_C3)).to(dev)[None].contiguous()
+        c3ffit = Fitter(c3f.clone(), c3t)
+        c3ffit.step()
+        torch.cuda.synchronize(dev)
+        c3_fit_fitted = rate(c3ffit.capture(1), max(10, K // 2))
+        c3_render_fitted = rate(capture(lambda: c3pipe.render_frame(c3f)), max(10, K // 2))
+        c3 = {"workload": "configs[2]: DIV2K-shaped 2040x1356 synthetic image, 100k Gaussians",
+              "fit_its": c3_fit, "render_fps": c3_render,
+              "fit_its_fitted_proxy": c3_fit_fitted, "render_fps_fitted_proxy": c3_render_fitted,
+              "tile_kernel_ms": c3_stage[2], "finalize_ms": c3_stage[3],
+              "tile_kernel_lane_frac": c3_lane / lane_peak, "pairs": c3_pairs, "keys": c3_keys,
+              "tiles_streamed": c3_seg[0], "tiles_past_sort_buffer": c3_seg[1],
+              "tile_counts_fitted_proxy": tile_counts(c3f, W_C3, H_C3)}
+        del c3fit, c3ffit, c3pipe, c3plain, c3staged
 
     # ---------------- the paper's training run: 50k steps (106.59 s on V100) ----
-    # Adam (north_star) and Adan (the paper's), chained, CUDA graphs of 100 steps,
-    # warm L2 as a real fit runs; device time (events), max over ranks; final PSNR
-    full_fit = {}
-    psnr_pipe = Pipeline(N_GAUSS, W_IMG, H_IMG, 1, device=dev)
-    for opt in ("adam", "adan"):
-        ffit = Fitter(params.clone(), target, optimizer=opt)
+    full_fit, fitted_state, warm_its, encode_fps, qat_its = None, None, None, None, None
+    if not quick:
+        full_fit = {}
+        psnr_pipe = Pipeline(N_GAUSS, W_IMG, H_IMG, 1, device=dev)
+        for opt in ("adam", "adan"):
+            ffit = Fitter(params.clone(), target, optimizer=opt)
+            ffit.step()
+            torch.cuda.synchronize(dev)
+            fg = ffit.capture(100)
+            barrier()
+            s_ev[0].record(stream)
+            for _ in range(500):                  # 1 + 500 x 100 = 50,001 steps
+                fg.replay()
+            e_ev[0].record(stream)
+            barrier()
+            secs = max_over_ranks(s_ev[0].elapsed_time(e_ev[0])) / 1000.0
+            img = psnr_pipe.render_frame(ffit.params)
+            full_fit[opt] = {"steps": 50001, "seconds": secs,
+                             "psnr_db": float(psnr_pipe.psnr(img, target)[0])}
+            if ffit.check() != gi.GI_OK:
+                raise RuntimeError("50k fit status")
+            if opt == "adam":
+                fitted = ffit.params.clone()
+            del ffit, fg
+
+        # the fitted state (SURVEY d.1): render FPS of the cloud the 50k-step fit
+        # produced, its per-tile key counts, and configs[4] from it -- C5 payload
+        # by the survey's recipe: fp16 positions, l codes with gamma = (max -
+        # min)/63, beta = min, colours by 5 K-means iterations per RVQ stage
+        # (gi_kmeans_step, B = 8, M = 2), packed by gi_vq_encode
+        fpipe = Pipeline(N_GAUSS, W_IMG, H_IMG, 1, device=dev)
+        fpipe.render_frame(fitted)
+        torch.cuda.synchronize(dev)
+        fitted_state = {"render_fps": rate(capture(lambda: fpipe.render_frame(fitted)), K)}
+        fpipe.render_frame(fitted)
+        torch.cuda.synchronize(dev)
+        fitted_state["tile_counts"] = tile_counts(fitted, W_IMG, H_IMG)
+        ffit = Fitter(fitted.clone(), target)
         ffit.step()
         torch.cuda.synchronize(dev)
-        fg = ffit.capture(100)
+        fitted_state["tiles_streamed_past_sort_buffer"] = list(ffit.seg_stats())
+        fitted_state["fit_its"] = rate(ffit.capture(1), K)
+        del ffit
+        fp_host = fitted[0].cpu().numpy()
+        lmin, lmax = fp_host[:, 2:5].min(axis=0), fp_host[:, 2:5].max(axis=0)
+        c_gamma = [float(x) for x in np.maximum((lmax - lmin) / 63.0, 1e-6)]
+        c_beta = [float(x) for x in lmin]
+        cols = torch.from_numpy(np.ascontiguousarray(fp_host[:, 5:8])).to(dev)
+        kws = torch.zeros(gi.gi_kmeans_workspace_bytes(8), dtype=torch.uint8, device=dev)
+        asg = torch.zeros(N_GAUSS, dtype=torch.int32, device=dev)
+        cbooks = torch.zeros(2, 8, 3, dtype=torch.float32, device=dev)
+        pts = cols
+        for st in range(2):
+            cent = pts[:: N_GAUSS // 8][:8].clone()
+            for _ in range(5):
+                gi.gi_kmeans_step(pts, cent, asg, kws)
+            gi.gi_kmeans_step(pts, cent, asg, kws)        # final assignment for the residuals
+            cbooks[st] = cent
+            pts = (pts - cent[asg.long()]).contiguous()   # stage-2 input: residuals
+        cmeta = gi.codec_meta(N_GAUSS, c_gamma, c_beta, cbooks)
+        cpay = torch.zeros((N_GAUSS * 56 + 7) // 8 + 16, dtype=torch.uint8, device=dev)
+        gi.gi_vq_encode(fitted[0].contiguous(), cmeta, cpay)
+        cparams = torch.zeros(1, N_GAUSS, 8, dtype=torch.float32, device=dev)
+        cpipe = Pipeline(N_GAUSS, W_IMG, H_IMG, 1, device=dev)
+        cpipe.decode_render_frame(cpay, cmeta, cparams)
+        torch.cuda.synchronize(dev)
+        fitted_state["decode_fps"] = rate(
+            capture(lambda: cpipe.decode_render_frame(cpay, cmeta, cparams)), K)
+        dimg = cpipe.decode_render_frame(cpay, cmeta, cparams)
+        fitted_state["psnr_db_fitted"] = float(fpipe.psnr(fpipe.render_frame(fitted), target)[0])
+        fitted_state["psnr_db_decoded"] = float(cpipe.psnr(dimg, target)[0])
+        fitted_state["bpp"] = 56.0 * N_GAUSS / (W_IMG * H_IMG)
+        # the paper's remedy (Fig. 3): quantisation-aware fine-tuning,
+        # then re-encode with the learned gamma / beta and EMA codebooks
+        from paper_2403_08551_b200.pipeline import QatFitter
+        qf = QatFitter(fitted[0].clone(), target, c_gamma, c_beta, cbooks)
+        for _ in range(2000):
+            qf.step()
+        torch.cuda.synchronize(dev)
+        qp = qf.qparams.cpu().numpy()
+        qmeta = gi.codec_meta(N_GAUSS, qp[:3], qp[3:], qf.books)
+        gi.gi_vq_encode(qf.params, qmeta, cpay)
+        dimg = cpipe.decode_render_frame(cpay, qmeta, cparams)
+        fitted_state["psnr_db_decoded_after_qat2000"] = float(cpipe.psnr(dimg, target)[0])
+        del psnr_pipe, fpipe, cpipe, qf
+
+        # fitting as a user runs it: 100 chained steps per graph, warm L2 (context)
+        wfit = Fitter(params.clone(), target)
+        wfit.step()
+        torch.cuda.synchronize(dev)
+        wg = wfit.capture(100)
+        wg.replay()
         barrier()
         s_ev[0].record(stream)
-        for _ in range(500):                  # 1 + 500 x 100 = 50,001 steps
-            fg.replay()
+        for _ in range(3):
+            wg.replay()
         e_ev[0].record(stream)
         barrier()
-        secs = max_over_ranks(s_ev[0].elapsed_time(e_ev[0])) / 1000.0
-        img = psnr_pipe.render_frame(ffit.params)
-        full_fit[opt] = {"steps": 50001, "seconds": secs,
-                         "psnr_db": float(psnr_pipe.psnr(img, target)[0])}
-        if ffit.check() != gi.GI_OK:
-            raise RuntimeError("50k fit status")
-        if opt == "adam":
-            fitted = ffit.params.clone()
-        del ffit, fg
+        warm_its = world * 300 / (max_over_ranks(s_ev[0].elapsed_time(e_ev[0])) / 1000.0)
+        if wfit.check() != gi.GI_OK:
+            raise RuntimeError("warm fit status")
+        del wfit, wg
 
-    # ---------------- the fitted state (SURVEY d.1): render FPS of the cloud the
-    # 50k-step fit produced, and configs[4] from it -- C5 payload built as the
-    # survey's recipe: fp16 positions, l codes with gamma = (max - min)/63,
-    # beta = min, colours by 5 K-means iterations per RVQ stage (gi_kmeans_step,
-    # B = 8, M = 2), packed by gi_vq_encode; then decode + render timed
-    def timed_fps(fn):
-        gs = torch.cuda.Stream(device=dev)
-        gs.wait_stream(stream)
-        gg = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(gg, stream=gs):
-            fn()
-        stream.wait_stream(gs)
-        for _ in range(Wm):
-            gg.replay()
-        barrier()
-        for i in range(K):
-            flush.zero_()
-            s_ev[i].record(stream)
-            gg.replay()
-            e_ev[i].record(stream)
-        barrier()
-        return world * K / (max_over_ranks(sum(s_ev[i].elapsed_time(e_ev[i]) for i in range(K)))
-                            / 1000.0)
+        # NEXT-2: encoder (gi_vq_encode) and QAT step (gi_qat_step)
+        fp = torch.from_numpy(synth.fitted_params(seed, N_GAUSS)).to(dev).contiguous()
+        qgamma, qbeta = [0.05, 0.04, 0.05], [-1.0, -1.2, -1.0]
+        qbooks = torch.from_numpy(np.random.default_rng(seed).normal(0, 0.3, (2, 8, 3))
+                                  .astype(np.float32)).to(dev)
+        emeta = gi.codec_meta(N_GAUSS, qgamma, qbeta, qbooks)
+        epay = torch.zeros((N_GAUSS * 56 + 7) // 8 + 16, dtype=torch.uint8, device=dev)
+        eeff = torch.zeros(N_GAUSS, 8, dtype=torch.float32, device=dev)
+        gi.gi_vq_encode(fp, emeta, epay, eeff)
+        torch.cuda.synchronize(dev)
+        encode_fps = rate(capture(lambda: gi.gi_vq_encode(fp, emeta, epay, eeff,
+                                                          stream=torch.cuda.current_stream())), K)
+        qfit = QatFitter(fp.clone(), target, qgamma, qbeta, qbooks)
+        qfit.step()
+        torch.cuda.synchronize(dev)
+        qat_its = rate(qfit.capture(1), K)
+        if qfit.check() != gi.GI_OK:
+            raise RuntimeError("qat status")
+        del qfit
 
-    fpipe = Pipeline(N_GAUSS, W_IMG, H_IMG, 1, device=dev)
-    fitted_state = {"render_fps": timed_fps(lambda: fpipe.render_frame(fitted))}
-    fpipe.render_frame(fitted)
-    torch.cuda.synchronize(dev)
-    fitted_state["keys"] = fpipe.frame_keys()
-    fp_host = fitted[0].cpu().numpy()
-    lmin, lmax = fp_host[:, 2:5].min(axis=0), fp_host[:, 2:5].max(axis=0)
-    c_gamma = [float(x) for x in np.maximum((lmax - lmin) / 63.0, 1e-6)]
-    c_beta = [float(x) for x in lmin]
-    cols = torch.from_numpy(np.ascontiguousarray(fp_host[:, 5:8])).to(dev)
-    kws = torch.zeros(gi.gi_kmeans_workspace_bytes(8), dtype=torch.uint8, device=dev)
-    asg = torch.zeros(N_GAUSS, dtype=torch.int32, device=dev)
-    books = torch.zeros(2, 8, 3, dtype=torch.float32, device=dev)
-    pts = cols
-    for st in range(2):
-        cent = pts[:: N_GAUSS // 8][:8].clone()
-        for _ in range(5):
-            gi.gi_kmeans_step(pts, cent, asg, kws)
-        gi.gi_kmeans_step(pts, cent, asg, kws)        # final assignment for the residuals
-        books[st] = cent
-        pts = (pts - cent[asg.long()]).contiguous()   # stage-2 input: residuals
-    cmeta = gi.codec_meta(N_GAUSS, c_gamma, c_beta, books)
-    cpay = torch.zeros((N_GAUSS * 56 + 7) // 8 + 16, dtype=torch.uint8, device=dev)
-    gi.gi_vq_encode(fitted[0].contiguous(), cmeta, cpay)
-    cparams = torch.zeros(1, N_GAUSS, 8, dtype=torch.float32, device=dev)
-    cpipe = Pipeline(N_GAUSS, W_IMG, H_IMG, 1, device=dev)
-    fitted_state["decode_fps"] = timed_fps(lambda: cpipe.decode_render_frame(cpay, cmeta, cparams))
-    dimg = cpipe.decode_render_frame(cpay, cmeta, cparams)
-    fitted_state["psnr_db_fitted"] = float(fpipe.psnr(fpipe.render_frame(fitted), target)[0])
-    fitted_state["psnr_db_decoded"] = float(cpipe.psnr(dimg, target)[0])
-    fitted_state["bpp"] = 56.0 * N_GAUSS / (W_IMG * H_IMG)
-    # the paper's remedy (Fig. 3): quantisation-aware fine-tuning,
-    # then re-encode with the learned gamma / beta and EMA codebooks
-    from paper_2403_08551_b200.pipeline import QatFitter
-    qf = QatFitter(fitted[0].clone(), target, c_gamma, c_beta, books)
-    for _ in range(2000):
-        qf.step()
-    torch.cuda.synchronize(dev)
-    qp = qf.qparams.cpu().numpy()
-    qmeta = gi.codec_meta(N_GAUSS, qp[:3], qp[3:], qf.books)
-    gi.gi_vq_encode(qf.params, qmeta, cpay)
-    dimg = cpipe.decode_render_frame(cpay, qmeta, cparams)
-    fitted_state["psnr_db_decoded_after_qat2000"] = float(cpipe.psnr(dimg, target)[0])
-    del psnr_pipe, fpipe, cpipe, qf
-
-    # ---------------- fitting as a user runs it: 100 chained steps per graph, warm L2 ----
-    # (context only: `value` above is the cold-L2 single-step number)
-    wfit = Fitter(params.clone(), target)
-    wfit.step()
-    torch.cuda.synchronize(dev)
-    wg = wfit.capture(100)
-    wg.replay()
-    barrier()
-    s_ev[0].record(stream)
-    for _ in range(3):
-        wg.replay()
-    e_ev[0].record(stream)
-    barrier()
-    warm_its = world * 300 / (max_over_ranks(s_ev[0].elapsed_time(e_ev[0])) / 1000.0)
-    if wfit.check() != gi.GI_OK:
-        raise RuntimeError("warm fit status")
-    del wfit, wg
-
-    # ---------------- NEXT-2: encoder (gi_vq_encode) and QAT step (gi_qat_step) ------------
-    from paper_2403_08551_b200.pipeline import QatFitter
-    fp = torch.from_numpy(synth.fitted_params(seed, N_GAUSS)).to(dev).contiguous()
-    qgamma, qbeta = [0.05, 0.04, 0.05], [-1.0, -1.2, -1.0]
-    qbooks = torch.from_numpy(np.random.default_rng(seed).normal(0, 0.3, (2, 8, 3))
-                              .astype(np.float32)).to(dev)
-    emeta = gi.codec_meta(N_GAUSS, qgamma, qbeta, qbooks)
-    epay = torch.zeros((N_GAUSS * 56 + 7) // 8 + 16, dtype=torch.uint8, device=dev)
-    eeff = torch.zeros(N_GAUSS, 8, dtype=torch.float32, device=dev)
-    gi.gi_vq_encode(fp, emeta, epay, eeff)
-    es = torch.cuda.Stream(device=dev)
-    es.wait_stream(stream)
-    eg = torch.cuda.CUDAGraph()
-    with torch.cuda.graph(eg, stream=es):
-        gi.gi_vq_encode(fp, emeta, epay, eeff, stream=es)
-    stream.wait_stream(es)
-    for _ in range(Wm):
-        eg.replay()
-    barrier()
-    for i in range(K):
-        flush.zero_()
-        s_ev[i].record(stream)
-        eg.replay()
-        e_ev[i].record(stream)
-    barrier()
-    enc_ms = max_over_ranks(sum(s_ev[i].elapsed_time(e_ev[i]) for i in range(K)))
-    encode_fps = world * K / (enc_ms / 1000.0)
-    qfit = QatFitter(fp.clone(), target, qgamma, qbeta, qbooks)
-    qfit.step()
-    torch.cuda.synchronize(dev)
-    qg = qfit.capture(1)
-    for _ in range(Wm):
-        qg.replay()
-    barrier()
-    for i in range(K):
-        flush.zero_()
-        s_ev[i].record(stream)
-        qg.replay()
-        e_ev[i].record(stream)
-    barrier()
-    qat_ms = max_over_ranks(sum(s_ev[i].elapsed_time(e_ev[i]) for i in range(K)))
-    qat_its = world * K / (qat_ms / 1000.0)
-    if qfit.check() != gi.GI_OK:
-        raise RuntimeError("qat status")
-    del qfit, qg, eg
-
-    # ---------------- batched launch (configs[3] pattern): B images per launch ------------
+    # ---------------- configs[3]: 64 images sharded over the ranks, one launch per rank ----
     batched = None
-    B = args.batch_images if args.batch_images >= 0 else max(1, 64 // world)
+    B = args.batch_images if args.batch_images >= 0 else (max(1, 64 // world) if not quick else 2)
     if B > 1:
-        bp = torch.from_numpy(np.stack([synth.init_params(100 + B * rank + b, N_GAUSS)
-                                        for b in range(B)])).to(dev).contiguous()
-        bt = torch.from_numpy(np.stack([synth.image(100 + B * rank + b, W_IMG, H_IMG)
-                                        for b in range(B)])).to(dev).contiguous()
-        bfit = Fitter(bp.clone(), bt)
-        bfit.step()
-        torch.cuda.synchronize(dev)
-        bplain = bfit.capture(1)
-        bev = [torch.cuda.Event(enable_timing=True, external=True) for _ in range(6)]
-        for e in bev:
-            e.record(stream)
-        torch.cuda.synchronize(dev)
-        bstaged = bfit.capture(1, stage_events=bev)
-        for _ in range(Wm):
-            bplain.replay()
+        ids = [100 + B * rank + b for b in range(B)]
+        bp = torch.from_numpy(np.stack([synth.init_params(i, N_GAUSS) for i in ids])).to(dev)
+        bt = torch.from_numpy(np.stack([synth.image(i, W_IMG, H_IMG) for i in ids])).to(dev)
+        bfit = Fitter(bp.contiguous().clone(), bt.contiguous())
+        bplain, bstaged, bev = fit_graphs(bfit)
         KB = max(10, K // 4)
-        barrier()
-        for i in range(KB):
-            flush.zero_()
-            s_ev[i].record(stream)
-            bplain.replay()
-            e_ev[i].record(stream)
-        barrier()
-        b_ms = max_over_ranks(sum(s_ev[i].elapsed_time(e_ev[i]) for i in range(KB)))
-        bk_ms = 0.0
-        for i in range(min(KB, 20)):
-            flush.zero_()
-            bstaged.replay()
-            torch.cuda.synchronize(dev)
-            bk_ms += bev[2].elapsed_time(bev[3])
-        bk_ms /= min(KB, 20)
+        b_ms = max_over_ranks(timed_ms(bplain, KB))
+        bk_ms = stage_split(bstaged, bev, min(KB, 20))[2]
         bpipe = Pipeline(N_GAUSS, W_IMG, H_IMG, B, device=dev)
-        bpipe.project(bp)
+        bpipe.project(bp.contiguous())
         torch.cuda.synchronize(dev)
-        bpairs = pairs_of(bpipe, np)
-        brs = torch.cuda.Stream(device=dev)
-        brs.wait_stream(stream)
-        brg = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(brg, stream=brs):
-            bpipe.render_frame(bp)
-        stream.wait_stream(brs)
-        for _ in range(Wm):
-            brg.replay()
-        barrier()
-        for i in range(KB):
-            flush.zero_()
-            s_ev[i].record(stream)
-            brg.replay()
-            e_ev[i].record(stream)
-        barrier()
-        br_ms = max_over_ranks(sum(s_ev[i].elapsed_time(e_ev[i]) for i in range(KB)))
+        bpairs, _ = pairs_keys(bpipe)
+        bpc = bp.contiguous()
+        br_ms = max_over_ranks(timed_ms(capture(lambda: bpipe.render_frame(bpc)), KB))
+        # per-image PSNR after the timed steps, gathered in global image order
+        bimg = bpipe.render_frame(bfit.params)
+        bpsnr = gather_psnr(bpipe.psnr(bimg, bfit.target).clone(), world * B, world, rank)
         batched = {"workload": "configs[3]: 64 Kodak-shaped images (70k Gaussians each) sharded "
                                "over the ranks, each rank's share fit in one launch"
-                               if args.batch_images < 0 else f"{B} C2 images per launch",
+                               if args.batch_images < 0 and not quick
+                               else f"{B} C2 images per launch per rank",
                    "images_per_launch": B, "images_total": world * B, "steps": KB,
                    "fit_image_its_per_s": world * B * KB / (b_ms / 1000.0),
                    "render_image_fps": world * B * KB / (br_ms / 1000.0),
                    "ms_per_fit_step": b_ms / KB, "fused_tile_kernel_ms": bk_ms,
-                   "fused_tile_kernel_tflops": bpairs * FLOP_PER_PAIR_FUSED / (bk_ms * 1e-3) / 1e12,
-                   "pixel_gaussian_pairs": bpairs}
-        del bfit, bpipe, bplain, bstaged, brg
+                   "fused_tile_kernel_lane_frac":
+                       bpairs * LANE_OPS_FUSED / (bk_ms * 1e-3) / lane_peak,
+                   "pixel_gaussian_pairs": bpairs,
+                   "psnr_db_mean": float(np.nanmean(bpsnr.cpu().numpy())),
+                   "psnr_images": int(np.isfinite(bpsnr.cpu().numpy()).sum())}
+        del bfit, bpipe, bplain, bstaged
 
     # ---------------- e2e through the public API, host buffers ----------------
-    # Every step copies its target image H2D from pinned host memory (on a copy
-    # stream, double-buffered, so step i's copy overlaps step i-1's compute)
-    # and reads its loss back D2H; L2 is still flushed before every step.
-    # e2e = steps / device time of the whole pipelined run (events on the
-    # compute stream; the copy stream is joined before the end event).
+    # Every step: H2D of that step's input (the target image) from pinned host
+    # memory on a copy stream (double-buffered: step i's copy overlaps step
+    # i-1's compute), the fused chained step through the C ABI (no graph), and
+    # the step's result (the loss) written by the finalize kernel straight into
+    # pinned, UVA-mapped host memory.  No L2 flush here (the copies stream
+    # through L2 as a user's would).  e2e = steps / device time of the whole
+    # pipelined run, events on the compute stream after joining the copy stream.
     pinned_t = torch.from_numpy(t_host).pin_memory()
     pinned_loss = torch.zeros(K + Wm, dtype=torch.float32).pin_memory()
     cstream = torch.cuda.Stream(device=dev)
@@ -663,12 +633,8 @@ def main():
                         cstream.wait_event(consumed[b ^ 1])
                     tbuf[b ^ 1].view(-1).copy_(pinned_t.view(-1), non_blocking=True)
                     copied[b ^ 1].record(cstream)
-            flush.zero_()
             stream.wait_event(copied[b])
             e2e_fit.target = tbuf[b]
-            # the loss read-back: the finalize kernel writes it straight into
-            # pinned (UVA-mapped) host memory -- a copy-engine D2H per step
-            # queues behind the next step's H2D and halves the rate
             e2e_fit.step(loss_out=pinned_loss[loss_off + i].data_ptr())
             consumed[b].record(stream)
         stream.wait_stream(cstream)
@@ -680,26 +646,39 @@ def main():
     e_ev[0].record(stream)
     barrier()
     clk = clocks.stop()
-    e2e_ms = s_ev[0].elapsed_time(e_ev[0])
-    e2e_value = world * K / (max_over_ranks(e2e_ms) / 1000.0)
+    e2e_value = world * K / (max_over_ranks(s_ev[0].elapsed_time(e_ev[0])) / 1000.0)
     e2e_losses = pinned_loss.numpy()[: K + Wm]
     if not (np.all(np.isfinite(e2e_losses)) and np.all(e2e_losses > 0)):
         raise RuntimeError("e2e losses missing or not finite")
+    # a whole fit job through the API: params + target H2D once, 1000 chained
+    # steps, fitted params + loss D2H once (the per-fit host traffic)
+    job_steps = 1000
+    pinned_p = torch.from_numpy(p_host).pin_memory()
+    job_out = torch.zeros_like(pinned_p).pin_memory()
+    job_fit = Fitter(params.clone(), target.clone())
+    barrier()
+    s_ev[1].record(stream)
+    job_fit.params.view(-1).copy_(pinned_p.view(-1), non_blocking=True)
+    job_fit.target.view(-1).copy_(pinned_t.view(-1), non_blocking=True)
+    job_fit.unchain()
+    for _ in range(job_steps):
+        job_fit.step()
+    job_out.view(-1).copy_(job_fit.params.view(-1), non_blocking=True)
+    e_ev[1].record(stream)
+    barrier()
+    job_s = max_over_ranks(s_ev[1].elapsed_time(e_ev[1])) / 1000.0
 
-    # ---------------- quality + the one collective (NCCL all-gather of PSNR) ----
+    # ---------------- quality + the one collective (all-gather of PSNR) ----
     img = pipe.render_frame(fit.params)
     psnr = pipe.psnr(img, target).clone()
-    # the one collective of the path: NCCL all-gather of per-image PSNR
     psnrs = gather_psnr(psnr, world, world, rank).tolist()
 
     if rank == 0:
-        pk, pk_kind = peaks()
-        sm_mhz = float(pk.get("sm_max_mhz", 1965.0))
-        fp32_peak = 2 * FP32_LANES_PER_SM * N_SM * sm_mhz * 1e6 / 1e12     # TFLOP/s (FMA = 2)
         kern_ms = stage_ms[2]
-        if batched is not None:
-            batched["fused_tile_kernel_frac"] = batched["fused_tile_kernel_tflops"] / fp32_peak
-        achieved = pairs * FLOP_PER_PAIR_FUSED / (kern_ms * 1e-3) / 1e12
+        lane = pairs * LANE_OPS_FUSED / (kern_ms * 1e-3)
+        mufu = pairs * MUFU_FUSED / (kern_ms * 1e-3)
+        flop = pairs * FLOP_PER_PAIR_FUSED / (kern_ms * 1e-3)
+        r_lane = render_pairs * LANE_OPS_RENDER / (r_kernel_ms * 1e-3)
         traffic = None
         prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
         if os.path.exists(prof):
@@ -712,64 +691,62 @@ def main():
         line = {
             "metric": METRIC, "value": fit_value, "unit": "it/s", "n_gpus": world, "steps": K,
             "warmup": Wm, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": fit_value / world / PAPER_FIT_ITS if world == 1 else None,
-            "dtype": "f32", "data": "synthetic",
-            "config": {"workload": "C2 (configs[1]): Kodak-shaped 768x512 synthetic image, 70k "
-                                   "Gaussians at the paper's init, one Adam fit step "
-                                   "(project+bin+fwd+L2+bwd+finalize+adam)",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": "C2 (configs[1]): 768x512 synthetic image, 70k Gaussians at "
+                                   "the paper's init, one chained Adam fit step per rank",
                        "images_per_gpu": 1, "l2": "flushed (256 MB write) before every timed step",
                        "key_pairs_per_step": keys, "pixel_gaussian_pairs": pairs,
-                       "vs_baseline_ref": "paper fit 469.1 it/s (Table 1a P:331, V100, Adan, "
-                                          "real Kodak): context, other hardware"},
-            "render_fps": render_fps,
-            "fit_its_adan": adan_value,
-            "fit_its_warm_graph100": warm_its,
+                       "render_fps": render_fps,
+                       "c3_fit_its": c3["fit_its"] if c3 else None,
+                       "c3_render_fps": c3["render_fps"] if c3 else None,
+                       "paper": "fit 469.1 it/s, render 2,092 FPS on a V100 (Table 1a P:331, "
+                                "Adan, real Kodak): context, other hardware"},
+            # ---- context (long) ----
             "fit_50k_steps": full_fit,
             "fitted_state": fitted_state,
-            "fitted_note": "context: the cloud the 50k-step Adam fit produced -- render FPS, and "
-                           "configs[4] decode + render of its C5 payload (fp16 positions, 6-bit "
-                           "l codes, 2x8 RVQ colours by K-means, 56-bit records); PSNR before "
-                           "and after the codec, without and with 2000 QAT steps (gi_qat_step)",
-            "fit_50k_note": "the paper's training length (50k steps, P:381) on the C2 synthetic "
-                            "image from the init cloud: device seconds per rank (max), PSNR of "
-                            "the result; paper: 106.59 s on a V100 (Table 1a, P:331), context",
-            "fit_warm_note": "context, not `value`: 100 chained Adam steps per CUDA graph "
-                             "replay, no L2 flush between steps (a long fit as a user runs it)",
-            "batched": batched,
-            "decode_fps": decode_fps,
-            "decode_fps_codec_sizes": decode_small,
+            "fit_its_warm_graph100": warm_its,
             "encode_fps": encode_fps,
             "qat_its": qat_its,
-            "next2_note": "encode_fps: gi_vq_encode of 70k fitted records (fp16 positions, "
-                          "6-bit codes, 2x8 RVQ, packed 56-bit records + dequantised params); "
-                          "qat_its: gi_qat_step on the C2 fitted proxy (quantise, fused fit "
-                          "core, straight-through Adam, EMA codebooks)",
+            "decode_fps_codec_sizes": decode_small,
+            "batched": batched,
             "stage_ms": {"tile_kernel_fwd_l2_bwd": stage_ms[2],
                          "finalize_adam_next_projection_binning": stage_ms[3],
-                         "event_overhead_empty_stages": stage_ms[0] + stage_ms[1],
-                         "note": "chained step = 2 kernels; staged graph with event nodes "
-                                 "(each costs a few us), so the stages add up to more than "
-                                 "ms_per_step"},
-            "render_kernel_ms": r_kernel_ms,
+                         "event_overhead_empty_stages": stage_ms[0] + stage_ms[1]},
+            "segments": {"c2_tiles_streamed": fit_seg[0],
+                         "c2_tiles_past_sort_buffer": fit_seg[1]},
+            "rank_ms": rank_ms,
             "psnr_db_after_fit_steps": psnrs,
-            "roofline": {"kernel": "backward_tile_kernel (fused Eq.7 fwd + L2 + App.A bwd)",
-                         "bound": "alu", "achieved": achieved, "peak": fp32_peak,
-                         "unit": "TFLOP/s", "frac": achieved / fp32_peak, "traffic": traffic,
-                         "peak_kind": f"FP32 FMA pipe: 128 lanes x 2 FLOP x 148 SM x "
-                                      f"{sm_mhz:.0f} MHz ({pk_kind} sm_max_mhz)",
-                         "algorithmic": f"{FLOP_PER_PAIR_FUSED} FLOP per in-box pair x {pairs} "
-                                        f"pairs per launch",
-                         "render_kernel_frac": render_pairs * FLOP_PER_PAIR_RENDER
-                         / (r_kernel_ms * 1e-3) / 1e12 / fp32_peak},
+            "fit_job": {"steps": job_steps, "seconds": job_s, "its": job_steps / job_s,
+                        "h2d_bytes": int(p_host.nbytes + t_host.nbytes),
+                        "d2h_bytes": int(p_host.nbytes)},
+            # ---- headline (kept at the end of the line) ----
+            "c3": c3,
+            "render_fps": render_fps,
+            "render_kernel_ms": r_kernel_ms,
+            "decode_fps": decode_fps,
+            "fit_its_adan": adan_value,
+            "roofline": {"kernel": "backward_tile_kernel (fused Eq.7 fwd + L2 + App.A bwd), C2",
+                         "bound": "alu", "achieved": lane / 1e12, "peak": lane_peak / 1e12,
+                         "unit": "T FP32 lane-op/s", "frac": lane / lane_peak,
+                         "traffic": traffic,
+                         "algorithmic": f"{LANE_OPS_FUSED} FP32 lane-ops + {MUFU_FUSED} ex2 per "
+                                        f"in-box pair (SURVEY d.3) x {pairs} pairs per launch "
+                                        f"/ {kern_ms * 1e3:.1f} us",
+                         "peak_kind": f"128 FP32 lanes x 148 SM x {sm_mhz:.0f} MHz ({pk_kind} "
+                                      f"sm_max_mhz)",
+                         "mufu_frac": mufu / mufu_peak,
+                         "frac_flop49": flop / flop_peak,
+                         "render_kernel_frac": r_lane / lane_peak,
+                         "c3_tile_kernel_frac": c3["tile_kernel_lane_frac"] if c3 else None,
+                         "batched_tile_kernel_frac":
+                             batched["fused_tile_kernel_lane_frac"] if batched else None},
             "clocks": clk,
             "e2e": {"value": e2e_value, "unit": "it/s",
                     "h2d_bytes_per_step": int(t_host.nbytes), "d2h_bytes_per_step": 4,
-                    "path": "Fitter.step -> gi_fit_step_chained (C ABI, no graph); per step: "
-                            "H2D of the target from pinned host on a copy stream (double-"
-                            "buffered, overlapping the previous step), L2 flush, fit step whose "
-                            "finalize kernel writes the loss into pinned, UVA-mapped host "
-                            "memory (the step's D2H); value = steps / device time; bound by "
-                            "the host link (pinned H2D 22-37 GB/s across boxes)"},
+                    "path": "Fitter.step -> gi_fit_step_chained (C ABI, no graph): target H2D "
+                            "from pinned host per step (copy stream, double-buffered), loss "
+                            "written by the finalize kernel into mapped pinned host memory; "
+                            "host-link bound"},
             "gpu_launches": int(launches_per_step * K),
             "gpu_launches_per_step": int(launches_per_step),
         }
@@ -779,15 +756,6 @@ def main():
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
-
-
-def pairs_of(pipe, np_):
-    rec = pipe.proj.view(-1, 12).cpu().numpy()
-    bx, by = rec[:, 7].view(np_.uint32), rec[:, 11].view(np_.uint32)
-    wx = (bx >> 16).astype(np_.int64) - (bx & 0xffff).astype(np_.int64) + 1
-    wy = (by >> 16).astype(np_.int64) - (by & 0xffff).astype(np_.int64) + 1
-    touched = pipe.tiles_touched.cpu().numpy() > 0
-    return int(np_.sum(np_.where(touched, wx * wy, 0)))
 
 
 if __name__ == "__main__":

@@ -177,7 +177,10 @@ double gi_lr_at(int32_t step, double lr0, int32_t half_every);
  *   fit_ws        gi_fit_workspace_bytes() bytes: holds proj, tiles_touched,
  *                 keys, ranges, n_keys and both stage workspaces.  MUST be
  *                 zero-filled once before its first use (it carries per-tile
- *                 counters that every fused call leaves zeroed for the next)
+ *                 counters that every non-chained fused call leaves zeroed
+ *                 for the next).  gi_fit_step, gi_fit_grads and gi_fit_prime
+ *                 clear the binning state themselves (one memset), so they
+ *                 may follow chained steps on the same workspace
  *   loss          [B] fp32 out (L2 loss of the step's forward), may be NULL
  *   status_flags  device u32, bit 0 set on a non-finite parameter, may be NULL
  *   stage_events  NULL, or 6 cudaEvent_t (as void*) recorded (external) at
@@ -209,7 +212,17 @@ gi_status gi_fit_step_adan(float* params, float* grads, float* m, float* v, floa
  * gi_fit_step_chained call then REQUIRES that fit_ws holds the projection of
  * the current params -- i.e. it follows gi_fit_prime or another chained call
  * on the same params/fit_ws with no other writer of params in between -- and
- * leaves it so for the next call.  Same arguments as gi_fit_step. */
+ * leaves it so for the next call.  Same arguments as gi_fit_step.
+ * A chained call leaves the NEXT step's keys (per-tile counts, slab entries)
+ * in fit_ws.  gi_fit_prime clears that state before it projects, so it is
+ * also the recovery path after params were modified between chained steps.
+ * gi_fit_reset clears it without projecting: required before gi_render_frame
+ * or gi_decode_render_frame reuse a workspace a chained step left (they
+ * assume zeroed counters and do not clear them, to stay one memset-free
+ * graph).  Errors: GI_EINVAL (frame, n, capacity, workspace size/alignment),
+ * GI_ECUDA. */
+gi_status gi_fit_reset(int32_t n, const gi_frame* f, int64_t key_capacity, void* fit_ws,
+                       size_t ws_bytes, void* stream);
 gi_status gi_fit_prime(const float* params, int32_t n, const gi_frame* f, uint32_t flags,
                        int64_t key_capacity, void* fit_ws, size_t ws_bytes, void* stream);
 gi_status gi_fit_step_chained(float* params, float* grads, float* m, float* v, const float* target,
@@ -284,6 +297,26 @@ gi_status gi_render_frame(const float* params, int32_t n, const gi_frame* f, uin
                           int64_t key_capacity, void* frame_ws, size_t ws_bytes, float* image,
                           void* stream);
 
+/* Direct-binning state inside fit_ws (inspection, e.g. parity tests): after
+ * gi_fit_prime or a chained step, image b's tile t (global tile g = b*T + t)
+ * holds tile_count[g * count_stride] keys; the first min(count, slab_capacity)
+ * gids are slab[g * slab_capacity + 0 ..) in atomic (unordered) order; a
+ * tile with more keys streams them from all Gaussians of its image.  Device
+ * pointers into fit_ws; nothing is launched.  GI_EINVAL on bad arguments. */
+gi_status gi_fit_bin_view(const void* fit_ws, int32_t n, int64_t key_capacity, const gi_frame* f,
+                          const uint32_t** tile_count, uint32_t* count_stride,
+                          const uint32_t** slab, uint32_t* slab_capacity);
+
+/* Segment statistics inside fit_ws (device u32[2], accumulated by every
+ * consumer tile kernel since the last gi_fit_prime / gi_fit_reset /
+ * non-chained step, which zero them): [0] tiles whose key count exceeded the
+ * direct-binning slab (streamed from all N Gaussians of the image: the slow
+ * path), [1] tiles whose segment exceeded the kernel's shared sort buffer
+ * (rebuilt in gid order in global memory).  The per-tile slab holds
+ * max(key_capacity / tiles, 1024) keys (GI_SLAB_MIN overrides the 1024).
+ * NULL on bad arguments; nothing is launched. */
+uint32_t* gi_fit_seg_stats(void* fit_ws, int32_t n, int64_t key_capacity, const gi_frame* f);
+
 /* Device status words inside fit_ws (for gi_check): */
 const uint32_t* gi_fit_n_keys(const void* fit_ws, int32_t n, int64_t key_capacity,
                               const gi_frame* f);
@@ -296,7 +329,9 @@ const uint32_t* gi_fit_n_keys(const void* fit_ws, int32_t n, int64_t key_capacit
  *   c'        = C^1[i^1] + ... + C^M[i^M] (fp32, stage order)         Eq. 9
  * params [n][8] fp32 out, positions normalised: project with
  * GI_POS_NORMALIZED.  GI_EFORMAT if R > 64, bits > 16, codebook < 2 or
- * stages > 8 or payload_bytes too small. */
+ * stages > 8 or payload_bytes too small.  An index field >= codebook (only
+ * possible when codebook is not a power of two: a corrupt record) is clamped
+ * to codebook - 1, so no read leaves the codebooks. */
 typedef struct {
     int32_t n, bits, stages, codebook;
     float gamma[3], beta[3];
@@ -331,7 +366,9 @@ gi_status gi_decode_render_frame(const uint8_t* payload, size_t payload_bytes,
  * may be NULL): payload -- the records packed exactly as gi_vq_decode reads
  * them (the call zero-fills the first ceil(n*R/8) bytes; payload_bytes must
  * cover them); eff [n][8] fp32 -- the dequantised parameters, bit-identical
- * to gi_vq_decode(payload).  Same GI_EFORMAT rules as gi_vq_decode. */
+ * to gi_vq_decode(payload).  Same GI_EFORMAT rules as gi_vq_decode.
+ * payload must be 4-byte aligned (records are OR-ed into 32-bit words):
+ * GI_EINVAL otherwise. */
 gi_status gi_vq_encode(const float* params, uint32_t flags, const gi_codec_meta* meta,
                        uint8_t* payload, size_t payload_bytes, float* eff, void* stream);
 

@@ -1,6 +1,7 @@
 // C ABI of libgi (include/gi.h): argument validation, workspace carving and
 // dispatch to the sm_100a kernels.  Host-side only; no allocation, no sync
 // except in gi_check.
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -84,7 +85,9 @@ FitWs carve_fit(void* base, int32_t n, int64_t cap, const gi_frame& f) {
     w.proj = reinterpret_cast<gi::Proj*>(p + off); off += align_up(sizeof(gi::Proj) * total);
     w.touched = reinterpret_cast<uint32_t*>(p + off); off += align_up(4 * total);
     w.key_tile = reinterpret_cast<uint32_t*>(p + off); off += align_up(4 * (size_t)cap);
-    w.key_gid = reinterpret_cast<uint32_t*>(p + off); off += align_up(4 * (size_t)cap);
+    // key_gid doubles as the direct-binning slab array (>= cap words)
+    const size_t kg = std::max((size_t)cap, gi::slab_words(cap, f));
+    w.key_gid = reinterpret_cast<uint32_t*>(p + off); off += align_up(4 * kg);
     w.tile_range = reinterpret_cast<uint32_t*>(p + off); off += align_up(4 * (T + 1));
     w.n_keys = reinterpret_cast<uint32_t*>(p + off); off += align_up(4);
     w.bin_ws = p + off; off += align_up(gi::bin_ws_bytes(n, cap, f));
@@ -286,6 +289,29 @@ const uint32_t* gi_fit_n_keys(const void* fit_ws, int32_t n, int64_t key_capacit
     return carve_fit(const_cast<void*>(fit_ws), n, key_capacity, *f).n_keys;
 }
 
+gi_status gi_fit_bin_view(const void* fit_ws, int32_t n, int64_t key_capacity, const gi_frame* f,
+                          const uint32_t** tile_count, uint32_t* count_stride,
+                          const uint32_t** slab, uint32_t* slab_capacity) {
+    gi_status st;
+    if ((st = check_frame(f)) != GI_OK || (st = check_n(n, f)) != GI_OK) return st;
+    if (!fit_ws || key_capacity < 0 || !tile_count || !count_stride || !slab || !slab_capacity)
+        return invalid("NULL argument");
+    FitWs w = carve_fit(const_cast<void*>(fit_ws), n, key_capacity, *f);
+    const gi::BinCounts bc =
+        gi::bin_counts_direct(w.bin_ws, n, key_capacity, *f, w.key_gid, nullptr);
+    *tile_count = bc.tile_count;
+    *count_stride = (uint32_t)gi::kCountStride;
+    *slab = w.key_gid;
+    *slab_capacity = gi::slab_capacity(key_capacity, *f);
+    return GI_OK;
+}
+
+uint32_t* gi_fit_seg_stats(void* fit_ws, int32_t n, int64_t key_capacity, const gi_frame* f) {
+    if (check_frame(f) != GI_OK || !fit_ws || n < 0 || key_capacity < 0) return nullptr;
+    FitWs w = carve_fit(fit_ws, n, key_capacity, *f);
+    return gi::bin_seg_stats(w.bin_ws, n, key_capacity, *f);
+}
+
 static cudaError_t record_stage(void* const* ev, int i, cudaStream_t s) {
     if (ev == nullptr || ev[i] == nullptr) return cudaSuccess;
     // external: becomes an event-record node when the stream is being captured
@@ -349,6 +375,8 @@ static gi_status fit_step_impl(float* params, float* grads, float* m, float* v, 
         cs.wd = adan->weight_decay;
     }
     GI_TRY(record_stage(stage_events, 0, s), "gi_fit_step/event");
+    if (!chained)   // the workspace may hold a chained step's pending keys: start from zero
+        GI_TRY(gi::bin_clear(w.bin_ws, n, key_capacity, *f, s), "gi_fit_step/clear");
     if (!chained)
         GI_TRY(gi::launch_project(params, n, *f, flags, w.proj, w.touched,
                                   gi::ProjectFuse{step_counter, bc}, s),
@@ -418,6 +446,7 @@ gi_status gi_fit_grads(const float* params, float* grads, const float* target, i
         return GI_OK;
     }
     const int r0 = tile_row0, r1 = tile_row0 + tile_rows;
+    GI_TRY(gi::bin_clear(w.bin_ws, n, key_capacity, *f, s), "gi_fit_grads/clear");
     uint32_t* gauss_off = gi::backward_gauss_off(w.bwd_ws, n, key_capacity, *f);
     gi::BinCounts bc = gi::bin_counts_direct(w.bin_ws, n, key_capacity, *f, w.key_gid, gauss_off);
     bc.row0 = r0;
@@ -487,12 +516,28 @@ gi_status gi_fit_prime(const float* params, int32_t n, const gi_frame* f, uint32
     if (!aligned16(params) || !aligned16(fit_ws)) return invalid("alignment");
     FitWs w = carve_fit(fit_ws, n, key_capacity, *f);
     uint32_t* gauss_off = gi::backward_gauss_off(w.bwd_ws, n, key_capacity, *f);
+    // a workspace left by a chained step already holds the next step's keys
+    // (per-tile counts, slab entries, allocation counter): start from zero
+    cudaError_t e = gi::bin_clear(w.bin_ws, n, key_capacity, *f, S(stream));
+    if (e != cudaSuccess) return cuda_status(e, "gi_fit_prime/clear");
     return cuda_status(
         gi::launch_project(params, n, *f, flags, w.proj, w.touched,
                            gi::ProjectFuse{nullptr, gi::bin_counts_direct(w.bin_ws, n, key_capacity,
                                                                           *f, w.key_gid, gauss_off)},
                            S(stream)),
         "gi_fit_prime");
+}
+
+gi_status gi_fit_reset(int32_t n, const gi_frame* f, int64_t key_capacity, void* fit_ws,
+                       size_t ws_bytes, void* stream) {
+    gi_status st;
+    if ((st = check_frame(f)) != GI_OK || (st = check_n(n, f)) != GI_OK) return st;
+    if (key_capacity < 0 || key_capacity >= (1LL << 31)) return invalid("key_capacity");
+    if (!fit_ws || ws_bytes < carve_fit(nullptr, n, key_capacity, *f).bytes)
+        return invalid("fit workspace too small");
+    if (!aligned16(fit_ws)) return invalid("alignment");
+    FitWs w = carve_fit(fit_ws, n, key_capacity, *f);
+    return cuda_status(gi::bin_clear(w.bin_ws, n, key_capacity, *f, S(stream)), "gi_fit_reset");
 }
 
 gi_status gi_fit_step_chained(float* params, float* grads, float* m, float* v, const float* target,
@@ -645,6 +690,8 @@ gi_status gi_vq_encode(const float* params, uint32_t flags, const gi_codec_meta*
     }
     if (meta->n > 0 && (!params || !meta->codebooks)) return invalid("NULL buffer");
     if (!aligned16(params) || !aligned16(eff)) return invalid("alignment");
+    // records narrower than a byte multiple are OR-ed into 32-bit words from the base
+    if (reinterpret_cast<uintptr_t>(payload) % 4 != 0) return invalid("payload alignment (4 B)");
     return cuda_status(gi::launch_vq_encode(params, !(flags & GI_POS_NORMALIZED), *meta, payload,
                                             eff, S(stream)),
                        "gi_vq_encode");

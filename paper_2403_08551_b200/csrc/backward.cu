@@ -259,15 +259,16 @@ __global__ void __launch_bounds__(256, GI_TILE_MINB) backward_tile_kernel(
             // row-major walk: dx steps by 1 and wraps half a pixel past the
             // box's last column (far above the stepping's rounding), c dy
             // advances by c per row
+            const float2 O = sh.sr.o[r];          // {u0, v0}
             const float dx0 = ((float)lx0 + 0.5f) - B.z;
             const float dx1 = ((float)lx1 + 1.0f) - B.z;
             float dx = ((float)(lx0 + col) + 0.5f) - B.z;
-            float cdy = A.z * (((float)(ly0 + row) + 0.5f) - B.w);
+            float cdy = fmaf(A.z, ((float)(ly0 + row) + 0.5f) - B.w, O.y);   // c dy + v0
             const float4* gp_ptr = &sh.g[(ly0 + row) * kTile + lx0 + col];
             const int wrap = kTile - wdt;
             float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f, a4 = 0.f, a5 = 0.f, a6 = 0.f, a7 = 0.f;
             for (int k = k0; k < k1; ++k) {
-                const float u = A.x * dx;
+                const float u = fmaf(A.x, dx, O.x);
                 const float v = fmaf(A.y, dx, cdy);
                 const float w = ex2_approx(fmaf(-u, u, -(v * v)));
                 const float4 gp = *gp_ptr;
@@ -454,10 +455,11 @@ __global__ void __launch_bounds__(128, GI_TILE2_MINB) backward_tile2_kernel(
 #endif
                 const float4 A = sh.sr.a[en.x];      // {a, b, c, c'r}
                 const float4 B = sh.sr.b[en.x];      // {c'g, c'b, mx, my}
+                const float2 O = sh.sr.o[en.x];      // {u0, v0}
                 const float dx = cx - B.z;
                 const float dy = cy0 - B.w;
-                const float u = A.x * dx;
-                const float v0 = fmaf(A.y, dx, A.z * dy);
+                const float u = fmaf(A.x, dx, O.x);
+                const float v0 = fmaf(A.y, dx, fmaf(A.z, dy, O.y));
                 const float v1 = fmaf(A.z, 4.0f, v0);
                 const float uu = u * u;
                 float w0 = ex2_approx(fmaf(-v0, v0, -uu));
@@ -635,15 +637,16 @@ __global__ void __launch_bounds__(128, GI_TILE2_MINB) backward_tile2_kernel(
             // row-major walk: dx steps by 1 and wraps half a pixel past the
             // box's last column (far above the stepping's rounding), c dy
             // advances by c per row
+            const float2 O = sh.sr.o[r];          // {u0, v0}
             const float dx0 = ((float)lx0 + 0.5f) - B.z;
             const float dx1 = ((float)lx1 + 1.0f) - B.z;
             float dx = ((float)(lx0 + col) + 0.5f) - B.z;
-            float cdy = A.z * (((float)(ly0 + row) + 0.5f) - B.w);
+            float cdy = fmaf(A.z, ((float)(ly0 + row) + 0.5f) - B.w, O.y);   // c dy + v0
             const float4* gp_ptr = &sh.g[(ly0 + row) * kTile + lx0 + col];
             const int wrap = kTile - wdt;
             float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f, a4 = 0.f, a5 = 0.f, a6 = 0.f, a7 = 0.f;
             for (int k = k0; k < k1; ++k) {
-                const float u = A.x * dx;
+                const float u = fmaf(A.x, dx, O.x);
                 const float v = fmaf(A.y, dx, cdy);
                 const float w = ex2_approx(fmaf(-u, u, -(v * v)));
                 const float4 gp = *gp_ptr;
@@ -731,15 +734,6 @@ __global__ void __launch_bounds__(256) alloc_kernel(const Proj* __restrict__ pro
         if (cnt > 4u) off = first + cnt <= pcap ? (uint32_t)first : kOffOverflow;
     }
     if (g < total) gauss_off[g] = off;
-}
-
-__device__ __forceinline__ float adam1(float p, float g, float& m, float& v, float b1, float b2,
-                                       float lr, float ibc1, float ibc2, float eps) {
-    m = fmaf(b1, m, (1.0f - b1) * g);
-    v = fmaf(b2, v, (1.0f - b2) * (g * g));
-    float sq;
-    asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(sq) : "f"(v * ibc2));
-    return p - __fdividef(lr * (m * ibc1), sq + eps);
 }
 
 // Per Gaussian: sum its tiles' partials (row-major tile order), then the
@@ -844,20 +838,23 @@ __device__ __forceinline__ void finalize_one(int g, bool live, const FinArgs& a,
         }
         float4 r0 = make_float4(0.f, 0.f, 0.f, 0.f), r1 = r0;
         if (any && !cov_rs(flags)) {
-            // Cholesky, fp32 (the 1e-4 gradient bar leaves ample room)
-            const float l1 = p0.z + 0.5f, l2 = p0.w, l3 = p1.x + 0.5f;
-            const float il1 = 1.0f / l1, il3 = 1.0f / l3;
-            const float ik = (float)(1.0 / kKappa), ik2 = (float)(1.0 / (kKappa * kKappa));
-            const float Sp = S[3] * ik, Sq = S[4] * ik;
-            const float Spp = S[5] * ik2, Spq = S[6] * ik2, Sqq = S[7] * ik2;
-            const float l2l3 = l2 * il3;
-            const float Ax = (Sp - Sq * l2l3) * il1;         // sum gamma dsigma/ddx
-            const float Ay = Sq * il3;
-            r0.x = -Ax;                                       // dmu_pix = -dsigma/dd (R13)
-            r0.y = -Ay;
-            r0.z = -(Spp - Spq * l2l3) * il1;                 // dl1
-            r0.w = -Spq * il3;                                // dl2
-            r1.x = -Sqq * il3;                                // dl3
+            // Cholesky, in fp64: (Sp - Sq l2/l3) / l1 and (Spp - Spq l2/l3) / l1
+            // cancel for near-line Gaussians (|l2 / l3| large); one thread
+            // per Gaussian, so the wider arithmetic is off the critical path
+            const double l1 = (double)__fadd_rn(p0.z, 0.5f), l2 = (double)p0.w;
+            const double l3 = (double)__fadd_rn(p1.x, 0.5f);
+            const double il1 = 1.0 / l1, il3 = 1.0 / l3;
+            const double ik = 1.0 / kKappa, ik2 = 1.0 / (kKappa * kKappa);
+            const double Sp = S[3] * ik, Sq = S[4] * ik;
+            const double Spp = S[5] * ik2, Spq = S[6] * ik2, Sqq = S[7] * ik2;
+            const double l2l3 = l2 * il3;
+            const double Ax = (Sp - Sq * l2l3) * il1;        // sum gamma dsigma/ddx
+            const double Ay = Sq * il3;
+            r0.x = (float)-Ax;                                // dmu_pix = -dsigma/dd (R13)
+            r0.y = (float)-Ay;
+            r0.z = (float)(-(Spp - Spq * l2l3) * il1);        // dl1
+            r0.w = (float)(-Spq * il3);                       // dl2
+            r1.x = (float)(-Sqq * il3);                       // dl3
         } else if (any) {
             // NEXT-3 rotation-scaling: L = chol(Sigma) as in the projection, then
             // G = dL/dSigma = -1/2 L^-T M L^-1 with M = sum gamma (p, q)(p, q)^T,
@@ -924,15 +921,24 @@ __device__ __forceinline__ void finalize_one(int g, bool live, const FinArgs& a,
                 float4* nn = reinterpret_cast<float4*>(adam.n) + 2 * (size_t)g;
                 float4* gg = reinterpret_cast<float4*>(adam.gprev) + 2 * (size_t)g;
                 nn[0] = n0; nn[1] = n1; gg[0] = gp0; gg[1] = gp1;
-            } else {
-                q0.x = adam1(p0.x, r0.x, m0.x, v0.x, b1, b2, lr, ibc1, ibc2, eps);
-                q0.y = adam1(p0.y, r0.y, m0.y, v0.y, b1, b2, lr, ibc1, ibc2, eps);
-                q0.z = adam1(p0.z, r0.z, m0.z, v0.z, b1, b2, lr, ibc1, ibc2, eps);
-                q0.w = adam1(p0.w, r0.w, m0.w, v0.w, b1, b2, lr, ibc1, ibc2, eps);
-                q1.x = adam1(p1.x, r1.x, m1.x, v1.x, b1, b2, lr, ibc1, ibc2, eps);
-                q1.y = adam1(p1.y, r1.y, m1.y, v1.y, b1, b2, lr, ibc1, ibc2, eps);
-                q1.z = adam1(p1.z, r1.z, m1.z, v1.z, b1, b2, lr, ibc1, ibc2, eps);
-                q1.w = adam1(p1.w, r1.w, m1.w, v1.w, b1, b2, lr, ibc1, ibc2, eps);
+            } else {   // gi_adam_step's arithmetic (adam_update: IEEE sqrt and division)
+                const float omb1 = 1.0f - b1, omb2 = 1.0f - b2;
+                q0.x = p0.x;
+                adam_update(q0.x, r0.x, m0.x, v0.x, b1, b2, omb1, omb2, lr, ibc1, ibc2, eps);
+                q0.y = p0.y;
+                adam_update(q0.y, r0.y, m0.y, v0.y, b1, b2, omb1, omb2, lr, ibc1, ibc2, eps);
+                q0.z = p0.z;
+                adam_update(q0.z, r0.z, m0.z, v0.z, b1, b2, omb1, omb2, lr, ibc1, ibc2, eps);
+                q0.w = p0.w;
+                adam_update(q0.w, r0.w, m0.w, v0.w, b1, b2, omb1, omb2, lr, ibc1, ibc2, eps);
+                q1.x = p1.x;
+                adam_update(q1.x, r1.x, m1.x, v1.x, b1, b2, omb1, omb2, lr, ibc1, ibc2, eps);
+                q1.y = p1.y;
+                adam_update(q1.y, r1.y, m1.y, v1.y, b1, b2, omb1, omb2, lr, ibc1, ibc2, eps);
+                q1.z = p1.z;
+                adam_update(q1.z, r1.z, m1.z, v1.z, b1, b2, omb1, omb2, lr, ibc1, ibc2, eps);
+                q1.w = p1.w;
+                adam_update(q1.w, r1.w, m1.w, v1.w, b1, b2, omb1, omb2, lr, ibc1, ibc2, eps);
             }
             mm[0] = m0; mm[1] = m1; vv[0] = v0; vv[1] = v1;
             pw[0] = q0; pw[1] = q1;

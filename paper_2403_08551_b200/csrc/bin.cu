@@ -276,6 +276,7 @@ struct BinWs {
     uint32_t* fill;
     uint32_t* alloc_counter;
     uint32_t* n_keys_acc;
+    uint32_t* seg_stats;
     uint4* key_rank;
     uint32_t* scan_ws;
     size_t bytes;
@@ -294,6 +295,7 @@ BinWs carve(void* base, int n, int64_t cap, const gi_frame& f) {
     w.fill = reinterpret_cast<uint32_t*>(p + off); off += sizeof(uint32_t) * (size_t)TT;
     w.alloc_counter = reinterpret_cast<uint32_t*>(p + off); off += sizeof(uint32_t);
     w.n_keys_acc = reinterpret_cast<uint32_t*>(p + off); off += sizeof(uint32_t);
+    w.seg_stats = reinterpret_cast<uint32_t*>(p + off); off += 2 * sizeof(uint32_t);
     off = align_up(off);                                   // 256-B (uint4 key_rank)
     w.key_rank = reinterpret_cast<uint4*>(p + off); off += align_up(sizeof(uint4) * (total + 1));
     w.scan_ws = reinterpret_cast<uint32_t*>(p + off); off += align_up(sizeof(uint32_t) * scan_ws_words(TT + 1));
@@ -312,9 +314,28 @@ BinCounts bin_counts(void* ws, int n, int64_t cap, const gi_frame& f) {
     return BinCounts{w.tile_count, w.big_count, w.key_rank, nullptr, 0u, nullptr, nullptr, nullptr, 0u};
 }
 
+uint32_t slab_min() {
+    static const uint32_t v = [] {
+        const char* e = std::getenv("GI_SLAB_MIN");
+        return e == nullptr ? 1024u : (uint32_t)std::strtoul(e, nullptr, 10);
+    }();
+    return v;
+}
+
 uint32_t slab_capacity(int64_t cap, const gi_frame& f) {
     const int64_t TT = (int64_t)tiles_x(f.width) * tiles_y(f.height) * f.batch;
-    return TT > 0 ? (uint32_t)(cap / TT) : 0u;
+    if (TT <= 0) return 0u;
+    const int64_t s = cap / TT, lo = (int64_t)slab_min();
+    return (uint32_t)(s > lo ? s : lo);
+}
+
+size_t slab_words(int64_t cap, const gi_frame& f) {
+    const size_t TT = (size_t)tiles_x(f.width) * tiles_y(f.height) * f.batch;
+    return TT * slab_capacity(cap, f);
+}
+
+uint32_t* bin_seg_stats(void* ws, int n, int64_t cap, const gi_frame& f) {
+    return carve(ws, n, cap, f).seg_stats;
 }
 
 BinCounts bin_counts_direct(void* ws, int n, int64_t cap, const gi_frame& f, uint32_t* slab,
@@ -337,6 +358,7 @@ ChainState bin_chain_direct(void* ws, int n, int64_t cap, const gi_frame& f, uin
     cs.slab_cap = slab_capacity(cap, f);
     cs.n_keys = n_keys;
     cs.n_keys_acc = w.n_keys_acc;
+    cs.seg_stats = w.seg_stats;
     cs.step_counter = step_counter;
     return cs;
 }
@@ -348,7 +370,8 @@ uint32_t* bin_alloc_counter(void* ws, int n, int64_t cap, const gi_frame& f) {
 cudaError_t bin_clear(void* ws, int n, int64_t cap, const gi_frame& f, cudaStream_t s) {
     BinWs w = carve(ws, n, cap, f);
     const size_t TT = (size_t)tiles_x(f.width) * tiles_y(f.height) * f.batch;
-    return cudaMemsetAsync(w.tile_count, 0, sizeof(uint32_t) * ((kCountStride + 2) * TT + 2), s);
+    // tile_count .. n_keys_acc, seg_stats: adjacent
+    return cudaMemsetAsync(w.tile_count, 0, sizeof(uint32_t) * ((kCountStride + 2) * TT + 4), s);
 }
 
 cudaError_t launch_bin(const Proj* proj, const uint32_t* tiles_touched, int n, const gi_frame& f,

@@ -49,7 +49,9 @@ __device__ __forceinline__ void decode_one(const uint8_t* __restrict__ payload, 
     const float l3 = __fmaf_rn((float)take(qp.bits), qp.gamma[2], qp.beta[2]);
     float c0 = 0.f, c1 = 0.f, c2 = 0.f;
     for (int m = 0; m < qp.stages; ++m) {
-        const uint32_t idx = take(qp.ib);
+        // an ib-bit field can exceed B - 1 when B is not a power of two (a
+        // corrupt payload): clamp, so no read leaves the staged codebooks
+        const uint32_t idx = min(take(qp.ib), (uint32_t)(qp.codebook - 1));
         const float* cw = sb + (m * qp.codebook + (int)idx) * 3;
         if (m == 0) {
             c0 = cw[0]; c1 = cw[1]; c2 = cw[2];

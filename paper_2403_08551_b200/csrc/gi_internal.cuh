@@ -314,6 +314,10 @@ struct ChainState {
     uint32_t* n_keys;
     uint32_t* n_keys_acc;
     uint32_t* step_counter;   // chained fit: incremented once by the consumer
+    // statistics (may be null): [0] tiles whose count exceeded the slab
+    // (streamed from all Gaussians), [1] tiles whose segment exceeded the
+    // kernel's sort buffer (rebuilt in order in global memory)
+    uint32_t* seg_stats;
     int row0, row1;           // NEXT-4 tile-row window (row1 = 0: whole image)
     // fused Adam: the consumer's CTA 0 turns the step t (after the increment)
     // into {lr_t, 1 / (1 - b1^t), 1 / (1 - b2^t)} for the finalize kernel
@@ -375,7 +379,15 @@ size_t bin_ws_bytes(int n, int64_t cap, const gi_frame& f);
 BinCounts bin_counts(void* ws, int n, int64_t cap, const gi_frame& f);
 // Direct binning (fused paths): keys go to slab = a key_gid array of cap
 // entries, slab_cap = cap / (tiles x batch) per tile.
+// Direct-binning slab per tile: cap / tiles, at least slab_min() keys (the
+// slab array is slab_words() long, which may exceed cap: memory is plentiful,
+// and a tile past its slab streams its keys from all N Gaussians).
+// slab_min() = 1024, or GI_SLAB_MIN from the environment (tests force small
+// slabs to exercise the streaming path; results never depend on it).
+uint32_t slab_min();
 uint32_t slab_capacity(int64_t cap, const gi_frame& f);
+size_t slab_words(int64_t cap, const gi_frame& f);
+uint32_t* bin_seg_stats(void* ws, int n, int64_t cap, const gi_frame& f);
 BinCounts bin_counts_direct(void* ws, int n, int64_t cap, const gi_frame& f, uint32_t* slab,
                             uint32_t* gauss_off);
 ChainState bin_chain_direct(void* ws, int n, int64_t cap, const gi_frame& f, uint32_t* slab,

@@ -72,11 +72,10 @@ __global__ void __launch_bounds__(256) qat_quantize_kernel(
             for (int j = 0; j < 5; ++j) atomicAdd(&acc[5 * k + j], shared_read_u64(sa + 10 * k + 2 * j));
 }
 
+// gi_adam_step's arithmetic (one definition: adam_update)
 __device__ __forceinline__ float adam_step(float p, float g, float& m, float& v, float b1, float b2,
                                            float lr, float ibc1, float ibc2, float eps) {
-    m = fmaf(b1, m, (1.0f - b1) * g);
-    v = fmaf(b2, v, (1.0f - b2) * (g * g));
-    return p - lr * (m * ibc1) / (sqrtf(v * ibc2) + eps);
+    return adam_update(p, g, m, v, b1, b2, 1.0f - b1, 1.0f - b2, lr, ibc1, ibc2, eps);
 }
 
 // grads holds d/dp^ on entry and d/draw on exit.

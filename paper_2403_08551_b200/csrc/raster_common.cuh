@@ -74,13 +74,23 @@ __device__ __forceinline__ TileCtx make_tile_ctx(int W, int H, int TX, int row0)
 
 // Staged record j (tile-local):
 //   a = {a, b, c, c'r}          factored conic (sigma log2 e = (a dx)^2 + (b dx + c dy)^2)
-//   b = {c'g, c'b, mx, my}      centre minus the tile origin
+//   b = {c'g, c'b, mx, my}      centre minus the tile origin, rounded to fp32
+//   o = {u0, v0}                the rounding of (mx, my) carried into (u, v):
+//                               u = a dx + u0, v = b dx + c dy + v0 with
+//                               dx = cx - mx, u0 = -a mx_lo, v0 = -(b mx_lo + c my_lo)
 //   c = {lx0 | lx1 << 8 | ly0 << 16 | ly1 << 24   box clipped to the tile,
 //        column mask | row mask << 16,            the same as 16-bit masks,
 //        partial slot (backward only), gid}
+// Why o: a tile-local centre rounds to ulp(|mx|) (~5e-7 px at |mx| ~ 10),
+// and the conic multiplies that by a (or b) -- ~70 px^-1 for a Gaussian
+// 0.012 px wide, enough to move sigma by 1e-4 and its gradient past the 1e-4
+// bar.  With the exact remainder mx_lo folded into (u0, v0), (u, v) carry an
+// error of ulp(dx) instead, at no extra instruction per pair (u, v become
+// FMAs with the correction as addend).
 struct StagedRecords {
     float4 a[kBatch];
     float4 b[kBatch];
+    float2 o[kBatch];
     uint4 c[kBatch];
 };
 
@@ -104,8 +114,12 @@ __device__ __forceinline__ void stage_gid(StagedRecords& sr, const Proj* __restr
     const Proj r = proj[gid];
     const int tx0 = t.tx * kTile, ty0 = t.ty * kTile;
     const int ix = __float_as_int(r.q0.x), iy = __float_as_int(r.q0.y);
-    const float mx = __fadd_rn((float)(ix - tx0), r.q0.z);
-    const float my = __fadd_rn((float)(iy - ty0), r.q0.w);
+    // (ix - tx0) + fx as mx + mx_lo exactly (TwoSum; the integer is exact in fp32)
+    const float ixf = (float)(ix - tx0), iyf = (float)(iy - ty0);
+    const float mx = __fadd_rn(ixf, r.q0.z), my = __fadd_rn(iyf, r.q0.w);
+    const float bx_ = __fsub_rn(mx, ixf), by_ = __fsub_rn(my, iyf);
+    const float mx_lo = __fadd_rn(__fsub_rn(ixf, __fsub_rn(mx, bx_)), __fsub_rn(r.q0.z, bx_));
+    const float my_lo = __fadd_rn(__fsub_rn(iyf, __fsub_rn(my, by_)), __fsub_rn(r.q0.w, by_));
     const uint32_t bx = __float_as_uint(r.q1.w), by = __float_as_uint(r.q2.w);
     const int x0 = (int)(bx & 0xffffu), x1 = (int)(bx >> 16);
     const int y0 = (int)(by & 0xffffu), y1 = (int)(by >> 16);
@@ -124,6 +138,7 @@ __device__ __forceinline__ void stage_gid(StagedRecords& sr, const Proj* __restr
     }
     sr.a[j] = make_float4(r.q1.x, r.q1.y, r.q1.z, r.q2.x);
     sr.b[j] = make_float4(r.q2.y, r.q2.z, mx, my);
+    sr.o[j] = make_float2(-(r.q1.x * mx_lo), -fmaf(r.q1.y, mx_lo, r.q1.z * my_lo));
     sr.c[j] = make_uint4((uint32_t)(lx0 | lx1 << 8 | ly0 << 16 | ly1 << 24),
                          span_mask16(lx0, lx1) | span_mask16(ly0, ly1) << 16, slot, gid);
 }
@@ -158,12 +173,13 @@ struct PairEval {
     float w, u, v;
 };
 
-__device__ __forceinline__ PairEval eval_pair(const float4 A, const float4 B, const TileCtx& t) {
+__device__ __forceinline__ PairEval eval_pair(const float4 A, const float4 B, const float2 O,
+                                              const TileCtx& t) {
     PairEval e;
     const float dx = t.cx - B.z;
     const float dy = t.cy - B.w;
-    e.u = A.x * dx;
-    e.v = fmaf(A.y, dx, A.z * dy);
+    e.u = fmaf(A.x, dx, O.x);
+    e.v = fmaf(A.y, dx, fmaf(A.z, dy, O.y));
     e.w = ex2_approx(fmaf(-e.u, e.u, -(e.v * e.v)));
     return e;
 }
@@ -180,7 +196,7 @@ __device__ __forceinline__ void forward_batch(const StagedRecords& sr, const War
         const uint2 en = ent[k];
         const float4 A = sr.a[en.x];
         const float4 B = sr.b[en.x];
-        const PairEval pe = eval_pair(A, B, t);
+        const PairEval pe = eval_pair(A, B, sr.o[en.x], t);
         const float w = (en.y & bit) ? pe.w : 0.f;
         acc0 = fmaf(A.w, w, acc0);
         acc1 = fmaf(B.x, w, acc1);
@@ -327,10 +343,15 @@ __device__ __forceinline__ Seg open_segment(const Proj* __restrict__ proj,
         const uint32_t count = *(volatile const uint32_t*)&cs.tile_count[(size_t)tt * kCountStride];
         const uint32_t s = (uint32_t)tt * cs.slab_cap;
         if (count > cs.slab_cap) {
-            if (threadIdx.x == 0) *cursor = 0u;
+            if (threadIdx.x == 0) {
+                *cursor = 0u;
+                if (cs.seg_stats != nullptr) atomicAdd(&cs.seg_stats[0], 1u);
+            }
             __syncthreads();
             return Seg{s, count, kSegStream};
         }
+        if (count > (uint32_t)SMAX && threadIdx.x == 0 && cs.seg_stats != nullptr)
+            atomicAdd(&cs.seg_stats[1], 1u);
         const int r = sorted_segment<NT, SMAX>(proj, key_gid, s, s + count, n, t.img, t.tx,
                                                t.ty, sl, scratch8);
         return Seg{s, count, r >= 0 ? kSegSorted : kSegGlobal};

@@ -131,10 +131,11 @@ __global__ void __launch_bounds__(128, GI_RENDER2_MINB) render2_kernel(const Pro
             const uint4 en = ent[k];
             const float4 A = sh.sr.a[en.x];      // {a, b, c, c'r}
             const float4 B = sh.sr.b[en.x];      // {c'g, c'b, mx, my}
+            const float2 O = sh.sr.o[en.x];      // {u0, v0}
             const float dx = cx - B.z;
             const float dy = cy0 - B.w;
-            const float u = A.x * dx;
-            const float v0 = fmaf(A.y, dx, A.z * dy);
+            const float u = fmaf(A.x, dx, O.x);
+            const float v0 = fmaf(A.y, dx, fmaf(A.z, dy, O.y));
             const float v1 = fmaf(A.z, 4.0f, v0);
             const float uu = u * u;
             float w0 = ex2_approx(fmaf(-v0, v0, -uu));

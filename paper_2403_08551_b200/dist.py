@@ -41,8 +41,12 @@ def gather_psnr(local: torch.Tensor, n_images: int, world: int, rank: int) -> to
     if world == 1:
         parts = [buf]
     else:
-        parts = [torch.empty_like(buf) for _ in range(world)]
-        dist.all_gather(parts, buf)
+        # NCCL gathers device buffers; gloo (CPU tests, several ranks sharing
+        # one GPU in the multi-rank tests) gathers host-staged copies
+        staged = buf.cpu() if buf.is_cuda and dist.get_backend() == "gloo" else buf
+        parts = [torch.empty_like(staged) for _ in range(world)]
+        dist.all_gather(parts, staged)
+        parts = [p.to(local.device) for p in parts]
     out = torch.empty(int(n_images), dtype=torch.float32, device=local.device)
     for r in range(world):
         idx = shard(n_images, world, r)
@@ -107,6 +111,17 @@ class SpatialFitter:
     grad_fn(params, row0, rows) -> (grads, loss) may replace the libgi call
     (CPU tests of the collective plumbing).
 
+    adam_fn(params, grads, m, v, t, lr) may replace gi_adam_step (with
+    grad_fn: the CPU tests' stand-in; the product path takes neither).  The
+    learning rate is gi_lr_at's schedule (the library's definition, R17).
+
+    Measurement status: NEXT-4 has only run with G ranks on ONE GPU (two
+    processes, host barriers); it is unmeasured across GPUs.  Each step has
+    two host synchronisations + process-group barriers, ~tens of us against a
+    ~80 us C3 step on one B200, so at G = 2 it is likely SLOWER than one GPU
+    until those become device-side flags in peer memory (not built: a flag
+    barrier cannot be exercised with one GPU).
+
     exchange="peer" (GPU ranks of one node): instead of all_reduce + Adam,
     every rank writes its window's gradients and loss into an IPC-mapped
     exchange buffer (gi_peer_alloc / gi_peer_open, handles swapped over the
@@ -116,7 +131,8 @@ class SpatialFitter:
 
     def __init__(self, params: torch.Tensor, target: torch.Tensor, rank: int = 0, world: int = 1,
                  k: float = 3.0, key_capacity: int | None = None, lr0: float = 1e-3,
-                 half_every: int = 20000, grad_fn=None, flags: int = 0, exchange: str = "nccl"):
+                 half_every: int = 20000, grad_fn=None, flags: int = 0, exchange: str = "nccl",
+                 adam_fn=None):
         self.rank, self.world = int(rank), int(world)
         self.params = params.contiguous()
         self.target = target.contiguous()
@@ -130,11 +146,14 @@ class SpatialFitter:
         self.n = self.params.shape[-2]
         self.window = row_windows((H + 15) // 16, self.world)[self.rank]
         self.grad_fn = grad_fn
+        self.adam_fn = adam_fn
+        if (grad_fn is None) != (adam_fn is None):
+            raise ValueError("grad_fn and adam_fn replace the libgi calls together (CPU tests)")
         self.flags = flags
+        from . import gi
+        self.gi = gi
         if grad_fn is None:
-            from . import gi
             from .pipeline import _bytes, default_capacity
-            self.gi = gi
             self.f = gi.frame(W, H, 1, k)
             self.cap = int(key_capacity) if key_capacity else default_capacity(self.n, 1)
             self.ws = _bytes(gi.gi_fit_workspace_bytes(self.n, self.cap, self.f), self.params.device)
@@ -184,7 +203,7 @@ class SpatialFitter:
             torch.cuda.synchronize()
             dist.barrier()
         self.t += 1
-        lr = self.lr0 * 0.5 ** ((self.t - 1) // self.half_every)
+        lr = self.gi.gi_lr_at(self.t, self.lr0, self.half_every)
         self.gi.gi_peer_adam_step(self.params, self.m, self.v, self.peers, self.count, self.t, lr,
                                   n_loss=1, loss_out=self.loss)
         if self.world > 1:                 # every peer read done before the next overwrite
@@ -200,14 +219,9 @@ class SpatialFitter:
             dist.all_reduce(self.grads, op=dist.ReduceOp.SUM)
             dist.all_reduce(self.loss, op=dist.ReduceOp.SUM)
         self.t += 1
-        lr = self.lr0 * 0.5 ** ((self.t - 1) // self.half_every)
-        if self.grad_fn is not None:          # CPU plumbing test: the textbook update
-            b1, b2, eps = 0.9, 0.999, 1e-8
-            self.m.mul_(b1).add_(self.grads, alpha=1 - b1)
-            self.v.mul_(b2).addcmul_(self.grads, self.grads, value=1 - b2)
-            mh = self.m / (1 - b1 ** self.t)
-            vh = self.v / (1 - b2 ** self.t)
-            self.params.sub_(lr * mh / (vh.sqrt() + eps))
+        lr = self.gi.gi_lr_at(self.t, self.lr0, self.half_every)
+        if self.adam_fn is not None:
+            self.adam_fn(self.params, self.grads, self.m, self.v, self.t, lr)
         else:
             self.gi.gi_adam_step(self.params, self.grads, self.m, self.v, self.params.numel(),
                                  self.t, lr)
@@ -218,12 +232,19 @@ if __name__ == "__main__":
     import sys
     n_img = int(sys.argv[1]) if len(sys.argv) > 1 else 64
     steps = int(sys.argv[2]) if len(sys.argv) > 2 else 100
+    n_g = int(sys.argv[3]) if len(sys.argv) > 3 else 70000
+    W = int(sys.argv[4]) if len(sys.argv) > 4 else 768
+    H = int(sys.argv[5]) if len(sys.argv) > 5 else 512
     rank, world, local = env_rank_world()
+    dev = torch.device("cuda", local % torch.cuda.device_count())
     if world > 1:
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl")
-    ps, mine = fit_sharded(n_img, steps, 70000, 768, 512)
+        torch.cuda.set_device(dev)
+        # GI_DIST_BACKEND=gloo: several ranks on one GPU (tests); NCCL otherwise
+        dist.init_process_group(os.environ.get("GI_DIST_BACKEND", "nccl"))
+    ps, mine = fit_sharded(n_img, steps, n_g, W, H, device=dev)
     if rank == 0:
-        print({"images": n_img, "ranks": world, "mean_psnr": float(ps.mean()), "psnr": ps.tolist()})
+        import json
+        print(json.dumps({"images": n_img, "ranks": world, "mean_psnr": float(ps.mean()),
+                          "psnr": ps.tolist()}), flush=True)
     if world > 1:
         dist.destroy_process_group()

@@ -94,6 +94,10 @@ SIGNATURES = {
                                    _sz, _vp, _f32, _i32, _f32, _f32, _f32, _f32, _f32, _vp, _vp,
                                    _vp]),
     "gi_fit_prime": (C.c_int, [_vp, _i32, _FP, _u32, _i64, _vp, _sz, _vp]),
+    "gi_fit_reset": (C.c_int, [_i32, _FP, _i64, _vp, _sz, _vp]),
+    "gi_fit_seg_stats": (_vp, [_vp, _i32, _i64, _FP]),
+    "gi_fit_bin_view": (C.c_int, [_vp, _i32, _i64, _FP, C.POINTER(_vp), C.POINTER(C.c_uint32),
+                                  C.POINTER(_vp), C.POINTER(C.c_uint32)]),
     "gi_fit_step_chained": (C.c_int, [_vp, _vp, _vp, _vp, _vp, _i32, _FP, _u32, _i64, _vp, _sz, _vp,
                                       _f32, _i32, _f32, _f32, _f32, _vp, _vp, _vp, _vp]),
     "gi_render_frame": (C.c_int, [_vp, _i32, _FP, _u32, _i64, _vp, _sz, _vp, _vp]),
@@ -303,6 +307,27 @@ def gi_fit_prime(params, n, f, flags, key_capacity, fit_ws, stream=None):
     _ok(load().gi_fit_prime(_ptr(params), int(n), C.byref(f), int(flags), int(key_capacity),
                             _ptr(fit_ws), fit_ws.numel() * fit_ws.element_size(), _stream(stream)),
         "gi_fit_prime")
+
+
+def gi_fit_reset(n, f, key_capacity, fit_ws, stream=None):
+    _ok(load().gi_fit_reset(int(n), C.byref(f), int(key_capacity), _ptr(fit_ws),
+                            fit_ws.numel() * fit_ws.element_size(), _stream(stream)),
+        "gi_fit_reset")
+
+
+def gi_fit_seg_stats(fit_ws, n, key_capacity, f) -> int:
+    """Device address of the u32[2] segment statistics inside fit_ws."""
+    return load().gi_fit_seg_stats(_ptr(fit_ws), int(n), int(key_capacity), C.byref(f)) or 0
+
+
+def gi_fit_bin_view(fit_ws, n, key_capacity, f):
+    """Device addresses of the direct-binning state inside fit_ws:
+    (tile_count address, count stride in u32, slab address, slab capacity)."""
+    tc, sl = _vp(), _vp()
+    stride, scap = C.c_uint32(), C.c_uint32()
+    _ok(load().gi_fit_bin_view(_ptr(fit_ws), int(n), int(key_capacity), C.byref(f), C.byref(tc),
+                               C.byref(stride), C.byref(sl), C.byref(scap)), "gi_fit_bin_view")
+    return int(tc.value or 0), int(stride.value), int(sl.value or 0), int(scap.value)
 
 
 def gi_render_frame(params, n, f, flags, key_capacity, frame_ws, image, stream=None):

@@ -219,6 +219,14 @@ class Fitter:
         off = (ptr - base) // 4
         return int(self.fit_ws.view(torch.int32)[off].item()) & 0xffffffff
 
+    def seg_stats(self) -> tuple[int, int]:
+        """(tiles streamed past their slab, tiles past the sort buffer) since
+        the last prime / reset / non-chained step."""
+        ptr = gi.gi_fit_seg_stats(self.fit_ws, self.n, self.cap, self.f)
+        off = (ptr - self.fit_ws.data_ptr()) // 4
+        w = self.fit_ws.view(torch.int32)[off:off + 2].cpu().tolist()
+        return int(w[0]) & 0xffffffff, int(w[1]) & 0xffffffff
+
     def check(self) -> int:
         # direct binning has no hard key capacity (overflowing tiles are
         # streamed), so only the device status word is checked

@@ -87,6 +87,14 @@ def _fake_grads(params, r0, rows):
     return torch.sin(params) * (rows / TY) * (1.0 + 0.0 * r0), torch.tensor([rows / TY])
 
 
+def _torch_adam(params, grads, m, v, t, lr, b1=0.9, b2=0.999, eps=1e-8):
+    # CPU stand-in for gi_adam_step in the collective-plumbing tests (the
+    # textbook update; the product path runs libgi's kernel)
+    m.mul_(b1).add_(grads, alpha=1 - b1)
+    v.mul_(b2).addcmul_(grads, grads, value=1 - b2)
+    params.sub_(lr * (m / (1 - b1 ** t)) / ((v / (1 - b2 ** t)).sqrt() + eps))
+
+
 def _spatial_worker(rank, world, port, q):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
@@ -94,7 +102,7 @@ def _spatial_worker(rank, world, port, q):
     torch.manual_seed(0)
     p = torch.randn(1, 50, 8)
     t = torch.zeros(1, 3, 16 * TY, 64)
-    fit = SpatialFitter(p.clone(), t, rank, world, grad_fn=_fake_grads)
+    fit = SpatialFitter(p.clone(), t, rank, world, grad_fn=_fake_grads, adam_fn=_torch_adam)
     for _ in range(3):
         fit.step()
     q.put((rank, fit.params.clone(), float(fit.loss[0]), fit.window))
@@ -118,7 +126,7 @@ def test_spatial_sharding_gloo_world2():
         assert p.exitcode == 0
     torch.manual_seed(0)
     p = torch.randn(1, 50, 8)
-    ref = SpatialFitter(p.clone(), torch.zeros(1, 3, 16 * TY, 64), 0, 1, grad_fn=_fake_grads)
+    ref = SpatialFitter(p.clone(), torch.zeros(1, 3, 16 * TY, 64), 0, 1, grad_fn=_fake_grads, adam_fn=_torch_adam)
     for _ in range(3):
         ref.step()
     assert res[0][2] == (0, TY // 2) and res[1][2] == (TY // 2, TY // 2)

@@ -262,15 +262,13 @@ def fuzz_params(rng, n):
     k = rng.random(n)
     p[k < 0.05, 2] = -0.5
     p[(k >= 0.05) & (k < 0.1), 4] = -0.5
-    # signed (negative) diagonals; |l_ii + 1/2| >= 0.3 and |l2| <= 1 keep the
-    # correlation away from +-1: a near-line Gaussian (|rho| -> 1, sigma_min
-    # -> 0) evaluates v = b dx + c dy with cancellation, and its gradients are
-    # fp32-limited at ~1e-4 relative (parity margins)
+    # signed (negative) diagonals, any off-diagonal: near-singular and
+    # near-line Gaussians included (|l_ii + 1/2| down to 0, |l2| up to 3)
     neg = (k >= 0.1) & (k < 0.2)
     m = int(neg.sum())
-    p[neg, 2] = -rng.uniform(0.8, 3.0, size=m)
-    p[neg, 3] = rng.uniform(-1.0, 1.0, size=m)
-    p[neg, 4] = -rng.uniform(0.8, 3.0, size=m)
+    p[neg, 2] = -rng.uniform(0.0, 3.0, size=m)
+    p[neg, 3] = rng.uniform(-3.0, 3.0, size=m)
+    p[neg, 4] = -rng.uniform(0.0, 3.0, size=m)
     edge = (k >= 0.2) & (k < 0.3)
     p[edge, 0:2] = rng.choice([-4.0, 4.0], size=(int(edge.sum()), 2)) * rng.uniform(0.5, 1.0, size=(int(edge.sum()), 2))
     huge = (k >= 0.3) & (k < 0.32)
@@ -278,18 +276,6 @@ def fuzz_params(rng, n):
     p[huge, 4] = rng.uniform(10, 60, size=int(huge.sum()))
     p[(k >= 0.32) & (k < 0.4), 5:8] *= -1.0
     return p.astype(np.float32)
-
-
-def fuzz_regime(gio, p, W, H):
-    """Scale the colours (the image is linear in c') so that the frame stays
-    within the paper's regime (pixel sums <= 2 for targets on [0, 1]): far
-    above it fp32 sums of ~10 with cancelling residuals meet the 1e-4
-    gradient bar only by luck -- a precision limit, not a defect."""
-    peak = float(np.abs(gio.render(p, W, H)).max()) if len(p) else 0.0
-    if peak > 2.0:
-        p = p.copy()
-        p[:, 5:8] *= np.float32(2.0 / peak)
-    return p
 
 
 def pix_ok(img, ref):
@@ -309,7 +295,7 @@ def test_fuzz_small_frames(gi, gio, seed):
     rng = np.random.default_rng(1000 + seed)
     W, H = int(rng.integers(1, 200)), int(rng.integers(1, 150))
     n = int(rng.integers(1, 1500))
-    p = fuzz_regime(gio, fuzz_params(rng, n), W, H)
+    p = fuzz_params(rng, n)
     tgt = synth.image(seed, W, H)
     pipe = run_gpu(gi, p[None], W, H)["pipe"]
     kt, kg, _ = gio.bin(p, W, H)
@@ -345,7 +331,7 @@ def test_fuzz_batched(gi, gio, seed):
     B = int(rng.integers(2, 5))
     W, H = int(rng.integers(8, 160)), int(rng.integers(8, 120))
     n = int(rng.integers(1, 800))
-    ps = np.stack([fuzz_regime(gio, fuzz_params(rng, n), W, H) for _ in range(B)])
+    ps = np.stack([fuzz_params(rng, n) for _ in range(B)])
     ts = np.stack([synth.image(50 + 7 * seed + b, W, H) for b in range(B)])
     fp = Pipeline(n, W, H, B, device=DEV)
     img = fp.render_frame(to_dev(ps).contiguous()).cpu().numpy()
@@ -687,36 +673,57 @@ def test_rs_fit_steps(gi, gio):
 
 
 @pytest.mark.parametrize("per_tile", [2, 40])
-def test_direct_binning_overflow(gi, gio, per_tile):
-    # slab capacity below the per-tile key count: overflowing tiles stream
-    # their keys in gid order from all Gaussians, so frames, gradients and
-    # updates are bitwise those of a roomy slab (and match the oracle)
-    from paper_2403_08551_b200.pipeline import Fitter, Pipeline
-    W, H, n = 96, 64, 600
-    p = params_for(n, 3, True)
-    tgt = synth.image(3, W, H)
-    TT = (W // 16) * (H // 16)
-    small = TT * per_tile
-    pd = to_dev(p)[None].contiguous()
-    a = Pipeline(n, W, H, 1, device=DEV).render_frame(pd).clone()
-    b = Pipeline(n, W, H, 1, key_capacity=small, device=DEV).render_frame(pd).clone()
+def test_direct_binning_overflow(per_tile):
+    # slab capacity below the per-tile key count (GI_SLAB_MIN=0 lets the
+    # capacity set the slab): overflowing tiles stream their keys in gid order
+    # from all Gaussians, so frames, gradients and updates are bitwise those
+    # of a roomy slab (and match the oracle); run in a fresh process
+    import os
+    import subprocess
+    import sys
+    code = f"""
+import numpy as np, torch, synth
+from oracle import gio
+from paper_2403_08551_b200 import gi
+from paper_2403_08551_b200.pipeline import Fitter, Pipeline
+W, H, n = 96, 64, 600
+p = synth.fitted_params(3, n)
+tgt = synth.image(3, W, H)
+TT = (W // 16) * (H // 16)
+small = TT * {per_tile}
+pd = torch.from_numpy(p).cuda()[None].contiguous()
+big = 4 * TT * 600
+a = Pipeline(n, W, H, 1, key_capacity=big).render_frame(pd).clone()
+b = Pipeline(n, W, H, 1, key_capacity=small).render_frame(pd).clone()
+torch.cuda.synchronize()
+assert torch.equal(a, b)
+ref_img, loss, g = gio.loss_and_grads(p, tgt, mode=gio.ALL_PAIRS)
+assert np.abs(b[0].cpu().numpy() - ref_img).max() <= 2e-5
+res = []
+for cap in (big, small):
+    fit = Fitter(pd.clone(), torch.from_numpy(tgt).cuda()[None].contiguous(), key_capacity=cap)
+    fit.step()
     torch.cuda.synchronize()
-    assert torch.equal(a, b)
-    ref_img, loss, g = gio.loss_and_grads(p, tgt, mode=gio.ALL_PAIRS)
-    assert np.abs(b[0].cpu().numpy() - ref_img).max() <= PIX_TOL
-    res = []
-    for cap in (None, small):
-        fit = Fitter(pd.clone(), to_dev(tgt)[None].contiguous(), key_capacity=cap)
+    gg = fit.grads[0].cpu().numpy().astype(np.float64)
+    for cols in ([0, 1], [2, 3, 4], [5, 6, 7]):
+        e = np.linalg.norm(gg[:, cols] - g[:, cols]) / np.linalg.norm(g[:, cols])
+        assert e <= 1e-4, (cols, e)
+    streamed = fit.seg_stats()[0]
+    assert streamed == 0 if cap == big else (streamed > 0 or {per_tile} >= 40), streamed
+    for _ in range(3):
         fit.step()
-        torch.cuda.synchronize()
-        assert max(group_err(fit.grads[0].cpu().numpy().astype(np.float64), g).values()) <= GRAD_TOL
-        for _ in range(3):
-            fit.step()
-        torch.cuda.synchronize()
-        assert fit.check() == gi.GI_OK
-        res.append((fit.params.clone(), fit.loss.clone(), fit.n_keys()))
-    assert torch.equal(res[0][0], res[1][0]) and torch.equal(res[0][1], res[1][1])
-    assert res[0][2] == res[1][2]
+    torch.cuda.synchronize()
+    assert fit.check() == gi.GI_OK
+    res.append((fit.params.clone(), fit.loss.clone(), fit.n_keys()))
+assert torch.equal(res[0][0], res[1][0]) and torch.equal(res[0][1], res[1][1])
+assert res[0][2] == res[1][2]
+print("ok")
+"""
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, GI_SLAB_MIN="0", PYTHONPATH=root)
+    out = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True,
+                         text=True, timeout=600)
+    assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-2000:]
 
 
 def test_partial_slot_overflow(gi, gio):
