@@ -105,6 +105,29 @@ def fitted_params(seed: int, n: int) -> np.ndarray:
     return np.ascontiguousarray(p.astype(np.float32))
 
 
+def clustered_params(seed: int, n: int, width: int, height: int, clusters: int = 8,
+                     frac: float = 0.5, radius_px: float = 6.0) -> np.ndarray:
+    """A clustered cloud (dense features, as fitted images concentrate
+    Gaussians on edges and detail): the paper's init, except that a fraction
+    `frac` of the Gaussians is moved into `clusters` discs of `radius_px`
+    pixels.  Positions are drawn in normalised image coordinates and stored
+    as logits, u = tanh(mu_raw) (App. C, P:758-761)."""
+    rng = _rng(50_000 + seed)
+    p = init_params(seed, n).astype(np.float64)
+    m = int(round(frac * n))
+    cx = rng.uniform(0.1, 0.9, size=clusters) * width
+    cy = rng.uniform(0.1, 0.9, size=clusters) * height
+    k = rng.integers(0, clusters, size=m)
+    r = radius_px * np.sqrt(rng.uniform(0.0, 1.0, size=m))
+    a = rng.uniform(0.0, 2.0 * np.pi, size=m)
+    x = np.clip(cx[k] + r * np.cos(a), 0.0, width)
+    y = np.clip(cy[k] + r * np.sin(a), 0.0, height)
+    u = np.stack([2.0 * x / width - 1.0, 2.0 * y / height - 1.0], 1)
+    u = np.clip(u, -1.0 + 2.0**-24, 1.0 - 2.0**-24)
+    p[:m, 0:2] = np.arctanh(u)
+    return np.ascontiguousarray(p.astype(np.float32))
+
+
 def target_images(seed: int, batch: int, width: int, height: int) -> np.ndarray:
     return np.stack([image(seed + b, width, height) for b in range(int(batch))], 0)
 

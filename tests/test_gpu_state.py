@@ -361,3 +361,43 @@ def test_adam_step_nonzero_state_vs_oracle(gi, gio, step):
     for name, got, ref in (("p", pt, po), ("m", mt, mo), ("v", vt, vo)):
         got = got.cpu().numpy().astype(np.float64)
         assert np.all(np.abs(got - ref) <= 1e-6 * scale[name] + 1e-12), name
+
+
+# ---------------------------------------------------------------- clustered cloud
+def test_clustered_cloud(gi, gio):
+    # half of 30k Gaussians in 4 discs of 6 px: tiles of up to ~4,100 keys,
+    # past the 1,024-key slab (streamed) and every sort buffer -- parity and
+    # bitwise chained == plain hold on the slow paths too
+    from paper_2403_08551_b200.pipeline import Fitter, Pipeline
+    W, H, n = 256, 192, 30000
+    p = synth.clustered_params(3, n, W, H, clusters=4, frac=0.5, radius_px=6.0)
+    tgt = synth.image(3, W, H)
+    ref_img, ref_loss, ref_g = gio.loss_and_grads(p, tgt, mode=gio.TILED)
+    kt, kg, rng = gio.bin(p, W, H)
+    assert np.diff(rng.astype(np.int64)).max() > 1024
+    pipe = Pipeline(n, W, H, 1, device=DEV)
+    pipe.render(to_dev(p)[None].contiguous())
+    torch.cuda.synchronize()
+    K = len(kt)
+    assert pipe.keys() == K
+    assert np.array_equal(pipe.key_gid[:K].cpu().numpy().view(np.uint32), kg)
+    scale = np.maximum(1.0, np.abs(ref_img))           # R26: sums far above 1
+    assert np.all(np.abs(pipe.image[0].cpu().numpy() - ref_img) <= PIX_TOL * scale)
+    img = Pipeline(n, W, H, 1, device=DEV).render_frame(to_dev(p)[None].contiguous())
+    assert np.all(np.abs(img[0].cpu().numpy() - ref_img) <= PIX_TOL * scale)
+    outs = []
+    for chained in (True, False):
+        fit = Fitter(to_dev(p)[None].contiguous(), to_dev(tgt)[None].contiguous(), chained=chained)
+        fit.step()
+        torch.cuda.synchronize()
+        assert fit.check() == gi.GI_OK
+        streamed, _ = fit.seg_stats()
+        assert streamed > 0
+        errs = group_err(fit.grads[0].cpu().numpy().astype(np.float64), ref_g)
+        assert max(errs.values()) <= GRAD_TOL, errs
+        assert abs(float(fit.loss[0]) - ref_loss) <= 1e-5 * ref_loss
+        for _ in range(2):
+            fit.step()
+        torch.cuda.synchronize()
+        outs.append((fit.params.clone(), fit.loss.clone()))
+    assert torch.equal(outs[0][0], outs[1][0]) and torch.equal(outs[0][1], outs[1][1])

@@ -21,7 +21,7 @@ if [ "${AB_PDL:-0}" = "1" ]; then
   echo "bench (no PDL) rc=$?"
   python -c "import json;d=json.load(open('$OUT/${TAG}_bench_nopdl.json'));print('NO-PDL fit',d['value'],'render',d['render_fps'],'decode',d['decode_fps'],d['stage_ms'])"
 fi
-PCMD="python bench.py --steps 5 --warmup 3 --no-cpu-baseline"
+PCMD="python bench.py --steps 5 --warmup 3 --no-cpu-baseline --quick --batch-images 0"
 timeout 300 $PCMD > $OUT/${TAG}_prof_plain.json 2> $OUT/${TAG}_prof_plain.err
 rc=$?
 echo "prof plain rc=$rc"
