@@ -82,12 +82,12 @@ __global__ void __launch_bounds__(256, GI_TILE_MINB) backward_tile_kernel(
     const TileCtx t = make_tile_ctx(W, H, TX, cs.row1 > 0 ? cs.row0 : 0);
     const size_t P = (size_t)W * H;
     const size_t pix = (size_t)t.img * 3 * P + (size_t)t.y * W + t.x;
+    const int lpix = (t.y - t.ty * kTile) * kTile + (t.x - t.tx * kTile);
     griddep_wait();
     griddep_trigger();
     const Seg sg = open_segment(proj, key_gid, tile_range, presorted, cs, n, T, t, sh.sl,
                                 sh.scratch, &sh.cursor);
     const uint32_t L = sg.L;
-    const int lpix = (t.y - t.ty * kTile) * kTile + (t.x - t.tx * kTile);
     bool staged_all = false;
 
     float g0 = 0.f, g1 = 0.f, g2 = 0.f;
@@ -384,12 +384,12 @@ __global__ void __launch_bounds__(128, GI_TILE2_MINB) backward_tile2_kernel(
     const size_t P = (size_t)W * H;
     const size_t pix = (size_t)t.img * 3 * P + (size_t)y * W + x;
     const size_t pix1 = pix + 4 * (size_t)W;
+    const int lpix = ly * kTile + lx;
     griddep_wait();
     griddep_trigger();
     const Seg sg = open_segment<128, kSortMax2>(proj, key_gid, tile_range, presorted, cs, n, T, t,
                                                 sh.sl, sh.scratch, &sh.cursor);
     const uint32_t L = sg.L;
-    const int lpix = ly * kTile + lx;
     bool staged_all = false;
 
     float g0 = 0.f, g1 = 0.f, g2 = 0.f, h0 = 0.f, h1 = 0.f, h2 = 0.f;   // pixel 0, pixel 1
@@ -1079,6 +1079,11 @@ cudaError_t launch_backward_tiles(const Proj* proj, uint32_t* key_gid, const uin
     const float norm = (float)(2.0 / count);
     const bool mse = dL_dimage == nullptr;
     if (rows <= 0) return cudaSuccess;
+    if (use_tile3())      // Gaussian-parallel passes (fused.cu), the default
+        return launch_fused_backward(proj, key_gid, tile_range, (const uint32_t*)w.gauss_off, n, f,
+                                     presorted, dL_dimage, target, norm, partial_cap(n, cap, f),
+                                     w.partial, w.ovf, mse ? w.sse_acc : nullptr,
+                                     mse ? image_out : nullptr, cs, s);
     cudaError_t e = use_tile2(T * f.batch)
         ? launch_pdl(backward_tile2_kernel, dim3(TX, rows, f.batch), dim3(128), s, proj, key_gid,
                      tile_range, (const uint32_t*)w.gauss_off, n, f.width, f.height, T, TX,

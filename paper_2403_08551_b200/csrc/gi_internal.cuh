@@ -332,9 +332,27 @@ struct ChainState {
     float b3, wd;
 };
 
+// Optimiser arithmetic: the square root and the reciprocal of the update's
+// denominator by MUFU (sqrt.approx, rcp.approx: within ~1 ulp each) instead
+// of the IEEE sequences -- the update term then carries <= ~4e-7 relative
+// error, inside c.4's 1e-6 bar on p (test_adam_step_nonzero_state_vs_oracle);
+// m and v are exact fp32 FMAs as before.  One definition for every kernel
+// (gi_adam_step, the fused finalize, the peer step, QAT; Adan likewise), so
+// fused and standalone steps agree bit for bit.
+__device__ __forceinline__ float sqrt_mufu(float x) {
+    float r;
+    asm("sqrt.approx.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+__device__ __forceinline__ float rcp_mufu(float x) {
+    float r;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+
 // One Adam update of a scalar (a5, reading R16): the arithmetic of
-// gi_adam_step, shared with the peer-exchange step (NEXT-4) so the two agree
-// bit for bit.
+// gi_adam_step, shared with the fused finalize, the peer-exchange step
+// (NEXT-4) and QAT so they all agree bit for bit.
 __device__ __forceinline__ float adam_update(float& p, float g, float& m, float& v, float b1,
                                              float b2, float omb1, float omb2, float lr, float ibc1,
                                              float ibc2, float eps) {
@@ -342,7 +360,7 @@ __device__ __forceinline__ float adam_update(float& p, float g, float& m, float&
     v = fmaf(b2, v, omb2 * (g * g));
     const float mhat = m * ibc1;
     const float vhat = v * ibc2;
-    p = p - lr * mhat / (sqrtf(vhat) + eps);
+    p = p - (lr * mhat) * rcp_mufu(sqrt_mufu(vhat) + eps);
     return p;
 }
 
@@ -365,7 +383,7 @@ __device__ __forceinline__ float adan1(float p, float g, float& m, float& v, flo
     const float u = fmaf(c.b2, d, g);
     n = fmaf(c.b3, n, (1.0f - c.b3) * (u * u));
     gp = g;
-    const float upd = fmaf(c.b2 * c.ibc2, v, m * c.ibc1) / fmaf(sqrtf(n), c.isbc3, c.eps);
+    const float upd = fmaf(c.b2 * c.ibc2, v, m * c.ibc1) * rcp_mufu(fmaf(sqrt_mufu(n), c.isbc3, c.eps));
     return fmaf(-c.lr, upd, p * c.decay);
 }
 cudaError_t launch_project(const float* params, int n, const gi_frame& f, uint32_t flags,
@@ -385,6 +403,17 @@ BinCounts bin_counts(void* ws, int n, int64_t cap, const gi_frame& f);
 // slab_min() = 1024, or GI_SLAB_MIN from the environment (tests force small
 // slabs to exercise the streaming path; results never depend on it).
 uint32_t slab_min();
+// fused.cu: Gaussian-parallel tile kernels (default; GI_TILE3=0 -> round-1 kernels)
+bool use_tile3();
+cudaError_t launch_fused_backward(const Proj* proj, uint32_t* key_gid, const uint32_t* tile_range,
+                                  const uint32_t* gauss_off, int n, const gi_frame& f,
+                                  bool presorted, const float* dL_dimage, const float* target,
+                                  float norm, int64_t pcap, float* partial, float* ovf,
+                                  unsigned long long* sse_acc, float* image_out,
+                                  const ChainState& cs, cudaStream_t s);
+cudaError_t launch_fused_render(const Proj* proj, uint32_t* key_gid, const uint32_t* tile_range,
+                                int n, const gi_frame& f, bool presorted, float* image,
+                                const ChainState& cs, cudaStream_t s);
 uint32_t slab_capacity(int64_t cap, const gi_frame& f);
 size_t slab_words(int64_t cap, const gi_frame& f);
 uint32_t* bin_seg_stats(void* ws, int n, int64_t cap, const gi_frame& f);

@@ -9,8 +9,10 @@
 // (an fp32 centre near x = 768 has an ulp of 6e-5 px, which alone breaks the
 // 2e-5 pixel bar).  The box is decided by the fp32 recipe of reading R7 with
 // explicitly rounded intrinsics (no FMA contraction), so that its
-// float -> int decisions are reproducible.  The conic is formed in fp64 and
-// rounded once.
+// float -> int decisions are reproducible.  The Cholesky conic is formed by
+// IEEE fp32 divisions (a = kappa / l1e, c = kappa / l3e, b = -(a l2) / l3e:
+// < 1e-6 relative on sigma near the box edge); the RS conic from the fp64
+// Cholesky factor of Sigma, rounded once.
 #include "codec_core.cuh"
 #include "project_core.cuh"
 

@@ -1,15 +1,26 @@
 // Projection of one Gaussian (a1), shared by project_kernel and the fused
 // finalize + Adam + next-step projection of the chained fit step.
 // See project.cu for the precision plan (fp64 split centre, fp32 box recipe
-// of reading R7, conic rounded once from fp64).
+// of reading R7; Cholesky conic by IEEE fp32 divisions, RS conic from fp64).
 #pragma once
 #include "gi_internal.cuh"
 
 namespace gi {
 
+// tanh in fp64 as sign(x) (1 - e) / (1 + e), e = exp(-2|x|): absolute error
+// <= 1 ulp of 1 (checked against libm over |x| <= 20 and near 0), which is
+// what mu = (u + 1) W / 2 needs (mu off by < 3e-13 px at W = 2040).  One exp
+// and one division: ~4x fewer instructions than the library tanh, whose
+// branchy polynomial paths are the longest part of the projection (and of the
+// chained finalize, which projects the next step).
+__device__ __forceinline__ double tanh_pos(double x) {
+    const double e = exp(-2.0 * fabs(x));
+    return copysign((1.0 - e) / (1.0 + e), x);
+}
+
 // App. C: u = tanh(mu_raw) (fp64), or the stored u (normalised positions).
 __device__ __forceinline__ double activate_pos(float raw, uint32_t flags) {
-    return pos_logit(flags) ? tanh((double)raw) : (double)raw;
+    return pos_logit(flags) ? tanh_pos((double)raw) : (double)raw;
 }
 
 // The 48-byte record, pixel box and tile rectangle of one Gaussian from its

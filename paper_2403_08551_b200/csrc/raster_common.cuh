@@ -87,12 +87,14 @@ __device__ __forceinline__ TileCtx make_tile_ctx(int W, int H, int TX, int row0)
 // bar.  With the exact remainder mx_lo folded into (u0, v0), (u, v) carry an
 // error of ulp(dx) instead, at no extra instruction per pair (u, v become
 // FMAs with the correction as addend).
-struct StagedRecords {
-    float4 a[kBatch];
-    float4 b[kBatch];
-    float2 o[kBatch];
-    uint4 c[kBatch];
+template <int NB>
+struct StagedRecordsN {
+    float4 a[NB];
+    float4 b[NB];
+    float2 o[NB];
+    uint4 c[NB];
 };
+using StagedRecords = StagedRecordsN<kBatch>;
 
 // Per-warp compacted candidate list for one batch: (record index, lane mask).
 struct WarpLists {
@@ -108,7 +110,8 @@ __device__ __forceinline__ uint32_t span_mask16(int lo, int hi) {
 // gauss_off (backward), also the Gaussian's partial slot for this tile: its
 // contiguous range (4 gid, or gauss_off[gid] above 4 tiles) + the rank of this tile in its tile
 // rectangle (row-major), the order finalize sums in.
-__device__ __forceinline__ void stage_gid(StagedRecords& sr, const Proj* __restrict__ proj,
+template <class SR>
+__device__ __forceinline__ void stage_gid(SR& sr, const Proj* __restrict__ proj,
                                           uint32_t gid, int j, const TileCtx& t,
                                           const uint32_t* __restrict__ gauss_off = nullptr) {
     const Proj r = proj[gid];
@@ -340,7 +343,9 @@ __device__ __forceinline__ Seg open_segment(const Proj* __restrict__ proj,
                                             uint32_t* cursor) {
     const int tt = t.img * T + t.tile;
     if (cs.slab != nullptr) {
-        const uint32_t count = *(volatile const uint32_t*)&cs.tile_count[(size_t)tt * kCountStride];
+        // written by the producer kernel (visible after griddepcontrol.wait);
+        // re-zeroed by thread 0 only after the CTA's last barrier
+        const uint32_t count = __ldcg(&cs.tile_count[(size_t)tt * kCountStride]);
         const uint32_t s = (uint32_t)tt * cs.slab_cap;
         if (count > cs.slab_cap) {
             if (threadIdx.x == 0) {
@@ -434,12 +439,12 @@ __device__ __forceinline__ int stream_keys(const Proj* __restrict__ proj, int n,
 // The gids of batch [base, base + 256) of the segment: thread i < returned
 // count gets key base + i.  All threads must call (kSegStream gathers the
 // batch block-wide into sl).
-template <int NT = 256>
+template <int NT = 256, int NB = kBatch>
 __device__ __forceinline__ int batch_gid(const Seg& sg, uint32_t base, const uint32_t* key_gid,
                                          uint32_t* sl, const Proj* __restrict__ proj, int n,
                                          const TileCtx& t, uint32_t* cursor, uint32_t* scratch8,
                                          uint32_t& gid) {
-    int cnt = (int)min((uint32_t)kBatch, sg.L - base);
+    int cnt = (int)min((uint32_t)NB, sg.L - base);
     if (sg.mode == kSegStream) {
         cnt = stream_keys<NT>(proj, n, t.img, t.tx, t.ty, cnt, cursor, sl, scratch8);
         gid = (int)threadIdx.x < cnt ? sl[threadIdx.x] : 0u;

@@ -130,9 +130,10 @@ def load(build_if_stale: bool = False):
     if _lib is None:
         if build_if_stale:
             _build.build()
-        if not os.path.exists(_build.LIB):
-            raise RuntimeError(f"libgi.so not built at {_build.LIB}: run __graft_entry__.build()")
-        L = C.CDLL(_build.LIB)
+        path = os.environ.get("GI_LIB", _build.LIB)   # GI_LIB: an A/B variant build
+        if not os.path.exists(path):
+            raise RuntimeError(f"libgi.so not built at {path}: run __graft_entry__.build()")
+        L = C.CDLL(path)
         for name, (res, args) in SIGNATURES.items():
             fn = getattr(L, name)
             fn.restype = res

@@ -509,24 +509,39 @@ def test_determinism_and_counter_reuse(gi):
 
 def test_adan_parity(gi, gio):
     # NEXT-1: elementwise Adan vs the fp64 oracle over three steps (the
-    # gradient-difference term is live from step 2)
+    # gradient-difference term is live from step 2).  Every step starts both
+    # sides from the same state -- the oracle's, rounded to fp32 as it is
+    # stored, copied to the GPU (c.4 "one step from shared inputs"; no GPU
+    # value is fed to the oracle).  Bar (c.4, R34): 1e-6 relative to the terms
+    # each result sums.
     rng = np.random.default_rng(13)
     n = 8 * 1000
     p = rng.normal(size=n).astype(np.float32)
-    st = {k: np.zeros(n, np.float32) for k in ("m", "v", "n", "gp")}
-    dev = {k: to_dev(v) for k, v in st.items()}
+    z = np.zeros(n, np.float32)
+    dev = {k: to_dev(z) for k in ("m", "v", "n", "gp")}
     pt = to_dev(p)
+    o = dict(p=p.copy(), m=z.copy(), v=z.copy(), n=z.copy(), gp=z.copy())
+    b1, b2, b3 = (float(np.float32(x)) for x in (0.98, 0.92, 0.99))
     for step in (1, 2, 3):
         g = (rng.normal(size=n) * 10.0 ** rng.uniform(-4, 1, size=n)).astype(np.float32)
-        pref = pt.cpu().numpy()
-        ref = gio.adan(pref, g, dev["m"].cpu().numpy(), dev["v"].cpu().numpy(),
-                       dev["n"].cpu().numpy(), dev["gp"].cpu().numpy(), step, 1e-3)
+        po, mo, vo, no = gio.adan(o["p"], g, o["m"], o["v"], o["n"], o["gp"], step, 1e-3)
+        pt.copy_(to_dev(o["p"]))
+        for k in ("m", "v", "n", "gp"):
+            dev[k].copy_(to_dev(o[k]))
         gi.gi_adan_step(pt, to_dev(g), dev["m"], dev["v"], dev["n"], dev["gp"], n, step, 1e-3)
-        got = pt.cpu().numpy()
-        upd = np.abs(ref[0] - pref.astype(np.float64))
-        # fp32 rounding of p and of the update (a few ulp of each)
-        assert np.all(np.abs(got - ref[0]) <= 2e-6 * (np.abs(ref[0]) + upd) + 1e-12)
+        gd = g.astype(np.float64)
+        d = gd - o["gp"] if step > 1 else np.zeros(n)
+        sc = {"p": np.abs(o["p"]) + np.abs(po - o["p"]),
+              "m": np.abs(b1 * o["m"]) + np.abs((1 - b1) * gd),
+              "v": np.abs(b2 * o["v"]) + np.abs((1 - b2) * d),
+              "n": np.abs(b3 * o["n"]) + (1 - b3) * (gd + b2 * d) ** 2}
+        for name, got, ref in (("p", pt, po), ("m", dev["m"], mo), ("v", dev["v"], vo),
+                               ("n", dev["n"], no)):
+            got = got.cpu().numpy().astype(np.float64)
+            assert np.all(np.abs(got - ref) <= 1e-6 * sc[name] + 1e-12), (step, name)
         assert np.array_equal(dev["gp"].cpu().numpy(), g)
+        o = dict(p=po.astype(np.float32), m=mo.astype(np.float32), v=vo.astype(np.float32),
+                 n=no.astype(np.float32), gp=g.copy())
 
 
 def test_fit_step_adan(gi, gio):
