@@ -365,14 +365,30 @@ bool use_tile3() {
     }();
     return v;
 }
+// CTA size by launch size: 256 threads for one C2 image (1,536 tiles: the
+// per-lane chunks stay short), 128 from 3,072 tiles up, where sparse tiles
+// make the per-warp fixed work dominate (C3 init fit: 9.6k it/s at 256,
+// 13.2k at 128; round-1 two-pixel kernel 12.2k).  GI_TILE3_NT forces either.
+constexpr int kTile3SmallCta = 3072;
 static int tile3_nt(int tiles) {
     static const int force = [] {
         const char* e = std::getenv("GI_TILE3_NT");
         return e == nullptr ? 0 : std::atoi(e);
     }();
     if (force == 128 || force == 256) return force;
-    (void)tiles;
-    return 256;
+    return tiles >= kTile3SmallCta ? 128 : 256;
+}
+
+// The render: the Gaussian-parallel kernel below 3,072 tiles (C2 frame 37.9k
+// -> 41.3k FPS); from 3,072 tiles up the round-1 two-pixel kernel stays
+// faster (C3 frame: 24.4k FPS vs 23.3k at 128 threads, 16.3k at 256).
+bool use_render3(int tiles) {
+    static const int force = [] {
+        const char* e = std::getenv("GI_RENDER3");
+        return e == nullptr ? -1 : (e[0] == '1' ? 1 : 0);
+    }();
+    if (!use_tile3()) return false;
+    return force >= 0 ? force == 1 : tiles < kTile3SmallCta;
 }
 
 cudaError_t launch_fused_backward(const Proj* proj, uint32_t* key_gid, const uint32_t* tile_range,
