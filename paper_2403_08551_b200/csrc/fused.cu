@@ -204,7 +204,6 @@ __global__ void __launch_bounds__(NT, NT == 256 ? (kBwd ? GI_TILE3_MINB : GI_REN
     const Seg sg = open_segment3<NT, NB>(proj, key_gid, tile_range, presorted, cs, n, T, t, sh.sl,
                                      sh.scratch, &sh.cursor);
     const uint32_t L = sg.L;
-    const bool single = L <= (uint32_t)NB && sg.mode != kSegStream;
     const bool fwd = !kBwd || dL_dimage == nullptr;
     const uint32_t* goff = kBwd ? gauss_off : nullptr;
 
@@ -295,13 +294,19 @@ __global__ void __launch_bounds__(NT, NT == 256 ? (kBwd ? GI_TILE3_MINB : GI_REN
         }
 
         // ---- backward: the same chunks accumulate the 8 sums of backward.cu's pass 2 ----
-        const bool reuse = fwd && single;     // staging and plan of the forward still in smem
+        // The forward's LAST batch is still staged and planned in shared
+        // memory: pass 2 takes it first (no re-staging), then the others
+        // (a record's partial does not depend on the batch order).  Streamed
+        // segments (past the slab) are re-streamed in order.
+        const uint32_t nbat = (L + NB - 1) / NB;
+        const bool reuse = fwd && sg.mode != kSegStream && nbat > 0;
         if (threadIdx.x == 0) sh.cursor = 0u; // kSegStream: pass 2 streams from the start
-        for (uint32_t base = 0; base < L; base += NB) {
+        for (uint32_t ib = 0; ib < nbat; ++ib) {
+            const uint32_t base = reuse ? (ib == 0 ? (nbat - 1) * NB : (ib - 1) * NB) : ib * NB;
             __syncthreads();
             int cnt = cnt1;
             ChunkPlanOut pl = plan;
-            if (!reuse)
+            if (!(reuse && ib == 0))
                 pl = stage_and_plan<NT, NB, kBwd>(sh, sg, base, key_gid, proj, n, t, gauss_off, cnt);
             if (j < (int)pl.n_items) {
                 float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f, a4 = 0.f, a5 = 0.f, a6 = 0.f, a7 = 0.f;
