@@ -725,7 +725,8 @@ def main():
             "render_kernel_ms": r_kernel_ms,
             "decode_fps": decode_fps,
             "fit_its_adan": adan_value,
-            "roofline": {"kernel": "backward_tile_kernel (fused Eq.7 fwd + L2 + App.A bwd), C2",
+            "roofline": {"kernel": "fused_tile_kernel<256,128,true> (fused.cu: Eq.7 fwd + L2 + "
+                                   "App.A bwd, Gaussian-parallel), C2",
                          "bound": "alu", "achieved": lane / 1e12, "peak": lane_peak / 1e12,
                          "unit": "T FP32 lane-op/s", "frac": lane / lane_peak,
                          "traffic": traffic,

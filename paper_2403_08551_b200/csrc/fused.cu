@@ -385,15 +385,19 @@ static int tile3_nt(int tiles) {
 }
 
 // The render: the Gaussian-parallel kernel below 3,072 tiles (C2 frame 37.9k
-// -> 41.3k FPS); from 3,072 tiles up the round-1 two-pixel kernel stays
-// faster (C3 frame: 24.4k FPS vs 23.3k at 128 threads, 16.3k at 256).
-bool use_render3(int tiles) {
+// -> 44.1k FPS) when the cloud has >= 8 Gaussians per tile; from 3,072 tiles
+// up, and for sparse clouds (codec frames of 2.2k-4.5k records over 1,536
+// tiles), the round-1 two-pixel kernel's smaller per-tile work wins (C3 frame:
+// 24.4k FPS vs 23.3k at 128 threads, 16.3k at 256; 2.2k records 40.8k vs
+// 37.6k).
+bool use_render3(int tiles_per_launch, int n_per_image, int tiles_per_image) {
     static const int force = [] {
         const char* e = std::getenv("GI_RENDER3");
         return e == nullptr ? -1 : (e[0] == '1' ? 1 : 0);
     }();
     if (!use_tile3()) return false;
-    return force >= 0 ? force == 1 : tiles < kTile3SmallCta;
+    if (force >= 0) return force == 1;
+    return tiles_per_launch < kTile3SmallCta && n_per_image >= 8 * tiles_per_image;
 }
 
 cudaError_t launch_fused_backward(const Proj* proj, uint32_t* key_gid, const uint32_t* tile_range,

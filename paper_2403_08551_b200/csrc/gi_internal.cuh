@@ -405,7 +405,7 @@ BinCounts bin_counts(void* ws, int n, int64_t cap, const gi_frame& f);
 uint32_t slab_min();
 // fused.cu: Gaussian-parallel tile kernels (default; GI_TILE3=0 -> round-1 kernels)
 bool use_tile3();
-bool use_render3(int tiles);
+bool use_render3(int tiles_per_launch, int n_per_image, int tiles_per_image);
 cudaError_t launch_fused_backward(const Proj* proj, uint32_t* key_gid, const uint32_t* tile_range,
                                   const uint32_t* gauss_off, int n, const gi_frame& f,
                                   bool presorted, const float* dL_dimage, const float* target,
