@@ -118,7 +118,8 @@ __device__ __forceinline__ ChunkPlanOut plan_chunks_few(ChunkShared<NT>& ch, int
     ChunkPlanOut out;
     out.n_items = F;
     out.scale = ldexpf(1.0f, s);
-    out.inv_scale = ldexpf(1.0f, -s);
+    // a non-finite colour poisons the batch's pixels (as an fp32 sum would)
+    out.inv_scale = cmx >= 0x7f800000u ? __int_as_float(0x7fffffff) : ldexpf(1.0f, -s);
     return out;
 }
 
@@ -214,7 +215,8 @@ __device__ __forceinline__ ChunkPlanOut plan_chunks_many(ChunkShared<NT>& ch, in
     ChunkPlanOut out;
     out.n_items = ch.n_items;
     out.scale = ldexpf(1.0f, s);
-    out.inv_scale = ldexpf(1.0f, -s);
+    // a non-finite colour poisons the batch's pixels (as an fp32 sum would)
+    out.inv_scale = cmx >= 0x7f800000u ? __int_as_float(0x7fffffff) : ldexpf(1.0f, -s);
     return out;
 }
 

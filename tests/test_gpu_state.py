@@ -401,3 +401,20 @@ def test_clustered_cloud(gi, gio):
         torch.cuda.synchronize()
         outs.append((fit.params.clone(), fit.loss.clone()))
     assert torch.equal(outs[0][0], outs[1][0]) and torch.equal(outs[0][1], outs[1][1])
+
+
+def test_nonfinite_colour_propagates(gi):
+    # a NaN colour must not vanish in the fixed-point forward: the pixels of
+    # that Gaussian's tiles come out NaN (as an fp32 sum would), and a fit
+    # step raises the non-finite status
+    from paper_2403_08551_b200.pipeline import Fitter, Pipeline
+    W, H, n = 64, 64, 256
+    p = synth.init_params(4, n)
+    p[7, 5] = np.nan
+    img = Pipeline(n, W, H, 1, device=DEV).render_frame(to_dev(p)[None].contiguous())
+    torch.cuda.synchronize()
+    assert torch.isnan(img).any()
+    fit = Fitter(to_dev(p)[None].contiguous(), to_dev(synth.image(4, W, H))[None].contiguous())
+    fit.step()
+    torch.cuda.synchronize()
+    assert fit.check() == gi.GI_ENONFINITE
