@@ -418,3 +418,43 @@ def test_nonfinite_colour_propagates(gi):
     fit.step()
     torch.cuda.synchronize()
     assert fit.check() == gi.GI_ENONFINITE
+
+
+@pytest.mark.parametrize("optimizer", ["adam", "adan"])
+def test_fit_trajectory_band(gi, gio, optimizer):
+    # SURVEY c.3: long fitting trajectories are chaotic in fp32 vs fp64, so
+    # they are pinned by a band: C1 (64x64, 256 Gaussians, the paper's init),
+    # 2000 steps of the paper's loop on the GPU (chained fused steps) and in
+    # the oracle (fp64 steps, state rounded to fp32 between steps, as stored);
+    # final PSNR within 0.1 dB, and both fits far above the start
+    from paper_2403_08551_b200.pipeline import Fitter, Pipeline
+    W, H, n, steps = 64, 64, 256, 2000
+    p0 = synth.init_params(0, n)
+    tgt = synth.image(0, W, H)
+    fit = Fitter(to_dev(p0)[None].contiguous(), to_dev(tgt)[None].contiguous(), optimizer=optimizer)
+    fit.capture(100)
+    for _ in range(steps // 100):
+        fit.replay()
+    pipe = Pipeline(n, W, H, 1, device=DEV)
+    img = pipe.render_frame(fit.params)
+    gpu_psnr = float(pipe.psnr(img, to_dev(tgt)[None].contiguous())[0])
+    torch.cuda.synchronize()
+    assert fit.check() == gi.GI_OK and fit.steps_done() == steps
+    p = p0.copy()
+    z = np.zeros_like(p)
+    st = dict(m=z.copy(), v=z.copy(), n=z.copy(), gp=z.copy())
+    for t in range(1, steps + 1):
+        _, _, g = gio.loss_and_grads(p, tgt, mode=gio.ALL_PAIRS)
+        g = g.astype(np.float32)
+        if optimizer == "adam":
+            po, mo, vo = gio.adam(p, g, st["m"], st["v"], t, gio.lr_at(t))
+            st.update(m=mo.astype(np.float32), v=vo.astype(np.float32))
+        else:
+            po, mo, vo, no = gio.adan(p, g, st["m"], st["v"], st["n"], st["gp"], t, gio.lr_at(t))
+            st.update(m=mo.astype(np.float32), v=vo.astype(np.float32), n=no.astype(np.float32),
+                      gp=g)
+        p = po.astype(np.float32)
+    ref_psnr = gio.psnr(gio.render(p, W, H, mode=gio.ALL_PAIRS), tgt)
+    start = gio.psnr(gio.render(p0, W, H, mode=gio.ALL_PAIRS), tgt)
+    assert ref_psnr > start + 5.0 and gpu_psnr > start + 5.0, (start, ref_psnr, gpu_psnr)
+    assert abs(gpu_psnr - ref_psnr) <= 0.1, (gpu_psnr, ref_psnr)
