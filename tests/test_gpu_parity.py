@@ -687,8 +687,9 @@ def test_rs_fit_steps(gi, gio):
     assert torch.equal(res[0], res[1])
 
 
+@pytest.mark.parametrize("nt", ["256", "128"])
 @pytest.mark.parametrize("per_tile", [2, 40])
-def test_direct_binning_overflow(per_tile):
+def test_direct_binning_overflow(per_tile, nt):
     # slab capacity below the per-tile key count (GI_SLAB_MIN=0 lets the
     # capacity set the slab): overflowing tiles stream their keys in gid order
     # from all Gaussians, so frames, gradients and updates are bitwise those
@@ -735,7 +736,7 @@ assert res[0][2] == res[1][2]
 print("ok")
 """
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    env = dict(os.environ, GI_SLAB_MIN="0", PYTHONPATH=root)
+    env = dict(os.environ, GI_SLAB_MIN="0", GI_TILE3_NT=nt, PYTHONPATH=root)
     out = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True,
                          text=True, timeout=600)
     assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-2000:]
@@ -1066,8 +1067,8 @@ def test_new_entry_edge_cases(gi, gio):
 
 
 def test_render_one_pixel_variant():
-    # the one-pixel-per-thread render kernel (GI_RENDER2=0, the A/B baseline
-    # of the default two-pixel kernel) stays within the pixel bar: C2 init and
+    # the round-1 one-pixel-per-thread render kernel (GI_RENDER3=0
+    # GI_RENDER2=0, the A/B baseline) stays within the pixel bar: C2 init and
     # a ragged frame, fused frame vs the oracle, in a fresh process
     import os
     import subprocess
@@ -1085,17 +1086,27 @@ for W, H, n, seed in ((768, 512, 70000, 1), (70, 45, 300, 1)):
 print("ok")
 """
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    env = dict(os.environ, GI_RENDER2="0", PYTHONPATH=root)
+    env = dict(os.environ, GI_RENDER2="0", GI_RENDER3="0", PYTHONPATH=root)
     out = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True,
                          text=True, timeout=600)
     assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-2000:]
 
 
-@pytest.mark.parametrize("force", ["0", "1"])
-def test_tile_kernel_variants(force):
-    # both fused tile kernels (one pixel per thread, two per thread) in a
-    # fresh process with the choice forced: C2 init frame + fused fit-step
-    # gradients and a 3-image launch vs the oracle
+VARIANTS = {
+    "tile3_256": {"GI_TILE3_NT": "256", "GI_RENDER3": "1"},
+    "tile3_128": {"GI_TILE3_NT": "128", "GI_RENDER3": "1"},
+    "round1_onepixel": {"GI_TILE3": "0", "GI_TILE2": "0", "GI_RENDER2": "0"},
+    "round1_twopixel": {"GI_TILE3": "0", "GI_TILE2": "1"},
+}
+
+
+@pytest.mark.parametrize("variant", list(VARIANTS))
+def test_tile_kernel_variants(variant):
+    # every fused tile kernel (Gaussian-parallel at 256 / 128 threads, the
+    # round-1 one- and two-pixel kernels) and render kernel in a fresh
+    # process with the choice forced: C2 init frame + fused fit-step
+    # gradients, a 3-image launch and a tile past every sort buffer vs the
+    # oracle
     import os
     import subprocess
     import sys
@@ -1111,14 +1122,17 @@ cases = [(768, 512, [synth.init_params(1, 70000)], [synth.image(1, 768, 512)]),
          (96, 70, [synth.fitted_params(s, 900) for s in (3, 4, 5)],
           [synth.image(s, 96, 70) for s in (3, 4, 5)]),
          (32, 32, [big], [synth.image(6, 32, 32)])]
+from paper_2403_08551_b200.pipeline import Pipeline
 for W, H, ps, ts in cases:
-    fit = Fitter(torch.from_numpy(np.stack(ps)).cuda().contiguous(),
-                 torch.from_numpy(np.stack(ts)).cuda().contiguous())
+    pd = torch.from_numpy(np.stack(ps)).cuda().contiguous()
+    fit = Fitter(pd.clone(), torch.from_numpy(np.stack(ts)).cuda().contiguous())
     fit.step()
     g = fit.grads.cpu().numpy().astype(np.float64)
+    img = Pipeline(ps[0].shape[0], W, H, len(ps)).render_frame(pd).cpu().numpy()
     for b in range(len(ps)):
         mode = gio.TILED if W * H > 10000 else gio.ALL_PAIRS
-        _, loss, rg = gio.loss_and_grads(ps[b], ts[b], mode=mode)
+        ref_img, loss, rg = gio.loss_and_grads(ps[b], ts[b], mode=mode)
+        assert np.all(np.abs(img[b] - ref_img) <= 2e-5 * np.maximum(1.0, np.abs(ref_img)))
         assert abs(float(fit.loss[b]) - loss) <= 1e-5 * loss
         for cols in ([0, 1], [2, 3, 4], [5, 6, 7]):
             e = np.linalg.norm(g[b][:, cols] - rg[:, cols]) / np.linalg.norm(rg[:, cols])
@@ -1126,7 +1140,7 @@ for W, H, ps, ts in cases:
 print("ok")
 """
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    env = dict(os.environ, GI_TILE2=force, PYTHONPATH=root)
+    env = dict(os.environ, PYTHONPATH=root, **VARIANTS[variant])
     out = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True,
                          text=True, timeout=900)
     assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-2000:]
