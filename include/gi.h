@@ -114,9 +114,14 @@ gi_status gi_bin(const void* proj, const uint32_t* tiles_touched, int32_t n, con
                  uint32_t* key_gid, uint32_t* tile_range, uint32_t* n_keys, void* stream);
 
 /* --- a3. Forward accumulated summation (Eq. 7) -----------------------------
- * C_k(x, y) = sum over keys of tile(x, y), ascending gid, of
+ * C_k(x, y) = sum over keys of tile(x, y) of
  *             [x0 <= x <= x1 and y0 <= y <= y1] c'_k exp(-sigma(x + 1/2, y + 1/2))
- * Unclamped (R10).  image [B][3][H][W] fp32 out. */
+ * Unclamped (R10).  image [B][3][H][W] fp32 out.  The sum is order-free
+ * (P:214): per batch of a tile's keys each term is rounded to a 2^-s fixed
+ * point (s from the batch's largest |c'|, terms <= 2^22) and added exactly
+ * with integer atomics, then converted once (launches of < 3,072 tiles with
+ * >= 8 Gaussians per tile; else fp32 sums in ascending gid) -- deterministic
+ * either way.  A non-finite c' makes its tiles' pixels NaN. */
 gi_status gi_render(const void* proj, const uint32_t* key_gid, const uint32_t* tile_range,
                     int32_t n, const gi_frame* f, float* image, void* stream);
 
