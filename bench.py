@@ -11,8 +11,12 @@ fused forward (Eq. 7) + L2 loss + Appendix-A backward -> per-Gaussian
 finalize fused with Adam (paper schedule).  The JSON line's `value` is
 fit iterations/s over all ranks; `render_fps` (project + bin + render) and
 `decode_fps` (RVQ/fp16/b-bit decode + project + bin + render, configs[4] at
-70k records) are measured in the same run.  The L2 cache (126 MB) is flushed
-with a 256 MB write before every timed step (the C2 working set is ~60 MB).
+70k records) are measured in the same run.  Those four headline numbers
+(fit, render, decode, Adan fit) are timed with inputs larger than the 126 MB
+L2: 8 independent instances of the step (~35 MB touched each) are stepped in
+turn, 8 steps per graph replay, so every step starts L2-cold; the round-1
+protocol (one step per replay, L2 flushed with a 256 MB write before each)
+is kept beside them (`flush_per_replay`) and times the context numbers.
 
 Multi-GPU (torchrun): each rank fits its own image (weak scaling, no
 collective on the data path); per-image PSNR is all-gathered over NCCL at
@@ -41,6 +45,7 @@ W_IMG, H_IMG, N_GAUSS = 768, 512, 70000
 W_C3, H_C3, N_C3 = 2040, 1356, 100000          # configs[2], DIV2K-shaped (R24)
 PAPER_FIT_ITS = 50000 / 106.59        # Table 1a, V100, Adan: 469.1 it/s
 L2_FLUSH_BYTES = 256 << 20
+ROT = 8     # independent instances stepped in turn for the L2-cold headline timings (rot_ms)
 # Algorithmic work per (pixel, Gaussian) pair in the box, SURVEY.md §8(d.3):
 #   render (Eq. 5 + 7): 10 FP32 lane-ops + 1 MUFU.EX2
 #   backward (App. A):  26 FP32 lane-ops + 1 MUFU.EX2
@@ -282,6 +287,35 @@ def main():
         """Whole-job units/s: all ranks' units / the max-over-ranks time."""
         return world * steps * units_per_replay / (max_over_ranks(timed_ms(g, steps)) / 1000.0)
 
+    def rot_ms(step_fns, steps):
+        """Device ms of exactly `steps` steps, this rank, with inputs larger
+        than L2 instead of a flush: the R = len(step_fns) callables each step
+        one independent instance of the same seeded problem (own buffers, ~35
+        MB touched per C2 step), stepped in turn, so every step finds its
+        working set evicted by the other R - 1 instances' steps (R x 35 MB >
+        2 x 126 MB L2 for R = 8).  R steps per graph replay (the host's
+        graph-launch latency, ~6 us per replay on a B200, is paid once per R
+        steps as in a training loop); one event pair around the whole run,
+        barriers on both sides."""
+        R = len(step_fns)
+        full, rem = divmod(steps, R)
+        g_full = capture(lambda: [f() for f in step_fns])
+        g_rem = capture(lambda: [f() for f in step_fns[:rem]]) if rem else None
+        for _ in range(max(1, (Wm + R - 1) // R)):
+            g_full.replay()
+        barrier()
+        s_ev[0].record(stream)
+        for _ in range(full):
+            g_full.replay()
+        if g_rem is not None:
+            g_rem.replay()
+        e_ev[0].record(stream)
+        barrier()
+        return s_ev[0].elapsed_time(e_ev[0])
+
+    def rot_rate(step_fns, steps):
+        return world * steps / (max_over_ranks(rot_ms(step_fns, steps)) / 1000.0)
+
     def pairs_keys(pipe):
         rec = pipe.proj.view(-1, 12).cpu().numpy()
         bx, by = rec[:, 7].view(np.uint32), rec[:, 11].view(np.uint32)
@@ -348,11 +382,22 @@ def main():
     probe.project(fit.params)
     pairs, keys = pairs_keys(probe)
     del probe
+    # R independent instances of the C2 step for the L2-cold rotation (rot_ms)
+    rot_fits = [Fitter(params.clone(), target.clone()) for _ in range(ROT)]
+    for f in rot_fits:
+        f.step()
+    torch.cuda.synchronize(dev)
     clocks.start()
-    fit_ms = timed_ms(plain_g, K)
+    fit_ms = rot_ms([f.step for f in rot_fits], K)
     rank_ms = all_ranks(fit_ms)
     fit_ms_max = max(rank_ms)
     fit_value = world * K / (fit_ms_max / 1000.0)
+    for f in rot_fits:
+        if f.check() != gi.GI_OK:
+            raise RuntimeError("fit status after timing")
+    del rot_fits
+    # the round-1 protocol (one step per graph replay, L2 flushed before each)
+    fit_flush_value = rate(plain_g, K)
     stage_ms = stage_split(staged_g, stage_ev, min(K, 100))
     if fit.check() != gi.GI_OK:
         raise RuntimeError("fit status after timing")
@@ -363,7 +408,15 @@ def main():
     rparams = params.clone()
     pipe.render_frame(rparams)
     torch.cuda.synchronize(dev)
-    render_fps = rate(capture(lambda: pipe.render_frame(rparams)), K)
+    render_fps_flush = rate(capture(lambda: pipe.render_frame(rparams)), K)
+    rot_pipes = [(Pipeline(N_GAUSS, W_IMG, H_IMG, 1, device=dev), params.clone())
+                 for _ in range(ROT)]
+    for rp, rpar in rot_pipes:
+        rp.render_frame(rpar)
+    torch.cuda.synchronize(dev)
+    render_fps = rot_rate([(lambda rp=rp, rpar=rpar: rp.render_frame(rpar))
+                           for rp, rpar in rot_pipes], K)
+    del rot_pipes
     # render-kernel-only time (ABI gi_render on gi_bin output, events around it)
     pipe.project(rparams)
     pipe.bin()
@@ -387,7 +440,15 @@ def main():
     dpipe = Pipeline(N_GAUSS, W_IMG, H_IMG, 1, device=dev)
     dpipe.decode_render_frame(d_payload, meta, dparams)
     torch.cuda.synchronize(dev)
-    decode_fps = rate(capture(lambda: dpipe.decode_render_frame(d_payload, meta, dparams)), K)
+    decode_fps_flush = rate(capture(lambda: dpipe.decode_render_frame(d_payload, meta, dparams)), K)
+    rot_dec = [(Pipeline(N_GAUSS, W_IMG, H_IMG, 1, device=dev), d_payload.clone(), dparams.clone())
+               for _ in range(ROT)]
+    for dp, dpay, dpar in rot_dec:
+        dp.decode_render_frame(dpay, meta, dpar)
+    torch.cuda.synchronize(dev)
+    decode_fps = rot_rate([(lambda dp=dp, dpay=dpay, dpar=dpar: dp.decode_render_frame(dpay, meta, dpar))
+                           for dp, dpay, dpar in rot_dec], K)
+    del rot_dec
     decode_small = {}
     for n_small in (() if quick else (2200, 4500)):   # ~0.3 / 0.6 bpp at 56 bits
         sdata, sg, sb, sbooks = synth.payload(seed, n_small)
@@ -403,13 +464,15 @@ def main():
         del s_pipe
 
     # ---------------- Adan fit step (the paper's optimiser, NEXT-1) ----------------
-    afit = Fitter(params.clone(), target, optimizer="adan")
-    afit.step()
+    afits = [Fitter(params.clone(), target.clone(), optimizer="adan") for _ in range(ROT)]
+    for f in afits:
+        f.step()
     torch.cuda.synchronize(dev)
-    adan_value = rate(afit.capture(1), K)
-    if afit.check() != gi.GI_OK:
-        raise RuntimeError("adan fit status")
-    del afit
+    adan_value = rot_rate([f.step for f in afits], K)
+    for f in afits:
+        if f.check() != gi.GI_OK:
+            raise RuntimeError("adan fit status")
+    del afits
 
     # ---------------- configs[2]: C3, DIV2K-shaped 2040x1356, 100k Gaussians ----------------
     c3 = None
@@ -694,7 +757,14 @@ def main():
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {"workload": "C2 (configs[1]): 768x512 synthetic image, 70k Gaussians at "
                                    "the paper's init, one chained Adam fit step per rank",
-                       "images_per_gpu": 1, "l2": "flushed (256 MB write) before every timed step",
+                       "images_per_gpu": 1,
+                       "l2": f"inputs larger than L2: {ROT} independent instances of the step "
+                             f"(same seeded problem, own buffers, ~35 MB each) stepped in turn, "
+                             f"{ROT} steps per graph replay, so each step's working set was "
+                             f"evicted by the other {ROT - 1} (fit, render, decode, Adan); "
+                             f"the *_flush_per_replay keys: one step per replay, 256 MB L2 "
+                             f"flush before each (the round-1 protocol; includes ~6 us of "
+                             f"graph-launch latency per step)",
                        "key_pairs_per_step": keys, "pixel_gaussian_pairs": pairs,
                        "render_fps": render_fps,
                        "c3_fit_its": c3["fit_its"] if c3 else None,
@@ -705,6 +775,8 @@ def main():
             "fit_50k_steps": full_fit,
             "fitted_state": fitted_state,
             "fit_its_warm_graph100": warm_its,
+            "flush_per_replay": {"fit_its": fit_flush_value, "render_fps": render_fps_flush,
+                                 "decode_fps": decode_fps_flush},
             "encode_fps": encode_fps,
             "qat_its": qat_its,
             "decode_fps_codec_sizes": decode_small,
