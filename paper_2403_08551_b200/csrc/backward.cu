@@ -736,6 +736,32 @@ __global__ void __launch_bounds__(256) alloc_kernel(const Proj* __restrict__ pro
     if (g < total) gauss_off[g] = off;
 }
 
+// The partial sums of a > 4-tile Gaussian: slots o0 .. o0 + n - 1, four
+// loads in flight, summed in slot order (kept out of line: the common <= 4-
+// tile path of finalize_one is scheduled as if this loop did not exist).
+struct Sums8 {
+    float4 u, w;
+};
+__device__ __noinline__ Sums8 sum_slots(const float4* __restrict__ pp, uint32_t o0, uint32_t n) {
+    Sums8 s{make_float4(0.f, 0.f, 0.f, 0.f), make_float4(0.f, 0.f, 0.f, 0.f)};
+    for (uint32_t k = 0; k < n; k += 4) {
+        float4 u4[4], w4[4];
+#pragma unroll
+        for (uint32_t q = 0; q < 4; ++q)
+            if (k + q < n) {
+                u4[q] = __ldcg(pp + 2 * (size_t)(o0 + k + q));
+                w4[q] = __ldcg(pp + 2 * (size_t)(o0 + k + q) + 1);
+            }
+#pragma unroll
+        for (uint32_t q = 0; q < 4; ++q)
+            if (k + q < n) {
+                s.u.x += u4[q].x; s.u.y += u4[q].y; s.u.z += u4[q].z; s.u.w += u4[q].w;
+                s.w.x += w4[q].x; s.w.y += w4[q].y; s.w.z += w4[q].z; s.w.w += w4[q].w;
+            }
+    }
+    return s;
+}
+
 // Per Gaussian: sum its tiles' partials (row-major tile order), then the
 // closed-form chain rule.  With p = u / kappa, q = v / kappa (so
 // sigma = (p^2 + q^2) / 2, p = dx / l1, q = (dy - l2 p) / l3):
@@ -828,10 +854,12 @@ __device__ __forceinline__ void finalize_one(int g, bool live, const FinArgs& a,
                     o[0] = make_float4(0.f, 0.f, 0.f, 0.f);
                     o[1] = make_float4(0.f, 0.f, 0.f, 0.f);
                 } else {
-                    for (uint32_t k = 0; k < cnt; ++k) {
-                        if ((int64_t)(o0 + k) >= a.pcap) break;
-                        add(__ldcg(pp + 2 * (size_t)(o0 + k)), __ldcg(pp + 2 * (size_t)(o0 + k) + 1));
-                    }
+                    // below pcap: alloc_kernel and post_project_warp allocate
+                    // whole ranges or none (the clip keeps the old loop's break)
+                    const uint32_t n_ok = (int64_t)o0 + cnt <= a.pcap
+                        ? cnt : (uint32_t)max(a.pcap - (int64_t)o0, (int64_t)0);
+                    const Sums8 s8 = sum_slots(pp, o0, n_ok);
+                    add(s8.u, s8.w);
                 }
             }
             any = true;

@@ -275,18 +275,38 @@ __device__ __forceinline__ void post_project_warp(const BinCounts& bc, uint32_t 
         const uint64_t first = 4ull * (uint32_t)total + off;
         if (big) bc.gauss_off[g] = first + touched <= bc.part_cap ? (uint32_t)first : kOffOverflow;
     }
-    while (m) {
-        const int j = __ffs(m) - 1;
-        m &= m - 1;
+    // The warp's big Gaussians' keys as one flat list (exclusive scan of their
+    // counts): lane l emits keys l, l + 32, ... of the list, so the rank
+    // atomics of all of them are issued in ceil(total / 32) rounds instead of
+    // one round trip per big Gaussian.  Owner of flat key f = the last lane
+    // whose offset is <= f (binary search over the non-decreasing offsets;
+    // lanes with no keys share the next owner's offset and come before it).
+    const uint32_t c_l = big ? touched : 0u;
+    uint32_t incl = c_l;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(kFull, incl, o);
+        if (lane >= o) incl += y;
+    }
+    const uint32_t off_l = incl - c_l;
+    const uint32_t total_w = __shfl_sync(kFull, incl, 31);
+    for (uint32_t f0 = 0; f0 < total_w; f0 += 32) {
+        const uint32_t f = f0 + (uint32_t)lane;
+        int j = 0;
+#pragma unroll
+        for (int step = 16; step > 0; step >>= 1) {
+            const uint32_t oj = __shfl_sync(kFull, off_l, j + step);
+            if (oj <= f) j += step;
+        }
         const int tx0 = __shfl_sync(kFull, rect.x, j), tx1 = __shfl_sync(kFull, rect.y, j);
         const int ty0 = __shfl_sync(kFull, rect.z, j);
-        const uint32_t c = __shfl_sync(kFull, touched, j);
         const int b = __shfl_sync(kFull, base, j);
         const uint32_t gid = (uint32_t)__shfl_sync(kFull, g, j);
-        const int w = tx1 - tx0 + 1;
-        for (uint32_t i = lane; i < c; i += 32) {
-            const int dy = (int)i / w;
-            const int t = b + (ty0 + dy) * TX + tx0 + ((int)i - dy * w);
+        const uint32_t oj = __shfl_sync(kFull, off_l, j);
+        if (f < total_w) {
+            const int i = (int)(f - oj), w = tx1 - tx0 + 1;
+            const int dy = i / w;
+            const int t = b + (ty0 + dy) * TX + tx0 + (i - dy * w);
             const uint32_t r = atomicAdd(count_word(bc, t), 1u);
             if (r < bc.slab_cap) bc.slab[(size_t)t * bc.slab_cap + r] = gid;
         }

@@ -43,11 +43,11 @@ for r in range(reps):
         row = dict(fit=d["value"], render=d["render_fps"], decode=d["decode_fps"],
                    adan=d["fit_its_adan"], tile=1e3 * sm["tile_kernel_fwd_l2_bwd"],
                    fin=1e3 * sm["finalize_adam_next_projection_binning"],
-                   rk=1e3 * d["render_kernel_ms"], rep=d.get("fit_its_replay_events") or 0.0)
+                   rk=1e3 * d["render_kernel_ms"], rep=(d.get("flush_per_replay") or {}).get("fit_its") or 0.0)
         res[name].append(row)
         print(f"{name:14s} rep {r}: fit {row['fit']:7.0f}  render {row['render']:7.0f}  "
               f"decode {row['decode']:7.0f}  adan {row['adan']:7.0f}  tile {row['tile']:5.1f} us  "
-              f"fin {row['fin']:5.1f} us  rkern {row['rk']:5.1f} us  fit(replay ev) {row['rep']:7.0f}", flush=True)
+              f"fin {row['fin']:5.1f} us  rkern {row['rk']:5.1f} us  fit(flush) {row['rep']:7.0f}", flush=True)
 print("median:")
 for name, rows in res.items():
     if not rows:
@@ -55,4 +55,4 @@ for name, rows in res.items():
     med = {k: sorted(r[k] for r in rows)[len(rows) // 2] for k in rows[0]}
     print(f"{name:14s} fit {med['fit']:7.0f}  render {med['render']:7.0f}  decode {med['decode']:7.0f}"
           f"  adan {med['adan']:7.0f}  tile {med['tile']:5.1f}  fin {med['fin']:5.1f}  rk {med['rk']:5.1f}"
-          f"  fit(replay ev) {med['rep']:7.0f}")
+          f"  fit(flush) {med['rep']:7.0f}")
