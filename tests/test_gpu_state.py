@@ -206,6 +206,58 @@ def test_direct_binning_slabs_bitexact(gi, gio, cfg):
     _check_direct_binning(gi, gio, ps, W, H)
 
 
+def huge_params(seed, n, every=5):
+    """The paper's init with every `every`-th Gaussian blown up to sigma 6-40 px
+    (boxes of up to ~15 x 15 tiles: single Gaussians with more keys than a
+    warp has lanes, several of them per warp) and its colour scaled down."""
+    rng = np.random.default_rng(seed)
+    p = synth.init_params(seed, n)
+    idx = np.arange(0, n, every)
+    s = rng.uniform(6.0, 40.0, size=len(idx)).astype(np.float32)
+    p[idx, 2] = s - 0.5
+    p[idx, 3] = rng.uniform(-0.5, 0.5, size=len(idx)).astype(np.float32) * s
+    p[idx, 4] = rng.uniform(0.3, 1.0, size=len(idx)).astype(np.float32) * s - 0.5
+    p[idx, 5:8] *= 0.05
+    return p
+
+
+def test_huge_gaussians(gi, gio):
+    # > 32-key Gaussians: the flat key emission of post_project_warp (prime and
+    # the chained finalize) bit-exact against the oracle's binning, and the
+    # finalize's long slot ranges in the gradients, frame and chained step
+    from paper_2403_08551_b200.pipeline import Fitter, Pipeline
+    W, H, n = 256, 192, 2000
+    p = huge_params(11, n)
+    r = gio.project(p, W, H)
+    tt = np.asarray(r["touched"])
+    assert tt.max() > 64 and (tt > 32).sum() > 50
+    _check_direct_binning(gi, gio, p[None], W, H)
+    tgt = synth.image(11, W, H)
+    ref_img, ref_loss, ref_g = gio.loss_and_grads(p, tgt, mode=gio.TILED)
+    pipe = Pipeline(n, W, H, 1, device=DEV)
+    img = pipe.render_frame(to_dev(p)[None].contiguous())[0].cpu().numpy()
+    assert np.abs(img - ref_img).max() <= PIX_TOL
+    for chained in (True, False):
+        fit = Fitter(to_dev(p)[None].contiguous(), to_dev(tgt)[None].contiguous(), chained=chained)
+        fit.step()
+        torch.cuda.synchronize()
+        assert fit.check() == gi.GI_OK
+        errs = group_err(fit.grads[0].cpu().numpy().astype(np.float64), ref_g)
+        assert max(errs.values()) <= GRAD_TOL, errs
+        assert abs(float(fit.loss[0]) - ref_loss) <= 1e-5 * ref_loss
+    # the chained finalize's projection + binning of the updated cloud equals a prime of it
+    a = Fitter(to_dev(p)[None].contiguous(), to_dev(tgt)[None].contiguous())
+    for _ in range(3):
+        a.step()
+    b = Fitter(a.params.clone(), to_dev(tgt)[None].contiguous())
+    gi.gi_fit_prime(b.params, b.n, b.f, b.flags, b.cap, b.fit_ws)
+    torch.cuda.synchronize()
+    ca, la, _ = _bin_state(gi, a)
+    cb, lb, _ = _bin_state(gi, b)
+    assert np.array_equal(ca, cb)
+    assert all((x is None and y is None) or np.array_equal(x, y) for x, y in zip(la, lb))
+
+
 def test_direct_binning_small_slabs():
     # slabs so small (GI_SLAB_MIN=0, capacity 6 keys per tile) that many tiles
     # overflow: the counts stay exact, in-slab tiles exact, the overflowing
