@@ -418,6 +418,32 @@ gi_status gi_qat_step(float* params, float* m, float* v, float* eff, float* grad
                       int64_t key_capacity, void* ws, size_t ws_bytes, uint32_t* step_counter,
                       float* losses, uint32_t* status_flags, void* stream);
 
+/* --- fit targets from 8-bit images ------------------------------------------
+ * The paper's datasets (Kodak, DIV2K) are 24-bit RGB images.  A fit
+ * whose targets stream in (one image per step) moves each across the host
+ * link as 8-bit RGB (1.18 MB for a Kodak image, a quarter of its fp32 form):
+ * gi_target_upload_rgb8 on a copy stream, gi_target_from_rgb8 on the compute
+ * stream before the step.  Events are cudaEvent_t handles the caller created
+ * (NULL: no wait / no record).  Errors: GI_EINVAL for a bad frame or a NULL
+ * buffer with a non-empty frame (nothing enqueued); a failed event, copy or
+ * launch call is GI_ECUDA.  B, H, W from f (k unused).  Caller owns every
+ * buffer; no alignment needed.
+ *
+ * gi_target_from_rgb8: on `stream`, wait for wait_event, then expand
+ * rgb (device u8 [B][H][W][3], interleaved as a decoder returns it) into
+ * target (device fp32 [B][3][H][W], planar: the layout every fit / loss entry
+ * point reads), target = u / 255 (IEEE fp32 division, round to nearest), then
+ * record done_event (rgb may be overwritten after it).  One kernel. */
+gi_status gi_target_from_rgb8(const uint8_t* rgb, const gi_frame* f, float* target,
+                              void* wait_event, void* done_event, void* stream);
+
+/* gi_target_upload_rgb8: on `stream`, wait for wait_event (e.g. the previous
+ * expansion's done_event: dev_rgb is free), copy host_rgb (host u8
+ * [B][H][W][3]; pinned for an asynchronous copy) to dev_rgb (device, same
+ * size), record ready_event.  One copy, no kernel. */
+gi_status gi_target_upload_rgb8(const uint8_t* host_rgb, uint8_t* dev_rgb, const gi_frame* f,
+                                void* wait_event, void* ready_event, void* stream);
+
 /* --- harness helpers (not on the hot path) ---------------------------------
  * PSNR of each image on [0,1]-clamped values, capped at 100 dB:
  * psnr[B] fp32 out; ws of gi_psnr_workspace_bytes() bytes (device). */

@@ -13,7 +13,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libgi.so")
 SOURCES = ["api.cu", "project.cu", "scan.cu", "bin.cu", "render.cu", "backward.cu", "adam.cu",
-           "adan.cu", "decode.cu", "psnr.cu", "qat.cu", "peer.cu", "fused.cu"]
+           "adan.cu", "decode.cu", "psnr.cu", "qat.cu", "peer.cu", "fused.cu", "image.cu"]
 HEADERS = ["gi_internal.cuh", "raster_common.cuh", "project_core.cuh", "codec_core.cuh",
            "chunks.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")

@@ -797,6 +797,43 @@ gi_status gi_qat_step(float* params, float* m, float* v, float* eff, float* grad
     return GI_OK;
 }
 
+static cudaError_t wait_on(void* ev, cudaStream_t s) {
+    return ev == nullptr ? cudaSuccess : cudaStreamWaitEvent(s, static_cast<cudaEvent_t>(ev), 0);
+}
+static cudaError_t record_on(void* ev, cudaStream_t s) {
+    return ev == nullptr ? cudaSuccess : cudaEventRecord(static_cast<cudaEvent_t>(ev), s);
+}
+
+gi_status gi_target_from_rgb8(const uint8_t* rgb, const gi_frame* f, float* target,
+                              void* wait_event, void* done_event, void* stream) {
+    gi_status st;
+    if ((st = check_frame(f)) != GI_OK) return st;
+    if ((int64_t)f->width * f->height * f->batch > 0 && (!rgb || !target)) return invalid("NULL buffer");
+    cudaStream_t s = S(stream);
+    cudaError_t e;
+    if ((e = wait_on(wait_event, s)) != cudaSuccess) return cuda_status(e, "gi_target_from_rgb8/wait");
+    if ((e = gi::launch_target_from_rgb8(rgb, *f, target, s)) != cudaSuccess)
+        return cuda_status(e, "gi_target_from_rgb8");
+    if ((e = record_on(done_event, s)) != cudaSuccess) return cuda_status(e, "gi_target_from_rgb8/record");
+    return GI_OK;
+}
+
+gi_status gi_target_upload_rgb8(const uint8_t* host_rgb, uint8_t* dev_rgb, const gi_frame* f,
+                                void* wait_event, void* ready_event, void* stream) {
+    gi_status st;
+    if ((st = check_frame(f)) != GI_OK) return st;
+    const size_t bytes = (size_t)3 * f->width * f->height * f->batch;
+    if (bytes > 0 && (!host_rgb || !dev_rgb)) return invalid("NULL buffer");
+    cudaStream_t s = S(stream);
+    cudaError_t e;
+    if ((e = wait_on(wait_event, s)) != cudaSuccess) return cuda_status(e, "gi_target_upload_rgb8/wait");
+    if (bytes > 0 &&
+        (e = cudaMemcpyAsync(dev_rgb, host_rgb, bytes, cudaMemcpyHostToDevice, s)) != cudaSuccess)
+        return cuda_status(e, "gi_target_upload_rgb8/copy");
+    if ((e = record_on(ready_event, s)) != cudaSuccess) return cuda_status(e, "gi_target_upload_rgb8/record");
+    return GI_OK;
+}
+
 gi_status gi_psnr(const float* image, const float* target, const gi_frame* f, float* psnr, void* ws,
                   void* stream) {
     gi_status st;

@@ -527,6 +527,8 @@ cudaError_t launch_vq_decode(const uint8_t* payload, const gi_codec_meta& meta, 
 cudaError_t launch_decode_project(const uint8_t* payload, const gi_codec_meta& meta,
                                   float* params_out, const gi_frame& f, Proj* proj,
                                   uint32_t* tiles_touched, const ProjectFuse& fuse, cudaStream_t s);
+cudaError_t launch_target_from_rgb8(const uint8_t* rgb, const gi_frame& f, float* target,
+                                    cudaStream_t s);
 cudaError_t launch_psnr(const float* image, const float* target, const gi_frame& f, float* psnr,
                         void* ws, cudaStream_t s);
 

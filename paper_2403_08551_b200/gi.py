@@ -114,6 +114,8 @@ SIGNATURES = {
     "gi_kmeans_step": (C.c_int, [_vp, C.c_int32, C.c_int32, _vp, _vp, _vp, _sz, _vp]),
     "gi_psnr_workspace_bytes": (_sz, [_FP]),
     "gi_psnr": (C.c_int, [_vp, _vp, _FP, _vp, _vp, _vp]),
+    "gi_target_from_rgb8": (C.c_int, [_vp, _FP, _vp, _vp, _vp, _vp]),
+    "gi_target_upload_rgb8": (C.c_int, [_vp, _vp, _FP, _vp, _vp, _vp]),
     "gi_check": (C.c_int, [_vp, _i64, _vp, _vp]),
 }
 
@@ -154,8 +156,15 @@ def _ptr(t) -> int | None:
     return t.data_ptr()
 
 
+_raw_stream = getattr(torch._C, "_cuda_getCurrentRawStream", None)
+
+
 def _stream(stream) -> int | None:
     if stream is None:
+        # torch's current stream on the current device (the capture stream
+        # inside torch.cuda.graph); the raw getter skips building a Stream object
+        if _raw_stream is not None:
+            return _raw_stream(torch.cuda.current_device())
         return torch.cuda.current_stream().cuda_stream
     if isinstance(stream, int):
         return stream
@@ -250,6 +259,34 @@ def _fit_step(fn, params, grads, m, v, target, n, f, flags, key_capacity, fit_ws
            int(flags), int(key_capacity), _ptr(fit_ws), fit_ws.numel() * fit_ws.element_size(),
            _ptr(step_counter), float(lr0), int(half_every), float(beta1), float(beta2), float(eps),
            _ptr(loss), _ptr(status_flags), ev, _stream(stream)), name)
+
+
+class FitStepCall:
+    """A prepared gi_fit_step_chained / gi_fit_step call (Adam) for a loop of
+    steps on fixed buffers: the argument list is marshalled once; each call
+    substitutes the target, the loss destination and the stream (the host cost
+    per step is then one ctypes call -- it bounds a streaming fit's e2e rate)."""
+
+    def __init__(self, chained, params, grads, m, v, n, f, flags, key_capacity, fit_ws,
+                 step_counter, lr0, half_every, beta1, beta2, eps, status_flags):
+        lib = load()
+        self.fn = lib.gi_fit_step_chained if chained else lib.gi_fit_step
+        self.name = "gi_fit_step_chained" if chained else "gi_fit_step"
+        self.f = f
+        self.argv = [_ptr(params), _ptr(grads), _ptr(m), _ptr(v), None, int(n), C.byref(f),
+                     int(flags), int(key_capacity), _ptr(fit_ws),
+                     fit_ws.numel() * fit_ws.element_size(), _ptr(step_counter), float(lr0),
+                     int(half_every), float(beta1), float(beta2), float(eps), None,
+                     _ptr(status_flags), None, None]
+
+    def __call__(self, target: int, loss: int, stream: int):
+        a = self.argv
+        a[4] = target
+        a[17] = loss
+        a[20] = stream
+        rc = self.fn(*a)
+        if rc != GI_OK:
+            _ok(rc, self.name)
 
 
 def gi_fit_step(params, grads, m, v, target, n, f, flags, key_capacity, fit_ws, step_counter,
@@ -435,6 +472,30 @@ def gi_decode_render_frame(payload, meta: gi_codec_meta, f: gi_frame, key_capaci
                                       C.byref(meta), C.byref(f), int(key_capacity), _ptr(frame_ws),
                                       frame_ws.numel() * frame_ws.element_size(), _ptr(params),
                                       _ptr(image), _stream(stream)), "gi_decode_render_frame")
+
+
+def _event(e):
+    if e is None:
+        return None
+    return e if isinstance(e, int) else e.cuda_event
+
+
+def gi_target_from_rgb8(rgb, f, target, wait_event=None, done_event=None, stream=None):
+    """rgb: device u8 [B][H][W][3]; target: device fp32 [B][3][H][W] <- rgb / 255.
+    Events: created torch.cuda.Event (recorded once) or raw handles."""
+    _ok(load().gi_target_from_rgb8(_ptr(rgb), C.byref(f), _ptr(target), _event(wait_event),
+                                   _event(done_event), _stream(stream)), "gi_target_from_rgb8")
+
+
+def gi_target_upload_rgb8(host_rgb, dev_rgb, f, wait_event=None, ready_event=None, stream=None):
+    """host_rgb: (pinned) host u8 [B][H][W][3] tensor or address -> dev_rgb (device)."""
+    if isinstance(host_rgb, torch.Tensor):
+        if host_rgb.is_cuda or not host_rgb.is_contiguous():
+            raise ValueError("host_rgb: a contiguous host tensor")
+        host_rgb = host_rgb.data_ptr()
+    _ok(load().gi_target_upload_rgb8(host_rgb, _ptr(dev_rgb), C.byref(f), _event(wait_event),
+                                     _event(ready_event), _stream(stream)),
+        "gi_target_upload_rgb8")
 
 
 def gi_psnr(image, target, f, psnr, ws, stream=None):

@@ -157,6 +157,8 @@ class Fitter:
             self.adan_extra = dict(beta3=beta3, weight_decay=weight_decay)
         self.flags = flags
         self.graph = None
+        self._call = None                       # prepared gi.FitStepCall (Adam, built on first step)
+        self._tshape = self.target.shape
 
     def step(self, stream=None, stage_events=None, loss_out=None):
         """One fused step.  In chained mode (default) the first call primes
@@ -176,7 +178,21 @@ class Fitter:
                self.n, self.f, self.flags, self.cap, self.fit_ws, self.step_counter, loss=loss,
                status_flags=self.status, stream=stream, **self.hyper, **self.adan_extra)
             return
-        if self.chained:
+        if stage_events is None:
+            # the prepared call (gi.FitStepCall): same entry point, arguments
+            # marshalled once per Fitter
+            if self._call is None:
+                h = self.hyper
+                self._call = gi.FitStepCall(self.chained, self.params, self.grads, self.m, self.v,
+                                            self.n, self.f, self.flags, self.cap, self.fit_ws,
+                                            self.step_counter, h["lr0"], h["half_every"],
+                                            h["beta1"], h["beta2"], h["eps"], self.status)
+            t = self.target
+            if not (t.is_cuda and t.is_contiguous() and t.shape == self._tshape):
+                raise ValueError("target: a contiguous device tensor [B][3][H][W]")
+            self._call(t.data_ptr(), loss if isinstance(loss, int) else gi._ptr(loss),
+                       gi._stream(stream))
+        elif self.chained:
             gi.gi_fit_step_chained(self.params, self.grads, self.m, self.v, self.target, self.n,
                                    self.f, self.flags, self.cap, self.fit_ws, self.step_counter,
                                    loss=loss, status_flags=self.status,

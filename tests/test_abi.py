@@ -90,6 +90,10 @@ def test_host_queries_and_validation(lib):
     assert rc == gi.GI_EINVAL and b"tile window" in lib.gi_last_error()
     rc = lib.gi_fit_grads(None, None, None, 10, C.byref(f), 0, -1, 0, 1 << 16, None, 0, None, None)
     assert rc == gi.GI_EINVAL and b"tile window" in lib.gi_last_error()
+    # 8-bit targets: NULL buffers with a non-empty frame, a bad frame
+    assert lib.gi_target_from_rgb8(None, C.byref(f), None, None, None, None) == gi.GI_EINVAL
+    assert lib.gi_target_from_rgb8(None, C.byref(bad), None, None, None, None) == gi.GI_EINVAL
+    assert lib.gi_target_upload_rgb8(None, None, C.byref(f), None, None, None) == gi.GI_EINVAL
 
 
 def test_product_package_does_not_import_oracle():

@@ -1183,3 +1183,31 @@ def test_next_edge_cases(gi, gio):
                     cap, fws, lo)
     torch.cuda.synchronize()
     assert not gr.any() and float(lo[0]) == 0.0
+
+
+def test_target_from_rgb8(gi):
+    # 8-bit RGB targets (the paper's datasets): interleaved u8 -> planar
+    # fp32 u / 255, bit-exact against the definition (IEEE fp32 division)
+    rng = np.random.default_rng(8)
+    for W, H, B in ((768, 512, 1), (70, 45, 3), (5, 3, 2)):
+        rgb = rng.integers(0, 256, size=(B, H, W, 3), dtype=np.uint8)
+        rgb.reshape(-1)[:2] = (0, 255)
+        ref = np.ascontiguousarray((rgb.astype(np.float32) / np.float32(255)).transpose(0, 3, 1, 2))
+        out = torch.full((B, 3, H, W), float("nan"), device=DEV)
+        gi.gi_target_from_rgb8(to_dev(rgb), gi.frame(W, H, B), out)
+        torch.cuda.synchronize()
+        assert np.array_equal(out.cpu().numpy().view(np.uint32), ref.view(np.uint32)), (W, H, B)
+        # from host memory: upload on a copy stream, expansion on the compute
+        # stream after the upload's event -- same bits
+        host = torch.from_numpy(rgb).pin_memory()
+        stage = torch.empty(rgb.shape, dtype=torch.uint8, device=DEV)
+        out2 = torch.full((B, 3, H, W), float("nan"), device=DEV)
+        cs = torch.cuda.Stream()
+        ready, done = torch.cuda.Event(), torch.cuda.Event()
+        ready.record(torch.cuda.current_stream())
+        done.record(torch.cuda.current_stream())
+        fr = gi.frame(W, H, B)
+        gi.gi_target_upload_rgb8(host, stage, fr, None, ready, cs)
+        gi.gi_target_from_rgb8(stage, fr, out2, ready, done)
+        torch.cuda.synchronize()
+        assert np.array_equal(out2.cpu().numpy().view(np.uint32), ref.view(np.uint32)), (W, H, B)
