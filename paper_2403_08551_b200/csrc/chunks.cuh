@@ -71,7 +71,7 @@ struct ChunkPlanOut {
 // chunks: C2 init tile kernel 28.7 -> 27.7 us; on batches of many records
 // (dense tiles) the longer chunks cost more than the barriers (fitted proxy
 // 118 -> 125 us), so those keep the candidate planner.
-template <int NT>
+template <int NT, bool kIlv>
 __device__ __forceinline__ ChunkPlanOut plan_chunks_few(ChunkShared<NT>& ch, int cnt, uint32_t wj,
                                                         uint32_t cabs_bits) {
     constexpr int NW = NT / 32;
@@ -90,6 +90,8 @@ __device__ __forceinline__ ChunkPlanOut plan_chunks_few(ChunkShared<NT>& ch, int
     }
     const uint32_t room = max((uint32_t)NT - (uint32_t)cnt, 1u);
     const uint32_t C = max((tot + room - 1u) / room, 1u);
+    // contiguous: nf chunks of C + a remainder; interleaved: ceil(wj / C)
+    // chunks of ~wj / nc pairs (the same count)
     const uint32_t nf = chunk_div(wj, chunk_rcp((float)C)), rm = wj - nf * C;
     const uint32_t nc = nf + (rm != 0u ? 1u : 0u);
     uint32_t incl = nc;
@@ -107,10 +109,15 @@ __device__ __forceinline__ ChunkPlanOut plan_chunks_few(ChunkShared<NT>& ch, int
         fstart = incl - nc + __reduce_add_sync(kFull, lane < warp ? x : 0u);
     }
     if (j < cnt) {
-        for (uint32_t i = 0; i < nf; ++i)
-            ch.item[fstart + i] = (uint32_t)j | (i * C) << 8 | ((i + 1u) * C) << 17;
-        if (rm != 0u) ch.item[fstart + nf] = (uint32_t)j | (nf * C) << 8 | wj << 17;
-        ch.jplan[j] = fstart | nf << 9 | (fstart + nf) << 18 | (rm != 0u ? 1u << 27 : 0u);
+        if constexpr (kIlv) {     // chunk i of record j walks pairs i, i + nc, ...
+            for (uint32_t i = 0; i < nc; ++i) ch.item[fstart + i] = (uint32_t)j | i << 8 | nc << 17;
+            ch.jplan[j] = fstart | nc << 9;
+        } else {
+            for (uint32_t i = 0; i < nf; ++i)
+                ch.item[fstart + i] = (uint32_t)j | (i * C) << 8 | ((i + 1u) * C) << 17;
+            if (rm != 0u) ch.item[fstart + nf] = (uint32_t)j | (nf * C) << 8 | wj << 17;
+            ch.jplan[j] = fstart | nf << 9 | (fstart + nf) << 18 | (rm != 0u ? 1u << 27 : 0u);
+        }
     }
     const int e = cmx == 0u ? 0 : (int)((cmx >> 23) & 0xffu) - 126;
     const int s = min(max(22 - e, -100), 100);
@@ -123,7 +130,7 @@ __device__ __forceinline__ ChunkPlanOut plan_chunks_few(ChunkShared<NT>& ch, int
     return out;
 }
 
-template <int NT>
+template <int NT, bool kIlv>
 __device__ __forceinline__ ChunkPlanOut plan_chunks_many(ChunkShared<NT>& ch, int cnt, uint32_t wj,
                                                          uint32_t cabs_bits) {
     constexpr int NW = NT / 32;
@@ -167,8 +174,18 @@ __device__ __forceinline__ ChunkPlanOut plan_chunks_many(ChunkShared<NT>& ch, in
         if ((n01 >> 16) <= (uint32_t)NT) C = c1;
         if ((n01 & 0xffffu) <= (uint32_t)NT) C = c0;
     }
-    // (3) full chunks: block scan of their counts; remainders: size bins
-    const uint32_t nf = chunk_div(wj, chunk_rcp((float)C)), rm = wj - nf * C;
+    // (3) full chunks: block scan of their counts; remainders: size bins.
+    // Interleaved: records of >= 2 chunks (ceil(wj / C), lengths ~wj / nc)
+    // in the scanned region, one-chunk records (the whole record) binned
+    uint32_t nf, rm;
+    if constexpr (kIlv) {
+        const uint32_t nc = chunk_div(wj + C - 1u, chunk_rcp((float)C));
+        nf = nc >= 2u ? nc : 0u;
+        rm = nc == 1u ? wj : 0u;
+    } else {
+        nf = chunk_div(wj, chunk_rcp((float)C));
+        rm = wj - nf * C;
+    }
     uint32_t incl = nf;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -202,9 +219,14 @@ __device__ __forceinline__ ChunkPlanOut plan_chunks_many(ChunkShared<NT>& ch, in
     __syncthreads();
     const uint32_t rpos = rm != 0u ? ch.hist[rbin] + rrank : 0u;
     if (j < cnt) {
-        for (uint32_t i = 0; i < nf; ++i)
-            ch.item[fstart + i] = (uint32_t)j | (i * C) << 8 | ((i + 1u) * C) << 17;
-        if (rm != 0u) ch.item[rpos] = (uint32_t)j | (nf * C) << 8 | wj << 17;
+        if constexpr (kIlv) {
+            for (uint32_t i = 0; i < nf; ++i) ch.item[fstart + i] = (uint32_t)j | i << 8 | nf << 17;
+            if (rm != 0u) ch.item[rpos] = (uint32_t)j | 1u << 17;
+        } else {
+            for (uint32_t i = 0; i < nf; ++i)
+                ch.item[fstart + i] = (uint32_t)j | (i * C) << 8 | ((i + 1u) * C) << 17;
+            if (rm != 0u) ch.item[rpos] = (uint32_t)j | (nf * C) << 8 | wj << 17;
+        }
         ch.jplan[j] = fstart | nf << 9 | rpos << 18 | (rm != 0u ? 1u << 27 : 0u);
     }
     // s: the largest |c'| rounded up to a power of two, 2^e >= max |c'|; then
@@ -220,12 +242,13 @@ __device__ __forceinline__ ChunkPlanOut plan_chunks_many(ChunkShared<NT>& ch, in
     return out;
 }
 
-template <int NT>
+// kIlv: interleaved chunks (walk_chunk_ilv) instead of contiguous ones.
+template <int NT, bool kIlv = false>
 __device__ __forceinline__ ChunkPlanOut plan_chunks(ChunkShared<NT>& ch, int cnt, uint32_t wj,
                                                     uint32_t cabs_bits) {
     // cnt is uniform over the CTA
-    return cnt * 8 <= NT * 3 ? plan_chunks_few<NT>(ch, cnt, wj, cabs_bits)
-                             : plan_chunks_many<NT>(ch, cnt, wj, cabs_bits);
+    return cnt * 8 <= NT * 3 ? plan_chunks_few<NT, kIlv>(ch, cnt, wj, cabs_bits)
+                             : plan_chunks_many<NT, kIlv>(ch, cnt, wj, cabs_bits);
 }
 
 // The pixel walk of one chunk: record r's in-tile box, row-major pairs
@@ -261,6 +284,52 @@ __device__ __forceinline__ void walk_chunk(const SR& sr, uint32_t it, F&& f) {
         if (dx > dx1) {
             p += wrap;
             dx = dx0;
+            cdy += A.z;
+        }
+    }
+}
+
+// The interleaved walk (plan_chunks<NT, true>): record r's in-tile box,
+// row-major pair index k = k0, k0 + n, k0 + 2n, ... < w (the record's n
+// chunks interleave, so the lanes walking one record touch adjacent pixels at
+// each step and their shared-memory accumulators fall in distinct banks).
+// The render kernel uses it (C2 frame 53.6k -> 55.0k FPS); on the fit kernel
+// the chunk lengths (~w / n, no longer exactly C) balance the warps worse
+// than the bank conflicts cost (C2 tile kernel 28.4 -> 29.5 us).
+template <class SR, typename F>
+__device__ __forceinline__ void walk_chunk_ilv(const SR& sr, uint32_t it, F&& f) {
+    const int r = (int)(it & 0xffu);
+    const int k0 = (int)((it >> 8) & 0x1ffu), n = (int)((it >> 17) & 0x1ffu);
+    const float4 A = sr.a[r];          // {a, b, c, c'r}
+    const float4 B = sr.b[r];          // {c'g, c'b, mx, my}
+    const float2 O = sr.o[r];          // {u0, v0}
+    const uint32_t box = sr.c[r].x;
+    const int lx0 = box & 0xff, lx1 = (box >> 8) & 0xff, ly0 = (box >> 16) & 0xff, ly1 = box >> 24;
+    const int wdt = lx1 - lx0 + 1;
+    const float rw = chunk_rcp((float)wdt);
+    const int row = (int)chunk_div((uint32_t)k0, rw), col = k0 - row * wdt;
+    const int srow = (int)chunk_div((uint32_t)n, rw), scol = n - srow * wdt;
+    const int cnt = (int)chunk_div((uint32_t)(wdt * (ly1 - ly0 + 1) - k0 + n - 1),
+                                   chunk_rcp((float)n));   // pairs of this chunk
+    // dx steps by scol and wraps half a pixel past the box's last column (far
+    // above the stepping's rounding); c dy (+ v0) advances by c per row
+    const float dx1 = ((float)lx1 + 1.0f) - B.z;
+    const float fscol = (float)scol, fwdt = (float)wdt, cstep = A.z * (float)srow;
+    float dx = ((float)(lx0 + col) + 0.5f) - B.z;
+    float cdy = fmaf(A.z, ((float)(ly0 + row) + 0.5f) - B.w, O.y);
+    int p = (ly0 + row) * kTile + lx0 + col;
+    const int pstep = srow * kTile + scol, wrap = kTile - wdt;
+    for (int k = 0; k < cnt; ++k) {
+        const float u = fmaf(A.x, dx, O.x);
+        const float v = fmaf(A.y, dx, cdy);
+        const float w = ex2_approx(fmaf(-u, u, -(v * v)));
+        f(p, A, B, u, v, w);
+        p += pstep;
+        dx += fscol;
+        cdy += cstep;
+        if (dx > dx1) {
+            p += wrap;
+            dx -= fwdt;
             cdy += A.z;
         }
     }

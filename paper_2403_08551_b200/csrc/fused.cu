@@ -119,7 +119,7 @@ __device__ __forceinline__ ChunkPlanOut stage_and_plan(FusedShared<NT, NB, kBwd>
         cabs = max(abs_bits(sh.sr.a[j].w), max(abs_bits(sh.sr.b[j].x), abs_bits(sh.sr.b[j].y)));
     }
     cnt_out = cnt;
-    return plan_chunks<NT>(sh.ch, cnt, wj, cabs);
+    return plan_chunks<NT, !kBwd>(sh.ch, cnt, wj, cabs);     // interleaved chunks for the render
 }
 
 // Forward of a planned batch: fixed-point sums into sh.u.acc (zeroed by the
@@ -136,11 +136,13 @@ __device__ __forceinline__ void forward_chunks(FusedShared<NT, NB, kBwd>& sh,
     int* a0 = sh.u.acc[0];
     int* a1 = sh.u.acc[1];
     int* a2 = sh.u.acc[2];
-    walk_chunk(sh.sr, it, [&](int p, const float4&, const float4&, float, float, float w) {
+    auto add = [&](int p, const float4&, const float4&, float, float, float w) {
         atomicAdd(&a0[p], __float_as_int(fmaf(cr, w, kFixMagic)) - kFixMagicBits);
         atomicAdd(&a1[p], __float_as_int(fmaf(cg, w, kFixMagic)) - kFixMagicBits);
         atomicAdd(&a2[p], __float_as_int(fmaf(cb, w, kFixMagic)) - kFixMagicBits);
-    });
+    };
+    if constexpr (kBwd) walk_chunk(sh.sr, it, add);
+    else walk_chunk_ilv(sh.sr, it, add);
 }
 
 #ifndef GI_TILE3_MINB
