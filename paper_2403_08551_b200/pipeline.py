@@ -158,6 +158,7 @@ class Fitter:
         self.flags = flags
         self.graph = None
         self._call = None                       # prepared gi.FitStepCall (Adam, built on first step)
+        self._call_key = None
         self._tshape = self.target.shape
 
     def step(self, stream=None, stage_events=None, loss_out=None):
@@ -181,7 +182,10 @@ class Fitter:
         if stage_events is None:
             # the prepared call (gi.FitStepCall): same entry point, arguments
             # marshalled once per Fitter
-            if self._call is None:
+            key = (self.params.data_ptr(), self.grads.data_ptr(), self.m.data_ptr(),
+                   self.v.data_ptr(), self.fit_ws.data_ptr())
+            if self._call is None or self._call_key != key:    # (re)built if a buffer was replaced
+                self._call_key = key
                 h = self.hyper
                 self._call = gi.FitStepCall(self.chained, self.params, self.grads, self.m, self.v,
                                             self.n, self.f, self.flags, self.cap, self.fit_ws,

@@ -334,6 +334,29 @@ def test_unchain_reprime_matches_fresh(gi):
     assert torch.equal(a.m, b.m) and torch.equal(a.v, b.v)
 
 
+def test_replaced_buffers_after_steps(gi):
+    # Fitter's prepared step call (gi.FitStepCall) follows buffers replaced
+    # between steps: new params / moment tensors are the ones stepped
+    from paper_2403_08551_b200.pipeline import Fitter
+    W, H, n = 160, 120, 4000
+    p = synth.init_params(12, n)
+    tgt = to_dev(synth.image(12, W, H))[None].contiguous()
+    a = Fitter(to_dev(p)[None].contiguous(), tgt)
+    for _ in range(2):
+        a.step()
+    a.params = a.params.clone()
+    a.m, a.v = a.m.clone(), a.v.clone()
+    a.unchain()
+    b = Fitter(a.params.clone(), tgt, chained=False)
+    b.m.copy_(a.m)
+    b.v.copy_(a.v)
+    b.step_counter.copy_(a.step_counter)
+    a.step()
+    b.step()
+    torch.cuda.synchronize()
+    assert torch.equal(a.params, b.params) and torch.equal(a.m, b.m) and torch.equal(a.v, b.v)
+
+
 def test_non_chained_and_render_after_chained(gi):
     # gi_fit_step (non-chained) clears the pending keys itself; gi_render_frame
     # on that workspace needs gi_fit_reset first (documented in gi.h)
