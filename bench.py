@@ -526,6 +526,7 @@ def main():
 
     # ---------------- the paper's training run: 50k steps (106.59 s on V100) ----
     full_fit, fitted_state, warm_its, encode_fps, qat_its = None, None, None, None, None
+    warm_fps = None
     if not quick:
         full_fit = {}
         psnr_pipe = Pipeline(N_GAUSS, W_IMG, H_IMG, 1, device=dev)
@@ -535,14 +536,18 @@ def main():
             torch.cuda.synchronize(dev)
             fg = ffit.capture(100)
             barrier()
+            w0 = time.perf_counter()
             s_ev[0].record(stream)
-            for _ in range(500):                  # 1 + 500 x 100 = 50,001 steps
+            for i in range(500):                  # 1 + 500 x 100 = 50,001 steps
                 fg.replay()
+                if i % 10 == 9:                   # host sync every 1,000 steps (SURVEY d.3)
+                    torch.cuda.synchronize(dev)
             e_ev[0].record(stream)
             barrier()
+            wall = max_over_ranks(time.perf_counter() - w0)
             secs = max_over_ranks(s_ev[0].elapsed_time(e_ev[0])) / 1000.0
             img = psnr_pipe.render_frame(ffit.params)
-            full_fit[opt] = {"steps": 50001, "seconds": secs,
+            full_fit[opt] = {"steps": 50001, "seconds": secs, "wall_seconds": wall,
                              "psnr_db": float(psnr_pipe.psnr(img, target)[0])}
             if ffit.check() != gi.GI_OK:
                 raise RuntimeError("50k fit status")
@@ -627,6 +632,27 @@ def main():
         if wfit.check() != gi.GI_OK:
             raise RuntimeError("warm fit status")
         del wfit, wg
+        # warm-L2 FPS (SURVEY d.3 asks for warm and flushed): 100 frames per graph replay
+        wpipe = Pipeline(N_GAUSS, W_IMG, H_IMG, 1, device=dev)
+        wpar = params.clone()
+        wpipe.render_frame(wpar)
+        wpay, wdp = d_payload.clone(), dparams.clone()
+        wpipe.decode_render_frame(wpay, meta, wdp)
+        torch.cuda.synchronize(dev)
+        warm_fps = {}
+        for name, fn in (("render_fps", lambda: wpipe.render_frame(wpar)),
+                         ("decode_fps", lambda: wpipe.decode_render_frame(wpay, meta, wdp))):
+            wgr = capture(lambda: [fn() for _ in range(100)])
+            wgr.replay()
+            barrier()
+            s_ev[0].record(stream)
+            for _ in range(5):
+                wgr.replay()
+            e_ev[0].record(stream)
+            barrier()
+            warm_fps[name] = world * 500 / (max_over_ranks(s_ev[0].elapsed_time(e_ev[0])) / 1000.0)
+            del wgr
+        del wpipe
 
         # NEXT-2: encoder (gi_vq_encode) and QAT step (gi_qat_step)
         fp = torch.from_numpy(synth.fitted_params(seed, N_GAUSS)).to(dev).contiguous()
@@ -825,6 +851,7 @@ def main():
             "fit_50k_steps": full_fit,
             "fitted_state": fitted_state,
             "fit_its_warm_graph100": warm_its,
+            "warm_l2_graph100": warm_fps,
             "flush_per_replay": {"fit_its": fit_flush_value, "render_fps": render_fps_flush,
                                  "decode_fps": decode_fps_flush},
             "encode_fps": encode_fps,
