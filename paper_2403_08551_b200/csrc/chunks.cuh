@@ -65,8 +65,8 @@ struct ChunkPlanOut {
 // threads must call; ends with a barrier.
 // Planner for batches of few records (cnt <= 3/8 NT; 3 barriers): C =
 // ceil(tot / (NT - cnt)), so that the chunk count sum ceil(w / C) <= tot / C
-// + cnt <= NT, and items in record-major order (a record's full chunks, then
-// its remainder) from one block scan.  Two barriers fewer than the
+// + cnt <= NT; all full chunks first (record-major), then the remainders in
+// record order, from one block scan of packed counts.  Two barriers fewer than the
 // candidate search below at the price of up to NT / (NT - cnt) longer
 // chunks: C2 init tile kernel 28.7 -> 27.7 us; on batches of many records
 // (dense tiles) the longer chunks cost more than the barriers (fitted proxy
@@ -94,7 +94,11 @@ __device__ __forceinline__ ChunkPlanOut plan_chunks_few(ChunkShared<NT>& ch, int
     // chunks of ~wj / nc pairs (the same count)
     const uint32_t nf = chunk_div(wj, chunk_rcp((float)C)), rm = wj - nf * C;
     const uint32_t nc = nf + (rm != 0u ? 1u : 0u);
-    uint32_t incl = nc;
+    // contiguous: the full chunks (all of length C) first, record-major, then
+    // the remainders in record order -- one scan of (nf | has_remainder << 16)
+    // gives both offsets, so the lanes of a warp mostly walk equal lengths
+    const uint32_t val = kIlv ? nc : (nf | (rm != 0u ? 1u << 16 : 0u));
+    uint32_t incl = val;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
         const uint32_t y = __shfl_up_sync(kFull, incl, o);
@@ -102,21 +106,28 @@ __device__ __forceinline__ ChunkPlanOut plan_chunks_few(ChunkShared<NT>& ch, int
     }
     if (lane == 31) ch.pc[warp] = incl;
     __syncthreads();
-    uint32_t fstart, F;
+    uint32_t excl, Fp;
     {
         const uint32_t x = lane < NW ? ch.pc[lane] : 0u;
-        F = __reduce_add_sync(kFull, x);
-        fstart = incl - nc + __reduce_add_sync(kFull, lane < warp ? x : 0u);
+        Fp = __reduce_add_sync(kFull, x);
+        excl = incl - val + __reduce_add_sync(kFull, lane < warp ? x : 0u);
     }
-    if (j < cnt) {
-        if constexpr (kIlv) {     // chunk i of record j walks pairs i, i + nc, ...
-            for (uint32_t i = 0; i < nc; ++i) ch.item[fstart + i] = (uint32_t)j | i << 8 | nc << 17;
-            ch.jplan[j] = fstart | nc << 9;
-        } else {
+    uint32_t F;
+    if constexpr (kIlv) {
+        F = Fp;
+        if (j < cnt) {     // chunk i of record j walks pairs i, i + nc, ...
+            for (uint32_t i = 0; i < nc; ++i) ch.item[excl + i] = (uint32_t)j | i << 8 | nc << 17;
+            ch.jplan[j] = excl | nc << 9;
+        }
+    } else {
+        const uint32_t Ffull = Fp & 0xffffu;
+        F = Ffull + (Fp >> 16);
+        if (j < cnt) {
+            const uint32_t fstart = excl & 0xffffu, rpos = Ffull + (excl >> 16);
             for (uint32_t i = 0; i < nf; ++i)
                 ch.item[fstart + i] = (uint32_t)j | (i * C) << 8 | ((i + 1u) * C) << 17;
-            if (rm != 0u) ch.item[fstart + nf] = (uint32_t)j | (nf * C) << 8 | wj << 17;
-            ch.jplan[j] = fstart | nf << 9 | (fstart + nf) << 18 | (rm != 0u ? 1u << 27 : 0u);
+            if (rm != 0u) ch.item[rpos] = (uint32_t)j | (nf * C) << 8 | wj << 17;
+            ch.jplan[j] = fstart | nf << 9 | rpos << 18 | (rm != 0u ? 1u << 27 : 0u);
         }
     }
     const int e = cmx == 0u ? 0 : (int)((cmx >> 23) & 0xffu) - 126;
