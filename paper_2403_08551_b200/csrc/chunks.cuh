@@ -63,7 +63,7 @@ struct ChunkPlanOut {
 // its record's in-tile pair count wj and max(|c'_r|, |c'_g|, |c'_b|) (as
 // float bits).  Writes ch.item[0 .. n_items) and ch.jplan[0 .. cnt); all
 // threads must call; ends with a barrier.
-// Planner for batches of few records (cnt <= 3/8 NT; 3 barriers): C =
+// Planner for batches of few records (cnt <= 7/16 NT; 3 barriers): C =
 // ceil(tot / (NT - cnt)), so that the chunk count sum ceil(w / C) <= tot / C
 // + cnt <= NT; all full chunks first (record-major), then the remainders in
 // record order, from one block scan of packed counts.  Two barriers fewer than the
@@ -253,12 +253,20 @@ __device__ __forceinline__ ChunkPlanOut plan_chunks_many(ChunkShared<NT>& ch, in
     return out;
 }
 
+// batches of <= 7/16 NT records take plan_chunks_few (3/8: render -0.8 %;
+// 1/2: the fitted proxy's tile kernel 118 -> 127 us; 5/16: C2 fit -3 %)
+#ifndef GI_FEW_NUM
+#define GI_FEW_NUM 7
+#endif
+#ifndef GI_FEW_DEN
+#define GI_FEW_DEN 16
+#endif
 // kIlv: interleaved chunks (walk_chunk_ilv) instead of contiguous ones.
 template <int NT, bool kIlv = false>
 __device__ __forceinline__ ChunkPlanOut plan_chunks(ChunkShared<NT>& ch, int cnt, uint32_t wj,
                                                     uint32_t cabs_bits) {
     // cnt is uniform over the CTA
-    return cnt * 8 <= NT * 3 ? plan_chunks_few<NT, kIlv>(ch, cnt, wj, cabs_bits)
+    return cnt * GI_FEW_DEN <= NT * GI_FEW_NUM ? plan_chunks_few<NT, kIlv>(ch, cnt, wj, cabs_bits)
                              : plan_chunks_many<NT, kIlv>(ch, cnt, wj, cabs_bits);
 }
 
