@@ -9,6 +9,17 @@
 
 #include "codec_core.cuh"
 #include "gi_internal.cuh"
+#include <nvtx3/nvToolsExt.h>
+
+// NVTX range around every compute entry point (SURVEY §5 tracing): a no-op
+// unless a tool (nsys, ncu --nvtx) is attached.
+namespace {
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+};
+}  // namespace
+#define GI_NVTX(name) const NvtxRange gi_nvtx_range_(name)
 
 namespace gi {
 namespace {
@@ -128,6 +139,7 @@ size_t gi_proj_bytes(int32_t n, const gi_frame* f) {
 
 gi_status gi_project(const float* params, int32_t n, const gi_frame* f, uint32_t flags, void* proj,
                      uint32_t* tiles_touched, void* stream) {
+    GI_NVTX("gi_project");
     gi_status st;
     if ((st = check_frame(f)) != GI_OK || (st = check_n(n, f)) != GI_OK) return st;
     if (!gi::flags_valid(flags)) return invalid("flags");
@@ -148,6 +160,7 @@ size_t gi_bin_workspace_bytes(int32_t n, int64_t key_capacity, const gi_frame* f
 gi_status gi_bin(const void* proj, const uint32_t* tiles_touched, int32_t n, const gi_frame* f,
                  int64_t key_capacity, void* ws, size_t ws_bytes, uint32_t* key_tile,
                  uint32_t* key_gid, uint32_t* tile_range, uint32_t* n_keys, void* stream) {
+    GI_NVTX("gi_bin");
     gi_status st;
     if ((st = check_frame(f)) != GI_OK || (st = check_n(n, f)) != GI_OK) return st;
     if (key_capacity < 0 || key_capacity >= (1LL << 31)) return invalid("key_capacity");
@@ -163,6 +176,7 @@ gi_status gi_bin(const void* proj, const uint32_t* tiles_touched, int32_t n, con
 
 gi_status gi_render(const void* proj, const uint32_t* key_gid, const uint32_t* tile_range,
                     int32_t n, const gi_frame* f, float* image, void* stream) {
+    GI_NVTX("gi_render");
     gi_status st;
     if ((st = check_frame(f)) != GI_OK || (st = check_n(n, f)) != GI_OK) return st;
     if (!tile_range || !image || (n > 0 && (!proj || !key_gid))) return invalid("NULL buffer");
@@ -183,6 +197,7 @@ gi_status gi_render_backward(const float* params, const void* proj, const uint32
                              uint32_t flags, const float* dL_dimage, const float* target,
                              int64_t key_capacity, void* ws, size_t ws_bytes, float* grads,
                              float* loss, float* image_out, void* stream) {
+    GI_NVTX("gi_render_backward");
     gi_status st;
     if ((st = check_frame(f)) != GI_OK || (st = check_n(n, f)) != GI_OK) return st;
     if (!gi::flags_valid(flags)) return invalid("flags");
@@ -201,6 +216,7 @@ gi_status gi_render_backward(const float* params, const void* proj, const uint32
 gi_status gi_adam_step(float* params, const float* grads, float* m, float* v, int64_t count,
                        int32_t step, float lr, float beta1, float beta2, float eps,
                        uint32_t* nonfinite_flag, void* stream) {
+    GI_NVTX("gi_adam_step");
     if (count < 0) return invalid("count");
     if (step < 1) return invalid("step is 1-based");
     if (!(beta1 >= 0.f && beta1 < 1.f && beta2 >= 0.f && beta2 < 1.f)) return invalid("betas");
@@ -241,6 +257,7 @@ gi_status gi_peer_adam_step(float* params, float* m, float* v, const float* cons
                             int32_t G, int64_t count, int32_t step, float lr, float beta1,
                             float beta2, float eps, int32_t n_loss, float* loss_out,
                             uint32_t* nonfinite_flag, void* stream) {
+    GI_NVTX("gi_peer_adam_step");
     if (count < 0) return invalid("count");
     if (G < 1 || G > gi::kMaxPeers) return invalid("G must be 1..8");
     if (n_loss < 0 || n_loss > 32) return invalid("n_loss must be 0..32");
@@ -260,6 +277,7 @@ gi_status gi_adan_step(float* params, const float* grads, float* m, float* v, fl
                        float* grad_prev, int64_t count, int32_t step, float lr, float beta1,
                        float beta2, float beta3, float eps, float weight_decay,
                        uint32_t* nonfinite_flag, void* stream) {
+    GI_NVTX("gi_adan_step");
     if (count < 0 || count % 8 != 0) return invalid("count must be a multiple of 8");
     if (step < 1) return invalid("step is 1-based");
     if (!(beta1 >= 0.f && beta1 < 1.f && beta2 >= 0.f && beta2 < 1.f && beta3 >= 0.f && beta3 < 1.f))
@@ -419,6 +437,7 @@ gi_status gi_fit_grads(const float* params, float* grads, const float* target, i
                        const gi_frame* f, uint32_t flags, int32_t tile_row0, int32_t tile_rows,
                        int64_t key_capacity, void* fit_ws, size_t ws_bytes, float* loss,
                        void* stream) {
+    GI_NVTX("gi_fit_grads");
     gi_status st;
     if ((st = check_frame(f)) != GI_OK || (st = check_n(n, f)) != GI_OK) return st;
     if (!gi::flags_valid(flags)) return invalid("flags");
@@ -474,6 +493,7 @@ gi_status gi_fit_step(float* params, float* grads, float* m, float* v, const flo
                       void* fit_ws, size_t ws_bytes, uint32_t* step_counter, float lr0,
                       int32_t half_every, float beta1, float beta2, float eps, float* loss,
                       uint32_t* status_flags, void* const* stage_events, void* stream) {
+    GI_NVTX("gi_fit_step");
     return fit_step_impl(params, grads, m, v, target, n, f, flags, key_capacity, fit_ws, ws_bytes,
                          step_counter, lr0, half_every, beta1, beta2, eps, loss, status_flags,
                          stage_events, stream, false);
@@ -485,6 +505,7 @@ gi_status gi_fit_step_adan(float* params, float* grads, float* m, float* v, floa
                            uint32_t* step_counter, float lr0, int32_t half_every, float beta1,
                            float beta2, float beta3, float eps, float weight_decay, float* loss,
                            uint32_t* status_flags, void* stream) {
+    GI_NVTX("gi_fit_step_adan");
     const AdanOpt opt{n, grad_prev, beta3, weight_decay};
     return fit_step_impl(params, grads, m, v, target, n_gauss, f, flags, key_capacity, fit_ws,
                          ws_bytes, step_counter, lr0, half_every, beta1, beta2, eps, loss,
@@ -498,6 +519,7 @@ gi_status gi_fit_step_adan_chained(float* params, float* grads, float* m, float*
                                    int32_t half_every, float beta1, float beta2, float beta3,
                                    float eps, float weight_decay, float* loss,
                                    uint32_t* status_flags, void* stream) {
+    GI_NVTX("gi_fit_step_adan_chained");
     const AdanOpt opt{n, grad_prev, beta3, weight_decay};
     return fit_step_impl(params, grads, m, v, target, n_gauss, f, flags, key_capacity, fit_ws,
                          ws_bytes, step_counter, lr0, half_every, beta1, beta2, eps, loss,
@@ -506,6 +528,7 @@ gi_status gi_fit_step_adan_chained(float* params, float* grads, float* m, float*
 
 gi_status gi_fit_prime(const float* params, int32_t n, const gi_frame* f, uint32_t flags,
                        int64_t key_capacity, void* fit_ws, size_t ws_bytes, void* stream) {
+    GI_NVTX("gi_fit_prime");
     gi_status st;
     if ((st = check_frame(f)) != GI_OK || (st = check_n(n, f)) != GI_OK) return st;
     if (!gi::flags_valid(flags)) return invalid("flags");
@@ -530,6 +553,7 @@ gi_status gi_fit_prime(const float* params, int32_t n, const gi_frame* f, uint32
 
 gi_status gi_fit_reset(int32_t n, const gi_frame* f, int64_t key_capacity, void* fit_ws,
                        size_t ws_bytes, void* stream) {
+    GI_NVTX("gi_fit_reset");
     gi_status st;
     if ((st = check_frame(f)) != GI_OK || (st = check_n(n, f)) != GI_OK) return st;
     if (key_capacity < 0 || key_capacity >= (1LL << 31)) return invalid("key_capacity");
@@ -545,6 +569,7 @@ gi_status gi_fit_step_chained(float* params, float* grads, float* m, float* v, c
                               void* fit_ws, size_t ws_bytes, uint32_t* step_counter, float lr0,
                               int32_t half_every, float beta1, float beta2, float eps, float* loss,
                               uint32_t* status_flags, void* const* stage_events, void* stream) {
+    GI_NVTX("gi_fit_step_chained");
     return fit_step_impl(params, grads, m, v, target, n, f, flags, key_capacity, fit_ws, ws_bytes,
                          step_counter, lr0, half_every, beta1, beta2, eps, loss, status_flags,
                          stage_events, stream, true);
@@ -555,6 +580,7 @@ int64_t gi_launch_count(void) { return gi::g_launches_get(); }
 gi_status gi_render_frame(const float* params, int32_t n, const gi_frame* f, uint32_t flags,
                           int64_t key_capacity, void* frame_ws, size_t ws_bytes, float* image,
                           void* stream) {
+    GI_NVTX("gi_render_frame");
     gi_status st;
     if ((st = check_frame(f)) != GI_OK || (st = check_n(n, f)) != GI_OK) return st;
     if (!gi::flags_valid(flags)) return invalid("flags");
@@ -583,6 +609,7 @@ gi_status gi_render_frame(const float* params, int32_t n, const gi_frame* f, uin
 
 gi_status gi_vq_decode(const uint8_t* payload, size_t payload_bytes, const gi_codec_meta* meta,
                        float* params, void* stream) {
+    GI_NVTX("gi_vq_decode");
     if (!meta) return invalid("meta is NULL");
     if (meta->n < 0) return invalid("n");
     if (meta->bits < 1 || meta->bits > 16 || meta->stages < 1 || meta->stages > 8 ||
@@ -634,6 +661,7 @@ gi_status gi_decode_render_frame(const uint8_t* payload, size_t payload_bytes,
                                  const gi_codec_meta* meta, const gi_frame* f,
                                  int64_t key_capacity, void* frame_ws, size_t ws_bytes,
                                  float* params, float* image, void* stream) {
+    GI_NVTX("gi_decode_render_frame");
     gi_status st;
     int64_t rec = 0;
     if ((st = check_codec(meta, payload_bytes, &rec)) != GI_OK) return st;
@@ -667,6 +695,7 @@ gi_status gi_decode_render_frame(const uint8_t* payload, size_t payload_bytes,
 
 gi_status gi_vq_encode(const float* params, uint32_t flags, const gi_codec_meta* meta,
                        uint8_t* payload, size_t payload_bytes, float* eff, void* stream) {
+    GI_NVTX("gi_vq_encode");
     if (!meta) return invalid("meta is NULL");
     if (meta->n < 0) return invalid("n");
     if (!gi::flags_valid(flags) || (flags & GI_COV_RS)) return invalid("flags");
@@ -703,6 +732,7 @@ size_t gi_kmeans_workspace_bytes(int32_t B) {
 
 gi_status gi_kmeans_step(const float* points, int32_t n, int32_t B, float* centroids,
                          uint32_t* assign, void* ws, size_t ws_bytes, void* stream) {
+    GI_NVTX("gi_kmeans_step");
     if (n < 0) return invalid("n");
     if (B < 2 || B > 256) return invalid("B");
     if (!ws || ws_bytes < gi_kmeans_workspace_bytes(B)) return invalid("workspace too small");
@@ -743,6 +773,7 @@ gi_status gi_qat_step(float* params, float* m, float* v, float* eff, float* grad
                       const float* target, int32_t n, const gi_frame* f, const gi_qat_config* cfg,
                       int64_t key_capacity, void* ws, size_t ws_bytes, uint32_t* step_counter,
                       float* losses, uint32_t* status_flags, void* stream) {
+    GI_NVTX("gi_qat_step");
     gi_status st;
     if ((st = check_frame(f)) != GI_OK || (st = check_n(n, f)) != GI_OK) return st;
     if (f->batch != 1) return invalid("gi_qat_step takes one image (batch 1)");
@@ -806,6 +837,7 @@ static cudaError_t record_on(void* ev, cudaStream_t s) {
 
 gi_status gi_target_from_rgb8(const uint8_t* rgb, const gi_frame* f, float* target,
                               void* wait_event, void* done_event, void* stream) {
+    GI_NVTX("gi_target_from_rgb8");
     gi_status st;
     if ((st = check_frame(f)) != GI_OK) return st;
     if ((int64_t)f->width * f->height * f->batch > 0 && (!rgb || !target)) return invalid("NULL buffer");
@@ -820,6 +852,7 @@ gi_status gi_target_from_rgb8(const uint8_t* rgb, const gi_frame* f, float* targ
 
 gi_status gi_target_upload_rgb8(const uint8_t* host_rgb, uint8_t* dev_rgb, const gi_frame* f,
                                 void* wait_event, void* ready_event, void* stream) {
+    GI_NVTX("gi_target_upload_rgb8");
     gi_status st;
     if ((st = check_frame(f)) != GI_OK) return st;
     const size_t bytes = (size_t)3 * f->width * f->height * f->batch;
@@ -836,6 +869,7 @@ gi_status gi_target_upload_rgb8(const uint8_t* host_rgb, uint8_t* dev_rgb, const
 
 gi_status gi_psnr(const float* image, const float* target, const gi_frame* f, float* psnr, void* ws,
                   void* stream) {
+    GI_NVTX("gi_psnr");
     gi_status st;
     if ((st = check_frame(f)) != GI_OK) return st;
     if (!image || !target || !psnr || !ws) return invalid("NULL buffer");
@@ -849,6 +883,7 @@ size_t gi_psnr_workspace_bytes(const gi_frame* f) {
 
 gi_status gi_check(const uint32_t* n_keys, int64_t key_capacity, const uint32_t* status_flags,
                    void* stream) {
+    GI_NVTX("gi_check");
     cudaError_t e = cudaStreamSynchronize(S(stream));
     if (e != cudaSuccess) return cuda_status(e, "gi_check/sync");
     if (status_flags) {

@@ -255,6 +255,102 @@ class Fitter:
     def steps_done(self) -> int:
         return int(self.step_counter[0].item())
 
+    # -- checkpoint / resume ---------------------------------------------------
+    _STATE = ("params", "m", "v", "n_acc", "grad_prev")
+
+    def save(self, path: str) -> None:
+        """Checkpoint (SURVEY §5): params and the optimiser state (Adam m, v;
+        Adan also n and the previous gradient), the device step counter and
+        the hyper-parameters, as one .npz of the raw fp32 / u32 bits.  Resuming
+        from it continues the fit bit for bit (`Fitter.load`)."""
+        import numpy as np
+        torch.cuda.synchronize(self.device)
+        arrays = {k: getattr(self, k).cpu().numpy() for k in self._STATE if hasattr(self, k)}
+        arrays["step_counter"] = self.step_counter.cpu().numpy()
+        meta = dict(optimizer=self.optimizer, flags=int(self.flags), k=float(self.f.k),
+                    width=int(self.f.width), height=int(self.f.height), batch=int(self.B),
+                    n=int(self.n), key_capacity=int(self.cap), chained=bool(self.chained),
+                    **{k: float(v) for k, v in self.hyper.items()},
+                    **({k: float(v) for k, v in self.adan_extra.items()}
+                       if self.optimizer == "adan" else {}))
+        arrays["meta_json"] = np.frombuffer(__import__("json").dumps(meta).encode(), np.uint8)
+        np.savez(path, **arrays)
+
+    @classmethod
+    def load(cls, path: str, target: torch.Tensor) -> "Fitter":
+        """A Fitter resumed from `save(path)` on `target`'s device (the target
+        image is not part of the checkpoint).  The next step re-primes (chained
+        mode) from the restored params, so the trajectory equals the one the
+        saving Fitter would have followed."""
+        import json
+
+        import numpy as np
+        z = np.load(path)
+        meta = json.loads(bytes(z["meta_json"]).decode())
+        dev = target.device
+        params = torch.from_numpy(z["params"]).to(dev)
+        kw = dict(k=meta["k"], key_capacity=meta["key_capacity"], lr0=meta["lr0"],
+                  half_every=int(meta["half_every"]), beta1=meta["beta1"], beta2=meta["beta2"],
+                  eps=meta["eps"], flags=meta["flags"], chained=meta["chained"],
+                  optimizer=meta["optimizer"])
+        if meta["optimizer"] == "adan":
+            kw.update(beta3=meta["beta3"], weight_decay=meta["weight_decay"])
+        f = cls(params, target, **kw)
+        if (f.f.width, f.f.height, f.B, f.n) != (meta["width"], meta["height"], meta["batch"],
+                                                   meta["n"]):
+            raise ValueError("checkpoint does not match the target's frame")
+        for k in cls._STATE:
+            if k in z.files and k != "params":
+                getattr(f, k).copy_(torch.from_numpy(z[k]).to(dev))
+        f.step_counter.copy_(torch.from_numpy(z["step_counter"]).to(dev))
+        return f
+
+    # -- a logged fit loop -------------------------------------------------------
+    def fit(self, steps: int, log_every: int = 100, log=None, psnr: bool = True) -> list:
+        """Run `steps` fused steps, `log_every` per CUDA-graph replay, and at
+        every log point check the device status (GI_ENONFINITE raises) and
+        record {"step", "loss", "psnr_db", "it_per_s"} -- one JSON object per
+        line to `log` (a path or a writable text file) if given (SURVEY §5:
+        PSNR, loss and it/s as JSONL; SPEC logs every 100 steps).  Returns the
+        records."""
+        import json
+        import time
+        rec, fh, own = [], None, False
+        if isinstance(log, str):
+            fh, own = open(log, "a"), True
+        elif log is not None:
+            fh = log
+        pipe = Pipeline(self.n, self.f.width, self.f.height, self.B, self.f.k, self.cap,
+                        self.device) if psnr else None
+        full, rem = divmod(int(steps), int(log_every))
+        g = self.capture(log_every) if full else None
+        try:
+            t0 = time.perf_counter()
+            for chunk in [log_every] * full + ([rem] if rem else []):
+                if chunk == log_every:
+                    g.replay()
+                else:
+                    for _ in range(chunk):
+                        self.step()
+                st = self.check()
+                if st != gi.GI_OK:
+                    raise gi.GiError(st, "Fitter.fit", "non-finite parameters or gradients")
+                t1 = time.perf_counter()
+                r = {"step": self.steps_done(), "loss": [float(x) for x in self.loss.cpu()],
+                     "it_per_s": chunk / max(t1 - t0, 1e-9)}
+                if pipe is not None:
+                    img = pipe.render_frame(self.params, self.flags)
+                    r["psnr_db"] = [float(x) for x in pipe.psnr(img, self.target).cpu()]
+                rec.append(r)
+                if fh is not None:
+                    fh.write(json.dumps(r) + "\n")
+                    fh.flush()
+                t0 = time.perf_counter()
+        finally:
+            if own:
+                fh.close()
+        return rec
+
 
 class QatFitter:
     """NEXT-2 attribute quantisation-aware fine-tuning (gi_qat_step) of one

@@ -533,3 +533,54 @@ def test_fit_trajectory_band(gi, gio, optimizer):
     start = gio.psnr(gio.render(p0, W, H, mode=gio.ALL_PAIRS), tgt)
     assert ref_psnr > start + 5.0 and gpu_psnr > start + 5.0, (start, ref_psnr, gpu_psnr)
     assert abs(gpu_psnr - ref_psnr) <= 0.1, (gpu_psnr, ref_psnr)
+
+
+# ---------------------------------------------------------------- checkpoint / log
+@pytest.mark.parametrize("optimizer", ["adam", "adan"])
+def test_checkpoint_resume_bitwise(gi, tmp_path, optimizer):
+    # save after 15 steps, resume in a new Fitter, 15 more: bitwise the 30-step fit
+    from paper_2403_08551_b200.pipeline import Fitter
+    W, H, n = 160, 120, 3000
+    p = to_dev(synth.init_params(21, n))[None].contiguous()
+    tgt = to_dev(synth.image(21, W, H))[None].contiguous()
+    a = Fitter(p.clone(), tgt, optimizer=optimizer)
+    for _ in range(30):
+        a.step()
+    b = Fitter(p.clone(), tgt, optimizer=optimizer)
+    for _ in range(15):
+        b.step()
+    path = str(tmp_path / "ckpt.npz")
+    b.save(path)
+    c = Fitter.load(path, tgt)
+    assert c.optimizer == optimizer and c.steps_done() == 15
+    for _ in range(15):
+        c.step()
+    torch.cuda.synchronize()
+    assert c.check() == gi.GI_OK
+    assert torch.equal(a.params, c.params) and torch.equal(a.m, c.m) and torch.equal(a.v, c.v)
+    assert torch.equal(a.step_counter, c.step_counter)
+    if optimizer == "adan":
+        assert torch.equal(a.n_acc, c.n_acc) and torch.equal(a.grad_prev, c.grad_prev)
+
+
+def test_fit_loop_jsonl_log(gi, tmp_path):
+    # Fitter.fit: graph replays of log_every steps, a JSON line per log point
+    # (step, loss, PSNR, it/s); the same params as stepping eagerly
+    import json
+    from paper_2403_08551_b200.pipeline import Fitter
+    W, H, n = 160, 120, 3000
+    p = to_dev(synth.init_params(22, n))[None].contiguous()
+    tgt = to_dev(synth.image(22, W, H))[None].contiguous()
+    a = Fitter(p.clone(), tgt)
+    log = tmp_path / "fit.jsonl"
+    rec = a.fit(250, log_every=100, log=str(log))
+    lines = [json.loads(x) for x in log.read_text().splitlines()]
+    assert [r["step"] for r in lines] == [100, 200, 250] == [r["step"] for r in rec]
+    assert lines[0]["loss"][0] > lines[-1]["loss"][0] > 0
+    assert lines[-1]["psnr_db"][0] > lines[0]["psnr_db"][0]
+    assert all(r["it_per_s"] > 0 for r in lines)
+    b = Fitter(p.clone(), tgt)
+    for _ in range(250):
+        b.step()
+    torch.cuda.synchronize()
+    assert torch.equal(a.params, b.params) and torch.equal(a.m, b.m)
