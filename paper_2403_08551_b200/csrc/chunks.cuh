@@ -124,6 +124,7 @@ __device__ __forceinline__ ChunkPlanOut plan_chunks_few(ChunkShared<NT>& ch, int
         F = Ffull + (Fp >> 16);
         if (j < cnt) {
             const uint32_t fstart = excl & 0xffffu, rpos = Ffull + (excl >> 16);
+            GI_ASSERT(fstart + nf <= (uint32_t)NT && (rm == 0u || rpos < (uint32_t)NT));
             for (uint32_t i = 0; i < nf; ++i)
                 ch.item[fstart + i] = (uint32_t)j | (i * C) << 8 | ((i + 1u) * C) << 17;
             if (rm != 0u) ch.item[rpos] = (uint32_t)j | (nf * C) << 8 | wj << 17;
@@ -293,7 +294,9 @@ __device__ __forceinline__ void walk_chunk(const SR& sr, uint32_t it, F&& f) {
     float cdy = fmaf(A.z, ((float)(ly0 + row) + 0.5f) - B.w, O.y);
     int p = (ly0 + row) * kTile + lx0 + col;
     const int wrap = kTile - wdt;
+    GI_ASSERT(k0 >= 0 && k0 <= k1 && k1 <= wdt * ((int)(box >> 24) - ly0 + 1));
     for (int k = k0; k < k1; ++k) {
+        GI_ASSERT(p >= 0 && p < kTilePix);
         const float u = fmaf(A.x, dx, O.x);
         const float v = fmaf(A.y, dx, cdy);
         const float w = ex2_approx(fmaf(-u, u, -(v * v)));
@@ -339,6 +342,7 @@ __device__ __forceinline__ void walk_chunk_ilv(const SR& sr, uint32_t it, F&& f)
     int p = (ly0 + row) * kTile + lx0 + col;
     const int pstep = srow * kTile + scol, wrap = kTile - wdt;
     for (int k = 0; k < cnt; ++k) {
+        GI_ASSERT(p >= 0 && p < kTilePix);
         const float u = fmaf(A.x, dx, O.x);
         const float v = fmaf(A.y, dx, cdy);
         const float w = ex2_approx(fmaf(-u, u, -(v * v)));

@@ -131,6 +131,7 @@ __device__ __forceinline__ void forward_chunks(FusedShared<NT, NB, kBwd>& sh,
     if (j >= (int)pl.n_items) return;
     const uint32_t it = sh.ch.item[j];
     const int r = (int)(it & 0xffu);
+    GI_ASSERT(r < NB);
     const float cr = sh.sr.a[r].w * pl.scale, cg = sh.sr.b[r].x * pl.scale,
                 cb = sh.sr.b[r].y * pl.scale;
     int* a0 = sh.u.acc[0];
@@ -343,6 +344,7 @@ __global__ void __launch_bounds__(NT, NT == 256 ? (kBwd ? GI_TILE3_MINB : GI_REN
                         s0.x += x.x; s0.y += x.y; s0.z += x.z; s0.w += x.w;
                         s1.x += y.x; s1.y += y.y; s1.z += y.z; s1.w += y.w;
                     };
+                    GI_ASSERT(fstart + nf <= (uint32_t)NT && (!(jp >> 27) || ((jp >> 18) & 0x1ffu) < (uint32_t)NT));
                     for (uint32_t i = 0; i < nf; ++i) add(fstart + i);
                     if (jp >> 27) add((jp >> 18) & 0x1ffu);
                     if (slot == kOffOverflow) {     // > 4-tile Gaussian without slots

@@ -10,6 +10,17 @@
 
 #include "../../include/gi.h"
 
+// GI_ASSERT: device-side bounds checks compiled in only with -DGI_DEBUG (the
+// pool's GPU boxes do not allow compute-sanitizer; the whole GPU test suite
+// is run against a -DGI_DEBUG build instead: a violated check traps the
+// kernel and fails the test).
+#ifdef GI_DEBUG
+#include <cassert>
+#define GI_ASSERT(c) assert(c)
+#else
+#define GI_ASSERT(c) ((void)0)
+#endif
+
 #if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ != 1000)
 #error "libgi is written for sm_100a only"
 #endif
@@ -236,6 +247,7 @@ __device__ __forceinline__ void count_keys(const BinCounts& bc, int g, int tx0, 
             if ((uint32_t)i < touched) {
                 const int dy = (i >= w) + (i >= 2 * w) + (i >= 3 * w);
                 t[i] = base + (ty0 + dy) * TX + tx0 + (i - dy * w);
+                GI_ASSERT(t[i] >= 0 && dy <= ty1 - ty0);
                 r[i] = atomicAdd(count_word(bc, t[i]), 1u);
             }
         }
@@ -303,8 +315,12 @@ __device__ __forceinline__ void post_project_warp(const BinCounts& bc, uint32_t 
         const int b = __shfl_sync(kFull, base, j);
         const uint32_t gid = (uint32_t)__shfl_sync(kFull, g, j);
         const uint32_t oj = __shfl_sync(kFull, off_l, j);
+#ifdef GI_DEBUG
+        const uint32_t cj = __shfl_sync(kFull, c_l, j);     // the owner's key count
+#endif
         if (f < total_w) {
             const int i = (int)(f - oj), w = tx1 - tx0 + 1;
+            GI_ASSERT(j >= 0 && j < 32 && i >= 0 && (uint32_t)i < cj);
             const int dy = i / w;
             const int t = b + (ty0 + dy) * TX + tx0 + (i - dy * w);
             const uint32_t r = atomicAdd(count_word(bc, t), 1u);

@@ -89,6 +89,7 @@ __device__ __forceinline__ TileCtx make_tile_ctx(int W, int H, int TX, int row0)
 // FMAs with the correction as addend).
 template <int NB>
 struct StagedRecordsN {
+    static constexpr int kN = NB;
     float4 a[NB];
     float4 b[NB];
     float2 o[NB];
@@ -139,6 +140,8 @@ __device__ __forceinline__ void stage_gid(SR& sr, const Proj* __restrict__ proj,
                    ? kOffOverflow
                    : off + (uint32_t)((t.ty - t.row0 - rw.z) * (rw.y - rw.x + 1) + (t.tx - rw.x));
     }
+    // a staged record overlaps the tile (its key is in the tile's list)
+    GI_ASSERT(j >= 0 && j < SR::kN && lx0 <= lx1 && ly0 <= ly1);
     sr.a[j] = make_float4(r.q1.x, r.q1.y, r.q1.z, r.q2.x);
     sr.b[j] = make_float4(r.q2.y, r.q2.z, mx, my);
     sr.o[j] = make_float2(-(r.q1.x * mx_lo), -fmaf(r.q1.y, mx_lo, r.q1.z * my_lo));
@@ -265,7 +268,10 @@ __device__ __forceinline__ int sorted_segment(const Proj* __restrict__ proj,
         __syncthreads();
 #pragma unroll
         for (int q = 0; q < E; ++q)
-            if ((int)threadIdx.x + q * NT < cnt) sl[0u - r[q]] = mine[q];
+            if ((int)threadIdx.x + q * NT < cnt) {
+                GI_ASSERT((0u - r[q]) < (uint32_t)cnt);
+                sl[0u - r[q]] = mine[q];
+            }
         __syncthreads();
         return cnt;
     }
