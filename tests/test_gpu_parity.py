@@ -1211,3 +1211,24 @@ def test_target_from_rgb8(gi):
         gi.gi_target_from_rgb8(stage, fr, out2, ready, done)
         torch.cuda.synchronize()
         assert np.array_equal(out2.cpu().numpy().view(np.uint32), ref.view(np.uint32)), (W, H, B)
+
+
+@pytest.mark.parametrize("W,H", [(32767, 40), (40, 32767)])
+def test_max_frame_dims(gi, gio, W, H):
+    # the largest frame gi_frame accepts along each axis (ragged: 32767 = 2047
+    # tiles + 15 px): 16-bit box words at their limit, 2,048 x 3 tiles (the
+    # >= 3,072-tile kernels); frame, fused fit-step gradients and loss vs the oracle
+    from paper_2403_08551_b200.pipeline import Fitter, Pipeline
+    n = 4000
+    p = synth.init_params(31, n)
+    tgt = synth.image(31, W, H)
+    ref_img, ref_loss, ref_g = gio.loss_and_grads(p, tgt, mode=gio.TILED)
+    pipe = Pipeline(n, W, H, 1, device=DEV)
+    img = pipe.render_frame(to_dev(p)[None].contiguous())[0].cpu().numpy()
+    assert np.abs(img - ref_img).max() <= PIX_TOL
+    fit = Fitter(to_dev(p)[None].contiguous(), to_dev(tgt)[None].contiguous())
+    fit.step()
+    torch.cuda.synchronize()
+    assert fit.check() == gi.GI_OK
+    assert max(group_err(fit.grads[0].cpu().numpy().astype(np.float64), ref_g).values()) <= GRAD_TOL
+    assert abs(float(fit.loss[0]) - ref_loss) <= 1e-5 * ref_loss
