@@ -59,19 +59,26 @@ struct FusedShared {
 // segment of <= NT keys (one batch) is used in slab (atomic) order -- nothing in
 // these kernels depends on the order within one batch; longer segments are
 // brought into gid order (sorted_segment) or streamed past the slab.
-template <int NT, int NB>
+template <int NT, int NB, bool kGidAhead>
 __device__ __forceinline__ Seg open_segment3(const Proj* __restrict__ proj,
                                              uint32_t* __restrict__ key_gid,
                                              const uint32_t* __restrict__ tile_range,
                                              bool presorted, const ChainState& cs, int n, int T,
                                              const TileCtx& t, uint32_t* sl, uint32_t* scratch,
-                                             uint32_t* cursor) {
+                                             uint32_t* cursor, uint32_t& gid0) {
     const int tt = t.img * T + t.tile;
     if (cs.slab != nullptr) {
         // written by the producer kernel (visible after griddepcontrol.wait);
-        // re-zeroed by thread 0 only after the CTA's last barrier
-        const uint32_t count = __ldcg(&cs.tile_count[(size_t)tt * kCountStride]);
+        // re-zeroed by thread 0 only after the CTA's last barrier.  The slab's
+        // first NB entries are read with the count, before it is known (the
+        // slab holds >= 1,024 entries; entries past the count are ignored):
+        // one memory round trip for both instead of two
         const uint32_t s = (uint32_t)tt * cs.slab_cap;
+        // (the 256-thread fit kernel reads them after the count: at its 40-
+        // register budget the early value costs a spill -- tile kernel 27.5
+        // -> 29.3 us; render 55.3k -> 56.3k FPS, C3 fit 12.5k -> 12.8k it/s)
+        if (kGidAhead && (int)threadIdx.x < NB) gid0 = __ldcg(&key_gid[s + threadIdx.x]);
+        const uint32_t count = __ldcg(&cs.tile_count[(size_t)tt * kCountStride]);
         if (count <= (uint32_t)NB && count <= cs.slab_cap) return Seg{s, count, kSegGlobal};
         if (count > cs.slab_cap) {
             if (threadIdx.x == 0) {
@@ -104,11 +111,20 @@ __device__ __forceinline__ ChunkPlanOut stage_and_plan(FusedShared<NT, NB, kBwd>
                                                        const Proj* __restrict__ proj, int n,
                                                        const TileCtx& t,
                                                        const uint32_t* __restrict__ gauss_off,
-                                                       int& cnt_out) {
+                                                       int& cnt_out, uint32_t gid0 = 0xffffffffu) {
     const int j = threadIdx.x;
     uint32_t gid = 0;
-    const int cnt = batch_gid<NT, NB>(sg, base, key_gid, sh.sl, proj, n, t, &sh.cursor, sh.scratch,
-                                      gid);
+    int cnt;
+    // slab entries read ahead (open_segment3): only for a one-batch segment
+    // used in slab order (longer ones are re-ordered by sorted_segment)
+    constexpr bool kAhead = !kBwd || NT == 128;
+    if (kAhead && base == 0 && sg.mode == kSegGlobal && sg.L <= (uint32_t)NB &&
+        gid0 != 0xffffffffu) {
+        cnt = (int)sg.L;
+        if (j < cnt) gid = gid0;
+    } else {
+        cnt = batch_gid<NT, NB>(sg, base, key_gid, sh.sl, proj, n, t, &sh.cursor, sh.scratch, gid);
+    }
     uint32_t wj = 0, cabs = 0;
     if (j < cnt) {
         stage_gid(sh.sr, proj, gid, j, t, gauss_off);
@@ -204,8 +220,10 @@ __global__ void __launch_bounds__(NT, NT == 256 ? (kBwd ? GI_TILE3_MINB : GI_REN
 #endif
     griddep_wait();
     griddep_trigger();
-    const Seg sg = open_segment3<NT, NB>(proj, key_gid, tile_range, presorted, cs, n, T, t, sh.sl,
-                                     sh.scratch, &sh.cursor);
+    uint32_t gid0 = 0xffffffffu;     // the slab's entry threadIdx.x, read with the count
+    const Seg sg = open_segment3<NT, NB, !kBwd || NT == 128>(proj, key_gid, tile_range, presorted,
+                                                             cs, n, T, t, sh.sl, sh.scratch,
+                                                             &sh.cursor, gid0);
     const uint32_t L = sg.L;
     const bool fwd = !kBwd || dL_dimage == nullptr;
     const uint32_t* goff = kBwd ? gauss_off : nullptr;
@@ -225,7 +243,7 @@ __global__ void __launch_bounds__(NT, NT == 256 ? (kBwd ? GI_TILE3_MINB : GI_REN
                 sh.u.acc[1][p] = 0;
                 sh.u.acc[2][p] = 0;
             }
-            plan = stage_and_plan<NT, NB, kBwd>(sh, sg, base, key_gid, proj, n, t, goff, cnt1);
+            plan = stage_and_plan<NT, NB, kBwd>(sh, sg, base, key_gid, proj, n, t, goff, cnt1, gid0);
             forward_chunks<NT, NB, kBwd>(sh, plan);
             __syncthreads();
 #pragma unroll
@@ -310,7 +328,8 @@ __global__ void __launch_bounds__(NT, NT == 256 ? (kBwd ? GI_TILE3_MINB : GI_REN
             int cnt = cnt1;
             ChunkPlanOut pl = plan;
             if (!(reuse && ib == 0))
-                pl = stage_and_plan<NT, NB, kBwd>(sh, sg, base, key_gid, proj, n, t, gauss_off, cnt);
+                pl = stage_and_plan<NT, NB, kBwd>(sh, sg, base, key_gid, proj, n, t, gauss_off, cnt,
+                                                  gid0);
             if (j < (int)pl.n_items) {
                 float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f, a4 = 0.f, a5 = 0.f, a6 = 0.f, a7 = 0.f;
                 walk_chunk(sh.sr, sh.ch.item[j],
