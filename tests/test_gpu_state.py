@@ -584,3 +584,42 @@ def test_fit_loop_jsonl_log(gi, tmp_path):
         b.step()
     torch.cuda.synchronize()
     assert torch.equal(a.params, b.params) and torch.equal(a.m, b.m)
+
+
+def test_streamed_8bit_target_fit(gi):
+    # the bench's e2e loop: each step's target uploaded as 8-bit RGB on a copy
+    # stream (gi_target_upload_rgb8), expanded on the compute stream
+    # (gi_target_from_rgb8), then the chained step -- bitwise a plain fit on
+    # the same (8-bit rounded) target
+    from paper_2403_08551_b200.pipeline import Fitter
+    W, H, n = 160, 120, 3000
+    p = to_dev(synth.init_params(23, n))[None].contiguous()
+    t = synth.image(23, W, H)
+    t8 = np.ascontiguousarray(np.clip(np.rint(t * 255.0), 0, 255).astype(np.uint8).transpose(1, 2, 0))
+    tq = to_dev((t8.astype(np.float32) / np.float32(255)).transpose(2, 0, 1))[None].contiguous()
+    ref = Fitter(p.clone(), tq.clone())
+    for _ in range(6):
+        ref.step()
+    host = torch.from_numpy(t8).pin_memory()
+    stage = [torch.empty(t8.shape, dtype=torch.uint8, device=DEV) for _ in range(2)]
+    ready = [torch.cuda.Event() for _ in range(2)]
+    free = [torch.cuda.Event() for _ in range(2)]
+    stream = torch.cuda.current_stream()
+    for e in ready + free:
+        e.record(stream)
+    tbuf = torch.zeros_like(tq)
+    a = Fitter(p.clone(), tbuf)
+    cs = torch.cuda.Stream()
+    cs.wait_stream(stream)
+    gi.gi_target_upload_rgb8(host, stage[0], a.f, None, ready[0], cs)
+    for i in range(6):
+        b = i & 1
+        if i + 1 < 6:
+            gi.gi_target_upload_rgb8(host, stage[b ^ 1], a.f, free[b ^ 1] if i >= 1 else None,
+                                     ready[b ^ 1], cs)
+        gi.gi_target_from_rgb8(stage[b], a.f, tbuf, ready[b], free[b], stream)
+        a.step()
+    stream.wait_stream(cs)
+    torch.cuda.synchronize()
+    assert torch.equal(tbuf, tq)
+    assert torch.equal(a.params, ref.params) and torch.equal(a.m, ref.m) and torch.equal(a.v, ref.v)
