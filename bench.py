@@ -893,14 +893,9 @@ def main():
             "clocks": clk,
             "e2e": {"value": e2e_value, "unit": "it/s",
                     "h2d_bytes_per_step": int(t8_host.nbytes), "d2h_bytes_per_step": 4,
-                    "path": "Fitter.step -> gi_fit_step_chained (C ABI, no graph): the step's "
-                            "target as an 8-bit RGB image (P:375 datasets) copied H2D from pinned "
-                            "host memory per step by gi_target_upload_rgb8 on a copy stream "
-                            "(double-buffered), expanded to fp32 by gi_target_from_rgb8 on the "
-                            "compute stream, loss written by the finalize kernel into mapped "
-                            "pinned host memory; these calls for 8 steps captured in one CUDA "
-                            "graph per replay (eager_value: the same calls issued one by one "
-                            "from Python, host-launch bound)",
+                    "path": "per step: 8-bit target H2D (gi_target_upload_rgb8, copy stream) + "
+                            "gi_target_from_rgb8 + gi_fit_step_chained + loss to mapped host "
+                            "memory; 8 steps per graph replay (DESIGN.md sec. 9)",
                     "eager_value": e2e_eager},
             "gpu_launches": int(launches_per_step * K),
             "gpu_launches_per_step": int(launches_per_step),
