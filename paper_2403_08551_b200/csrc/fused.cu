@@ -77,7 +77,8 @@ __device__ __forceinline__ Seg open_segment3(const Proj* __restrict__ proj,
         // (the 256-thread fit kernel reads them after the count: at its 40-
         // register budget the early value costs a spill -- tile kernel 27.5
         // -> 29.3 us; render 55.3k -> 56.3k FPS, C3 fit 12.5k -> 12.8k it/s)
-        if (kGidAhead && (int)threadIdx.x < NB) gid0 = __ldcg(&key_gid[s + threadIdx.x]);
+        if (kGidAhead && (int)threadIdx.x < NB && threadIdx.x < cs.slab_cap)   // inside the tile's slab
+            gid0 = __ldcg(&key_gid[s + threadIdx.x]);
         const uint32_t count = __ldcg(&cs.tile_count[(size_t)tt * kCountStride]);
         if (count <= (uint32_t)NB && count <= cs.slab_cap) return Seg{s, count, kSegGlobal};
         if (count > cs.slab_cap) {
