@@ -318,7 +318,8 @@ gi_status gi_fit_bin_view(const void* fit_ws, int32_t n, int64_t key_capacity, c
     const gi::BinCounts bc =
         gi::bin_counts_direct(w.bin_ws, n, key_capacity, *f, w.key_gid, nullptr);
     *tile_count = bc.tile_count;
-    *count_stride = (uint32_t)gi::kCountStride;
+    *count_stride = gi::count_stride_for((int64_t)gi::tiles_x(f->width) * gi::tiles_y(f->height) *
+                                         f->batch);
     *slab = w.key_gid;
     *slab_capacity = gi::slab_capacity(key_capacity, *f);
     return GI_OK;

@@ -74,11 +74,12 @@ __global__ void __launch_bounds__(1024) tile_scan_kernel(const uint32_t* __restr
     griddep_wait();
     griddep_trigger();
     const int per = (TT + blockDim.x - 1) / blockDim.x;       // consecutive items per thread
+    const uint32_t cst = count_stride_for(TT);
     const int i0 = threadIdx.x * per;
     uint32_t s = 0;
     for (int k = 0; k < per; ++k) {
         const int i = i0 + k;
-        if (i < TT) s += tile_count[(size_t)i * kCountStride] + big_count[i];
+        if (i < TT) s += tile_count[(size_t)i * cst] + big_count[i];
     }
     uint32_t x = s;
 #pragma unroll
@@ -105,7 +106,7 @@ __global__ void __launch_bounds__(1024) tile_scan_kernel(const uint32_t* __restr
         const int i = i0 + k;
         if (i < TT) {
             tile_range[i] = (int64_t)run < cap ? run : (uint32_t)cap;
-            run += tile_count[(size_t)i * kCountStride] + big_count[i];
+            run += tile_count[(size_t)i * cst] + big_count[i];
         }
     }
     if (threadIdx.x == 0) {
@@ -117,7 +118,7 @@ __global__ void __launch_bounds__(1024) tile_scan_kernel(const uint32_t* __restr
 __global__ void combine_kernel(const uint32_t* __restrict__ a, const uint32_t* __restrict__ b,
                                uint32_t* __restrict__ out, int64_t count) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < count) out[i] = a[i * kCountStride] + b[i];
+    if (i < count) out[i] = a[i * count_stride_for(count)] + b[i];
 }
 
 __global__ void clamp_kernel(uint32_t* __restrict__ v, int64_t count, int64_t cap) {
@@ -166,7 +167,7 @@ __global__ void __launch_bounds__(256) scatter_kernel(const Proj* __restrict__ p
         uint32_t sum = 0;
         for (int k = 0; k < per; ++k)
             if (i0 + k < TT) {
-                const uint32_t sm = bc.tile_count[(size_t)(i0 + k) * kCountStride];
+                const uint32_t sm = bc.tile_count[(size_t)(i0 + k) * bc.cstride];
                 small_s[i0 + k] = sm;
                 sum += sm + bc.big_count[i0 + k];
             }
@@ -221,7 +222,7 @@ __global__ void __launch_bounds__(256) scatter_kernel(const Proj* __restrict__ p
             for (int tx = q.tx0; tx <= q.tx1; ++tx) {
                 const int t = base + ty * TX + tx;
                 const uint32_t st = fuse_scan ? start_s[t] : tile_range[t];
-                const uint32_t sm = fuse_scan ? small_s[t] : bc.tile_count[(size_t)t * kCountStride];
+                const uint32_t sm = fuse_scan ? small_s[t] : bc.tile_count[(size_t)t * bc.cstride];
                 const int64_t slot = (int64_t)st + sm + atomicAdd(&fill[t], 1u);
                 if (slot < cap) {
                     key_tile[slot] = (uint32_t)t;
@@ -242,7 +243,7 @@ __global__ void __launch_bounds__(256) scatter_kernel(const Proj* __restrict__ p
         for (uint32_t i = lane; i < c; i += 32) {
             const int t = b + (ty0 + (int)i / w) * TX + tx0 + (int)i % w;
             const uint32_t st = fuse_scan ? start_s[t] : tile_range[t];
-            const uint32_t sm = fuse_scan ? small_s[t] : bc.tile_count[(size_t)t * kCountStride];
+            const uint32_t sm = fuse_scan ? small_s[t] : bc.tile_count[(size_t)t * bc.cstride];
             const int64_t slot = (int64_t)st + sm + atomicAdd(&fill[t], 1u);
             if (slot < cap) {
                 key_tile[slot] = (uint32_t)t;
@@ -290,7 +291,8 @@ BinWs carve(void* base, int n, int64_t cap, const gi_frame& f) {
     BinWs w;
     size_t off = 0;
     // tile_count (strided), big_count, fill and alloc_counter are adjacent: one memset
-    w.tile_count = reinterpret_cast<uint32_t*>(p + off); off += sizeof(uint32_t) * (size_t)TT * kCountStride;
+    w.tile_count = reinterpret_cast<uint32_t*>(p + off);
+    off += sizeof(uint32_t) * (size_t)TT * count_stride_for(TT);
     w.big_count = reinterpret_cast<uint32_t*>(p + off); off += sizeof(uint32_t) * (size_t)TT;
     w.fill = reinterpret_cast<uint32_t*>(p + off); off += sizeof(uint32_t) * (size_t)TT;
     w.alloc_counter = reinterpret_cast<uint32_t*>(p + off); off += sizeof(uint32_t);
@@ -311,7 +313,10 @@ size_t bin_ws_bytes(int n, int64_t cap, const gi_frame& f) { return carve(nullpt
 
 BinCounts bin_counts(void* ws, int n, int64_t cap, const gi_frame& f) {
     BinWs w = carve(ws, n, cap, f);
-    return BinCounts{w.tile_count, w.big_count, w.key_rank, nullptr, 0u, nullptr, nullptr, nullptr, 0u};
+    const int64_t TT = (int64_t)tiles_x(f.width) * tiles_y(f.height) * f.batch;
+    BinCounts bc{w.tile_count, w.big_count, w.key_rank, nullptr, 0u, nullptr, nullptr, nullptr, 0u};
+    bc.cstride = count_stride_for(TT);
+    return bc;
 }
 
 uint32_t slab_min() {
@@ -342,9 +347,11 @@ BinCounts bin_counts_direct(void* ws, int n, int64_t cap, const gi_frame& f, uin
                             uint32_t* gauss_off) {
     BinWs w = carve(ws, n, cap, f);
     const int64_t pc = partial_cap(n, cap, f);
-    return BinCounts{w.tile_count, w.big_count, w.key_rank, slab, slab_capacity(cap, f),
-                     w.n_keys_acc, gauss_off, gauss_off ? w.alloc_counter : nullptr,
-                     (uint32_t)(pc < 0xffffffffll ? pc : 0xffffffffll)};
+    BinCounts bc{w.tile_count, w.big_count, w.key_rank, slab, slab_capacity(cap, f),
+                 w.n_keys_acc, gauss_off, gauss_off ? w.alloc_counter : nullptr,
+                 (uint32_t)(pc < 0xffffffffll ? pc : 0xffffffffll)};
+    bc.cstride = count_stride_for((int64_t)tiles_x(f.width) * tiles_y(f.height) * f.batch);
+    return bc;
 }
 
 ChainState bin_chain_direct(void* ws, int n, int64_t cap, const gi_frame& f, uint32_t* slab,
@@ -352,6 +359,7 @@ ChainState bin_chain_direct(void* ws, int n, int64_t cap, const gi_frame& f, uin
     BinWs w = carve(ws, n, cap, f);
     ChainState cs{};
     cs.tile_count = w.tile_count;
+    cs.cstride = count_stride_for((int64_t)tiles_x(f.width) * tiles_y(f.height) * f.batch);
     cs.alloc_counter = w.alloc_counter;
     cs.gauss_off = gauss_off;
     cs.slab = slab;
@@ -371,7 +379,7 @@ cudaError_t bin_clear(void* ws, int n, int64_t cap, const gi_frame& f, cudaStrea
     BinWs w = carve(ws, n, cap, f);
     const size_t TT = (size_t)tiles_x(f.width) * tiles_y(f.height) * f.batch;
     // tile_count .. n_keys_acc, seg_stats: adjacent
-    return cudaMemsetAsync(w.tile_count, 0, sizeof(uint32_t) * ((kCountStride + 2) * TT + 4), s);
+    return cudaMemsetAsync(w.tile_count, 0, sizeof(uint32_t) * ((count_stride_for(TT) + 2) * TT + 4), s);
 }
 
 cudaError_t launch_bin(const Proj* proj, const uint32_t* tiles_touched, int n, const gi_frame& f,

@@ -79,7 +79,7 @@ __device__ __forceinline__ Seg open_segment3(const Proj* __restrict__ proj,
         // -> 29.3 us; render 55.3k -> 56.3k FPS, C3 fit 12.5k -> 12.8k it/s)
         if (kGidAhead && (int)threadIdx.x < NB && threadIdx.x < cs.slab_cap)   // inside the tile's slab
             gid0 = __ldcg(&key_gid[s + threadIdx.x]);
-        const uint32_t count = __ldcg(&cs.tile_count[(size_t)tt * kCountStride]);
+        const uint32_t count = __ldcg(&cs.tile_count[(size_t)tt * cs.cstride]);
         if (count <= (uint32_t)NB && count <= cs.slab_cap) return Seg{s, count, kSegGlobal};
         if (count > cs.slab_cap) {
             if (threadIdx.x == 0) {
@@ -210,7 +210,7 @@ __global__ void __launch_bounds__(NT, NT == 256 ? (kBwd ? GI_TILE3_MINB : GI_REN
 #ifndef GI_NO_TILE3_PREFETCH
     if (cs.slab != nullptr && j < 5) {
         const size_t tt = (size_t)t.img * T + t.tile;
-        if (j == 4) prefetch_l2(&cs.tile_count[tt * kCountStride]);
+        if (j == 4) prefetch_l2(&cs.tile_count[tt * cs.cstride]);
         else prefetch_l2(key_gid + tt * cs.slab_cap + 32 * j);
     }
     if (kBwd && target != nullptr && dL_dimage == nullptr && j >= 32 && j < 32 + 3 * kTile) {

@@ -351,7 +351,7 @@ __device__ __forceinline__ Seg open_segment(const Proj* __restrict__ proj,
     if (cs.slab != nullptr) {
         // written by the producer kernel (visible after griddepcontrol.wait);
         // re-zeroed by thread 0 only after the CTA's last barrier
-        const uint32_t count = __ldcg(&cs.tile_count[(size_t)tt * kCountStride]);
+        const uint32_t count = __ldcg(&cs.tile_count[(size_t)tt * cs.cstride]);
         const uint32_t s = (uint32_t)tt * cs.slab_cap;
         if (count > cs.slab_cap) {
             if (threadIdx.x == 0) {
@@ -379,7 +379,7 @@ __device__ __forceinline__ Seg open_segment(const Proj* __restrict__ proj,
 // step counter.  The next kernel runs after this grid completes.
 __device__ __forceinline__ void close_segment(const ChainState& cs, int tt) {
     if (threadIdx.x != 0 || cs.slab == nullptr) return;
-    cs.tile_count[(size_t)tt * kCountStride] = 0u;
+    cs.tile_count[(size_t)tt * cs.cstride] = 0u;
     if (tt == 0) {
         if (cs.n_keys != nullptr) {
             *cs.n_keys = *cs.n_keys_acc;
