@@ -304,8 +304,8 @@ gi_status gi_render_frame(const float* params, int32_t n, const gi_frame* f, uin
 
 /* Direct-binning state inside fit_ws (inspection, e.g. parity tests): after
  * gi_fit_prime or a chained step, image b's tile t (global tile g = b*T + t)
- * holds tile_count[g * count_stride] keys (count_stride: 32 u32 below 3,072
- * tiles per launch, else 8 -- the counters' L2 spread); the first min(count, slab_capacity)
+ * holds tile_count[g * count_stride] keys (the fit paths' layout; the frame
+ * entry points space the counters 4x wider below 3,072 tiles per launch); the first min(count, slab_capacity)
  * gids are slab[g * slab_capacity + 0 ..) in atomic (unordered) order; a
  * tile with more keys streams them from all Gaussians of its image.  Device
  * pointers into fit_ws; nothing is launched.  GI_EINVAL on bad arguments. */

@@ -319,7 +319,7 @@ gi_status gi_fit_bin_view(const void* fit_ws, int32_t n, int64_t key_capacity, c
         gi::bin_counts_direct(w.bin_ws, n, key_capacity, *f, w.key_gid, nullptr);
     *tile_count = bc.tile_count;
     *count_stride = gi::count_stride_for((int64_t)gi::tiles_x(f->width) * gi::tiles_y(f->height) *
-                                         f->batch);
+                                         f->batch);   // the fit paths' layout
     *slab = w.key_gid;
     *slab_capacity = gi::slab_capacity(key_capacity, *f);
     return GI_OK;
@@ -596,10 +596,11 @@ gi_status gi_render_frame(const float* params, int32_t n, const gi_frame* f, uin
 #define GI_TRY(expr, where) \
     if ((e = (expr)) != cudaSuccess) return cuda_status(e, where)
     const gi::ChainState cs = gi::bin_chain_direct(w.bin_ws, n, key_capacity, *f, w.key_gid, nullptr,
-                                                   w.n_keys, nullptr);
+                                                   w.n_keys, nullptr, true);
     GI_TRY(gi::launch_project(params, n, *f, flags, w.proj, w.touched,
                               gi::ProjectFuse{nullptr, gi::bin_counts_direct(w.bin_ws, n, key_capacity,
-                                                                             *f, w.key_gid, nullptr)},
+                                                                             *f, w.key_gid, nullptr,
+                                                                             true)},
                               s),
            "gi_render_frame/project");
     GI_TRY(gi::launch_render(w.proj, w.key_gid, nullptr, n, *f, false, image, cs, s),
@@ -681,11 +682,11 @@ gi_status gi_decode_render_frame(const uint8_t* payload, size_t payload_bytes,
 #define GI_TRY(expr, where) \
     if ((e = (expr)) != cudaSuccess) return cuda_status(e, where)
     const gi::ChainState cs = gi::bin_chain_direct(w.bin_ws, n, key_capacity, *f, w.key_gid, nullptr,
-                                                   w.n_keys, nullptr);
+                                                   w.n_keys, nullptr, true);
     GI_TRY(gi::launch_decode_project(payload, *meta, params, *f, w.proj, w.touched,
                                      gi::ProjectFuse{nullptr, gi::bin_counts_direct(
                                                                   w.bin_ws, n, key_capacity, *f,
-                                                                  w.key_gid, nullptr)},
+                                                                  w.key_gid, nullptr, true)},
                                      s),
            "gi_decode_render_frame/decode+project");
     GI_TRY(gi::launch_render(w.proj, w.key_gid, nullptr, n, *f, false, image, cs, s),

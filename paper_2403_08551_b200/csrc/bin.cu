@@ -292,7 +292,7 @@ BinWs carve(void* base, int n, int64_t cap, const gi_frame& f) {
     size_t off = 0;
     // tile_count (strided), big_count, fill and alloc_counter are adjacent: one memset
     w.tile_count = reinterpret_cast<uint32_t*>(p + off);
-    off += sizeof(uint32_t) * (size_t)TT * count_stride_for(TT);
+    off += sizeof(uint32_t) * (size_t)TT * count_alloc_stride(TT);
     w.big_count = reinterpret_cast<uint32_t*>(p + off); off += sizeof(uint32_t) * (size_t)TT;
     w.fill = reinterpret_cast<uint32_t*>(p + off); off += sizeof(uint32_t) * (size_t)TT;
     w.alloc_counter = reinterpret_cast<uint32_t*>(p + off); off += sizeof(uint32_t);
@@ -344,22 +344,23 @@ uint32_t* bin_seg_stats(void* ws, int n, int64_t cap, const gi_frame& f) {
 }
 
 BinCounts bin_counts_direct(void* ws, int n, int64_t cap, const gi_frame& f, uint32_t* slab,
-                            uint32_t* gauss_off) {
+                            uint32_t* gauss_off, bool frame) {
     BinWs w = carve(ws, n, cap, f);
     const int64_t pc = partial_cap(n, cap, f);
     BinCounts bc{w.tile_count, w.big_count, w.key_rank, slab, slab_capacity(cap, f),
                  w.n_keys_acc, gauss_off, gauss_off ? w.alloc_counter : nullptr,
                  (uint32_t)(pc < 0xffffffffll ? pc : 0xffffffffll)};
-    bc.cstride = count_stride_for((int64_t)tiles_x(f.width) * tiles_y(f.height) * f.batch);
+    bc.cstride = count_stride_for((int64_t)tiles_x(f.width) * tiles_y(f.height) * f.batch, frame);
     return bc;
 }
 
 ChainState bin_chain_direct(void* ws, int n, int64_t cap, const gi_frame& f, uint32_t* slab,
-                            uint32_t* gauss_off, uint32_t* n_keys, uint32_t* step_counter) {
+                            uint32_t* gauss_off, uint32_t* n_keys, uint32_t* step_counter,
+                            bool frame) {
     BinWs w = carve(ws, n, cap, f);
     ChainState cs{};
     cs.tile_count = w.tile_count;
-    cs.cstride = count_stride_for((int64_t)tiles_x(f.width) * tiles_y(f.height) * f.batch);
+    cs.cstride = count_stride_for((int64_t)tiles_x(f.width) * tiles_y(f.height) * f.batch, frame);
     cs.alloc_counter = w.alloc_counter;
     cs.gauss_off = gauss_off;
     cs.slab = slab;
@@ -379,7 +380,7 @@ cudaError_t bin_clear(void* ws, int n, int64_t cap, const gi_frame& f, cudaStrea
     BinWs w = carve(ws, n, cap, f);
     const size_t TT = (size_t)tiles_x(f.width) * tiles_y(f.height) * f.batch;
     // tile_count .. n_keys_acc, seg_stats: adjacent
-    return cudaMemsetAsync(w.tile_count, 0, sizeof(uint32_t) * ((count_stride_for(TT) + 2) * TT + 4), s);
+    return cudaMemsetAsync(w.tile_count, 0, sizeof(uint32_t) * ((count_alloc_stride(TT) + 2) * TT + 4), s);
 }
 
 cudaError_t launch_bin(const Proj* proj, const uint32_t* tiles_touched, int n, const gi_frame& f,

@@ -196,16 +196,22 @@ int64_t g_launches_get();
 #define GI_COUNT_STRIDE 8
 #endif
 constexpr int kCountStride = GI_COUNT_STRIDE;
-// Launches of fewer than kCountStrideWideTiles tiles (one C2-sized image) put
-// the words 128 B apart instead: the few thousand counters then spread over
-// more L2 slices (C2 frame 56.2k -> 58.0k FPS, decode +3 %); larger launches
-// keep 32 B (C3 frame -4.7 % at 128 B: the wider table)
+// The frame paths (gi_render_frame, gi_decode_render_frame) on launches of
+// fewer than kCountStrideWideTiles tiles (one C2-sized image) put the words
+// 128 B apart instead: the few thousand counters then spread over more L2
+// slices (C2 frame 56.2k -> 57.7k FPS, decode +2.7 %); the fit paths keep 32 B
+// (-0.5 % at 128 B) and so do larger launches (C3 frame -4.7 % at 128 B).
+// The workspace always has room for the wide layout, so both index the same
+// allocation and the zero-fill rule is unchanged.
 #ifndef GI_COUNT_STRIDE_WIDE
 #define GI_COUNT_STRIDE_WIDE 32
 #endif
 constexpr int64_t kCountStrideWideTiles = 3072;
-__host__ __device__ inline uint32_t count_stride_for(int64_t tiles) {
+__host__ __device__ inline uint32_t count_alloc_stride(int64_t tiles) {
     return tiles < kCountStrideWideTiles ? (uint32_t)GI_COUNT_STRIDE_WIDE : (uint32_t)kCountStride;
+}
+__host__ __device__ inline uint32_t count_stride_for(int64_t tiles, bool frame = false) {
+    return frame ? count_alloc_stride(tiles) : (uint32_t)kCountStride;
 }
 
 struct BinCounts {
@@ -467,10 +473,12 @@ cudaError_t launch_fused_render(const Proj* proj, uint32_t* key_gid, const uint3
 uint32_t slab_capacity(int64_t cap, const gi_frame& f);
 size_t slab_words(int64_t cap, const gi_frame& f);
 uint32_t* bin_seg_stats(void* ws, int n, int64_t cap, const gi_frame& f);
+// frame: the gi_render_frame / gi_decode_render_frame count layout (count_stride_for)
 BinCounts bin_counts_direct(void* ws, int n, int64_t cap, const gi_frame& f, uint32_t* slab,
-                            uint32_t* gauss_off);
+                            uint32_t* gauss_off, bool frame = false);
 ChainState bin_chain_direct(void* ws, int n, int64_t cap, const gi_frame& f, uint32_t* slab,
-                            uint32_t* gauss_off, uint32_t* n_keys, uint32_t* step_counter);
+                            uint32_t* gauss_off, uint32_t* n_keys, uint32_t* step_counter,
+                            bool frame = false);
 uint32_t* bin_alloc_counter(void* ws, int n, int64_t cap, const gi_frame& f);
 cudaError_t bin_clear(void* ws, int n, int64_t cap, const gi_frame& f, cudaStream_t s);
 cudaError_t launch_render(const Proj* proj, uint32_t* key_gid, const uint32_t* tile_range, int n,
