@@ -426,7 +426,7 @@ static gi_status fit_step_impl(float* params, float* grads, float* m, float* v, 
     fa.k = f->k;
     fa.pos_flags = flags;
     GI_TRY(gi::launch_backward_finalize(params, w.proj, n, *f, flags, true, key_capacity, w.bwd_ws,
-                                        grads, loss, &fa, s, 0, 0, w.touched),
+                                        grads, loss, &fa, s),
            "gi_fit_step/finalize+adam");
     GI_TRY(record_stage(stage_events, 4, s), "gi_fit_step/event");
     GI_TRY(record_stage(stage_events, 5, s), "gi_fit_step/event");
@@ -483,7 +483,7 @@ gi_status gi_fit_grads(const float* params, float* grads, const float* target, i
                                          key_capacity, w.bwd_ws, nullptr, cs, s),
                "gi_fit_grads/backward");
     GI_TRY(gi::launch_backward_finalize(params, w.proj, n, *f, flags, true, key_capacity, w.bwd_ws,
-                                        grads, loss, nullptr, s, r0, r1, w.touched),
+                                        grads, loss, nullptr, s, r0, r1),
            "gi_fit_grads/finalize");
 #undef GI_TRY
     return GI_OK;

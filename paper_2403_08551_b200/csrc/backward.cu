@@ -773,7 +773,6 @@ __device__ __noinline__ Sums8 sum_slots(const float4* __restrict__ pp, uint32_t 
 struct FinArgs {
     const float4* params;
     const Proj* proj;          // this step's records (the chained step rewrites proj[g] in place)
-    const uint32_t* touched;   // the projection's tiles_touched (same window) or null: box words
     const uint32_t* gauss_off;
     int total, n_per_image, W, H;
     uint32_t flags;
@@ -796,21 +795,14 @@ __device__ __forceinline__ void finalize_one(int g, bool live, const FinArgs& a,
     const uint32_t flags = a.flags;
     // independent loads first (their latency overlaps the partial-sum chain)
     float4 p0 = make_float4(0.f, 0.f, 0.f, 0.f), p1 = p0, m0 = p0, m1 = p0, v0 = p0, v1 = p0;
-    // the Gaussian's tile count: from the projection's tiles_touched (4 B,
-    // coalesced; the fused fit paths) or else from the record's box words
-    // (two 32-B sectors)
-    uint32_t bx = 0u, by = 0u, tw = 0u;
+    uint32_t bx = 0u, by = 0u;     // the record's box words: all finalize needs of it
     const float4* pp = reinterpret_cast<const float4*>(a.partial);
     if (live) {
         p0 = a.params[2 * (size_t)g];
         p1 = a.params[2 * (size_t)g + 1];
-        if (a.touched != nullptr) {
-            tw = a.touched[g];
-        } else {
-            const uint32_t* rw = reinterpret_cast<const uint32_t*>(a.proj + g);
-            bx = rw[7];             // q1.w: x0 | x1 << 16
-            by = rw[11];            // q2.w: y0 | y1 << 16
-        }
+        const uint32_t* rw = reinterpret_cast<const uint32_t*>(a.proj + g);
+        bx = rw[7];                 // q1.w: x0 | x1 << 16
+        by = rw[11];                // q2.w: y0 | y1 << 16
         if (adam.m != nullptr) {
             const float4* mm = reinterpret_cast<const float4*>(adam.m) + 2 * (size_t)g;
             const float4* vv = reinterpret_cast<const float4*>(adam.v) + 2 * (size_t)g;
@@ -828,21 +820,15 @@ __device__ __forceinline__ void finalize_one(int g, bool live, const FinArgs& a,
     uint32_t touched = 0;
     int4 rect = make_int4(0, -1, 0, -1);
     if (live) {
+        const int x0 = (int)(bx & 0xffffu), x1 = (int)(bx >> 16);
+        const int y0 = (int)(by & 0xffffu), y1 = (int)(by >> 16);
         float S[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
         bool any = false;
         // tiles of the (window-clipped, NEXT-4) rectangle
-        uint32_t cnt;
-        if (a.touched != nullptr) {
-            cnt = tw;                // the projection's count, the same window
-        } else {
-            const int x0 = (int)(bx & 0xffffu), x1 = (int)(bx >> 16);
-            const int y0 = (int)(by & 0xffffu), y1 = (int)(by >> 16);
-            cnt = x0 <= x1 && y0 <= y1
-                ? rect_area(window_rect(make_int4(x0 / kTile, x1 / kTile, y0 / kTile, y1 / kTile),
-                                        a.row0, a.row1))
-                : 0u;
-        }
-        if (cnt > 0u) {
+        const uint32_t cnt =
+            rect_area(window_rect(make_int4(x0 / kTile, x1 / kTile, y0 / kTile, y1 / kTile), a.row0,
+                                  a.row1));
+        if (x0 <= x1 && y0 <= y1 && cnt > 0u) {
             auto add = [&](const float4 u, const float4 w) {
                 S[0] += u.x; S[1] += u.y; S[2] += u.z; S[3] += u.w;
                 S[4] += w.x; S[5] += w.y; S[6] += w.z; S[7] += w.w;
@@ -1142,7 +1128,7 @@ cudaError_t launch_backward_tiles(const Proj* proj, uint32_t* key_gid, const uin
 cudaError_t launch_backward_finalize(const float* params, const Proj* proj, int n,
                                      const gi_frame& f, uint32_t flags, bool mse, int64_t cap,
                                      void* ws, float* grads, float* loss, const FusedAdam* adam,
-                                     cudaStream_t s, int row0, int row1, const uint32_t* touched) {
+                                     cudaStream_t s, int row0, int row1) {
     BwdWs w = carve(ws, n, cap, f);
     const double count = 3.0 * (double)f.width * (double)f.height;
     const int total = n * f.batch;
@@ -1150,8 +1136,7 @@ cudaError_t launch_backward_finalize(const float* params, const Proj* proj, int 
     if (total > 0) {
         FusedAdam fa{};
         if (adam) fa = *adam;
-        FinArgs fa_args{reinterpret_cast<const float4*>(params), proj, touched,
-                        (const uint32_t*)w.gauss_off,
+        FinArgs fa_args{reinterpret_cast<const float4*>(params), proj, (const uint32_t*)w.gauss_off,
                         total, n, f.width, f.height, flags, partial_cap(n, cap, f),
                         (const float*)w.partial, w.ovf, reinterpret_cast<float4*>(grads), fa, row0,
                         row1 > 0 ? row1 : tiles_y(f.height)};

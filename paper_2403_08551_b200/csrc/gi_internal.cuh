@@ -525,8 +525,7 @@ struct FusedAdam {
 cudaError_t launch_backward_finalize(const float* params, const Proj* proj, int n,
                                      const gi_frame& f, uint32_t flags, bool mse, int64_t cap,
                                      void* ws, float* grads, float* loss, const FusedAdam* adam,
-                                     cudaStream_t s, int row0 = 0, int row1 = 0,
-                                     const uint32_t* touched = nullptr);
+                                     cudaStream_t s, int row0 = 0, int row1 = 0);
 cudaError_t launch_adam(float* params, const float* grads, float* m, float* v, int64_t count,
                         int step, const uint32_t* step_dev, float lr, int half_every, float b1,
                         float b2, float eps, uint32_t* flag, cudaStream_t s);
