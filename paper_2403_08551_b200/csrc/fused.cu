@@ -59,7 +59,7 @@ struct FusedShared {
 // segment of <= NT keys (one batch) is used in slab (atomic) order -- nothing in
 // these kernels depends on the order within one batch; longer segments are
 // brought into gid order (sorted_segment) or streamed past the slab.
-template <int NT, int NB, bool kGidAhead>
+template <int NT, int NB, bool kGidAhead, bool kFit>
 __device__ __forceinline__ Seg open_segment3(const Proj* __restrict__ proj,
                                              uint32_t* __restrict__ key_gid,
                                              const uint32_t* __restrict__ tile_range,
@@ -79,7 +79,9 @@ __device__ __forceinline__ Seg open_segment3(const Proj* __restrict__ proj,
         // -> 29.3 us; render 55.3k -> 56.3k FPS, C3 fit 12.5k -> 12.8k it/s)
         if (kGidAhead && (int)threadIdx.x < NB && threadIdx.x < cs.slab_cap)   // inside the tile's slab
             gid0 = __ldcg(&key_gid[s + threadIdx.x]);
-        const uint32_t count = __ldcg(&cs.tile_count[(size_t)tt * cs.cstride]);
+        // the fit paths always use the narrow count layout (count_stride_for)
+        const uint32_t cst = kFit ? (uint32_t)kCountStride : cs.cstride;
+        const uint32_t count = __ldcg(&cs.tile_count[(size_t)tt * cst]);
         if (count <= (uint32_t)NB && count <= cs.slab_cap) return Seg{s, count, kSegGlobal};
         if (count > cs.slab_cap) {
             if (threadIdx.x == 0) {
@@ -210,7 +212,7 @@ __global__ void __launch_bounds__(NT, NT == 256 ? (kBwd ? GI_TILE3_MINB : GI_REN
 #ifndef GI_NO_TILE3_PREFETCH
     if (cs.slab != nullptr && j < 5) {
         const size_t tt = (size_t)t.img * T + t.tile;
-        if (j == 4) prefetch_l2(&cs.tile_count[tt * cs.cstride]);
+        if (j == 4) prefetch_l2(&cs.tile_count[tt * (kBwd ? (uint32_t)kCountStride : cs.cstride)]);
         else prefetch_l2(key_gid + tt * cs.slab_cap + 32 * j);
     }
     if (kBwd && target != nullptr && dL_dimage == nullptr && j >= 32 && j < 32 + 3 * kTile) {
@@ -222,7 +224,7 @@ __global__ void __launch_bounds__(NT, NT == 256 ? (kBwd ? GI_TILE3_MINB : GI_REN
     griddep_wait();
     griddep_trigger();
     uint32_t gid0 = 0xffffffffu;     // the slab's entry threadIdx.x, read with the count
-    const Seg sg = open_segment3<NT, NB, !kBwd || NT == 128>(proj, key_gid, tile_range, presorted,
+    const Seg sg = open_segment3<NT, NB, !kBwd || NT == 128, kBwd>(proj, key_gid, tile_range, presorted,
                                                              cs, n, T, t, sh.sl, sh.scratch,
                                                              &sh.cursor, gid0);
     const uint32_t L = sg.L;
