@@ -990,8 +990,11 @@ __device__ __forceinline__ void finalize_one(int g, bool live, const FinArgs& a,
 }
 
 template <bool kAdan>
+// 256 threads per CTA: 274 CTAs on one C2 image instead of 547; in the
+// pipelined step (PDL behind the tile kernel) fit 32.5k -> 33.4k it/s
+// (flushed per replay 27.2k -> 28.5k); 128 and 512 measured lower
 #ifndef GI_FIN_THREADS
-#define GI_FIN_THREADS 128
+#define GI_FIN_THREADS 256
 #endif
 __global__ void __launch_bounds__(GI_FIN_THREADS) finalize_kernel(FinArgs a,
                                                        unsigned long long* __restrict__ sse_acc,
