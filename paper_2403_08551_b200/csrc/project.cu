@@ -23,7 +23,10 @@ namespace {
 // g of the codec payload (decode_one, codebooks staged in dynamic shared
 // memory) instead of a load -- a6 and a1 in one pass, no parameter round trip.
 template <bool kDecode>
-__global__ void __launch_bounds__(256) project_kernel(const float4* __restrict__ params, int n,
+#ifndef GI_PROJ_THREADS
+#define GI_PROJ_THREADS 256
+#endif
+__global__ void __launch_bounds__(GI_PROJ_THREADS) project_kernel(const float4* __restrict__ params, int n,
                                                       int total, int W, int H, float k,
                                                       uint32_t flags, Proj* __restrict__ proj,
                                                       uint32_t* __restrict__ tiles_touched,
@@ -70,9 +73,9 @@ cudaError_t launch_project(const float* params, int n, const gi_frame& f, uint32
                            Proj* proj, uint32_t* tiles_touched, const ProjectFuse& fuse,
                            cudaStream_t s) {
     const int total = n * f.batch;
-    const int blocks = (total + 255) / 256;
+    const int blocks = (total + GI_PROJ_THREADS - 1) / GI_PROJ_THREADS;
     if (blocks == 0 && fuse.step_counter == nullptr) return cudaSuccess;
-    launch_pdl(project_kernel<false>, dim3(blocks > 0 ? blocks : 1), dim3(256), s,
+    launch_pdl(project_kernel<false>, dim3(blocks > 0 ? blocks : 1), dim3(GI_PROJ_THREADS), s,
                reinterpret_cast<const float4*>(params), n, total, f.width, f.height, f.k, flags, proj,
                tiles_touched, fuse, DecodeSrc{});
     note_launches(1);
@@ -83,7 +86,7 @@ cudaError_t launch_decode_project(const uint8_t* payload, const gi_codec_meta& m
                                   float* params_out, const gi_frame& f, Proj* proj,
                                   uint32_t* tiles_touched, const ProjectFuse& fuse, cudaStream_t s) {
     const int n = meta.n;
-    const int blocks = (n + 255) / 256;
+    const int blocks = (n + GI_PROJ_THREADS - 1) / GI_PROJ_THREADS;
     if (blocks == 0) return cudaSuccess;
     int ib = 1;
     while ((1 << ib) < meta.codebook) ++ib;
@@ -93,7 +96,7 @@ cudaError_t launch_decode_project(const uint8_t* payload, const gi_codec_meta& m
                               {meta.beta[0], meta.beta[1], meta.beta[2]}},
                   reinterpret_cast<float4*>(params_out)};
     const size_t smem = (size_t)meta.stages * meta.codebook * 3 * sizeof(float);
-    launch_pdl_smem(project_kernel<true>, dim3(blocks), dim3(256), smem, s,
+    launch_pdl_smem(project_kernel<true>, dim3(blocks), dim3(GI_PROJ_THREADS), smem, s,
                     static_cast<const float4*>(nullptr), n, n, f.width, f.height, f.k,
                     (uint32_t)GI_POS_NORMALIZED, proj, tiles_touched, fuse, dec);
     note_launches(1);
