@@ -689,7 +689,7 @@ gi_status gi_decode_render_frame(const uint8_t* payload, size_t payload_bytes,
                                                                   w.key_gid, nullptr, true)},
                                      s),
            "gi_decode_render_frame/decode+project");
-    GI_TRY(gi::launch_render(w.proj, w.key_gid, nullptr, n, *f, false, image, cs, s),
+    GI_TRY(gi::launch_render(w.proj, w.key_gid, nullptr, n, *f, false, image, cs, s, true),
            "gi_decode_render_frame/render");
 #undef GI_TRY
     return GI_OK;

@@ -469,7 +469,7 @@ cudaError_t launch_fused_backward(const Proj* proj, uint32_t* key_gid, const uin
                                   const ChainState& cs, cudaStream_t s);
 cudaError_t launch_fused_render(const Proj* proj, uint32_t* key_gid, const uint32_t* tile_range,
                                 int n, const gi_frame& f, bool presorted, float* image,
-                                const ChainState& cs, cudaStream_t s);
+                                const ChainState& cs, cudaStream_t s, bool decode = false);
 uint32_t slab_capacity(int64_t cap, const gi_frame& f);
 size_t slab_words(int64_t cap, const gi_frame& f);
 uint32_t* bin_seg_stats(void* ws, int n, int64_t cap, const gi_frame& f);
@@ -483,7 +483,7 @@ uint32_t* bin_alloc_counter(void* ws, int n, int64_t cap, const gi_frame& f);
 cudaError_t bin_clear(void* ws, int n, int64_t cap, const gi_frame& f, cudaStream_t s);
 cudaError_t launch_render(const Proj* proj, uint32_t* key_gid, const uint32_t* tile_range, int n,
                           const gi_frame& f, bool presorted, float* image, const ChainState& cs,
-                          cudaStream_t s);
+                          cudaStream_t s, bool decode = false);
 size_t backward_ws_bytes(int n, int64_t cap, const gi_frame& f);
 cudaError_t launch_backward(const float* params, const Proj* proj, const uint32_t* key_gid,
                             const uint32_t* tile_range, int n, const gi_frame& f, uint32_t flags,

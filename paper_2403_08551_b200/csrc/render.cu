@@ -180,13 +180,13 @@ bool use_render2() {
 
 cudaError_t launch_render(const Proj* proj, uint32_t* key_gid, const uint32_t* tile_range, int n,
                           const gi_frame& f, bool presorted, float* image, const ChainState& cs,
-                          cudaStream_t s) {
+                          cudaStream_t s, bool decode) {
     const int TX = tiles_x(f.width);
     const int rows = cs.row1 > 0 ? cs.row1 - cs.row0 : tiles_y(f.height);   // NEXT-4 window
     const int T = TX * rows;
     if (rows <= 0) return cudaSuccess;
     if (use_render3(T * f.batch, n, T))   // Gaussian-parallel forward (fused.cu)
-        return launch_fused_render(proj, key_gid, tile_range, n, f, presorted, image, cs, s);
+        return launch_fused_render(proj, key_gid, tile_range, n, f, presorted, image, cs, s, decode);
     cudaError_t e = use_render2()
         ? launch_pdl(render2_kernel, dim3(TX, rows, f.batch), dim3(128), s, proj, key_gid,
                      tile_range, n, f.width, f.height, T, TX, presorted, image, cs)
