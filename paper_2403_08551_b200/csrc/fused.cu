@@ -168,8 +168,11 @@ __device__ __forceinline__ void forward_chunks(FusedShared<NT, NB, kBwd>& sh,
 #ifndef GI_TILE3_MINB
 #define GI_TILE3_MINB 6
 #endif
+// 128-thread fit kernel (launches of >= 3,072 tiles): 8 CTAs per SM, 64
+// registers (10 -> 48 registers: 64 C2 images 42.5k -> 45.9k image-it/s,
+// C3 fit 12.5k -> 12.8k it/s at 8; 6 / 7 measured lower)
 #ifndef GI_TILE3_MINB128
-#define GI_TILE3_MINB128 10
+#define GI_TILE3_MINB128 8
 #endif
 #ifndef GI_RENDER3_MINB
 #define GI_RENDER3_MINB 6
