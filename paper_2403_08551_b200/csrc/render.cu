@@ -66,8 +66,10 @@ __global__ void __launch_bounds__(256, GI_RENDER_MINB) render_kernel(const Proj*
 // 21.2k -> 24.4k FPS) and on long segments (fitted proxy, decoded clouds);
 // 8x8 culling evaluates more lane-pairs than 8x4, which evens it out at the
 // C2 init scale.
+// 12 CTAs per SM (40 registers; was 9 / 56): C3 frame 24.4k -> 25.7k FPS,
+// 64-image frames -0.7 %
 #ifndef GI_RENDER2_MINB
-#define GI_RENDER2_MINB 9
+#define GI_RENDER2_MINB 12
 #endif
 constexpr int kSortMaxR2 = 1024;     // 4 KB sort buffer; longer segments are rebuilt in order
 struct Render2Shared {
