@@ -1143,13 +1143,14 @@ cudaError_t launch_backward_finalize(const float* params, const Proj* proj, int 
                         total, n, f.width, f.height, flags, partial_cap(n, cap, f),
                         (const float*)w.partial, w.ovf, reinterpret_cast<float4*>(grads), fa, row0,
                         row1 > 0 ? row1 : tiles_y(f.height)};
+        // 128-thread CTAs on launches of >= 3,072 tiles (64 C2 images +1 %)
+        const int ft = (int64_t)tiles_x(f.width) * tiles_y(f.height) * f.batch >= 3072
+                           ? 128 : GI_FIN_THREADS;
         if (adam != nullptr && adam->n != nullptr)
-            e = launch_pdl(finalize_kernel<true>, dim3((total + GI_FIN_THREADS - 1) / GI_FIN_THREADS),
-                           dim3(GI_FIN_THREADS), s, fa_args,
+            e = launch_pdl(finalize_kernel<true>, dim3((total + ft - 1) / ft), dim3(ft), s, fa_args,
                            mse ? w.sse_acc : nullptr, f.batch, 1.0 / count, mse ? loss : nullptr);
         else
-            e = launch_pdl(finalize_kernel<false>, dim3((total + GI_FIN_THREADS - 1) / GI_FIN_THREADS),
-                           dim3(GI_FIN_THREADS), s, fa_args,
+            e = launch_pdl(finalize_kernel<false>, dim3((total + ft - 1) / ft), dim3(ft), s, fa_args,
                            mse ? w.sse_acc : nullptr, f.batch, 1.0 / count, mse ? loss : nullptr);
         note_launches(1);
         if ((e = cudaGetLastError()) != cudaSuccess) return e;
