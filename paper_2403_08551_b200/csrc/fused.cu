@@ -29,13 +29,14 @@ constexpr double kSseScale3 = 1099511627776.0;   // 2^40, backward.cu's loss fix
 constexpr int kSortMax3 = 1024;                  // sort buffer of multi-batch segments
 // records per batch (256-thread CTAs): the fit kernel stages 128 (its shared
 // memory then leaves room for the finalize CTAs that start in its tail, PDL:
-// fit 23.9k -> 26.6k it/s vs 256), the render kernel 256 (one batch for the
-// decoded C5 cloud's ~120-key tiles: decode 23.3k -> 25.2k FPS)
+// fit 23.9k -> 26.6k it/s vs 256; 112: -2 %), the render kernel 192 (one
+// batch for the decoded C5 cloud's ~120-key tiles -- 128: decode -11 % --;
+// C2 frame 57.8k -> 58.5k FPS vs 256)
 #ifndef GI_TILE3_BATCH
 #define GI_TILE3_BATCH 128
 #endif
 #ifndef GI_RENDER3_BATCH
-#define GI_RENDER3_BATCH 256
+#define GI_RENDER3_BATCH 192
 #endif
 constexpr int kBwdBatch = GI_TILE3_BATCH, kRenderBatch = GI_RENDER3_BATCH;
 
